@@ -1,0 +1,212 @@
+/*
+ * nf.h — C ABI of the B200-native NanoFlow hot path (arXiv 2408.12757).
+ *
+ * One thing is exported: the forward pass of a LLaMA-style decoder layer over
+ * a dense batch that mixes prefill chunks and decode tokens (PAPER.md:155,
+ * :504), with a paged KV cache, split into nano-batches whose
+ * dense projections, paged attention and tensor-parallel collectives are
+ * issued as an operation-level pipeline on SM-bounded kernels
+ * (PAPER.md:537-563, :602-614), plus the model step around it.
+ *
+ * Conventions (all entry points):
+ *  - Plain C types only.  Device buffers are `void*` device pointers owned by
+ *    the caller; `stream` is a `cudaStream_t` passed as `void*`.  Host arrays
+ *    are read during the call only.
+ *  - bf16 tensors are row-major [rows, cols] with the stated shapes.
+ *  - Calls are stream-ordered and do not synchronise the host, except
+ *    nf_plan_* / nf_comm_* (host only) and the pack calls (stream-ordered).
+ *  - Every argument is validated on the host before any launch.  On error the
+ *    call returns a non-zero nf_status, launches nothing (validation errors) and
+ *    nf_last_error() describes it.  No exception crosses the ABI.
+ *  - The library never allocates device memory inside nf_layer_forward /
+ *    nf_model_step / nf_attention / nf_gemm_bf16: scratch comes from the
+ *    caller's workspace (size from nf_workspace_size).
+ */
+#ifndef NF_H_
+#define NF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NF_ABI_VERSION 1
+
+typedef enum {
+  NF_OK = 0,
+  NF_EINVAL = 1,        /* invalid argument (shape, batch, buffer size) */
+  NF_EUNSUPPORTED = 2,  /* valid but not implemented (e.g. head_dim not in {64,128}) */
+  NF_EINFEASIBLE = 3,   /* planner: no SM assignment fits the budget */
+  NF_ECUDA = 4,         /* a CUDA call failed; nf_last_error names it */
+  NF_ENCCL = 5,         /* an NCCL call failed */
+  NF_ENOMEM = 6         /* host allocation failed */
+} nf_status;
+
+/* Thread-local description of the last error on this thread; valid until the
+ * next nf_* call on the same thread.  Never NULL. */
+const char* nf_last_error(void);
+int32_t nf_abi_version(void);
+
+/* Model shape and this rank's place in tensor parallelism.
+ * head-parallel TP: tp_size must divide n_kv_heads
+ * and d_ffn; head_dim in {64, 128}; d_model % 256 == 0; page_size == 16. */
+typedef struct {
+  int32_t d_model, n_layers, n_q_heads, n_kv_heads, head_dim, d_ffn, vocab;
+  float rms_eps;    /* RMSNorm epsilon (reading A-2: 1e-5) */
+  float rope_theta; /* RoPE base (reading A-4) */
+  int32_t page_size;
+  int32_t tp_size, tp_rank;
+} nf_model_cfg;
+
+/* One step's global batch (PAPER.md:155 chunked prefill co-batched with
+ * decode).  Token rows are request-major in this order: request r owns rows
+ * [sum(q_len[0..r)), +q_len[r]).  Token i of request r has position
+ * kv_prefix[r] + i; its K/V go to logical page (pos / page_size) of the
+ * request, slot pos % page_size.  All arrays are HOST arrays.
+ * NF_EINVAL: n_req < 1, q_len < 1, kv_prefix < 0, fewer than
+ * ceil((kv_prefix+q_len)/page_size) pages for a request, page id outside
+ * [0, n_pages_pool). */
+typedef struct {
+  int32_t n_req;
+  const int32_t* q_len;       /* [n_req]  1 = decode, >1 = prefill chunk */
+  const int32_t* kv_prefix;   /* [n_req]  tokens cached before this step */
+  const int32_t* page_indptr; /* [n_req+1] CSR into page_ids */
+  const int32_t* page_ids;    /* [page_indptr[n_req]] physical page of logical page i */
+  int32_t n_pages_pool;       /* pages in each layer's pool */
+  const int32_t* emit;        /* [n_req] or NULL (= all): 1 if the request samples a token */
+} nf_batch;
+
+/* ------------------------------------------------------------------ host-only metadata (a1) */
+/* pos_out[t] = kv_prefix[r] + i; slot_out[t] = page_ids[page_indptr[r] + pos/page] * page + pos % page.
+ * Arrays sized [T = sum q_len].  Bit-exact contract with oracle/metadata.py. */
+nf_status nf_batch_metadata(const nf_model_cfg* cfg, const nf_batch* b, int32_t* pos_out, int32_t* slot_out);
+/* Nano-batch cut snapping (reading A-10): share[k] are integer token-share
+ * weights of n_nano nano-batches; cut k is the request boundary nearest to
+ * T * (share[0]+..+share[k-1]) / sum(share), ties to the lower one.
+ * req_cuts_out: [n_nano+1] request indices (0 .. n_req). */
+nf_status nf_snap_cuts(const nf_batch* b, int32_t n_nano, const int32_t* share, int32_t* req_cuts_out);
+
+/* ------------------------------------------------------------------ plans */
+enum { NF_SEQUENTIAL = 0, NF_NANO_ONLY = 1, NF_OVERLAP = 2 }; /* ablation modes */
+enum {
+  NF_OP_KQV = 0,
+  NF_OP_DECODE_ATTN = 1,
+  NF_OP_PREFILL_ATTN = 2,
+  NF_OP_O = 3,
+  NF_OP_UG = 4,
+  NF_OP_DOWN = 5,
+  NF_OP_NET = 6,
+  NF_OP_COUNT = 7
+};
+#define NF_MAX_NANO 4
+/* A nano-batch plan: "the size of each nano-batch and the allocation of
+ * execution units to the operations".  share: token-share
+ * weights of the nano-batches (snapped to requests per batch); sm: SM budget
+ * per op kind (1..148).  SEQUENTIAL ignores n_nano/share (one nano-batch). */
+typedef struct {
+  int32_t mode;
+  int32_t n_nano;              /* 1..NF_MAX_NANO */
+  int32_t share[NF_MAX_NANO];
+  int32_t sm[NF_OP_COUNT];
+  int32_t balance;             /* 1: assign requests to nano-batches balancing tokens and KV (model step only) */
+} nf_plan_spec;
+
+/* One measured kernel-curve sample, CSV `op_kind,resource_class,units,work,latency_s`. */
+typedef struct {
+  int32_t op_kind;   /* NF_OP_* */
+  int32_t units;     /* SMs */
+  double work;       /* tokens (dense/net) or KV keys (attention) */
+  double latency_s;
+} nf_curve_point;
+
+typedef struct {
+  int32_t sm_budget;  /* total SMs (148) */
+  int32_t sm_quantum; /* assignment granularity (8) */
+  int32_t mode;
+  int32_t n_nano;     /* 2 single GPU, 4 attention / 2 dense at TP>1 */
+  int32_t max_iters;  /* greedy iterations (200) */
+} nf_plan_opts;
+
+typedef struct nf_plan nf_plan;
+/* Explicit plan (tests, ablations).  NF_EINVAL on out-of-range fields. */
+nf_status nf_plan_create_explicit(const nf_model_cfg* cfg, const nf_plan_spec* spec, nf_plan** out);
+/* Autosearch: critical-path greedy SM assignment per
+ * candidate split over measured curves; keeps the shortest per-layer period.
+ * NF_EINFEASIBLE if no candidate fits opts->sm_budget. */
+nf_status nf_plan_create(const nf_model_cfg* cfg, const nf_batch* shape, const nf_curve_point* pts, int32_t n_pts,
+                         const nf_plan_opts* opts, nf_plan** out);
+nf_status nf_plan_get_spec(const nf_plan* plan, nf_plan_spec* out);
+/* Gantt CSV `node_id,kind,nano_index,units,start_s,end_s` of the searched schedule. */
+nf_status nf_plan_export_csv(const nf_plan* plan, char* buf, size_t cap, size_t* len);
+void nf_plan_destroy(nf_plan* plan);
+
+/* ------------------------------------------------------------------ tensor-parallel communicator */
+typedef struct nf_comm nf_comm;
+/* 128-byte NCCL unique id, created on rank 0 and broadcast by the caller. */
+nf_status nf_comm_unique_id(void* id_out_128);
+nf_status nf_comm_create(int32_t tp_size, int32_t tp_rank, const void* id_128, nf_comm** out);
+void nf_comm_destroy(nf_comm* comm);
+
+/* ------------------------------------------------------------------ weights */
+/* This rank's shards in canonical [out, in] row-major bf16 (device):
+ * w_q [qh/N*hd, D], w_k/w_v [kh/N*hd, D], w_o [D, qh*hd] FULL (TP1) or NULL,
+ * w_o_col [D/N, qh*hd] and w_o_row [D, qh/N*hd] (TP>1), w_gate/w_up [F/N, D],
+ * w_down [D, F/N], norms [D]. */
+typedef struct {
+  const void *attn_norm, *w_q, *w_k, *w_v, *w_o, *w_o_col, *w_o_row, *ffn_norm, *w_gate, *w_up, *w_down;
+} nf_layer_weights;
+/* Packed, kernel-ready layer (caller-allocated device buffers, sizes from nf_packed_layer_bytes):
+ * w_qkv [(qh+2kh)/N*hd, D] with gamma_attn folded into columns;
+ * w_o: TP1 [D, qh*hd]; TP>1 w_o = w_o_col [D/N, D] and w_o_row [D, D/N];
+ * w_gate_up [ceil(F/N/128)*256, D] gate/up interleaved in 128-row blocks, gamma_ffn folded;
+ * w_down [D, F/N]. */
+typedef struct {
+  void *w_qkv, *w_o, *w_o_row, *w_gate_up, *w_down;
+} nf_packed_layer;
+nf_status nf_packed_layer_bytes(const nf_model_cfg* cfg, size_t bytes_out[5]);
+nf_status nf_pack_layer(const nf_model_cfg* cfg, const nf_layer_weights* src, const nf_packed_layer* dst, void* stream);
+/* lm_head_packed [V, D] = lm_head * gamma_final (vocab is not sharded in this version). */
+nf_status nf_pack_lm_head(const nf_model_cfg* cfg, const void* lm_head, const void* final_norm, void* dst, void* stream);
+
+typedef struct {
+  const void* embed;               /* [V, D] */
+  const nf_packed_layer* layers;   /* host array [n_layers] of device pointers */
+  const void* lm_head_packed;      /* [V, D] */
+} nf_model_weights;
+
+/* ------------------------------------------------------------------ forward */
+/* Workspace bytes for nf_layer_forward / nf_model_step / nf_attention with this batch. */
+nf_status nf_workspace_size(const nf_model_cfg* cfg, const nf_batch* b, size_t* bytes);
+
+/* One decoder layer: x_out = layer(x_in), appending this
+ * step's K/V into kv_pool (layout [n_pages_pool][2][kh/N][page][hd] bf16).
+ * x_in, x_out: [T, D] bf16, replicated on every rank.  comm may be NULL at TP1. */
+nf_status nf_layer_forward(const nf_plan* plan, nf_comm* comm, const nf_packed_layer* w, void* kv_pool,
+                           const nf_batch* b, const void* x_in, void* x_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Embedding gather -> n_layers decoder layers -> final RMSNorm -> LM head on
+ * the last row of each emitting request -> greedy argmax (ties: lowest id).
+ * token_ids: device int32 [T]; next_ids: device int32 [n_req] (-1 if not emitted).
+ * kv_pools: host array [n_layers] of device pool pointers. */
+nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weights* w, void* const* kv_pools,
+                        const nf_batch* b, const int32_t* token_ids, int32_t* next_ids, void* ws, size_t ws_bytes,
+                        void* stream);
+
+/* ------------------------------------------------------------------ op-level entry points (tests, profiling) */
+/* C[M, N] = A[M, K] . B[N, K]^T, bf16 in/out, f32 accumulation (tcgen05).
+ * Leading dimensions in elements, multiples of 8; N % 32 == 0. */
+nf_status nf_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t M,
+                       int32_t N, int32_t K, int32_t sm_budget, void* stream);
+/* Paged causal GQA attention of PAPER.md:161 for every token of the batch:
+ * q [T, qh, hd] (post-RoPE), kv_pool already holding this step's K/V,
+ * o [T, qh*hd].  Decode tokens (q_len == 1) run on the decode kernel with
+ * sm_decode SMs, prefill chunks on the prefill kernel with sm_prefill SMs. */
+nf_status nf_attention(const nf_model_cfg* cfg, const nf_batch* b, const void* q, const void* kv_pool, void* o,
+                       void* ws, size_t ws_bytes, int32_t sm_decode, int32_t sm_prefill, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NF_H_ */

@@ -1,0 +1,854 @@
+// C ABI of the NanoFlow hot path: validation, step metadata, workspace,
+// weight packing, the nano-batch pipeline executor and the op-level entries.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+
+#include "attention.cuh"
+#include "gemm.cuh"
+#include "host.h"
+#include "misc.cuh"
+
+namespace nf {
+
+namespace {
+thread_local std::string g_err = "no error";
+int g_num_sms = 0;
+
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      g_num_sms = n;
+    else
+      g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+nf_status set_error(nf_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+int64_t batch_tokens(const nf_batch* b) {
+  int64_t T = 0;
+  for (int r = 0; r < b->n_req; ++r) T += b->q_len[r];
+  return T;
+}
+
+nf_status validate_cfg(const nf_model_cfg* c) {
+  if (!c) return set_error(NF_EINVAL, "cfg is NULL");
+  if (c->tp_size < 1 || c->tp_rank < 0 || c->tp_rank >= c->tp_size)
+    return set_error(NF_EINVAL, "bad tp_size/tp_rank %d/%d", c->tp_size, c->tp_rank);
+  if (c->d_model <= 0 || c->n_q_heads <= 0 || c->n_kv_heads <= 0 || c->d_ffn <= 0 || c->vocab <= 0 || c->n_layers <= 0)
+    return set_error(NF_EINVAL, "non-positive model dimension");
+  if (c->n_q_heads % c->n_kv_heads) return set_error(NF_EINVAL, "n_kv_heads must divide n_q_heads");
+  if (c->n_kv_heads % c->tp_size) return set_error(NF_EINVAL, "tp_size must divide n_kv_heads");
+  if (c->d_ffn % c->tp_size || c->d_model % c->tp_size) return set_error(NF_EINVAL, "tp_size must divide d_ffn and d_model");
+  if (c->head_dim != 64 && c->head_dim != 128) return set_error(NF_EUNSUPPORTED, "head_dim %d not in {64,128}", c->head_dim);
+  if (c->page_size != 16) return set_error(NF_EUNSUPPORTED, "page_size must be 16");
+  if (c->d_model % 256) return set_error(NF_EUNSUPPORTED, "d_model must be a multiple of 256");
+  if ((c->d_ffn / c->tp_size) % 32) return set_error(NF_EUNSUPPORTED, "d_ffn/tp_size must be a multiple of 32");
+  if (c->vocab % 32) return set_error(NF_EUNSUPPORTED, "vocab must be a multiple of 32");
+  if (c->n_q_heads / c->n_kv_heads > 16) return set_error(NF_EUNSUPPORTED, "GQA group > 16");
+  if (!(c->rms_eps > 0) || !(c->rope_theta > 1)) return set_error(NF_EINVAL, "bad rms_eps / rope_theta");
+  return NF_OK;
+}
+
+nf_status validate_batch(const nf_model_cfg* c, const nf_batch* b) {
+  if (!b) return set_error(NF_EINVAL, "batch is NULL");
+  if (b->n_req < 1) return set_error(NF_EINVAL, "n_req must be >= 1");
+  if (!b->q_len || !b->kv_prefix || !b->page_indptr || !b->page_ids)
+    return set_error(NF_EINVAL, "batch arrays must be non-NULL");
+  if (b->page_indptr[0] != 0) return set_error(NF_EINVAL, "page_indptr[0] must be 0");
+  const int P = c ? c->page_size : 16;
+  for (int r = 0; r < b->n_req; ++r) {
+    if (b->q_len[r] < 1) return set_error(NF_EINVAL, "q_len[%d] = %d < 1", r, b->q_len[r]);
+    if (b->kv_prefix[r] < 0) return set_error(NF_EINVAL, "kv_prefix[%d] = %d < 0", r, b->kv_prefix[r]);
+    const int64_t need = ((int64_t)b->kv_prefix[r] + b->q_len[r] + P - 1) / P;
+    const int64_t have = (int64_t)b->page_indptr[r + 1] - b->page_indptr[r];
+    if (have < need) return set_error(NF_EINVAL, "request %d has %lld pages, needs %lld", r, (long long)have, (long long)need);
+  }
+  const int64_t np = b->page_indptr[b->n_req];
+  for (int64_t i = 0; i < np; ++i)
+    if (b->page_ids[i] < 0 || b->page_ids[i] >= b->n_pages_pool)
+      return set_error(NF_EINVAL, "page id %d at %lld outside pool of %d", b->page_ids[i], (long long)i, b->n_pages_pool);
+  if (batch_tokens(b) > (1 << 24)) return set_error(NF_EINVAL, "too many tokens");
+  return NF_OK;
+}
+
+std::vector<int> snap_cuts_impl(const std::vector<int64_t>& bound, int n_nano, const int32_t* share) {
+  // bound[b] = token offset of request boundary b (b = 0..n_req); reading A-10
+  const int n_req = (int)bound.size() - 1;
+  const int64_t T = bound[n_req];
+  int64_t tot = 0;
+  for (int k = 0; k < n_nano; ++k) tot += share[k];
+  std::vector<int> cuts{0};
+  int64_t acc = 0;
+  for (int k = 0; k + 1 < n_nano; ++k) {
+    acc += share[k];
+    // target = T*acc/tot; compare |bound*tot - T*acc| exactly in integers
+    int best = 0;
+    __int128 bd = -1;
+    for (int b = 0; b <= n_req; ++b) {
+      __int128 d = (__int128)bound[b] * tot - (__int128)T * acc;
+      if (d < 0) d = -d;
+      if (bd < 0 || d < bd) { bd = d; best = b; }
+    }
+    cuts.push_back(std::max(best, cuts.back()));
+  }
+  cuts.push_back(n_req);
+  return cuts;
+}
+
+size_t meta_words_bound(const nf_model_cfg* c, const nf_batch* b) {
+  const int64_t T = batch_tokens(b);
+  const int qh = c->n_q_heads / c->tp_size, kh = c->n_kv_heads / c->tp_size;
+  int64_t pf_tiles = 0;
+  for (int r = 0; r < b->n_req; ++r)
+    if (b->q_len[r] > 1) pf_tiles += (b->q_len[r] + 63) / 64;
+  const int64_t words = 3 * T + b->page_indptr[b->n_req] + 4 * (int64_t)b->n_req * kh + 8 * pf_tiles * qh +
+                        2 * (int64_t)b->n_req + 64;
+  return (size_t)words;
+}
+
+void build_meta(const nf_model_cfg* c, const nf_batch* b, const std::vector<int>& order, const std::vector<int>& req_cuts,
+                StepMeta* m) {
+  const int P = c->page_size;
+  const int qh = c->n_q_heads / c->tp_size, kh = c->n_kv_heads / c->tp_size;
+  const int n_req = b->n_req;
+  int64_t T = batch_tokens(b);
+  m->T = (int)T;
+  m->n_req = n_req;
+  const int64_t npg = b->page_indptr[n_req];
+  m->off_pos = 0;
+  m->off_slot = T;
+  m->off_tok_src = 2 * T;
+  m->off_pages = 3 * T;
+  m->off_dec = m->off_pages + npg;
+  // token rows in internal order
+  std::vector<int64_t> caller_start(n_req + 1, 0);
+  for (int r = 0; r < n_req; ++r) caller_start[r + 1] = caller_start[r] + b->q_len[r];
+  std::vector<int> row_start(n_req);
+  {
+    int t = 0;
+    for (int i = 0; i < n_req; ++i) {
+      row_start[order[i]] = t;
+      t += b->q_len[order[i]];
+    }
+  }
+  std::vector<int32_t> head(3 * T + npg);
+  for (int r = 0; r < n_req; ++r) {
+    for (int i = 0; i < b->q_len[r]; ++i) {
+      const int t = row_start[r] + i;
+      const int pos = b->kv_prefix[r] + i;
+      head[t] = pos;
+      head[T + t] = b->page_ids[b->page_indptr[r] + pos / P] * P + pos % P;
+      head[2 * T + t] = (int32_t)(caller_start[r] + i);
+    }
+  }
+  std::memcpy(head.data() + 3 * T, b->page_ids, npg * sizeof(int32_t));
+  std::vector<DecodeItem> dec;
+  std::vector<PrefillItem> pf;
+  m->nanos.clear();
+  for (size_t k = 0; k + 1 < req_cuts.size(); ++k) {
+    NanoRange nr;
+    nr.r0 = req_cuts[k];
+    nr.r1 = req_cuts[k + 1];
+    nr.t0 = nr.r0 < n_req ? row_start[order[nr.r0]] : (int)T;
+    nr.t1 = nr.r1 < n_req ? row_start[order[nr.r1]] : (int)T;
+    if (nr.r0 == nr.r1) nr.t1 = nr.t0;
+    nr.dec_off = (int)dec.size();
+    nr.pf_off = (int)pf.size();
+    for (int i = nr.r0; i < nr.r1; ++i) {
+      const int r = order[i];
+      const int kvl = b->kv_prefix[r] + b->q_len[r];
+      if (b->q_len[r] == 1) {
+        for (int g = 0; g < kh; ++g) dec.push_back(DecodeItem{row_start[r], g, kvl, b->page_indptr[r]});
+      } else {
+        for (int i0 = 0; i0 < b->q_len[r]; i0 += 64)
+          for (int h = 0; h < qh; ++h)
+            pf.push_back(PrefillItem{row_start[r] + i0, std::min(64, b->q_len[r] - i0), b->kv_prefix[r] + i0, h, kvl,
+                                     b->page_indptr[r], 0, 0});
+      }
+    }
+    nr.dec_n = (int)dec.size() - nr.dec_off;
+    nr.pf_n = (int)pf.size() - nr.pf_off;
+    // longest first: static round-robin over warps/CTAs is then LPT-like
+    std::stable_sort(dec.begin() + nr.dec_off, dec.end(),
+                     [](const DecodeItem& x, const DecodeItem& y) { return x.kv_len > y.kv_len; });
+    std::stable_sort(pf.begin() + nr.pf_off, pf.end(),
+                     [](const PrefillItem& x, const PrefillItem& y) { return x.pos0 + x.n > y.pos0 + y.n; });
+    m->nanos.push_back(nr);
+  }
+  m->off_pf = m->off_dec + dec.size() * 4;
+  m->off_emit_row = m->off_pf + pf.size() * 8;
+  std::vector<int32_t> erow, ereq;
+  for (int i = 0; i < n_req; ++i) {
+    const int r = order[i];
+    if (b->emit == nullptr || b->emit[r]) {
+      erow.push_back(row_start[r] + b->q_len[r] - 1);
+      ereq.push_back(r);
+    }
+  }
+  m->n_emit = (int)erow.size();
+  m->off_emit_req = m->off_emit_row + erow.size();
+  m->buf.resize(m->off_emit_req + ereq.size());
+  std::memcpy(m->buf.data(), head.data(), head.size() * 4);
+  std::memcpy(m->buf.data() + m->off_dec, dec.data(), dec.size() * sizeof(DecodeItem));
+  std::memcpy(m->buf.data() + m->off_pf, pf.data(), pf.size() * sizeof(PrefillItem));
+  std::memcpy(m->buf.data() + m->off_emit_row, erow.data(), erow.size() * 4);
+  std::memcpy(m->buf.data() + m->off_emit_req, ereq.data(), ereq.size() * 4);
+}
+
+Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base) {
+  const int64_t T = batch_tokens(b);
+  const int N = c->tp_size;
+  const int64_t qd = (int64_t)c->n_q_heads / N * c->head_dim, D = c->d_model, F = c->d_ffn / N;
+  const int64_t NP = D / GEMM_BN;
+  const int64_t VT = (c->vocab + GEMM_BN - 1) / GEMM_BN;
+  const int64_t R = b->n_req;
+  Workspace w{};
+  size_t off = 0;
+  char* p = static_cast<char*>(base);
+  auto take = [&](size_t bytes) -> void* {
+    void* r = p ? p + off : nullptr;
+    off = align_up(off + bytes, 256);
+    return r;
+  };
+  w.meta = (int32_t*)take(meta_words_bound(c, b) * 4);
+  w.q = (__nv_bfloat16*)take(T * qd * 2);
+  w.o = (__nv_bfloat16*)take(T * qd * 2);
+  w.o_full = N > 1 ? (__nv_bfloat16*)take(T * (int64_t)c->n_q_heads * c->head_dim * 2) : nullptr;
+  w.h1 = (__nv_bfloat16*)take(T * D * 2);
+  w.m = (__nv_bfloat16*)take(T * F * 2);
+  w.xa = (__nv_bfloat16*)take(T * D * 2);
+  w.xb = (__nv_bfloat16*)take(T * D * 2);
+  w.part_a = (float*)take(NP * T * 4);
+  w.part_b = (float*)take(NP * T * 4);
+  w.part_h1 = (float*)take(NP * T * 4);
+  w.lm_rows = (__nv_bfloat16*)take(R * D * 2);
+  w.lm_part = (float*)take(R * 4);
+  w.am_val = (float*)take(VT * R * 4);
+  w.am_idx = (int*)take(VT * R * 4);
+  w.red = N > 1 ? (float*)take(T * D * 4) : nullptr;
+  w.total = off;
+  return w;
+}
+
+}  // namespace nf
+
+using namespace nf;
+
+extern "C" {
+
+const char* nf_last_error(void) { return g_err.c_str(); }
+int32_t nf_abi_version(void) { return NF_ABI_VERSION; }
+
+nf_status nf_batch_metadata(const nf_model_cfg* cfg, const nf_batch* b, int32_t* pos_out, int32_t* slot_out) {
+  NF_TRY(validate_cfg(cfg));
+  NF_TRY(validate_batch(cfg, b));
+  if (!pos_out || !slot_out) return set_error(NF_EINVAL, "output arrays are NULL");
+  std::vector<int> order(b->n_req);
+  std::iota(order.begin(), order.end(), 0);
+  StepMeta m;
+  build_meta(cfg, b, order, {0, b->n_req}, &m);
+  std::memcpy(pos_out, m.buf.data() + m.off_pos, m.T * 4);
+  std::memcpy(slot_out, m.buf.data() + m.off_slot, m.T * 4);
+  return NF_OK;
+}
+
+nf_status nf_snap_cuts(const nf_batch* b, int32_t n_nano, const int32_t* share, int32_t* req_cuts_out) {
+  NF_TRY(validate_batch(nullptr, b));
+  if (n_nano < 1 || n_nano > NF_MAX_NANO || !share || !req_cuts_out) return set_error(NF_EINVAL, "bad n_nano/share");
+  int64_t tot = 0;
+  for (int k = 0; k < n_nano; ++k) {
+    if (share[k] < 0) return set_error(NF_EINVAL, "negative share");
+    tot += share[k];
+  }
+  if (tot <= 0) return set_error(NF_EINVAL, "shares sum to zero");
+  std::vector<int64_t> bound(b->n_req + 1, 0);
+  for (int r = 0; r < b->n_req; ++r) bound[r + 1] = bound[r] + b->q_len[r];
+  auto cuts = snap_cuts_impl(bound, n_nano, share);
+  for (int k = 0; k <= n_nano; ++k) req_cuts_out[k] = cuts[k];
+  return NF_OK;
+}
+
+nf_status nf_workspace_size(const nf_model_cfg* cfg, const nf_batch* b, size_t* bytes) {
+  NF_TRY(validate_cfg(cfg));
+  NF_TRY(validate_batch(cfg, b));
+  if (!bytes) return set_error(NF_EINVAL, "bytes is NULL");
+  *bytes = carve_workspace(cfg, b, nullptr).total;
+  return NF_OK;
+}
+
+// ------------------------------------------------------------------ packing
+nf_status nf_packed_layer_bytes(const nf_model_cfg* c, size_t out[5]) {
+  NF_TRY(validate_cfg(c));
+  if (!out) return set_error(NF_EINVAL, "out is NULL");
+  const int N = c->tp_size;
+  const size_t D = c->d_model, hd = c->head_dim, qh = c->n_q_heads / N, kh = c->n_kv_heads / N;
+  const size_t F = c->d_ffn / N;
+  out[0] = (qh + 2 * kh) * hd * D * 2;
+  out[1] = N == 1 ? D * c->n_q_heads * hd * 2 : (D / N) * c->n_q_heads * hd * 2;
+  out[2] = N == 1 ? 0 : D * qh * hd * 2;
+  out[3] = ((F + 127) / 128) * 256 * D * 2;
+  out[4] = D * F * 2;
+  return NF_OK;
+}
+
+nf_status nf_pack_layer(const nf_model_cfg* c, const nf_layer_weights* s, const nf_packed_layer* d, void* stream) {
+  NF_TRY(validate_cfg(c));
+  if (!s || !d) return set_error(NF_EINVAL, "NULL weights");
+  const int N = c->tp_size;
+  if (!s->attn_norm || !s->w_q || !s->w_k || !s->w_v || !s->ffn_norm || !s->w_gate || !s->w_up || !s->w_down)
+    return set_error(NF_EINVAL, "NULL source weight");
+  if (N == 1 && !s->w_o) return set_error(NF_EINVAL, "w_o required at tp_size 1");
+  if (N > 1 && (!s->w_o_col || !s->w_o_row)) return set_error(NF_EINVAL, "w_o_col and w_o_row required at tp_size > 1");
+  if (!d->w_qkv || !d->w_o || !d->w_gate_up || !d->w_down || (N > 1 && !d->w_o_row))
+    return set_error(NF_EINVAL, "NULL destination buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  using B = __nv_bfloat16;
+  const int64_t D = c->d_model, hd = c->head_dim, qh = c->n_q_heads / N, kh = c->n_kv_heads / N, F = c->d_ffn / N;
+  B* qkv = (B*)d->w_qkv;
+  NF_CUDA(launch_scale_cols((const B*)s->w_q, (const B*)s->attn_norm, qh * hd, (int)D, qkv, st));
+  NF_CUDA(launch_scale_cols((const B*)s->w_k, (const B*)s->attn_norm, kh * hd, (int)D, qkv + qh * hd * D, st));
+  NF_CUDA(launch_scale_cols((const B*)s->w_v, (const B*)s->attn_norm, kh * hd, (int)D, qkv + (qh + kh) * hd * D, st));
+  if (N == 1) {
+    NF_CUDA(cudaMemcpyAsync(d->w_o, s->w_o, (size_t)D * c->n_q_heads * hd * 2, cudaMemcpyDeviceToDevice, st));
+  } else {
+    NF_CUDA(cudaMemcpyAsync(d->w_o, s->w_o_col, (size_t)(D / N) * c->n_q_heads * hd * 2, cudaMemcpyDeviceToDevice, st));
+    NF_CUDA(cudaMemcpyAsync(d->w_o_row, s->w_o_row, (size_t)D * qh * hd * 2, cudaMemcpyDeviceToDevice, st));
+  }
+  NF_CUDA(launch_pack_gate_up((const B*)s->w_gate, (const B*)s->w_up, (const B*)s->ffn_norm, (int)F, (int)D,
+                              (B*)d->w_gate_up, st));
+  NF_CUDA(cudaMemcpyAsync(d->w_down, s->w_down, (size_t)D * F * 2, cudaMemcpyDeviceToDevice, st));
+  return NF_OK;
+}
+
+nf_status nf_pack_lm_head(const nf_model_cfg* c, const void* lm_head, const void* final_norm, void* dst, void* stream) {
+  NF_TRY(validate_cfg(c));
+  if (!lm_head || !final_norm || !dst) return set_error(NF_EINVAL, "NULL pointer");
+  NF_CUDA(launch_scale_cols((const __nv_bfloat16*)lm_head, (const __nv_bfloat16*)final_norm, c->vocab, c->d_model,
+                            (__nv_bfloat16*)dst, (cudaStream_t)stream));
+  return NF_OK;
+}
+
+// ------------------------------------------------------------------ plans
+nf_status nf_plan_create_explicit(const nf_model_cfg* cfg, const nf_plan_spec* spec, nf_plan** out) {
+  NF_TRY(validate_cfg(cfg));
+  if (!spec || !out) return set_error(NF_EINVAL, "NULL spec/out");
+  if (spec->mode < NF_SEQUENTIAL || spec->mode > NF_OVERLAP) return set_error(NF_EINVAL, "bad mode %d", spec->mode);
+  if (spec->n_nano < 1 || spec->n_nano > NF_MAX_NANO) return set_error(NF_EINVAL, "n_nano %d out of range", spec->n_nano);
+  int64_t tot = 0;
+  for (int k = 0; k < spec->n_nano; ++k) {
+    if (spec->share[k] <= 0) return set_error(NF_EINVAL, "share[%d] must be > 0", k);
+    tot += spec->share[k];
+  }
+  for (int o = 0; o < NF_OP_COUNT; ++o)
+    if (spec->sm[o] < 1 || spec->sm[o] > 1024) return set_error(NF_EINVAL, "sm[%d] = %d out of range", o, spec->sm[o]);
+  nf_plan* p = new (std::nothrow) nf_plan();
+  if (!p) return set_error(NF_ENOMEM, "plan allocation failed");
+  p->cfg = *cfg;
+  p->spec = *spec;
+  if (spec->mode == NF_SEQUENTIAL) {
+    p->spec.n_nano = 1;
+    p->spec.share[0] = 1;
+  }
+  *out = p;
+  return NF_OK;
+}
+
+nf_status nf_plan_get_spec(const nf_plan* plan, nf_plan_spec* out) {
+  if (!plan || !out) return set_error(NF_EINVAL, "NULL plan/out");
+  *out = plan->spec;
+  return NF_OK;
+}
+
+nf_status nf_plan_export_csv(const nf_plan* plan, char* buf, size_t cap, size_t* len) {
+  if (!plan || !len) return set_error(NF_EINVAL, "NULL plan/len");
+  *len = plan->csv.size();
+  if (buf && cap > 0) {
+    const size_t n = std::min(cap - 1, plan->csv.size());
+    std::memcpy(buf, plan->csv.data(), n);
+    buf[n] = 0;
+  }
+  return NF_OK;
+}
+
+void nf_plan_destroy(nf_plan* p) {
+  if (!p) return;
+  if (p->mem_stream) cudaStreamDestroy(p->mem_stream);
+  for (int k = 0; k < NF_MAX_NANO; ++k) {
+    if (p->ev_kqv[k]) cudaEventDestroy(p->ev_kqv[k]);
+    if (p->ev_att[k]) cudaEventDestroy(p->ev_att[k]);
+  }
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
+  for (int i = 0; i < 2; ++i) {
+    if (p->ev_upload[i]) cudaEventDestroy(p->ev_upload[i]);
+    if (p->pinned[i]) cudaFreeHost(p->pinned[i]);
+  }
+  delete p;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ executor
+namespace nf {
+
+namespace {
+
+nf_status ensure_runtime(nf_plan* p) {
+  if (p->mem_stream) return NF_OK;
+  NF_CUDA(cudaGetDevice(&p->device));
+  int lo = 0, hi = 0;
+  NF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  // attention stream at higher priority: its CTAs are admitted first when both are pending
+  NF_CUDA(cudaStreamCreateWithPriority(&p->mem_stream, cudaStreamNonBlocking, hi));
+  for (int k = 0; k < NF_MAX_NANO; ++k) {
+    NF_CUDA(cudaEventCreateWithFlags(&p->ev_kqv[k], cudaEventDisableTiming));
+    NF_CUDA(cudaEventCreateWithFlags(&p->ev_att[k], cudaEventDisableTiming));
+  }
+  NF_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) NF_CUDA(cudaEventCreateWithFlags(&p->ev_upload[i], cudaEventDisableTiming));
+  return NF_OK;
+}
+
+// Copy the step metadata into the workspace through a double-buffered pinned staging buffer.
+nf_status upload_meta(nf_plan* p, const StepMeta& m, int32_t* dev, cudaStream_t st) {
+  const size_t bytes = m.buf.size() * 4;
+  const int i = p->upload_idx;
+  p->upload_idx ^= 1;
+  NF_CUDA(cudaEventSynchronize(p->ev_upload[i]));
+  if (p->pinned_cap[i] < bytes) {
+    if (p->pinned[i]) NF_CUDA(cudaFreeHost(p->pinned[i]));
+    const size_t cap = bytes * 2 + 4096;
+    NF_CUDA(cudaHostAlloc(&p->pinned[i], cap, cudaHostAllocDefault));
+    p->pinned_cap[i] = cap;
+  }
+  std::memcpy(p->pinned[i], m.buf.data(), bytes);
+  NF_CUDA(cudaMemcpyAsync(dev, p->pinned[i], bytes, cudaMemcpyHostToDevice, st));
+  NF_CUDA(cudaEventRecord(p->ev_upload[i], st));
+  return NF_OK;
+}
+
+// Internal request order and nano-batch cuts for this plan and batch.
+void plan_order(const nf_plan* p, const nf_batch* b, bool allow_balance, std::vector<int>* order, std::vector<int>* cuts) {
+  const int n_req = b->n_req;
+  const int nn = p->spec.n_nano;
+  order->resize(n_req);
+  std::iota(order->begin(), order->end(), 0);
+  if (nn == 1) {
+    *cuts = {0, n_req};
+    return;
+  }
+  if (!(allow_balance && p->spec.balance)) {
+    std::vector<int64_t> bound(n_req + 1, 0);
+    for (int r = 0; r < n_req; ++r) bound[r + 1] = bound[r] + b->q_len[r];
+    *cuts = snap_cuts_impl(bound, nn, p->spec.share);
+    return;
+  }
+  // Balanced assignment: prefill chunks by tokens (largest first to the nano
+  // with most remaining token share), decode requests by KV length (LPT).
+  int64_t T = batch_tokens(b), tot = 0;
+  for (int k = 0; k < nn; ++k) tot += p->spec.share[k];
+  std::vector<double> cap(nn), kv(nn, 0.0);
+  for (int k = 0; k < nn; ++k) cap[k] = (double)T * p->spec.share[k] / tot;
+  std::vector<std::vector<int>> grp(nn);
+  std::vector<int> pre, dec;
+  for (int r = 0; r < n_req; ++r) (b->q_len[r] > 1 ? pre : dec).push_back(r);
+  std::stable_sort(pre.begin(), pre.end(), [&](int x, int y) { return b->q_len[x] > b->q_len[y]; });
+  std::stable_sort(dec.begin(), dec.end(), [&](int x, int y) { return b->kv_prefix[x] > b->kv_prefix[y]; });
+  for (int r : pre) {
+    int best = 0;
+    for (int k = 1; k < nn; ++k)
+      if (cap[k] > cap[best]) best = k;
+    grp[best].push_back(r);
+    cap[best] -= b->q_len[r];
+    kv[best] += (double)b->q_len[r] * (b->kv_prefix[r] + b->q_len[r] / 2.0) / 64.0;  // prefill attention, rough
+  }
+  for (int r : dec) {
+    int best = 0;
+    for (int k = 1; k < nn; ++k)
+      if (kv[k] < kv[best]) best = k;
+    grp[best].push_back(r);
+    cap[best] -= 1;
+    kv[best] += b->kv_prefix[r] + 1;
+  }
+  order->clear();
+  cuts->assign(1, 0);
+  for (int k = 0; k < nn; ++k) {
+    std::sort(grp[k].begin(), grp[k].end());
+    for (int r : grp[k]) order->push_back(r);
+    cuts->push_back((int)order->size());
+  }
+}
+
+struct LayerCtx {
+  const nf_plan* p;
+  const nf_model_cfg* c;
+  const StepMeta* m;
+  const Workspace* w;
+  const int32_t* meta_dev;
+  CUtensorMap pool_map;
+  cudaStream_t cs, ms;  // compute / memory streams
+};
+
+int clampsm(int v) { return std::max(1, std::min(v, num_sms())); }
+
+nf_status run_kqv(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x, const float* part, int nparts,
+                  const nf_packed_layer* wt, void* pool) {
+  const nf_model_cfg* c = L.c;
+  const int N = c->tp_size;
+  const int M = nr.t1 - nr.t0;
+  if (M <= 0) return NF_OK;
+  GemmArgs a{};
+  a.epi = EPI_QKV;
+  a.M = M;
+  a.N = (c->n_q_heads + 2 * c->n_kv_heads) / N * c->head_dim;
+  a.K = c->d_model;
+  a.n_valid = a.N;
+  a.norm_part = part + nr.t0;
+  a.norm_nparts = nparts;
+  a.norm_stride = L.m->T;
+  a.inv_d = 1.f / c->d_model;
+  a.eps = c->rms_eps;
+  a.qh = c->n_q_heads / N;
+  a.kh = c->n_kv_heads / N;
+  a.hd = c->head_dim;
+  a.page_size = c->page_size;
+  a.log2_theta = (float)std::log2((double)c->rope_theta);
+  a.tok_pos = L.meta_dev + L.m->off_pos + nr.t0;
+  a.tok_slot = L.meta_dev + L.m->off_slot + nr.t0;
+  a.q_out = L.w->q + (int64_t)nr.t0 * a.qh * a.hd;
+  a.kv_pool = (__nv_bfloat16*)pool;
+  NF_CUDA(launch_gemm(x + (int64_t)nr.t0 * c->d_model, c->d_model, (const __nv_bfloat16*)wt->w_qkv, c->d_model, a,
+                      clampsm(L.p->spec.sm[NF_OP_KQV]), L.cs));
+  return NF_OK;
+}
+
+nf_status run_attn(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
+  const nf_model_cfg* c = L.c;
+  AttnArgs a{};
+  a.q = L.w->q;
+  a.o = L.w->o;
+  a.page_ids = L.meta_dev + L.m->off_pages;
+  a.qh = c->n_q_heads / c->tp_size;
+  a.kh = c->n_kv_heads / c->tp_size;
+  a.hd = c->head_dim;
+  a.page_size = c->page_size;
+  a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
+  const DecodeItem* dec = reinterpret_cast<const DecodeItem*>(L.meta_dev + L.m->off_dec) + nr.dec_off;
+  const PrefillItem* pf = reinterpret_cast<const PrefillItem*>(L.meta_dev + L.m->off_pf) + nr.pf_off;
+  NF_CUDA(launch_prefill_attention(L.pool_map, a, pf, nr.pf_n, clampsm(L.p->spec.sm[NF_OP_PREFILL_ATTN]), st));
+  NF_CUDA(launch_decode_attention(L.pool_map, a, dec, nr.dec_n, clampsm(L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
+  return NF_OK;
+}
+
+// O + residual, RMS(FFN) fold, Up/Gate + SiLU, Down + residual for one nano-batch (TP1).
+nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x, const nf_packed_layer* wt,
+                         __nv_bfloat16* x_out, float* part_out) {
+  const nf_model_cfg* c = L.c;
+  const int M = nr.t1 - nr.t0;
+  if (M <= 0) return NF_OK;
+  const int64_t D = c->d_model, F = c->d_ffn, qd = (int64_t)c->n_q_heads * c->head_dim;
+  const int T = L.m->T;
+  const int NP = (int)(D / GEMM_BN);
+  // O projection + residual: h1 = x + o W_o^T, with sum-of-squares partials of h1
+  GemmArgs a{};
+  a.epi = EPI_RESID;
+  a.M = M;
+  a.N = (int)D;
+  a.K = (int)qd;
+  a.n_valid = (int)D;
+  a.out = L.w->h1 + nr.t0 * D;
+  a.ldo = D;
+  a.resid = x + nr.t0 * D;
+  a.ldr = D;
+  a.sq_out = L.w->part_h1 + nr.t0;
+  a.sq_stride = T;
+  NF_CUDA(launch_gemm(L.w->o + nr.t0 * qd, qd, (const __nv_bfloat16*)wt->w_o, qd, a, clampsm(L.p->spec.sm[NF_OP_O]), L.cs));
+  // Up/Gate + SiLU(gate) * up, RMSNorm(h1) folded as a row scale
+  GemmArgs u{};
+  u.epi = EPI_SILU;
+  u.M = M;
+  u.N = (int)(((F + 127) / 128) * 256);
+  u.K = (int)D;
+  u.n_valid = (int)F;
+  u.out = L.w->m + nr.t0 * F;
+  u.ldo = F;
+  u.norm_part = L.w->part_h1 + nr.t0;
+  u.norm_nparts = NP;
+  u.norm_stride = T;
+  u.inv_d = 1.f / D;
+  u.eps = c->rms_eps;
+  NF_CUDA(launch_gemm(L.w->h1 + nr.t0 * D, D, (const __nv_bfloat16*)wt->w_gate_up, D, u, clampsm(L.p->spec.sm[NF_OP_UG]),
+                      L.cs));
+  // Down + residual: x_out = h1 + m W_d^T, partials of x_out for the next layer's norm
+  GemmArgs d{};
+  d.epi = EPI_RESID;
+  d.M = M;
+  d.N = (int)D;
+  d.K = (int)F;
+  d.n_valid = (int)D;
+  d.out = x_out + nr.t0 * D;
+  d.ldo = D;
+  d.resid = L.w->h1 + nr.t0 * D;
+  d.ldr = D;
+  d.sq_out = part_out ? part_out + nr.t0 : nullptr;
+  d.sq_stride = T;
+  NF_CUDA(launch_gemm(L.w->m + nr.t0 * F, F, (const __nv_bfloat16*)wt->w_down, F, d, clampsm(L.p->spec.sm[NF_OP_DOWN]),
+                      L.cs));
+  return NF_OK;
+}
+
+}  // namespace
+
+// One layer with the plan's pipeline.  x/part: input + its RMS partials (nparts),
+// x_out/part_out: output + partials for the next layer.  first/last control the
+// cross-layer overlap bookkeeping in model steps (KQV of layer l+1 issued early).
+nf_status run_layer(nf_plan* p, const LayerCtx& L, const nf_packed_layer* wt, void* pool, const __nv_bfloat16* x,
+                    const float* part, int nparts, __nv_bfloat16* x_out, float* part_out, bool kqv_done) {
+  const auto& nanos = L.m->nanos;
+  const int mode = p->spec.mode;
+  if (mode != NF_OVERLAP) {
+    for (const auto& nr : nanos) {
+      if (!kqv_done) NF_TRY(run_kqv(L, nr, x, part, nparts, wt, pool));
+      NF_TRY(run_attn(L, nr, L.cs));
+      NF_TRY(run_dense_tail(L, nr, x, wt, x_out, part_out));
+    }
+    return NF_OK;
+  }
+  // OVERLAP: KQV of every nano first, attention on the memory stream as soon as
+  // its KQV lands, then the dense tail of each nano after its attention.
+  for (size_t k = 0; k < nanos.size(); ++k) {
+    if (!kqv_done) NF_TRY(run_kqv(L, nanos[k], x, part, nparts, wt, pool));
+    NF_CUDA(cudaEventRecord(p->ev_kqv[k], L.cs));
+    NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
+    NF_TRY(run_attn(L, nanos[k], L.ms));
+    NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
+  }
+  for (size_t k = 0; k < nanos.size(); ++k) {
+    NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_att[k], 0));
+    NF_TRY(run_dense_tail(L, nanos[k], x, wt, x_out, part_out));
+  }
+  return NF_OK;
+}
+
+}  // namespace nf
+
+extern "C" {
+
+nf_status nf_layer_forward(const nf_plan* plan, nf_comm* comm, const nf_packed_layer* w, void* kv_pool, const nf_batch* b,
+                           const void* x_in, void* x_out, void* ws, size_t ws_bytes, void* stream) {
+  if (!plan) return set_error(NF_EINVAL, "plan is NULL");
+  nf_plan* p = const_cast<nf_plan*>(plan);
+  const nf_model_cfg* c = &p->cfg;
+  NF_TRY(validate_batch(c, b));
+  if (c->tp_size > 1) return set_error(NF_EUNSUPPORTED, "tp_size > 1 requires the TP executor (not built yet)");
+  (void)comm;
+  if (!w || !kv_pool || !x_in || !x_out || !ws) return set_error(NF_EINVAL, "NULL pointer argument");
+  Workspace wsp = carve_workspace(c, b, ws);
+  if (ws_bytes < wsp.total) return set_error(NF_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, wsp.total);
+  NF_TRY(ensure_runtime(p));
+  std::vector<int> order, cuts;
+  plan_order(p, b, false, &order, &cuts);
+  StepMeta m;
+  build_meta(c, b, order, cuts, &m);
+  cudaStream_t cs = (cudaStream_t)stream;
+  NF_TRY(upload_meta(p, m, wsp.meta, cs));
+  LayerCtx L{};
+  L.p = p;
+  L.c = c;
+  L.m = &m;
+  L.w = &wsp;
+  L.meta_dev = wsp.meta;
+  L.cs = cs;
+  L.ms = p->mem_stream;
+  NF_CUDA(make_pool_tmap(&L.pool_map, kv_pool, b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim, c->page_size));
+  // RMS partials of x_in (one part per row)
+  NF_CUDA(launch_gather_rows((const __nv_bfloat16*)x_in, nullptr, m.T, c->d_model, nullptr, wsp.part_a, cs));
+  NF_TRY(run_layer(p, L, w, kv_pool, (const __nv_bfloat16*)x_in, wsp.part_a, 1, (__nv_bfloat16*)x_out, nullptr, false));
+  return NF_OK;
+}
+
+nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weights* w, void* const* kv_pools,
+                        const nf_batch* b, const int32_t* token_ids, int32_t* next_ids, void* ws, size_t ws_bytes,
+                        void* stream) {
+  if (!plan) return set_error(NF_EINVAL, "plan is NULL");
+  nf_plan* p = const_cast<nf_plan*>(plan);
+  const nf_model_cfg* c = &p->cfg;
+  NF_TRY(validate_batch(c, b));
+  if (c->tp_size > 1) return set_error(NF_EUNSUPPORTED, "tp_size > 1 requires the TP executor (not built yet)");
+  (void)comm;
+  if (!w || !w->embed || !w->layers || !w->lm_head_packed || !kv_pools || !token_ids || !next_ids || !ws)
+    return set_error(NF_EINVAL, "NULL pointer argument");
+  for (int l = 0; l < c->n_layers; ++l)
+    if (!kv_pools[l]) return set_error(NF_EINVAL, "kv_pools[%d] is NULL", l);
+  Workspace wsp = carve_workspace(c, b, ws);
+  if (ws_bytes < wsp.total) return set_error(NF_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, wsp.total);
+  NF_TRY(ensure_runtime(p));
+  std::vector<int> order, cuts;
+  plan_order(p, b, true, &order, &cuts);
+  StepMeta m;
+  build_meta(c, b, order, cuts, &m);
+  cudaStream_t cs = (cudaStream_t)stream;
+  NF_TRY(upload_meta(p, m, wsp.meta, cs));
+  const int D = c->d_model;
+  const int NP = D / GEMM_BN;
+  // token ids in internal row order: gather ids then embedding rows (+ RMS partials, one part)
+  // tok_src maps internal row -> caller row; ids are gathered on the fly by the embedding gather.
+  NF_CUDA(launch_gather_ids_embed((const __nv_bfloat16*)w->embed, token_ids, wsp.meta + m.off_tok_src, m.T, D, wsp.xa,
+                                  wsp.part_a, cs));
+  LayerCtx L{};
+  L.p = p;
+  L.c = c;
+  L.m = &m;
+  L.w = &wsp;
+  L.meta_dev = wsp.meta;
+  L.cs = cs;
+  L.ms = p->mem_stream;
+  __nv_bfloat16 *x = wsp.xa, *y = wsp.xb;
+  float *px = wsp.part_a, *py = wsp.part_b;
+  std::vector<CUtensorMap> maps(c->n_layers);
+  for (int l = 0; l < c->n_layers; ++l)
+    NF_CUDA(make_pool_tmap(&maps[l], kv_pools[l], b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim,
+                           c->page_size));
+  if (p->spec.mode != NF_OVERLAP) {
+    int nparts = 1;
+    for (int l = 0; l < c->n_layers; ++l) {
+      L.pool_map = maps[l];
+      NF_TRY(run_layer(p, L, &w->layers[l], kv_pools[l], x, px, nparts, y, py, false));
+      std::swap(x, y);
+      std::swap(px, py);
+      nparts = NP;
+    }
+  } else {
+    // Operation-level pipeline across layers (single-GPU variant
+    // PAPER.md:691): the compute stream runs, per nano-batch k, O_k UG_k D_k of
+    // layer l then KQV_k of layer l+1; the memory stream runs ATT_k(l+1) as
+    // soon as KQV_k(l+1) lands, overlapping the other nano-batches' dense ops.
+    const auto& nanos = m.nanos;
+    L.pool_map = maps[0];
+    for (size_t k = 0; k < nanos.size(); ++k) {
+      NF_TRY(run_kqv(L, nanos[k], x, px, 1, &w->layers[0], kv_pools[0]));
+      NF_CUDA(cudaEventRecord(p->ev_kqv[k], cs));
+      NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
+      NF_TRY(run_attn(L, nanos[k], L.ms));
+      NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
+    }
+    for (int l = 0; l < c->n_layers; ++l) {
+      for (size_t k = 0; k < nanos.size(); ++k) {
+        NF_CUDA(cudaStreamWaitEvent(cs, p->ev_att[k], 0));
+        NF_TRY(run_dense_tail(L, nanos[k], x, &w->layers[l], y, py));
+        if (l + 1 < c->n_layers) {
+          L.pool_map = maps[l + 1];
+          NF_TRY(run_kqv(L, nanos[k], y, py, NP, &w->layers[l + 1], kv_pools[l + 1]));
+          NF_CUDA(cudaEventRecord(p->ev_kqv[k], cs));
+          NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
+          NF_TRY(run_attn(L, nanos[k], L.ms));
+          NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
+        }
+      }
+      std::swap(x, y);
+      std::swap(px, py);
+    }
+  }
+  // final RMSNorm (gamma folded into lm_head_packed) + LM head + argmax
+  NF_CUDA(launch_fill_i32(next_ids, b->n_req, -1, cs));
+  if (m.n_emit > 0) {
+    const int* erow = wsp.meta + m.off_emit_row;
+    NF_CUDA(launch_gather_rows(x, erow, m.n_emit, D, wsp.lm_rows, wsp.lm_part, cs));
+    GemmArgs a{};
+    a.epi = EPI_ARGMAX;
+    a.M = m.n_emit;
+    a.N = c->vocab;
+    a.K = D;
+    a.n_valid = c->vocab;
+    a.am_val = wsp.am_val;
+    a.am_idx = wsp.am_idx;
+    a.am_stride = m.n_emit;
+    NF_CUDA(launch_gemm(wsp.lm_rows, D, (const __nv_bfloat16*)w->lm_head_packed, D, a, num_sms(), cs));
+    NF_CUDA(launch_argmax_reduce(wsp.am_val, wsp.am_idx, (c->vocab + GEMM_BN - 1) / GEMM_BN, m.n_emit, m.n_emit,
+                                 wsp.meta + m.off_emit_req, next_ids, cs));
+  }
+  // join the memory stream (nothing outstanding in sequential modes)
+  NF_CUDA(cudaEventRecord(p->ev_join, p->mem_stream));
+  NF_CUDA(cudaStreamWaitEvent(cs, p->ev_join, 0));
+  return NF_OK;
+}
+
+// ------------------------------------------------------------------ op-level entry points
+nf_status nf_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t M,
+                       int32_t N, int32_t K, int32_t sm_budget, void* stream) {
+  if (!A || !B || !C) return set_error(NF_EINVAL, "NULL pointer");
+  if (M < 0 || N <= 0 || K <= 0) return set_error(NF_EINVAL, "bad shape M=%d N=%d K=%d", M, N, K);
+  if (N % 32) return set_error(NF_EINVAL, "N must be a multiple of 32");
+  if (lda % 8 || ldb % 8 || ldc % 8 || lda < K || ldb < K || ldc < N) return set_error(NF_EINVAL, "bad leading dimension");
+  if (((uintptr_t)A | (uintptr_t)B | (uintptr_t)C) & 15) return set_error(NF_EINVAL, "pointers must be 16-byte aligned");
+  GemmArgs a{};
+  a.epi = EPI_STORE;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.n_valid = N;
+  a.out = (__nv_bfloat16*)C;
+  a.ldo = ldc;
+  NF_CUDA(launch_gemm((const __nv_bfloat16*)A, lda, (const __nv_bfloat16*)B, ldb, a,
+                      std::max(1, std::min<int>(sm_budget, num_sms())), (cudaStream_t)stream));
+  return NF_OK;
+}
+
+nf_status nf_attention(const nf_model_cfg* cfg, const nf_batch* b, const void* q, const void* kv_pool, void* o, void* ws,
+                       size_t ws_bytes, int32_t sm_decode, int32_t sm_prefill, void* stream) {
+  NF_TRY(validate_cfg(cfg));
+  NF_TRY(validate_batch(cfg, b));
+  if (!q || !kv_pool || !o || !ws) return set_error(NF_EINVAL, "NULL pointer");
+  Workspace wsp = carve_workspace(cfg, b, ws);
+  if (ws_bytes < wsp.total) return set_error(NF_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, wsp.total);
+  static thread_local nf_plan* tmp = nullptr;
+  if (!tmp) {
+    tmp = new nf_plan();
+    tmp->spec.n_nano = 1;
+    tmp->spec.share[0] = 1;
+  }
+  tmp->cfg = *cfg;
+  for (int k = 0; k < NF_OP_COUNT; ++k) tmp->spec.sm[k] = num_sms();
+  tmp->spec.sm[NF_OP_DECODE_ATTN] = std::max(1, sm_decode);
+  tmp->spec.sm[NF_OP_PREFILL_ATTN] = std::max(1, sm_prefill);
+  NF_TRY(ensure_runtime(tmp));
+  std::vector<int> order(b->n_req);
+  std::iota(order.begin(), order.end(), 0);
+  StepMeta m;
+  build_meta(cfg, b, order, {0, b->n_req}, &m);
+  cudaStream_t st = (cudaStream_t)stream;
+  NF_TRY(upload_meta(tmp, m, wsp.meta, st));
+  Workspace w2 = wsp;
+  w2.q = (__nv_bfloat16*)q;
+  w2.o = (__nv_bfloat16*)o;
+  LayerCtx L{};
+  L.p = tmp;
+  L.c = cfg;
+  L.m = &m;
+  L.w = &w2;
+  L.meta_dev = wsp.meta;
+  NF_CUDA(make_pool_tmap(&L.pool_map, kv_pool, b->n_pages_pool, cfg->n_kv_heads / cfg->tp_size, cfg->head_dim,
+                         cfg->page_size));
+  NF_TRY(run_attn(L, m.nanos[0], st));
+  return NF_OK;
+}
+
+}  // extern "C"

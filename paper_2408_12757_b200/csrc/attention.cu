@@ -1,0 +1,461 @@
+// Paged GQA attention for sm_100a.
+//
+// KV pool layout [n_pages][2][kv_heads][16][head_dim] bf16: the
+// K (or V) block of one page and one KV head is 16 contiguous rows, fetched by
+// TMA as 128B-swizzled boxes of 16 rows x 64 columns into shared memory, so
+// the mma.sync fragment loads (ldmatrix) are bank-conflict free.
+//
+// Decode: one warp per (decode token, KV head) item; the R = qh/kh query heads
+// of the group are the M rows of m16n8k16 tensor-core MMAs, so each K/V byte
+// read from HBM is used R times on the tensor pipe (HBM-bound by design).
+// Every warp runs its own NS-deep TMA ring that streams ahead across items.
+// Prefill: FlashAttention-2 style, one CTA per (64-query tile, query head),
+// double-buffered 64-key K/V tiles, causal mask j <= pos.
+#include <algorithm>
+
+#include "attention.cuh"
+#include "common.cuh"
+
+namespace nf {
+
+cudaError_t make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                           uint32_t box_inner, uint32_t box_outer);
+
+cudaError_t make_pool_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, int kh, int hd, int page_size) {
+  return make_tmap_bf16(m, pool, hd, (uint64_t)n_pages * 2 * kh * page_size, hd, 64, page_size);
+}
+
+namespace {
+
+constexpr int DEC_WARPS = 8;
+constexpr int BOX_BYTES = 16 * 128;  // 16 rows x 64 bf16
+
+NF_DEV uint32_t swz(int row, int chunk) { return row * 128 + (((chunk & 7) ^ (row & 7)) << 4); }
+
+NF_DEV uint32_t ldg_u32(const __nv_bfloat16* p) { return *reinterpret_cast<const uint32_t*>(p); }
+
+template <int HD>
+constexpr int dec_stages() { return HD == 128 ? 3 : 6; }
+
+template <int HD>
+constexpr int dec_smem() { return DEC_WARPS * dec_stages<HD>() * (2 * 16 * HD * 2) + DEC_WARPS * dec_stages<HD>() * 8 + 1024; }
+
+// ---------------------------------------------------------------------------- decode
+template <int HD>
+__global__ void __launch_bounds__(DEC_WARPS * 32, 1)
+    decode_attn_kernel(const __grid_constant__ CUtensorMap pool, const AttnArgs a,
+                       const DecodeItem* __restrict__ items, int n_items) {
+  constexpr int NBOX = HD / 64;
+  constexpr int PAGE_BYTES = 16 * HD * 2;
+  constexpr int STAGE_BYTES = 2 * PAGE_BYTES;
+  constexpr int NS = dec_stages<HD>();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * NS * STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + DEC_WARPS * NS * STAGE_BYTES) + warp * NS;
+  if (lane == 0) {
+    if (warp == 0) tma_prefetch_desc(&pool);
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+
+  const int gw = blockIdx.x * DEC_WARPS + warp, TW = gridDim.x * DEC_WARPS;
+  const int kh = a.kh, R = a.qh / a.kh;
+
+  // look-ahead loader cursor (warp-uniform)
+  int l_item = gw, l_page = 0, l_np = 0, l_ps = 0, l_kvh = 0;
+  if (l_item < n_items) {
+    const DecodeItem it = items[l_item];
+    l_np = (it.kv_len + 15) >> 4;
+    l_ps = it.page_start;
+    l_kvh = it.kvh;
+  }
+  uint32_t issued = 0, consumed = 0;
+  auto issue_one = [&]() {
+    if (l_item >= n_items) return;
+    const int s = issued % NS;
+    if (lane == 0) {
+      const int64_t page = a.page_ids[l_ps + l_page];
+      uint8_t* dst = ring + s * STAGE_BYTES;
+      const int rowK = (int)(((page * 2 + 0) * kh + l_kvh) * 16);
+      const int rowV = rowK + kh * 16;
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bars[s], STAGE_BYTES);
+#pragma unroll
+      for (int b = 0; b < NBOX; ++b) tma_load_2d(dst + b * BOX_BYTES, &pool, &bars[s], b * 64, rowK);
+#pragma unroll
+      for (int b = 0; b < NBOX; ++b) tma_load_2d(dst + PAGE_BYTES + b * BOX_BYTES, &pool, &bars[s], b * 64, rowV);
+    }
+    ++issued;
+    if (++l_page == l_np) {
+      l_item += TW;
+      l_page = 0;
+      if (l_item < n_items) {
+        const DecodeItem it = items[l_item];
+        l_np = (it.kv_len + 15) >> 4;
+        l_ps = it.page_start;
+        l_kvh = it.kvh;
+      }
+    }
+  };
+  for (int i = 0; i < NS; ++i) issue_one();
+
+  for (int item = gw; item < n_items; item += TW) {
+    const DecodeItem it = items[item];
+    const int kv_len = it.kv_len;
+    const __nv_bfloat16* qbase = a.q + ((int64_t)it.t * a.qh + (int64_t)it.kvh * R) * HD;
+    const int row0 = lane >> 2, row1 = row0 + 8;
+    uint32_t qf[HD / 16][4];
+#pragma unroll
+    for (int ks = 0; ks < HD / 16; ++ks) {
+      const int kc = ks * 16 + 2 * (lane & 3);
+      qf[ks][0] = row0 < R ? ldg_u32(qbase + row0 * HD + kc) : 0u;
+      qf[ks][1] = row1 < R ? ldg_u32(qbase + row1 * HD + kc) : 0u;
+      qf[ks][2] = row0 < R ? ldg_u32(qbase + row0 * HD + kc + 8) : 0u;
+      qf[ks][3] = row1 < R ? ldg_u32(qbase + row1 * HD + kc + 8) : 0u;
+    }
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    float oacc[HD / 8][4];
+#pragma unroll
+    for (int d = 0; d < HD / 8; ++d) oacc[d][0] = oacc[d][1] = oacc[d][2] = oacc[d][3] = 0.f;
+
+    const int np = (kv_len + 15) >> 4;
+    for (int p = 0; p < np; ++p) {
+      const int s = consumed % NS;
+      mbar_wait(&bars[s], (consumed / NS) & 1);
+      uint8_t* kb = ring + s * STAGE_BYTES;
+      uint8_t* vb = kb + PAGE_BYTES;
+      const int valid = min(16, kv_len - p * 16);
+      if (valid < 16) {  // zero V rows of slots past kv_len (pool may hold anything there)
+        for (int i = lane; i < (16 - valid) * NBOX * 8; i += 32) {
+          const int row = valid + i / (NBOX * 8), rem = i % (NBOX * 8);
+          *reinterpret_cast<uint4*>(vb + (rem >> 3) * BOX_BYTES + row * 128 + (rem & 7) * 16) = make_uint4(0, 0, 0, 0);
+        }
+        __syncwarp();
+      }
+      // S = Q K^T (16 x 16 keys)
+      float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      {
+        const int key = (lane & 7) + ((lane >> 4) << 3);
+        const int hi = (lane >> 3) & 1;
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+          const int ch = ks * 2 + hi;
+          uint32_t kf[4];
+          ldmatrix_x4(kf, smem_u32(kb) + (ch >> 3) * BOX_BYTES + swz(key, ch));
+          const uint32_t b0[2] = {kf[0], kf[1]}, b1[2] = {kf[2], kf[3]};
+          mma_bf16_16816(sacc[0], qf[ks], b0);
+          mma_bf16_16816(sacc[1], qf[ks], b1);
+        }
+      }
+      // scale, mask, online softmax (rows row0 / row1)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int key = nt * 8 + 2 * (lane & 3) + (e & 1);
+          sacc[nt][e] = key < valid ? sacc[nt][e] * a.scale_log2 : -INFINITY;
+        }
+      float mx0 = fmaxf(fmaxf(sacc[0][0], sacc[0][1]), fmaxf(sacc[1][0], sacc[1][1]));
+      float mx1 = fmaxf(fmaxf(sacc[0][2], sacc[0][3]), fmaxf(sacc[1][2], sacc[1][3]));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
+      m0 = mn0;
+      m1 = mn1;
+      float ps[2][4];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        ps[nt][0] = exp2f(sacc[nt][0] - mn0);
+        ps[nt][1] = exp2f(sacc[nt][1] - mn0);
+        ps[nt][2] = exp2f(sacc[nt][2] - mn1);
+        ps[nt][3] = exp2f(sacc[nt][3] - mn1);
+      }
+      l0 = l0 * al0 + ps[0][0] + ps[0][1] + ps[1][0] + ps[1][1];
+      l1 = l1 * al1 + ps[0][2] + ps[0][3] + ps[1][2] + ps[1][3];
+#pragma unroll
+      for (int d = 0; d < HD / 8; ++d) {
+        oacc[d][0] *= al0; oacc[d][1] *= al0;
+        oacc[d][2] *= al1; oacc[d][3] *= al1;
+      }
+      const uint32_t pf[4] = {pack_bf16x2(ps[0][0], ps[0][1]), pack_bf16x2(ps[0][2], ps[0][3]),
+                              pack_bf16x2(ps[1][0], ps[1][1]), pack_bf16x2(ps[1][2], ps[1][3])};
+      // O += P V
+      {
+        const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
+        const int hi = lane >> 4;
+#pragma unroll
+        for (int dp = 0; dp < HD / 16; ++dp) {
+          const int ch = dp * 2 + hi;
+          uint32_t vf[4];
+          ldmatrix_x4_trans(vf, smem_u32(vb) + (ch >> 3) * BOX_BYTES + swz(key, ch));
+          const uint32_t b0[2] = {vf[0], vf[1]}, b1[2] = {vf[2], vf[3]};
+          mma_bf16_16816(oacc[2 * dp], pf, b0);
+          mma_bf16_16816(oacc[2 * dp + 1], pf, b1);
+        }
+      }
+      __syncwarp();
+      ++consumed;
+      issue_one();
+    }
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    const float i0 = 1.f / l0, i1 = 1.f / l1;
+    __nv_bfloat16* obase = a.o + (int64_t)it.t * a.qh * HD + (int64_t)it.kvh * R * HD;
+#pragma unroll
+    for (int d = 0; d < HD / 8; ++d) {
+      const int col = d * 8 + 2 * (lane & 3);
+      if (row0 < R)
+        *reinterpret_cast<uint32_t*>(obase + row0 * HD + col) = pack_bf16x2(oacc[d][0] * i0, oacc[d][1] * i0);
+      if (row1 < R)
+        *reinterpret_cast<uint32_t*>(obase + row1 * HD + col) = pack_bf16x2(oacc[d][2] * i1, oacc[d][3] * i1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- prefill
+constexpr int PF_THREADS = 128;
+constexpr int PF_KT = 64;  // keys per tile (4 pages)
+
+template <int HD>
+constexpr int pf_smem() { return 2 * 2 * 4 * 16 * HD * 2 + 64 + 1024; }
+
+template <int HD>
+__global__ void __launch_bounds__(PF_THREADS)
+    prefill_attn_kernel(const __grid_constant__ CUtensorMap pool, const AttnArgs a,
+                        const PrefillItem* __restrict__ items, int n_items) {
+  constexpr int NBOX = HD / 64;
+  constexpr int BLK = 16 * HD * 2;        // one page block (K or V)
+  constexpr int TILE = 4 * BLK;           // 64 keys of K (or V)
+  constexpr int STAGE = 2 * TILE;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * STAGE);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  if (tid == 0) {
+    tma_prefetch_desc(&pool);
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int kh = a.kh, R = a.qh / a.kh;
+  uint32_t tiles_done = 0;  // running count of consumed tiles (phase tracking)
+
+  for (int idx = blockIdx.x; idx < n_items; idx += gridDim.x) {
+    const PrefillItem it = items[idx];
+    const int g = it.h / R;
+    const int n_pages = (it.kv_total + 15) >> 4;
+    const int last_pos = it.pos0 + it.n - 1;
+    const int n_kt = last_pos / PF_KT + 1;
+
+    auto issue = [&](int kt, int s) {  // thread 0 only
+      int np = min(4, n_pages - kt * 4);
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bars[s], np * 2 * BLK);
+      uint8_t* dst = smem + s * STAGE;
+      for (int i = 0; i < np; ++i) {
+        const int64_t page = a.page_ids[it.page_start + kt * 4 + i];
+        const int rowK = (int)(((page * 2 + 0) * kh + g) * 16);
+        const int rowV = rowK + kh * 16;
+        for (int b = 0; b < NBOX; ++b) {
+          tma_load_2d(dst + i * BLK + b * BOX_BYTES, &pool, &bars[s], b * 64, rowK);
+          tma_load_2d(dst + TILE + i * BLK + b * BOX_BYTES, &pool, &bars[s], b * 64, rowV);
+        }
+      }
+    };
+    if (tid == 0) {
+      issue(0, tiles_done & 1);
+      if (n_kt > 1) issue(1, (tiles_done + 1) & 1);
+    }
+
+    // Q fragments of this warp's 16 rows
+    const int r0 = warp * 16 + (lane >> 2), r1 = r0 + 8;
+    const int p0 = it.pos0 + min(r0, it.n - 1), p1 = it.pos0 + min(r1, it.n - 1);
+    const __nv_bfloat16* q0 = a.q + ((int64_t)(it.t0 + min(r0, it.n - 1)) * a.qh + it.h) * HD;
+    const __nv_bfloat16* q1 = a.q + ((int64_t)(it.t0 + min(r1, it.n - 1)) * a.qh + it.h) * HD;
+    uint32_t qf[HD / 16][4];
+#pragma unroll
+    for (int ks = 0; ks < HD / 16; ++ks) {
+      const int kc = ks * 16 + 2 * (lane & 3);
+      qf[ks][0] = ldg_u32(q0 + kc);
+      qf[ks][1] = ldg_u32(q1 + kc);
+      qf[ks][2] = ldg_u32(q0 + kc + 8);
+      qf[ks][3] = ldg_u32(q1 + kc + 8);
+    }
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    float oacc[HD / 8][4];
+#pragma unroll
+    for (int d = 0; d < HD / 8; ++d) oacc[d][0] = oacc[d][1] = oacc[d][2] = oacc[d][3] = 0.f;
+
+    for (int kt = 0; kt < n_kt; ++kt) {
+      const int s = tiles_done & 1;
+      mbar_wait(&bars[s], (tiles_done >> 1) & 1);
+      uint8_t* kb = smem + s * STAGE;
+      uint8_t* vb = kb + TILE;
+      const int valid = min(PF_KT, it.kv_total - kt * PF_KT);
+      if (valid < PF_KT) {  // zero V rows past kv_total (incl. pages not loaded)
+        for (int i = tid; i < (PF_KT - valid) * NBOX * 8; i += PF_THREADS) {
+          const int key = valid + i / (NBOX * 8), rem = i % (NBOX * 8);
+          *reinterpret_cast<uint4*>(vb + (key >> 4) * BLK + (rem >> 3) * BOX_BYTES + (key & 15) * 128 + (rem & 7) * 16) =
+              make_uint4(0, 0, 0, 0);
+        }
+        __syncthreads();
+      }
+      const int kbase = kt * PF_KT;
+      const bool active = kbase <= it.pos0 + min(warp * 16 + 15, it.n - 1);  // warp has visible keys
+      if (active) {
+        float sacc[8][4];
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+        const int hi = (lane >> 3) & 1;
+#pragma unroll
+        for (int n2 = 0; n2 < 4; ++n2) {
+          const int key = n2 * 16 + (lane & 7) + ((lane >> 4) << 3);
+          const uint32_t base = smem_u32(kb) + (key >> 4) * BLK;
+#pragma unroll
+          for (int ks = 0; ks < HD / 16; ++ks) {
+            const int ch = ks * 2 + hi;
+            uint32_t kf[4];
+            ldmatrix_x4(kf, base + (ch >> 3) * BOX_BYTES + swz(key & 15, ch));
+            const uint32_t b0[2] = {kf[0], kf[1]}, b1[2] = {kf[2], kf[3]};
+            mma_bf16_16816(sacc[2 * n2], qf[ks], b0);
+            mma_bf16_16816(sacc[2 * n2 + 1], qf[ks], b1);
+          }
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int key = kbase + nt * 8 + 2 * (lane & 3) + (e & 1);
+            const int pr = e < 2 ? p0 : p1;
+            const float v = key <= pr ? sacc[nt][e] * a.scale_log2 : -INFINITY;
+            sacc[nt][e] = v;
+            if (e < 2) mx0 = fmaxf(mx0, v); else mx1 = fmaxf(mx1, v);
+          }
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
+        m0 = mn0;
+        m1 = mn1;
+        float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          sacc[nt][0] = exp2f(sacc[nt][0] - mn0);
+          sacc[nt][1] = exp2f(sacc[nt][1] - mn0);
+          sacc[nt][2] = exp2f(sacc[nt][2] - mn1);
+          sacc[nt][3] = exp2f(sacc[nt][3] - mn1);
+          rs0 += sacc[nt][0] + sacc[nt][1];
+          rs1 += sacc[nt][2] + sacc[nt][3];
+        }
+        l0 = l0 * al0 + rs0;
+        l1 = l1 * al1 + rs1;
+#pragma unroll
+        for (int d = 0; d < HD / 8; ++d) {
+          oacc[d][0] *= al0; oacc[d][1] *= al0;
+          oacc[d][2] *= al1; oacc[d][3] *= al1;
+        }
+        const int vk = (lane & 7) + (((lane >> 3) & 1) << 3);
+        const int vhi = lane >> 4;
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) {
+          const uint32_t pf[4] = {pack_bf16x2(sacc[2 * kc][0], sacc[2 * kc][1]),
+                                  pack_bf16x2(sacc[2 * kc][2], sacc[2 * kc][3]),
+                                  pack_bf16x2(sacc[2 * kc + 1][0], sacc[2 * kc + 1][1]),
+                                  pack_bf16x2(sacc[2 * kc + 1][2], sacc[2 * kc + 1][3])};
+          const int key = kc * 16 + vk;
+          const uint32_t base = smem_u32(vb) + (key >> 4) * BLK;
+#pragma unroll
+          for (int dp = 0; dp < HD / 16; ++dp) {
+            const int ch = dp * 2 + vhi;
+            uint32_t vf[4];
+            ldmatrix_x4_trans(vf, base + (ch >> 3) * BOX_BYTES + swz(key & 15, ch));
+            const uint32_t b0[2] = {vf[0], vf[1]}, b1[2] = {vf[2], vf[3]};
+            mma_bf16_16816(oacc[2 * dp], pf, b0);
+            mma_bf16_16816(oacc[2 * dp + 1], pf, b1);
+          }
+        }
+      }
+      __syncthreads();
+      ++tiles_done;
+      if (tid == 0 && kt + 2 < n_kt) issue(kt + 2, s);
+    }
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    const float i0 = 1.f / l0, i1 = 1.f / l1;
+#pragma unroll
+    for (int d = 0; d < HD / 8; ++d) {
+      const int col = d * 8 + 2 * (lane & 3);
+      if (r0 < it.n)
+        *reinterpret_cast<uint32_t*>(a.o + ((int64_t)(it.t0 + r0) * a.qh + it.h) * HD + col) =
+            pack_bf16x2(oacc[d][0] * i0, oacc[d][1] * i0);
+      if (r1 < it.n)
+        *reinterpret_cast<uint32_t*>(a.o + ((int64_t)(it.t0 + r1) * a.qh + it.h) * HD + col) =
+            pack_bf16x2(oacc[d][2] * i1, oacc[d][3] * i1);
+    }
+  }
+}
+
+template <int HD>
+cudaError_t launch_decode_hd(const CUtensorMap& m, const AttnArgs& a, const DecodeItem* items, int n_items,
+                             int sm_budget, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         dec_smem<HD>());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int grid = std::min((n_items + DEC_WARPS - 1) / DEC_WARPS, std::max(sm_budget, 1));
+  decode_attn_kernel<HD><<<grid, DEC_WARPS * 32, dec_smem<HD>(), st>>>(m, a, items, n_items);
+  return cudaGetLastError();
+}
+
+template <int HD>
+cudaError_t launch_prefill_hd(const CUtensorMap& m, const AttnArgs& a, const PrefillItem* items, int n_items,
+                              int sm_budget, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         pf_smem<HD>());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int per_sm = std::max(1, (227 * 1024) / pf_smem<HD>());
+  int grid = std::min(n_items, std::max(sm_budget, 1) * per_sm);
+  prefill_attn_kernel<HD><<<grid, PF_THREADS, pf_smem<HD>(), st>>>(m, a, items, n_items);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_decode_attention(const CUtensorMap& m, const AttnArgs& a, const DecodeItem* items, int n_items,
+                                    int sm_budget, cudaStream_t st) {
+  if (n_items <= 0) return cudaSuccess;
+  if (a.hd == 128) return launch_decode_hd<128>(m, a, items, n_items, sm_budget, st);
+  if (a.hd == 64) return launch_decode_hd<64>(m, a, items, n_items, sm_budget, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_prefill_attention(const CUtensorMap& m, const AttnArgs& a, const PrefillItem* items,
+                                     int n_items, int sm_budget, cudaStream_t st) {
+  if (n_items <= 0) return cudaSuccess;
+  if (a.hd == 128) return launch_prefill_hd<128>(m, a, items, n_items, sm_budget, st);
+  if (a.hd == 64) return launch_prefill_hd<64>(m, a, items, n_items, sm_budget, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace nf

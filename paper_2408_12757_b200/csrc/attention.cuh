@@ -1,0 +1,37 @@
+// Internal interface of the paged attention kernels.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nf {
+
+// One decode work item: query token row t attends with its R = qh/kh query
+// heads of KV group `kvh` over kv_len keys listed from page_ids[page_start].
+struct DecodeItem {
+  int t, kvh, kv_len, page_start;
+};
+// One prefill work item: query rows [t0, t0+n) of one request (positions
+// prefix+i0 ..), query head h; keys 0..prefix+i0+n-1 causal.
+struct PrefillItem {
+  int t0, n, pos0, h;   // first token row, rows in tile (<=64), position of row 0, query head
+  int kv_total, page_start, pad0, pad1;
+};
+
+struct AttnArgs {
+  const __nv_bfloat16* q;   // [T, qh, hd]
+  __nv_bfloat16* o;         // [T, qh*hd]
+  const int* page_ids;
+  int qh, kh, hd, page_size;
+  float scale_log2;         // log2(e)/sqrt(hd)
+};
+
+cudaError_t make_pool_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, int kh, int hd, int page_size);
+
+cudaError_t launch_decode_attention(const CUtensorMap& pool_map, const AttnArgs& a, const DecodeItem* items,
+                                    int n_items, int sm_budget, cudaStream_t stream);
+cudaError_t launch_prefill_attention(const CUtensorMap& pool_map, const AttnArgs& a, const PrefillItem* items,
+                                     int n_items, int sm_budget, cudaStream_t stream);
+
+}  // namespace nf

@@ -1,0 +1,366 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a with the decoder
+// layer's fused epilogues.
+//
+//   warp 0 lane 0 : TMA producer (A and B 128B-swizzled K-major tiles, 4-stage ring)
+//   warp 1 lane 0 : tcgen05.mma issuer (M=128, N=256, K=16 per instruction, f32 in TMEM)
+//   warp 2        : TMEM allocator (2 accumulator stages x 256 columns = 512 columns)
+//   warps 4..7    : epilogue (tcgen05.ld: one thread per accumulator row)
+//
+// The grid is min(#tiles, SM budget): one CTA per SM (smem-bound), so the SM
+// budget of the nano-batch plan ("limits the execution units
+// usage of each kernel") is exactly the number of SMs the GEMM occupies.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace nf {
+
+namespace {
+
+constexpr int A_STAGE_ELEMS = GEMM_BM * GEMM_BK;
+constexpr int B_STAGE_ELEMS = GEMM_BN * GEMM_BK;
+constexpr uint32_t STAGE_BYTES = (A_STAGE_ELEMS + B_STAGE_ELEMS) * 2;
+
+NF_DEV void store32_bf16(__nv_bfloat16* dst, const float (&v)[32]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u;
+    u.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+    u.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+    u.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+    u.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+    d[q] = u;
+  }
+}
+
+NF_DEV void load32_bf16(const __nv_bfloat16* src, float (&v)[32]) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u = s[q];
+    float2 a = unpack_bf16x2(u.x), b = unpack_bf16x2(u.y), c = unpack_bf16x2(u.z), d = unpack_bf16x2(u.w);
+    v[q * 8 + 0] = a.x; v[q * 8 + 1] = a.y; v[q * 8 + 2] = b.x; v[q * 8 + 3] = b.y;
+    v[q * 8 + 4] = c.x; v[q * 8 + 5] = c.y; v[q * 8 + 6] = d.x; v[q * 8 + 7] = d.y;
+  }
+}
+
+NF_DEV void ld32f(uint32_t taddr, float s, float (&v)[32]) {
+  uint32_t r[32];
+  tmem_ld32(taddr, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * s;
+}
+
+// sin/cos of a large fp32 angle: Cody-Waite reduction to [-pi, pi] then SFU.
+NF_DEV void sincos_reduced(float a, float* s, float* c) {
+  const float k = rintf(a * 0.15915494309189535f);
+  float r = fmaf(-k, 6.28318548202514648f, a);
+  r = fmaf(-k, -1.7484556e-07f, r);
+  __sincosf(r, s, c);
+}
+
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __nv_bfloat16* sA = reinterpret_cast<__nv_bfloat16*>(smem);
+  __nv_bfloat16* sB = sA + GEMM_STAGES * A_STAGE_ELEMS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + GEMM_STAGES * B_STAGE_ELEMS);
+  uint64_t* empty = full + GEMM_STAGES;
+  uint64_t* tfull = empty + GEMM_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* inv_freq = reinterpret_cast<float*>(tmem_slot + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int M = args.M, N = args.N, K = args.K;
+  const int tiles_m = (M + GEMM_BM - 1) / GEMM_BM;
+  const int tiles_n = (N + GEMM_BN - 1) / GEMM_BN;
+  const int tiles = tiles_m * tiles_n;
+  const int num_kb = (K + GEMM_BK - 1) / GEMM_BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < GEMM_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (args.epi == EPI_QKV && warp >= 4) {
+    const int i = threadIdx.x - 128;
+    if (i < args.hd / 2) inv_freq[i] = (float)exp2(-(2.0 * i / args.hd) * (double)args.log2_theta);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int mb = tile % tiles_m, nb = tile / tiles_m;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(sA + stage * A_STAGE_ELEMS, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM);
+          tma_load_2d(sB + stage * B_STAGE_ELEMS, &tmB, &full[stage], kb * GEMM_BK, nb * GEMM_BN);
+          if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, GEMM_BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int as = 0;
+      uint32_t aphase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + as * GEMM_BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = sdesc_sw128(sA + stage * A_STAGE_ELEMS);
+          const uint64_t bd = sdesc_sw128(sB + stage * B_STAGE_ELEMS);
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k)
+            umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          umma_commit(&empty[stage]);
+          if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[as]);
+        as ^= 1;
+        if (as == 0) aphase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------------- epilogue
+    const int ew = warp - 4;
+    int as = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const int mb = tile % tiles_m, nb = tile / tiles_m;
+      mbar_wait(&tfull[as], aphase);
+      tc_fence_after();
+      const int r = mb * GEMM_BM + ew * 32 + lane;
+      const bool valid = r < M;
+      const uint32_t taddr = tmem_base + as * GEMM_BN + ((uint32_t)(ew * 32) << 16);
+      float s = 1.f;
+      if (args.norm_part != nullptr && valid) {
+        float acc = 0.f;
+        for (int p = 0; p < args.norm_nparts; ++p) acc += args.norm_part[(int64_t)p * args.norm_stride + r];
+        s = rsqrtf(acc * args.inv_d + args.eps);
+      }
+      const int n0 = nb * GEMM_BN;
+      float v[32];
+      switch (args.epi) {
+        case EPI_STORE:
+        case EPI_F32: {
+#pragma unroll 1
+          for (int c = 0; c < GEMM_BN / 32; ++c) {
+            ld32f(taddr + c * 32, s, v);
+            const int col = n0 + c * 32;
+            if (valid && col < N) {
+              if (args.epi == EPI_STORE) {
+                store32_bf16(args.out + (int64_t)r * args.ldo + col, v);
+              } else {
+                float4* d = reinterpret_cast<float4*>(args.outf + (int64_t)r * args.ldo + col);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              }
+            }
+          }
+          break;
+        }
+        case EPI_RESID: {
+          float sq = 0.f;
+#pragma unroll 1
+          for (int c = 0; c < GEMM_BN / 32; ++c) {
+            ld32f(taddr + c * 32, s, v);
+            const int col = n0 + c * 32;
+            if (valid && col < N) {
+              float rr[32];
+              load32_bf16(args.resid + (int64_t)r * args.ldr + col, rr);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                v[j] = round_bf16(rr[j] + v[j]);
+                sq = fmaf(v[j], v[j], sq);
+              }
+              store32_bf16(args.out + (int64_t)r * args.ldo + col, v);
+            }
+          }
+          if (args.sq_out != nullptr && valid) args.sq_out[(int64_t)nb * args.sq_stride + r] = sq;
+          break;
+        }
+        case EPI_SILU: {
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            float u[32];
+            ld32f(taddr + c * 32, s, v);
+            ld32f(taddr + 128 + c * 32, s, u);
+            const int col = nb * 128 + c * 32;
+            if (valid && col < args.n_valid) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const float g = v[j];
+                v[j] = g / (1.f + __expf(-g)) * u[j];
+              }
+              store32_bf16(args.out + (int64_t)r * args.ldo + col, v);
+            }
+          }
+          break;
+        }
+        case EPI_QKV: {
+          const int hd = args.hd, qh = args.qh, kh = args.kh;
+          const int hpt = GEMM_BN / hd;
+          const int pos = valid ? args.tok_pos[r] : 0;
+          const int slot = valid ? args.tok_slot[r] : 0;
+          const int64_t page = slot / args.page_size, off = slot % args.page_size;
+#pragma unroll 1
+          for (int hh = 0; hh < hpt; ++hh) {
+            const int gh = nb * hpt + hh;
+            if (gh >= qh + 2 * kh) break;
+            __nv_bfloat16* dst;
+            if (gh < qh) {
+              dst = args.q_out + (int64_t)r * qh * hd + (int64_t)gh * hd;
+            } else {
+              const int kv = gh < qh + kh ? 0 : 1;
+              const int kvh = gh - qh - kv * kh;
+              dst = args.kv_pool + (((page * 2 + kv) * kh + kvh) * args.page_size + off) * hd;
+            }
+            if (gh >= qh + kh) {  // V: no rotation
+#pragma unroll 1
+              for (int c = 0; c < hd / 32; ++c) {
+                ld32f(taddr + hh * hd + c * 32, s, v);
+                if (valid) store32_bf16(dst + c * 32, v);
+              }
+            } else {  // Q or K: rotate-half RoPE at pos (reading A-4)
+#pragma unroll 1
+              for (int c = 0; c < hd / 64; ++c) {
+                float x2[32];
+                ld32f(taddr + hh * hd + c * 32, s, v);
+                ld32f(taddr + hh * hd + hd / 2 + c * 32, s, x2);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                  float sn, cs;
+                  sincos_reduced((float)pos * inv_freq[c * 32 + j], &sn, &cs);
+                  const float a = v[j], b = x2[j];
+                  v[j] = a * cs - b * sn;
+                  x2[j] = b * cs + a * sn;
+                }
+                if (valid) {
+                  store32_bf16(dst + c * 32, v);
+                  store32_bf16(dst + hd / 2 + c * 32, x2);
+                }
+              }
+            }
+          }
+          break;
+        }
+        case EPI_ARGMAX: {
+          float best = -INFINITY;
+          int bi = 0x7fffffff;
+#pragma unroll 1
+          for (int c = 0; c < GEMM_BN / 32; ++c) {
+            ld32f(taddr + c * 32, 1.f, v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int col = n0 + c * 32 + j;
+              if (col < N && v[j] > best) { best = v[j]; bi = col; }
+            }
+          }
+          if (valid) {
+            args.am_val[(int64_t)nb * args.am_stride + r] = best;
+            args.am_idx[(int64_t)nb * args.am_stride + r] = bi;
+          }
+          break;
+        }
+        default:
+          break;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+      as ^= 1;
+      if (as == 0) aphase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_once;
+bool g_attr_set = false;
+
+cudaError_t get_encode() {
+  std::call_once(g_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode ? cudaSuccess : cudaErrorNotSupported;
+}
+
+}  // namespace
+
+// 2D bf16 tensor map [outer rows, inner cols] with 128B swizzle.
+cudaError_t make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                           uint32_t box_inner, uint32_t box_outer) {
+  cudaError_t e = get_encode();
+  if (e != cudaSuccess) return e;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb,
+                        const GemmArgs& args, int sm_budget, cudaStream_t stream) {
+  if (args.M <= 0) return cudaSuccess;
+  CUtensorMap ta, tb;
+  cudaError_t e = make_tmap_bf16(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
+  if (e != cudaSuccess) return e;
+  e = make_tmap_bf16(&tb, B, args.K, args.N, ldb, GEMM_BK, GEMM_BN);
+  if (e != cudaSuccess) return e;
+  if (!g_attr_set) {
+    e = cudaFuncSetAttribute(gemm_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+    if (e != cudaSuccess) return e;
+    g_attr_set = true;
+  }
+  const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + GEMM_BN - 1) / GEMM_BN);
+  int grid = tiles < sm_budget ? tiles : sm_budget;
+  if (grid < 1) grid = 1;
+  gemm_tcgen05_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(ta, tb, args);
+  return cudaGetLastError();
+}
+
+}  // namespace nf

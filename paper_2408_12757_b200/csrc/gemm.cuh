@@ -1,0 +1,62 @@
+// Internal interface of the persistent tcgen05 GEMM (C = A . B^T, bf16 in, f32
+// accumulate in TMEM) with the fused epilogues of the decoder layer.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nf {
+
+enum GemmEpiMode : int {
+  EPI_STORE = 0,   // out = bf16(acc * row_scale)
+  EPI_RESID = 1,   // out = bf16(resid + acc); optional sum-of-squares partials of out
+  EPI_SILU = 2,    // tile = [gate 128 | up 128]: out = bf16(silu(g*s) * (u*s))
+  EPI_QKV = 3,     // q/k RoPE at pos, q -> q_out, k/v -> paged KV pool slots
+  EPI_ARGMAX = 4,  // per (n-tile,row) partial (max, argmax) of acc
+  EPI_F32 = 5,     // outf = acc * row_scale (f32, for TP partial sums)
+};
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BN = 256;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_STAGES = 4;
+constexpr int GEMM_THREADS = 256;  // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warps 4-7 epilogue
+constexpr int GEMM_SMEM = GEMM_STAGES * (GEMM_BM + GEMM_BN) * GEMM_BK * 2 + 1024 + 256;
+
+struct GemmArgs {
+  int epi;
+  int M, N, K;          // rows of A in this launch, rows of B (packed output columns), reduction dim
+  int n_valid;          // valid output columns (EPI_SILU: F; else N)
+  // outputs (row-indexed pointers are pre-offset to the launch's first row)
+  __nv_bfloat16* out;
+  int64_t ldo;
+  float* outf;
+  const __nv_bfloat16* resid;
+  int64_t ldr;
+  // row scale from RMS partials: s = rsqrt(sum_p norm_part[p*norm_stride + r] * inv_d + eps)
+  const float* norm_part;
+  int norm_nparts;
+  int64_t norm_stride;
+  float inv_d, eps;
+  // sum-of-squares partial output: sq_out[n_tile * sq_stride + r]
+  float* sq_out;
+  int64_t sq_stride;
+  // EPI_QKV
+  int qh, kh, hd, page_size;
+  float log2_theta;
+  const int* tok_pos;    // [M]
+  const int* tok_slot;   // [M] page*page_size + offset
+  __nv_bfloat16* q_out;  // [M, qh, hd]
+  __nv_bfloat16* kv_pool;
+  // EPI_ARGMAX
+  float* am_val;
+  int* am_idx;
+  int64_t am_stride;
+};
+
+// A: [M, K] row-major (lda elements), B: [N, K] row-major (ldb elements).
+// grid = min(tiles, sm_budget) persistent CTAs, one per SM.
+cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb,
+                        const GemmArgs& args, int sm_budget, cudaStream_t stream);
+
+}  // namespace nf

@@ -1,0 +1,82 @@
+// Host-side internals shared by the ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/nf.h"
+#include "attention.cuh"
+
+namespace nf {
+
+nf_status set_error(nf_status s, const char* fmt, ...);
+inline nf_status ok() { return NF_OK; }
+
+#define NF_CUDA(call)                                                                                  \
+  do {                                                                                                 \
+    cudaError_t _e = (call);                                                                           \
+    if (_e != cudaSuccess) return set_error(NF_ECUDA, "%s failed: %s", #call, cudaGetErrorString(_e)); \
+  } while (0)
+#define NF_TRY(call)                   \
+  do {                                 \
+    nf_status _s = (call);             \
+    if (_s != NF_OK) return _s;        \
+  } while (0)
+
+nf_status validate_cfg(const nf_model_cfg* c);
+nf_status validate_batch(const nf_model_cfg* c, const nf_batch* b);
+int64_t batch_tokens(const nf_batch* b);
+
+struct NanoRange {
+  int r0, r1;        // requests [r0, r1) in the internal (permuted) order
+  int t0, t1;        // token rows
+  int dec_off, dec_n;  // decode items
+  int pf_off, pf_n;    // prefill items
+};
+
+// Per-step metadata in the internal token order (request permutation `order`).
+struct StepMeta {
+  std::vector<int32_t> buf;   // int32 words uploaded to the workspace
+  size_t off_pos = 0, off_slot = 0, off_pages = 0, off_dec = 0, off_pf = 0, off_emit_row = 0, off_emit_req = 0,
+         off_tok_src = 0;
+  int T = 0, n_req = 0, n_emit = 0;
+  std::vector<NanoRange> nanos;
+};
+
+// Upper bound of StepMeta words for a batch (workspace sizing).
+size_t meta_words_bound(const nf_model_cfg* c, const nf_batch* b);
+// order: internal request order (size n_req); req_cuts: nano-batch boundaries in that order.
+void build_meta(const nf_model_cfg* c, const nf_batch* b, const std::vector<int>& order, const std::vector<int>& req_cuts,
+                StepMeta* m);
+std::vector<int> snap_cuts_impl(const std::vector<int64_t>& row_start_of_boundary, int n_nano, const int32_t* share);
+
+struct Workspace {
+  int32_t* meta;
+  __nv_bfloat16 *q, *o, *o_full, *h1, *m, *xa, *xb, *lm_rows;
+  float *part_a, *part_b, *part_h1, *lm_part, *am_val;
+  int* am_idx;
+  float* red;  // TP partial sums (f32)
+  size_t total;
+};
+Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base);
+
+}  // namespace nf
+
+struct nf_plan {
+  nf_model_cfg cfg;
+  nf_plan_spec spec;
+  std::string csv;
+  // runtime resources (lazily created)
+  int device = -1;
+  cudaStream_t mem_stream = nullptr;
+  cudaEvent_t ev_kqv[NF_MAX_NANO] = {};
+  cudaEvent_t ev_att[NF_MAX_NANO] = {};
+  cudaEvent_t ev_join = nullptr;
+  cudaEvent_t ev_upload[2] = {};
+  void* pinned[2] = {nullptr, nullptr};
+  size_t pinned_cap[2] = {0, 0};
+  int upload_idx = 0;
+};

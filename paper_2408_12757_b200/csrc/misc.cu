@@ -1,0 +1,139 @@
+// Small bandwidth-bound kernels around the GEMMs: embedding gather, RMS
+// sum-of-squares partials, LM-head row gather, argmax reduction and the
+// one-time weight packing (RMSNorm gamma folding, gate/up interleave).
+#include "common.cuh"
+#include "misc.cuh"
+
+namespace nf {
+
+namespace {
+
+// one warp per row: dst[row] = src[idx[row]] (bf16, D % 8 == 0), sumsq -> part[row]
+// (idx2 != null: source row = idx[idx2[row]], an embedding lookup in a permuted row order)
+__global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, const int* __restrict__ idx,
+                                   const int* __restrict__ idx2, int rows, int D, __nv_bfloat16* __restrict__ dst,
+                                   float* __restrict__ part) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const int64_t s = idx ? (int64_t)idx[idx2 ? idx2[warp] : warp] : (int64_t)warp;
+  const uint4* in = reinterpret_cast<const uint4*>(src + s * D);
+  uint4* out = dst ? reinterpret_cast<uint4*>(dst + (int64_t)warp * D) : nullptr;
+  float sq = 0.f;
+  for (int i = lane; i < D / 8; i += 32) {
+    uint4 u = in[i];
+    if (out) out[i] = u;
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 f = unpack_bf16x2(w[k]);
+      sq = fmaf(f.x, f.x, sq);
+      sq = fmaf(f.y, f.y, sq);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane == 0 && part) part[warp] = sq;
+}
+
+// ids[r] = argmax over tiles of (val, idx); ties -> lowest index
+__global__ void argmax_reduce_kernel(const float* __restrict__ val, const int* __restrict__ idx, int ntiles,
+                                     int64_t stride, int rows, const int* __restrict__ row_req,
+                                     int* __restrict__ next_ids) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int t = 0; t < ntiles; ++t) {
+    const float v = val[t * stride + r];
+    const int i = idx[t * stride + r];
+    if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+  }
+  next_ids[row_req ? row_req[r] : r] = bi;
+}
+
+__global__ void fill_i32_kernel(int* p, int n, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// dst[o, i] = bf16(src[o, i] * gamma[i]) for rows [0, rows) (gamma may be null)
+__global__ void scale_cols_kernel(const __nv_bfloat16* __restrict__ src, const __nv_bfloat16* __restrict__ gamma,
+                                  int64_t rows, int cols, __nv_bfloat16* __restrict__ dst) {
+  const int64_t n = rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % cols);
+    float v = __bfloat162float(src[e]);
+    if (gamma) v *= __bfloat162float(gamma[c]);
+    dst[e] = __float2bfloat16_rn(v);
+  }
+}
+
+// packed [nblk*256, D]: block j rows 0..127 = gate[j*128 + r], rows 128..255 = up[j*128 + r]
+// (zero rows past F), each scaled by gamma over columns.
+__global__ void pack_gate_up_kernel(const __nv_bfloat16* __restrict__ gate, const __nv_bfloat16* __restrict__ up,
+                                    const __nv_bfloat16* __restrict__ gamma, int F, int D, int nblk,
+                                    __nv_bfloat16* __restrict__ dst) {
+  const int64_t n = (int64_t)nblk * 256 * D;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % D);
+    const int64_t row = e / D;
+    const int j = (int)(row / 256), rr = (int)(row % 256);
+    const int f = j * 128 + (rr & 127);
+    float v = 0.f;
+    if (f < F) {
+      const __nv_bfloat16* srcm = rr < 128 ? gate : up;
+      v = __bfloat162float(srcm[(int64_t)f * D + c]);
+      if (gamma) v *= __bfloat162float(gamma[c]);
+    }
+    dst[e] = __float2bfloat16_rn(v);
+  }
+}
+
+int grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  return (int)(g > 148 * 32 ? 148 * 32 : (g < 1 ? 1 : g));
+}
+
+}  // namespace
+
+cudaError_t launch_gather_rows(const __nv_bfloat16* src, const int* idx, int rows, int D, __nv_bfloat16* dst,
+                               float* part, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  gather_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(src, idx, nullptr, rows, D, dst, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_ids_embed(const __nv_bfloat16* embed, const int* token_ids, const int* tok_src, int rows, int D,
+                                    __nv_bfloat16* dst, float* part, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  gather_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(embed, token_ids, tok_src, rows, D, dst, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_argmax_reduce(const float* val, const int* idx, int ntiles, int64_t stride, int rows,
+                                 const int* row_req, int* next_ids, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  argmax_reduce_kernel<<<(rows + 127) / 128, 128, 0, st>>>(val, idx, ntiles, stride, rows, row_req, next_ids);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_i32(int* p, int n, int v, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  fill_i32_kernel<<<(n + 255) / 256, 256, 0, st>>>(p, n, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_cols(const __nv_bfloat16* src, const __nv_bfloat16* gamma, int64_t rows, int cols,
+                              __nv_bfloat16* dst, cudaStream_t st) {
+  scale_cols_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(src, gamma, rows, cols, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_gate_up(const __nv_bfloat16* gate, const __nv_bfloat16* up, const __nv_bfloat16* gamma, int F,
+                                int D, __nv_bfloat16* dst, cudaStream_t st) {
+  const int nblk = (F + 127) / 128;
+  pack_gate_up_kernel<<<grid_for((int64_t)nblk * 256 * D, 256), 256, 0, st>>>(gate, up, gamma, F, D, nblk, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace nf

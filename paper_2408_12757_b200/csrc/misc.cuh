@@ -1,0 +1,18 @@
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nf {
+cudaError_t launch_gather_rows(const __nv_bfloat16* src, const int* idx, int rows, int D, __nv_bfloat16* dst,
+                               float* part, cudaStream_t st);
+cudaError_t launch_gather_ids_embed(const __nv_bfloat16* embed, const int* token_ids, const int* tok_src, int rows, int D,
+                                    __nv_bfloat16* dst, float* part, cudaStream_t st);
+cudaError_t launch_argmax_reduce(const float* val, const int* idx, int ntiles, int64_t stride, int rows,
+                                 const int* row_req, int* next_ids, cudaStream_t st);
+cudaError_t launch_fill_i32(int* p, int n, int v, cudaStream_t st);
+cudaError_t launch_scale_cols(const __nv_bfloat16* src, const __nv_bfloat16* gamma, int64_t rows, int cols,
+                              __nv_bfloat16* dst, cudaStream_t st);
+cudaError_t launch_pack_gate_up(const __nv_bfloat16* gate, const __nv_bfloat16* up, const __nv_bfloat16* gamma, int F,
+                                int D, __nv_bfloat16* dst, cudaStream_t st);
+}  // namespace nf

@@ -1,0 +1,281 @@
+"""Thin ctypes binding of include/nf.h (argument marshalling only).
+
+Every compute step runs in libnf.so's CUDA kernels; there is no Python or CPU
+fallback.  If the library is missing, importing this module raises.
+Device buffers are passed as integer device pointers (e.g. torch
+``tensor.data_ptr()``), streams as integer ``cudaStream_t`` handles.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("NF_LIB", os.path.join(_HERE, "libnf.so"))
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libnf.so not built at {LIB_PATH}: run `python -m paper_2408_12757_b200.build` "
+                      "(there is no CPU fallback)")
+lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+
+NF_OK, NF_EINVAL, NF_EUNSUPPORTED, NF_EINFEASIBLE, NF_ECUDA, NF_ENCCL, NF_ENOMEM = range(7)
+SEQUENTIAL, NANO_ONLY, OVERLAP = 0, 1, 2
+OP_KQV, OP_DECODE_ATTN, OP_PREFILL_ATTN, OP_O, OP_UG, OP_DOWN, OP_NET, OP_COUNT = range(8)
+MAX_NANO = 4
+P_i32 = C.POINTER(C.c_int32)
+
+
+class NFError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"nf status {status}: {msg}")
+        self.status = status
+
+
+class ModelCfg(C.Structure):
+    _fields_ = [("d_model", C.c_int32), ("n_layers", C.c_int32), ("n_q_heads", C.c_int32),
+                ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("d_ffn", C.c_int32),
+                ("vocab", C.c_int32), ("rms_eps", C.c_float), ("rope_theta", C.c_float),
+                ("page_size", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32)]
+
+
+class _Batch(C.Structure):
+    _fields_ = [("n_req", C.c_int32), ("q_len", P_i32), ("kv_prefix", P_i32), ("page_indptr", P_i32),
+                ("page_ids", P_i32), ("n_pages_pool", C.c_int32), ("emit", P_i32)]
+
+
+class PlanSpec(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("n_nano", C.c_int32), ("share", C.c_int32 * MAX_NANO),
+                ("sm", C.c_int32 * OP_COUNT), ("balance", C.c_int32)]
+
+
+class CurvePoint(C.Structure):
+    _fields_ = [("op_kind", C.c_int32), ("units", C.c_int32), ("work", C.c_double), ("latency_s", C.c_double)]
+
+
+class PlanOpts(C.Structure):
+    _fields_ = [("sm_budget", C.c_int32), ("sm_quantum", C.c_int32), ("mode", C.c_int32),
+                ("n_nano", C.c_int32), ("max_iters", C.c_int32)]
+
+
+class LayerWeights(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("attn_norm", "w_q", "w_k", "w_v", "w_o", "w_o_col", "w_o_row",
+                                          "ffn_norm", "w_gate", "w_up", "w_down")]
+
+
+class PackedLayer(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("w_qkv", "w_o", "w_o_row", "w_gate_up", "w_down")]
+
+
+class ModelWeights(C.Structure):
+    _fields_ = [("embed", C.c_void_p), ("layers", C.POINTER(PackedLayer)), ("lm_head_packed", C.c_void_p)]
+
+
+def _sig(name, restype, *args):
+    f = getattr(lib, name)
+    f.restype = restype
+    f.argtypes = list(args)
+    return f
+
+
+_sig("nf_last_error", C.c_char_p)
+_sig("nf_abi_version", C.c_int32)
+_sig("nf_batch_metadata", C.c_int, C.POINTER(ModelCfg), C.POINTER(_Batch), P_i32, P_i32)
+_sig("nf_snap_cuts", C.c_int, C.POINTER(_Batch), C.c_int32, P_i32, P_i32)
+_sig("nf_plan_create_explicit", C.c_int, C.POINTER(ModelCfg), C.POINTER(PlanSpec), C.POINTER(C.c_void_p))
+_sig("nf_plan_create", C.c_int, C.POINTER(ModelCfg), C.POINTER(_Batch), C.POINTER(CurvePoint), C.c_int32,
+     C.POINTER(PlanOpts), C.POINTER(C.c_void_p))
+_sig("nf_plan_get_spec", C.c_int, C.c_void_p, C.POINTER(PlanSpec))
+_sig("nf_plan_export_csv", C.c_int, C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t))
+_sig("nf_plan_destroy", None, C.c_void_p)
+_sig("nf_comm_unique_id", C.c_int, C.c_void_p)
+_sig("nf_comm_create", C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p))
+_sig("nf_comm_destroy", None, C.c_void_p)
+_sig("nf_packed_layer_bytes", C.c_int, C.POINTER(ModelCfg), C.POINTER(C.c_size_t))
+_sig("nf_pack_layer", C.c_int, C.POINTER(ModelCfg), C.POINTER(LayerWeights), C.POINTER(PackedLayer), C.c_void_p)
+_sig("nf_pack_lm_head", C.c_int, C.POINTER(ModelCfg), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+_sig("nf_workspace_size", C.c_int, C.POINTER(ModelCfg), C.POINTER(_Batch), C.POINTER(C.c_size_t))
+_sig("nf_layer_forward", C.c_int, C.c_void_p, C.c_void_p, C.POINTER(PackedLayer), C.c_void_p, C.POINTER(_Batch),
+     C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+_sig("nf_model_step", C.c_int, C.c_void_p, C.c_void_p, C.POINTER(ModelWeights), C.POINTER(C.c_void_p),
+     C.POINTER(_Batch), C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+_sig("nf_gemm_bf16", C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
+     C.c_int32, C.c_int32, C.c_int32, C.c_void_p)
+_sig("nf_attention", C.c_int, C.POINTER(ModelCfg), C.POINTER(_Batch), C.c_void_p, C.c_void_p, C.c_void_p,
+     C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.c_void_p)
+
+EXPORTED = ["nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
+            "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_comm_unique_id",
+            "nf_comm_create", "nf_comm_destroy", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
+            "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_gemm_bf16", "nf_attention"]
+
+
+def _check(status: int):
+    if status != NF_OK:
+        raise NFError(status, lib.nf_last_error().decode())
+
+
+def last_error() -> str:
+    return lib.nf_last_error().decode()
+
+
+def model_cfg(d_model, n_layers, n_q_heads, n_kv_heads, head_dim, d_ffn, vocab, rms_eps=1e-5, rope_theta=1e4,
+              page_size=16, tp_size=1, tp_rank=0) -> ModelCfg:
+    return ModelCfg(d_model, n_layers, n_q_heads, n_kv_heads, head_dim, d_ffn, vocab, rms_eps, rope_theta,
+                    page_size, tp_size, tp_rank)
+
+
+class Batch:
+    """Host-side nf_batch; keeps its int32 arrays alive."""
+
+    def __init__(self, q_len, kv_prefix, page_indptr, page_ids, n_pages_pool: int, emit=None):
+        self.q_len = np.ascontiguousarray(q_len, dtype=np.int32)
+        self.kv_prefix = np.ascontiguousarray(kv_prefix, dtype=np.int32)
+        self.page_indptr = np.ascontiguousarray(page_indptr, dtype=np.int32)
+        self.page_ids = np.ascontiguousarray(page_ids, dtype=np.int32)
+        self.emit = None if emit is None else np.ascontiguousarray(emit, dtype=np.int32)
+        p = lambda a: a.ctypes.data_as(P_i32)
+        self.c = _Batch(len(self.q_len), p(self.q_len), p(self.kv_prefix), p(self.page_indptr), p(self.page_ids),
+                        int(n_pages_pool), p(self.emit) if self.emit is not None else None)
+
+    @classmethod
+    def from_any(cls, b, emit=None) -> "Batch":
+        return cls(b.q_len, b.kv_prefix, b.page_indptr, b.page_ids, b.n_pages_pool, emit)
+
+    @property
+    def n_tokens(self) -> int:
+        return int(self.q_len.sum())
+
+
+def batch_metadata(cfg: ModelCfg, b: Batch):
+    T = b.n_tokens
+    pos = np.zeros(T, np.int32)
+    slot = np.zeros(T, np.int32)
+    _check(lib.nf_batch_metadata(C.byref(cfg), C.byref(b.c), pos.ctypes.data_as(P_i32), slot.ctypes.data_as(P_i32)))
+    return pos, slot
+
+
+def snap_cuts(b: Batch, shares: Sequence[int]):
+    sh = np.ascontiguousarray(shares, dtype=np.int32)
+    out = np.zeros(len(sh) + 1, np.int32)
+    _check(lib.nf_snap_cuts(C.byref(b.c), len(sh), sh.ctypes.data_as(P_i32), out.ctypes.data_as(P_i32)))
+    return out
+
+
+class Plan:
+    def __init__(self, handle: int):
+        self.h = C.c_void_p(handle)
+
+    @classmethod
+    def explicit(cls, cfg: ModelCfg, mode: int = SEQUENTIAL, shares: Sequence[int] = (1,),
+                 sm: Optional[Sequence[int]] = None, balance: bool = False) -> "Plan":
+        spec = PlanSpec()
+        spec.mode = mode
+        spec.n_nano = len(shares)
+        for i, s in enumerate(shares):
+            spec.share[i] = int(s)
+        sm = [148] * OP_COUNT if sm is None else list(sm)
+        for i in range(OP_COUNT):
+            spec.sm[i] = int(sm[i])
+        spec.balance = int(balance)
+        h = C.c_void_p()
+        _check(lib.nf_plan_create_explicit(C.byref(cfg), C.byref(spec), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def search(cls, cfg: ModelCfg, shape: Batch, points: Sequence[tuple], sm_budget=148, sm_quantum=8,
+               mode=OVERLAP, n_nano=2, max_iters=200) -> "Plan":
+        arr = (CurvePoint * len(points))(*[CurvePoint(int(k), int(u), float(w), float(t)) for k, u, w, t in points])
+        opts = PlanOpts(sm_budget, sm_quantum, mode, n_nano, max_iters)
+        h = C.c_void_p()
+        _check(lib.nf_plan_create(C.byref(cfg), C.byref(shape.c), arr, len(points), C.byref(opts), C.byref(h)))
+        return cls(h.value)
+
+    def spec(self) -> PlanSpec:
+        s = PlanSpec()
+        _check(lib.nf_plan_get_spec(self.h, C.byref(s)))
+        return s
+
+    def csv(self) -> str:
+        n = C.c_size_t()
+        _check(lib.nf_plan_export_csv(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib.nf_plan_export_csv(self.h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value:
+            lib.nf_plan_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+def packed_layer_bytes(cfg: ModelCfg):
+    out = (C.c_size_t * 5)()
+    _check(lib.nf_packed_layer_bytes(C.byref(cfg), out))
+    return list(out)
+
+
+def pack_layer(cfg: ModelCfg, src: dict, dst: dict, stream: int):
+    lw = LayerWeights(*[src.get(n) for n, _ in LayerWeights._fields_])
+    pl = PackedLayer(*[dst.get(n) for n, _ in PackedLayer._fields_])
+    _check(lib.nf_pack_layer(C.byref(cfg), C.byref(lw), C.byref(pl), C.c_void_p(stream)))
+
+
+def pack_lm_head(cfg: ModelCfg, lm_head: int, final_norm: int, dst: int, stream: int):
+    _check(lib.nf_pack_lm_head(C.byref(cfg), C.c_void_p(lm_head), C.c_void_p(final_norm), C.c_void_p(dst),
+                               C.c_void_p(stream)))
+
+
+def workspace_size(cfg: ModelCfg, b: Batch) -> int:
+    n = C.c_size_t()
+    _check(lib.nf_workspace_size(C.byref(cfg), C.byref(b.c), C.byref(n)))
+    return n.value
+
+
+def layer_forward(plan: Plan, packed: dict, kv_pool: int, b: Batch, x_in: int, x_out: int, ws: int, ws_bytes: int,
+                  stream: int, comm: Optional[int] = None):
+    pl = PackedLayer(*[packed.get(n) for n, _ in PackedLayer._fields_])
+    _check(lib.nf_layer_forward(plan.h, C.c_void_p(comm), C.byref(pl), C.c_void_p(kv_pool), C.byref(b.c),
+                                C.c_void_p(x_in), C.c_void_p(x_out), C.c_void_p(ws), ws_bytes, C.c_void_p(stream)))
+
+
+class ModelHandle:
+    """Keeps the ctypes arrays of nf_model_weights alive."""
+
+    def __init__(self, embed: int, layers: Sequence[dict], lm_head_packed: int):
+        self.layers = (PackedLayer * len(layers))(*[PackedLayer(*[d.get(n) for n, _ in PackedLayer._fields_])
+                                                    for d in layers])
+        self.c = ModelWeights(embed, C.cast(self.layers, C.POINTER(PackedLayer)), lm_head_packed)
+
+
+def model_step(plan: Plan, model: ModelHandle, kv_pools: Sequence[int], b: Batch, token_ids: int, next_ids: int,
+               ws: int, ws_bytes: int, stream: int, comm: Optional[int] = None):
+    pools = (C.c_void_p * len(kv_pools))(*kv_pools)
+    _check(lib.nf_model_step(plan.h, C.c_void_p(comm), C.byref(model.c), pools, C.byref(b.c), C.c_void_p(token_ids),
+                             C.c_void_p(next_ids), C.c_void_p(ws), ws_bytes, C.c_void_p(stream)))
+
+
+def gemm_bf16(A: int, lda: int, B: int, ldb: int, Cp: int, ldc: int, M: int, N: int, K: int, sm_budget: int,
+              stream: int):
+    _check(lib.nf_gemm_bf16(C.c_void_p(A), lda, C.c_void_p(B), ldb, C.c_void_p(Cp), ldc, M, N, K, sm_budget,
+                            C.c_void_p(stream)))
+
+
+def attention(cfg: ModelCfg, b: Batch, q: int, kv_pool: int, o: int, ws: int, ws_bytes: int, sm_decode: int,
+              sm_prefill: int, stream: int):
+    _check(lib.nf_attention(C.byref(cfg), C.byref(b.c), C.c_void_p(q), C.c_void_p(kv_pool), C.c_void_p(o),
+                            C.c_void_p(ws), ws_bytes, sm_decode, sm_prefill, C.c_void_p(stream)))
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib.nf_comm_unique_id(buf))
+    return buf.raw
+
+
+def comm_create(tp_size: int, tp_rank: int, uid: bytes) -> int:
+    h = C.c_void_p()
+    buf = C.create_string_buffer(uid, 128)
+    _check(lib.nf_comm_create(tp_size, tp_rank, buf, C.byref(h)))
+    return h.value

@@ -1,0 +1,89 @@
+"""PyTorch plumbing around the C ABI: device memory (weights, packed weights,
+KV pools, workspace) and streams.  No compute happens here: every step of the
+path runs inside libnf.so (see nf.py)."""
+from __future__ import annotations
+
+from typing import Dict, List, Optional, Sequence
+
+import torch
+
+from . import nf
+
+BF16 = torch.bfloat16
+
+
+def cfg_from_shape(shape, tp_size: int = 1, tp_rank: int = 0, n_layers: Optional[int] = None) -> nf.ModelCfg:
+    """nf_model_cfg from any object with the synth.ModelShape attributes."""
+    return nf.model_cfg(shape.d_model, shape.n_layers if n_layers is None else n_layers, shape.n_q_heads,
+                        shape.n_kv_heads, shape.head_dim, shape.d_ffn, shape.vocab, shape.rms_eps,
+                        shape.rope_theta, shape.page_size, tp_size, tp_rank)
+
+
+def stream_handle(stream: Optional[torch.cuda.Stream] = None) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+def alloc_packed_layer(cfg: nf.ModelCfg, device="cuda") -> Dict[str, torch.Tensor]:
+    sizes = nf.packed_layer_bytes(cfg)
+    names = ["w_qkv", "w_o", "w_o_row", "w_gate_up", "w_down"]
+    return {n: torch.empty(max(s, 2) // 2, dtype=BF16, device=device) for n, s in zip(names, sizes) if s > 0}
+
+
+def ptrs(d: Dict[str, torch.Tensor]) -> Dict[str, int]:
+    return {k: v.data_ptr() for k, v in d.items()}
+
+
+def pack_layer(cfg: nf.ModelCfg, w: Dict[str, torch.Tensor], stream: Optional[int] = None) -> Dict[str, torch.Tensor]:
+    """w: canonical device bf16 weights (nf_layer_weights names)."""
+    packed = alloc_packed_layer(cfg, next(iter(w.values())).device)
+    nf.pack_layer(cfg, ptrs(w), ptrs(packed), stream_handle() if stream is None else stream)
+    return packed
+
+
+def pack_lm_head(cfg: nf.ModelCfg, lm_head: torch.Tensor, final_norm: torch.Tensor) -> torch.Tensor:
+    out = torch.empty_like(lm_head)
+    nf.pack_lm_head(cfg, lm_head.data_ptr(), final_norm.data_ptr(), out.data_ptr(), stream_handle())
+    return out
+
+
+def kv_pool(cfg: nf.ModelCfg, n_pages: int, device="cuda") -> torch.Tensor:
+    kh = cfg.n_kv_heads // cfg.tp_size
+    return torch.empty((n_pages, 2, kh, cfg.page_size, cfg.head_dim), dtype=BF16, device=device)
+
+
+def workspace(cfg: nf.ModelCfg, b: nf.Batch, device="cuda") -> torch.Tensor:
+    n = nf.workspace_size(cfg, b)
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def layer_forward(plan: nf.Plan, cfg: nf.ModelCfg, packed: Dict[str, torch.Tensor], pool: torch.Tensor, b: nf.Batch,
+                  x_in: torch.Tensor, ws: Optional[torch.Tensor] = None, x_out: Optional[torch.Tensor] = None,
+                  comm: Optional[int] = None) -> torch.Tensor:
+    if ws is None:
+        ws = workspace(cfg, b, x_in.device)
+    if x_out is None:
+        x_out = torch.empty_like(x_in)
+    nf.layer_forward(plan, ptrs(packed), pool.data_ptr(), b, x_in.data_ptr(), x_out.data_ptr(), ws.data_ptr(),
+                     ws.numel(), stream_handle(), comm)
+    return x_out
+
+
+class Model:
+    """Packed model weights on the device plus the nf_model_weights view."""
+
+    def __init__(self, cfg: nf.ModelCfg, embed: torch.Tensor, packed_layers: Sequence[Dict[str, torch.Tensor]],
+                 lm_head_packed: torch.Tensor):
+        self.cfg = cfg
+        self.embed = embed
+        self.layers = list(packed_layers)
+        self.lm_head_packed = lm_head_packed
+        self.handle = nf.ModelHandle(embed.data_ptr(), [ptrs(d) for d in self.layers], lm_head_packed.data_ptr())
+
+    def step(self, plan: nf.Plan, pools: Sequence[torch.Tensor], b: nf.Batch, token_ids: torch.Tensor,
+             ws: torch.Tensor, next_ids: Optional[torch.Tensor] = None, comm: Optional[int] = None) -> torch.Tensor:
+        if next_ids is None:
+            next_ids = torch.empty(len(b.q_len), dtype=torch.int32, device=token_ids.device)
+        nf.model_step(plan, self.handle, [p.data_ptr() for p in pools], b, token_ids.data_ptr(), next_ids.data_ptr(),
+                      ws.data_ptr(), ws.numel(), stream_handle(), comm)
+        return next_ids

@@ -224,10 +224,36 @@ def kv_pool(shape: ModelShape, batch: Batch, seed: int = 2, layer: int = 0,
     hk = shape.n_kv_heads if n_kv_heads is None else n_kv_heads
     P, hd = shape.page_size, shape.head_dim
     pool = np.full((batch.n_pages_pool, 2, hk, P, hd), fill, dtype=np.float32)
-    pages, offs = cached_slots(batch, P)
-    if pages.size:
-        vals = randn_bf16((pages.size, 2, hk, hd), seed, f"kv{layer}")
-        pool[pages, :, :, offs, :] = vals
+    for r in range(batch.n_req):
+        n = int(batch.kv_prefix[r])
+        if n:
+            j = np.arange(n)
+            pages = batch.page_ids[batch.page_indptr[r] + j // P]
+            pool[pages, :, :, j % P, :] = request_kv(shape, r, n, seed, layer, hk)
+    return pool
+
+
+def request_kv(shape: ModelShape, r: int, n: int, seed: int = 2, layer: int = 0,
+               n_kv_heads: Optional[int] = None) -> np.ndarray:
+    """Cached K/V of request r's first n positions: [n, 2, kv_heads, head_dim]
+    (its own RNG stream, so a subset of requests can be regenerated alone)."""
+    hk = shape.n_kv_heads if n_kv_heads is None else n_kv_heads
+    return randn_bf16((n, 2, hk, shape.head_dim), seed, f"kv{layer}.r{r}")
+
+
+def kv_pool_bits(shape: ModelShape, batch: Batch, seed: int = 2, layer: int = 0, fill_bits: int = 0,
+                 n_kv_heads: Optional[int] = None) -> np.ndarray:
+    """Same values as kv_pool, as a bf16 bit-pattern array (uint16) — half the
+    host memory, for full-size pools uploaded to the GPU."""
+    hk = shape.n_kv_heads if n_kv_heads is None else n_kv_heads
+    P, hd = shape.page_size, shape.head_dim
+    pool = np.full((batch.n_pages_pool, 2, hk, P, hd), fill_bits, dtype=np.uint16)
+    for r in range(batch.n_req):
+        n = int(batch.kv_prefix[r])
+        if n:
+            j = np.arange(n)
+            pages = batch.page_ids[batch.page_indptr[r] + j // P]
+            pool[pages, :, :, j % P, :] = f32_to_bf16_bits(request_kv(shape, r, n, seed, layer, hk))
     return pool
 
 

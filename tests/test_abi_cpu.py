@@ -1,0 +1,112 @@
+"""C-ABI library: loads without a GPU, exports every symbol include/nf.h
+declares, host-only metadata is bit-exact with the oracle, validation errors.
+CPU only (no compute calls)."""
+import os
+import re
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import metadata as md
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def nf():
+    from paper_2408_12757_b200 import build
+    build.build()
+    from paper_2408_12757_b200 import nf as _nf
+    return _nf
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "nf.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(nf_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(nf):
+    names = header_functions()
+    assert len(names) >= 18
+    for n in names:
+        assert hasattr(nf.lib, n), f"{n} declared in nf.h but not exported"
+    assert set(names) == set(nf.EXPORTED)
+    assert nf.lib.nf_abi_version() == 1
+
+
+def _cfg(nf, shape, **kw):
+    from paper_2408_12757_b200.runtime import cfg_from_shape
+    return cfg_from_shape(shape, **kw)
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "random"])
+def test_metadata_bit_exact_vs_oracle(nf, case):
+    if case == "c1":
+        b, shape = synth.c1_batch(), synth.SHAPES["c1"]
+    elif case == "c2":
+        b, shape = synth.workload_batch(2048, 1024, 512), synth.SHAPES["llama3-8b"]
+    else:
+        rng = np.random.default_rng(0)
+        n = 37
+        b = synth.make_batch(rng.integers(1, 40, n), rng.integers(0, 200, n), seed=9, pool_slack=11)
+        shape = synth.SHAPES["c1"]
+    cfg = _cfg(nf, shape)
+    nb = nf.Batch.from_any(b)
+    pos, slot = nf.batch_metadata(cfg, nb)
+    opos = md.positions(b.q_len, b.kv_prefix)
+    pages, offs = md.write_slots(b.q_len, b.kv_prefix, b.page_indptr, b.page_ids)
+    assert np.array_equal(pos, opos)
+    assert np.array_equal(slot, pages * 16 + offs)
+
+
+def test_snap_cuts_bit_exact_vs_oracle(nf):
+    rng = np.random.default_rng(1)
+    for trial in range(30):
+        n = int(rng.integers(1, 30))
+        q = rng.integers(1, 50, n)
+        b = synth.make_batch(q, np.zeros(n, int), seed=trial)
+        k = int(rng.integers(1, 5))
+        shares = rng.integers(1, 9, k)
+        got = nf.snap_cuts(nf.Batch.from_any(b), shares)
+        exp = md.snap_cuts(q, [Fraction(int(s), int(shares.sum())) for s in shares])
+        assert list(got) == exp
+
+
+def test_validation_errors(nf):
+    cfg = _cfg(nf, synth.SHAPES["c1"])
+    b = synth.make_batch([1, 3], [5, 0])
+    bad = nf.Batch(b.q_len, b.kv_prefix, b.page_indptr, b.page_ids, n_pages_pool=1)  # page id out of pool
+    with pytest.raises(nf.NFError) as e:
+        nf.batch_metadata(cfg, bad)
+    assert e.value.status == nf.NF_EINVAL and "outside pool" in str(e.value)
+    few = nf.Batch([1, 3], [40, 0], b.page_indptr, b.page_ids, b.n_pages_pool)  # too few pages
+    with pytest.raises(nf.NFError):
+        nf.batch_metadata(cfg, few)
+    neg = nf.Batch([0, 3], [5, 0], b.page_indptr, b.page_ids, b.n_pages_pool)
+    with pytest.raises(nf.NFError):
+        nf.workspace_size(cfg, neg)
+    bad_cfg = _cfg(nf, synth.shape_with(synth.SHAPES["c1"], head_dim=96))
+    with pytest.raises(nf.NFError) as e:
+        nf.workspace_size(bad_cfg, nf.Batch.from_any(b))
+    assert e.value.status == nf.NF_EUNSUPPORTED
+    with pytest.raises(nf.NFError):
+        _ = nf.workspace_size(_cfg(nf, synth.SHAPES["c1"], tp_size=4), nf.Batch.from_any(b))  # 4 does not divide kh=2
+    with pytest.raises(nf.NFError):
+        nf.Plan.explicit(cfg, mode=7)
+    with pytest.raises(nf.NFError):
+        nf.Plan.explicit(cfg, mode=nf.OVERLAP, shares=(1, 0))
+    p = nf.Plan.explicit(cfg, mode=nf.SEQUENTIAL, shares=(1, 1))
+    assert p.spec().n_nano == 1
+    p2 = nf.Plan.explicit(cfg, mode=nf.OVERLAP, shares=(1, 1), balance=True)
+    s = p2.spec()
+    assert s.n_nano == 2 and s.balance == 1 and list(s.share)[:2] == [1, 1]
+
+
+def test_workspace_size_monotone(nf):
+    cfg = _cfg(nf, synth.SHAPES["llama3-8b"])
+    small = nf.workspace_size(cfg, nf.Batch.from_any(synth.c1_batch()))
+    big = nf.workspace_size(cfg, nf.Batch.from_any(synth.workload_batch(2048, 1024, 512)))
+    assert 0 < small < big

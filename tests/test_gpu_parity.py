@@ -1,0 +1,286 @@
+"""GPU parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Every test is @pytest.mark.gpu and runs on a B200.  Inputs are seeded and
+synthetic (synth), the oracle runs on the same bf16 values in float64.
+Tolerances: integer/index work bit-exact; floating point per BASELINE.json
+north_star (rel L2 <= 1e-2, max abs <= 5e-2) unless stated."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import layer as OL
+from oracle import metadata as md
+
+from gpu_common import (assert_close, compact_case, dev, dev_bits, device_weights, errors, host, require_gpu,
+                        token_rows)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    return require_gpu()
+
+
+# ------------------------------------------------------------------ GEMM
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (1, 32, 64), (200, 768, 512), (77, 2816, 1376),
+                                   (1000, 6144, 4096), (2048, 4096, 14336), (513, 32000, 512)])
+def test_gemm_vs_oracle(env, M, N, K):
+    nf, rt = env
+    rng = np.random.default_rng(M * 7 + N + K)
+    A = synth.round_bf16(rng.standard_normal((M, K), dtype=np.float32))
+    B = synth.round_bf16(rng.standard_normal((N, K), dtype=np.float32) / np.float32(np.sqrt(K)))
+    Ad, Bd = dev(A), dev(B)
+    C = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    nf.gemm_bf16(Ad.data_ptr(), K, Bd.data_ptr(), K, C.data_ptr(), N, M, N, K, 148, rt.stream_handle())
+    torch.cuda.synchronize()
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    # bf16 output rounding (2^-9 relative) + fp32 accumulation
+    rel, mx = errors(host(C), ref)
+    assert rel < 4e-3 and mx < 2e-2 * max(1.0, np.abs(ref).max()), (rel, mx)
+
+
+@pytest.mark.parametrize("sm", [1, 7, 64, 148])
+def test_gemm_sm_budget_bit_identical(env, sm):
+    """The SM budget only changes which CTA computes a tile, never the math."""
+    nf, rt = env
+    rng = np.random.default_rng(3)
+    M, N, K = 600, 1024, 1024
+    A, B = dev(synth.round_bf16(rng.standard_normal((M, K), dtype=np.float32))), \
+        dev(synth.round_bf16(rng.standard_normal((N, K), dtype=np.float32) * 0.03))
+    outs = []
+    for budget in (148, sm):
+        C = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+        nf.gemm_bf16(A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N, M, N, K, budget, rt.stream_handle())
+        outs.append(C)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+
+
+# ------------------------------------------------------------------ attention
+def _attn_case(shape, q_len, prefix, seed=0, fill=0.0):
+    b = synth.make_batch(q_len, prefix, seed=3 + seed, pool_slack=5)
+    pool = synth.kv_pool(shape, b, seed=2 + seed, fill=fill)
+    T = b.n_tokens
+    q = synth.randn_bf16((T, shape.n_q_heads, shape.head_dim), 7 + seed, "q")
+    k = synth.randn_bf16((T, shape.n_kv_heads, shape.head_dim), 7 + seed, "k")
+    v = synth.randn_bf16((T, shape.n_kv_heads, shape.head_dim), 7 + seed, "v")
+    opool = OL.as_pool(pool)
+    OL.kv_append(opool, k, v, b)
+    return b, opool, q
+
+
+def _run_attn(env, shape, b, pool64, q, sm_dec=148, sm_pf=148):
+    nf, rt = env
+    cfg = rt.cfg_from_shape(shape)
+    nb = nf.Batch.from_any(b)
+    pool_d = dev(pool64)
+    q_d = dev(q)
+    o = torch.full((b.n_tokens, shape.n_q_heads * shape.head_dim), float("nan"), dtype=torch.bfloat16, device="cuda")
+    ws = rt.workspace(cfg, nb)
+    nf.attention(cfg, nb, q_d.data_ptr(), pool_d.data_ptr(), o.data_ptr(), ws.data_ptr(), ws.numel(), sm_dec, sm_pf,
+                 rt.stream_handle())
+    torch.cuda.synchronize()
+    return host(o).reshape(b.n_tokens, shape.n_q_heads, shape.head_dim)
+
+
+@pytest.mark.parametrize("shape_name", ["c1", "llama3-8b"])
+def test_attention_vs_oracle(env, shape_name):
+    shape = synth.SHAPES[shape_name]
+    rng = np.random.default_rng(11)
+    n_dec = 40
+    q_len = [1] * n_dec + [150, 200, 64, 65, 2]
+    prefix = list(rng.integers(0, 1500, n_dec)) + [300, 0, 17, 0, 1000]
+    b, pool, q = _attn_case(shape, q_len, prefix)
+    out = _run_attn(env, shape, b, pool, q)
+    ref = OL.paged_attention(q, pool, b)
+    assert_close(out, ref, what="attention")
+
+
+def test_attention_c1_config(env):
+    shape = synth.SHAPES["c1"]
+    b = synth.c1_batch()
+    pool = OL.as_pool(synth.kv_pool(shape, b))
+    T = b.n_tokens
+    q = synth.randn_bf16((T, shape.n_q_heads, shape.head_dim), 7, "q")
+    k = synth.randn_bf16((T, shape.n_kv_heads, shape.head_dim), 7, "k")
+    v = synth.randn_bf16((T, shape.n_kv_heads, shape.head_dim), 7, "v")
+    OL.kv_append(pool, k, v, b)
+    for sm in (148, 5, 1):
+        out = _run_attn(env, shape, b, pool, q, sm, sm)
+        assert_close(out, OL.paged_attention(q, pool, b), what=f"attention C1 sm={sm}")
+
+
+def test_attention_single_key_bit_exact(env):
+    """T1: a request with one key returns V exactly (p = 1)."""
+    shape = synth.SHAPES["llama3-8b"]
+    b, pool, q = _attn_case(shape, [1, 1, 1], [0, 0, 0])
+    out = _run_attn(env, shape, b, pool, q)
+    ref = OL.paged_attention(q, pool, b)
+    assert np.array_equal(out, ref)
+
+
+def test_attention_page_permutation_bit_exact(env):
+    """T4: relabelling physical pages leaves the output bit-identical."""
+    shape = synth.SHAPES["llama3-8b"]
+    q_len, prefix = [1] * 9 + [70], [5, 16, 17, 100, 255, 256, 1023, 1024, 1500, 33]
+    outs = []
+    for seed_pages in (3, 4):
+        b = synth.make_batch(q_len, prefix, seed=seed_pages, pool_slack=7)
+        pool = OL.as_pool(synth.kv_pool(shape, b, seed=2))
+        T = b.n_tokens
+        q = synth.randn_bf16((T, shape.n_q_heads, shape.head_dim), 7, "q")
+        k = synth.randn_bf16((T, shape.n_kv_heads, shape.head_dim), 7, "k")
+        v = synth.randn_bf16((T, shape.n_kv_heads, shape.head_dim), 7, "v")
+        OL.kv_append(pool, k, v, b)
+        outs.append(_run_attn(env, shape, b, pool, q))
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_attention_nan_outside_context_is_ignored(env):
+    """Slots past kv_len hold NaN: masked keys and zeroed V rows must not leak."""
+    shape = synth.SHAPES["llama3-8b"]
+    b, pool, q = _attn_case(shape, [1, 1, 37, 1], [3, 40, 5, 16], fill=np.nan)
+    out = _run_attn(env, shape, b, pool, q)
+    assert np.isfinite(out).all()
+    assert_close(out, OL.paged_attention(q, np.nan_to_num(pool), b), what="attention NaN sentinel")
+
+
+# ------------------------------------------------------------------ decoder layer
+def _layer_case(shape, b, seed=0, fill=0.0):
+    w = synth.layer_weights(shape, 0, seed=seed)
+    x = synth.activations(shape, b.n_tokens, seed=1 + seed)
+    pool = synth.kv_pool(shape, b, seed=2 + seed, fill=fill)
+    return w, x, pool
+
+
+def _gpu_layer(env, shape, b, w, x, pool, mode, shares=(1,), sm=None, balance=False):
+    nf, rt = env
+    cfg = rt.cfg_from_shape(shape)
+    nb = nf.Batch.from_any(b)
+    wd = device_weights(w)
+    packed = rt.pack_layer(cfg, wd)
+    pool_d = dev(pool)
+    plan = nf.Plan.explicit(cfg, mode=mode, shares=shares, sm=sm, balance=balance)
+    out = rt.layer_forward(plan, cfg, packed, pool_d, nb, dev(x))
+    torch.cuda.synchronize()
+    return host(out), pool_d
+
+
+@pytest.mark.parametrize("mode,shares", [(0, (1,)), (1, (1, 1)), (2, (1, 1)), (2, (1, 2, 1)), (1, (3, 1, 1, 2))])
+def test_layer_c1_vs_oracle(env, mode, shares):
+    shape = synth.SHAPES["c1"]
+    b = synth.c1_batch()
+    w, x, pool = _layer_case(shape, b)
+    ref = OL.decoder_layer(x, w, OL.as_pool(pool), b, shape)
+    out, _ = _gpu_layer(env, shape, b, w, x, pool, mode, shares)
+    assert_close(out, ref, what=f"C1 layer mode={mode} shares={shares}")
+
+
+def test_layer_kv_write_map_bit_exact(env):
+    """T13: only this step's slots change (set identical to the oracle's);
+    written K/V match the oracle's post-RoPE K and V within tolerance."""
+    shape = synth.SHAPES["c1"]
+    b = synth.make_batch([1, 5, 1, 17, 1, 40], [15, 0, 16, 31, 0, 100], seed=5, pool_slack=9)
+    w, x, pool = _layer_case(shape, b, fill=np.nan)
+    opool = OL.as_pool(pool)
+    OL.decoder_layer(x, w, opool, b, shape)
+    _, pool_d = _gpu_layer(env, shape, b, w, x, pool, 2, (1, 1))
+    g = host(pool_d)
+    changed = ~(np.isnan(g) & np.isnan(pool)) & ~(g == pool)
+    exp = ~(np.isnan(opool) & np.isnan(pool)) & ~(opool == pool)
+    assert np.array_equal(changed, exp)
+    assert_close(g[exp], opool[exp], what="written K/V")
+
+
+def test_layer_split_invariance_and_modes_agree(env):
+    """T11: 1, 2, 3 nano-batches and the three pipeline modes give the same
+    layer output (within the bf16 tolerance; bit-identical for the same
+    row partition since every kernel's math is per-row)."""
+    shape = synth.SHAPES["c1"]
+    b = synth.make_batch([1] * 30 + [33, 1, 1, 20], list(range(3, 93, 3)) + [0, 7, 300, 50], seed=4, pool_slack=3)
+    w, x, pool = _layer_case(shape, b, seed=3)
+    ref = OL.decoder_layer(x, w, OL.as_pool(pool), b, shape)
+    outs = {}
+    for mode, shares in [(0, (1,)), (1, (1, 1)), (2, (1, 1)), (2, (2, 1, 1))]:
+        out, _ = _gpu_layer(env, shape, b, w, x, pool, mode, shares)
+        assert_close(out, ref, what=f"mode={mode} shares={shares}")
+        outs[(mode, shares)] = out
+    assert np.array_equal(outs[(1, (1, 1))], outs[(2, (1, 1))])
+
+
+def test_layer_8b_shape_small_batch(env):
+    shape = synth.SHAPES["llama3-8b"]
+    b = synth.make_batch([1] * 12 + [100, 1, 37], [1024, 5, 1535, 16, 1, 900, 64, 700, 33, 1200, 1300, 100, 341, 2, 0],
+                         seed=3, pool_slack=2)
+    w, x, pool = _layer_case(shape, b)
+    ref = OL.decoder_layer(x, w, OL.as_pool(pool), b, shape)
+    out, _ = _gpu_layer(env, shape, b, w, x, pool, 2, (1, 1))
+    assert_close(out, ref, what="8B-shape layer")
+
+
+def test_layer_8b_full_batch_sampled(env):
+    """configs[1] at full size: one LLaMA-3-8B-shape layer over the B_dense=2048
+    steady-state batch (683 decode + chunk 341 + prompt 1024), in the bench's
+    OVERLAP launch configuration; sampled requests checked against the oracle
+    (decode requests and both prefill requests in full)."""
+    nf, rt = env
+    shape = synth.SHAPES["llama3-8b"]
+    b = synth.workload_batch(2048, 1024, 512)
+    w = synth.layer_weights(shape, 0, seed=0)
+    x = synth.activations(shape, b.n_tokens, seed=1)
+    cfg = rt.cfg_from_shape(shape)
+    nb = nf.Batch.from_any(b)
+    packed = rt.pack_layer(cfg, device_weights(w))
+    pool_d = dev_bits(synth.kv_pool_bits(shape, b, seed=2))
+    plan = nf.Plan.explicit(cfg, mode=nf.OVERLAP, shares=(1, 1))
+    out = host(rt.layer_forward(plan, cfg, packed, pool_d, nb, dev(x)))
+    torch.cuda.synchronize()
+    reqs = [0, 1, 2, 100, 341, 500, 682, 683, 684]
+    sub, pool = compact_case(shape, b, reqs)
+    rows = token_rows(b, reqs)
+    ref = OL.decoder_layer(x[rows], w, pool, sub, shape)
+    assert_close(out[rows], ref, what="8B full batch sampled")
+    assert np.isfinite(out).all()
+
+
+# ------------------------------------------------------------------ model step
+def test_model_step_vs_oracle(env):
+    nf, rt = env
+    shape = synth.shape_with(synth.SHAPES["c1"], n_layers=2, vocab=4096)
+    b = synth.make_batch([1] * 20 + [30, 1, 12], list(range(10, 210, 10)) + [0, 33, 7], seed=6, pool_slack=4)
+    W = synth.model_weights(shape, seed=0)
+    toks = synth.token_ids(b.n_tokens, shape.vocab)
+    pools = [synth.kv_pool(shape, b, seed=2, layer=l) for l in range(2)]
+    ids_ref, logits, _ = OL.model_step(toks, W, [OL.as_pool(p) for p in pools], b, shape, return_logits=True)
+    cfg = rt.cfg_from_shape(shape)
+    layers = [rt.pack_layer(cfg, device_weights(W["layers"][l])) for l in range(2)]
+    model = rt.Model(cfg, dev(W["embed"]), layers, rt.pack_lm_head(cfg, dev(W["lm_head"]), dev(W["final_norm"])))
+    nb = nf.Batch.from_any(b)
+    ws = rt.workspace(cfg, nb)
+    tok_d = torch.from_numpy(toks).cuda()
+    for mode, shares, bal in [(0, (1,), False), (2, (1, 1), False), (2, (1, 1), True), (1, (1, 2), True)]:
+        pools_d = [dev(p) for p in pools]
+        plan = nf.Plan.explicit(cfg, mode=mode, shares=shares, balance=bal)
+        ids = model.step(plan, pools_d, nb, tok_d, ws).cpu().numpy()
+        srt = np.sort(logits, axis=1)
+        gap = srt[:, -1] - srt[:, -2]
+        sure = gap > 0.1
+        assert sure.sum() >= len(gap) // 2
+        assert np.array_equal(ids[sure], ids_ref[sure]), (mode, shares, bal)
+
+
+def test_model_step_emit_mask(env):
+    nf, rt = env
+    shape = synth.shape_with(synth.SHAPES["c1"], n_layers=1, vocab=2048)
+    b = synth.make_batch([1, 4, 1], [9, 0, 3], seed=1)
+    W = synth.model_weights(shape, seed=0)
+    cfg = rt.cfg_from_shape(shape)
+    model = rt.Model(cfg, dev(W["embed"]), [rt.pack_layer(cfg, device_weights(W["layers"][0]))],
+                     rt.pack_lm_head(cfg, dev(W["lm_head"]), dev(W["final_norm"])))
+    nb = nf.Batch.from_any(b, emit=[1, 0, 1])
+    ws = rt.workspace(cfg, nb)
+    ids = model.step(nf.Plan.explicit(cfg), [dev(synth.kv_pool(shape, b))], nb,
+                     torch.from_numpy(synth.token_ids(b.n_tokens, shape.vocab)).cuda(), ws).cpu().numpy()
+    assert ids[1] == -1 and ids[0] >= 0 and ids[2] >= 0
