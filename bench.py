@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the NanoFlow hot path on B200 (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], the largest config that fits one GPU; the
+metric's configs[2] 70B-TP8 does not): a LLaMA-3-8B-shape model (32 layers,
+D 4096, 32/8 heads, hd 128, F 14336, V 128256), random-init bf16 weights,
+serving step over the B_dense = 2048 steady state of the constant 1024-in /
+512-out workload: 683 decode requests (contexts 1024..1535) +
+a 341-token chunk (prefix 683) + one 1024-token prompt, paged KV (page 16).
+A "step" = one nf_model_step: embedding -> 32 decoder layers (KQV+RoPE+KV
+append, paged decode/prefill attention, O, RMSNorm, SwiGLU, Down) -> final
+norm -> LM head -> argmax, through the C ABI.  Inputs are resident in HBM
+(KV 115 GB + weights 15 GB per step, far above the 126 MB L2: no flush needed).
+
+--gpus N > 1 (torchrun): N independent replicas (data parallel, no exchange:
+the 8B shape fits one GPU), weak scaling; value = all ranks' tokens / max time.
+--impl reference: the CPU oracle (oracle/, float64 numpy) as the reference
+arm, timed on the host cores on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/s/GPU and % of compute-bound optimal, LLaMA-2-70B-shape TP8"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def p_active(shape):
+    """Matmul weights touched per token: L*(D*(Hq+2Hkv)*hd + Hq*hd*D + 3*D*F) + V*D."""
+    s = shape
+    return s.n_layers * (s.d_model * (s.n_q_heads + 2 * s.n_kv_heads) * s.head_dim +
+                         s.n_q_heads * s.head_dim * s.d_model + 3 * s.d_model * s.d_ffn) + s.vocab * s.d_model
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- oracle sample
+def oracle_sample(shape, n_dec=64, chunk=64):
+    """Bounded sample of the same workload for the CPU oracle: n_dec decode
+    requests drawn from the steady state (contexts 1024..1535) plus one prefill
+    chunk of `chunk` tokens (prefix 0), one decoder layer."""
+    import numpy as np
+    import synth
+    full = synth.workload_batch(2048, 1024, 512)
+    q_len = [1] * n_dec + [chunk]
+    prefix = list(full.kv_prefix[:n_dec]) + [0]
+    b = synth.make_batch(q_len, prefix, seed=3)
+    w = synth.layer_weights(shape, 0, seed=0)
+    x = synth.activations(shape, b.n_tokens, seed=1)
+    pool = synth.kv_pool(shape, b, seed=2)
+    return b, w, x, pool
+
+
+def time_oracle_layer(shape, b, w, x, pool, reps=1):
+    import numpy as np
+    from oracle import layer as OL
+    ts = []
+    for _ in range(reps):
+        p = OL.as_pool(pool)
+        t0 = time.perf_counter()
+        OL.decoder_layer(x, w, p, b, shape)
+        ts.append(time.perf_counter() - t0)
+    return ts
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads", 0) for i in threadpool_info()), default=None)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import synth
+    shape = synth.SHAPES["llama3-8b"]
+    b, w, x, pool = oracle_sample(shape)
+    T = b.n_tokens
+    for _ in range(args.warmup):
+        time_oracle_layer(shape, b, w, x, pool)
+    ts = []
+    for _ in range(args.steps):
+        ts += time_oracle_layer(shape, b, w, x, pool)
+    t_step = statistics.median(ts) * shape.n_layers  # x L-extrapolated step time for the sample
+    value = T / t_step
+    sample = (f"one float64 oracle decoder layer (numpy/BLAS) of the LLaMA-3-8B shape over {T} tokens "
+              f"(64 decode requests with the steady-state contexts + one 64-token prefill chunk), "
+              f"x{shape.n_layers} layers extrapolated")
+    cores = blas_threads() or cpu_cores()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[1] LLaMA-3-8B-shape serving step (oracle sample)", "sample_tokens": T},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- nf arm
+def run_nf(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2408_12757_b200 import nf, runtime as rt
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    shape = synth.SHAPES["llama3-8b"]
+    if args.layers:
+        shape = synth.shape_with(shape, n_layers=args.layers)
+    L = shape.n_layers
+    b = synth.workload_batch(2048, 1024, 512)
+    T = b.n_tokens
+    nb = nf.Batch.from_any(b)
+    cfg = rt.cfg_from_shape(shape)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+
+    def randn(shape_, std=1.0, mean=0.0):
+        t = torch.empty(shape_, dtype=torch.bfloat16, device=dev)
+        t.normal_(mean, std, generator=g)
+        return t
+
+    D, F, hd, Hq, Hk = shape.d_model, shape.d_ffn, shape.head_dim, shape.n_q_heads, shape.n_kv_heads
+    layers = []
+    for l in range(L):
+        w = {"attn_norm": randn((D,), 0.1, 1.0), "w_q": randn((Hq * hd, D), D ** -0.5),
+             "w_k": randn((Hk * hd, D), D ** -0.5), "w_v": randn((Hk * hd, D), D ** -0.5),
+             "w_o": randn((D, Hq * hd), (Hq * hd) ** -0.5), "ffn_norm": randn((D,), 0.1, 1.0),
+             "w_gate": randn((F, D), D ** -0.5), "w_up": randn((F, D), D ** -0.5), "w_down": randn((D, F), F ** -0.5)}
+        layers.append(rt.pack_layer(cfg, w))
+        del w
+    embed = randn((shape.vocab, D))
+    lm = rt.pack_lm_head(cfg, randn((shape.vocab, D), D ** -0.5), randn((D,), 0.1, 1.0))
+    model = rt.Model(cfg, embed, layers, lm)
+    pools = [randn((b.n_pages_pool, 2, Hk, 16, hd)) for _ in range(L)]
+    tok = torch.randint(0, shape.vocab, (T,), dtype=torch.int32, device=dev, generator=g)
+    ws = rt.workspace(cfg, nb, dev)
+    next_ids = torch.empty(b.n_req, dtype=torch.int32, device=dev)
+    torch.cuda.synchronize()
+
+    sm = [int(x) for x in args.sm.split(",")] if args.sm else None
+    if args.mode == "overlap":
+        plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=sm or [96, 52, 52, 96, 96, 96, 16],
+                                balance=True)
+    elif args.mode == "nano":
+        plan = nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=(1, 1), sm=sm, balance=True)
+    else:
+        plan = nf.Plan.explicit(cfg, nf.SEQUENTIAL, sm=sm)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        model.step(plan, pools, nb, tok, ws, next_ids)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    nf.profile_enable(True)
+    nf.profile_read()
+    launches0 = nf.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    nf.profile_enable(False)
+    launches = (nf.kernel_launches() - launches0) / args.steps
+    prof = nf.profile_read()
+    ms = e0.elapsed_time(e1)
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms_max = float(t_max.item())
+    ms_step = ms_max / args.steps
+    value = world * T * args.steps / (ms_max / 1e3)
+
+    if args.ncu:
+        return
+    # ---------------- end to end through the public API with host buffers
+    tok_host = tok.cpu().pin_memory()
+    ids_host = torch.empty(b.n_req, dtype=torch.int32).pin_memory()
+    tok_dev2 = torch.empty_like(tok)
+    for _ in range(2):
+        tok_dev2.copy_(tok_host, non_blocking=True)
+        model.step(plan, pools, nb, tok_dev2, ws, next_ids)
+        ids_host.copy_(next_ids, non_blocking=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        tok_dev2.copy_(tok_host, non_blocking=True)
+        model.step(plan, pools, nb, tok_dev2, ws, next_ids)
+        ids_host.copy_(next_ids, non_blocking=True)
+        stream.synchronize()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = world * T * args.steps / (float(e2e_ms.item()) / 1e3)
+    n_dec = int((b.q_len == 1).sum())
+    pf_items = sum(((int(q) + 63) // 64) * Hq for q in b.q_len if q > 1)
+    meta_words = 3 * T + int(b.page_indptr[-1]) + 4 * n_dec * Hk + 8 * pf_items + 2 * b.n_req
+    h2d = T * 4 + meta_words * 4
+    d2h = b.n_req * 4
+
+    if rank != 0:
+        return
+
+    # ---------------- roofline of the dominant kernel (per-op CUDA-event time in the timed region)
+    peaks, peak_src = load_peaks()
+    kv_keys = sum(int(b.kv_prefix[r]) + 1 for r in range(b.n_req) if b.q_len[r] == 1)
+    dec_bytes_step = L * (kv_keys * Hk * hd * 2 * 2 + n_dec * Hq * hd * 2 * 2)  # K+V read + q read + o write
+    qkv_n = (Hq + 2 * Hk) * hd
+    flops = {"kqv": 2 * T * qkv_n * D * L, "o_proj": 2 * T * D * Hq * hd * L, "up_gate": 2 * T * 2 * F * D * L,
+             "down": 2 * T * D * F * L, "lm_head": 2 * b.n_req * shape.vocab * D}
+    per_op = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+              for k, v in prof.items() if v[1]}
+    dom = max(per_op, key=lambda k: per_op[k]["ms_per_step"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    if dom == "decode_attn":
+        achieved = dec_bytes_step / (per_op[dom]["ms_per_step"] / 1e3) / 1e9
+        roof = {"kernel": "decode_attn", "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "peak_source": peak_src,
+                "algorithmic": "K+V bytes of every decode request's context + q/o rows, per launch"}
+    else:
+        achieved = flops.get(dom, 0) / (per_op[dom]["ms_per_step"] / 1e3) / 1e12
+        pk = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
+                "frac": achieved / pk, "traffic": traffic, "peak_source": peak_src + " sustained",
+                "algorithmic": "2*M*N*K per launch"}
+    for k in per_op:
+        if k in flops:
+            per_op[k]["tflops"] = flops[k] / (per_op[k]["ms_per_step"] / 1e3) / 1e12
+    if "decode_attn" in per_op:
+        per_op["decode_attn"]["hbm_gbs"] = dec_bytes_step / (per_op["decode_attn"]["ms_per_step"] / 1e3) / 1e9
+
+    optimal = peaks["bf16_tflops"] * 1e12 / (2 * p_active(shape))
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, seeded torch RNG on device)",
+            "config": {"workload": f"configs[1]: LLaMA-3-8B-shape {L}-layer serving step, B_dense 2048 "
+                                   f"(683 decode ctx 1024-1535 + 341-token chunk + 1024-token prompt), page 16",
+                       "b_dense": T, "n_layers": L, "mode": args.mode,
+                       "parallelism": "replicas" if world > 1 else "single-gpu",
+                       "plan_sm": list(plan.spec().sm), "l2": "no flush: per-step inputs (KV 115 GB) >> 126 MB L2"},
+            "tokens_per_s_per_gpu": value / world,
+            "pct_of_optimal": 100.0 * (value / world) / optimal,
+            "optimal_tokens_per_s_per_gpu": optimal,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "roofline": roof,
+            "per_op": per_op,
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}}
+    if world == 1 and not args.no_cpu_baseline:
+        b_s, w_s, x_s, pool_s = oracle_sample(shape)
+        ts = time_oracle_layer(shape, b_s, w_s, x_s, pool_s, reps=3)
+        t_step = statistics.median(ts) * shape.n_layers
+        line["cpu_baseline"] = {"value": b_s.n_tokens / t_step, "unit": "tokens/s",
+                                "cores": blas_threads() or cpu_cores(), "kind": "oracle",
+                                "sample": f"float64 oracle, one 8B-shape layer over {b_s.n_tokens} tokens (64 decode "
+                                          f"+ 64-token chunk), median of 3, x{shape.n_layers} layers extrapolated"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="nf", choices=["nf", "reference"])
+    ap.add_argument("--mode", default="overlap", choices=["overlap", "nano", "sequential"])
+    ap.add_argument("--sm", default="", help="comma-separated SM budget per op kind (7 values)")
+    ap.add_argument("--layers", type=int, default=0, help="(dev only) override layer count")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="profiling run: timed steps only, no e2e / JSON")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_nf(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

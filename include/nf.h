@@ -206,6 +206,19 @@ nf_status nf_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, v
 nf_status nf_attention(const nf_model_cfg* cfg, const nf_batch* b, const void* q, const void* kv_pool, void* o,
                        void* ws, size_t ws_bytes, int32_t sm_decode, int32_t sm_prefill, void* stream);
 
+/* ------------------------------------------------------------------ instrumentation */
+/* Cumulative number of CUDA kernels this process launched through libnf. */
+int64_t nf_kernel_launches(void);
+/* Op kinds of the per-kernel timing (NF_OP_* plus the LM head and small kernels). */
+enum { NF_PROF_LMHEAD = NF_OP_COUNT, NF_PROF_MISC = NF_OP_COUNT + 1, NF_PROF_COUNT = NF_OP_COUNT + 2 };
+/* on != 0: record CUDA events on the launching stream around every kernel
+ * launch (adds ~1 us host time per launch). */
+nf_status nf_profile_enable(int32_t on);
+/* Synchronises the recorded events and returns, per op kind, the summed
+ * event-to-event milliseconds (ms_out[NF_PROF_COUNT]) and the number of
+ * launches (count_out[NF_PROF_COUNT]); clears the records. */
+nf_status nf_profile_read(double* ms_out, int64_t* count_out);
+
 #ifdef __cplusplus
 }
 #endif

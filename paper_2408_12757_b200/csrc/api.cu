@@ -12,6 +12,7 @@
 #include "gemm.cuh"
 #include "host.h"
 #include "misc.cuh"
+#include "profile.h"
 
 namespace nf {
 
@@ -535,6 +536,7 @@ nf_status run_kqv(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x
   a.tok_slot = L.meta_dev + L.m->off_slot + nr.t0;
   a.q_out = L.w->q + (int64_t)nr.t0 * a.qh * a.hd;
   a.kv_pool = (__nv_bfloat16*)pool;
+  ProfScope ps(NF_OP_KQV, L.cs);
   NF_CUDA(launch_gemm(x + (int64_t)nr.t0 * c->d_model, c->d_model, (const __nv_bfloat16*)wt->w_qkv, c->d_model, a,
                       clampsm(L.p->spec.sm[NF_OP_KQV]), L.cs));
   return NF_OK;
@@ -553,8 +555,14 @@ nf_status run_attn(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
   a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
   const DecodeItem* dec = reinterpret_cast<const DecodeItem*>(L.meta_dev + L.m->off_dec) + nr.dec_off;
   const PrefillItem* pf = reinterpret_cast<const PrefillItem*>(L.meta_dev + L.m->off_pf) + nr.pf_off;
-  NF_CUDA(launch_prefill_attention(L.pool_map, a, pf, nr.pf_n, clampsm(L.p->spec.sm[NF_OP_PREFILL_ATTN]), st));
-  NF_CUDA(launch_decode_attention(L.pool_map, a, dec, nr.dec_n, clampsm(L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
+  if (nr.pf_n > 0) {
+    ProfScope ps(NF_OP_PREFILL_ATTN, st);
+    NF_CUDA(launch_prefill_attention(L.pool_map, a, pf, nr.pf_n, clampsm(L.p->spec.sm[NF_OP_PREFILL_ATTN]), st));
+  }
+  if (nr.dec_n > 0) {
+    ProfScope ps(NF_OP_DECODE_ATTN, st);
+    NF_CUDA(launch_decode_attention(L.pool_map, a, dec, nr.dec_n, clampsm(L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
+  }
   return NF_OK;
 }
 
@@ -580,7 +588,10 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   a.ldr = D;
   a.sq_out = L.w->part_h1 + nr.t0;
   a.sq_stride = T;
-  NF_CUDA(launch_gemm(L.w->o + nr.t0 * qd, qd, (const __nv_bfloat16*)wt->w_o, qd, a, clampsm(L.p->spec.sm[NF_OP_O]), L.cs));
+  {
+    ProfScope ps(NF_OP_O, L.cs);
+    NF_CUDA(launch_gemm(L.w->o + nr.t0 * qd, qd, (const __nv_bfloat16*)wt->w_o, qd, a, clampsm(L.p->spec.sm[NF_OP_O]), L.cs));
+  }
   // Up/Gate + SiLU(gate) * up, RMSNorm(h1) folded as a row scale
   GemmArgs u{};
   u.epi = EPI_SILU;
@@ -595,8 +606,11 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   u.norm_stride = T;
   u.inv_d = 1.f / D;
   u.eps = c->rms_eps;
-  NF_CUDA(launch_gemm(L.w->h1 + nr.t0 * D, D, (const __nv_bfloat16*)wt->w_gate_up, D, u, clampsm(L.p->spec.sm[NF_OP_UG]),
-                      L.cs));
+  {
+    ProfScope ps(NF_OP_UG, L.cs);
+    NF_CUDA(launch_gemm(L.w->h1 + nr.t0 * D, D, (const __nv_bfloat16*)wt->w_gate_up, D, u, clampsm(L.p->spec.sm[NF_OP_UG]),
+                        L.cs));
+  }
   // Down + residual: x_out = h1 + m W_d^T, partials of x_out for the next layer's norm
   GemmArgs d{};
   d.epi = EPI_RESID;
@@ -610,8 +624,11 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   d.ldr = D;
   d.sq_out = part_out ? part_out + nr.t0 : nullptr;
   d.sq_stride = T;
-  NF_CUDA(launch_gemm(L.w->m + nr.t0 * F, F, (const __nv_bfloat16*)wt->w_down, F, d, clampsm(L.p->spec.sm[NF_OP_DOWN]),
-                      L.cs));
+  {
+    ProfScope ps(NF_OP_DOWN, L.cs);
+    NF_CUDA(launch_gemm(L.w->m + nr.t0 * F, F, (const __nv_bfloat16*)wt->w_down, F, d, clampsm(L.p->spec.sm[NF_OP_DOWN]),
+                        L.cs));
+  }
   return NF_OK;
 }
 
@@ -781,6 +798,7 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
     a.am_val = wsp.am_val;
     a.am_idx = wsp.am_idx;
     a.am_stride = m.n_emit;
+    ProfScope ps(NF_PROF_LMHEAD, cs);
     NF_CUDA(launch_gemm(wsp.lm_rows, D, (const __nv_bfloat16*)w->lm_head_packed, D, a, num_sms(), cs));
     NF_CUDA(launch_argmax_reduce(wsp.am_val, wsp.am_idx, (c->vocab + GEMM_BN - 1) / GEMM_BN, m.n_emit, m.n_emit,
                                  wsp.meta + m.off_emit_req, next_ids, cs));

@@ -15,6 +15,7 @@
 
 #include "attention.cuh"
 #include "common.cuh"
+#include "profile.h"
 
 namespace nf {
 
@@ -421,6 +422,7 @@ cudaError_t launch_decode_hd(const CUtensorMap& m, const AttnArgs& a, const Deco
   }
   int grid = std::min((n_items + DEC_WARPS - 1) / DEC_WARPS, std::max(sm_budget, 1));
   decode_attn_kernel<HD><<<grid, DEC_WARPS * 32, dec_smem<HD>(), st>>>(m, a, items, n_items);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -437,6 +439,7 @@ cudaError_t launch_prefill_hd(const CUtensorMap& m, const AttnArgs& a, const Pre
   const int per_sm = std::max(1, (227 * 1024) / pf_smem<HD>());
   int grid = std::min(n_items, std::max(sm_budget, 1) * per_sm);
   prefill_attn_kernel<HD><<<grid, PF_THREADS, pf_smem<HD>(), st>>>(m, a, items, n_items);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -14,6 +14,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "profile.h"
 #include "gemm.cuh"
 
 namespace nf {
@@ -360,6 +361,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   int grid = tiles < sm_budget ? tiles : sm_budget;
   if (grid < 1) grid = 1;
   gemm_tcgen05_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(ta, tb, args);
+  count_launch();
   return cudaGetLastError();
 }
 

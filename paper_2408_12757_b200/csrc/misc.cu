@@ -2,6 +2,7 @@
 // sum-of-squares partials, LM-head row gather, argmax reduction and the
 // one-time weight packing (RMSNorm gamma folding, gate/up interleave).
 #include "common.cuh"
+#include "profile.h"
 #include "misc.cuh"
 
 namespace nf {
@@ -100,6 +101,7 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* src, const int* idx, int row
                                float* part, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
   gather_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(src, idx, nullptr, rows, D, dst, part);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -107,6 +109,7 @@ cudaError_t launch_gather_ids_embed(const __nv_bfloat16* embed, const int* token
                                     __nv_bfloat16* dst, float* part, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
   gather_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(embed, token_ids, tok_src, rows, D, dst, part);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -114,6 +117,7 @@ cudaError_t launch_argmax_reduce(const float* val, const int* idx, int ntiles, i
                                  const int* row_req, int* next_ids, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
   argmax_reduce_kernel<<<(rows + 127) / 128, 128, 0, st>>>(val, idx, ntiles, stride, rows, row_req, next_ids);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -126,6 +130,7 @@ cudaError_t launch_fill_i32(int* p, int n, int v, cudaStream_t st) {
 cudaError_t launch_scale_cols(const __nv_bfloat16* src, const __nv_bfloat16* gamma, int64_t rows, int cols,
                               __nv_bfloat16* dst, cudaStream_t st) {
   scale_cols_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(src, gamma, rows, cols, dst);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -133,6 +138,7 @@ cudaError_t launch_pack_gate_up(const __nv_bfloat16* gate, const __nv_bfloat16* 
                                 int D, __nv_bfloat16* dst, cudaStream_t st) {
   const int nblk = (F + 127) / 128;
   pack_gate_up_kernel<<<grid_for((int64_t)nblk * 256 * D, 256), 256, 0, st>>>(gate, up, gamma, F, D, nblk, dst);
+  count_launch();
   return cudaGetLastError();
 }
 

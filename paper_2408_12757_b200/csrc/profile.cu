@@ -1,0 +1,84 @@
+// Launch counter and optional per-op CUDA-event timing of every kernel the
+// library launches (events recorded on the kernel's own stream).
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "host.h"
+#include "profile.h"
+
+namespace nf {
+namespace {
+std::atomic<long long> g_launches{0};
+std::atomic<int> g_prof_on{0};
+struct Rec {
+  int op;
+  cudaEvent_t a, b;
+};
+std::mutex g_mu;
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+
+cudaEvent_t get_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+void count_launch(int n) { g_launches += n; }
+
+ProfScope::ProfScope(int op, cudaStream_t st) : op_(op), st_(st) {
+  if (!g_prof_on.load()) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  a_ = get_event();
+  b_ = get_event();
+  cudaEventRecord(a_, st_);
+}
+ProfScope::~ProfScope() {
+  if (!a_) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaEventRecord(b_, st_);
+  g_recs.push_back(Rec{op_, a_, b_});
+}
+
+}  // namespace nf
+
+extern "C" {
+
+int64_t nf_kernel_launches(void) { return nf::g_launches.load(); }
+
+nf_status nf_profile_enable(int32_t on) {
+  nf::g_prof_on = on ? 1 : 0;
+  return NF_OK;
+}
+
+nf_status nf_profile_read(double* ms_out, int64_t* count_out) {
+  if (!ms_out || !count_out) return nf::set_error(NF_EINVAL, "NULL output");
+  for (int i = 0; i < NF_PROF_COUNT; ++i) {
+    ms_out[i] = 0;
+    count_out[i] = 0;
+  }
+  std::lock_guard<std::mutex> lk(nf::g_mu);
+  for (auto& r : nf::g_recs) {
+    float ms = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+    if (e != cudaSuccess) return nf::set_error(NF_ECUDA, "profile event: %s", cudaGetErrorString(e));
+    if (r.op >= 0 && r.op < NF_PROF_COUNT) {
+      ms_out[r.op] += ms;
+      count_out[r.op] += 1;
+    }
+    nf::g_pool.push_back(r.a);
+    nf::g_pool.push_back(r.b);
+  }
+  nf::g_recs.clear();
+  return NF_OK;
+}
+
+}  // extern "C"

@@ -105,7 +105,13 @@ _sig("nf_gemm_bf16", C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_
 _sig("nf_attention", C.c_int, C.POINTER(ModelCfg), C.POINTER(_Batch), C.c_void_p, C.c_void_p, C.c_void_p,
      C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.c_void_p)
 
-EXPORTED = ["nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
+_sig("nf_kernel_launches", C.c_int64)
+_sig("nf_profile_enable", C.c_int, C.c_int32)
+_sig("nf_profile_read", C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64))
+PROF_LMHEAD, PROF_MISC, PROF_COUNT = OP_COUNT, OP_COUNT + 1, OP_COUNT + 2
+PROF_NAMES = ["kqv", "decode_attn", "prefill_attn", "o_proj", "up_gate", "down", "net", "lm_head", "misc"]
+
+EXPORTED = ["nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
             "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_comm_unique_id",
             "nf_comm_create", "nf_comm_destroy", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
             "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_gemm_bf16", "nf_attention"]
@@ -266,6 +272,22 @@ def attention(cfg: ModelCfg, b: Batch, q: int, kv_pool: int, o: int, ws: int, ws
               sm_prefill: int, stream: int):
     _check(lib.nf_attention(C.byref(cfg), C.byref(b.c), C.c_void_p(q), C.c_void_p(kv_pool), C.c_void_p(o),
                             C.c_void_p(ws), ws_bytes, sm_decode, sm_prefill, C.c_void_p(stream)))
+
+
+def kernel_launches() -> int:
+    return int(lib.nf_kernel_launches())
+
+
+def profile_enable(on: bool = True):
+    _check(lib.nf_profile_enable(1 if on else 0))
+
+
+def profile_read():
+    """{op name: (total ms, launches)} since the last read (synchronises)."""
+    ms = (C.c_double * PROF_COUNT)()
+    cnt = (C.c_int64 * PROF_COUNT)()
+    _check(lib.nf_profile_read(ms, cnt))
+    return {PROF_NAMES[i]: (ms[i], cnt[i]) for i in range(PROF_COUNT)}
 
 
 def comm_unique_id() -> bytes:
