@@ -222,8 +222,12 @@ def run_nf(args, rank, world, local_rank):
 
     sm = [int(x) for x in args.sm.split(",")] if args.sm else None
     if args.mode == "overlap":
-        plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=sm or [96, 52, 52, 96, 96, 96, 16],
-                                balance=True)
+        if args.colocate:
+            plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=sm or [148] * 7, balance=True,
+                                    colocate=True)
+        else:
+            plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=sm or [84, 64, 64, 84, 84, 84, 16],
+                                    balance=True)
     elif args.mode == "nano":
         plan = nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=(1, 1), sm=sm, balance=True)
     else:
@@ -264,6 +268,19 @@ def run_nf(args, rank, world, local_rank):
     ms_step = ms_max / args.steps
     value = world * T * args.steps / (ms_max / 1e3)
 
+    if args.timeline:
+        torch.cuda.synchronize()
+        nf.profile_enable(True)
+        nf.profile_read()
+        step()
+        torch.cuda.synchronize()
+        spans = nf.profile_timeline()
+        nf.profile_enable(False)
+        nf.profile_read()
+        with open(args.timeline, "w") as f:
+            f.write("op,stream,start_ms,end_ms\n")
+            for sp in spans:
+                f.write(f"{sp[0]},{sp[1]},{sp[2]:.4f},{sp[3]:.4f}\n")
     if args.ncu:
         return
     # ---------------- end to end through the public API with host buffers
@@ -336,7 +353,7 @@ def run_nf(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, seeded torch RNG on device)",
             "config": {"workload": f"configs[1]: LLaMA-3-8B-shape {L}-layer serving step, B_dense 2048 "
                                    f"(683 decode ctx 1024-1535 + 341-token chunk + 1024-token prompt), page 16",
-                       "b_dense": T, "n_layers": L, "mode": args.mode,
+                       "b_dense": T, "n_layers": L, "mode": args.mode, "colocate": bool(plan.spec().colocate),
                        "parallelism": "replicas" if world > 1 else "single-gpu",
                        "plan_sm": list(plan.spec().sm), "l2": "no flush: per-step inputs (KV 115 GB) >> 126 MB L2"},
             "tokens_per_s_per_gpu": value / world,
@@ -365,9 +382,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="nf", choices=["nf", "reference"])
     ap.add_argument("--mode", default="overlap", choices=["overlap", "nano", "sequential"])
+    ap.add_argument("--colocate", action="store_true", help="attention CTAs co-resident with GEMM CTAs")
     ap.add_argument("--sm", default="", help="comma-separated SM budget per op kind (7 values)")
     ap.add_argument("--layers", type=int, default=0, help="(dev only) override layer count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--timeline", default="", help="write one step's kernel spans (CSV) to this path")
     ap.add_argument("--ncu", action="store_true", help="profiling run: timed steps only, no e2e / JSON")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -111,6 +111,8 @@ typedef struct {
   int32_t share[NF_MAX_NANO];
   int32_t sm[NF_OP_COUNT];
   int32_t balance;             /* 1: assign requests to nano-batches balancing tokens and KV (model step only) */
+  int32_t colocate;            /* 1: attention CTAs co-reside with GEMM CTAs on the same SMs (3-stage GEMM ring,
+                                  4-warp decode CTAs) instead of disjoint SM partitions */
 } nf_plan_spec;
 
 /* One measured kernel-curve sample, CSV `op_kind,resource_class,units,work,latency_s`. */
@@ -218,6 +220,15 @@ nf_status nf_profile_enable(int32_t on);
  * event-to-event milliseconds (ms_out[NF_PROF_COUNT]) and the number of
  * launches (count_out[NF_PROF_COUNT]); clears the records. */
 nf_status nf_profile_read(double* ms_out, int64_t* count_out);
+/* One recorded kernel span: op kind, stream index (order of first use), start/end in ms
+ * since profiling was enabled. */
+typedef struct {
+  int32_t op, stream;
+  float start_ms, end_ms;
+} nf_span;
+/* Copies up to cap spans recorded since the last nf_profile_read (call before it);
+ * *n_out = number recorded.  Synchronises the events. */
+nf_status nf_profile_timeline(nf_span* out, int32_t cap, int32_t* n_out);
 
 #ifdef __cplusplus
 }

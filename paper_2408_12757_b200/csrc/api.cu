@@ -64,7 +64,7 @@ nf_status validate_cfg(const nf_model_cfg* c) {
   if (c->d_model % 256) return set_error(NF_EUNSUPPORTED, "d_model must be a multiple of 256");
   if ((c->d_ffn / c->tp_size) % 32) return set_error(NF_EUNSUPPORTED, "d_ffn/tp_size must be a multiple of 32");
   if (c->vocab % 32) return set_error(NF_EUNSUPPORTED, "vocab must be a multiple of 32");
-  if (c->n_q_heads / c->n_kv_heads > 16) return set_error(NF_EUNSUPPORTED, "GQA group > 16");
+  if (c->n_q_heads / c->n_kv_heads > 8) return set_error(NF_EUNSUPPORTED, "GQA group > 8 (decode kernel N = 8)");
   if (!(c->rms_eps > 0) || !(c->rope_theta > 1)) return set_error(NF_EINVAL, "bad rms_eps / rope_theta");
   return NF_OK;
 }
@@ -505,10 +505,24 @@ struct LayerCtx {
   const Workspace* w;
   const int32_t* meta_dev;
   CUtensorMap pool_map;
+  CUtensorMap page_map;
   cudaStream_t cs, ms;  // compute / memory streams
 };
 
 int clampsm(int v) { return std::max(1, std::min(v, num_sms())); }
+
+// Decode kernel choice: the mma.sync kernel (8 independent warps per SM, one
+// 4-D TMA box per page) is the default: it reaches the HBM roofline at ~80 SMs.
+// The tcgen05 kernel (decode_tc.cu, one item in flight per CTA) is selectable
+// with NF_DECODE_IMPL=tc for head_dim 128 / GQA <= 8 (not in co-located plans).
+bool use_tc_decode(const nf_model_cfg* c, const nf_plan* p) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("NF_DECODE_IMPL");
+    env = (e && std::string(e) == "tc") ? 1 : 0;
+  }
+  return env == 1 && !p->spec.colocate && c->head_dim == 128 && c->n_q_heads / c->n_kv_heads <= 8;
+}
 
 nf_status run_kqv(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x, const float* part, int nparts,
                   const nf_packed_layer* wt, void* pool) {
@@ -518,6 +532,7 @@ nf_status run_kqv(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x
   if (M <= 0) return NF_OK;
   GemmArgs a{};
   a.epi = EPI_QKV;
+  a.stages = L.p->spec.colocate ? 3 : 4;
   a.M = M;
   a.N = (c->n_q_heads + 2 * c->n_kv_heads) / N * c->head_dim;
   a.K = c->d_model;
@@ -553,6 +568,7 @@ nf_status run_attn(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
   a.hd = c->head_dim;
   a.page_size = c->page_size;
   a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
+  a.dec_warps = L.p->spec.colocate ? 4 : 8;
   const DecodeItem* dec = reinterpret_cast<const DecodeItem*>(L.meta_dev + L.m->off_dec) + nr.dec_off;
   const PrefillItem* pf = reinterpret_cast<const PrefillItem*>(L.meta_dev + L.m->off_pf) + nr.pf_off;
   if (nr.pf_n > 0) {
@@ -561,7 +577,10 @@ nf_status run_attn(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
   }
   if (nr.dec_n > 0) {
     ProfScope ps(NF_OP_DECODE_ATTN, st);
-    NF_CUDA(launch_decode_attention(L.pool_map, a, dec, nr.dec_n, clampsm(L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
+    if (use_tc_decode(c, L.p))
+      NF_CUDA(launch_decode_attention_tc(L.pool_map, a, dec, nr.dec_n, clampsm(L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
+    else
+      NF_CUDA(launch_decode_attention(L.pool_map, L.page_map, a, dec, nr.dec_n, clampsm(L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
   }
   return NF_OK;
 }
@@ -578,6 +597,7 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   // O projection + residual: h1 = x + o W_o^T, with sum-of-squares partials of h1
   GemmArgs a{};
   a.epi = EPI_RESID;
+  a.stages = L.p->spec.colocate ? 3 : 4;
   a.M = M;
   a.N = (int)D;
   a.K = (int)qd;
@@ -595,6 +615,7 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   // Up/Gate + SiLU(gate) * up, RMSNorm(h1) folded as a row scale
   GemmArgs u{};
   u.epi = EPI_SILU;
+  u.stages = L.p->spec.colocate ? 3 : 4;
   u.M = M;
   u.N = (int)(((F + 127) / 128) * 256);
   u.K = (int)D;
@@ -614,6 +635,7 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   // Down + residual: x_out = h1 + m W_d^T, partials of x_out for the next layer's norm
   GemmArgs d{};
   d.epi = EPI_RESID;
+  d.stages = L.p->spec.colocate ? 3 : 4;
   d.M = M;
   d.N = (int)D;
   d.K = (int)F;
@@ -696,6 +718,7 @@ nf_status nf_layer_forward(const nf_plan* plan, nf_comm* comm, const nf_packed_l
   L.cs = cs;
   L.ms = p->mem_stream;
   NF_CUDA(make_pool_tmap(&L.pool_map, kv_pool, b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim, c->page_size));
+  NF_CUDA(make_page_tmap(&L.page_map, kv_pool, b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim, c->page_size));
   // RMS partials of x_in (one part per row)
   NF_CUDA(launch_gather_rows((const __nv_bfloat16*)x_in, nullptr, m.T, c->d_model, nullptr, wsp.part_a, cs));
   NF_TRY(run_layer(p, L, w, kv_pool, (const __nv_bfloat16*)x_in, wsp.part_a, 1, (__nv_bfloat16*)x_out, nullptr, false));
@@ -740,14 +763,18 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
   L.ms = p->mem_stream;
   __nv_bfloat16 *x = wsp.xa, *y = wsp.xb;
   float *px = wsp.part_a, *py = wsp.part_b;
-  std::vector<CUtensorMap> maps(c->n_layers);
-  for (int l = 0; l < c->n_layers; ++l)
+  std::vector<CUtensorMap> maps(c->n_layers), pmaps(c->n_layers);
+  for (int l = 0; l < c->n_layers; ++l) {
     NF_CUDA(make_pool_tmap(&maps[l], kv_pools[l], b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim,
                            c->page_size));
+    NF_CUDA(make_page_tmap(&pmaps[l], kv_pools[l], b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim,
+                           c->page_size));
+  }
   if (p->spec.mode != NF_OVERLAP) {
     int nparts = 1;
     for (int l = 0; l < c->n_layers; ++l) {
       L.pool_map = maps[l];
+      L.page_map = pmaps[l];
       NF_TRY(run_layer(p, L, &w->layers[l], kv_pools[l], x, px, nparts, y, py, false));
       std::swap(x, y);
       std::swap(px, py);
@@ -760,6 +787,7 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
     // soon as KQV_k(l+1) lands, overlapping the other nano-batches' dense ops.
     const auto& nanos = m.nanos;
     L.pool_map = maps[0];
+    L.page_map = pmaps[0];
     for (size_t k = 0; k < nanos.size(); ++k) {
       NF_TRY(run_kqv(L, nanos[k], x, px, 1, &w->layers[0], kv_pools[0]));
       NF_CUDA(cudaEventRecord(p->ev_kqv[k], cs));
@@ -773,6 +801,7 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
         NF_TRY(run_dense_tail(L, nanos[k], x, &w->layers[l], y, py));
         if (l + 1 < c->n_layers) {
           L.pool_map = maps[l + 1];
+          L.page_map = pmaps[l + 1];
           NF_TRY(run_kqv(L, nanos[k], y, py, NP, &w->layers[l + 1], kv_pools[l + 1]));
           NF_CUDA(cudaEventRecord(p->ev_kqv[k], cs));
           NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
@@ -864,6 +893,8 @@ nf_status nf_attention(const nf_model_cfg* cfg, const nf_batch* b, const void* q
   L.w = &w2;
   L.meta_dev = wsp.meta;
   NF_CUDA(make_pool_tmap(&L.pool_map, kv_pool, b->n_pages_pool, cfg->n_kv_heads / cfg->tp_size, cfg->head_dim,
+                         cfg->page_size));
+  NF_CUDA(make_page_tmap(&L.page_map, kv_pool, b->n_pages_pool, cfg->n_kv_heads / cfg->tp_size, cfg->head_dim,
                          cfg->page_size));
   NF_TRY(run_attn(L, m.nanos[0], st));
   return NF_OK;

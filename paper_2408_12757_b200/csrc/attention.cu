@@ -28,35 +28,49 @@ cudaError_t make_pool_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, in
 
 namespace {
 
-constexpr int DEC_WARPS = 8;
 constexpr int BOX_BYTES = 16 * 128;  // 16 rows x 64 bf16
 
 NF_DEV uint32_t swz(int row, int chunk) { return row * 128 + (((chunk & 7) ^ (row & 7)) << 4); }
 
 NF_DEV uint32_t ldg_u32(const __nv_bfloat16* p) { return *reinterpret_cast<const uint32_t*>(p); }
 
-template <int HD>
-constexpr int dec_stages() { return HD == 128 ? 3 : 6; }
+template <int HD, int DEC_WARPS>
+constexpr int dec_stages() {
+  return HD == 128 ? (DEC_WARPS == 8 ? 3 : DEC_WARPS == 6 ? 4 : 2) : (DEC_WARPS == 8 ? 6 : DEC_WARPS == 6 ? 8 : 4);
+}
 
-template <int HD>
-constexpr int dec_smem() { return DEC_WARPS * dec_stages<HD>() * (2 * 16 * HD * 2) + DEC_WARPS * dec_stages<HD>() * 8 + 1024; }
+template <int HD, int DEC_WARPS>
+constexpr int dec_smem() {
+  return DEC_WARPS * dec_stages<HD, DEC_WARPS>() * (2 * 16 * HD * 2) + DEC_WARPS * dec_stages<HD, DEC_WARPS>() * 8 + 1024;
+}
 
 // ---------------------------------------------------------------------------- decode
-template <int HD>
-__global__ void __launch_bounds__(DEC_WARPS * 32, 1)
-    decode_attn_kernel(const __grid_constant__ CUtensorMap pool, const AttnArgs a,
+// Transposed formulation: S^T[16 keys x 8 heads] = K[16 x hd] . Q^T[hd x 8]
+// (m16n8k16: the page's 16 keys are the M rows, the GQA group's R <= 8 query
+// heads the N columns), then O^T[hd x 8] += V^T[hd x 16] . P^T[16 x 8] with P^T
+// turned into a B fragment in registers by movmatrix.  16 MMAs per 16-key page.
+NF_DEV uint32_t movmatrix_trans(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
+}
+
+template <int HD, int DEC_WARPS>
+__global__ void __launch_bounds__(DEC_WARPS * 32)
+    decode_attn_kernel(const __grid_constant__ CUtensorMap pool, const __grid_constant__ CUtensorMap pages,
+                       const AttnArgs a,
                        const DecodeItem* __restrict__ items, int n_items) {
   constexpr int NBOX = HD / 64;
   constexpr int PAGE_BYTES = 16 * HD * 2;
   constexpr int STAGE_BYTES = 2 * PAGE_BYTES;
-  constexpr int NS = dec_stages<HD>();
+  constexpr int NS = dec_stages<HD, DEC_WARPS>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * NS * STAGE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + DEC_WARPS * NS * STAGE_BYTES) + warp * NS;
   if (lane == 0) {
-    if (warp == 0) tma_prefetch_desc(&pool);
+    if (warp == 0) tma_prefetch_desc(&pages);
     for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
   }
@@ -65,62 +79,59 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 1)
   const int gw = blockIdx.x * DEC_WARPS + warp, TW = gridDim.x * DEC_WARPS;
   const int kh = a.kh, R = a.qh / a.kh;
 
-  // look-ahead loader cursor (warp-uniform)
-  int l_item = gw, l_page = 0, l_np = 0, l_ps = 0, l_kvh = 0;
-  if (l_item < n_items) {
-    const DecodeItem it = items[l_item];
-    l_np = (it.kv_len + 15) >> 4;
-    l_ps = it.page_start;
-    l_kvh = it.kvh;
-  }
+  // look-ahead loader cursor (warp-uniform) + a 32-entry window of page ids (one per lane)
+  int l_item = gw, l_page = 0, l_np = 0, l_ps = 0, l_kvh = 0, pid_win = 0;
+  auto load_item = [&]() {
+    if (l_item < n_items) {
+      const DecodeItem it = items[l_item];
+      l_np = (it.kv_len + 15) >> 4;
+      l_ps = it.page_start;
+      l_kvh = it.kvh;
+      pid_win = lane < l_np ? a.page_ids[l_ps + lane] : 0;
+    }
+  };
+  load_item();
   uint32_t issued = 0, consumed = 0;
+  const uint64_t kv_policy = policy_evict_first();  // K/V pages are read exactly once: keep L2 for the GEMMs
   auto issue_one = [&]() {
     if (l_item >= n_items) return;
     const int s = issued % NS;
+    const int64_t page = __shfl_sync(0xffffffffu, pid_win, l_page & 31);
     if (lane == 0) {
-      const int64_t page = a.page_ids[l_ps + l_page];
       uint8_t* dst = ring + s * STAGE_BYTES;
       const int rowK = (int)(((page * 2 + 0) * kh + l_kvh) * 16);
-      const int rowV = rowK + kh * 16;
       fence_proxy_async();
       mbar_arrive_expect_tx(&bars[s], STAGE_BYTES);
-#pragma unroll
-      for (int b = 0; b < NBOX; ++b) tma_load_2d(dst + b * BOX_BYTES, &pool, &bars[s], b * 64, rowK);
-#pragma unroll
-      for (int b = 0; b < NBOX; ++b) tma_load_2d(dst + PAGE_BYTES + b * BOX_BYTES, &pool, &bars[s], b * 64, rowV);
+      tma_load_4d_hint(dst, &pages, &bars[s], 0, rowK, 0, 0, kv_policy);  // K and V of the page: one 4-D box
     }
     ++issued;
     if (++l_page == l_np) {
       l_item += TW;
       l_page = 0;
-      if (l_item < n_items) {
-        const DecodeItem it = items[l_item];
-        l_np = (it.kv_len + 15) >> 4;
-        l_ps = it.page_start;
-        l_kvh = it.kvh;
-      }
+      load_item();
+    } else if ((l_page & 31) == 0) {
+      pid_win = l_page + lane < l_np ? a.page_ids[l_ps + l_page + lane] : 0;
     }
   };
   for (int i = 0; i < NS; ++i) issue_one();
 
+  const int hq = lane >> 2;            // query head of this lane's B-fragment column (n = lane/4)
+  const int hc = 2 * (lane & 3);       // first of the two head columns this lane holds in C fragments
   for (int item = gw; item < n_items; item += TW) {
     const DecodeItem it = items[item];
     const int kv_len = it.kv_len;
     const __nv_bfloat16* qbase = a.q + ((int64_t)it.t * a.qh + (int64_t)it.kvh * R) * HD;
-    const int row0 = lane >> 2, row1 = row0 + 8;
-    uint32_t qf[HD / 16][4];
+    uint32_t qb[HD / 16][2];
 #pragma unroll
     for (int ks = 0; ks < HD / 16; ++ks) {
       const int kc = ks * 16 + 2 * (lane & 3);
-      qf[ks][0] = row0 < R ? ldg_u32(qbase + row0 * HD + kc) : 0u;
-      qf[ks][1] = row1 < R ? ldg_u32(qbase + row1 * HD + kc) : 0u;
-      qf[ks][2] = row0 < R ? ldg_u32(qbase + row0 * HD + kc + 8) : 0u;
-      qf[ks][3] = row1 < R ? ldg_u32(qbase + row1 * HD + kc + 8) : 0u;
+      qb[ks][0] = hq < R ? ldg_u32(qbase + hq * HD + kc) : 0u;
+      qb[ks][1] = hq < R ? ldg_u32(qbase + hq * HD + kc + 8) : 0u;
     }
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-    float oacc[HD / 8][4];
+    float oacc[HD / 16][4];
 #pragma unroll
-    for (int d = 0; d < HD / 8; ++d) oacc[d][0] = oacc[d][1] = oacc[d][2] = oacc[d][3] = 0.f;
+    for (int d = 0; d < HD / 16; ++d) oacc[d][0] = oacc[d][1] = oacc[d][2] = oacc[d][3] = 0.f;
 
     const int np = (kv_len + 15) >> 4;
     for (int p = 0; p < np; ++p) {
@@ -136,87 +147,76 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 1)
         }
         __syncwarp();
       }
-      // S = Q K^T (16 x 16 keys)
-      float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      // S^T = K Q^T: two independent accumulation chains over the head dim
+      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
       {
-        const int key = (lane & 7) + ((lane >> 4) << 3);
-        const int hi = (lane >> 3) & 1;
+        const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
+        const int hi = lane >> 4;
 #pragma unroll
         for (int ks = 0; ks < HD / 16; ++ks) {
           const int ch = ks * 2 + hi;
           uint32_t kf[4];
           ldmatrix_x4(kf, smem_u32(kb) + (ch >> 3) * BOX_BYTES + swz(key, ch));
-          const uint32_t b0[2] = {kf[0], kf[1]}, b1[2] = {kf[2], kf[3]};
-          mma_bf16_16816(sacc[0], qf[ks], b0);
-          mma_bf16_16816(sacc[1], qf[ks], b1);
+          mma_bf16_16816(ks & 1 ? sb : sa, kf, qb[ks]);
         }
       }
-      // scale, mask, online softmax (rows row0 / row1)
+      float sc[4];
+      const int k0 = p * 16 + hq, k1 = k0 + 8;
+      sc[0] = k0 < kv_len ? (sa[0] + sb[0]) * a.scale_log2 : -INFINITY;
+      sc[1] = k0 < kv_len ? (sa[1] + sb[1]) * a.scale_log2 : -INFINITY;
+      sc[2] = k1 < kv_len ? (sa[2] + sb[2]) * a.scale_log2 : -INFINITY;
+      sc[3] = k1 < kv_len ? (sa[3] + sb[3]) * a.scale_log2 : -INFINITY;
+      // online softmax over keys (rows) per head column: reduce across lanes xor 4, 8, 16
+      float mx0 = fmaxf(sc[0], sc[2]), mx1 = fmaxf(sc[1], sc[3]);
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int key = nt * 8 + 2 * (lane & 3) + (e & 1);
-          sacc[nt][e] = key < valid ? sacc[nt][e] * a.scale_log2 : -INFINITY;
-        }
-      float mx0 = fmaxf(fmaxf(sacc[0][0], sacc[0][1]), fmaxf(sacc[1][0], sacc[1][1]));
-      float mx1 = fmaxf(fmaxf(sacc[0][2], sacc[0][3]), fmaxf(sacc[1][2], sacc[1][3]));
-      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      for (int o = 4; o < 32; o <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+      }
       const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
       const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
       m0 = mn0;
       m1 = mn1;
-      float ps[2][4];
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        ps[nt][0] = exp2f(sacc[nt][0] - mn0);
-        ps[nt][1] = exp2f(sacc[nt][1] - mn0);
-        ps[nt][2] = exp2f(sacc[nt][2] - mn1);
-        ps[nt][3] = exp2f(sacc[nt][3] - mn1);
-      }
-      l0 = l0 * al0 + ps[0][0] + ps[0][1] + ps[1][0] + ps[1][1];
-      l1 = l1 * al1 + ps[0][2] + ps[0][3] + ps[1][2] + ps[1][3];
-#pragma unroll
-      for (int d = 0; d < HD / 8; ++d) {
-        oacc[d][0] *= al0; oacc[d][1] *= al0;
-        oacc[d][2] *= al1; oacc[d][3] *= al1;
-      }
-      const uint32_t pf[4] = {pack_bf16x2(ps[0][0], ps[0][1]), pack_bf16x2(ps[0][2], ps[0][3]),
-                              pack_bf16x2(ps[1][0], ps[1][1]), pack_bf16x2(ps[1][2], ps[1][3])};
-      // O += P V
+      const float p0 = exp2f(sc[0] - mn0), p1 = exp2f(sc[1] - mn1), p2 = exp2f(sc[2] - mn0), p3 = exp2f(sc[3] - mn1);
+      l0 = l0 * al0 + p0 + p2;
+      l1 = l1 * al1 + p1 + p3;
+      const uint32_t pb[2] = {movmatrix_trans(pack_bf16x2(p0, p1)), movmatrix_trans(pack_bf16x2(p2, p3))};
+      // O^T += V^T P^T
       {
-        const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
-        const int hi = lane >> 4;
+        const int key = (lane & 7) + ((lane >> 4) << 3);
+        const int hi = (lane >> 3) & 1;
 #pragma unroll
-        for (int dp = 0; dp < HD / 16; ++dp) {
-          const int ch = dp * 2 + hi;
+        for (int mt = 0; mt < HD / 16; ++mt) {
+          const int ch = mt * 2 + hi;
           uint32_t vf[4];
           ldmatrix_x4_trans(vf, smem_u32(vb) + (ch >> 3) * BOX_BYTES + swz(key, ch));
-          const uint32_t b0[2] = {vf[0], vf[1]}, b1[2] = {vf[2], vf[3]};
-          mma_bf16_16816(oacc[2 * dp], pf, b0);
-          mma_bf16_16816(oacc[2 * dp + 1], pf, b1);
+          oacc[mt][0] *= al0; oacc[mt][1] *= al1;
+          oacc[mt][2] *= al0; oacc[mt][3] *= al1;
+          mma_bf16_16816(oacc[mt], vf, pb);
         }
       }
       __syncwarp();
       ++consumed;
       issue_one();
     }
-    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
     const float i0 = 1.f / l0, i1 = 1.f / l1;
     __nv_bfloat16* obase = a.o + (int64_t)it.t * a.qh * HD + (int64_t)it.kvh * R * HD;
 #pragma unroll
-    for (int d = 0; d < HD / 8; ++d) {
-      const int col = d * 8 + 2 * (lane & 3);
-      if (row0 < R)
-        *reinterpret_cast<uint32_t*>(obase + row0 * HD + col) = pack_bf16x2(oacc[d][0] * i0, oacc[d][1] * i0);
-      if (row1 < R)
-        *reinterpret_cast<uint32_t*>(obase + row1 * HD + col) = pack_bf16x2(oacc[d][2] * i1, oacc[d][3] * i1);
+    for (int mt = 0; mt < HD / 16; ++mt) {
+      const int d0 = mt * 16 + hq;
+      if (hc < R) {
+        obase[hc * HD + d0] = __float2bfloat16_rn(oacc[mt][0] * i0);
+        obase[hc * HD + d0 + 8] = __float2bfloat16_rn(oacc[mt][2] * i0);
+      }
+      if (hc + 1 < R) {
+        obase[(hc + 1) * HD + d0] = __float2bfloat16_rn(oacc[mt][1] * i1);
+        obase[(hc + 1) * HD + d0 + 8] = __float2bfloat16_rn(oacc[mt][3] * i1);
+      }
     }
   }
 }
@@ -410,20 +410,35 @@ __global__ void __launch_bounds__(PF_THREADS)
   }
 }
 
-template <int HD>
-cudaError_t launch_decode_hd(const CUtensorMap& m, const AttnArgs& a, const DecodeItem* items, int n_items,
-                             int sm_budget, cudaStream_t st) {
+template <int HD, int W>
+cudaError_t launch_decode_hdw(const CUtensorMap& m, const CUtensorMap& pm, const AttnArgs& a, const DecodeItem* items, int n_items,
+                              int sm_budget, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         dec_smem<HD>());
+    cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         dec_smem<HD, W>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  int grid = std::min((n_items + DEC_WARPS - 1) / DEC_WARPS, std::max(sm_budget, 1));
-  decode_attn_kernel<HD><<<grid, DEC_WARPS * 32, dec_smem<HD>(), st>>>(m, a, items, n_items);
+  // one CTA per SM of the budget (8-warp CTAs fill an SM's smem; 4-warp CTAs leave room for a GEMM CTA)
+  int grid = std::min((n_items + W - 1) / W, std::max(sm_budget, 1));
+  decode_attn_kernel<HD, W><<<grid, W * 32, dec_smem<HD, W>(), st>>>(m, pm, a, items, n_items);
   count_launch();
   return cudaGetLastError();
+}
+
+template <int HD>
+cudaError_t launch_decode_hd(const CUtensorMap& m, const CUtensorMap& pm, const AttnArgs& a, const DecodeItem* items, int n_items,
+                             int sm_budget, cudaStream_t st) {
+  static int env_w = -1;
+  if (env_w < 0) {
+    const char* e = getenv("NF_DEC_WARPS");
+    env_w = e ? atoi(e) : 0;
+  }
+  const int w = a.dec_warps == 4 ? 4 : (env_w == 6 ? 6 : 8);
+  if (w == 4) return launch_decode_hdw<HD, 4>(m, pm, a, items, n_items, sm_budget, st);
+  if (w == 6) return launch_decode_hdw<HD, 6>(m, pm, a, items, n_items, sm_budget, st);
+  return launch_decode_hdw<HD, 8>(m, pm, a, items, n_items, sm_budget, st);
 }
 
 template <int HD>
@@ -445,11 +460,11 @@ cudaError_t launch_prefill_hd(const CUtensorMap& m, const AttnArgs& a, const Pre
 
 }  // namespace
 
-cudaError_t launch_decode_attention(const CUtensorMap& m, const AttnArgs& a, const DecodeItem* items, int n_items,
+cudaError_t launch_decode_attention(const CUtensorMap& m, const CUtensorMap& pm, const AttnArgs& a, const DecodeItem* items, int n_items,
                                     int sm_budget, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
-  if (a.hd == 128) return launch_decode_hd<128>(m, a, items, n_items, sm_budget, st);
-  if (a.hd == 64) return launch_decode_hd<64>(m, a, items, n_items, sm_budget, st);
+  if (a.hd == 128) return launch_decode_hd<128>(m, pm, a, items, n_items, sm_budget, st);
+  if (a.hd == 64) return launch_decode_hd<64>(m, pm, a, items, n_items, sm_budget, st);
   return cudaErrorInvalidValue;
 }
 

@@ -25,12 +25,17 @@ struct AttnArgs {
   const int* page_ids;
   int qh, kh, hd, page_size;
   float scale_log2;         // log2(e)/sqrt(hd)
+  int dec_warps;            // decode CTA size: 8 (own SMs) or 4 (co-resident with a GEMM CTA)
 };
 
+cudaError_t make_page_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, int kh, int hd, int page_size);
 cudaError_t make_pool_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, int kh, int hd, int page_size);
 
-cudaError_t launch_decode_attention(const CUtensorMap& pool_map, const AttnArgs& a, const DecodeItem* items,
+cudaError_t launch_decode_attention(const CUtensorMap& pool_map, const CUtensorMap& page_map, const AttnArgs& a, const DecodeItem* items,
                                     int n_items, int sm_budget, cudaStream_t stream);
+// tcgen05 decode attention (head_dim 128, GQA group <= 8); decode_tc.cu
+cudaError_t launch_decode_attention_tc(const CUtensorMap& pool_map, const AttnArgs& a, const DecodeItem* items,
+                                       int n_items, int sm_budget, cudaStream_t stream);
 cudaError_t launch_prefill_attention(const CUtensorMap& pool_map, const AttnArgs& a, const PrefillItem* items,
                                      int n_items, int sm_budget, cudaStream_t stream);
 

@@ -65,6 +65,7 @@ NF_DEV void sincos_reduced(float a, float* s, float* c) {
   __sincosf(r, s, c);
 }
 
+template <int GEMM_STAGES>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ GemmArgs args) {
@@ -114,12 +115,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // ------------------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t a_policy = policy_evict_last();  // activations are re-read by every n-tile
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         const int mb = tile % tiles_m, nb = tile / tiles_m;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(sA + stage * A_STAGE_ELEMS, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM);
+          tma_load_2d_hint(sA + stage * A_STAGE_ELEMS, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM, a_policy);
           tma_load_2d(sB + stage * B_STAGE_ELEMS, &tmB, &full[stage], kb * GEMM_BK, nb * GEMM_BN);
           if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
         }
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_once;
-bool g_attr_set = false;
+bool g_attr_set[5] = {false, false, false, false, false};
 
 cudaError_t get_encode() {
   std::call_once(g_once, [] {
@@ -344,6 +346,22 @@ cudaError_t make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Paged-KV page map: dims (64 cols, rows, half, kv) so one box {64, 16, hd/64, 2} = one page's
+// K and V block of one KV head (hd*16*2*2 bytes) lands as [kv][half][16 rows][128 B], 128B-swizzled.
+cudaError_t make_page_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, int kh, int hd, int page_size) {
+  cudaError_t e = get_encode();
+  if (e != cudaSuccess) return e;
+  const uint64_t rows = (uint64_t)n_pages * 2 * kh * page_size;
+  cuuint64_t dims[4] = {64, rows, (cuuint64_t)(hd / 64), 2};
+  cuuint64_t strides[3] = {(cuuint64_t)hd * 2, 128, (cuuint64_t)kh * page_size * hd * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)page_size, (cuuint32_t)(hd / 64), 2};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pool), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb,
                         const GemmArgs& args, int sm_budget, cudaStream_t stream) {
   if (args.M <= 0) return cudaSuccess;
@@ -352,15 +370,17 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   if (e != cudaSuccess) return e;
   e = make_tmap_bf16(&tb, B, args.K, args.N, ldb, GEMM_BK, GEMM_BN);
   if (e != cudaSuccess) return e;
-  if (!g_attr_set) {
-    e = cudaFuncSetAttribute(gemm_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+  const int stages = args.stages == 3 ? 3 : 4;
+  auto kern = stages == 3 ? gemm_tcgen05_kernel<3> : gemm_tcgen05_kernel<4>;
+  if (!g_attr_set[stages]) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem(stages));
     if (e != cudaSuccess) return e;
-    g_attr_set = true;
+    g_attr_set[stages] = true;
   }
   const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + GEMM_BN - 1) / GEMM_BN);
   int grid = tiles < sm_budget ? tiles : sm_budget;
   if (grid < 1) grid = 1;
-  gemm_tcgen05_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(ta, tb, args);
+  kern<<<grid, GEMM_THREADS, gemm_smem(stages), stream>>>(ta, tb, args);
   count_launch();
   return cudaGetLastError();
 }

@@ -19,12 +19,13 @@ enum GemmEpiMode : int {
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BN = 256;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_STAGES = 4;
+constexpr int GEMM_STAGES = 4;      // default ring depth; 3 when co-resident with attention CTAs
 constexpr int GEMM_THREADS = 256;  // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warps 4-7 epilogue
-constexpr int GEMM_SMEM = GEMM_STAGES * (GEMM_BM + GEMM_BN) * GEMM_BK * 2 + 1024 + 256;
+constexpr int gemm_smem(int stages) { return stages * (GEMM_BM + GEMM_BN) * GEMM_BK * 2 + 1024 + 512; }
 
 struct GemmArgs {
   int epi;
+  int stages;           // smem ring depth: 4 (default) or 3 (co-resident with attention)
   int M, N, K;          // rows of A in this launch, rows of B (packed output columns), reduction dim
   int n_valid;          // valid output columns (EPI_SILU: F; else N)
   // outputs (row-indexed pointers are pre-offset to the launch's first row)

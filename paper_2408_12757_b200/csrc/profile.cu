@@ -13,8 +13,10 @@ std::atomic<long long> g_launches{0};
 std::atomic<int> g_prof_on{0};
 struct Rec {
   int op;
+  cudaStream_t st;
   cudaEvent_t a, b;
 };
+cudaEvent_t g_base = nullptr;
 std::mutex g_mu;
 std::vector<Rec> g_recs;
 std::vector<cudaEvent_t> g_pool;
@@ -44,7 +46,7 @@ ProfScope::~ProfScope() {
   if (!a_) return;
   std::lock_guard<std::mutex> lk(g_mu);
   cudaEventRecord(b_, st_);
-  g_recs.push_back(Rec{op_, a_, b_});
+  g_recs.push_back(Rec{op_, st_, a_, b_});
 }
 
 }  // namespace nf
@@ -54,7 +56,39 @@ extern "C" {
 int64_t nf_kernel_launches(void) { return nf::g_launches.load(); }
 
 nf_status nf_profile_enable(int32_t on) {
+  if (on && !nf::g_prof_on.load()) {
+    std::lock_guard<std::mutex> lk(nf::g_mu);
+    if (!nf::g_base) cudaEventCreate(&nf::g_base);
+    cudaEventRecord(nf::g_base, 0);
+  }
   nf::g_prof_on = on ? 1 : 0;
+  return NF_OK;
+}
+
+nf_status nf_profile_timeline(nf_span* out, int32_t cap, int32_t* n_out) {
+  if (!n_out) return nf::set_error(NF_EINVAL, "NULL n_out");
+  std::lock_guard<std::mutex> lk(nf::g_mu);
+  std::vector<cudaStream_t> streams;
+  int n = 0;
+  for (auto& r : nf::g_recs) {
+    if (out && n < cap) {
+      float a = 0.f, b = 0.f;
+      cudaError_t e = cudaEventSynchronize(r.b);
+      if (e == cudaSuccess) e = cudaEventElapsedTime(&a, nf::g_base, r.a);
+      if (e == cudaSuccess) e = cudaEventElapsedTime(&b, nf::g_base, r.b);
+      if (e != cudaSuccess) return nf::set_error(NF_ECUDA, "timeline event: %s", cudaGetErrorString(e));
+      int si = -1;
+      for (size_t i = 0; i < streams.size(); ++i)
+        if (streams[i] == r.st) si = (int)i;
+      if (si < 0) {
+        si = (int)streams.size();
+        streams.push_back(r.st);
+      }
+      out[n] = nf_span{r.op, si, a, b};
+    }
+    ++n;
+  }
+  *n_out = n;
   return NF_OK;
 }
 

@@ -47,7 +47,7 @@ class _Batch(C.Structure):
 
 class PlanSpec(C.Structure):
     _fields_ = [("mode", C.c_int32), ("n_nano", C.c_int32), ("share", C.c_int32 * MAX_NANO),
-                ("sm", C.c_int32 * OP_COUNT), ("balance", C.c_int32)]
+                ("sm", C.c_int32 * OP_COUNT), ("balance", C.c_int32), ("colocate", C.c_int32)]
 
 
 class CurvePoint(C.Structure):
@@ -109,9 +109,16 @@ _sig("nf_kernel_launches", C.c_int64)
 _sig("nf_profile_enable", C.c_int, C.c_int32)
 _sig("nf_profile_read", C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64))
 PROF_LMHEAD, PROF_MISC, PROF_COUNT = OP_COUNT, OP_COUNT + 1, OP_COUNT + 2
+
+
+class Span(C.Structure):
+    _fields_ = [("op", C.c_int32), ("stream", C.c_int32), ("start_ms", C.c_float), ("end_ms", C.c_float)]
+
+
+_sig("nf_profile_timeline", C.c_int, C.POINTER(Span), C.c_int32, P_i32)
 PROF_NAMES = ["kqv", "decode_attn", "prefill_attn", "o_proj", "up_gate", "down", "net", "lm_head", "misc"]
 
-EXPORTED = ["nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
+EXPORTED = ["nf_profile_timeline", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
             "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_comm_unique_id",
             "nf_comm_create", "nf_comm_destroy", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
             "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_gemm_bf16", "nf_attention"]
@@ -175,7 +182,7 @@ class Plan:
 
     @classmethod
     def explicit(cls, cfg: ModelCfg, mode: int = SEQUENTIAL, shares: Sequence[int] = (1,),
-                 sm: Optional[Sequence[int]] = None, balance: bool = False) -> "Plan":
+                 sm: Optional[Sequence[int]] = None, balance: bool = False, colocate: bool = False) -> "Plan":
         spec = PlanSpec()
         spec.mode = mode
         spec.n_nano = len(shares)
@@ -185,6 +192,7 @@ class Plan:
         for i in range(OP_COUNT):
             spec.sm[i] = int(sm[i])
         spec.balance = int(balance)
+        spec.colocate = int(colocate)
         h = C.c_void_p()
         _check(lib.nf_plan_create_explicit(C.byref(cfg), C.byref(spec), C.byref(h)))
         return cls(h.value)
@@ -280,6 +288,15 @@ def kernel_launches() -> int:
 
 def profile_enable(on: bool = True):
     _check(lib.nf_profile_enable(1 if on else 0))
+
+
+def profile_timeline():
+    """[(op name, stream index, start ms, end ms)] recorded since the last profile_read()."""
+    n = C.c_int32()
+    _check(lib.nf_profile_timeline(None, 0, C.byref(n)))
+    arr = (Span * max(n.value, 1))()
+    _check(lib.nf_profile_timeline(arr, n.value, C.byref(n)))
+    return [(PROF_NAMES[s.op], s.stream, s.start_ms, s.end_ms) for s in arr[:n.value]]
 
 
 def profile_read():

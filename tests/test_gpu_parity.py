@@ -155,14 +155,14 @@ def _layer_case(shape, b, seed=0, fill=0.0):
     return w, x, pool
 
 
-def _gpu_layer(env, shape, b, w, x, pool, mode, shares=(1,), sm=None, balance=False):
+def _gpu_layer(env, shape, b, w, x, pool, mode, shares=(1,), sm=None, balance=False, colocate=False):
     nf, rt = env
     cfg = rt.cfg_from_shape(shape)
     nb = nf.Batch.from_any(b)
     wd = device_weights(w)
     packed = rt.pack_layer(cfg, wd)
     pool_d = dev(pool)
-    plan = nf.Plan.explicit(cfg, mode=mode, shares=shares, sm=sm, balance=balance)
+    plan = nf.Plan.explicit(cfg, mode=mode, shares=shares, sm=sm, balance=balance, colocate=colocate)
     out = rt.layer_forward(plan, cfg, packed, pool_d, nb, dev(x))
     torch.cuda.synchronize()
     return host(out), pool_d
@@ -208,6 +208,18 @@ def test_layer_split_invariance_and_modes_agree(env):
         assert_close(out, ref, what=f"mode={mode} shares={shares}")
         outs[(mode, shares)] = out
     assert np.array_equal(outs[(1, (1, 1))], outs[(2, (1, 1))])
+
+
+@pytest.mark.parametrize("shape_name", ["c1", "llama3-8b"])
+def test_layer_colocated_plan(env, shape_name):
+    """3-stage GEMM ring + 4-warp decode CTAs sharing SMs: same numbers."""
+    shape = synth.SHAPES[shape_name]
+    b = synth.make_batch([1] * 12 + [100, 1, 37], [1024, 5, 1535, 16, 1, 900, 64, 700, 33, 1200, 1300, 100, 341, 2, 0],
+                         seed=3, pool_slack=2)
+    w, x, pool = _layer_case(shape, b)
+    ref = OL.decoder_layer(x, w, OL.as_pool(pool), b, shape)
+    out, _ = _gpu_layer(env, shape, b, w, x, pool, 2, (1, 1), sm=[148] * 7, colocate=True)
+    assert_close(out, ref, what="colocated layer")
 
 
 def test_layer_8b_shape_small_batch(env):
@@ -260,9 +272,10 @@ def test_model_step_vs_oracle(env):
     nb = nf.Batch.from_any(b)
     ws = rt.workspace(cfg, nb)
     tok_d = torch.from_numpy(toks).cuda()
-    for mode, shares, bal in [(0, (1,), False), (2, (1, 1), False), (2, (1, 1), True), (1, (1, 2), True)]:
+    for mode, shares, bal, col in [(0, (1,), False, False), (2, (1, 1), False, False), (2, (1, 1), True, False),
+                                   (1, (1, 2), True, False), (2, (1, 1), True, True)]:
         pools_d = [dev(p) for p in pools]
-        plan = nf.Plan.explicit(cfg, mode=mode, shares=shares, balance=bal)
+        plan = nf.Plan.explicit(cfg, mode=mode, shares=shares, balance=bal, colocate=col)
         ids = model.step(plan, pools_d, nb, tok_d, ws).cpu().numpy()
         srt = np.sort(logits, axis=1)
         gap = srt[:, -1] - srt[:, -2]

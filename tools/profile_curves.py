@@ -1,0 +1,103 @@
+#!/usr/bin/env python
+"""Offline kernel profiling vs SM budget ("estimates the kernel
+performance based on offline profiling"; Fig. 5 / SPEC S:237-269).
+
+Times each hot-path kernel of the 8B-shape step at SM budgets
+{8, 16, ..., 144, 148} with CUDA events and writes the SPEC curve CSV
+`op_kind,resource_class,units,work,latency_s` (op_kind = NF_OP_* index), the
+input of nf_plan_create.  Work: tokens for dense ops, KV keys for attention.
+
+Usage: python tools/profile_curves.py [--out profiles/curves_b200.csv] [--quick]
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "curves_b200.csv"))
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--reps", type=int, default=5)
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_2408_12757_b200 import nf, runtime as rt
+
+    dev = torch.device("cuda")
+    shape = synth.SHAPES["llama3-8b"]
+    D, F, hd, Hq, Hk = shape.d_model, shape.d_ffn, shape.head_dim, shape.n_q_heads, shape.n_kv_heads
+    units = [8, 16, 32, 48, 64, 80, 96, 112, 128, 148] if args.quick else list(range(8, 145, 8)) + [148]
+    rows = []
+    st = rt.stream_handle()
+
+    def timeit(fn):
+        for _ in range(2):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / args.reps / 1e3
+
+    # dense GEMMs at the nano-batch size (1024 tokens) and the full batch
+    gemms = {nf.OP_KQV: ((Hq + 2 * Hk) * hd, D), nf.OP_O: (D, Hq * hd), nf.OP_UG: (2 * F, D), nf.OP_DOWN: (D, F)}
+    for M in (512, 1024, 2048):
+        A = torch.randn(M, max(D, F), device=dev).to(torch.bfloat16)
+        for op, (N, K) in gemms.items():
+            B = (torch.randn(N, K, device=dev) * K ** -0.5).to(torch.bfloat16)
+            C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+            for u in units:
+                t = timeit(lambda: nf.gemm_bf16(A.data_ptr(), A.shape[1], B.data_ptr(), K, C.data_ptr(), N, M, N, K,
+                                                u, st))
+                rows.append((op, "compute", u, M, t))
+            del B, C
+        del A
+    # decode attention over the steady-state decode requests (683, contexts 1024..1535)
+    full = synth.workload_batch(2048, 1024, 512)
+    n_dec = int((full.q_len == 1).sum())
+    for frac in (0.5, 1.0):
+        n = int(n_dec * frac)
+        b = synth.make_batch([1] * n, full.kv_prefix[:n], seed=3)
+        nb = nf.Batch.from_any(b)
+        cfg = rt.cfg_from_shape(shape)
+        pool = torch.randn((b.n_pages_pool, 2, Hk, 16, hd), device=dev).to(torch.bfloat16)
+        q = torch.randn((n, Hq, hd), device=dev).to(torch.bfloat16)
+        o = torch.empty((n, Hq * hd), device=dev, dtype=torch.bfloat16)
+        ws = rt.workspace(cfg, nb)
+        keys = int((b.kv_prefix + 1).sum())
+        for u in units:
+            t = timeit(lambda: nf.attention(cfg, nb, q.data_ptr(), pool.data_ptr(), o.data_ptr(), ws.data_ptr(),
+                                            ws.numel(), u, u, st))
+            rows.append((nf.OP_DECODE_ATTN, "memory", u, keys, t))
+            print(f"decode n={n} sm={u}: {t*1e6:.1f} us  {keys*Hk*hd*4/t/1e9:.0f} GB/s", flush=True)
+        del pool
+    # prefill attention: the chunk (341, prefix 683) + prompt (1024)
+    b = synth.make_batch([341, 1024], [683, 0], seed=3)
+    nb = nf.Batch.from_any(b)
+    pool = torch.randn((b.n_pages_pool, 2, Hk, 16, hd), device=dev).to(torch.bfloat16)
+    q = torch.randn((b.n_tokens, Hq, hd), device=dev).to(torch.bfloat16)
+    o = torch.empty((b.n_tokens, Hq * hd), device=dev, dtype=torch.bfloat16)
+    ws = rt.workspace(cfg, nb)
+    keys = int(sum(p + (i + 1) for p, ql in zip(b.kv_prefix, b.q_len) for i in range(ql)))
+    for u in units:
+        t = timeit(lambda: nf.attention(cfg, nb, q.data_ptr(), pool.data_ptr(), o.data_ptr(), ws.data_ptr(),
+                                        ws.numel(), u, u, st))
+        rows.append((nf.OP_PREFILL_ATTN, "compute", u, keys, t))
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as f:
+        f.write("op_kind,resource_class,units,work,latency_s\n")
+        for r in rows:
+            f.write(f"{r[0]},{r[1]},{r[2]},{r[3]},{r[4]:.9g}\n")
+    print(f"wrote {len(rows)} rows to {args.out}")
+
+
+if __name__ == "__main__":
+    main()
