@@ -91,6 +91,41 @@ nf_status validate_batch(const nf_model_cfg* c, const nf_batch* b) {
   return NF_OK;
 }
 
+// Balanced request -> nano-batch assignment (reading A-10b): prefill
+// chunks by tokens (largest first, to the nano-batch with the most remaining
+// token share), then decode requests by KV length (longest first, to the
+// nano-batch with the least accumulated attention work).
+void balance_requests(const nf_batch* b, int nn, const int32_t* share, std::vector<std::vector<int>>* groups) {
+  const int n_req = b->n_req;
+  int64_t T = batch_tokens(b), tot = 0;
+  for (int k = 0; k < nn; ++k) tot += share[k];
+  std::vector<double> cap(nn), kv(nn, 0.0);
+  for (int k = 0; k < nn; ++k) cap[k] = (double)T * share[k] / tot;
+  std::vector<std::vector<int>>& grp = *groups;
+  grp.assign(nn, {});
+  std::vector<int> pre, dec;
+  for (int r = 0; r < n_req; ++r) (b->q_len[r] > 1 ? pre : dec).push_back(r);
+  std::stable_sort(pre.begin(), pre.end(), [&](int x, int y) { return b->q_len[x] > b->q_len[y]; });
+  std::stable_sort(dec.begin(), dec.end(), [&](int x, int y) { return b->kv_prefix[x] > b->kv_prefix[y]; });
+  for (int r : pre) {
+    int best = 0;
+    for (int k = 1; k < nn; ++k)
+      if (cap[k] > cap[best]) best = k;
+    grp[best].push_back(r);
+    cap[best] -= b->q_len[r];
+    kv[best] += (double)b->q_len[r] * (b->kv_prefix[r] + b->q_len[r] / 2.0) / 64.0;
+  }
+  for (int r : dec) {
+    int best = 0;
+    for (int k = 1; k < nn; ++k)
+      if (kv[k] < kv[best]) best = k;
+    grp[best].push_back(r);
+    cap[best] -= 1;
+    kv[best] += b->kv_prefix[r] + 1;
+  }
+  for (auto& g : grp) std::sort(g.begin(), g.end());
+}
+
 std::vector<int> snap_cuts_impl(const std::vector<int64_t>& bound, int n_nano, const int32_t* share) {
   // bound[b] = token offset of request boundary b (b = 0..n_req); reading A-10
   const int n_req = (int)bound.size() - 1;
@@ -462,37 +497,11 @@ void plan_order(const nf_plan* p, const nf_batch* b, bool allow_balance, std::ve
     *cuts = snap_cuts_impl(bound, nn, p->spec.share);
     return;
   }
-  // Balanced assignment: prefill chunks by tokens (largest first to the nano
-  // with most remaining token share), decode requests by KV length (LPT).
-  int64_t T = batch_tokens(b), tot = 0;
-  for (int k = 0; k < nn; ++k) tot += p->spec.share[k];
-  std::vector<double> cap(nn), kv(nn, 0.0);
-  for (int k = 0; k < nn; ++k) cap[k] = (double)T * p->spec.share[k] / tot;
-  std::vector<std::vector<int>> grp(nn);
-  std::vector<int> pre, dec;
-  for (int r = 0; r < n_req; ++r) (b->q_len[r] > 1 ? pre : dec).push_back(r);
-  std::stable_sort(pre.begin(), pre.end(), [&](int x, int y) { return b->q_len[x] > b->q_len[y]; });
-  std::stable_sort(dec.begin(), dec.end(), [&](int x, int y) { return b->kv_prefix[x] > b->kv_prefix[y]; });
-  for (int r : pre) {
-    int best = 0;
-    for (int k = 1; k < nn; ++k)
-      if (cap[k] > cap[best]) best = k;
-    grp[best].push_back(r);
-    cap[best] -= b->q_len[r];
-    kv[best] += (double)b->q_len[r] * (b->kv_prefix[r] + b->q_len[r] / 2.0) / 64.0;  // prefill attention, rough
-  }
-  for (int r : dec) {
-    int best = 0;
-    for (int k = 1; k < nn; ++k)
-      if (kv[k] < kv[best]) best = k;
-    grp[best].push_back(r);
-    cap[best] -= 1;
-    kv[best] += b->kv_prefix[r] + 1;
-  }
+  std::vector<std::vector<int>> grp;
+  balance_requests(b, nn, p->spec.share, &grp);
   order->clear();
   cuts->assign(1, 0);
   for (int k = 0; k < nn; ++k) {
-    std::sort(grp[k].begin(), grp[k].end());
     for (int r : grp[k]) order->push_back(r);
     cuts->push_back((int)order->size());
   }

@@ -51,6 +51,7 @@ size_t meta_words_bound(const nf_model_cfg* c, const nf_batch* b);
 // order: internal request order (size n_req); req_cuts: nano-batch boundaries in that order.
 void build_meta(const nf_model_cfg* c, const nf_batch* b, const std::vector<int>& order, const std::vector<int>& req_cuts,
                 StepMeta* m);
+void balance_requests(const nf_batch* b, int nn, const int32_t* share, std::vector<std::vector<int>>* groups);
 std::vector<int> snap_cuts_impl(const std::vector<int64_t>& row_start_of_boundary, int n_nano, const int32_t* share);
 
 struct Workspace {

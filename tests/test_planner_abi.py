@@ -1,0 +1,75 @@
+"""nf_plan_create (C++ autosearch in libnf) against the oracle planner
+(oracle/planner.py) on the same curves and batch: identical split, SM units
+and schedule.  Host-only: runs on CPU."""
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import planner as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def nf():
+    from paper_2408_12757_b200 import build
+    build.build()
+    from paper_2408_12757_b200 import nf as _nf
+    return _nf
+
+
+def load_curves(path):
+    rows = [l.split(",") for l in open(path).read().splitlines()[1:] if l.strip()]
+    return [(int(k), int(u), float(w), float(t)) for k, _, u, w, t in rows]
+
+
+def synthetic_curves():
+    pts = []
+    for k in range(6):
+        a = 0.9 if k != P.DECODE else 0.55
+        scale = {P.KQV: 1.5e-6, P.O: 1.1e-6, P.UG: 5.5e-6, P.DOWN: 3.2e-6, P.PREFILL: 1.7e-10, P.DECODE: 6.5e-10}[k]
+        for u in (8, 16, 32, 48, 64, 96, 128, 148):
+            for w in (512.0, 2048.0, 1e5, 1e6):
+                pts.append((k, u, w, scale * w * (148 / u) ** a))
+    return pts
+
+
+@pytest.mark.parametrize("which", ["synthetic", "measured"])
+def test_autosearch_matches_oracle(nf, which):
+    from paper_2408_12757_b200.runtime import cfg_from_shape
+    pts = synthetic_curves() if which == "synthetic" else load_curves(os.path.join(ROOT, "profiles", "curves_b200_quick.csv"))
+    rng = np.random.default_rng(4)
+    q_len = [1] * 60 + [96, 40]
+    prefix = list(rng.integers(500, 1500, 60)) + [0, 300]
+    b = synth.make_batch(q_len, prefix, seed=2)
+    cfg = cfg_from_shape(synth.SHAPES["llama3-8b"])
+    iters = 40
+    best, table = P.search(q_len, prefix, P.Curves(pts), budget=148, q=8, max_iters=iters, n_layers=3)
+    plan = nf.Plan.search(cfg, nf.Batch.from_any(b), pts, sm_budget=148, sm_quantum=8, mode=nf.OVERLAP, n_nano=2,
+                          max_iters=iters)
+    spec = plan.spec()
+    assert [spec.share[0], spec.share[1]] == best[0]
+    kinds = sorted({n.kind for n in best[3]})
+    assert [spec.sm[k] for k in kinds] == [best[1][k] for k in kinds]
+    csv = [l.split(",") for l in plan.csv().splitlines()[1:]]
+    assert len(csv) == len(best[3])
+    for row, n in zip(csv, best[3]):
+        assert int(row[2]) == n.nano
+        assert float(row[4]) == pytest.approx(best[4][n.id], rel=1e-7, abs=1e-12)
+        assert float(row[5]) == pytest.approx(best[5][n.id], rel=1e-7, abs=1e-12)
+    assert max(float(r[5]) for r in csv) == pytest.approx(best[2], rel=1e-9)
+
+
+def test_autosearch_errors_and_sequential(nf):
+    from paper_2408_12757_b200.runtime import cfg_from_shape
+    cfg = cfg_from_shape(synth.SHAPES["llama3-8b"])
+    b = nf.Batch.from_any(synth.make_batch([1, 1, 30], [100, 7, 0]))
+    with pytest.raises(nf.NFError) as e:   # decode attention has work but no curve
+        nf.Plan.search(cfg, b, [(0, 148, 512.0, 1e-4)], mode=nf.OVERLAP)
+    assert e.value.status == nf.NF_EINVAL
+    with pytest.raises(nf.NFError):
+        nf.Plan.search(cfg, b, [], sm_budget=0)
+    p = nf.Plan.search(cfg, b, [], mode=nf.SEQUENTIAL)
+    assert p.spec().n_nano == 1 and list(p.spec().sm) == [148] * 7
