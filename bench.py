@@ -186,11 +186,18 @@ def run_nf(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    shape = synth.SHAPES["llama3-8b"]
+    if args.config == "c3rank":
+        # rank-local proxy of configs[2] (70B TP8): one rank's head/FFN shards, no collectives
+        shape = synth.shape_with(synth.SHAPES["llama2-70b"], name="llama2-70b-tp8-rank", n_q_heads=8, n_kv_heads=1,
+                                 d_ffn=28672 // 8)
+        p_in, d_out = 512, 1024
+    else:
+        shape = synth.SHAPES["llama3-8b"]
+        p_in, d_out = 1024, 512
     if args.layers:
         shape = synth.shape_with(shape, n_layers=args.layers)
     L = shape.n_layers
-    b = synth.workload_batch(2048, 1024, 512)
+    b = synth.workload_batch(2048, p_in, d_out)
     T = b.n_tokens
     nb = nf.Batch.from_any(b)
     cfg = rt.cfg_from_shape(shape)
@@ -222,7 +229,11 @@ def run_nf(args, rank, world, local_rank):
 
     sm = [int(x) for x in args.sm.split(",")] if args.sm else None
     if args.mode == "overlap":
-        if args.colocate:
+        if args.plan == "auto":
+            rows = [l.split(",") for l in open(os.path.join(ROOT, args.curves)).read().splitlines()[1:] if l.strip()]
+            pts = [(int(k), int(u), float(w), float(t)) for k, _, u, w, t in rows]
+            plan = nf.Plan.search(cfg, nb, pts, mode=nf.OVERLAP, n_nano=2)
+        elif args.colocate:
             plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=sm or [148] * 7, balance=True,
                                     colocate=True)
         else:
@@ -351,11 +362,16 @@ def run_nf(args, rank, world, local_rank):
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, seeded torch RNG on device)",
-            "config": {"workload": f"configs[1]: LLaMA-3-8B-shape {L}-layer serving step, B_dense 2048 "
-                                   f"(683 decode ctx 1024-1535 + 341-token chunk + 1024-token prompt), page 16",
+            "config": {"workload": (f"configs[1]: LLaMA-3-8B-shape {L}-layer serving step, B_dense 2048 "
+                                    f"(683 decode ctx 1024-1535 + 341-token chunk + 1024-token prompt), page 16")
+                       if args.config == "c2" else
+                       (f"configs[2] rank-local proxy: one LLaMA-2-70B TP8 rank's shards (D 8192, 8/1 heads, "
+                        f"F 3584), {L} layers, B_dense 2048 (1365 decode ctx 512-1535 + 171 chunk + 512 prompt), "
+                        f"no collectives"),
                        "b_dense": T, "n_layers": L, "mode": args.mode, "colocate": bool(plan.spec().colocate),
                        "parallelism": "replicas" if world > 1 else "single-gpu",
-                       "plan_sm": list(plan.spec().sm), "l2": "no flush: per-step inputs (KV 115 GB) >> 126 MB L2"},
+                       "plan_sm": list(plan.spec().sm), "plan_shares": list(plan.spec().share)[:plan.spec().n_nano],
+                       "plan": args.plan, "l2": "no flush: per-step inputs (KV 115 GB) >> 126 MB L2"},
             "tokens_per_s_per_gpu": value / world,
             "pct_of_optimal": 100.0 * (value / world) / optimal,
             "optimal_tokens_per_s_per_gpu": optimal,
@@ -382,8 +398,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="nf", choices=["nf", "reference"])
     ap.add_argument("--mode", default="overlap", choices=["overlap", "nano", "sequential"])
+    ap.add_argument("--plan", default="explicit", choices=["explicit", "auto"],
+                    help="auto: nf_plan_create autosearch over --curves (overlap mode)")
+    ap.add_argument("--curves", default="profiles/curves_b200_quick.csv")
     ap.add_argument("--colocate", action="store_true", help="attention CTAs co-resident with GEMM CTAs")
     ap.add_argument("--sm", default="", help="comma-separated SM budget per op kind (7 values)")
+    ap.add_argument("--config", default="c2", choices=["c2", "c3rank"])
     ap.add_argument("--layers", type=int, default=0, help="(dev only) override layer count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--timeline", default="", help="write one step's kernel spans (CSV) to this path")

@@ -198,9 +198,13 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
 
 /* ------------------------------------------------------------------ op-level entry points (tests, profiling) */
 /* C[M, N] = A[M, K] . B[N, K]^T, bf16 in/out, f32 accumulation (tcgen05).
- * Leading dimensions in elements, multiples of 8; N % 32 == 0. */
+ * Leading dimensions in elements, multiples of 8; N % 32 == 0.  ws (device,
+ * 256-byte aligned, >= nf_gemm_workspace_bytes(M, N)) enables the stream-K
+ * tail schedule; ws == NULL runs whole tiles only.  The fp32 summation order
+ * depends on the grid (SM budget) when stream-K is active. */
 nf_status nf_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t M,
-                       int32_t N, int32_t K, int32_t sm_budget, void* stream);
+                       int32_t N, int32_t K, int32_t sm_budget, void* ws, size_t ws_bytes, void* stream);
+size_t nf_gemm_workspace_bytes(int32_t M, int32_t N);
 /* Paged causal GQA attention of PAPER.md:161 for every token of the batch:
  * q [T, qh, hd] (post-RoPE), kv_pool already holding this step's K/V,
  * o [T, qh*hd].  Decode tokens (q_len == 1) run on the decode kernel with

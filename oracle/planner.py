@@ -250,11 +250,12 @@ def nano_work(q_len, kv_prefix, groups):
 
 def build_pipeline(work: List[Tuple[int, int, int]], n_layers: int = 3) -> List[Node]:
     """The executor's OVERLAP schedule as a DAG (PAPER.md:691 single-GPU
-    pipeline; api.cu nf_model_step): per nano k, KQV_k(l) -> PREFILL_k(l) ->
-    DECODE_k(l) (memory stream) -> O_k(l) -> UG_k(l) -> DOWN_k(l) ->
-    KQV_k(l+1) (compute stream).  Stream order adds edges: the compute stream
-    runs [O UG DOWN KQV(next)] nano by nano, the memory stream the attention
-    of nano 0, 1, ... in issue order."""
+    pipeline; api.cu nf_model_step): per nano k, KQV_k(l) -> DECODE_k(l)
+    (memory stream) and KQV_k(l) -> PREFILL_k(l) (compute stream, reading
+    A-11); O_k(l) waits for both, then UG_k(l) -> DOWN_k(l) -> KQV_k(l+1).
+    Stream order adds edges: the compute stream runs
+    [O UG DOWN KQV(next) PREFILL(next)] nano by nano, the memory stream the
+    decode attention of nano 0, 1, ... in issue order."""
     nodes: List[Node] = []
 
     def add(kind, nano, w, deps):
@@ -264,26 +265,23 @@ def build_pipeline(work: List[Tuple[int, int, int]], n_layers: int = 3) -> List[
     K = len(work)
     last_compute = None
     last_memory = None
-    kqv = [None] * K
-    for k in range(K):  # prologue: KQV of layer 0 for every nano
-        kqv[k] = add(KQV, k, work[k][0], [last_compute])
-        last_compute = kqv[k]
-    att = [None] * K
+    dec = [None] * K
+    for k in range(K):  # prologue: KQV (+ prefill) of layer 0 for every nano
+        kq = add(KQV, k, work[k][0], [last_compute])
+        dec[k] = add(DECODE, k, work[k][1], [kq, last_memory])
+        last_memory = dec[k]
+        last_compute = add(PREFILL, k, work[k][2], [kq])
     for l in range(n_layers):
         for k in range(K):
-            pf = add(PREFILL, k, work[k][2], [kqv[k], last_memory])
-            dc = add(DECODE, k, work[k][1], [pf])
-            last_memory = dc
-            att[k] = dc
-        for k in range(K):
-            o = add(O, k, work[k][0], [att[k], last_compute])
+            o = add(O, k, work[k][0], [dec[k], last_compute])
             ug = add(UG, k, work[k][0], [o])
             dn = add(DOWN, k, work[k][0], [ug])
             last_compute = dn
             if l + 1 < n_layers:
-                kqv[k] = add(KQV, k, work[k][0], [dn])
-                last_compute = kqv[k]
-        # the next layer's attention of nano k is added at the top of the loop
+                kq = add(KQV, k, work[k][0], [dn])
+                dec[k] = add(DECODE, k, work[k][1], [kq, last_memory])
+                last_memory = dec[k]
+                last_compute = add(PREFILL, k, work[k][2], [kq])
     return nodes
 
 

@@ -254,7 +254,7 @@ Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base) 
   const int64_t T = batch_tokens(b);
   const int N = c->tp_size;
   const int64_t qd = (int64_t)c->n_q_heads / N * c->head_dim, D = c->d_model, F = c->d_ffn / N;
-  const int64_t NP = D / GEMM_BN;
+  const int64_t NP = D / GEMM_NORM_COLS;
   const int64_t VT = (c->vocab + GEMM_BN - 1) / GEMM_BN;
   const int64_t R = b->n_req;
   Workspace w{};
@@ -281,6 +281,12 @@ Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base) 
   w.am_val = (float*)take(VT * R * 4);
   w.am_idx = (int*)take(VT * R * 4);
   w.red = N > 1 ? (float*)take(T * D * 4) : nullptr;
+  w.sk_part = (float*)take((size_t)148 * GEMM_BM * GEMM_BN * 4);
+  const int64_t maxN = std::max<int64_t>({(int64_t)(c->n_q_heads + 2 * c->n_kv_heads) / N * c->head_dim, D,
+                                          ((F + 127) / 128) * 256});
+  w.sk_flag_n = (int)(((T + GEMM_BM - 1) / GEMM_BM) * ((maxN + 127) / 128) +
+                      ((R + GEMM_BM - 1) / GEMM_BM) * VT + 64);
+  w.sk_flag = (int*)take((size_t)w.sk_flag_n * 4);
   w.total = off;
   return w;
 }
@@ -541,6 +547,8 @@ nf_status run_kqv(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x
   if (M <= 0) return NF_OK;
   GemmArgs a{};
   a.epi = EPI_QKV;
+  a.sk_part = L.w->sk_part;
+  a.sk_flag = L.w->sk_flag;
   a.stages = L.p->spec.colocate ? 3 : 4;
   a.M = M;
   a.N = (c->n_q_heads + 2 * c->n_kv_heads) / N * c->head_dim;
@@ -566,7 +574,7 @@ nf_status run_kqv(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x
   return NF_OK;
 }
 
-nf_status run_attn(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
+AttnArgs attn_args(const LayerCtx& L) {
   const nf_model_cfg* c = L.c;
   AttnArgs a{};
   a.q = L.w->q;
@@ -578,20 +586,39 @@ nf_status run_attn(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
   a.page_size = c->page_size;
   a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
   a.dec_warps = L.p->spec.colocate ? 4 : 8;
-  const DecodeItem* dec = reinterpret_cast<const DecodeItem*>(L.meta_dev + L.m->off_dec) + nr.dec_off;
+  return a;
+}
+
+// Prefill attention of one nano-batch: compute-bound, so it runs on the compute
+// stream right after the nano-batch's KQV (reading A-11), within the GEMMs' SM
+// budget; its small multi-CTA-per-SM grid must not spill onto the memory partition.
+nf_status run_prefill(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
+  if (nr.pf_n <= 0) return NF_OK;
+  const AttnArgs a = attn_args(L);
   const PrefillItem* pf = reinterpret_cast<const PrefillItem*>(L.meta_dev + L.m->off_pf) + nr.pf_off;
-  if (nr.pf_n > 0) {
-    ProfScope ps(NF_OP_PREFILL_ATTN, st);
-    NF_CUDA(launch_prefill_attention(L.pool_map, a, pf, nr.pf_n, clampsm(L.p->spec.sm[NF_OP_PREFILL_ATTN]), st));
-  }
-  if (nr.dec_n > 0) {
-    ProfScope ps(NF_OP_DECODE_ATTN, st);
-    if (use_tc_decode(c, L.p))
-      NF_CUDA(launch_decode_attention_tc(L.pool_map, a, dec, nr.dec_n, clampsm(L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
-    else
-      NF_CUDA(launch_decode_attention(L.pool_map, L.page_map, a, dec, nr.dec_n, clampsm(L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
-  }
+  ProfScope ps(NF_OP_PREFILL_ATTN, st);
+  NF_CUDA(launch_prefill_attention(L.pool_map, a, pf, nr.pf_n, clampsm(L.p->spec.sm[NF_OP_PREFILL_ATTN]), st));
   return NF_OK;
+}
+
+// Decode attention of one nano-batch: HBM-bound, on the memory stream in OVERLAP mode.
+nf_status run_decode(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
+  if (nr.dec_n <= 0) return NF_OK;
+  const nf_model_cfg* c = L.c;
+  const AttnArgs a = attn_args(L);
+  const DecodeItem* dec = reinterpret_cast<const DecodeItem*>(L.meta_dev + L.m->off_dec) + nr.dec_off;
+  ProfScope ps(NF_OP_DECODE_ATTN, st);
+  if (use_tc_decode(c, L.p))
+    NF_CUDA(launch_decode_attention_tc(L.pool_map, a, dec, nr.dec_n, clampsm(L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
+  else
+    NF_CUDA(launch_decode_attention(L.pool_map, L.page_map, a, dec, nr.dec_n,
+                                    clampsm(L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
+  return NF_OK;
+}
+
+nf_status run_attn(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
+  NF_TRY(run_prefill(L, nr, st));
+  return run_decode(L, nr, st);
 }
 
 // O + residual, RMS(FFN) fold, Up/Gate + SiLU, Down + residual for one nano-batch (TP1).
@@ -602,10 +629,12 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   if (M <= 0) return NF_OK;
   const int64_t D = c->d_model, F = c->d_ffn, qd = (int64_t)c->n_q_heads * c->head_dim;
   const int T = L.m->T;
-  const int NP = (int)(D / GEMM_BN);
+  const int NP = (int)(D / GEMM_NORM_COLS);
   // O projection + residual: h1 = x + o W_o^T, with sum-of-squares partials of h1
   GemmArgs a{};
   a.epi = EPI_RESID;
+  a.sk_part = L.w->sk_part;
+  a.sk_flag = L.w->sk_flag;
   a.stages = L.p->spec.colocate ? 3 : 4;
   a.M = M;
   a.N = (int)D;
@@ -624,6 +653,8 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   // Up/Gate + SiLU(gate) * up, RMSNorm(h1) folded as a row scale
   GemmArgs u{};
   u.epi = EPI_SILU;
+  u.sk_part = L.w->sk_part;
+  u.sk_flag = L.w->sk_flag;
   u.stages = L.p->spec.colocate ? 3 : 4;
   u.M = M;
   u.N = (int)(((F + 127) / 128) * 256);
@@ -644,6 +675,8 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   // Down + residual: x_out = h1 + m W_d^T, partials of x_out for the next layer's norm
   GemmArgs d{};
   d.epi = EPI_RESID;
+  d.sk_part = L.w->sk_part;
+  d.sk_flag = L.w->sk_flag;
   d.stages = L.p->spec.colocate ? 3 : 4;
   d.M = M;
   d.N = (int)D;
@@ -686,8 +719,9 @@ nf_status run_layer(nf_plan* p, const LayerCtx& L, const nf_packed_layer* wt, vo
     if (!kqv_done) NF_TRY(run_kqv(L, nanos[k], x, part, nparts, wt, pool));
     NF_CUDA(cudaEventRecord(p->ev_kqv[k], L.cs));
     NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
-    NF_TRY(run_attn(L, nanos[k], L.ms));
+    NF_TRY(run_decode(L, nanos[k], L.ms));
     NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
+    NF_TRY(run_prefill(L, nanos[k], L.cs));
   }
   for (size_t k = 0; k < nanos.size(); ++k) {
     NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_att[k], 0));
@@ -718,6 +752,7 @@ nf_status nf_layer_forward(const nf_plan* plan, nf_comm* comm, const nf_packed_l
   build_meta(c, b, order, cuts, &m);
   cudaStream_t cs = (cudaStream_t)stream;
   NF_TRY(upload_meta(p, m, wsp.meta, cs));
+  NF_CUDA(cudaMemsetAsync(wsp.sk_flag, 0, (size_t)wsp.sk_flag_n * 4, cs));
   LayerCtx L{};
   L.p = p;
   L.c = c;
@@ -756,8 +791,9 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
   build_meta(c, b, order, cuts, &m);
   cudaStream_t cs = (cudaStream_t)stream;
   NF_TRY(upload_meta(p, m, wsp.meta, cs));
+  NF_CUDA(cudaMemsetAsync(wsp.sk_flag, 0, (size_t)wsp.sk_flag_n * 4, cs));
   const int D = c->d_model;
-  const int NP = D / GEMM_BN;
+  const int NP = D / GEMM_NORM_COLS;
   // token ids in internal row order: gather ids then embedding rows (+ RMS partials, one part)
   // tok_src maps internal row -> caller row; ids are gathered on the fly by the embedding gather.
   NF_CUDA(launch_gather_ids_embed((const __nv_bfloat16*)w->embed, token_ids, wsp.meta + m.off_tok_src, m.T, D, wsp.xa,
@@ -801,8 +837,9 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
       NF_TRY(run_kqv(L, nanos[k], x, px, 1, &w->layers[0], kv_pools[0]));
       NF_CUDA(cudaEventRecord(p->ev_kqv[k], cs));
       NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
-      NF_TRY(run_attn(L, nanos[k], L.ms));
+      NF_TRY(run_decode(L, nanos[k], L.ms));
       NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
+      NF_TRY(run_prefill(L, nanos[k], cs));
     }
     for (int l = 0; l < c->n_layers; ++l) {
       for (size_t k = 0; k < nanos.size(); ++k) {
@@ -814,8 +851,9 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
           NF_TRY(run_kqv(L, nanos[k], y, py, NP, &w->layers[l + 1], kv_pools[l + 1]));
           NF_CUDA(cudaEventRecord(p->ev_kqv[k], cs));
           NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
-          NF_TRY(run_attn(L, nanos[k], L.ms));
+          NF_TRY(run_decode(L, nanos[k], L.ms));
           NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
+          NF_TRY(run_prefill(L, nanos[k], cs));
         }
       }
       std::swap(x, y);
@@ -829,6 +867,8 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
     NF_CUDA(launch_gather_rows(x, erow, m.n_emit, D, wsp.lm_rows, wsp.lm_part, cs));
     GemmArgs a{};
     a.epi = EPI_ARGMAX;
+    a.sk_part = (&wsp)->sk_part;
+    a.sk_flag = (&wsp)->sk_flag;
     a.M = m.n_emit;
     a.N = c->vocab;
     a.K = D;
@@ -849,7 +889,7 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
 
 // ------------------------------------------------------------------ op-level entry points
 nf_status nf_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t M,
-                       int32_t N, int32_t K, int32_t sm_budget, void* stream) {
+                       int32_t N, int32_t K, int32_t sm_budget, void* ws, size_t ws_bytes, void* stream) {
   if (!A || !B || !C) return set_error(NF_EINVAL, "NULL pointer");
   if (M < 0 || N <= 0 || K <= 0) return set_error(NF_EINVAL, "bad shape M=%d N=%d K=%d", M, N, K);
   if (N % 32) return set_error(NF_EINVAL, "N must be a multiple of 32");
@@ -863,9 +903,22 @@ nf_status nf_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, v
   a.n_valid = N;
   a.out = (__nv_bfloat16*)C;
   a.ldo = ldc;
-  NF_CUDA(launch_gemm((const __nv_bfloat16*)A, lda, (const __nv_bfloat16*)B, ldb, a,
-                      std::max(1, std::min<int>(sm_budget, num_sms())), (cudaStream_t)stream));
+  const int grid_max = std::max(1, std::min<int>(sm_budget, num_sms()));
+  const int tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + 127) / 128);
+  if (ws) {
+    if (ws_bytes < gemm_sk_bytes(148, tiles)) return set_error(NF_EINVAL, "gemm workspace too small");
+    if ((uintptr_t)ws & 255) return set_error(NF_EINVAL, "gemm workspace must be 256-byte aligned");
+    a.sk_part = (float*)ws;
+    a.sk_flag = (int*)((char*)ws + (size_t)148 * GEMM_BM * GEMM_BN * 4);
+    NF_CUDA(cudaMemsetAsync(a.sk_flag, 0, (size_t)tiles * 4, (cudaStream_t)stream));
+  }
+  NF_CUDA(launch_gemm((const __nv_bfloat16*)A, lda, (const __nv_bfloat16*)B, ldb, a, grid_max, (cudaStream_t)stream));
   return NF_OK;
+}
+
+size_t nf_gemm_workspace_bytes(int32_t M, int32_t N) {
+  const int tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + 127) / 128);
+  return gemm_sk_bytes(148, tiles);
 }
 
 nf_status nf_attention(const nf_model_cfg* cfg, const nf_batch* b, const void* q, const void* kv_pool, void* o, void* ws,

@@ -22,8 +22,6 @@ namespace nf {
 namespace {
 
 constexpr int A_STAGE_ELEMS = GEMM_BM * GEMM_BK;
-constexpr int B_STAGE_ELEMS = GEMM_BN * GEMM_BK;
-constexpr uint32_t STAGE_BYTES = (A_STAGE_ELEMS + B_STAGE_ELEMS) * 2;
 
 NF_DEV void store32_bf16(__nv_bfloat16* dst, const float (&v)[32]) {
   uint4* d = reinterpret_cast<uint4*>(dst);
@@ -49,13 +47,13 @@ NF_DEV void load32_bf16(const __nv_bfloat16* src, float (&v)[32]) {
   }
 }
 
-NF_DEV void ld32f(uint32_t taddr, float s, float (&v)[32]) {
-  uint32_t r[32];
-  tmem_ld32(taddr, r);
-  tmem_ld_wait();
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * s;
+NF_DEV int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
+NF_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 
 // sin/cos of a large fp32 angle: Cody-Waite reduction to [-pi, pi] then SFU.
 NF_DEV void sincos_reduced(float a, float* s, float* c) {
@@ -65,10 +63,13 @@ NF_DEV void sincos_reduced(float a, float* s, float* c) {
   __sincosf(r, s, c);
 }
 
-template <int GEMM_STAGES>
+template <int GEMM_STAGES, int BN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ GemmArgs args) {
+  constexpr int B_STAGE_ELEMS = BN * GEMM_BK;
+  constexpr uint32_t STAGE_BYTES = (A_STAGE_ELEMS + B_STAGE_ELEMS) * 2;
+  constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator stages
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __nv_bfloat16* sA = reinterpret_cast<__nv_bfloat16*>(smem);
@@ -83,9 +84,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = args.M, N = args.N, K = args.K;
   const int tiles_m = (M + GEMM_BM - 1) / GEMM_BM;
-  const int tiles_n = (N + GEMM_BN - 1) / GEMM_BN;
+  const int tiles_n = (N + BN - 1) / BN;
   const int tiles = tiles_m * tiles_n;
   const int num_kb = (K + GEMM_BK - 1) / GEMM_BK;
+  // Hybrid stream-K schedule: whole tiles data-parallel for all but the last
+  // (partial) wave, then the remaining tiles' k-iterations split evenly over
+  // the G CTAs.  A CTA whose range starts inside a tile computes that tile's
+  // tail first and writes an fp32 partial; the CTA holding the tile's first
+  // iterations (the end of its range) adds the partials in CTA order and runs
+  // the fused epilogue -- no CTA ever waits on a lower one (no serial chain).
+  const int G = gridDim.x;
+  const bool sk = args.sk_part != nullptr && (tiles % G) != 0;
+  const int tiles_dp = sk ? max(0, tiles / G - 1) * G : tiles;
+  const int64_t total_sk = (int64_t)(tiles - tiles_dp) * num_kb;
+  auto for_each_seg = [&](auto&& fn) {
+    for (int t = blockIdx.x; t < tiles_dp; t += G) fn(t, 0, num_kb);
+    if (total_sk > 0) {
+      int64_t i = (int64_t)blockIdx.x * total_sk / G;
+      const int64_t e = (int64_t)(blockIdx.x + 1) * total_sk / G;
+      while (i < e) {
+        const int t = (int)(i / num_kb), kb0 = (int)(i % num_kb);
+        const int kb1 = (int)min((int64_t)num_kb, kb0 + (e - i));
+        fn(tiles_dp + t, kb0, kb1);
+        i += kb1 - kb0;
+      }
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -100,7 +124,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
   if (args.epi == EPI_QKV && warp >= 4) {
     const int i = threadIdx.x - 128;
     if (i < args.hd / 2) inv_freq[i] = (float)exp2(-(2.0 * i / args.hd) * (double)args.log2_theta);
@@ -116,71 +140,128 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint64_t a_policy = policy_evict_last();  // activations are re-read by every n-tile
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for_each_seg([&](int tile, int kb0, int kb1) {
         const int mb = tile % tiles_m, nb = tile / tiles_m;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
           tma_load_2d_hint(sA + stage * A_STAGE_ELEMS, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM, a_policy);
-          tma_load_2d(sB + stage * B_STAGE_ELEMS, &tmB, &full[stage], kb * GEMM_BK, nb * GEMM_BN);
+          tma_load_2d(sB + stage * B_STAGE_ELEMS, &tmB, &full[stage], kb * GEMM_BK, nb * BN);
           if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
         }
-      }
+      });
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, GEMM_BN);
+      constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int as = 0;
       uint32_t aphase = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for_each_seg([&](int tile, int kb0, int kb1) {
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + as * GEMM_BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const uint32_t d = tmem_base + as * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(sA + stage * A_STAGE_ELEMS);
           const uint64_t bd = sdesc_sw128(sB + stage * B_STAGE_ELEMS);
 #pragma unroll
           for (int k = 0; k < GEMM_BK / 16; ++k)
-            umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           umma_commit(&empty[stage]);
           if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
         }
         umma_commit(&tfull[as]);
         as ^= 1;
         if (as == 0) aphase ^= 1;
-      }
+      });
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
     const int ew = warp - 4;
     int as = 0;
     uint32_t aphase = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int trow = ew * 32 + lane;  // row within the tile
+    for_each_seg([&](int tile, int kb0, int kb1) {
       const int mb = tile % tiles_m, nb = tile / tiles_m;
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
-      const int r = mb * GEMM_BM + ew * 32 + lane;
+      const int r = mb * GEMM_BM + trow;
       const bool valid = r < M;
-      const uint32_t taddr = tmem_base + as * GEMM_BN + ((uint32_t)(ew * 32) << 16);
+      const uint32_t taddr = tmem_base + as * BN + ((uint32_t)(ew * 32) << 16);
+      if (kb0 > 0) {
+        // stream-K contributor (tile tail, processed first in this CTA's range):
+        // raw fp32 partial tile to this CTA's slot, then signal the tile's owner
+        float* slot = args.sk_part + ((size_t)blockIdx.x * GEMM_BM + trow) * GEMM_SK_LD;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t rr[32];
+          tmem_ld32(taddr + c * 32, rr);
+          tmem_ld_wait();
+          float4* d = reinterpret_cast<float4*>(slot + c * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            d[q] = make_float4(__uint_as_float(rr[4 * q]), __uint_as_float(rr[4 * q + 1]),
+                               __uint_as_float(rr[4 * q + 2]), __uint_as_float(rr[4 * q + 3]));
+        }
+        __threadfence();
+        tc_fence_before();
+        named_bar_sync(1, 128);
+        if (trow == 0) atomicAdd(args.sk_flag + tile, 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[as]);
+        as ^= 1;
+        if (as == 0) aphase ^= 1;
+        return;
+      }
+      // owner: this CTA holds the tile's first k-iterations (processed last in its
+      // range); the tail iterations were done by the next CTAs, which run them first
+      int c_first = blockIdx.x + 1, n_contrib = 0;
+      if (kb1 < num_kb) {
+        const int64_t last = (int64_t)(tile - tiles_dp) * num_kb + num_kb - 1;
+        n_contrib = (int)(((last + 1) * G - 1) / total_sk) - (int)blockIdx.x;
+        if (trow == 0) {
+          while (ld_acquire_gpu(args.sk_flag + tile) < n_contrib) __nanosleep(32);
+          args.sk_flag[tile] = 0;  // self-reset for the next launch
+        }
+        named_bar_sync(1, 128);
+        (void)ld_acquire_gpu(args.sk_flag + tile);
+      }
+      // accumulator + contributors' partials (fixed CTA order), times the row scale
+      auto ldacc = [&](int col, float sc, float (&v)[32]) {
+        uint32_t rr[32];
+        tmem_ld32(taddr + col, rr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
+        for (int c = c_first; c < c_first + n_contrib; ++c) {
+          const float4* src = reinterpret_cast<const float4*>(args.sk_part + ((size_t)c * GEMM_BM + trow) * GEMM_SK_LD + col);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 f = src[q];
+            v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= sc;
+      };
       float s = 1.f;
       if (args.norm_part != nullptr && valid) {
         float acc = 0.f;
         for (int p = 0; p < args.norm_nparts; ++p) acc += args.norm_part[(int64_t)p * args.norm_stride + r];
         s = rsqrtf(acc * args.inv_d + args.eps);
       }
-      const int n0 = nb * GEMM_BN;
+      const int n0 = nb * BN;
       float v[32];
       switch (args.epi) {
         case EPI_STORE:
         case EPI_F32: {
 #pragma unroll 1
-          for (int c = 0; c < GEMM_BN / 32; ++c) {
-            ld32f(taddr + c * 32, s, v);
+          for (int c = 0; c < BN / 32; ++c) {
+            ldacc(c * 32, s, v);
             const int col = n0 + c * 32;
             if (valid && col < N) {
               if (args.epi == EPI_STORE) {
@@ -195,10 +276,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           break;
         }
         case EPI_RESID: {
+          // sum-of-squares partials in 128-column units (independent of the tile width)
           float sq = 0.f;
 #pragma unroll 1
-          for (int c = 0; c < GEMM_BN / 32; ++c) {
-            ld32f(taddr + c * 32, s, v);
+          for (int c = 0; c < BN / 32; ++c) {
+            ldacc(c * 32, s, v);
             const int col = n0 + c * 32;
             if (valid && col < N) {
               float rr[32];
@@ -210,16 +292,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               }
               store32_bf16(args.out + (int64_t)r * args.ldo + col, v);
             }
+            if ((c & 3) == 3) {
+              if (args.sq_out != nullptr && valid) args.sq_out[(int64_t)((n0 >> 7) + (c >> 2)) * args.sq_stride + r] = sq;
+              sq = 0.f;
+            }
           }
-          if (args.sq_out != nullptr && valid) args.sq_out[(int64_t)nb * args.sq_stride + r] = sq;
           break;
         }
         case EPI_SILU: {
 #pragma unroll 1
           for (int c = 0; c < 4; ++c) {
             float u[32];
-            ld32f(taddr + c * 32, s, v);
-            ld32f(taddr + 128 + c * 32, s, u);
+            ldacc(c * 32, s, v);
+            ldacc(128 + c * 32, s, u);
             const int col = nb * 128 + c * 32;
             if (valid && col < args.n_valid) {
 #pragma unroll
@@ -234,7 +319,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         case EPI_QKV: {
           const int hd = args.hd, qh = args.qh, kh = args.kh;
-          const int hpt = GEMM_BN / hd;
+          const int hpt = BN / hd;
           const int pos = valid ? args.tok_pos[r] : 0;
           const int slot = valid ? args.tok_slot[r] : 0;
           const int64_t page = slot / args.page_size, off = slot % args.page_size;
@@ -253,15 +338,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (gh >= qh + kh) {  // V: no rotation
 #pragma unroll 1
               for (int c = 0; c < hd / 32; ++c) {
-                ld32f(taddr + hh * hd + c * 32, s, v);
+                ldacc(hh * hd + c * 32, s, v);
                 if (valid) store32_bf16(dst + c * 32, v);
               }
             } else {  // Q or K: rotate-half RoPE at pos (reading A-4)
 #pragma unroll 1
               for (int c = 0; c < hd / 64; ++c) {
                 float x2[32];
-                ld32f(taddr + hh * hd + c * 32, s, v);
-                ld32f(taddr + hh * hd + hd / 2 + c * 32, s, x2);
+                ldacc(hh * hd + c * 32, s, v);
+                ldacc(hh * hd + hd / 2 + c * 32, s, x2);
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                   float sn, cs;
@@ -283,8 +368,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           float best = -INFINITY;
           int bi = 0x7fffffff;
 #pragma unroll 1
-          for (int c = 0; c < GEMM_BN / 32; ++c) {
-            ld32f(taddr + c * 32, 1.f, v);
+          for (int c = 0; c < BN / 32; ++c) {
+            ldacc(c * 32, 1.f, v);
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int col = n0 + c * 32 + j;
@@ -305,18 +390,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (lane == 0) mbar_arrive(&tempty[as]);
       as ^= 1;
       if (as == 0) aphase ^= 1;
-    }
+    });
   }
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_once;
-bool g_attr_set[5] = {false, false, false, false, false};
+bool g_attr_set[4] = {false, false, false, false};
 
 cudaError_t get_encode() {
   std::call_once(g_once, [] {
@@ -365,22 +450,56 @@ cudaError_t make_page_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, in
 cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb,
                         const GemmArgs& args, int sm_budget, cudaStream_t stream) {
   if (args.M <= 0) return cudaSuccess;
+  // Tile width: 128x256.  A 128x128 variant (6-stage ring, NF_GEMM_BN=128)
+  // halves wave quantisation for nano-batch-sized GEMMs but measured slower:
+  // with a 1-CTA N=128 MMA the A+B smem reads reach the smem bandwidth.
+  // SiLU / argmax epilogues need the 256-wide tile layout.
+  const int tiles256 = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + 255) / 256);
+  static int bn_env = -1;
+  if (bn_env < 0) {
+    const char* e = getenv("NF_GEMM_BN");
+    bn_env = e ? atoi(e) : 0;
+  }
+  const bool need256 = args.epi == EPI_SILU || args.epi == EPI_ARGMAX;  // tile-layout-dependent epilogues
+  (void)tiles256;
+  const int bn = (bn_env == 128 && !need256) ? 128 : 256;
   CUtensorMap ta, tb;
   cudaError_t e = make_tmap_bf16(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
   if (e != cudaSuccess) return e;
-  e = make_tmap_bf16(&tb, B, args.K, args.N, ldb, GEMM_BK, GEMM_BN);
+  e = make_tmap_bf16(&tb, B, args.K, args.N, ldb, GEMM_BK, bn);
   if (e != cudaSuccess) return e;
-  const int stages = args.stages == 3 ? 3 : 4;
-  auto kern = stages == 3 ? gemm_tcgen05_kernel<3> : gemm_tcgen05_kernel<4>;
-  if (!g_attr_set[stages]) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem(stages));
-    if (e != cudaSuccess) return e;
-    g_attr_set[stages] = true;
+  // smem ring: 4 x 48 KB (BN 256) or 6 x 32 KB (BN 128); co-located plans use 3 / 4 stages
+  const bool coloc = args.stages == 3;
+  int stages;
+  void (*kern)(CUtensorMap, CUtensorMap, GemmArgs);
+  if (bn == 256) {
+    stages = coloc ? 3 : 4;
+    kern = coloc ? gemm_tcgen05_kernel<3, 256> : gemm_tcgen05_kernel<4, 256>;
+  } else {
+    stages = coloc ? 4 : 6;
+    kern = coloc ? gemm_tcgen05_kernel<4, 128> : gemm_tcgen05_kernel<6, 128>;
   }
-  const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + GEMM_BN - 1) / GEMM_BN);
+  const int smem = gemm_smem_bn(stages, bn);
+  const int attr_idx = (bn == 256 ? 0 : 2) + (coloc ? 1 : 0);
+  if (!g_attr_set[attr_idx]) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    g_attr_set[attr_idx] = true;
+  }
+  const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + bn - 1) / bn);
   int grid = tiles < sm_budget ? tiles : sm_budget;
+  // Stream-K tail is opt-in (NF_STREAMK=1): it removes wave quantisation but its
+  // k-staggered CTAs lose the L2 reuse of weight tiles across m-tiles, which
+  // measured slower on the decoder GEMMs.
+  static int sk_env = -1;
+  if (sk_env < 0) {
+    const char* e = getenv("NF_STREAMK");
+    sk_env = (e && e[0] == '1') ? 1 : 0;
+  }
+  GemmArgs a2 = args;
+  if (!sk_env) a2.sk_part = nullptr;
   if (grid < 1) grid = 1;
-  kern<<<grid, GEMM_THREADS, gemm_smem(stages), stream>>>(ta, tb, args);
+  kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, a2);
   count_launch();
   return cudaGetLastError();
 }

@@ -21,7 +21,9 @@ constexpr int GEMM_BN = 256;
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_STAGES = 4;      // default ring depth; 3 when co-resident with attention CTAs
 constexpr int GEMM_THREADS = 256;  // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warps 4-7 epilogue
-constexpr int gemm_smem(int stages) { return stages * (GEMM_BM + GEMM_BN) * GEMM_BK * 2 + 1024 + 512; }
+constexpr int GEMM_SK_LD = 256;    // stream-K partial tile row stride (floats)
+constexpr int gemm_smem_bn(int stages, int bn) { return stages * (GEMM_BM + bn) * GEMM_BK * 2 + 1024 + 512; }
+constexpr int GEMM_NORM_COLS = 128;  // columns per RMS sum-of-squares partial (EPI_RESID)
 
 struct GemmArgs {
   int epi;
@@ -39,7 +41,7 @@ struct GemmArgs {
   int norm_nparts;
   int64_t norm_stride;
   float inv_d, eps;
-  // sum-of-squares partial output: sq_out[n_tile * sq_stride + r]
+  // sum-of-squares partial output per 128 columns: sq_out[(col / 128) * sq_stride + r]
   float* sq_out;
   int64_t sq_stride;
   // EPI_QKV
@@ -49,11 +51,18 @@ struct GemmArgs {
   const int* tok_slot;   // [M] page*page_size + offset
   __nv_bfloat16* q_out;  // [M, qh, hd]
   __nv_bfloat16* kv_pool;
+  // stream-K scratch (null: data-parallel tiles only): fp32 partial tile per CTA
+  // [grid][128][256], arrival counters per tile (zero at launch, self-resetting)
+  float* sk_part;
+  int* sk_flag;
   // EPI_ARGMAX
   float* am_val;
   int* am_idx;
   int64_t am_stride;
 };
+
+// Bytes of stream-K scratch for a GEMM with this many tiles at this grid.
+inline size_t gemm_sk_bytes(int grid, int tiles) { return (size_t)grid * GEMM_BM * GEMM_BN * 4 + (size_t)tiles * 4 + 256; }
 
 // A: [M, K] row-major (lda elements), B: [N, K] row-major (ldb elements).
 // grid = min(tiles, sm_budget) persistent CTAs, one per SM.

@@ -60,6 +60,9 @@ struct Workspace {
   float *part_a, *part_b, *part_h1, *lm_part, *am_val;
   int* am_idx;
   float* red;  // TP partial sums (f32)
+  float* sk_part;  // stream-K partial tiles [148][128][256] f32
+  int* sk_flag;    // stream-K tile counters
+  int sk_flag_n;
   size_t total;
 };
 Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base);

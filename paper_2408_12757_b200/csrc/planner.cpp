@@ -188,7 +188,8 @@ Result local_search(const std::vector<PNode>& g, const std::vector<int>& order, 
   return Result{units, cur};
 }
 
-// the executor's OVERLAP schedule (api.cu nf_model_step) as a DAG over n_layers layers
+// the executor's OVERLAP schedule (api.cu nf_model_step) as a DAG over n_layers layers:
+// decode attention on the memory stream, prefill attention on the compute stream (A-11)
 std::vector<PNode> build_pipeline(const std::vector<std::array<double, 3>>& work, int n_layers) {
   std::vector<PNode> g;
   auto add = [&](int kind, int nano, double w, std::vector<int> deps) {
@@ -203,26 +204,24 @@ std::vector<PNode> build_pipeline(const std::vector<std::array<double, 3>>& work
   };
   const int K = (int)work.size();
   int last_c = -1, last_m = -1;
-  std::vector<int> kqv(K, -1), att(K, -1);
+  std::vector<int> dec(K, -1);
   for (int k = 0; k < K; ++k) {
-    kqv[k] = add(NF_OP_KQV, k, work[k][0], {last_c});
-    last_c = kqv[k];
+    const int kq = add(NF_OP_KQV, k, work[k][0], {last_c});
+    dec[k] = add(NF_OP_DECODE_ATTN, k, work[k][1], {kq, last_m});
+    last_m = dec[k];
+    last_c = add(NF_OP_PREFILL_ATTN, k, work[k][2], {kq});
   }
   for (int l = 0; l < n_layers; ++l) {
     for (int k = 0; k < K; ++k) {
-      const int pf = add(NF_OP_PREFILL_ATTN, k, work[k][2], {kqv[k], last_m});
-      const int dc = add(NF_OP_DECODE_ATTN, k, work[k][1], {pf});
-      last_m = dc;
-      att[k] = dc;
-    }
-    for (int k = 0; k < K; ++k) {
-      const int o = add(NF_OP_O, k, work[k][0], {att[k], last_c});
+      const int o = add(NF_OP_O, k, work[k][0], {dec[k], last_c});
       const int ug = add(NF_OP_UG, k, work[k][0], {o});
       const int dn = add(NF_OP_DOWN, k, work[k][0], {ug});
       last_c = dn;
       if (l + 1 < n_layers) {
-        kqv[k] = add(NF_OP_KQV, k, work[k][0], {dn});
-        last_c = kqv[k];
+        const int kq = add(NF_OP_KQV, k, work[k][0], {dn});
+        dec[k] = add(NF_OP_DECODE_ATTN, k, work[k][1], {kq, last_m});
+        last_m = dec[k];
+        last_c = add(NF_OP_PREFILL_ATTN, k, work[k][2], {kq});
       }
     }
   }

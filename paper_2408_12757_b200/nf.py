@@ -101,7 +101,8 @@ _sig("nf_layer_forward", C.c_int, C.c_void_p, C.c_void_p, C.POINTER(PackedLayer)
 _sig("nf_model_step", C.c_int, C.c_void_p, C.c_void_p, C.POINTER(ModelWeights), C.POINTER(C.c_void_p),
      C.POINTER(_Batch), C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 _sig("nf_gemm_bf16", C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
-     C.c_int32, C.c_int32, C.c_int32, C.c_void_p)
+     C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p)
+_sig("nf_gemm_workspace_bytes", C.c_size_t, C.c_int32, C.c_int32)
 _sig("nf_attention", C.c_int, C.POINTER(ModelCfg), C.POINTER(_Batch), C.c_void_p, C.c_void_p, C.c_void_p,
      C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.c_void_p)
 
@@ -118,7 +119,7 @@ class Span(C.Structure):
 _sig("nf_profile_timeline", C.c_int, C.POINTER(Span), C.c_int32, P_i32)
 PROF_NAMES = ["kqv", "decode_attn", "prefill_attn", "o_proj", "up_gate", "down", "net", "lm_head", "misc"]
 
-EXPORTED = ["nf_profile_timeline", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
+EXPORTED = ["nf_gemm_workspace_bytes", "nf_profile_timeline", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
             "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_comm_unique_id",
             "nf_comm_create", "nf_comm_destroy", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
             "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_gemm_bf16", "nf_attention"]
@@ -270,10 +271,14 @@ def model_step(plan: Plan, model: ModelHandle, kv_pools: Sequence[int], b: Batch
                              C.c_void_p(next_ids), C.c_void_p(ws), ws_bytes, C.c_void_p(stream)))
 
 
+def gemm_workspace_bytes(M: int, N: int) -> int:
+    return int(lib.nf_gemm_workspace_bytes(M, N))
+
+
 def gemm_bf16(A: int, lda: int, B: int, ldb: int, Cp: int, ldc: int, M: int, N: int, K: int, sm_budget: int,
-              stream: int):
+              stream: int, ws: int = 0, ws_bytes: int = 0):
     _check(lib.nf_gemm_bf16(C.c_void_p(A), lda, C.c_void_p(B), ldb, C.c_void_p(Cp), ldc, M, N, K, sm_budget,
-                            C.c_void_p(stream)))
+                            C.c_void_p(ws or None), ws_bytes, C.c_void_p(stream)))
 
 
 def attention(cfg: ModelCfg, b: Batch, q: int, kv_pool: int, o: int, ws: int, ws_bytes: int, sm_decode: int,

@@ -41,6 +41,47 @@ def test_gemm_vs_oracle(env, M, N, K):
     assert rel < 4e-3 and mx < 2e-2 * max(1.0, np.abs(ref).max()), (rel, mx)
 
 
+@pytest.mark.parametrize("M,N,K,sm", [(1024, 4096, 4096, 108), (1024, 6144, 4096, 100), (2048, 4096, 14336, 148),
+                                      (333, 2816, 1376, 37), (77, 768, 512, 148), (1024, 28672, 4096, 96)])
+def test_gemm_stream_k_vs_oracle(env, M, N, K, sm, monkeypatch):
+    """Hybrid stream-K tail (partial fp32 tiles reduced in CTA order; opt-in via
+    NF_STREAMK=1, read at first GEMM launch -- exercised in a subprocess so the
+    default path stays untouched): oracle values, bit-identical on repeat."""
+    import subprocess
+    import sys
+    code = f"""
+import sys, numpy as np, torch
+sys.path.insert(0, {repr(str(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))})
+sys.path.insert(0, {repr(str(__import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__)))))})
+import test_gpu_parity as T
+T._stream_k_case({M}, {N}, {K}, {sm})
+print("OK")
+"""
+    env2 = dict(__import__('os').environ, NF_STREAMK="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env2, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+def _stream_k_case(M, N, K, sm):
+    nf, rt = require_gpu()
+    rng = np.random.default_rng(M + N + K + sm)
+    A = synth.round_bf16(rng.standard_normal((M, K), dtype=np.float32))
+    B = synth.round_bf16(rng.standard_normal((N, K), dtype=np.float32) / np.float32(np.sqrt(K)))
+    Ad, Bd = dev(A), dev(B)
+    ws = torch.empty(nf.gemm_workspace_bytes(M, N), dtype=torch.uint8, device="cuda")
+    outs = []
+    for _ in range(2):
+        C = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+        nf.gemm_bf16(Ad.data_ptr(), K, Bd.data_ptr(), K, C.data_ptr(), N, M, N, K, sm, rt.stream_handle(),
+                     ws.data_ptr(), ws.numel())
+        outs.append(C)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    rel, mx = errors(host(outs[0]), ref)
+    assert rel < 4e-3 and mx < 2e-2 * max(1.0, np.abs(ref).max()), (rel, mx)
+
+
 @pytest.mark.parametrize("sm", [1, 7, 64, 148])
 def test_gemm_sm_budget_bit_identical(env, sm):
     """The SM budget only changes which CTA computes a tile, never the math."""

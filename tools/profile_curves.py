@@ -54,9 +54,10 @@ def main():
         for op, (N, K) in gemms.items():
             B = (torch.randn(N, K, device=dev) * K ** -0.5).to(torch.bfloat16)
             C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+            gws = torch.empty(nf.gemm_workspace_bytes(M, N), dtype=torch.uint8, device=dev)
             for u in units:
                 t = timeit(lambda: nf.gemm_bf16(A.data_ptr(), A.shape[1], B.data_ptr(), K, C.data_ptr(), N, M, N, K,
-                                                u, st))
+                                                u, st, gws.data_ptr(), gws.numel()))
                 rows.append((op, "compute", u, M, t))
             del B, C
         del A

@@ -1,0 +1,90 @@
+#!/usr/bin/env python
+"""Time nf_model_step for many explicit plans in one process (weights and KV
+allocated once).  Usage: sweep_plans.py [--config c2|c3rank] [--steps N]
+Prints ms/step per plan, best first."""
+import argparse
+import itertools
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--layers", type=int, default=0)
+    args = ap.parse_args()
+    import torch
+
+    import synth
+    from paper_2408_12757_b200 import nf, runtime as rt
+    if args.config == "c3rank":
+        shape = synth.shape_with(synth.SHAPES["llama2-70b"], n_q_heads=8, n_kv_heads=1, d_ffn=3584)
+        p_in, d_out = 512, 1024
+    else:
+        shape = synth.SHAPES["llama3-8b"]
+        p_in, d_out = 1024, 512
+    if args.layers:
+        shape = synth.shape_with(shape, n_layers=args.layers)
+    b = synth.workload_batch(2048, p_in, d_out)
+    nb = nf.Batch.from_any(b)
+    cfg = rt.cfg_from_shape(shape)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+
+    def randn(s, std=1.0, mean=0.0):
+        t = torch.empty(s, dtype=torch.bfloat16, device="cuda")
+        t.normal_(mean, std, generator=g)
+        return t
+
+    D, F, hd, Hq, Hk = shape.d_model, shape.d_ffn, shape.head_dim, shape.n_q_heads, shape.n_kv_heads
+    layers = []
+    for _ in range(shape.n_layers):
+        w = {"attn_norm": randn((D,), 0.1, 1.0), "w_q": randn((Hq * hd, D), D ** -0.5),
+             "w_k": randn((Hk * hd, D), D ** -0.5), "w_v": randn((Hk * hd, D), D ** -0.5),
+             "w_o": randn((D, Hq * hd), (Hq * hd) ** -0.5), "ffn_norm": randn((D,), 0.1, 1.0),
+             "w_gate": randn((F, D), D ** -0.5), "w_up": randn((F, D), D ** -0.5), "w_down": randn((D, F), F ** -0.5)}
+        layers.append(rt.pack_layer(cfg, w))
+    model = rt.Model(cfg, randn((shape.vocab, D)), layers,
+                     rt.pack_lm_head(cfg, randn((shape.vocab, D), D ** -0.5), randn((D,), 0.1, 1.0)))
+    pools = [randn((b.n_pages_pool, 2, Hk, 16, hd)) for _ in range(shape.n_layers)]
+    tok = torch.randint(0, shape.vocab, (b.n_tokens,), dtype=torch.int32, device="cuda", generator=g)
+    ws = rt.workspace(cfg, nb)
+    ids = torch.empty(b.n_req, dtype=torch.int32, device="cuda")
+
+    def run(plan):
+        for _ in range(2):
+            model.step(plan, pools, nb, tok, ws, ids)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            model.step(plan, pools, nb, tok, ws, ids)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / args.steps
+
+    results = []
+    results.append(("sequential", run(nf.Plan.explicit(cfg, nf.SEQUENTIAL))))
+    print(results[-1], flush=True)
+    for shares, bal in [((1, 1), True), ((3, 5), False), ((5, 3), True), ((3, 5), True), ((1, 1), False)]:
+        for dense, dec in [(148, 148), (116, 32), (108, 40), (100, 48), (92, 56), (84, 64), (128, 64), (148, 48)]:
+            sm = [dense, dec, dense, dense, dense, dense, 8]
+            name = f"overlap shares={shares} bal={bal} dense={dense} dec={dec}"
+            results.append((name, run(nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm, balance=bal))))
+            print(results[-1], flush=True)
+    for shares in [(1, 1), (3, 5)]:
+        name = f"colocate shares={shares}"
+        results.append((name, run(nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=[148] * 7, balance=True,
+                                                   colocate=True))))
+        print(results[-1], flush=True)
+    print("---- best first")
+    for n, t in sorted(results, key=lambda x: x[1])[:12]:
+        print(f"{t:8.2f} ms  {n}")
+
+
+if __name__ == "__main__":
+    main()
