@@ -186,7 +186,16 @@ def run_nf(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if args.config == "c3rank":
+    tp = 1
+    comm = None
+    if args.config == "c3":
+        # configs[2]: LLaMA-2-70B shape, tensor parallel over all ranks (NCCL over NVLink)
+        if world < 2:
+            raise SystemExit("--config c3 needs torchrun with >= 2 GPUs (70B weights + KV do not fit one B200)")
+        tp = world
+        shape = synth.SHAPES["llama2-70b"]
+        p_in, d_out = 512, 1024
+    elif args.config == "c3rank":
         # rank-local proxy of configs[2] (70B TP8): one rank's head/FFN shards, no collectives
         shape = synth.shape_with(synth.SHAPES["llama2-70b"], name="llama2-70b-tp8-rank", n_q_heads=8, n_kv_heads=1,
                                  d_ffn=28672 // 8)
@@ -197,10 +206,15 @@ def run_nf(args, rank, world, local_rank):
     if args.layers:
         shape = synth.shape_with(shape, n_layers=args.layers)
     L = shape.n_layers
-    b = synth.workload_batch(2048, p_in, d_out)
+    b_dense = 768 if (args.config == "c3" and tp == 2) else 2048   # TP2: memory cap
+    b = synth.workload_batch(b_dense, p_in, d_out)
     T = b.n_tokens
     nb = nf.Batch.from_any(b)
-    cfg = rt.cfg_from_shape(shape)
+    cfg = rt.cfg_from_shape(shape, tp_size=tp, tp_rank=rank if tp > 1 else 0)
+    if tp > 1:
+        uid = [nf.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = nf.comm_create(tp, rank, uid[0])
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
 
@@ -212,16 +226,25 @@ def run_nf(args, rank, world, local_rank):
     D, F, hd, Hq, Hk = shape.d_model, shape.d_ffn, shape.head_dim, shape.n_q_heads, shape.n_kv_heads
     layers = []
     for l in range(L):
-        w = {"attn_norm": randn((D,), 0.1, 1.0), "w_q": randn((Hq * hd, D), D ** -0.5),
-             "w_k": randn((Hk * hd, D), D ** -0.5), "w_v": randn((Hk * hd, D), D ** -0.5),
-             "w_o": randn((D, Hq * hd), (Hq * hd) ** -0.5), "ffn_norm": randn((D,), 0.1, 1.0),
-             "w_gate": randn((F, D), D ** -0.5), "w_up": randn((F, D), D ** -0.5), "w_down": randn((D, F), F ** -0.5)}
+        if tp == 1:
+            w = {"attn_norm": randn((D,), 0.1, 1.0), "w_q": randn((Hq * hd, D), D ** -0.5),
+                 "w_k": randn((Hk * hd, D), D ** -0.5), "w_v": randn((Hk * hd, D), D ** -0.5),
+                 "w_o": randn((D, Hq * hd), (Hq * hd) ** -0.5), "ffn_norm": randn((D,), 0.1, 1.0),
+                 "w_gate": randn((F, D), D ** -0.5), "w_up": randn((F, D), D ** -0.5),
+                 "w_down": randn((D, F), F ** -0.5)}
+        else:  # this rank's shards only
+            qs, ks, Dl, Fl = Hq // tp * hd, Hk // tp * hd, D // tp, F // tp
+            w = {"attn_norm": randn((D,), 0.1, 1.0), "w_q": randn((qs, D), D ** -0.5),
+                 "w_k": randn((ks, D), D ** -0.5), "w_v": randn((ks, D), D ** -0.5),
+                 "w_o_col": randn((Dl, Hq * hd), (Hq * hd) ** -0.5), "w_o_row": randn((D, qs), (Hq * hd) ** -0.5),
+                 "ffn_norm": randn((D,), 0.1, 1.0), "w_gate": randn((Fl, D), D ** -0.5),
+                 "w_up": randn((Fl, D), D ** -0.5), "w_down": randn((D, Fl), F ** -0.5)}
         layers.append(rt.pack_layer(cfg, w))
         del w
     embed = randn((shape.vocab, D))
     lm = rt.pack_lm_head(cfg, randn((shape.vocab, D), D ** -0.5), randn((D,), 0.1, 1.0))
     model = rt.Model(cfg, embed, layers, lm)
-    pools = [randn((b.n_pages_pool, 2, Hk, 16, hd)) for _ in range(L)]
+    pools = [randn((b.n_pages_pool, 2, Hk // tp, 16, hd)) for _ in range(L)]
     tok = torch.randint(0, shape.vocab, (T,), dtype=torch.int32, device=dev, generator=g)
     ws = rt.workspace(cfg, nb, dev)
     next_ids = torch.empty(b.n_req, dtype=torch.int32, device=dev)
@@ -237,16 +260,18 @@ def run_nf(args, rank, world, local_rank):
             plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=sm or [148] * 7, balance=True,
                                     colocate=True)
         else:
-            plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=sm or [84, 64, 64, 84, 84, 84, 16],
-                                    balance=True)
+            shares = tuple(int(x) for x in args.shares.split(","))
+            plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm or [108, 40, 108, 108, 108, 108, 8],
+                                    balance=args.balance)
     elif args.mode == "nano":
-        plan = nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=(1, 1), sm=sm, balance=True)
+        plan = nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=tuple(int(x) for x in args.shares.split(",")), sm=sm,
+                                balance=args.balance)
     else:
         plan = nf.Plan.explicit(cfg, nf.SEQUENTIAL, sm=sm)
     stream = torch.cuda.current_stream()
 
     def step():
-        model.step(plan, pools, nb, tok, ws, next_ids)
+        model.step(plan, pools, nb, tok, ws, next_ids, comm=comm)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -277,7 +302,8 @@ def run_nf(args, rank, world, local_rank):
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms_max = float(t_max.item())
     ms_step = ms_max / args.steps
-    value = world * T * args.steps / (ms_max / 1e3)
+    replicas = world // tp                                    # independent model copies (1 under TP)
+    value = replicas * T * args.steps / (ms_max / 1e3)
 
     if args.timeline:
         torch.cuda.synchronize()
@@ -294,13 +320,50 @@ def run_nf(args, rank, world, local_rank):
                 f.write(f"{sp[0]},{sp[1]},{sp[2]:.4f},{sp[3]:.4f}\n")
     if args.ncu:
         return
+    n_dec = int((b.q_len == 1).sum())
+    kv_keys = sum(int(b.kv_prefix[r]) + 1 for r in range(b.n_req) if b.q_len[r] == 1)
+    Hq_l, Hk_l, F_l = Hq // tp, Hk // tp, F // tp      # this rank's share under TP
+    dec_bytes_step = L * (kv_keys * Hk_l * hd * 2 * 2 + n_dec * Hq_l * hd * 2 * 2)  # K+V read + q read + o write
+    # ---------------- F7 ablation with the same kernels: sequential and nano-batch-only
+    ablation = {}
+    if not args.no_ablation:
+        for name, pl in (("sequential", nf.Plan.explicit(cfg, nf.SEQUENTIAL)),
+                         ("nano_only", nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=plan.spec().share[:2]
+                                                        if plan.spec().n_nano == 2 else (1, 1),
+                                                        balance=args.balance))):
+            for _ in range(2):
+                model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            nf.profile_enable(True)
+            nf.profile_read()
+            a0.record(stream)
+            for _ in range(args.steps):
+                model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            nf.profile_enable(False)
+            prof_ab = nf.profile_read()
+            ablation[name + "_per_op_ms"] = {k: v[0] / args.steps for k, v in prof_ab.items() if v[1]}
+            t_ab = torch.tensor([a0.elapsed_time(a1) / args.steps], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(t_ab, op=dist.ReduceOp.MAX)
+            ablation[name + "_ms_per_step"] = float(t_ab.item())
+        ablation["timed_mode_ms_per_step"] = ms_step
+        ablation["timed_mode"] = args.mode
+        ablation["speedup_vs_sequential"] = ablation["sequential_ms_per_step"] / ms_step
+        seq_dec = ablation["sequential_per_op_ms"].get("decode_attn")
+        if seq_dec:
+            ablation["sequential_decode_attn_hbm_gbs"] = dec_bytes_step / (seq_dec / 1e3) / 1e9
     # ---------------- end to end through the public API with host buffers
     tok_host = tok.cpu().pin_memory()
     ids_host = torch.empty(b.n_req, dtype=torch.int32).pin_memory()
     tok_dev2 = torch.empty_like(tok)
     for _ in range(2):
         tok_dev2.copy_(tok_host, non_blocking=True)
-        model.step(plan, pools, nb, tok_dev2, ws, next_ids)
+        model.step(plan, pools, nb, tok_dev2, ws, next_ids, comm=comm)
         ids_host.copy_(next_ids, non_blocking=True)
     torch.cuda.synchronize()
     if world > 1:
@@ -309,7 +372,7 @@ def run_nf(args, rank, world, local_rank):
     f0.record(stream)
     for _ in range(args.steps):
         tok_dev2.copy_(tok_host, non_blocking=True)
-        model.step(plan, pools, nb, tok_dev2, ws, next_ids)
+        model.step(plan, pools, nb, tok_dev2, ws, next_ids, comm=comm)
         ids_host.copy_(next_ids, non_blocking=True)
         stream.synchronize()
     f1.record(stream)
@@ -317,7 +380,7 @@ def run_nf(args, rank, world, local_rank):
     e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = world * T * args.steps / (float(e2e_ms.item()) / 1e3)
+    e2e_value = replicas * T * args.steps / (float(e2e_ms.item()) / 1e3)
     n_dec = int((b.q_len == 1).sum())
     pf_items = sum(((int(q) + 63) // 64) * Hq for q in b.q_len if q > 1)
     meta_words = 3 * T + int(b.page_indptr[-1]) + 4 * n_dec * Hk + 8 * pf_items + 2 * b.n_req
@@ -329,11 +392,9 @@ def run_nf(args, rank, world, local_rank):
 
     # ---------------- roofline of the dominant kernel (per-op CUDA-event time in the timed region)
     peaks, peak_src = load_peaks()
-    kv_keys = sum(int(b.kv_prefix[r]) + 1 for r in range(b.n_req) if b.q_len[r] == 1)
-    dec_bytes_step = L * (kv_keys * Hk * hd * 2 * 2 + n_dec * Hq * hd * 2 * 2)  # K+V read + q read + o write
-    qkv_n = (Hq + 2 * Hk) * hd
-    flops = {"kqv": 2 * T * qkv_n * D * L, "o_proj": 2 * T * D * Hq * hd * L, "up_gate": 2 * T * 2 * F * D * L,
-             "down": 2 * T * D * F * L, "lm_head": 2 * b.n_req * shape.vocab * D}
+    qkv_n = (Hq_l + 2 * Hk_l) * hd
+    flops = {"kqv": 2 * T * qkv_n * D * L, "o_proj": 2 * T * D * Hq_l * hd * L, "up_gate": 2 * T * 2 * F_l * D * L,
+             "down": 2 * T * D * F_l * L, "lm_head": 2 * b.n_req * shape.vocab * D}
     per_op = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
               for k, v in prof.items() if v[1]}
     dom = max(per_op, key=lambda k: per_op[k]["ms_per_step"])
@@ -360,7 +421,8 @@ def run_nf(args, rank, world, local_rank):
 
     optimal = peaks["bf16_tflops"] * 1e12 / (2 * p_active(shape))
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if tp > 1 else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, seeded torch RNG on device)",
             "config": {"workload": (f"configs[1]: LLaMA-3-8B-shape {L}-layer serving step, B_dense 2048 "
                                     f"(683 decode ctx 1024-1535 + 341-token chunk + 1024-token prompt), page 16")
@@ -369,9 +431,9 @@ def run_nf(args, rank, world, local_rank):
                         f"F 3584), {L} layers, B_dense 2048 (1365 decode ctx 512-1535 + 171 chunk + 512 prompt), "
                         f"no collectives"),
                        "b_dense": T, "n_layers": L, "mode": args.mode, "colocate": bool(plan.spec().colocate),
-                       "parallelism": "replicas" if world > 1 else "single-gpu",
+                       "parallelism": (f"tp{tp}" if tp > 1 else ("replicas" if world > 1 else "single-gpu")),
                        "plan_sm": list(plan.spec().sm), "plan_shares": list(plan.spec().share)[:plan.spec().n_nano],
-                       "plan": args.plan, "l2": "no flush: per-step inputs (KV 115 GB) >> 126 MB L2"},
+                       "plan": args.plan, "partitions": plan.runtime_note(), "l2": "no flush: per-step inputs (KV 115 GB) >> 126 MB L2"},
             "tokens_per_s_per_gpu": value / world,
             "pct_of_optimal": 100.0 * (value / world) / optimal,
             "optimal_tokens_per_s_per_gpu": optimal,
@@ -379,6 +441,7 @@ def run_nf(args, rank, world, local_rank):
             "clocks": clk.summary(),
             "roofline": roof,
             "per_op": per_op,
+            "ablation": ablation,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}}
     if world == 1 and not args.no_cpu_baseline:
         b_s, w_s, x_s, pool_s = oracle_sample(shape)
@@ -401,11 +464,15 @@ def main():
     ap.add_argument("--plan", default="explicit", choices=["explicit", "auto"],
                     help="auto: nf_plan_create autosearch over --curves (overlap mode)")
     ap.add_argument("--curves", default="profiles/curves_b200_quick.csv")
+    ap.add_argument("--shares", default="5,3", help="nano-batch token shares (overlap / nano modes)")
+    ap.add_argument("--balance", type=int, default=2, help="0 request order, 1 balanced, 2 exact shares + KV")
     ap.add_argument("--colocate", action="store_true", help="attention CTAs co-resident with GEMM CTAs")
     ap.add_argument("--sm", default="", help="comma-separated SM budget per op kind (7 values)")
-    ap.add_argument("--config", default="c2", choices=["c2", "c3rank"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c3rank"],
+                    help="c2: configs[1] 8B 1 GPU (replicas for N>1); c3: configs[2] 70B TP=N; c3rank: 1-GPU proxy")
     ap.add_argument("--layers", type=int, default=0, help="(dev only) override layer count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ablation", action="store_true", help="skip the sequential / nano-only comparison runs")
     ap.add_argument("--timeline", default="", help="write one step's kernel spans (CSV) to this path")
     ap.add_argument("--ncu", action="store_true", help="profiling run: timed steps only, no e2e / JSON")
     args = ap.parse_args()

@@ -110,7 +110,9 @@ typedef struct {
   int32_t n_nano;              /* 1..NF_MAX_NANO */
   int32_t share[NF_MAX_NANO];
   int32_t sm[NF_OP_COUNT];
-  int32_t balance;             /* 1: assign requests to nano-batches balancing tokens and KV (model step only) */
+  int32_t balance;             /* model step only: 0 request-order cuts (A-10); 1 requests balanced by tokens
+                                  and decode KV (A-10b); 2 exact token shares + decode-KV balance, prefill
+                                  requests split across nano-batches where needed (A-10c) */
   int32_t colocate;            /* 1: attention CTAs co-reside with GEMM CTAs on the same SMs (3-stage GEMM ring,
                                   4-warp decode CTAs) instead of disjoint SM partitions */
 } nf_plan_spec;
@@ -143,12 +145,21 @@ nf_status nf_plan_get_spec(const nf_plan* plan, nf_plan_spec* out);
 /* Gantt CSV `node_id,kind,nano_index,units,start_s,end_s` of the searched schedule. */
 nf_status nf_plan_export_csv(const nf_plan* plan, char* buf, size_t cap, size_t* len);
 void nf_plan_destroy(nf_plan* plan);
+/* How an OVERLAP plan partitions the GPU at run time (green-context SM
+ * partitions, or why they are not used).  Valid until the plan is destroyed. */
+const char* nf_plan_runtime_note(const nf_plan* plan);
 
 /* ------------------------------------------------------------------ tensor-parallel communicator */
 typedef struct nf_comm nf_comm;
 /* 128-byte NCCL unique id, created on rank 0 and broadcast by the caller. */
 nf_status nf_comm_unique_id(void* id_out_128);
 nf_status nf_comm_create(int32_t tp_size, int32_t tp_rank, const void* id_128, nf_comm** out);
+/* tp_size communicators of one emulated group living in this process on one
+ * GPU (tests, rank-local studies): rank r's calls run on host thread r;
+ * collectives meet at a host barrier and exchange device buffers with
+ * stream-ordered copies; AllReduce sums in rank order (bit-identical on all
+ * ranks).  comms_out: [tp_size]. */
+nf_status nf_comm_create_local(int32_t tp_size, nf_comm** comms_out);
 void nf_comm_destroy(nf_comm* comm);
 
 /* ------------------------------------------------------------------ weights */

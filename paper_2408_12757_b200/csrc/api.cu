@@ -156,13 +156,14 @@ size_t meta_words_bound(const nf_model_cfg* c, const nf_batch* b) {
   int64_t pf_tiles = 0;
   for (int r = 0; r < b->n_req; ++r)
     if (b->q_len[r] > 1) pf_tiles += (b->q_len[r] + 63) / 64;
-  const int64_t words = 3 * T + b->page_indptr[b->n_req] + 4 * (int64_t)b->n_req * kh + 8 * pf_tiles * qh +
-                        2 * (int64_t)b->n_req + 64;
+  // (x2 pages and + NF_MAX_NANO requests/tiles: split prefill requests duplicate their page list)
+  const int64_t words = 3 * T + 2 * (int64_t)b->page_indptr[b->n_req] + 4 * ((int64_t)b->n_req + NF_MAX_NANO) * kh +
+                        8 * (pf_tiles + NF_MAX_NANO) * qh + 2 * ((int64_t)b->n_req + NF_MAX_NANO) + 64;
   return (size_t)words;
 }
 
 void build_meta(const nf_model_cfg* c, const nf_batch* b, const std::vector<int>& order, const std::vector<int>& req_cuts,
-                StepMeta* m) {
+                StepMeta* m, const std::vector<int32_t>* caller_row0, const std::vector<int32_t>* caller_req) {
   const int P = c->page_size;
   const int qh = c->n_q_heads / c->tp_size, kh = c->n_kv_heads / c->tp_size;
   const int n_req = b->n_req;
@@ -193,7 +194,7 @@ void build_meta(const nf_model_cfg* c, const nf_batch* b, const std::vector<int>
       const int pos = b->kv_prefix[r] + i;
       head[t] = pos;
       head[T + t] = b->page_ids[b->page_indptr[r] + pos / P] * P + pos % P;
-      head[2 * T + t] = (int32_t)(caller_start[r] + i);
+      head[2 * T + t] = (int32_t)((caller_row0 ? (*caller_row0)[r] : caller_start[r]) + i);
     }
   }
   std::memcpy(head.data() + 3 * T, b->page_ids, npg * sizeof(int32_t));
@@ -237,7 +238,7 @@ void build_meta(const nf_model_cfg* c, const nf_batch* b, const std::vector<int>
     const int r = order[i];
     if (b->emit == nullptr || b->emit[r]) {
       erow.push_back(row_start[r] + b->q_len[r] - 1);
-      ereq.push_back(r);
+      ereq.push_back(caller_req ? (*caller_req)[r] : r);
     }
   }
   m->n_emit = (int)erow.size();
@@ -281,9 +282,15 @@ Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base) 
   w.am_val = (float*)take(VT * R * 4);
   w.am_idx = (int*)take(VT * R * 4);
   w.red = N > 1 ? (float*)take(T * D * 4) : nullptr;
-  w.sk_part = (float*)take((size_t)148 * GEMM_BM * GEMM_BN * 4);
-  const int64_t maxN = std::max<int64_t>({(int64_t)(c->n_q_heads + 2 * c->n_kv_heads) / N * c->head_dim, D,
-                                          ((F + 127) / 128) * 256});
+  const int64_t qd_full = (int64_t)c->n_q_heads * c->head_dim;
+  w.ag = N > 1 ? (__nv_bfloat16*)take(T * std::max(qd_full, D) * 2) : nullptr;
+  w.ocat = N > 1 ? (__nv_bfloat16*)take(T * qd_full * 2) : nullptr;
+  w.hcol = N > 1 ? (__nv_bfloat16*)take(T * (D / N) * 2) : nullptr;
+  // stream-K / split-K partial slots: max(148 CTAs, tiles of the largest non-SiLU GEMM)
+  const int64_t qkv_n = (int64_t)(c->n_q_heads + 2 * c->n_kv_heads) / N * c->head_dim;
+  w.sk_slots = (int)std::max<int64_t>(148, ((T + GEMM_BM - 1) / GEMM_BM) * ((std::max(qkv_n, D) + 255) / 256));
+  w.sk_part = (float*)take((size_t)w.sk_slots * GEMM_BM * GEMM_SK_LD * 4);
+  const int64_t maxN = std::max<int64_t>({qkv_n, D, ((F + 127) / 128) * 256});
   w.sk_flag_n = (int)(((T + GEMM_BM - 1) / GEMM_BM) * ((maxN + 127) / 128) +
                       ((R + GEMM_BM - 1) / GEMM_BM) * VT + 64);
   w.sk_flag = (int*)take((size_t)w.sk_flag_n * 4);
@@ -402,6 +409,7 @@ nf_status nf_plan_create_explicit(const nf_model_cfg* cfg, const nf_plan_spec* s
   }
   for (int o = 0; o < NF_OP_COUNT; ++o)
     if (spec->sm[o] < 1 || spec->sm[o] > 1024) return set_error(NF_EINVAL, "sm[%d] = %d out of range", o, spec->sm[o]);
+  if (spec->balance < 0 || spec->balance > 2) return set_error(NF_EINVAL, "balance must be 0, 1 or 2");
   nf_plan* p = new (std::nothrow) nf_plan();
   if (!p) return set_error(NF_ENOMEM, "plan allocation failed");
   p->cfg = *cfg;
@@ -431,6 +439,11 @@ nf_status nf_plan_export_csv(const nf_plan* plan, char* buf, size_t cap, size_t*
   return NF_OK;
 }
 
+const char* nf_plan_runtime_note(const nf_plan* p) {
+  if (!p) return "";
+  return p->green_note.c_str();
+}
+
 void nf_plan_destroy(nf_plan* p) {
   if (!p) return;
   if (p->mem_stream) cudaStreamDestroy(p->mem_stream);
@@ -439,6 +452,9 @@ void nf_plan_destroy(nf_plan* p) {
     if (p->ev_att[k]) cudaEventDestroy(p->ev_att[k]);
   }
   if (p->ev_join) cudaEventDestroy(p->ev_join);
+  if (p->net_stream) cudaStreamDestroy(p->net_stream);
+  if (p->ev_c2n) cudaEventDestroy(p->ev_c2n);
+  if (p->ev_n2c) cudaEventDestroy(p->ev_n2c);
   for (int i = 0; i < 2; ++i) {
     if (p->ev_upload[i]) cudaEventDestroy(p->ev_upload[i]);
     if (p->pinned[i]) cudaFreeHost(p->pinned[i]);
@@ -465,6 +481,12 @@ nf_status ensure_runtime(nf_plan* p) {
     NF_CUDA(cudaEventCreateWithFlags(&p->ev_att[k], cudaEventDisableTiming));
   }
   NF_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+  NF_CUDA(cudaStreamCreateWithPriority(&p->net_stream, cudaStreamNonBlocking, hi));
+  NF_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  NF_CUDA(cudaEventCreateWithFlags(&p->ev_join_c, cudaEventDisableTiming));
+  NF_CUDA(cudaEventCreateWithFlags(&p->ev_join_m, cudaEventDisableTiming));
+  NF_CUDA(cudaEventCreateWithFlags(&p->ev_c2n, cudaEventDisableTiming));
+  NF_CUDA(cudaEventCreateWithFlags(&p->ev_n2c, cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) NF_CUDA(cudaEventCreateWithFlags(&p->ev_upload[i], cudaEventDisableTiming));
   return NF_OK;
 }
@@ -488,9 +510,102 @@ nf_status upload_meta(nf_plan* p, const StepMeta& m, int32_t* dev, cudaStream_t 
 }
 
 // Internal request order and nano-batch cuts for this plan and batch.
-void plan_order(const nf_plan* p, const nf_batch* b, bool allow_balance, std::vector<int>* order, std::vector<int>* cuts) {
+// Internal view of a caller batch in which prefill requests may be split into
+// consecutive parts living in successive nano-batches (reading A-10c): part j
+// keeps the request's page list, starts at kv_prefix + (tokens of parts < j),
+// and only the last part samples.  Equivalent to the unsplit request by T7
+// (chunked prefill == whole prefill): an earlier part's K/V are appended by an
+// earlier nano-batch's KQV, which precedes the later parts on the compute stream.
+struct BatchView {
+  std::vector<int32_t> q_len, kv_prefix, page_indptr, page_ids, emit, caller_req, caller_row0;
+  nf_batch b{};
+  void finish() {
+    b.n_req = (int32_t)q_len.size();
+    b.q_len = q_len.data();
+    b.kv_prefix = kv_prefix.data();
+    b.page_indptr = page_indptr.data();
+    b.page_ids = page_ids.data();
+    b.emit = emit.data();
+  }
+};
+
+// balance == 2: every nano-batch gets exactly its token share (so GEMM tile
+// counts split evenly) and decode requests are assigned longest-context first
+// to the nano-batch with the least decode KV that still has token room; the
+// prefill requests (largest first) then fill the remaining room in nano-batch
+// order, split across nano-batches where they do not fit.
+void split_view(const nf_batch* b, int nn, const int32_t* share, BatchView* v, std::vector<int>* order,
+                std::vector<int>* cuts) {
+  const int n_req = b->n_req;
+  const int64_t T = batch_tokens(b);
+  int64_t tot = 0;
+  for (int k = 0; k < nn; ++k) tot += share[k];
+  std::vector<int64_t> cap(nn);
+  int64_t acc = 0;
+  for (int k = 0; k < nn; ++k) {
+    const int64_t next = (k + 1 == nn) ? T : (T * (acc + share[k])) / tot;
+    cap[k] = next - (T * acc) / tot;
+    acc += share[k];
+  }
+  std::vector<int64_t> caller_start(n_req + 1, 0);
+  for (int r = 0; r < n_req; ++r) caller_start[r + 1] = caller_start[r] + b->q_len[r];
+  std::vector<int> pre, dec;
+  for (int r = 0; r < n_req; ++r) (b->q_len[r] > 1 ? pre : dec).push_back(r);
+  std::stable_sort(dec.begin(), dec.end(), [&](int x, int y) { return b->kv_prefix[x] > b->kv_prefix[y]; });
+  std::stable_sort(pre.begin(), pre.end(), [&](int x, int y) { return b->q_len[x] > b->q_len[y]; });
+  struct Part { int r, off, len; };
+  std::vector<std::vector<Part>> grp(nn);
+  std::vector<double> kv(nn, 0.0);
+  for (int r : dec) {
+    int best = -1;
+    for (int k = 0; k < nn; ++k)
+      if (cap[k] > 0 && (best < 0 || kv[k] < kv[best])) best = k;
+    if (best < 0) best = nn - 1;
+    grp[best].push_back({r, 0, 1});
+    cap[best] -= 1;
+    kv[best] += b->kv_prefix[r] + 1;
+  }
+  int k = 0;
+  for (int r : pre) {
+    int off = 0;
+    while (off < b->q_len[r]) {
+      while (k < nn - 1 && cap[k] <= 0) ++k;
+      const int len = (int)std::min<int64_t>(b->q_len[r] - off, k == nn - 1 ? INT32_MAX : cap[k]);
+      grp[k].push_back({r, off, len});
+      cap[k] -= len;
+      off += len;
+    }
+  }
+  order->clear();
+  cuts->assign(1, 0);
+  for (int kk = 0; kk < nn; ++kk) {
+    std::stable_sort(grp[kk].begin(), grp[kk].end(), [](const Part& x, const Part& y) { return x.r < y.r; });
+    for (const Part& pt : grp[kk]) {
+      const int r = pt.r;
+      const int idx = (int)v->q_len.size();
+      v->q_len.push_back(pt.len);
+      v->kv_prefix.push_back(b->kv_prefix[r] + pt.off);
+      v->page_indptr.push_back((int32_t)v->page_ids.size());
+      for (int i = b->page_indptr[r]; i < b->page_indptr[r + 1]; ++i) v->page_ids.push_back(b->page_ids[i]);
+      const bool last = pt.off + pt.len == b->q_len[r];
+      v->emit.push_back(last && (b->emit == nullptr || b->emit[r]) ? 1 : 0);
+      v->caller_req.push_back(r);
+      v->caller_row0.push_back((int32_t)(caller_start[r] + pt.off));
+      order->push_back(idx);
+    }
+    cuts->push_back((int)order->size());
+  }
+  v->page_indptr.push_back((int32_t)v->page_ids.size());
+  v->finish();
+}
+
+// Internal request order and nano-batch cuts for this plan and batch.  With
+// balance == 2 (model step) the batch is re-expressed as a split view.
+void plan_order(const nf_plan* p, const nf_batch* b, bool allow_balance, std::vector<int>* order, std::vector<int>* cuts,
+                BatchView* view = nullptr, bool* use_view = nullptr) {
   const int n_req = b->n_req;
   const int nn = p->spec.n_nano;
+  if (use_view) *use_view = false;
   order->resize(n_req);
   std::iota(order->begin(), order->end(), 0);
   if (nn == 1) {
@@ -501,6 +616,11 @@ void plan_order(const nf_plan* p, const nf_batch* b, bool allow_balance, std::ve
     std::vector<int64_t> bound(n_req + 1, 0);
     for (int r = 0; r < n_req; ++r) bound[r + 1] = bound[r] + b->q_len[r];
     *cuts = snap_cuts_impl(bound, nn, p->spec.share);
+    return;
+  }
+  if (p->spec.balance == 2 && view) {
+    split_view(b, nn, p->spec.share, view, order, cuts);
+    if (use_view) *use_view = true;
     return;
   }
   std::vector<std::vector<int>> grp;
@@ -522,9 +642,14 @@ struct LayerCtx {
   CUtensorMap pool_map;
   CUtensorMap page_map;
   cudaStream_t cs, ms;  // compute / memory streams
+  cudaStream_t ns;      // network stream (TP collectives; == cs outside OVERLAP)
+  nf_comm* comm;
+  int cap_dense = 0, cap_dec = 0;  // partition sizes when green contexts are active (0: whole GPU)
 };
 
 int clampsm(int v) { return std::max(1, std::min(v, num_sms())); }
+int clamp_dense(const LayerCtx& L, int v) { return clampsm(L.cap_dense ? std::min(v, L.cap_dense) : v); }
+int clamp_dec(const LayerCtx& L, int v) { return clampsm(L.cap_dec ? std::min(v, L.cap_dec) : v); }
 
 // Decode kernel choice: the mma.sync kernel (8 independent warps per SM, one
 // 4-D TMA box per page) is the default: it reaches the HBM roofline at ~80 SMs.
@@ -548,6 +673,7 @@ nf_status run_kqv(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x
   GemmArgs a{};
   a.epi = EPI_QKV;
   a.sk_part = L.w->sk_part;
+  a.sk_slots = L.w->sk_slots;
   a.sk_flag = L.w->sk_flag;
   a.stages = L.p->spec.colocate ? 3 : 4;
   a.M = M;
@@ -570,7 +696,7 @@ nf_status run_kqv(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x
   a.kv_pool = (__nv_bfloat16*)pool;
   ProfScope ps(NF_OP_KQV, L.cs);
   NF_CUDA(launch_gemm(x + (int64_t)nr.t0 * c->d_model, c->d_model, (const __nv_bfloat16*)wt->w_qkv, c->d_model, a,
-                      clampsm(L.p->spec.sm[NF_OP_KQV]), L.cs));
+                      clamp_dense(L, L.p->spec.sm[NF_OP_KQV]), L.cs));
   return NF_OK;
 }
 
@@ -597,7 +723,7 @@ nf_status run_prefill(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
   const AttnArgs a = attn_args(L);
   const PrefillItem* pf = reinterpret_cast<const PrefillItem*>(L.meta_dev + L.m->off_pf) + nr.pf_off;
   ProfScope ps(NF_OP_PREFILL_ATTN, st);
-  NF_CUDA(launch_prefill_attention(L.pool_map, a, pf, nr.pf_n, clampsm(L.p->spec.sm[NF_OP_PREFILL_ATTN]), st));
+  NF_CUDA(launch_prefill_attention(L.pool_map, a, pf, nr.pf_n, clamp_dense(L, L.p->spec.sm[NF_OP_PREFILL_ATTN]), st));
   return NF_OK;
 }
 
@@ -609,10 +735,10 @@ nf_status run_decode(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
   const DecodeItem* dec = reinterpret_cast<const DecodeItem*>(L.meta_dev + L.m->off_dec) + nr.dec_off;
   ProfScope ps(NF_OP_DECODE_ATTN, st);
   if (use_tc_decode(c, L.p))
-    NF_CUDA(launch_decode_attention_tc(L.pool_map, a, dec, nr.dec_n, clampsm(L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
+    NF_CUDA(launch_decode_attention_tc(L.pool_map, a, dec, nr.dec_n, clamp_dec(L, L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
   else
     NF_CUDA(launch_decode_attention(L.pool_map, L.page_map, a, dec, nr.dec_n,
-                                    clampsm(L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
+                                    clamp_dec(L, L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
   return NF_OK;
 }
 
@@ -634,6 +760,7 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   GemmArgs a{};
   a.epi = EPI_RESID;
   a.sk_part = L.w->sk_part;
+  a.sk_slots = L.w->sk_slots;
   a.sk_flag = L.w->sk_flag;
   a.stages = L.p->spec.colocate ? 3 : 4;
   a.M = M;
@@ -648,12 +775,13 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   a.sq_stride = T;
   {
     ProfScope ps(NF_OP_O, L.cs);
-    NF_CUDA(launch_gemm(L.w->o + nr.t0 * qd, qd, (const __nv_bfloat16*)wt->w_o, qd, a, clampsm(L.p->spec.sm[NF_OP_O]), L.cs));
+    NF_CUDA(launch_gemm(L.w->o + nr.t0 * qd, qd, (const __nv_bfloat16*)wt->w_o, qd, a, clamp_dense(L, L.p->spec.sm[NF_OP_O]), L.cs));
   }
   // Up/Gate + SiLU(gate) * up, RMSNorm(h1) folded as a row scale
   GemmArgs u{};
   u.epi = EPI_SILU;
   u.sk_part = L.w->sk_part;
+  u.sk_slots = L.w->sk_slots;
   u.sk_flag = L.w->sk_flag;
   u.stages = L.p->spec.colocate ? 3 : 4;
   u.M = M;
@@ -669,13 +797,14 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   u.eps = c->rms_eps;
   {
     ProfScope ps(NF_OP_UG, L.cs);
-    NF_CUDA(launch_gemm(L.w->h1 + nr.t0 * D, D, (const __nv_bfloat16*)wt->w_gate_up, D, u, clampsm(L.p->spec.sm[NF_OP_UG]),
+    NF_CUDA(launch_gemm(L.w->h1 + nr.t0 * D, D, (const __nv_bfloat16*)wt->w_gate_up, D, u, clamp_dense(L, L.p->spec.sm[NF_OP_UG]),
                         L.cs));
   }
   // Down + residual: x_out = h1 + m W_d^T, partials of x_out for the next layer's norm
   GemmArgs d{};
   d.epi = EPI_RESID;
   d.sk_part = L.w->sk_part;
+  d.sk_slots = L.w->sk_slots;
   d.sk_flag = L.w->sk_flag;
   d.stages = L.p->spec.colocate ? 3 : 4;
   d.M = M;
@@ -690,9 +819,173 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
   d.sq_stride = T;
   {
     ProfScope ps(NF_OP_DOWN, L.cs);
-    NF_CUDA(launch_gemm(L.w->m + nr.t0 * F, F, (const __nv_bfloat16*)wt->w_down, F, d, clampsm(L.p->spec.sm[NF_OP_DOWN]),
+    NF_CUDA(launch_gemm(L.w->m + nr.t0 * F, F, (const __nv_bfloat16*)wt->w_down, F, d, clamp_dense(L, L.p->spec.sm[NF_OP_DOWN]),
                         L.cs));
   }
+  return NF_OK;
+}
+
+// Hand a buffer produced on the compute stream to the network stream and back.
+nf_status to_net(const LayerCtx& L) {
+  if (L.ns == L.cs) return NF_OK;
+  NF_CUDA(cudaEventRecord(L.p->ev_c2n, L.cs));
+  NF_CUDA(cudaStreamWaitEvent(L.ns, L.p->ev_c2n, 0));
+  return NF_OK;
+}
+nf_status from_net(const LayerCtx& L) {
+  if (L.ns == L.cs) return NF_OK;
+  NF_CUDA(cudaEventRecord(L.p->ev_n2c, L.ns));
+  NF_CUDA(cudaStreamWaitEvent(L.cs, L.p->ev_n2c, 0));
+  return NF_OK;
+}
+
+// Tensor-parallel dense tail of one nano-batch (reading A-12):
+//   col (nano 0): AG(attention out) -> O_col (+ x columns) -> AG -> h1
+//   row (others): O_row partial (+ x on rank 0) -> AR -> h1
+//   then column Up/Gate + SiLU, row Down partial (+ h1 on rank 0) -> AR -> x_out.
+// Residuals are folded into rank 0's partial before the AllReduce (one rounding).
+// RMS statistics of h1 / x_out come from one sum-of-squares pass (1 part per row).
+nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, const __nv_bfloat16* x,
+                            const nf_packed_layer* wt, __nv_bfloat16* x_out, float* part_out) {
+  const nf_model_cfg* c = L.c;
+  const int M = nr.t1 - nr.t0;
+  if (M <= 0) return NF_OK;
+  nf_comm* cm = L.comm;
+  const int N = c->tp_size, rank = c->tp_rank;
+  const int64_t D = c->d_model, Fl = c->d_ffn / N, qd = (int64_t)c->n_q_heads / N * c->head_dim;
+  const int64_t qd_full = qd * N, Dl = D / N;
+  const int T = L.m->T;
+  const int stages = L.p->spec.colocate ? 3 : 4;
+  __nv_bfloat16* h1 = L.w->h1 + nr.t0 * D;
+  if (col) {
+    // AG of the attention output rows of this nano-batch, then rank-major -> row-major
+    NF_TRY(to_net(L));
+    {
+      ProfScope ps(NF_OP_NET, L.ns);
+      NF_TRY(comm_all_gather(cm, L.w->o + nr.t0 * qd, L.w->ag, (size_t)M * qd, L.ns));
+    }
+    NF_TRY(from_net(L));
+    NF_CUDA(launch_interleave(L.w->ag, N, M, (int)qd, L.w->ocat, nullptr, L.cs));
+    GemmArgs a{};
+    a.epi = EPI_RESID;
+    a.stages = stages;
+    a.M = M;
+    a.N = (int)Dl;
+    a.K = (int)qd_full;
+    a.n_valid = (int)Dl;
+    a.out = L.w->hcol;
+    a.ldo = Dl;
+    a.resid = x + nr.t0 * D + rank * Dl;
+    a.ldr = D;
+    {
+      ProfScope ps(NF_OP_O, L.cs);
+      NF_CUDA(launch_gemm(L.w->ocat, qd_full, (const __nv_bfloat16*)wt->w_o, qd_full, a,
+                          clamp_dense(L, L.p->spec.sm[NF_OP_O]), L.cs));
+    }
+    NF_TRY(to_net(L));
+    {
+      ProfScope ps(NF_OP_NET, L.ns);
+      NF_TRY(comm_all_gather(cm, L.w->hcol, L.w->ag, (size_t)M * Dl, L.ns));
+    }
+    NF_TRY(from_net(L));
+    NF_CUDA(launch_interleave(L.w->ag, N, M, (int)Dl, h1, L.w->part_h1 + nr.t0, L.cs));
+  } else {
+    GemmArgs a{};
+    a.epi = rank == 0 ? EPI_RESID : EPI_STORE;
+    a.stages = stages;
+    a.M = M;
+    a.N = (int)D;
+    a.K = (int)qd;
+    a.n_valid = (int)D;
+    a.out = h1;
+    a.ldo = D;
+    a.resid = x + nr.t0 * D;
+    a.ldr = D;
+    {
+      ProfScope ps(NF_OP_O, L.cs);
+      NF_CUDA(launch_gemm(L.w->o + nr.t0 * qd, qd, (const __nv_bfloat16*)wt->w_o_row, qd, a,
+                          clamp_dense(L, L.p->spec.sm[NF_OP_O]), L.cs));
+    }
+    NF_TRY(to_net(L));
+    {
+      ProfScope ps(NF_OP_NET, L.ns);
+      NF_TRY(comm_all_reduce_bf16(cm, h1, (size_t)M * D, L.ns, L.w->red));
+    }
+    NF_TRY(from_net(L));
+    NF_CUDA(launch_gather_rows(h1, nullptr, M, (int)D, nullptr, L.w->part_h1 + nr.t0, L.cs));
+  }
+  // column-parallel Up/Gate + SiLU with the RMSNorm(h1) row scale (one partial per row)
+  GemmArgs u{};
+  u.epi = EPI_SILU;
+  u.stages = stages;
+  u.M = M;
+  u.N = (int)(((Fl + 127) / 128) * 256);
+  u.K = (int)D;
+  u.n_valid = (int)Fl;
+  u.out = L.w->m + nr.t0 * Fl;
+  u.ldo = Fl;
+  u.norm_part = L.w->part_h1 + nr.t0;
+  u.norm_nparts = 1;
+  u.norm_stride = T;
+  u.inv_d = 1.f / D;
+  u.eps = c->rms_eps;
+  {
+    ProfScope ps(NF_OP_UG, L.cs);
+    NF_CUDA(launch_gemm(h1, D, (const __nv_bfloat16*)wt->w_gate_up, D, u, clamp_dense(L, L.p->spec.sm[NF_OP_UG]), L.cs));
+  }
+  // row-parallel Down partial (+ h1 on rank 0) -> AR -> x_out
+  GemmArgs d{};
+  d.epi = rank == 0 ? EPI_RESID : EPI_STORE;
+  d.stages = stages;
+  d.M = M;
+  d.N = (int)D;
+  d.K = (int)Fl;
+  d.n_valid = (int)D;
+  d.out = x_out + nr.t0 * D;
+  d.ldo = D;
+  d.resid = h1;
+  d.ldr = D;
+  {
+    ProfScope ps(NF_OP_DOWN, L.cs);
+    NF_CUDA(launch_gemm(L.w->m + nr.t0 * Fl, Fl, (const __nv_bfloat16*)wt->w_down, Fl, d,
+                        clamp_dense(L, L.p->spec.sm[NF_OP_DOWN]), L.cs));
+  }
+  NF_TRY(to_net(L));
+  {
+    ProfScope ps(NF_OP_NET, L.ns);
+    NF_TRY(comm_all_reduce_bf16(cm, x_out + nr.t0 * D, (size_t)M * D, L.ns, L.w->red));
+  }
+  NF_TRY(from_net(L));
+  if (part_out) NF_CUDA(launch_gather_rows(x_out + nr.t0 * D, nullptr, M, (int)D, nullptr, part_out + nr.t0, L.cs));
+  return NF_OK;
+}
+
+nf_status run_tail(const LayerCtx& L, size_t k, const NanoRange& nr, const __nv_bfloat16* x, const nf_packed_layer* wt,
+                   __nv_bfloat16* x_out, float* part_out) {
+  if (L.c->tp_size > 1) return run_dense_tail_tp(L, nr, k == 0, x, wt, x_out, part_out);
+  return run_dense_tail(L, nr, x, wt, x_out, part_out);
+}
+
+// OVERLAP plans run on green-context partitions when available: fork the
+// caller stream into the compute / memory partition streams, join at the end.
+nf_status enter_partitions(nf_plan* p, LayerCtx* L, cudaStream_t caller) {
+  if (p->spec.mode != NF_OVERLAP || p->spec.colocate) return NF_OK;
+  if (!green_setup(p, p->spec.sm[NF_OP_DECODE_ATTN])) return NF_OK;
+  NF_CUDA(cudaEventRecord(p->ev_fork, caller));
+  NF_CUDA(cudaStreamWaitEvent(p->green_cs, p->ev_fork, 0));
+  NF_CUDA(cudaStreamWaitEvent(p->green_ms, p->ev_fork, 0));
+  L->cs = p->green_cs;
+  L->ms = p->green_ms;
+  L->cap_dense = p->green_dense_sms;
+  L->cap_dec = p->green_dec_sms;
+  return NF_OK;
+}
+nf_status leave_partitions(nf_plan* p, const LayerCtx& L, cudaStream_t caller) {
+  if (L.cs == caller) return NF_OK;
+  NF_CUDA(cudaEventRecord(p->ev_join_c, L.cs));
+  NF_CUDA(cudaEventRecord(p->ev_join_m, L.ms));
+  NF_CUDA(cudaStreamWaitEvent(caller, p->ev_join_c, 0));
+  NF_CUDA(cudaStreamWaitEvent(caller, p->ev_join_m, 0));
   return NF_OK;
 }
 
@@ -706,10 +999,10 @@ nf_status run_layer(nf_plan* p, const LayerCtx& L, const nf_packed_layer* wt, vo
   const auto& nanos = L.m->nanos;
   const int mode = p->spec.mode;
   if (mode != NF_OVERLAP) {
-    for (const auto& nr : nanos) {
-      if (!kqv_done) NF_TRY(run_kqv(L, nr, x, part, nparts, wt, pool));
-      NF_TRY(run_attn(L, nr, L.cs));
-      NF_TRY(run_dense_tail(L, nr, x, wt, x_out, part_out));
+    for (size_t k = 0; k < nanos.size(); ++k) {
+      if (!kqv_done) NF_TRY(run_kqv(L, nanos[k], x, part, nparts, wt, pool));
+      NF_TRY(run_attn(L, nanos[k], L.cs));
+      NF_TRY(run_tail(L, k, nanos[k], x, wt, x_out, part_out));
     }
     return NF_OK;
   }
@@ -725,7 +1018,7 @@ nf_status run_layer(nf_plan* p, const LayerCtx& L, const nf_packed_layer* wt, vo
   }
   for (size_t k = 0; k < nanos.size(); ++k) {
     NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_att[k], 0));
-    NF_TRY(run_dense_tail(L, nanos[k], x, wt, x_out, part_out));
+    NF_TRY(run_tail(L, k, nanos[k], x, wt, x_out, part_out));
   }
   return NF_OK;
 }
@@ -740,8 +1033,12 @@ nf_status nf_layer_forward(const nf_plan* plan, nf_comm* comm, const nf_packed_l
   nf_plan* p = const_cast<nf_plan*>(plan);
   const nf_model_cfg* c = &p->cfg;
   NF_TRY(validate_batch(c, b));
-  if (c->tp_size > 1) return set_error(NF_EUNSUPPORTED, "tp_size > 1 requires the TP executor (not built yet)");
-  (void)comm;
+  if (c->tp_size > 1) {
+    if (!comm) return set_error(NF_EINVAL, "tp_size > 1 needs a communicator");
+    if (comm_size(comm) != c->tp_size || comm_rank(comm) != c->tp_rank)
+      return set_error(NF_EINVAL, "communicator size/rank %d/%d != cfg %d/%d", comm_size(comm), comm_rank(comm),
+                       c->tp_size, c->tp_rank);
+  }
   if (!w || !kv_pool || !x_in || !x_out || !ws) return set_error(NF_EINVAL, "NULL pointer argument");
   Workspace wsp = carve_workspace(c, b, ws);
   if (ws_bytes < wsp.total) return set_error(NF_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, wsp.total);
@@ -761,11 +1058,15 @@ nf_status nf_layer_forward(const nf_plan* plan, nf_comm* comm, const nf_packed_l
   L.meta_dev = wsp.meta;
   L.cs = cs;
   L.ms = p->mem_stream;
+  L.ns = p->spec.mode == NF_OVERLAP ? p->net_stream : cs;
+  L.comm = comm;
   NF_CUDA(make_pool_tmap(&L.pool_map, kv_pool, b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim, c->page_size));
   NF_CUDA(make_page_tmap(&L.page_map, kv_pool, b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim, c->page_size));
   // RMS partials of x_in (one part per row)
   NF_CUDA(launch_gather_rows((const __nv_bfloat16*)x_in, nullptr, m.T, c->d_model, nullptr, wsp.part_a, cs));
+  NF_TRY(enter_partitions(p, &L, cs));
   NF_TRY(run_layer(p, L, w, kv_pool, (const __nv_bfloat16*)x_in, wsp.part_a, 1, (__nv_bfloat16*)x_out, nullptr, false));
+  NF_TRY(leave_partitions(p, L, cs));
   return NF_OK;
 }
 
@@ -776,8 +1077,12 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
   nf_plan* p = const_cast<nf_plan*>(plan);
   const nf_model_cfg* c = &p->cfg;
   NF_TRY(validate_batch(c, b));
-  if (c->tp_size > 1) return set_error(NF_EUNSUPPORTED, "tp_size > 1 requires the TP executor (not built yet)");
-  (void)comm;
+  if (c->tp_size > 1) {
+    if (!comm) return set_error(NF_EINVAL, "tp_size > 1 needs a communicator");
+    if (comm_size(comm) != c->tp_size || comm_rank(comm) != c->tp_rank)
+      return set_error(NF_EINVAL, "communicator size/rank %d/%d != cfg %d/%d", comm_size(comm), comm_rank(comm),
+                       c->tp_size, c->tp_rank);
+  }
   if (!w || !w->embed || !w->layers || !w->lm_head_packed || !kv_pools || !token_ids || !next_ids || !ws)
     return set_error(NF_EINVAL, "NULL pointer argument");
   for (int l = 0; l < c->n_layers; ++l)
@@ -786,9 +1091,14 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
   if (ws_bytes < wsp.total) return set_error(NF_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, wsp.total);
   NF_TRY(ensure_runtime(p));
   std::vector<int> order, cuts;
-  plan_order(p, b, true, &order, &cuts);
+  BatchView view;
+  bool use_view = false;
+  plan_order(p, b, true, &order, &cuts, &view, &use_view);
   StepMeta m;
-  build_meta(c, b, order, cuts, &m);
+  if (use_view)
+    build_meta(c, &view.b, order, cuts, &m, &view.caller_row0, &view.caller_req);
+  else
+    build_meta(c, b, order, cuts, &m);
   cudaStream_t cs = (cudaStream_t)stream;
   NF_TRY(upload_meta(p, m, wsp.meta, cs));
   NF_CUDA(cudaMemsetAsync(wsp.sk_flag, 0, (size_t)wsp.sk_flag_n * 4, cs));
@@ -806,6 +1116,9 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
   L.meta_dev = wsp.meta;
   L.cs = cs;
   L.ms = p->mem_stream;
+  L.ns = p->spec.mode == NF_OVERLAP ? p->net_stream : cs;
+  L.comm = comm;
+  const int NPn = c->tp_size > 1 ? 1 : NP;  // RMS partials per row of layer outputs
   __nv_bfloat16 *x = wsp.xa, *y = wsp.xb;
   float *px = wsp.part_a, *py = wsp.part_b;
   std::vector<CUtensorMap> maps(c->n_layers), pmaps(c->n_layers);
@@ -815,6 +1128,7 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
     NF_CUDA(make_page_tmap(&pmaps[l], kv_pools[l], b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim,
                            c->page_size));
   }
+  NF_TRY(enter_partitions(p, &L, cs));
   if (p->spec.mode != NF_OVERLAP) {
     int nparts = 1;
     for (int l = 0; l < c->n_layers; ++l) {
@@ -823,7 +1137,7 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
       NF_TRY(run_layer(p, L, &w->layers[l], kv_pools[l], x, px, nparts, y, py, false));
       std::swap(x, y);
       std::swap(px, py);
-      nparts = NP;
+      nparts = NPn;
     }
   } else {
     // Operation-level pipeline across layers (single-GPU variant
@@ -835,31 +1149,32 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
     L.page_map = pmaps[0];
     for (size_t k = 0; k < nanos.size(); ++k) {
       NF_TRY(run_kqv(L, nanos[k], x, px, 1, &w->layers[0], kv_pools[0]));
-      NF_CUDA(cudaEventRecord(p->ev_kqv[k], cs));
+      NF_CUDA(cudaEventRecord(p->ev_kqv[k], L.cs));
       NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
       NF_TRY(run_decode(L, nanos[k], L.ms));
       NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
-      NF_TRY(run_prefill(L, nanos[k], cs));
+      NF_TRY(run_prefill(L, nanos[k], L.cs));
     }
     for (int l = 0; l < c->n_layers; ++l) {
       for (size_t k = 0; k < nanos.size(); ++k) {
-        NF_CUDA(cudaStreamWaitEvent(cs, p->ev_att[k], 0));
-        NF_TRY(run_dense_tail(L, nanos[k], x, &w->layers[l], y, py));
+        NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_att[k], 0));
+        NF_TRY(run_tail(L, k, nanos[k], x, &w->layers[l], y, py));
         if (l + 1 < c->n_layers) {
           L.pool_map = maps[l + 1];
           L.page_map = pmaps[l + 1];
-          NF_TRY(run_kqv(L, nanos[k], y, py, NP, &w->layers[l + 1], kv_pools[l + 1]));
-          NF_CUDA(cudaEventRecord(p->ev_kqv[k], cs));
+          NF_TRY(run_kqv(L, nanos[k], y, py, NPn, &w->layers[l + 1], kv_pools[l + 1]));
+          NF_CUDA(cudaEventRecord(p->ev_kqv[k], L.cs));
           NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
           NF_TRY(run_decode(L, nanos[k], L.ms));
           NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
-          NF_TRY(run_prefill(L, nanos[k], cs));
+          NF_TRY(run_prefill(L, nanos[k], L.cs));
         }
       }
       std::swap(x, y);
       std::swap(px, py);
     }
   }
+  NF_TRY(leave_partitions(p, L, cs));
   // final RMSNorm (gamma folded into lm_head_packed) + LM head + argmax
   NF_CUDA(launch_fill_i32(next_ids, b->n_req, -1, cs));
   if (m.n_emit > 0) {
@@ -868,6 +1183,7 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
     GemmArgs a{};
     a.epi = EPI_ARGMAX;
     a.sk_part = (&wsp)->sk_part;
+    a.sk_slots = (&wsp)->sk_slots;
     a.sk_flag = (&wsp)->sk_flag;
     a.M = m.n_emit;
     a.N = c->vocab;
@@ -881,8 +1197,10 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
     NF_CUDA(launch_argmax_reduce(wsp.am_val, wsp.am_idx, (c->vocab + GEMM_BN - 1) / GEMM_BN, m.n_emit, m.n_emit,
                                  wsp.meta + m.off_emit_req, next_ids, cs));
   }
-  // join the memory stream (nothing outstanding in sequential modes)
+  // join the memory and network streams (nothing outstanding in sequential modes)
   NF_CUDA(cudaEventRecord(p->ev_join, p->mem_stream));
+  NF_CUDA(cudaStreamWaitEvent(cs, p->ev_join, 0));
+  NF_CUDA(cudaEventRecord(p->ev_join, p->net_stream));
   NF_CUDA(cudaStreamWaitEvent(cs, p->ev_join, 0));
   return NF_OK;
 }
@@ -905,11 +1223,13 @@ nf_status nf_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, v
   a.ldo = ldc;
   const int grid_max = std::max(1, std::min<int>(sm_budget, num_sms()));
   const int tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + 127) / 128);
+  const int slots = std::max(148, ((M + GEMM_BM - 1) / GEMM_BM) * ((N + 255) / 256));
   if (ws) {
-    if (ws_bytes < gemm_sk_bytes(148, tiles)) return set_error(NF_EINVAL, "gemm workspace too small");
+    if (ws_bytes < gemm_sk_bytes(slots, tiles)) return set_error(NF_EINVAL, "gemm workspace too small");
     if ((uintptr_t)ws & 255) return set_error(NF_EINVAL, "gemm workspace must be 256-byte aligned");
     a.sk_part = (float*)ws;
-    a.sk_flag = (int*)((char*)ws + (size_t)148 * GEMM_BM * GEMM_BN * 4);
+    a.sk_slots = slots;
+    a.sk_flag = (int*)((char*)ws + (size_t)slots * GEMM_BM * GEMM_SK_LD * 4);
     NF_CUDA(cudaMemsetAsync(a.sk_flag, 0, (size_t)tiles * 4, (cudaStream_t)stream));
   }
   NF_CUDA(launch_gemm((const __nv_bfloat16*)A, lda, (const __nv_bfloat16*)B, ldb, a, grid_max, (cudaStream_t)stream));
@@ -918,7 +1238,8 @@ nf_status nf_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, v
 
 size_t nf_gemm_workspace_bytes(int32_t M, int32_t N) {
   const int tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + 127) / 128);
-  return gemm_sk_bytes(148, tiles);
+  const int slots = std::max(148, ((M + GEMM_BM - 1) / GEMM_BM) * ((N + 255) / 256));
+  return gemm_sk_bytes(slots, tiles);
 }
 
 nf_status nf_attention(const nf_model_cfg* cfg, const nf_batch* b, const void* q, const void* kv_pool, void* o, void* ws,

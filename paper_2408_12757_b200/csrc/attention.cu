@@ -36,7 +36,10 @@ NF_DEV uint32_t ldg_u32(const __nv_bfloat16* p) { return *reinterpret_cast<const
 
 template <int HD, int DEC_WARPS>
 constexpr int dec_stages() {
-  return HD == 128 ? (DEC_WARPS == 8 ? 3 : DEC_WARPS == 6 ? 4 : 2) : (DEC_WARPS == 8 ? 6 : DEC_WARPS == 6 ? 8 : 4);
+  // per-page compute (~1.3 us) exceeds HBM latency (~0.9 us, tools/tma_probe.py), so two stages per
+  // warp suffice and the smem goes to more warps (more pages in flight per SM)
+  return HD == 128 ? (DEC_WARPS >= 12 ? 2 : DEC_WARPS == 8 ? 3 : DEC_WARPS == 6 ? 4 : 2)
+                   : (DEC_WARPS >= 12 ? 4 : DEC_WARPS == 8 ? 6 : DEC_WARPS == 6 ? 8 : 4);
 }
 
 template <int HD, int DEC_WARPS>
@@ -435,9 +438,11 @@ cudaError_t launch_decode_hd(const CUtensorMap& m, const CUtensorMap& pm, const 
     const char* e = getenv("NF_DEC_WARPS");
     env_w = e ? atoi(e) : 0;
   }
-  const int w = a.dec_warps == 4 ? 4 : (env_w == 6 ? 6 : 8);
+  const int w = a.dec_warps == 4 ? 4 : (env_w ? env_w : (HD == 128 ? 12 : 8));
   if (w == 4) return launch_decode_hdw<HD, 4>(m, pm, a, items, n_items, sm_budget, st);
   if (w == 6) return launch_decode_hdw<HD, 6>(m, pm, a, items, n_items, sm_budget, st);
+  if (w == 12) return launch_decode_hdw<HD, 12>(m, pm, a, items, n_items, sm_budget, st);
+  if (w == 14) return launch_decode_hdw<HD, 14>(m, pm, a, items, n_items, sm_budget, st);
   return launch_decode_hdw<HD, 8>(m, pm, a, items, n_items, sm_budget, st);
 }
 

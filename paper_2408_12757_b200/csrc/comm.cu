@@ -6,13 +6,52 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 
 #include "host.h"
+#include "misc.cuh"
+
+namespace nf {
+// Single-process, single-GPU emulation of a TP group (tests / rank-local
+// studies): N ranks are N host threads sharing one device; collectives meet at
+// a host barrier and exchange device buffers with stream-ordered copies.
+// AllReduce sums the N inputs in rank order with fp32 accumulation, so every
+// rank gets bit-identical results.
+struct LocalGroup {
+  int n;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<const void*> src;
+  std::vector<cudaStream_t> st;
+  std::vector<cudaEvent_t> ev_ready, ev_done;
+  explicit LocalGroup(int n_) : n(n_), src(n_), st(n_), ev_ready(n_), ev_done(n_) {
+    for (int i = 0; i < n; ++i) {
+      cudaEventCreateWithFlags(&ev_ready[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming);
+    }
+  }
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+}  // namespace nf
 
 struct nf_comm {
   ncclComm_t comm = nullptr;
   int tp_size = 1, tp_rank = 0;
+  std::shared_ptr<nf::LocalGroup> group;  // emulated group (nf_comm_create_local)
 };
 
 namespace nf {
@@ -47,12 +86,56 @@ nf_status load_nccl() {
 }
 }  // namespace
 
+int comm_size(const nf_comm* c) { return c ? c->tp_size : 1; }
+int comm_rank(const nf_comm* c) { return c ? c->tp_rank : 0; }
+
+// recv = [rank 0's send | rank 1's send | ...] (count bf16 elements each)
 nf_status comm_all_gather(nf_comm* c, const void* send, void* recv, size_t count_bf16, cudaStream_t st) {
+  if (c->group) {
+    LocalGroup& g = *c->group;
+    const int r = c->tp_rank;
+    const size_t bytes = count_bf16 * 2;
+    g.src[r] = send;
+    g.st[r] = st;
+    if (cudaEventRecord(g.ev_ready[r], st) != cudaSuccess) return set_error(NF_ECUDA, "emulated AG record");
+    g.barrier();
+    for (int q = 0; q < g.n; ++q) {
+      cudaStreamWaitEvent(st, g.ev_ready[q], 0);
+      if (cudaMemcpyAsync((char*)recv + q * bytes, g.src[q], bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return set_error(NF_ECUDA, "emulated AG copy");
+    }
+    cudaEventRecord(g.ev_done[r], st);
+    g.barrier();
+    for (int q = 0; q < g.n; ++q) cudaStreamWaitEvent(st, g.ev_done[q], 0);  // senders reusable after all copies
+    g.barrier();
+    return NF_OK;
+  }
   ncclResult_t r = g_nccl.allGather(send, recv, count_bf16, ncclBfloat16, c->comm, st);
   if (r != ncclSuccess) return set_error(NF_ENCCL, "ncclAllGather: %s", g_nccl.getErrorString(r));
   return NF_OK;
 }
-nf_status comm_all_reduce_bf16(nf_comm* c, void* buf, size_t count, cudaStream_t st) {
+
+// in-place sum over ranks; scratch: count bf16 elements of device memory (emulation only)
+nf_status comm_all_reduce_bf16(nf_comm* c, void* buf, size_t count, cudaStream_t st, void* scratch) {
+  if (c->group) {
+    LocalGroup& g = *c->group;
+    const int r = c->tp_rank;
+    g.src[r] = buf;
+    g.st[r] = st;
+    if (cudaEventRecord(g.ev_ready[r], st) != cudaSuccess) return set_error(NF_ECUDA, "emulated AR record");
+    g.barrier();
+    for (int q = 0; q < g.n; ++q) cudaStreamWaitEvent(st, g.ev_ready[q], 0);
+    std::vector<const void*> srcs(g.src.begin(), g.src.end());
+    if (launch_sum_bf16(srcs.data(), g.n, (__nv_bfloat16*)scratch, count, st) != cudaSuccess)
+      return set_error(NF_ECUDA, "emulated AR sum");
+    cudaEventRecord(g.ev_done[r], st);
+    g.barrier();
+    for (int q = 0; q < g.n; ++q) cudaStreamWaitEvent(st, g.ev_done[q], 0);  // everyone has read every input
+    if (cudaMemcpyAsync(buf, scratch, count * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return set_error(NF_ECUDA, "emulated AR copy");
+    g.barrier();
+    return NF_OK;
+  }
   ncclResult_t r = g_nccl.allReduce(buf, buf, count, ncclBfloat16, ncclSum, c->comm, st);
   if (r != ncclSuccess) return set_error(NF_ENCCL, "ncclAllReduce: %s", g_nccl.getErrorString(r));
   return NF_OK;
@@ -100,9 +183,22 @@ nf_status nf_comm_create(int32_t tp_size, int32_t tp_rank, const void* id_128, n
   return NF_OK;
 }
 
+nf_status nf_comm_create_local(int32_t tp_size, nf_comm** comms_out) {
+  if (!comms_out || tp_size < 1 || tp_size > 64) return set_error(NF_EINVAL, "bad tp_size / output");
+  auto g = std::make_shared<LocalGroup>(tp_size);
+  for (int r = 0; r < tp_size; ++r) {
+    nf_comm* c = new nf_comm();
+    c->tp_size = tp_size;
+    c->tp_rank = r;
+    c->group = g;
+    comms_out[r] = c;
+  }
+  return NF_OK;
+}
+
 void nf_comm_destroy(nf_comm* c) {
   if (!c) return;
-  if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+  if (!c->group && c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
   delete c;
 }
 

@@ -94,10 +94,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // iterations (the end of its range) adds the partials in CTA order and runs
   // the fused epilogue -- no CTA ever waits on a lower one (no serial chain).
   const int G = gridDim.x;
-  const bool sk = args.sk_part != nullptr && (tiles % G) != 0;
-  const int tiles_dp = sk ? max(0, tiles / G - 1) * G : tiles;
-  const int64_t total_sk = (int64_t)(tiles - tiles_dp) * num_kb;
+  // split-K=2 schedule (args.split == 2): units (tile, K-half) in tile-major
+  // order, so both halves of a tile run at the same time on adjacent CTAs (L2
+  // reuse of the weight tile across m-tiles is kept); half 1 leaves an fp32
+  // partial in the tile's slot, half 0 adds it in its epilogue.
+  const bool split2 = args.split == 2 && args.sk_part != nullptr;
+  const bool sk = !split2 && args.sk_part != nullptr && (tiles % G) != 0;
+  const int tiles_dp = (sk || split2) ? (sk ? max(0, tiles / G - 1) * G : 0) : tiles;
+  const int64_t total_sk = sk ? (int64_t)(tiles - tiles_dp) * num_kb : 0;
+  const int kb_half = num_kb / 2;
   auto for_each_seg = [&](auto&& fn) {
+    if (split2) {
+      for (int u = blockIdx.x; u < 2 * tiles; u += G) {
+        if (u & 1) fn(u >> 1, kb_half, num_kb);
+        else fn(u >> 1, 0, kb_half);
+      }
+      return;
+    }
     for (int t = blockIdx.x; t < tiles_dp; t += G) fn(t, 0, num_kb);
     if (total_sk > 0) {
       int64_t i = (int64_t)blockIdx.x * total_sk / G;
@@ -195,7 +208,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (kb0 > 0) {
         // stream-K contributor (tile tail, processed first in this CTA's range):
         // raw fp32 partial tile to this CTA's slot, then signal the tile's owner
-        float* slot = args.sk_part + ((size_t)blockIdx.x * GEMM_BM + trow) * GEMM_SK_LD;
+        const size_t slot_idx = split2 ? (size_t)tile : (size_t)blockIdx.x;
+        float* slot = args.sk_part + (slot_idx * GEMM_BM + trow) * GEMM_SK_LD;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t rr[32];
@@ -221,8 +235,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // range); the tail iterations were done by the next CTAs, which run them first
       int c_first = blockIdx.x + 1, n_contrib = 0;
       if (kb1 < num_kb) {
-        const int64_t last = (int64_t)(tile - tiles_dp) * num_kb + num_kb - 1;
-        n_contrib = (int)(((last + 1) * G - 1) / total_sk) - (int)blockIdx.x;
+        if (split2) {
+          c_first = tile;  // the tile's own partial slot
+          n_contrib = 1;
+        } else {
+          const int64_t last = (int64_t)(tile - tiles_dp) * num_kb + num_kb - 1;
+          n_contrib = (int)(((last + 1) * G - 1) / total_sk) - (int)blockIdx.x;
+        }
         if (trow == 0) {
           while (ld_acquire_gpu(args.sk_flag + tile) < n_contrib) __nanosleep(32);
           args.sk_flag[tile] = 0;  // self-reset for the next launch
@@ -497,7 +516,25 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     sk_env = (e && e[0] == '1') ? 1 : 0;
   }
   GemmArgs a2 = args;
-  if (!sk_env) a2.sk_part = nullptr;
+  // split-K=2 when it strictly lowers the number of tile-rounds (nano-batch-sized
+  // GEMMs with 1-2 waves of tiles), needs the scratch slots and K >= 8192 (a half tile
+  // must outweigh writing + reading its 128 KB fp32 partial; measured on O vs Down)
+  const int num_kb = (args.K + GEMM_BK - 1) / GEMM_BK;
+  const int rounds1 = (tiles + grid - 1) / grid;
+  const int g2 = std::min(sm_budget, 2 * tiles);
+  const double rounds2 = ((2 * tiles + g2 - 1) / g2) / 2.0;
+  static int split_env = -1;
+  if (split_env < 0) {
+    const char* e = getenv("NF_SPLITK");
+    split_env = e ? atoi(e) : 1;
+  }
+  a2.split = 1;
+  if (split_env && args.sk_part != nullptr && args.sk_slots >= tiles && num_kb >= 128 && rounds2 < rounds1 &&
+      args.epi != EPI_SILU && args.epi != EPI_ARGMAX) {
+    a2.split = 2;
+    grid = g2;
+  }
+  if (!sk_env && a2.split != 2) a2.sk_part = nullptr;
   if (grid < 1) grid = 1;
   kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, a2);
   count_launch();

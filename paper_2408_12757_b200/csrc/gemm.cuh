@@ -55,6 +55,8 @@ struct GemmArgs {
   // [grid][128][256], arrival counters per tile (zero at launch, self-resetting)
   float* sk_part;
   int* sk_flag;
+  int sk_slots;         // partial slots available in sk_part (split-K=2 needs one per tile)
+  int split;            // set by the launcher: 1 or 2 (split-K=2 schedule)
   // EPI_ARGMAX
   float* am_val;
   int* am_idx;
@@ -62,7 +64,7 @@ struct GemmArgs {
 };
 
 // Bytes of stream-K scratch for a GEMM with this many tiles at this grid.
-inline size_t gemm_sk_bytes(int grid, int tiles) { return (size_t)grid * GEMM_BM * GEMM_BN * 4 + (size_t)tiles * 4 + 256; }
+inline size_t gemm_sk_bytes(int slots, int tiles) { return (size_t)slots * GEMM_BM * 256 * 4 + (size_t)tiles * 4 + 256; }
 
 // A: [M, K] row-major (lda elements), B: [N, K] row-major (ldb elements).
 // grid = min(tiles, sm_budget) persistent CTAs, one per SM.

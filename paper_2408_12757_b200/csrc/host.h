@@ -50,7 +50,8 @@ struct StepMeta {
 size_t meta_words_bound(const nf_model_cfg* c, const nf_batch* b);
 // order: internal request order (size n_req); req_cuts: nano-batch boundaries in that order.
 void build_meta(const nf_model_cfg* c, const nf_batch* b, const std::vector<int>& order, const std::vector<int>& req_cuts,
-                StepMeta* m);
+                StepMeta* m, const std::vector<int32_t>* caller_row0 = nullptr,
+                const std::vector<int32_t>* caller_req = nullptr);
 void balance_requests(const nf_batch* b, int nn, const int32_t* share, std::vector<std::vector<int>>* groups);
 std::vector<int> snap_cuts_impl(const std::vector<int64_t>& row_start_of_boundary, int n_nano, const int32_t* share);
 
@@ -60,13 +61,23 @@ struct Workspace {
   float *part_a, *part_b, *part_h1, *lm_part, *am_val;
   int* am_idx;
   float* red;  // TP partial sums (f32)
+  __nv_bfloat16 *ag, *ocat, *hcol;  // TP: gathered (rank-major) staging, interleaved O input, O-col output
   float* sk_part;  // stream-K partial tiles [148][128][256] f32
   int* sk_flag;    // stream-K tile counters
   int sk_flag_n;
+  int sk_slots;
   size_t total;
 };
 Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base);
 
+}  // namespace nf
+
+namespace nf {
+bool green_setup(nf_plan* p, int dec_sms);
+int comm_size(const nf_comm* c);
+int comm_rank(const nf_comm* c);
+nf_status comm_all_gather(nf_comm* c, const void* send, void* recv, size_t count_bf16, cudaStream_t st);
+nf_status comm_all_reduce_bf16(nf_comm* c, void* buf, size_t count, cudaStream_t st, void* scratch);
 }  // namespace nf
 
 struct nf_plan {
@@ -79,6 +90,14 @@ struct nf_plan {
   cudaEvent_t ev_kqv[NF_MAX_NANO] = {};
   cudaEvent_t ev_att[NF_MAX_NANO] = {};
   cudaEvent_t ev_join = nullptr;
+  cudaStream_t net_stream = nullptr;
+  cudaEvent_t ev_c2n = nullptr, ev_n2c = nullptr;
+  // green-context SM partitions (OVERLAP plans; green.cpp)
+  bool green_tried = false, green_ok = false;
+  std::string green_note = "not used";
+  cudaStream_t green_cs = nullptr, green_ms = nullptr;
+  int green_dec_sms = 0, green_dense_sms = 0;
+  cudaEvent_t ev_fork = nullptr, ev_join_c = nullptr, ev_join_m = nullptr;
   cudaEvent_t ev_upload[2] = {};
   void* pinned[2] = {nullptr, nullptr};
   size_t pinned_cap[2] = {0, 0};

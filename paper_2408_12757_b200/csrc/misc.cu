@@ -90,6 +90,43 @@ __global__ void pack_gate_up_kernel(const __nv_bfloat16* __restrict__ gate, cons
   }
 }
 
+// dst[row][q*C + c] = src[q][row][c] for q < n (rank-major gather -> row-major),
+// optional per-row sum of squares of the written values into part[row]
+__global__ void interleave_kernel(const __nv_bfloat16* __restrict__ src, int n, int rows, int C,
+                                  __nv_bfloat16* __restrict__ dst, float* __restrict__ part) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  float sq = 0.f;
+  const int cv = C / 8;
+  for (int i = lane; i < n * cv; i += 32) {
+    const int q = i / cv, c = i % cv;
+    const uint4 u = reinterpret_cast<const uint4*>(src + ((int64_t)q * rows + warp) * C)[c];
+    reinterpret_cast<uint4*>(dst + (int64_t)warp * n * C + (int64_t)q * C)[c] = u;
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = unpack_bf16x2(w[k]);
+      sq = fmaf(f.x, f.x, sq);
+      sq = fmaf(f.y, f.y, sq);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane == 0 && part) part[warp] = sq;
+}
+
+struct SumPtrs {
+  const __nv_bfloat16* p[8];
+};
+// out[i] = bf16(sum_q in_q[i]) accumulated in fp32 in rank order (n <= 8)
+__global__ void sum_bf16_kernel(SumPtrs in, int n, __nv_bfloat16* __restrict__ out, size_t count) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int q = 0; q < n; ++q) acc += __bfloat162float(in.p[q][i]);
+    out[i] = __float2bfloat16_rn(acc);
+  }
+}
+
 int grid_for(int64_t n, int block) {
   int64_t g = (n + block - 1) / block;
   return (int)(g > 148 * 32 ? 148 * 32 : (g < 1 ? 1 : g));
@@ -117,6 +154,23 @@ cudaError_t launch_argmax_reduce(const float* val, const int* idx, int ntiles, i
                                  const int* row_req, int* next_ids, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
   argmax_reduce_kernel<<<(rows + 127) / 128, 128, 0, st>>>(val, idx, ntiles, stride, rows, row_req, next_ids);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_interleave(const __nv_bfloat16* src, int n, int rows, int C, __nv_bfloat16* dst, float* part,
+                              cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  interleave_kernel<<<(rows + 7) / 8, 256, 0, st>>>(src, n, rows, C, dst, part);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_bf16(const void* const* in, int n, __nv_bfloat16* out, size_t count, cudaStream_t st) {
+  if (n > 8) return cudaErrorInvalidValue;
+  SumPtrs ps{};
+  for (int q = 0; q < n; ++q) ps.p[q] = (const __nv_bfloat16*)in[q];
+  sum_bf16_kernel<<<grid_for((int64_t)count, 256), 256, 0, st>>>(ps, n, out, count);
   count_launch();
   return cudaGetLastError();
 }

@@ -10,6 +10,9 @@ cudaError_t launch_gather_ids_embed(const __nv_bfloat16* embed, const int* token
                                     __nv_bfloat16* dst, float* part, cudaStream_t st);
 cudaError_t launch_argmax_reduce(const float* val, const int* idx, int ntiles, int64_t stride, int rows,
                                  const int* row_req, int* next_ids, cudaStream_t st);
+cudaError_t launch_interleave(const __nv_bfloat16* src, int n, int rows, int C, __nv_bfloat16* dst, float* part,
+                              cudaStream_t st);
+cudaError_t launch_sum_bf16(const void* const* in, int n, __nv_bfloat16* out, size_t count, cudaStream_t st);
 cudaError_t launch_fill_i32(int* p, int n, int v, cudaStream_t st);
 cudaError_t launch_scale_cols(const __nv_bfloat16* src, const __nv_bfloat16* gamma, int64_t rows, int cols,
                               __nv_bfloat16* dst, cudaStream_t st);

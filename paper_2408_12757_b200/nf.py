@@ -89,9 +89,11 @@ _sig("nf_plan_create", C.c_int, C.POINTER(ModelCfg), C.POINTER(_Batch), C.POINTE
 _sig("nf_plan_get_spec", C.c_int, C.c_void_p, C.POINTER(PlanSpec))
 _sig("nf_plan_export_csv", C.c_int, C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t))
 _sig("nf_plan_destroy", None, C.c_void_p)
+_sig("nf_plan_runtime_note", C.c_char_p, C.c_void_p)
 _sig("nf_comm_unique_id", C.c_int, C.c_void_p)
 _sig("nf_comm_create", C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p))
 _sig("nf_comm_destroy", None, C.c_void_p)
+_sig("nf_comm_create_local", C.c_int, C.c_int32, C.POINTER(C.c_void_p))
 _sig("nf_packed_layer_bytes", C.c_int, C.POINTER(ModelCfg), C.POINTER(C.c_size_t))
 _sig("nf_pack_layer", C.c_int, C.POINTER(ModelCfg), C.POINTER(LayerWeights), C.POINTER(PackedLayer), C.c_void_p)
 _sig("nf_pack_lm_head", C.c_int, C.POINTER(ModelCfg), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
@@ -119,7 +121,7 @@ class Span(C.Structure):
 _sig("nf_profile_timeline", C.c_int, C.POINTER(Span), C.c_int32, P_i32)
 PROF_NAMES = ["kqv", "decode_attn", "prefill_attn", "o_proj", "up_gate", "down", "net", "lm_head", "misc"]
 
-EXPORTED = ["nf_gemm_workspace_bytes", "nf_profile_timeline", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
+EXPORTED = ["nf_plan_runtime_note", "nf_comm_create_local", "nf_gemm_workspace_bytes", "nf_profile_timeline", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
             "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_comm_unique_id",
             "nf_comm_create", "nf_comm_destroy", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
             "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_gemm_bf16", "nf_attention"]
@@ -192,7 +194,7 @@ class Plan:
         sm = [148] * OP_COUNT if sm is None else list(sm)
         for i in range(OP_COUNT):
             spec.sm[i] = int(sm[i])
-        spec.balance = int(balance)
+        spec.balance = int(balance)  # bool True -> 1
         spec.colocate = int(colocate)
         h = C.c_void_p()
         _check(lib.nf_plan_create_explicit(C.byref(cfg), C.byref(spec), C.byref(h)))
@@ -206,6 +208,9 @@ class Plan:
         h = C.c_void_p()
         _check(lib.nf_plan_create(C.byref(cfg), C.byref(shape.c), arr, len(points), C.byref(opts), C.byref(h)))
         return cls(h.value)
+
+    def runtime_note(self) -> str:
+        return lib.nf_plan_runtime_note(self.h).decode()
 
     def spec(self) -> PlanSpec:
         s = PlanSpec()
@@ -316,6 +321,17 @@ def comm_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib.nf_comm_unique_id(buf))
     return buf.raw
+
+
+def comm_create_local(tp_size: int):
+    """Handles of an emulated single-GPU TP group (one per rank; drive rank r from thread r)."""
+    arr = (C.c_void_p * tp_size)()
+    _check(lib.nf_comm_create_local(tp_size, arr))
+    return [arr[i] for i in range(tp_size)]
+
+
+def comm_destroy(h: int):
+    lib.nf_comm_destroy(C.c_void_p(h))
 
 
 def comm_create(tp_size: int, tp_rank: int, uid: bytes) -> int:

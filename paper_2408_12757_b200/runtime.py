@@ -87,3 +87,32 @@ class Model:
         nf.model_step(plan, self.handle, [p.data_ptr() for p in pools], b, token_ids.data_ptr(), next_ids.data_ptr(),
                       ws.data_ptr(), ws.numel(), stream_handle(), comm)
         return next_ids
+
+
+def shard_layer(w: Dict[str, torch.Tensor], n_q_heads: int, n_kv_heads: int, head_dim: int, tp: int,
+                rank: int) -> Dict[str, torch.Tensor]:
+    """Rank `rank`'s canonical shards for head-parallel TP:
+    column W_q/W_k/W_v by heads, column O (rows of W_o) and row O (columns of
+    W_o), column gate/up, row down.  Slicing only (views made contiguous)."""
+    D = w["w_o"].shape[0]
+    F = w["w_gate"].shape[0]
+    qs, ks = n_q_heads // tp * head_dim, n_kv_heads // tp * head_dim
+    ds, fs = D // tp, F // tp
+    c = lambda t: t.contiguous()
+    return {
+        "attn_norm": w["attn_norm"], "ffn_norm": w["ffn_norm"],
+        "w_q": c(w["w_q"][rank * qs:(rank + 1) * qs]),
+        "w_k": c(w["w_k"][rank * ks:(rank + 1) * ks]),
+        "w_v": c(w["w_v"][rank * ks:(rank + 1) * ks]),
+        "w_o_col": c(w["w_o"][rank * ds:(rank + 1) * ds, :]),
+        "w_o_row": c(w["w_o"][:, rank * qs:(rank + 1) * qs]),
+        "w_gate": c(w["w_gate"][rank * fs:(rank + 1) * fs]),
+        "w_up": c(w["w_up"][rank * fs:(rank + 1) * fs]),
+        "w_down": c(w["w_down"][:, rank * fs:(rank + 1) * fs]),
+    }
+
+
+def shard_pool(pool: torch.Tensor, tp: int, rank: int) -> torch.Tensor:
+    """Rank's KV heads of a [n_pages, 2, kh, page, hd] pool (head-parallel KV)."""
+    kh = pool.shape[2] // tp
+    return pool[:, :, rank * kh:(rank + 1) * kh].contiguous()

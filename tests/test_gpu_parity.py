@@ -82,6 +82,14 @@ def _stream_k_case(M, N, K, sm):
     assert rel < 4e-3 and mx < 2e-2 * max(1.0, np.abs(ref).max()), (rel, mx)
 
 
+@pytest.mark.parametrize("M,N,K,sm", [(1280, 4096, 14336, 108), (768, 4096, 4096, 108), (1280, 6144, 4096, 100),
+                                      (300, 1024, 8192, 37)])
+def test_gemm_split_k2_vs_oracle(env, M, N, K, sm):
+    """Split-K=2 schedule (chosen when it lowers the tile rounds of nano-batch
+    GEMMs): both K-halves reduced in fixed order; oracle values, bit-identical on repeat."""
+    _stream_k_case(M, N, K, sm)
+
+
 @pytest.mark.parametrize("sm", [1, 7, 64, 148])
 def test_gemm_sm_budget_bit_identical(env, sm):
     """The SM budget only changes which CTA computes a tile, never the math."""
@@ -314,7 +322,8 @@ def test_model_step_vs_oracle(env):
     ws = rt.workspace(cfg, nb)
     tok_d = torch.from_numpy(toks).cuda()
     for mode, shares, bal, col in [(0, (1,), False, False), (2, (1, 1), False, False), (2, (1, 1), True, False),
-                                   (1, (1, 2), True, False), (2, (1, 1), True, True)]:
+                                   (1, (1, 2), True, False), (2, (1, 1), True, True), (2, (1, 1), 2, False),
+                                   (1, (1, 1, 1), 2, False), (2, (3, 1), 2, False)]:
         pools_d = [dev(p) for p in pools]
         plan = nf.Plan.explicit(cfg, mode=mode, shares=shares, balance=bal, colocate=col)
         ids = model.step(plan, pools_d, nb, tok_d, ws).cpu().numpy()

@@ -70,13 +70,17 @@ def main():
     results = []
     results.append(("sequential", run(nf.Plan.explicit(cfg, nf.SEQUENTIAL))))
     print(results[-1], flush=True)
-    for shares, bal in [((1, 1), True), ((3, 5), False), ((5, 3), True), ((3, 5), True), ((1, 1), False)]:
+    for bal in (1, 2):
+        results.append((f"nano_only bal={bal}", run(nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=(1, 1), balance=bal))))
+        print(results[-1], flush=True)
+    for shares, bal in [((1, 1), 2), ((1, 1), 1), ((3, 5), 2), ((5, 3), 2)]:
         for dense, dec in [(148, 148), (116, 32), (108, 40), (100, 48), (92, 56), (84, 64), (128, 64), (148, 48)]:
             sm = [dense, dec, dense, dense, dense, dense, 8]
             name = f"overlap shares={shares} bal={bal} dense={dense} dec={dec}"
-            results.append((name, run(nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm, balance=bal))))
-            print(results[-1], flush=True)
-    for shares in [(1, 1), (3, 5)]:
+            pl = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm, balance=bal)
+            results.append((name, run(pl)))
+            print(results[-1], pl.runtime_note(), flush=True)
+    for shares in []:
         name = f"colocate shares={shares}"
         results.append((name, run(nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=[148] * 7, balance=True,
                                                    colocate=True))))
