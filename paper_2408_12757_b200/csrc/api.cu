@@ -843,8 +843,9 @@ nf_status from_net(const LayerCtx& L) {
 //   col (nano 0): AG(attention out) -> O_col (+ x columns) -> AG -> h1
 //   row (others): O_row partial (+ x on rank 0) -> AR -> h1
 //   then column Up/Gate + SiLU, row Down partial (+ h1 on rank 0) -> AR -> x_out.
-// Residuals are folded into rank 0's partial before the AllReduce (one rounding).
-// RMS statistics of h1 / x_out come from one sum-of-squares pass (1 part per row).
+// The row-parallel partials are AllReduced without the residual; one pass then
+// adds the residual in fp32 (one rounding at the residual's magnitude, reading
+// A-12b) and emits the RMS sum-of-squares of h1 / x_out (1 part per row).
 nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, const __nv_bfloat16* x,
                             const nf_packed_layer* wt, __nv_bfloat16* x_out, float* part_out) {
   const nf_model_cfg* c = L.c;
@@ -891,7 +892,7 @@ nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, co
     NF_CUDA(launch_interleave(L.w->ag, N, M, (int)Dl, h1, L.w->part_h1 + nr.t0, L.cs));
   } else {
     GemmArgs a{};
-    a.epi = rank == 0 ? EPI_RESID : EPI_STORE;
+    a.epi = EPI_STORE;
     a.stages = stages;
     a.M = M;
     a.N = (int)D;
@@ -899,8 +900,6 @@ nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, co
     a.n_valid = (int)D;
     a.out = h1;
     a.ldo = D;
-    a.resid = x + nr.t0 * D;
-    a.ldr = D;
     {
       ProfScope ps(NF_OP_O, L.cs);
       NF_CUDA(launch_gemm(L.w->o + nr.t0 * qd, qd, (const __nv_bfloat16*)wt->w_o_row, qd, a,
@@ -912,7 +911,7 @@ nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, co
       NF_TRY(comm_all_reduce_bf16(cm, h1, (size_t)M * D, L.ns, L.w->red));
     }
     NF_TRY(from_net(L));
-    NF_CUDA(launch_gather_rows(h1, nullptr, M, (int)D, nullptr, L.w->part_h1 + nr.t0, L.cs));
+    NF_CUDA(launch_resid_add_rows(h1, x + nr.t0 * D, M, (int)D, L.w->part_h1 + nr.t0, L.cs));
   }
   // column-parallel Up/Gate + SiLU with the RMSNorm(h1) row scale (one partial per row)
   GemmArgs u{};
@@ -933,9 +932,9 @@ nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, co
     ProfScope ps(NF_OP_UG, L.cs);
     NF_CUDA(launch_gemm(h1, D, (const __nv_bfloat16*)wt->w_gate_up, D, u, clamp_dense(L, L.p->spec.sm[NF_OP_UG]), L.cs));
   }
-  // row-parallel Down partial (+ h1 on rank 0) -> AR -> x_out
+  // row-parallel Down partial -> AR -> x_out = h1 + sum
   GemmArgs d{};
-  d.epi = rank == 0 ? EPI_RESID : EPI_STORE;
+  d.epi = EPI_STORE;
   d.stages = stages;
   d.M = M;
   d.N = (int)D;
@@ -943,8 +942,6 @@ nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, co
   d.n_valid = (int)D;
   d.out = x_out + nr.t0 * D;
   d.ldo = D;
-  d.resid = h1;
-  d.ldr = D;
   {
     ProfScope ps(NF_OP_DOWN, L.cs);
     NF_CUDA(launch_gemm(L.w->m + nr.t0 * Fl, Fl, (const __nv_bfloat16*)wt->w_down, Fl, d,
@@ -956,7 +953,7 @@ nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, co
     NF_TRY(comm_all_reduce_bf16(cm, x_out + nr.t0 * D, (size_t)M * D, L.ns, L.w->red));
   }
   NF_TRY(from_net(L));
-  if (part_out) NF_CUDA(launch_gather_rows(x_out + nr.t0 * D, nullptr, M, (int)D, nullptr, part_out + nr.t0, L.cs));
+  NF_CUDA(launch_resid_add_rows(x_out + nr.t0 * D, h1, M, (int)D, part_out ? part_out + nr.t0 : nullptr, L.cs));
   return NF_OK;
 }
 

@@ -36,6 +36,35 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, const 
   if (lane == 0 && part) part[warp] = sq;
 }
 
+// one warp per row, in place: acc[row] = bf16(resid[row] + acc[row]) in fp32, sumsq of the
+// rounded row -> part[row] (the residual add after a TP AllReduce of partial sums)
+__global__ void resid_add_rows_kernel(__nv_bfloat16* __restrict__ acc, const __nv_bfloat16* __restrict__ resid,
+                                      int rows, int D, float* __restrict__ part) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  uint4* a = reinterpret_cast<uint4*>(acc + (int64_t)warp * D);
+  const uint4* r = reinterpret_cast<const uint4*>(resid + (int64_t)warp * D);
+  float sq = 0.f;
+  for (int i = lane; i < D / 8; i += 32) {
+    uint4 u = a[i], v = r[i];
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = unpack_bf16x2(w[k]), g = unpack_bf16x2(x[k]);
+      const __nv_bfloat162 h = __floats2bfloat162_rn(f.x + g.x, f.y + g.y);
+      const float2 q = __bfloat1622float2(h);
+      sq = fmaf(q.x, q.x, sq);
+      sq = fmaf(q.y, q.y, sq);
+      w[k] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    a[i] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane == 0 && part) part[warp] = sq;
+}
+
 // ids[r] = argmax over tiles of (val, idx); ties -> lowest index
 __global__ void argmax_reduce_kernel(const float* __restrict__ val, const int* __restrict__ idx, int ntiles,
                                      int64_t stride, int rows, const int* __restrict__ row_req,
@@ -138,6 +167,14 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* src, const int* idx, int row
                                float* part, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
   gather_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(src, idx, nullptr, rows, D, dst, part);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resid_add_rows(__nv_bfloat16* acc, const __nv_bfloat16* resid, int rows, int D, float* part,
+                                  cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  resid_add_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(acc, resid, rows, D, part);
   count_launch();
   return cudaGetLastError();
 }

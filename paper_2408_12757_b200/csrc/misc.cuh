@@ -6,6 +6,8 @@
 namespace nf {
 cudaError_t launch_gather_rows(const __nv_bfloat16* src, const int* idx, int rows, int D, __nv_bfloat16* dst,
                                float* part, cudaStream_t st);
+cudaError_t launch_resid_add_rows(__nv_bfloat16* acc, const __nv_bfloat16* resid, int rows, int D, float* part,
+                                  cudaStream_t st);
 cudaError_t launch_gather_ids_embed(const __nv_bfloat16* embed, const int* token_ids, const int* tok_src, int rows, int D,
                                     __nv_bfloat16* dst, float* part, cudaStream_t st);
 cudaError_t launch_argmax_reduce(const float* val, const int* idx, int ntiles, int64_t stride, int rows,

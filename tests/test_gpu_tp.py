@@ -132,3 +132,21 @@ def test_tp_model_step_matches_oracle():
     sure = (srt[:, -1] - srt[:, -2]) > 0.1
     assert sure.sum() >= len(sure) // 2
     assert np.array_equal(outs[0][sure], ids_ref[sure])
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+def test_tp_70b_layer_vs_oracle(tp):
+    """T15: one LLaMA-2-70B-shape layer (D 8192, 64/8 heads, F 28672) at TP 2 / 4 / 8
+    on the C3 steady-state mix (p=512, d=1024) scaled to B_dense 256, vs the
+    unsharded float64 oracle."""
+    nf, rt = require_gpu()
+    shape = synth.SHAPES["llama2-70b"]
+    b = synth.workload_batch(256, 512, 1024, pool_slack=3)
+    w = synth.layer_weights(shape, 0)
+    x = synth.activations(shape, b.n_tokens)
+    pool = synth.kv_pool(shape, b)
+    ref = OL.decoder_layer(x, w, OL.as_pool(pool), b, shape)
+    outs = _run_tp_layer(nf, rt, shape, b, w, x, pool, tp, 2, (1, 1))
+    for r in range(1, tp):
+        assert torch.equal(outs[0], outs[r])
+    assert_close(host(outs[0]), ref, what=f"70B TP{tp}")
