@@ -79,11 +79,16 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
   }
   __syncwarp();
 
-  const int gw = blockIdx.x * DEC_WARPS + warp, TW = gridDim.x * DEC_WARPS;
+  // Items are sorted longest-first (host); warps take them in snake order
+  // (round k: k*TW + gw, or k*TW + TW-1-gw for odd k) and warp-major across
+  // CTAs, so every SM gets a mix of lengths and the second round's short items
+  // go to the warps whose first item was shortest (LPT-like makespan).
+  const int gw = warp * gridDim.x + blockIdx.x, TW = gridDim.x * DEC_WARPS;
+  auto item_of = [&](int round) { return round * TW + ((round & 1) ? TW - 1 - gw : gw); };
   const int kh = a.kh, R = a.qh / a.kh;
 
   // look-ahead loader cursor (warp-uniform) + a 32-entry window of page ids (one per lane)
-  int l_item = gw, l_page = 0, l_np = 0, l_ps = 0, l_kvh = 0, pid_win = 0;
+  int l_round = 0, l_item = gw, l_page = 0, l_np = 0, l_ps = 0, l_kvh = 0, pid_win = 0;
   auto load_item = [&]() {
     if (l_item < n_items) {
       const DecodeItem it = items[l_item];
@@ -109,7 +114,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
     }
     ++issued;
     if (++l_page == l_np) {
-      l_item += TW;
+      l_item = item_of(++l_round);
       l_page = 0;
       load_item();
     } else if ((l_page & 31) == 0) {
@@ -120,7 +125,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
 
   const int hq = lane >> 2;            // query head of this lane's B-fragment column (n = lane/4)
   const int hc = 2 * (lane & 3);       // first of the two head columns this lane holds in C fragments
-  for (int item = gw; item < n_items; item += TW) {
+  for (int round = 0, item = gw; item < n_items; item = item_of(++round)) {
     const DecodeItem it = items[item];
     const int kv_len = it.kv_len;
     const __nv_bfloat16* qbase = a.q + ((int64_t)it.t * a.qh + (int64_t)it.kvh * R) * HD;
@@ -150,57 +155,77 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
         }
         __syncwarp();
       }
-      // S^T = K Q^T: two independent accumulation chains over the head dim
-      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+      // Pull the whole page into registers (K fragments for S^T, transposed V
+      // fragments for O^T) and hand the slot back to the TMA ring before any
+      // math: a slot is then busy for the load latency only, not latency +
+      // compute, so the same shared memory keeps more bytes in flight.
+      uint32_t kf[HD / 16][4], vf[HD / 16][4];
       {
         const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
         const int hi = lane >> 4;
 #pragma unroll
         for (int ks = 0; ks < HD / 16; ++ks) {
           const int ch = ks * 2 + hi;
-          uint32_t kf[4];
-          ldmatrix_x4(kf, smem_u32(kb) + (ch >> 3) * BOX_BYTES + swz(key, ch));
-          mma_bf16_16816(ks & 1 ? sb : sa, kf, qb[ks]);
+          ldmatrix_x4(kf[ks], smem_u32(kb) + (ch >> 3) * BOX_BYTES + swz(key, ch));
         }
       }
-      float sc[4];
-      const int k0 = p * 16 + hq, k1 = k0 + 8;
-      sc[0] = k0 < kv_len ? (sa[0] + sb[0]) * a.scale_log2 : -INFINITY;
-      sc[1] = k0 < kv_len ? (sa[1] + sb[1]) * a.scale_log2 : -INFINITY;
-      sc[2] = k1 < kv_len ? (sa[2] + sb[2]) * a.scale_log2 : -INFINITY;
-      sc[3] = k1 < kv_len ? (sa[3] + sb[3]) * a.scale_log2 : -INFINITY;
-      // online softmax over keys (rows) per head column: reduce across lanes xor 4, 8, 16
-      float mx0 = fmaxf(sc[0], sc[2]), mx1 = fmaxf(sc[1], sc[3]);
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
-      }
-      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-      const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
-      m0 = mn0;
-      m1 = mn1;
-      const float p0 = exp2f(sc[0] - mn0), p1 = exp2f(sc[1] - mn1), p2 = exp2f(sc[2] - mn0), p3 = exp2f(sc[3] - mn1);
-      l0 = l0 * al0 + p0 + p2;
-      l1 = l1 * al1 + p1 + p3;
-      const uint32_t pb[2] = {movmatrix_trans(pack_bf16x2(p0, p1)), movmatrix_trans(pack_bf16x2(p2, p3))};
-      // O^T += V^T P^T
       {
         const int key = (lane & 7) + ((lane >> 4) << 3);
         const int hi = (lane >> 3) & 1;
 #pragma unroll
         for (int mt = 0; mt < HD / 16; ++mt) {
           const int ch = mt * 2 + hi;
-          uint32_t vf[4];
-          ldmatrix_x4_trans(vf, smem_u32(vb) + (ch >> 3) * BOX_BYTES + swz(key, ch));
-          oacc[mt][0] *= al0; oacc[mt][1] *= al1;
-          oacc[mt][2] *= al0; oacc[mt][3] *= al1;
-          mma_bf16_16816(oacc[mt], vf, pb);
+          ldmatrix_x4_trans(vf[mt], smem_u32(vb) + (ch >> 3) * BOX_BYTES + swz(key, ch));
         }
       }
       __syncwarp();
       ++consumed;
       issue_one();
+      // S^T = K Q^T: two independent accumulation chains over the head dim
+      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < HD / 16; ++ks) mma_bf16_16816(ks & 1 ? sb : sa, kf[ks], qb[ks]);
+      float sc[4];
+      const int k0 = p * 16 + hq, k1 = k0 + 8;
+      sc[0] = k0 < kv_len ? (sa[0] + sb[0]) * a.scale_log2 : -INFINITY;
+      sc[1] = k0 < kv_len ? (sa[1] + sb[1]) * a.scale_log2 : -INFINITY;
+      sc[2] = k1 < kv_len ? (sa[2] + sb[2]) * a.scale_log2 : -INFINITY;
+      sc[3] = k1 < kv_len ? (sa[3] + sb[3]) * a.scale_log2 : -INFINITY;
+      // Online softmax with a lazily updated running max (per head column):
+      // probabilities are taken against a stale max m as long as no score
+      // exceeds it by more than 2^8, so the cross-lane max reduction and the
+      // O/l rescale run only when the max really moves (first page, rare
+      // later); p <= 256 is exact enough in bf16 (relative rounding) and the
+      // final 1/l normalisation makes the result independent of m.
+      {
+        const float mx0 = fmaxf(sc[0], sc[2]), mx1 = fmaxf(sc[1], sc[3]);
+        if (__any_sync(0xffffffffu, mx0 > m0 + 8.f || mx1 > m1 + 8.f)) {
+          float r0 = mx0, r1 = mx1;
+#pragma unroll
+          for (int o = 4; o < 32; o <<= 1) {
+            r0 = fmaxf(r0, __shfl_xor_sync(0xffffffffu, r0, o));
+            r1 = fmaxf(r1, __shfl_xor_sync(0xffffffffu, r1, o));
+          }
+          const float mn0 = fmaxf(m0, r0), mn1 = fmaxf(m1, r1);
+          const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
+          m0 = mn0;
+          m1 = mn1;
+          l0 *= al0;
+          l1 *= al1;
+#pragma unroll
+          for (int mt = 0; mt < HD / 16; ++mt) {
+            oacc[mt][0] *= al0; oacc[mt][1] *= al1;
+            oacc[mt][2] *= al0; oacc[mt][3] *= al1;
+          }
+        }
+      }
+      const float p0 = exp2f(sc[0] - m0), p1 = exp2f(sc[1] - m1), p2 = exp2f(sc[2] - m0), p3 = exp2f(sc[3] - m1);
+      l0 += p0 + p2;
+      l1 += p1 + p3;
+      const uint32_t pb[2] = {movmatrix_trans(pack_bf16x2(p0, p1)), movmatrix_trans(pack_bf16x2(p2, p3))};
+      // O^T += V^T P^T
+#pragma unroll
+      for (int mt = 0; mt < HD / 16; ++mt) mma_bf16_16816(oacc[mt], vf[mt], pb);
     }
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {

@@ -488,7 +488,12 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   e = make_tmap_bf16(&tb, B, args.K, args.N, ldb, GEMM_BK, bn);
   if (e != cudaSuccess) return e;
   // smem ring: 4 x 48 KB (BN 256) or 6 x 32 KB (BN 128); co-located plans use 3 / 4 stages
-  const bool coloc = args.stages == 3;
+  static int stages_env = -1;  // (dev) NF_GEMM_STAGES=3 forces the shallow ring, for interference A/B
+  if (stages_env < 0) {
+    const char* e = getenv("NF_GEMM_STAGES");
+    stages_env = e ? atoi(e) : 0;
+  }
+  const bool coloc = args.stages == 3 || stages_env == 3;
   int stages;
   void (*kern)(CUtensorMap, CUtensorMap, GemmArgs);
   if (bn == 256) {

@@ -16,6 +16,9 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--shares", default="1:1,5:3", help="comma list of a:b nano-batch shares")
+    ap.add_argument("--splits", default="148/148,116/32,108/40,100/48", help="comma list of dense/decode SMs")
+    ap.add_argument("--bal", default="2")
     args = ap.parse_args()
     import torch
 
@@ -70,16 +73,18 @@ def main():
     results = []
     results.append(("sequential", run(nf.Plan.explicit(cfg, nf.SEQUENTIAL))))
     print(results[-1], flush=True)
-    for bal in (1, 2):
-        results.append((f"nano_only bal={bal}", run(nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=(1, 1), balance=bal))))
-        print(results[-1], flush=True)
-    for shares, bal in [((1, 1), 2), ((1, 1), 1), ((3, 5), 2), ((5, 3), 2)]:
-        for dense, dec in [(148, 148), (116, 32), (108, 40), (100, 48), (92, 56), (84, 64), (128, 64), (148, 48)]:
-            sm = [dense, dec, dense, dense, dense, dense, 8]
-            name = f"overlap shares={shares} bal={bal} dense={dense} dec={dec}"
-            pl = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm, balance=bal)
-            results.append((name, run(pl)))
-            print(results[-1], pl.runtime_note(), flush=True)
+    results.append(("nano_only bal=2", run(nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=(1, 1), balance=2))))
+    print(results[-1], flush=True)
+    for sh in args.shares.split(","):
+        shares = tuple(int(x) for x in sh.split(":"))
+        for bal in [int(x) for x in args.bal.split(",")]:
+            for sp in args.splits.split(","):
+                dense, dec = (int(x) for x in sp.split("/"))
+                sm = [dense, dec, dense, dense, dense, dense, 8]
+                name = f"overlap shares={shares} bal={bal} dense={dense} dec={dec}"
+                pl = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm, balance=bal)
+                results.append((name, run(pl)))
+                print(results[-1], pl.runtime_note(), flush=True)
     for shares in []:
         name = f"colocate shares={shares}"
         results.append((name, run(nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=[148] * 7, balance=True,
