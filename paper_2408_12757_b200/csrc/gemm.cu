@@ -36,17 +36,6 @@ NF_DEV void store32_bf16(__nv_bfloat16* dst, const float (&v)[32]) {
   }
 }
 
-NF_DEV void load32_bf16(const __nv_bfloat16* src, float (&v)[32]) {
-  const uint4* s = reinterpret_cast<const uint4*>(src);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint4 u = s[q];
-    float2 a = unpack_bf16x2(u.x), b = unpack_bf16x2(u.y), c = unpack_bf16x2(u.z), d = unpack_bf16x2(u.w);
-    v[q * 8 + 0] = a.x; v[q * 8 + 1] = a.y; v[q * 8 + 2] = b.x; v[q * 8 + 3] = b.y;
-    v[q * 8 + 4] = c.x; v[q * 8 + 5] = c.y; v[q * 8 + 6] = d.x; v[q * 8 + 7] = d.y;
-  }
-}
-
 NF_DEV int ld_acquire_gpu(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -87,21 +76,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int tiles_n = (N + BN - 1) / BN;
   const int tiles = tiles_m * tiles_n;
   const int num_kb = (K + GEMM_BK - 1) / GEMM_BK;
-  // Hybrid stream-K schedule: whole tiles data-parallel for all but the last
-  // (partial) wave, then the remaining tiles' k-iterations split evenly over
-  // the G CTAs.  A CTA whose range starts inside a tile computes that tile's
-  // tail first and writes an fp32 partial; the CTA holding the tile's first
-  // iterations (the end of its range) adds the partials in CTA order and runs
-  // the fused epilogue -- no CTA ever waits on a lower one (no serial chain).
+  // Split-K tail schedule (args.tail_split = s > 1): the full waves of tiles run
+  // data-parallel in lockstep (CTA b: tiles b, b+G, ...), then each of the
+  // remaining `rem` tiles is split into s equal K ranges run at the same time by
+  // CTAs u = s*i .. s*i+s-1 (u < rem*s <= G).  Split j > 0 leaves an fp32 partial
+  // in slot u; split 0 (the owner) adds them in split order and runs the fused
+  // epilogue.  A partial last wave then costs 1/s of a tile round instead of a
+  // whole one, and concurrent splits stay aligned in K (L2 reuse is kept).
   const int G = gridDim.x;
   // split-K=2 schedule (args.split == 2): units (tile, K-half) in tile-major
   // order, so both halves of a tile run at the same time on adjacent CTAs (L2
   // reuse of the weight tile across m-tiles is kept); half 1 leaves an fp32
   // partial in the tile's slot, half 0 adds it in its epilogue.
   const bool split2 = args.split == 2 && args.sk_part != nullptr;
-  const bool sk = !split2 && args.sk_part != nullptr && (tiles % G) != 0;
-  const int tiles_dp = (sk || split2) ? (sk ? max(0, tiles / G - 1) * G : 0) : tiles;
-  const int64_t total_sk = sk ? (int64_t)(tiles - tiles_dp) * num_kb : 0;
+  const int ts = (!split2 && args.sk_part != nullptr) ? max(1, args.tail_split) : 1;
+  const int tiles_dp = split2 ? 0 : (ts > 1 ? (tiles / G) * G : tiles);
+  const int tail_units = ts > 1 ? (tiles - tiles_dp) * ts : 0;
   const int kb_half = num_kb / 2;
   auto for_each_seg = [&](auto&& fn) {
     if (split2) {
@@ -112,15 +102,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       return;
     }
     for (int t = blockIdx.x; t < tiles_dp; t += G) fn(t, 0, num_kb);
-    if (total_sk > 0) {
-      int64_t i = (int64_t)blockIdx.x * total_sk / G;
-      const int64_t e = (int64_t)(blockIdx.x + 1) * total_sk / G;
-      while (i < e) {
-        const int t = (int)(i / num_kb), kb0 = (int)(i % num_kb);
-        const int kb1 = (int)min((int64_t)num_kb, kb0 + (e - i));
-        fn(tiles_dp + t, kb0, kb1);
-        i += kb1 - kb0;
-      }
+    if ((int)blockIdx.x < tail_units) {
+      const int j = blockIdx.x % ts;
+      fn(tiles_dp + blockIdx.x / ts, j * num_kb / ts, (j + 1) * num_kb / ts);
     }
   };
 
@@ -200,26 +184,34 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int trow = ew * 32 + lane;  // row within the tile
     for_each_seg([&](int tile, int kb0, int kb1) {
       const int mb = tile % tiles_m, nb = tile / tiles_m;
-      mbar_wait(&tfull[as], aphase);
-      tc_fence_after();
       const int r = mb * GEMM_BM + trow;
       const bool valid = r < M;
+      if (args.epi == EPI_RESID && valid && kb0 == 0) {
+        // residual row segment -> L2 while the tile's mainloop still runs (short-K
+        // GEMMs are otherwise epilogue-bound on these dependent global loads)
+        const char* rp = reinterpret_cast<const char*>(args.resid + (int64_t)r * args.ldr + nb * BN);
+#pragma unroll
+        for (int q = 0; q < BN * 2 / 128; ++q)
+          if (nb * BN + q * 64 < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + q * 128));
+      }
+      mbar_wait(&tfull[as], aphase);
+      tc_fence_after();
       const uint32_t taddr = tmem_base + as * BN + ((uint32_t)(ew * 32) << 16);
       if (kb0 > 0) {
-        // stream-K contributor (tile tail, processed first in this CTA's range):
-        // raw fp32 partial tile to this CTA's slot, then signal the tile's owner
+        // split-K contributor: raw fp32 partial tile to its slot, then signal the
+        // tile's owner.  Slot layout float4[BN/4][128 rows]: a warp's 32 rows write
+        // (and the owner later reads) 512 contiguous bytes per instruction.
         const size_t slot_idx = split2 ? (size_t)tile : (size_t)blockIdx.x;
-        float* slot = args.sk_part + (slot_idx * GEMM_BM + trow) * GEMM_SK_LD;
+        float4* slot = reinterpret_cast<float4*>(args.sk_part + slot_idx * GEMM_BM * GEMM_SK_LD) + trow;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t rr[32];
           tmem_ld32(taddr + c * 32, rr);
           tmem_ld_wait();
-          float4* d = reinterpret_cast<float4*>(slot + c * 32);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            d[q] = make_float4(__uint_as_float(rr[4 * q]), __uint_as_float(rr[4 * q + 1]),
-                               __uint_as_float(rr[4 * q + 2]), __uint_as_float(rr[4 * q + 3]));
+            slot[(c * 8 + q) * GEMM_BM] = make_float4(__uint_as_float(rr[4 * q]), __uint_as_float(rr[4 * q + 1]),
+                                                      __uint_as_float(rr[4 * q + 2]), __uint_as_float(rr[4 * q + 3]));
         }
         __threadfence();
         tc_fence_before();
@@ -231,16 +223,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (as == 0) aphase ^= 1;
         return;
       }
-      // owner: this CTA holds the tile's first k-iterations (processed last in its
-      // range); the tail iterations were done by the next CTAs, which run them first
+      // owner: this CTA holds the tile's first K range; the other splits were run
+      // concurrently by the next CTAs (tail split) or the adjacent unit (split-K=2)
       int c_first = blockIdx.x + 1, n_contrib = 0;
       if (kb1 < num_kb) {
         if (split2) {
           c_first = tile;  // the tile's own partial slot
           n_contrib = 1;
         } else {
-          const int64_t last = (int64_t)(tile - tiles_dp) * num_kb + num_kb - 1;
-          n_contrib = (int)(((last + 1) * G - 1) / total_sk) - (int)blockIdx.x;
+          n_contrib = ts - 1;
         }
         if (trow == 0) {
           while (ld_acquire_gpu(args.sk_flag + tile) < n_contrib) __nanosleep(32);
@@ -257,10 +248,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
         for (int c = c_first; c < c_first + n_contrib; ++c) {
-          const float4* src = reinterpret_cast<const float4*>(args.sk_part + ((size_t)c * GEMM_BM + trow) * GEMM_SK_LD + col);
+          const float4* src = reinterpret_cast<const float4*>(args.sk_part + (size_t)c * GEMM_BM * GEMM_SK_LD) + trow +
+                              (col / 4) * GEMM_BM;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const float4 f = src[q];
+            const float4 f = src[q * GEMM_BM];
             v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
           }
         }
@@ -297,13 +289,33 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         case EPI_RESID: {
           // sum-of-squares partials in 128-column units (independent of the tile width)
           float sq = 0.f;
+          // residual loads run one 32-column chunk ahead of their use
+          uint4 rnext[4];
+          auto ld_resid = [&](int c) {
+            if (valid && n0 + c * 32 < N) {
+              const uint4* src = reinterpret_cast<const uint4*>(args.resid + (int64_t)r * args.ldr + n0 + c * 32);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) rnext[q] = src[q];
+            }
+          };
+          ld_resid(0);
 #pragma unroll 1
           for (int c = 0; c < BN / 32; ++c) {
+            uint4 rcur[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) rcur[q] = rnext[q];
+            if (c + 1 < BN / 32) ld_resid(c + 1);
             ldacc(c * 32, s, v);
             const int col = n0 + c * 32;
             if (valid && col < N) {
               float rr[32];
-              load32_bf16(args.resid + (int64_t)r * args.ldr + col, rr);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float2 a = unpack_bf16x2(rcur[q].x), b = unpack_bf16x2(rcur[q].y);
+                const float2 c2 = unpack_bf16x2(rcur[q].z), d = unpack_bf16x2(rcur[q].w);
+                rr[q * 8 + 0] = a.x; rr[q * 8 + 1] = a.y; rr[q * 8 + 2] = b.x; rr[q * 8 + 3] = b.y;
+                rr[q * 8 + 4] = c2.x; rr[q * 8 + 5] = c2.y; rr[q * 8 + 6] = d.x; rr[q * 8 + 7] = d.y;
+              }
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
                 v[j] = round_bf16(rr[j] + v[j]);
@@ -512,34 +524,46 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   }
   const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + bn - 1) / bn);
   int grid = tiles < sm_budget ? tiles : sm_budget;
-  // Stream-K tail is opt-in (NF_STREAMK=1): it removes wave quantisation but its
-  // k-staggered CTAs lose the L2 reuse of weight tiles across m-tiles, which
-  // measured slower on the decoder GEMMs.
-  static int sk_env = -1;
-  if (sk_env < 0) {
-    const char* e = getenv("NF_STREAMK");
-    sk_env = (e && e[0] == '1') ? 1 : 0;
-  }
   GemmArgs a2 = args;
-  // split-K=2 when it strictly lowers the number of tile-rounds (nano-batch-sized
-  // GEMMs with 1-2 waves of tiles), needs the scratch slots and K >= 8192 (a half tile
-  // must outweigh writing + reading its 128 KB fp32 partial; measured on O vs Down)
+  // Schedule choice by tile-rounds (cost in units of one whole tile's mainloop):
+  //   data-parallel        ceil(tiles / SB)
+  //   split-K tail (s)     floor(tiles / SB) + 1/s for the partial last wave, s = min(4, SB / rem)
+  //                        splits of >= 16 k-blocks each (also covers sub-wave GEMMs)
+  //   split-K=2            ceil(2 tiles / SB) / 2, for K >= 8192 (a half tile must outweigh
+  //                        writing + reading its 128 KB fp32 partial; measured on O vs Down)
+  // Ties keep the simpler schedule.  NF_STREAMK=0 / NF_SPLITK=0 disable the split schedules (A/B runs).
   const int num_kb = (args.K + GEMM_BK - 1) / GEMM_BK;
-  const int rounds1 = (tiles + grid - 1) / grid;
-  const int g2 = std::min(sm_budget, 2 * tiles);
-  const double rounds2 = ((2 * tiles + g2 - 1) / g2) / 2.0;
-  static int split_env = -1;
+  static int split_env = -1, tail_env = -1;
   if (split_env < 0) {
     const char* e = getenv("NF_SPLITK");
     split_env = e ? atoi(e) : 1;
+    e = getenv("NF_STREAMK");
+    tail_env = e ? atoi(e) : 1;
   }
-  a2.split = 1;
-  if (split_env && args.sk_part != nullptr && args.sk_slots >= tiles && num_kb >= 128 && rounds2 < rounds1 &&
+  const int SB = std::max(1, sm_budget);
+  double best = (double)((tiles + SB - 1) / SB);
+  int choice = 0, best_s = 1;
+  if (tail_env && args.sk_part != nullptr && args.sk_slots >= SB) {
+    const int rem = tiles % SB;
+    if (rem > 0) {
+      int s = std::min(4, SB / rem);
+      while (s > 1 && num_kb / s < 16) --s;
+      const double c = tiles / SB + 1.0 / s;
+      if (s > 1 && c < best - 1e-9) { best = c; choice = 1; best_s = s; }
+    }
+  }
+  const int g2 = std::min(SB, 2 * tiles);
+  const double rounds2 = ((2 * tiles + g2 - 1) / g2) / 2.0;
+  if (split_env && args.sk_part != nullptr && args.sk_slots >= tiles && num_kb >= 128 && rounds2 < best - 1e-9 &&
       args.epi != EPI_SILU && args.epi != EPI_ARGMAX) {
-    a2.split = 2;
-    grid = g2;
+    best = rounds2;
+    choice = 2;
   }
-  if (!sk_env && a2.split != 2) a2.sk_part = nullptr;
+  a2.split = choice == 2 ? 2 : 1;
+  a2.tail_split = choice == 1 ? best_s : 1;
+  if (choice == 1) grid = SB;
+  if (choice == 2) grid = g2;
+  if (choice == 0) a2.sk_part = nullptr;
   if (grid < 1) grid = 1;
   kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, a2);
   count_launch();

@@ -44,9 +44,10 @@ def test_gemm_vs_oracle(env, M, N, K):
 @pytest.mark.parametrize("M,N,K,sm", [(1024, 4096, 4096, 108), (1024, 6144, 4096, 100), (2048, 4096, 14336, 148),
                                       (333, 2816, 1376, 37), (77, 768, 512, 148), (1024, 28672, 4096, 96)])
 def test_gemm_stream_k_vs_oracle(env, M, N, K, sm, monkeypatch):
-    """Hybrid stream-K tail (partial fp32 tiles reduced in CTA order; opt-in via
-    NF_STREAMK=1, read at first GEMM launch -- exercised in a subprocess so the
-    default path stays untouched): oracle values, bit-identical on repeat."""
+    """Split-K tail schedule (the partial last wave's tiles split 2-4 ways in K,
+    fp32 partials reduced in split order; NF_STREAMK=1 forces it on, read at the
+    first GEMM launch -- exercised in a subprocess): oracle values, bit-identical
+    on repeat."""
     import subprocess
     import sys
     code = f"""

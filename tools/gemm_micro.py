@@ -15,8 +15,11 @@ SHAPES = {  # name: (N, K)
 }
 budgets = [int(x) for x in sys.argv[1:]] or [148, 108]
 st = rt.stream_handle()
+only = os.environ.get("ONLY")
 for name, (N, K) in SHAPES.items():
-    for M in (1024, 2048):
+    if only and not name.startswith(only):
+        continue
+    for M in [int(x) for x in os.environ.get("MS", "1024,2048").split(",")]:
         A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         B = (torch.randn(N, K, device="cuda") * K ** -0.5).to(torch.bfloat16)
         C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--shares", default="1:1,5:3", help="comma list of a:b nano-batch shares")
     ap.add_argument("--splits", default="148/148,116/32,108/40,100/48", help="comma list of dense/decode SMs")
     ap.add_argument("--bal", default="2")
+    ap.add_argument("--colocate", default="", help="comma list of a:b shares for co-located plans")
     args = ap.parse_args()
     import torch
 
@@ -85,7 +86,7 @@ def main():
                 pl = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm, balance=bal)
                 results.append((name, run(pl)))
                 print(results[-1], pl.runtime_note(), flush=True)
-    for shares in []:
+    for shares in ([tuple(int(x) for x in sh.split(":")) for sh in args.colocate.split(",")] if args.colocate else []):
         name = f"colocate shares={shares}"
         results.append((name, run(nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=[148] * 7, balance=True,
                                                    colocate=True))))
