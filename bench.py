@@ -260,11 +260,13 @@ def run_nf(args, rank, world, local_rank):
             plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=sm or [148] * 7, balance=True,
                                     colocate=True)
         else:
-            shares = tuple(int(x) for x in args.shares.split(","))
-            plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm or [108, 40, 108, 108, 108, 108, 8],
+            # defaults = best of tools/sweep_plans.py on B200 (profiles/r1_sweep_*.log)
+            dense, dec, dshares = (132, 16, "1,1") if args.config != "c2" else (116, 32, "3,5")
+            shares = tuple(int(x) for x in (args.shares or dshares).split(","))
+            plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm or [dense, dec, dense, dense, dense, dense, 8],
                                     balance=args.balance)
     elif args.mode == "nano":
-        plan = nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=tuple(int(x) for x in args.shares.split(",")), sm=sm,
+        plan = nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=tuple(int(x) for x in (args.shares or "1,1").split(",")), sm=sm,
                                 balance=args.balance)
     else:
         plan = nf.Plan.explicit(cfg, nf.SEQUENTIAL, sm=sm)
@@ -464,7 +466,7 @@ def main():
     ap.add_argument("--plan", default="explicit", choices=["explicit", "auto"],
                     help="auto: nf_plan_create autosearch over --curves (overlap mode)")
     ap.add_argument("--curves", default="profiles/curves_b200_quick.csv")
-    ap.add_argument("--shares", default="5,3", help="nano-batch token shares (overlap / nano modes)")
+    ap.add_argument("--shares", default="", help="nano-batch token shares (overlap / nano modes; default per config)")
     ap.add_argument("--balance", type=int, default=2, help="0 request order, 1 balanced, 2 exact shares + KV")
     ap.add_argument("--colocate", action="store_true", help="attention CTAs co-resident with GEMM CTAs")
     ap.add_argument("--sm", default="", help="comma-separated SM budget per op kind (7 values)")
