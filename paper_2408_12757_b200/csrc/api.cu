@@ -216,9 +216,10 @@ void build_meta(const nf_model_cfg* c, const nf_batch* b, const std::vector<int>
       if (b->q_len[r] == 1) {
         for (int g = 0; g < kh; ++g) dec.push_back(DecodeItem{row_start[r], g, kvl, b->page_indptr[r]});
       } else {
-        for (int i0 = 0; i0 < b->q_len[r]; i0 += 64)
+        const int rows = prefill_rows(c->head_dim);
+        for (int i0 = 0; i0 < b->q_len[r]; i0 += rows)
           for (int h = 0; h < qh; ++h)
-            pf.push_back(PrefillItem{row_start[r] + i0, std::min(64, b->q_len[r] - i0), b->kv_prefix[r] + i0, h, kvl,
+            pf.push_back(PrefillItem{row_start[r] + i0, std::min(rows, b->q_len[r] - i0), b->kv_prefix[r] + i0, h, kvl,
                                      b->page_indptr[r], 0, 0});
       }
     }
@@ -712,6 +713,7 @@ AttnArgs attn_args(const LayerCtx& L) {
   a.page_size = c->page_size;
   a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)c->head_dim));
   a.dec_warps = L.p->spec.colocate ? 4 : 8;
+  a.n_rows = L.m->T;
   return a;
 }
 

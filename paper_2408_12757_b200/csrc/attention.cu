@@ -12,6 +12,7 @@
 // Prefill: FlashAttention-2 style, one CTA per (64-query tile, query head),
 // double-buffered 64-key K/V tiles, causal mask j <= pos.
 #include <algorithm>
+#include <string>
 
 #include "attention.cuh"
 #include "common.cuh"
@@ -498,9 +499,19 @@ cudaError_t launch_decode_attention(const CUtensorMap& m, const CUtensorMap& pm,
   return cudaErrorInvalidValue;
 }
 
+int prefill_rows(int head_dim) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("NF_PREFILL_IMPL");
+    env = (e && std::string(e) == "mma") ? 1 : 0;
+  }
+  return (head_dim == 128 && env == 0) ? 128 : 64;
+}
+
 cudaError_t launch_prefill_attention(const CUtensorMap& m, const AttnArgs& a, const PrefillItem* items,
                                      int n_items, int sm_budget, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
+  if (a.hd == 128 && prefill_rows(128) == 128) return launch_prefill_attention_tc(m, a, items, n_items, sm_budget, st);
   if (a.hd == 128) return launch_prefill_hd<128>(m, a, items, n_items, sm_budget, st);
   if (a.hd == 64) return launch_prefill_hd<64>(m, a, items, n_items, sm_budget, st);
   return cudaErrorInvalidValue;

@@ -26,9 +26,12 @@ struct AttnArgs {
   int qh, kh, hd, page_size;
   float scale_log2;         // log2(e)/sqrt(hd)
   int dec_warps;            // decode CTA size: 8 (own SMs) or 4 (co-resident with a GEMM CTA)
+  int n_rows;               // T: rows of q / o (bound of the prefill kernel's q tensor map)
 };
 
 cudaError_t make_page_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, int kh, int hd, int page_size);
+// q [T, qh, hd] as a 3-D map {hd, qh, T}: box {64, 1, 128} = 128 token rows of one head, 128B-swizzled
+cudaError_t make_q_tmap(CUtensorMap* m, const void* q, int64_t T, int qh, int hd);
 cudaError_t make_pool_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, int kh, int hd, int page_size);
 
 cudaError_t launch_decode_attention(const CUtensorMap& pool_map, const CUtensorMap& page_map, const AttnArgs& a, const DecodeItem* items,
@@ -36,6 +39,12 @@ cudaError_t launch_decode_attention(const CUtensorMap& pool_map, const CUtensorM
 // tcgen05 decode attention (head_dim 128, GQA group <= 8); decode_tc.cu
 cudaError_t launch_decode_attention_tc(const CUtensorMap& pool_map, const AttnArgs& a, const DecodeItem* items,
                                        int n_items, int sm_budget, cudaStream_t stream);
+// tcgen05 prefill attention (head_dim 128, 128-row items); prefill_tc.cu
+cudaError_t launch_prefill_attention_tc(const CUtensorMap& pool_map, const AttnArgs& a, const PrefillItem* items,
+                                        int n_items, int sm_budget, cudaStream_t stream);
+// Query rows per prefill work item for this head_dim (128: tcgen05 kernel; 64: mma.sync kernel,
+// also for head_dim 128 with NF_PREFILL_IMPL=mma).
+int prefill_rows(int head_dim);
 cudaError_t launch_prefill_attention(const CUtensorMap& pool_map, const AttnArgs& a, const PrefillItem* items,
                                      int n_items, int sm_budget, cudaStream_t stream);
 

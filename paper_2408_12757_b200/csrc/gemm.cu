@@ -478,6 +478,19 @@ cudaError_t make_page_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, in
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+cudaError_t make_q_tmap(CUtensorMap* m, const void* q, int64_t T, int qh, int hd) {
+  cudaError_t e = get_encode();
+  if (e != cudaSuccess) return e;
+  cuuint64_t dims[3] = {(cuuint64_t)hd, (cuuint64_t)qh, (cuuint64_t)T};
+  cuuint64_t strides[2] = {(cuuint64_t)hd * 2, (cuuint64_t)qh * hd * 2};
+  cuuint32_t box[3] = {64, 1, 128};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(q), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* B, int64_t ldb,
                         const GemmArgs& args, int sm_budget, cudaStream_t stream) {
   if (args.M <= 0) return cudaSuccess;

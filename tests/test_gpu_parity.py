@@ -148,6 +148,22 @@ def test_attention_vs_oracle(env, shape_name):
     assert_close(out, ref, what="attention")
 
 
+def test_prefill_attention_bench_composition(env):
+    """a5 at the bench's prefill shapes (8B: a 341-token chunk over a 683-token
+    prefix + a 1024-token prompt, i.e. many 128-key blocks, ragged last tiles and
+    diagonal blocks) with NaN in every unused pool slot, at several SM budgets
+    (the tcgen05 kernel is persistent: the budget only changes which CTA runs
+    an item, so outputs are bit-identical across budgets)."""
+    shape = synth.SHAPES["llama3-8b"]
+    q_len, prefix = [1, 1, 341, 1024, 129], [100, 2000, 683, 0, 255]
+    b, pool, q = _attn_case(shape, q_len, prefix, seed=5, fill=np.nan)
+    ref = OL.paged_attention(q, np.nan_to_num(pool), b)
+    outs = [_run_attn(env, shape, b, pool, q, 148, sm) for sm in (148, 37, 1)]
+    assert np.isfinite(outs[0]).all()
+    assert_close(outs[0], ref, what="prefill attention (bench composition)")
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
 def test_attention_c1_config(env):
     shape = synth.SHAPES["c1"]
     b = synth.c1_batch()
