@@ -88,18 +88,29 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
   auto item_of = [&](int round) { return round * TW + ((round & 1) ? TW - 1 - gw : gw); };
   const int kh = a.kh, R = a.qh / a.kh;
 
-  // look-ahead loader cursor (warp-uniform) + a 32-entry window of page ids (one per lane)
-  int l_round = 0, l_item = gw, l_page = 0, l_np = 0, l_ps = 0, l_kvh = 0, pid_win = 0;
-  auto load_item = [&]() {
-    if (l_item < n_items) {
-      const DecodeItem it = items[l_item];
-      l_np = (it.kv_len + 15) >> 4;
-      l_ps = it.page_start;
-      l_kvh = it.kvh;
-      pid_win = lane < l_np ? a.page_ids[l_ps + lane] : 0;
+  // Look-ahead loader cursor (warp-uniform) with a 32-entry window of page ids
+  // (one per lane).  Metadata is software-pipelined across item switches so no
+  // load is consumed right after it is issued: at a switch the next item's
+  // header (loaded one switch earlier) becomes current, the item after it gets
+  // its first page-id window, and the header two items ahead is requested;
+  // within an item the following 32-page window is loaded 32 pages ahead.
+  struct Hdr { int np, ps, kvh; };
+  auto header = [&](int item) {
+    Hdr h{0, 0, 0};
+    if (item < n_items) {
+      const DecodeItem it = items[item];
+      h.np = (it.kv_len + 15) >> 4;
+      h.ps = it.page_start;
+      h.kvh = it.kvh;
     }
+    return h;
   };
-  load_item();
+  auto window = [&](const Hdr& h, int first) {
+    return first + lane < h.np ? a.page_ids[h.ps + first + lane] : 0;
+  };
+  int l_round = 0, l_item = gw, l_page = 0;
+  Hdr cur = header(l_item), nxt = header(item_of(1)), nn = header(item_of(2));
+  int pid_win = window(cur, 0), pid_nwin = window(cur, 32), n_win = window(nxt, 0);
   uint32_t issued = 0, consumed = 0;
   const uint64_t kv_policy = policy_evict_first();  // K/V pages are read exactly once: keep L2 for the GEMMs
   auto issue_one = [&]() {
@@ -108,22 +119,29 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
     const int64_t page = __shfl_sync(0xffffffffu, pid_win, l_page & 31);
     if (lane == 0) {
       uint8_t* dst = ring + s * STAGE_BYTES;
-      const int rowK = (int)(((page * 2 + 0) * kh + l_kvh) * 16);
-      fence_proxy_async();
+      const int rowK = (int)(((page * 2 + 0) * kh + cur.kvh) * 16);
+      fence_proxy_async();  // WAR: this warp's ldmatrix reads of the slot before the async-proxy refill
       mbar_arrive_expect_tx(&bars[s], STAGE_BYTES);
       tma_load_4d_hint(dst, &pages, &bars[s], 0, rowK, 0, 0, kv_policy);  // K and V of the page: one 4-D box
     }
     ++issued;
-    if (++l_page == l_np) {
+    if (++l_page == cur.np) {
       l_item = item_of(++l_round);
       l_page = 0;
-      load_item();
+      cur = nxt;
+      pid_win = n_win;
+      pid_nwin = window(cur, 32);
+      nxt = nn;
+      n_win = window(nxt, 0);
+      nn = header(item_of(l_round + 2));
     } else if ((l_page & 31) == 0) {
-      pid_win = l_page + lane < l_np ? a.page_ids[l_ps + l_page + lane] : 0;
+      pid_win = pid_nwin;
+      pid_nwin = window(cur, l_page + 32);
     }
   };
   for (int i = 0; i < NS; ++i) issue_one();
 
+  const float inv_scale = 1.f / a.scale_log2;
   const int hq = lane >> 2;            // query head of this lane's B-fragment column (n = lane/4)
   const int hc = 2 * (lane & 3);       // first of the two head columns this lane holds in C fragments
   for (int round = 0, item = gw; item < n_items; item = item_of(++round)) {
@@ -138,6 +156,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
       qb[ks][1] = hq < R ? ldg_u32(qbase + hq * HD + kc + 8) : 0u;
     }
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    float thr0 = -INFINITY, thr1 = -INFINITY;  // raw-score thresholds (m + 8) / scale of the lazy max
     float oacc[HD / 16][4];
 #pragma unroll
     for (int d = 0; d < HD / 16; ++d) oacc[d][0] = oacc[d][1] = oacc[d][2] = oacc[d][3] = 0.f;
@@ -182,45 +201,49 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
       __syncwarp();
       ++consumed;
       issue_one();
-      // S^T = K Q^T: two independent accumulation chains over the head dim
-      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+      // S^T = K Q^T: four independent accumulation chains over the head dim (raw scores)
+      float sacc[4][4];
 #pragma unroll
-      for (int ks = 0; ks < HD / 16; ++ks) mma_bf16_16816(ks & 1 ? sb : sa, kf[ks], qb[ks]);
+      for (int c = 0; c < 4; ++c) sacc[c][0] = sacc[c][1] = sacc[c][2] = sacc[c][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < HD / 16; ++ks) mma_bf16_16816(sacc[ks & 3], kf[ks], qb[ks]);
       float sc[4];
-      const int k0 = p * 16 + hq, k1 = k0 + 8;
-      sc[0] = k0 < kv_len ? (sa[0] + sb[0]) * a.scale_log2 : -INFINITY;
-      sc[1] = k0 < kv_len ? (sa[1] + sb[1]) * a.scale_log2 : -INFINITY;
-      sc[2] = k1 < kv_len ? (sa[2] + sb[2]) * a.scale_log2 : -INFINITY;
-      sc[3] = k1 < kv_len ? (sa[3] + sb[3]) * a.scale_log2 : -INFINITY;
-      // Online softmax with a lazily updated running max (per head column):
-      // probabilities are taken against a stale max m as long as no score
-      // exceeds it by more than 2^8, so the cross-lane max reduction and the
-      // O/l rescale run only when the max really moves (first page, rare
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sc[e] = (sacc[0][e] + sacc[1][e]) + (sacc[2][e] + sacc[3][e]);
+      if (p == np - 1) {  // keys past kv_len only exist in the last page
+        const int k0 = p * 16 + hq, k1 = k0 + 8;
+        if (k0 >= kv_len) sc[0] = sc[1] = -INFINITY;
+        if (k1 >= kv_len) sc[2] = sc[3] = -INFINITY;
+      }
+      // Online softmax with a lazily updated running max m (per head column, in
+      // log2 units): probabilities are taken against a stale max as long as no
+      // raw score exceeds thr = (m + 8) / scale, so the cross-lane max reduction
+      // and the O/l rescale run only when the max really moves (first page, rare
       // later); p <= 256 is exact enough in bf16 (relative rounding) and the
       // final 1/l normalisation makes the result independent of m.
-      {
-        const float mx0 = fmaxf(sc[0], sc[2]), mx1 = fmaxf(sc[1], sc[3]);
-        if (__any_sync(0xffffffffu, mx0 > m0 + 8.f || mx1 > m1 + 8.f)) {
-          float r0 = mx0, r1 = mx1;
+      if (__any_sync(0xffffffffu, fmaxf(sc[0], sc[2]) > thr0 || fmaxf(sc[1], sc[3]) > thr1)) {
+        float r0 = fmaxf(sc[0], sc[2]), r1 = fmaxf(sc[1], sc[3]);
 #pragma unroll
-          for (int o = 4; o < 32; o <<= 1) {
-            r0 = fmaxf(r0, __shfl_xor_sync(0xffffffffu, r0, o));
-            r1 = fmaxf(r1, __shfl_xor_sync(0xffffffffu, r1, o));
-          }
-          const float mn0 = fmaxf(m0, r0), mn1 = fmaxf(m1, r1);
-          const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
-          m0 = mn0;
-          m1 = mn1;
-          l0 *= al0;
-          l1 *= al1;
+        for (int o = 4; o < 32; o <<= 1) {
+          r0 = fmaxf(r0, __shfl_xor_sync(0xffffffffu, r0, o));
+          r1 = fmaxf(r1, __shfl_xor_sync(0xffffffffu, r1, o));
+        }
+        const float mn0 = fmaxf(m0, r0 * a.scale_log2), mn1 = fmaxf(m1, r1 * a.scale_log2);
+        const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
+        m0 = mn0;
+        m1 = mn1;
+        thr0 = (mn0 + 8.f) * inv_scale;
+        thr1 = (mn1 + 8.f) * inv_scale;
+        l0 *= al0;
+        l1 *= al1;
 #pragma unroll
-          for (int mt = 0; mt < HD / 16; ++mt) {
-            oacc[mt][0] *= al0; oacc[mt][1] *= al1;
-            oacc[mt][2] *= al0; oacc[mt][3] *= al1;
-          }
+        for (int mt = 0; mt < HD / 16; ++mt) {
+          oacc[mt][0] *= al0; oacc[mt][1] *= al1;
+          oacc[mt][2] *= al0; oacc[mt][3] *= al1;
         }
       }
-      const float p0 = exp2f(sc[0] - m0), p1 = exp2f(sc[1] - m1), p2 = exp2f(sc[2] - m0), p3 = exp2f(sc[3] - m1);
+      const float p0 = ex2_approx(fmaf(sc[0], a.scale_log2, -m0)), p1 = ex2_approx(fmaf(sc[1], a.scale_log2, -m1));
+      const float p2 = ex2_approx(fmaf(sc[2], a.scale_log2, -m0)), p3 = ex2_approx(fmaf(sc[3], a.scale_log2, -m1));
       l0 += p0 + p2;
       l1 += p1 + p3;
       const uint32_t pb[2] = {movmatrix_trans(pack_bf16x2(p0, p1)), movmatrix_trans(pack_bf16x2(p2, p3))};

@@ -149,6 +149,11 @@ NF_DEV float2 unpack_bf16x2(uint32_t u) {
   __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&u);
   return __bfloat1622float2(v);
 }
+NF_DEV float ex2_approx(float x) {  // 2^x (MUFU.EX2, flush-to-zero; 2^-inf = 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 NF_DEV float round_bf16(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
 NF_DEV void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
