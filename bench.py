@@ -261,7 +261,7 @@ def run_nf(args, rank, world, local_rank):
                                     colocate=True)
         else:
             # defaults = best of tools/sweep_plans.py on B200 (profiles/r1_sweep_*.log)
-            dense, dec, dshares = (132, 16, "1,1") if args.config != "c2" else (116, 32, "3,5")
+            dense, dec, dshares = (132, 16, "1,1") if args.config != "c2" else (116, 32, "1,1")
             shares = tuple(int(x) for x in (args.shares or dshares).split(","))
             plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm or [dense, dec, dense, dense, dense, dense, 8],
                                     balance=args.balance)
@@ -415,11 +415,28 @@ def run_nf(args, rank, world, local_rank):
         roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
                 "frac": achieved / pk, "traffic": traffic, "peak_source": peak_src + " sustained",
                 "algorithmic": "2*M*N*K per launch"}
+    pf_flops = L * sum(4 * hd * Hq_l * (int(b.kv_prefix[r]) + i + 1)
+                       for r in range(b.n_req) if b.q_len[r] > 1 for i in range(int(b.q_len[r])))
+    flops["prefill_attn"] = pf_flops  # causal: each row attends to its prefix + itself
     for k in per_op:
         if k in flops:
             per_op[k]["tflops"] = flops[k] / (per_op[k]["ms_per_step"] / 1e3) / 1e12
     if "decode_attn" in per_op:
         per_op["decode_attn"]["hbm_gbs"] = dec_bytes_step / (per_op["decode_attn"]["ms_per_step"] / 1e3) / 1e9
+    # every kernel against its own bound (timed mode), and decode attention in the
+    # sequential ablation (all 148 SMs: the kernel's own roofline, not its partition's)
+    pk_s = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    roof_all = {}
+    for k, v in per_op.items():
+        if k == "decode_attn":
+            roof_all[k] = {"bound": "hbm", "achieved_gbs": v["hbm_gbs"], "frac": v["hbm_gbs"] / peaks["hbm_gbs"],
+                           "sms": plan.spec().sm[1] if args.mode == "overlap" else 148}
+        elif "tflops" in v:
+            roof_all[k] = {"bound": "tensor", "achieved_tflops": v["tflops"], "frac": v["tflops"] / pk_s}
+    seq_dec = ablation.get("sequential_per_op_ms", {}).get("decode_attn")
+    if seq_dec:
+        gbs = dec_bytes_step / (seq_dec / 1e3) / 1e9
+        roof_all["decode_attn_sequential_148sm"] = {"bound": "hbm", "achieved_gbs": gbs, "frac": gbs / peaks["hbm_gbs"]}
 
     optimal = peaks["bf16_tflops"] * 1e12 / (2 * p_active(shape))
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -442,6 +459,7 @@ def run_nf(args, rank, world, local_rank):
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "roofline": roof,
+            "roofline_by_kernel": roof_all,
             "per_op": per_op,
             "ablation": ablation,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}}

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <mutex>
 #include <numeric>
+#include <string>
 
 #include "attention.cuh"
 #include "gemm.cuh"
@@ -1220,6 +1221,19 @@ nf_status nf_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, v
   a.n_valid = N;
   a.out = (__nv_bfloat16*)C;
   a.ldo = ldc;
+  {
+    // (dev) NF_GEMM_EPI=resid times the residual epilogue: C = C + A.B^T, in place
+    static int epi_env = -1;
+    if (epi_env < 0) {
+      const char* e = getenv("NF_GEMM_EPI");
+      epi_env = (e && std::string(e) == "resid") ? 1 : 0;
+    }
+    if (epi_env == 1) {
+      a.epi = EPI_RESID;
+      a.resid = (const __nv_bfloat16*)C;
+      a.ldr = ldc;
+    }
+  }
   const int grid_max = std::max(1, std::min<int>(sm_budget, num_sms()));
   const int tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + 127) / 128);
   const int slots = std::max(148, ((M + GEMM_BM - 1) / GEMM_BM) * ((N + 255) / 256));

@@ -24,6 +24,39 @@ o = torch.empty((n, shape.n_q_heads * 128), device="cuda", dtype=torch.bfloat16)
 ws = rt.workspace(cfg, nb)
 dec_bytes = int((b.kv_prefix + 1).sum()) * 8 * 128 * 4
 sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+import threading  # noqa: E402
+
+import pynvml  # noqa: E402
+
+pynvml.nvmlInit()
+_h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+
+
+class Clock:
+    """Median SM clock (MHz) and power (W) sampled every 5 ms while active."""
+
+    def __enter__(self):
+        self.s, self.p, self.on = [], [], True
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def _run(self):
+        import time
+        while self.on:
+            self.s.append(pynvml.nvmlDeviceGetClockInfo(_h, pynvml.NVML_CLOCK_SM))
+            self.p.append(pynvml.nvmlDeviceGetPowerUsage(_h) / 1000)
+            time.sleep(0.005)
+
+    def __exit__(self, *a):
+        self.on = False
+        self.t.join()
+
+    def summary(self):
+        import statistics
+        return f"{statistics.median(self.s) if self.s else 0:.0f}MHz/{statistics.median(self.p) if self.p else 0:.0f}W"
+
+
 
 
 def dec(st):
@@ -53,21 +86,25 @@ for name, (M, N, K) in {"ug": (1280, 28672, 4096), "down": (1280, 4096, 14336), 
         gemm(sa)
         dec(sb)
     torch.cuda.synchronize()
-    g0, g1 = timed(gemm, sa, 20)
-    torch.cuda.synchronize()
-    t_g = g0.elapsed_time(g1) / 20
-    d0, d1 = timed(dec, sb, 5)
-    torch.cuda.synchronize()
-    t_d = d0.elapsed_time(d1) / 5
+    with Clock() as ck_g:
+        g0, g1 = timed(gemm, sa, 200)
+        torch.cuda.synchronize()
+    t_g = g0.elapsed_time(g1) / 200
+    with Clock() as ck_d:
+        d0, d1 = timed(dec, sb, 30)
+        torch.cuda.synchronize()
+    t_d = d0.elapsed_time(d1) / 30
     # concurrent: decode loop long enough to cover the GEMM loop
-    nd = max(3, int(20 * t_g / t_d) + 3)
+    nd = max(3, int(200 * t_g / t_d) + 3)
     torch.cuda.synchronize()
-    d0, d1 = timed(dec, sb, nd)
-    g0, g1 = timed(gemm, sa, 20)
-    torch.cuda.synchronize()
-    t_gc = g0.elapsed_time(g1) / 20
+    with Clock() as ck_c:
+        d0, d1 = timed(dec, sb, nd)
+        g0, g1 = timed(gemm, sa, 200)
+        torch.cuda.synchronize()
+    t_gc = g0.elapsed_time(g1) / 200
     t_dc = d0.elapsed_time(d1) / nd
     fl = 2 * M * N * K
     print(f"{name}: G={G} D={Dsm} stages={os.environ.get('NF_GEMM_STAGES', '4')}  gemm alone {t_g*1e3:.0f} us "
           f"({fl/t_g/1e9:.0f} TF/s)  with decode {t_gc*1e3:.0f} us ({fl/t_gc/1e9:.0f} TF/s, x{t_gc/t_g:.2f})  | "
-          f"decode alone {dec_bytes/t_d/1e6:.0f} GB/s  concurrent {dec_bytes/t_dc/1e6:.0f} GB/s", flush=True)
+          f"decode alone {dec_bytes/t_d/1e6:.0f} GB/s  concurrent {dec_bytes/t_dc/1e6:.0f} GB/s | clocks gemm-alone "
+          f"{ck_g.summary()} decode-alone {ck_d.summary()} both {ck_c.summary()}", flush=True)

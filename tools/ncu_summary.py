@@ -39,7 +39,7 @@ def main():
         launches = args[i + 1]
         args = args[:i] + args[i + 2:]
     out_md, reps = args[0], args[1:]
-    lines = ["# ncu summaries (round 1)", "", "Captured with `ncu --set full --import-source on --clock-control none` "
+    lines = ["# ncu summaries", "", "Captured with `ncu --set full --import-source on --clock-control none` "
              "on one B200 (gpurun); one launch per report.  Durations under ncu are serialised and cold-cache.", ""]
     traffic = {}
     for rep in reps:
@@ -71,8 +71,10 @@ def main():
         per = defaultdict(lambda: [0, 0.0])
         tot = 0.0
         data = rows[hdr_i + 1:]
+        # step kernels only: weight generation (torch RNG) and one-time packing are setup
+        setup = ("CUDAGeneratorImpl", "pack_gate_up", "scale_cols", "elementwise", "vectorized", "fill_kernel")
         for r in data:
-            if len(r) <= vi:
+            if len(r) <= vi or any(k in r[ki] for k in setup):
                 continue
             nm = r[ki].split("(")[0].split("::")[-1]
             v = float(r[vi].replace(",", ""))
@@ -80,7 +82,7 @@ def main():
             per[nm][1] += v
             tot += v
         lines += ["## Launch list (`ncu --metrics gpu__time_duration.sum`, whole bench command)", "",
-                  f"{len(data)} launches; per-kernel share of summed device time (serialised, cold cache):", "",
+                  f"{sum(n for n, _ in per.values())} step launches (setup kernels excluded); per-kernel share of summed device time (serialised, cold cache):", "",
                   "| kernel | launches | total ms | share |", "|---|---|---|---|"]
         for nm, (n, t) in sorted(per.items(), key=lambda kv: -kv[1][1]):
             lines.append(f"| `{nm}` | {n} | {t / 1e6:.2f} | {100 * t / tot:.1f} % |")
