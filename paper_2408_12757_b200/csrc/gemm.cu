@@ -52,12 +52,20 @@ NF_DEV void sincos_reduced(float a, float* s, float* c) {
   __sincosf(r, s, c);
 }
 
-template <int GEMM_STAGES, int BN>
+// CG = 2: CTA-pair (cta_group::2) variant.  A cluster of two CTAs on one TPC computes
+// a 256 x BN tile: each CTA loads its 128 rows of A and half (BN/2 rows) of the B
+// tile, the even CTA issues tcgen05.mma.cta_group::2 (M = 256) over both CTAs' smem,
+// and each CTA's TMEM receives its own 128 x BN accumulator.  Per CTA the smem stage
+// is 32 KB instead of 48 KB, so the ring is 6 deep, and each B byte is fetched
+// once per pair.  Data-parallel schedule only (the split-K schedules are CG = 1).
+template <int GEMM_STAGES, int BN, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ GemmArgs args) {
-  constexpr int B_STAGE_ELEMS = BN * GEMM_BK;
-  constexpr uint32_t STAGE_BYTES = (A_STAGE_ELEMS + B_STAGE_ELEMS) * 2;
+  constexpr int B_ROWS = BN / CG;  // B tile rows held by this CTA
+  constexpr int B_STAGE_ELEMS = B_ROWS * GEMM_BK;
+  constexpr uint32_t STAGE_BYTES = (A_STAGE_ELEMS + B_STAGE_ELEMS) * 2;  // per CTA
+  constexpr int TM = GEMM_BM * CG;                                         // tile rows
   constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator stages
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -72,7 +80,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = args.M, N = args.N, K = args.K;
-  const int tiles_m = (M + GEMM_BM - 1) / GEMM_BM;
+  uint32_t rank = 0;  // CTA rank in the pair
+  if constexpr (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int wid = blockIdx.x / CG;  // tile worker: a CTA (CG 1) or a CTA pair (CG 2)
+  const int tiles_m = (M + TM - 1) / TM;
   const int tiles_n = (N + BN - 1) / BN;
   const int tiles = tiles_m * tiles_n;
   const int num_kb = (K + GEMM_BK - 1) / GEMM_BK;
@@ -83,28 +94,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // in slot u; split 0 (the owner) adds them in split order and runs the fused
   // epilogue.  A partial last wave then costs 1/s of a tile round instead of a
   // whole one, and concurrent splits stay aligned in K (L2 reuse is kept).
-  const int G = gridDim.x;
+  const int G = gridDim.x / CG;
   // split-K=2 schedule (args.split == 2): units (tile, K-half) in tile-major
   // order, so both halves of a tile run at the same time on adjacent CTAs (L2
   // reuse of the weight tile across m-tiles is kept); half 1 leaves an fp32
   // partial in the tile's slot, half 0 adds it in its epilogue.
-  const bool split2 = args.split == 2 && args.sk_part != nullptr;
-  const int ts = (!split2 && args.sk_part != nullptr) ? max(1, args.tail_split) : 1;
+  const bool split2 = CG == 1 && args.split == 2 && args.sk_part != nullptr;
+  const int ts = (CG == 1 && !split2 && args.sk_part != nullptr) ? max(1, args.tail_split) : 1;
   const int tiles_dp = split2 ? 0 : (ts > 1 ? (tiles / G) * G : tiles);
   const int tail_units = ts > 1 ? (tiles - tiles_dp) * ts : 0;
   const int kb_half = num_kb / 2;
   auto for_each_seg = [&](auto&& fn) {
     if (split2) {
-      for (int u = blockIdx.x; u < 2 * tiles; u += G) {
+      for (int u = wid; u < 2 * tiles; u += G) {
         if (u & 1) fn(u >> 1, kb_half, num_kb);
         else fn(u >> 1, 0, kb_half);
       }
       return;
     }
-    for (int t = blockIdx.x; t < tiles_dp; t += G) fn(t, 0, num_kb);
-    if ((int)blockIdx.x < tail_units) {
-      const int j = blockIdx.x % ts;
-      fn(tiles_dp + blockIdx.x / ts, j * num_kb / ts, (j + 1) * num_kb / ts);
+    for (int t = wid; t < tiles_dp; t += G) fn(t, 0, num_kb);
+    if (wid < tail_units) {
+      const int j = wid % ts;
+      fn(tiles_dp + wid / ts, j * num_kb / ts, (j + 1) * num_kb / ts);
     }
   };
 
@@ -117,11 +128,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 4 * CG);  // epilogue warps of both CTAs drain into the even CTA's barrier
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+  if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
+  if (warp == 2) {
+    if constexpr (CG == 2) tmem_alloc_cg2(tmem_slot, TMEM_COLS);
+    else tmem_alloc(tmem_slot, TMEM_COLS);
+  }
   if (args.epi == EPI_QKV && warp >= 4) {
     const int i = threadIdx.x - 128;
     if (i < args.hd / 2) inv_freq[i] = (float)exp2(-(2.0 * i / args.hd) * (double)args.log2_theta);
@@ -137,21 +152,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint64_t a_policy = policy_evict_last();  // activations are re-read by every n-tile
+      const uint64_t b_policy = policy_evict_normal();
       for_each_seg([&](int tile, int kb0, int kb1) {
         const int mb = tile % tiles_m, nb = tile / tiles_m;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d_hint(sA + stage * A_STAGE_ELEMS, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM, a_policy);
-          tma_load_2d(sB + stage * B_STAGE_ELEMS, &tmB, &full[stage], kb * GEMM_BK, nb * BN);
+          if constexpr (CG == 2) {
+            // both CTAs' loads complete on the even CTA's full barrier, armed once for both
+            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], STAGE_BYTES * CG);
+            tma_load_2d_cg2(sA + stage * A_STAGE_ELEMS, &tmA, fb, kb * GEMM_BK, mb * TM + (int)rank * GEMM_BM,
+                            a_policy);
+            tma_load_2d_cg2(sB + stage * B_STAGE_ELEMS, &tmB, fb, kb * GEMM_BK, nb * BN + (int)rank * B_ROWS,
+                            b_policy);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+            tma_load_2d_hint(sA + stage * A_STAGE_ELEMS, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM, a_policy);
+            tma_load_2d(sB + stage * B_STAGE_ELEMS, &tmB, &full[stage], kb * GEMM_BK, nb * BN);
+          }
           if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
         }
       });
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, BN);
+    if (lane == 0 && rank == 0) {
+      // ------------------------------------------------------------ MMA issuer (even CTA of a pair)
+      constexpr uint32_t idesc = idesc_bf16_f32(TM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int as = 0;
@@ -166,12 +192,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint64_t ad = sdesc_sw128(sA + stage * A_STAGE_ELEMS);
           const uint64_t bd = sdesc_sw128(sB + stage * B_STAGE_ELEMS);
 #pragma unroll
-          for (int k = 0; k < GEMM_BK / 16; ++k)
-            umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-          umma_commit(&empty[stage]);
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            if constexpr (CG == 2) umma_bf16_cg2(d, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            else umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          if constexpr (CG == 2) umma_commit_cg2_mc(&empty[stage]);  // frees the stage in both CTAs
+          else umma_commit(&empty[stage]);
           if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull[as]);
+        if constexpr (CG == 2) umma_commit_cg2_mc(&tfull[as]);
+        else umma_commit(&tfull[as]);
         as ^= 1;
         if (as == 0) aphase ^= 1;
       });
@@ -184,7 +214,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int trow = ew * 32 + lane;  // row within the tile
     for_each_seg([&](int tile, int kb0, int kb1) {
       const int mb = tile % tiles_m, nb = tile / tiles_m;
-      const int r = mb * GEMM_BM + trow;
+      const int r = mb * TM + (int)rank * GEMM_BM + trow;
       const bool valid = r < M;
       if (args.epi == EPI_RESID && valid && kb0 == 0) {
         // residual row segment -> L2 while the tile's mainloop still runs (short-K
@@ -201,7 +231,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // split-K contributor: raw fp32 partial tile to its slot, then signal the
         // tile's owner.  Slot layout float4[BN/4][128 rows]: a warp's 32 rows write
         // (and the owner later reads) 512 contiguous bytes per instruction.
-        const size_t slot_idx = split2 ? (size_t)tile : (size_t)blockIdx.x;
+        const size_t slot_idx = split2 ? (size_t)tile : (size_t)wid;
         float4* slot = reinterpret_cast<float4*>(args.sk_part + slot_idx * GEMM_BM * GEMM_SK_LD) + trow;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
@@ -225,7 +255,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       // owner: this CTA holds the tile's first K range; the other splits were run
       // concurrently by the next CTAs (tail split) or the adjacent unit (split-K=2)
-      int c_first = blockIdx.x + 1, n_contrib = 0;
+      int c_first = wid + 1, n_contrib = 0;
       if (kb1 < num_kb) {
         if (split2) {
           c_first = tile;  // the tile's own partial slot
@@ -418,21 +448,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[as]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+        else mbar_arrive(&tempty[as]);
+      }
       as ^= 1;
       if (as == 0) aphase ^= 1;
     });
   }
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // the peer's remote arrives / MMA writes are done before teardown
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    if constexpr (CG == 2) tmem_dealloc_cg2(tmem_base, TMEM_COLS);
+    else tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_once;
-bool g_attr_set[4] = {false, false, false, false};
+bool g_attr_set[5] = {false, false, false, false, false};
 
 cudaError_t get_encode() {
   std::call_once(g_once, [] {
@@ -498,53 +533,30 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   // halves wave quantisation for nano-batch-sized GEMMs but measured slower:
   // with a 1-CTA N=128 MMA the A+B smem reads reach the smem bandwidth.
   // SiLU / argmax epilogues need the 256-wide tile layout.
-  const int tiles256 = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + 255) / 256);
-  static int bn_env = -1;
+  static int bn_env = -1, stages_env = -1, cg2_env = -1;
   if (bn_env < 0) {
     const char* e = getenv("NF_GEMM_BN");
     bn_env = e ? atoi(e) : 0;
+    e = getenv("NF_GEMM_STAGES");  // (dev) NF_GEMM_STAGES=3 forces the shallow ring, for interference A/B
+    stages_env = e ? atoi(e) : 0;
+    e = getenv("NF_GEMM_CG2");     // CTA-pair kernel (default on; 0 = single-CTA tiles only)
+    cg2_env = e ? atoi(e) : 1;
   }
   const bool need256 = args.epi == EPI_SILU || args.epi == EPI_ARGMAX;  // tile-layout-dependent epilogues
-  (void)tiles256;
   const int bn = (bn_env == 128 && !need256) ? 128 : 256;
-  CUtensorMap ta, tb;
-  cudaError_t e = make_tmap_bf16(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
-  if (e != cudaSuccess) return e;
-  e = make_tmap_bf16(&tb, B, args.K, args.N, ldb, GEMM_BK, bn);
-  if (e != cudaSuccess) return e;
-  // smem ring: 4 x 48 KB (BN 256) or 6 x 32 KB (BN 128); co-located plans use 3 / 4 stages
-  static int stages_env = -1;  // (dev) NF_GEMM_STAGES=3 forces the shallow ring, for interference A/B
-  if (stages_env < 0) {
-    const char* e = getenv("NF_GEMM_STAGES");
-    stages_env = e ? atoi(e) : 0;
-  }
   const bool coloc = args.stages == 3 || stages_env == 3;
-  int stages;
-  void (*kern)(CUtensorMap, CUtensorMap, GemmArgs);
-  if (bn == 256) {
-    stages = coloc ? 3 : 4;
-    kern = coloc ? gemm_tcgen05_kernel<3, 256> : gemm_tcgen05_kernel<4, 256>;
-  } else {
-    stages = coloc ? 4 : 6;
-    kern = coloc ? gemm_tcgen05_kernel<4, 128> : gemm_tcgen05_kernel<6, 128>;
-  }
-  const int smem = gemm_smem_bn(stages, bn);
-  const int attr_idx = (bn == 256 ? 0 : 2) + (coloc ? 1 : 0);
-  if (!g_attr_set[attr_idx]) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    g_attr_set[attr_idx] = true;
-  }
   const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + bn - 1) / bn);
   int grid = tiles < sm_budget ? tiles : sm_budget;
   GemmArgs a2 = args;
-  // Schedule choice by tile-rounds (cost in units of one whole tile's mainloop):
+  // Schedule choice by tile-rounds (cost in units of one 128-row tile's mainloop per CTA):
   //   data-parallel        ceil(tiles / SB)
+  //   CTA pairs            ceil(pair_tiles / (SB/2)) for 256-row pair tiles (6-stage ring, B shared)
   //   split-K tail (s)     floor(tiles / SB) + 1/s for the partial last wave, s = min(4, SB / rem)
   //                        splits of >= 16 k-blocks each (also covers sub-wave GEMMs)
   //   split-K=2            ceil(2 tiles / SB) / 2, for K >= 8192 (a half tile must outweigh
   //                        writing + reading its 128 KB fp32 partial; measured on O vs Down)
-  // Ties keep the simpler schedule.  NF_STREAMK=0 / NF_SPLITK=0 disable the split schedules (A/B runs).
+  // Ties prefer CTA pairs (long-K, wide-N GEMMs only), then the simpler schedule.  NF_STREAMK=0 / NF_SPLITK=0 / NF_GEMM_CG2=0
+  // disable a schedule (A/B runs).
   const int num_kb = (args.K + GEMM_BK - 1) / GEMM_BK;
   static int split_env = -1, tail_env = -1;
   if (split_env < 0) {
@@ -572,12 +584,72 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     best = rounds2;
     choice = 2;
   }
+  const int pairs = SB / 2;
+  const int pair_tiles = ((args.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((args.N + bn - 1) / bn);
+  if (cg2_env && bn == 256 && !coloc && pairs >= 1) {
+    // on a tie the pair kernel measured faster only with a long mainloop and many n-tiles
+    // (>= 32 k-blocks, N >= 2048; tools/gemm_micro.py): short-K pairs couple the two CTAs'
+    // epilogues through the shared accumulator barrier
+    const double c = (double)((pair_tiles + pairs - 1) / pairs);
+    const bool tie_ok = num_kb >= 32 && args.N >= 2048;
+    if (c < best - 1e-9 || (tie_ok && c <= best + 1e-9)) {
+      best = c;
+      choice = 3;
+    }
+  }
   a2.split = choice == 2 ? 2 : 1;
   a2.tail_split = choice == 1 ? best_s : 1;
   if (choice == 1) grid = SB;
   if (choice == 2) grid = g2;
-  if (choice == 0) a2.sk_part = nullptr;
+  if (choice == 0 || choice == 3) a2.sk_part = nullptr;
   if (grid < 1) grid = 1;
+  CUtensorMap ta, tb;
+  cudaError_t e = make_tmap_bf16(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
+  if (e != cudaSuccess) return e;
+  e = make_tmap_bf16(&tb, B, args.K, args.N, ldb, GEMM_BK, choice == 3 ? bn / 2 : bn);
+  if (e != cudaSuccess) return e;
+  // smem ring: 4 x 48 KB (BN 256), 6 x 32 KB (BN 128 or CTA pairs); co-located plans use 3 / 4 stages
+  int stages, cg = 1;
+  void (*kern)(CUtensorMap, CUtensorMap, GemmArgs);
+  int attr_idx;
+  if (choice == 3) {
+    stages = 6;
+    cg = 2;
+    kern = gemm_tcgen05_kernel<6, 256, 2>;
+    attr_idx = 4;
+  } else if (bn == 256) {
+    stages = coloc ? 3 : 4;
+    kern = coloc ? gemm_tcgen05_kernel<3, 256, 1> : gemm_tcgen05_kernel<4, 256, 1>;
+    attr_idx = coloc ? 1 : 0;
+  } else {
+    stages = coloc ? 4 : 6;
+    kern = coloc ? gemm_tcgen05_kernel<4, 128, 1> : gemm_tcgen05_kernel<6, 128, 1>;
+    attr_idx = coloc ? 3 : 2;
+  }
+  const int smem = gemm_smem_bn(stages, bn / cg);
+  if (!g_attr_set[attr_idx]) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    g_attr_set[attr_idx] = true;
+  }
+  if (cg == 2) {
+    grid = 2 * std::min(pair_tiles, pairs);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, ta, tb, a2);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
   kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, a2);
   count_launch();
   return cudaGetLastError();
