@@ -57,7 +57,8 @@ NF_DEV void sincos_reduced(float a, float* s, float* c) {
 // tile, the even CTA issues tcgen05.mma.cta_group::2 (M = 256) over both CTAs' smem,
 // and each CTA's TMEM receives its own 128 x BN accumulator.  Per CTA the smem stage
 // is 32 KB instead of 48 KB, so the ring is 6 deep, and each B byte is fetched
-// once per pair.  Data-parallel schedule only (the split-K schedules are CG = 1).
+// once per pair.  Data-parallel or split-K tail schedule (split-K=2 is CG = 1 only);
+// split-K partial slots and arrival flags are per CTA of the pair.
 template <int GEMM_STAGES, int BN, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // reuse of the weight tile across m-tiles is kept); half 1 leaves an fp32
   // partial in the tile's slot, half 0 adds it in its epilogue.
   const bool split2 = CG == 1 && args.split == 2 && args.sk_part != nullptr;
-  const int ts = (CG == 1 && !split2 && args.sk_part != nullptr) ? max(1, args.tail_split) : 1;
+  const int ts = (!split2 && args.sk_part != nullptr) ? max(1, args.tail_split) : 1;
   const int tiles_dp = split2 ? 0 : (ts > 1 ? (tiles / G) * G : tiles);
   const int tail_units = ts > 1 ? (tiles - tiles_dp) * ts : 0;
   const int kb_half = num_kb / 2;
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // split-K contributor: raw fp32 partial tile to its slot, then signal the
         // tile's owner.  Slot layout float4[BN/4][128 rows]: a warp's 32 rows write
         // (and the owner later reads) 512 contiguous bytes per instruction.
-        const size_t slot_idx = split2 ? (size_t)tile : (size_t)wid;
+        const size_t slot_idx = split2 ? (size_t)tile : (size_t)(wid * CG + (int)rank);  // per CTA of a pair
         float4* slot = reinterpret_cast<float4*>(args.sk_part + slot_idx * GEMM_BM * GEMM_SK_LD) + trow;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
@@ -246,9 +247,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         __threadfence();
         tc_fence_before();
         named_bar_sync(1, 128);
-        if (trow == 0) atomicAdd(args.sk_flag + tile, 1);
+        if (trow == 0) atomicAdd(args.sk_flag + tile * CG + (int)rank, 1);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[as]);
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+          else mbar_arrive(&tempty[as]);
+        }
         as ^= 1;
         if (as == 0) aphase ^= 1;
         return;
@@ -264,11 +268,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           n_contrib = ts - 1;
         }
         if (trow == 0) {
-          while (ld_acquire_gpu(args.sk_flag + tile) < n_contrib) __nanosleep(32);
-          args.sk_flag[tile] = 0;  // self-reset for the next launch
+          while (ld_acquire_gpu(args.sk_flag + tile * CG + (int)rank) < n_contrib) __nanosleep(32);
+          args.sk_flag[tile * CG + (int)rank] = 0;  // self-reset for the next launch
         }
         named_bar_sync(1, 128);
-        (void)ld_acquire_gpu(args.sk_flag + tile);
+        (void)ld_acquire_gpu(args.sk_flag + tile * CG + (int)rank);
       }
       // accumulator + contributors' partials (fixed CTA order), times the row scale
       auto ldacc = [&](int col, float sc, float (&v)[32]) {
@@ -278,7 +282,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
         for (int c = c_first; c < c_first + n_contrib; ++c) {
-          const float4* src = reinterpret_cast<const float4*>(args.sk_part + (size_t)c * GEMM_BM * GEMM_SK_LD) + trow +
+          const size_t cs = split2 ? (size_t)c : (size_t)(c * CG + (int)rank);
+          const float4* src = reinterpret_cast<const float4*>(args.sk_part + cs * GEMM_BM * GEMM_SK_LD) + trow +
                               (col / 4) * GEMM_BM;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -586,22 +591,34 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   }
   const int pairs = SB / 2;
   const int pair_tiles = ((args.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((args.N + bn - 1) / bn);
+  int pair_s = 1;
   if (cg2_env && bn == 256 && !coloc && pairs >= 1) {
     // on a tie the pair kernel measured faster only with a long mainloop and many n-tiles
     // (>= 32 k-blocks, N >= 2048; tools/gemm_micro.py): short-K pairs couple the two CTAs'
     // epilogues through the shared accumulator barrier
-    const double c = (double)((pair_tiles + pairs - 1) / pairs);
     const bool tie_ok = num_kb >= 32 && args.N >= 2048;
+    double c = (double)((pair_tiles + pairs - 1) / pairs);
+    // pairs with a split-K tail (same rule as single CTAs, pair tiles over pairs)
+    const int rem = pair_tiles % pairs;
+    if (tail_env && rem > 0 && args.sk_part != nullptr && args.sk_slots >= SB && pair_tiles > pairs / 4) {
+      int s = std::min(4, pairs / rem);
+      while (s > 1 && num_kb / s < 16) --s;
+      const double ct = pair_tiles / pairs + 1.0 / s;
+      if (s > 1 && ct < c - 1e-9) {
+        c = ct;
+        pair_s = s;
+      }
+    }
     if (c < best - 1e-9 || (tie_ok && c <= best + 1e-9)) {
       best = c;
       choice = 3;
     }
   }
   a2.split = choice == 2 ? 2 : 1;
-  a2.tail_split = choice == 1 ? best_s : 1;
+  a2.tail_split = choice == 1 ? best_s : (choice == 3 ? pair_s : 1);
   if (choice == 1) grid = SB;
   if (choice == 2) grid = g2;
-  if (choice == 0 || choice == 3) a2.sk_part = nullptr;
+  if (choice == 0 || (choice == 3 && pair_s == 1)) a2.sk_part = nullptr;
   if (grid < 1) grid = 1;
   CUtensorMap ta, tb;
   cudaError_t e = make_tmap_bf16(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
@@ -633,7 +650,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     g_attr_set[attr_idx] = true;
   }
   if (cg == 2) {
-    grid = 2 * std::min(pair_tiles, pairs);
+    grid = 2 * (pair_s > 1 ? pairs : std::min(pair_tiles, pairs));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(GEMM_THREADS);

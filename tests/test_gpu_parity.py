@@ -83,6 +83,15 @@ def _stream_k_case(M, N, K, sm):
     assert rel < 4e-3 and mx < 2e-2 * max(1.0, np.abs(ref).max()), (rel, mx)
 
 
+@pytest.mark.parametrize("M,N,K,sm", [(1024, 4096, 14336, 116), (1024, 4096, 4096, 116), (768, 28672, 4096, 116),
+                                      (2048, 6144, 4096, 148), (1280, 4096, 14336, 148), (333, 4096, 4096, 20)])
+def test_gemm_cta_pair_vs_oracle(env, M, N, K, sm):
+    """CTA-pair (cta_group::2) schedules picked by the launcher for these shapes:
+    256-row pair tiles, data-parallel and with a split-K tail over pairs, ragged
+    M (333): oracle values, bit-identical on repeat."""
+    _stream_k_case(M, N, K, sm)
+
+
 @pytest.mark.parametrize("M,N,K,sm", [(1280, 4096, 14336, 108), (768, 4096, 4096, 108), (1280, 6144, 4096, 100),
                                       (300, 1024, 8192, 37)])
 def test_gemm_split_k2_vs_oracle(env, M, N, K, sm):
