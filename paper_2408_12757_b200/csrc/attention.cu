@@ -179,8 +179,12 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
       // fragments for O^T) and hand the slot back to the TMA ring before any
       // math: a slot is then busy for the load latency only, not latency +
       // compute, so the same shared memory keeps more bytes in flight.
-      uint32_t kf[HD / 16][4], vf[HD / 16][4];
+      // K fragments -> S^T = K Q^T (four independent accumulation chains over the
+      // head dim, raw scores), then V fragments; the slot goes back to the TMA ring
+      // as soon as both are in registers (kf and vf are never live together).
+      float sacc[4][4];
       {
+        uint32_t kf[HD / 16][4];
         const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
         const int hi = lane >> 4;
 #pragma unroll
@@ -188,7 +192,12 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
           const int ch = ks * 2 + hi;
           ldmatrix_x4(kf[ks], smem_u32(kb) + (ch >> 3) * BOX_BYTES + swz(key, ch));
         }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sacc[c][0] = sacc[c][1] = sacc[c][2] = sacc[c][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) mma_bf16_16816(sacc[ks & 3], kf[ks], qb[ks]);
       }
+      uint32_t vf[HD / 16][4];
       {
         const int key = (lane & 7) + ((lane >> 4) << 3);
         const int hi = (lane >> 3) & 1;
@@ -201,12 +210,6 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
       __syncwarp();
       ++consumed;
       issue_one();
-      // S^T = K Q^T: four independent accumulation chains over the head dim (raw scores)
-      float sacc[4][4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) sacc[c][0] = sacc[c][1] = sacc[c][2] = sacc[c][3] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < HD / 16; ++ks) mma_bf16_16816(sacc[ks & 3], kf[ks], qb[ks]);
       float sc[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) sc[e] = (sacc[0][e] + sacc[1][e]) + (sacc[2][e] + sacc[3][e]);
