@@ -326,36 +326,52 @@ def run_nf(args, rank, world, local_rank):
     kv_keys = sum(int(b.kv_prefix[r]) + 1 for r in range(b.n_req) if b.q_len[r] == 1)
     Hq_l, Hk_l, F_l = Hq // tp, Hk // tp, F // tp      # this rank's share under TP
     dec_bytes_step = L * (kv_keys * Hk_l * hd * 2 * 2 + n_dec * Hq_l * hd * 2 * 2)  # K+V read + q read + o write
-    # ---------------- F7 ablation with the same kernels: sequential and nano-batch-only
+    # ---------------- F7 ablation with the same kernels: sequential and nano-batch-only.
+    # The three plans are timed in interleaved rounds (seq, nano, timed mode, seq, ...) so that the
+    # GPU's power / thermal state (1 kW cap) drifts equally over all of them; the
+    # comparison uses per-plan medians of the rounds.
     ablation = {}
     if not args.no_ablation:
-        for name, pl in (("sequential", nf.Plan.explicit(cfg, nf.SEQUENTIAL)),
-                         ("nano_only", nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=plan.spec().share[:2]
-                                                        if plan.spec().n_nano == 2 else (1, 1),
-                                                        balance=args.balance))):
+        plans = [("sequential", nf.Plan.explicit(cfg, nf.SEQUENTIAL)),
+                 ("nano_only", nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=plan.spec().share[:2]
+                                                if plan.spec().n_nano == 2 else (1, 1), balance=args.balance)),
+                 ("timed_mode", plan)]
+        rounds = 3
+        per_round = max(2, args.steps // 2)
+        times = {n: [] for n, _ in plans}
+        prof_acc = {n: {} for n, _ in plans}
+        for _, pl in plans:
             for _ in range(2):
                 model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            nf.profile_enable(True)
-            nf.profile_read()
-            a0.record(stream)
-            for _ in range(args.steps):
-                model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
-            a1.record(stream)
-            torch.cuda.synchronize()
-            nf.profile_enable(False)
-            prof_ab = nf.profile_read()
-            ablation[name + "_per_op_ms"] = {k: v[0] / args.steps for k, v in prof_ab.items() if v[1]}
-            t_ab = torch.tensor([a0.elapsed_time(a1) / args.steps], dtype=torch.float64, device=dev)
-            if world > 1:
-                dist.all_reduce(t_ab, op=dist.ReduceOp.MAX)
-            ablation[name + "_ms_per_step"] = float(t_ab.item())
-        ablation["timed_mode_ms_per_step"] = ms_step
+        for _r in range(rounds):
+            for name, pl in plans:
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                if world > 1:
+                    dist.barrier()
+                nf.profile_enable(True)
+                nf.profile_read()
+                a0.record(stream)
+                for _ in range(per_round):
+                    model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
+                a1.record(stream)
+                torch.cuda.synchronize()
+                nf.profile_enable(False)
+                for k, v in nf.profile_read().items():
+                    if v[1]:
+                        prof_acc[name].setdefault(k, []).append(v[0] / per_round)
+                t_ab = torch.tensor([a0.elapsed_time(a1) / per_round], dtype=torch.float64, device=dev)
+                if world > 1:
+                    dist.all_reduce(t_ab, op=dist.ReduceOp.MAX)
+                times[name].append(float(t_ab.item()))
+        for name, _ in plans:
+            ablation[name + "_ms_per_step"] = statistics.median(times[name])
+            ablation[name + "_rounds_ms"] = times[name]
+            if name != "timed_mode":
+                ablation[name + "_per_op_ms"] = {k: statistics.median(v) for k, v in prof_acc[name].items()}
         ablation["timed_mode"] = args.mode
-        ablation["speedup_vs_sequential"] = ablation["sequential_ms_per_step"] / ms_step
+        ablation["interleaving"] = f"{rounds} rounds x {per_round} steps per plan, medians"
+        ablation["speedup_vs_sequential"] = ablation["sequential_ms_per_step"] / ablation["timed_mode_ms_per_step"]
         seq_dec = ablation["sequential_per_op_ms"].get("decode_attn")
         if seq_dec:
             ablation["sequential_decode_attn_hbm_gbs"] = dec_bytes_step / (seq_dec / 1e3) / 1e9

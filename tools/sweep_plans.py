@@ -71,26 +71,29 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / args.steps
 
-    results = []
-    results.append(("sequential", run(nf.Plan.explicit(cfg, nf.SEQUENTIAL))))
-    print(results[-1], flush=True)
-    results.append(("nano_only bal=2", run(nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=(1, 1), balance=2))))
-    print(results[-1], flush=True)
+    # build every plan first, then time them in a forward and a reverse pass (power / thermal
+    # drift of the 1 kW part would otherwise favour whichever plan runs first); mean of passes
+    plans = [("sequential", nf.Plan.explicit(cfg, nf.SEQUENTIAL)),
+             ("nano_only bal=2", nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=(1, 1), balance=2))]
     for sh in args.shares.split(","):
         shares = tuple(int(x) for x in sh.split(":"))
         for bal in [int(x) for x in args.bal.split(",")]:
             for sp in args.splits.split(","):
                 dense, dec = (int(x) for x in sp.split("/"))
                 sm = [dense, dec, dense, dense, dense, dense, 8]
-                name = f"overlap shares={shares} bal={bal} dense={dense} dec={dec}"
-                pl = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm, balance=bal)
-                results.append((name, run(pl)))
-                print(results[-1], pl.runtime_note(), flush=True)
+                plans.append((f"overlap shares={shares} bal={bal} dense={dense} dec={dec}",
+                              nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm, balance=bal)))
     for shares in ([tuple(int(x) for x in sh.split(":")) for sh in args.colocate.split(",")] if args.colocate else []):
-        name = f"colocate shares={shares}"
-        results.append((name, run(nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=[148] * 7, balance=True,
-                                                   colocate=True))))
-        print(results[-1], flush=True)
+        plans.append((f"colocate shares={shares}", nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=[148] * 7,
+                                                                     balance=True, colocate=True)))
+    acc = {n: [] for n, _ in plans}
+    for order in (plans, plans[::-1]):
+        for name, pl in order:
+            acc[name].append(run(pl))
+    results = []
+    for name, pl in plans:
+        results.append((name, sum(acc[name]) / len(acc[name])))
+        print((name, round(results[-1][1], 3), [round(x, 3) for x in acc[name]]), pl.runtime_note(), flush=True)
     print("---- best first")
     for n, t in sorted(results, key=lambda x: x[1])[:12]:
         print(f"{t:8.2f} ms  {n}")
