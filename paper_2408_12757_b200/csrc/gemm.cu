@@ -557,7 +557,8 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   //   data-parallel        ceil(tiles / SB)
   //   CTA pairs            ceil(pair_tiles / (SB/2)) for 256-row pair tiles (6-stage ring, B shared)
   //   split-K tail (s)     floor(tiles / SB) + 1/s for the partial last wave, s = min(4, SB / rem)
-  //                        splits of >= 16 k-blocks each (also covers sub-wave GEMMs)
+  //                        splits of >= 32 k-blocks each (also covers sub-wave GEMMs; 16 measured
+  //                        slower for K = 4096 under overlap: the fp32 fix-up outweighs the gain)
   //   split-K=2            ceil(2 tiles / SB) / 2, for K >= 8192 (a half tile must outweigh
   //                        writing + reading its 128 KB fp32 partial; measured on O vs Down)
   // Ties prefer CTA pairs (long-K, wide-N GEMMs only), then the simpler schedule.  NF_STREAMK=0 / NF_SPLITK=0 / NF_GEMM_CG2=0
@@ -577,7 +578,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     const int rem = tiles % SB;
     if (rem > 0) {
       int s = std::min(4, SB / rem);
-      while (s > 1 && num_kb / s < 16) --s;
+      while (s > 1 && num_kb / s < 32) --s;
       const double c = tiles / SB + 1.0 / s;
       if (s > 1 && c < best - 1e-9) { best = c; choice = 1; best_s = s; }
     }
@@ -602,7 +603,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     const int rem = pair_tiles % pairs;
     if (tail_env && rem > 0 && args.sk_part != nullptr && args.sk_slots >= SB && pair_tiles > pairs / 4) {
       int s = std::min(4, pairs / rem);
-      while (s > 1 && num_kb / s < 16) --s;
+      while (s > 1 && num_kb / s < 32) --s;
       const double ct = pair_tiles / pairs + 1.0 / s;
       if (s > 1 && ct < c - 1e-9) {
         c = ct;

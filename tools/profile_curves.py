@@ -7,7 +7,12 @@ Times each hot-path kernel of the 8B-shape step at SM budgets
 `op_kind,resource_class,units,work,latency_s` (op_kind = NF_OP_* index), the
 input of nf_plan_create.  Work: tokens for dense ops, KV keys for attention.
 
-Usage: python tools/profile_curves.py [--out profiles/curves_b200.csv] [--quick]
+With --corun every point is measured next to a co-runner on the complementary
+SMs (GEMM points next to decode attention on 148-u SMs, decode points next to the
+Up/Gate GEMM on 148-u SMs): the co-run-calibrated curves SURVEY.md §7 asks for
+("isolated curves are optimistic": HBM, L2 and power are shared).
+
+Usage: python tools/profile_curves.py [--out profiles/curves_b200.csv] [--quick] [--corun]
 """
 import argparse
 import os
@@ -22,6 +27,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "curves_b200.csv"))
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--corun", action="store_true", help="measure each point next to a co-runner on 148-u SMs")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -36,10 +42,45 @@ def main():
     rows = []
     st = rt.stream_handle()
 
-    def timeit(fn):
+    side = torch.cuda.Stream()
+    side_h = int(side.cuda_stream)
+    corunner = {"fn": None}  # fn(sm_budget, stream) launching one co-runner kernel
+
+    def timeit(fn, u=148):
         for _ in range(2):
             fn()
+        cr = corunner["fn"] if args.corun and u < 148 else None
+        if cr is not None:
+            # keep the complementary SMs busy for the whole measurement
+            torch.cuda.synchronize()
+            c0 = torch.cuda.Event(enable_timing=True)
+            c0.record(side)
+            cr(148 - u, side_h)
+            c0.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if cr is not None:
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(side)
+            cr(148 - u, side_h)
+            f1.record(side)
+            torch.cuda.synchronize()
+            per = max(f0.elapsed_time(f1), 1e-3)
+            e0.record()
+            for _ in range(args.reps):
+                fn()
+            e1.record()
+            # enough co-runner launches to outlast the timed loop (estimated from the isolated run)
+            e1.synchronize()
+            est = e0.elapsed_time(e1)
+            torch.cuda.synchronize()
+            for _ in range(int(est / per) + 3):
+                cr(148 - u, side_h)
+            e0.record()
+            for _ in range(args.reps):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / args.reps / 1e3
         e0.record()
         for _ in range(args.reps):
             fn()
@@ -47,8 +88,31 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / args.reps / 1e3
 
+    # co-runners: decode attention over the steady-state decode batch (next to GEMMs / prefill),
+    # the Up/Gate GEMM at M=1024 (next to decode attention)
+    full0 = synth.workload_batch(2048, 1024, 512)
+    n0 = int((full0.q_len == 1).sum())
+    b_cr = synth.make_batch([1] * n0, full0.kv_prefix[:n0], seed=5)
+    nb_cr = nf.Batch.from_any(b_cr)
+    cfg_cr = rt.cfg_from_shape(shape)
+    pool_cr = torch.randn((b_cr.n_pages_pool, 2, Hk, 16, hd), device=dev).to(torch.bfloat16) if args.corun else None
+    q_cr = torch.randn((n0, Hq, hd), device=dev).to(torch.bfloat16)
+    o_cr = torch.empty((n0, Hq * hd), device=dev, dtype=torch.bfloat16)
+    ws_cr = rt.workspace(cfg_cr, nb_cr)
+    A_cr = torch.randn(1024, D, device=dev).to(torch.bfloat16)
+    B_cr = (torch.randn(2 * F, D, device=dev) * D ** -0.5).to(torch.bfloat16)
+    C_cr = torch.empty(1024, 2 * F, device=dev, dtype=torch.bfloat16)
+
+    def cr_decode(sm, sth):
+        nf.attention(cfg_cr, nb_cr, q_cr.data_ptr(), pool_cr.data_ptr(), o_cr.data_ptr(), ws_cr.data_ptr(),
+                     ws_cr.numel(), sm, sm, sth)
+
+    def cr_gemm(sm, sth):
+        nf.gemm_bf16(A_cr.data_ptr(), D, B_cr.data_ptr(), D, C_cr.data_ptr(), 2 * F, 1024, 2 * F, D, sm, sth)
+
     # dense GEMMs at the nano-batch size (1024 tokens) and the full batch
     gemms = {nf.OP_KQV: ((Hq + 2 * Hk) * hd, D), nf.OP_O: (D, Hq * hd), nf.OP_UG: (2 * F, D), nf.OP_DOWN: (D, F)}
+    corunner["fn"] = cr_decode
     for M in (512, 1024, 2048):
         A = torch.randn(M, max(D, F), device=dev).to(torch.bfloat16)
         for op, (N, K) in gemms.items():
@@ -57,11 +121,12 @@ def main():
             gws = torch.empty(nf.gemm_workspace_bytes(M, N), dtype=torch.uint8, device=dev)
             for u in units:
                 t = timeit(lambda: nf.gemm_bf16(A.data_ptr(), A.shape[1], B.data_ptr(), K, C.data_ptr(), N, M, N, K,
-                                                u, st, gws.data_ptr(), gws.numel()))
+                                                u, st, gws.data_ptr(), gws.numel()), u)
                 rows.append((op, "compute", u, M, t))
             del B, C
         del A
     # decode attention over the steady-state decode requests (683, contexts 1024..1535)
+    corunner["fn"] = cr_gemm
     full = synth.workload_batch(2048, 1024, 512)
     n_dec = int((full.q_len == 1).sum())
     for frac in (0.5, 1.0):
@@ -76,11 +141,12 @@ def main():
         keys = int((b.kv_prefix + 1).sum())
         for u in units:
             t = timeit(lambda: nf.attention(cfg, nb, q.data_ptr(), pool.data_ptr(), o.data_ptr(), ws.data_ptr(),
-                                            ws.numel(), u, u, st))
+                                            ws.numel(), u, u, st), u)
             rows.append((nf.OP_DECODE_ATTN, "memory", u, keys, t))
             print(f"decode n={n} sm={u}: {t*1e6:.1f} us  {keys*Hk*hd*4/t/1e9:.0f} GB/s", flush=True)
         del pool
     # prefill attention: the chunk (341, prefix 683) + prompt (1024)
+    corunner["fn"] = cr_decode
     b = synth.make_batch([341, 1024], [683, 0], seed=3)
     nb = nf.Batch.from_any(b)
     pool = torch.randn((b.n_pages_pool, 2, Hk, 16, hd), device=dev).to(torch.bfloat16)
@@ -90,7 +156,7 @@ def main():
     keys = int(sum(p + (i + 1) for p, ql in zip(b.kv_prefix, b.q_len) for i in range(ql)))
     for u in units:
         t = timeit(lambda: nf.attention(cfg, nb, q.data_ptr(), pool.data_ptr(), o.data_ptr(), ws.data_ptr(),
-                                        ws.numel(), u, u, st))
+                                        ws.numel(), u, u, st), u)
         rows.append((nf.OP_PREFILL_ATTN, "compute", u, keys, t))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:

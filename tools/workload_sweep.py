@@ -1,0 +1,118 @@
+#!/usr/bin/env python
+"""NEXT-1: the hot path on Table 3-like workloads
+with the nano-batch plan re-searched per workload.
+
+For each workload (Splitwise / LMSYS-Chat / ShareGPT-like length distributions,
+synth/workloads.py) a steady-state dense batch of 2048 tokens is taken from the
+continuous-batching snapshot, and one model step is timed under
+  * SEQUENTIAL (the non-overlapped baseline, same kernels),
+  * the fixed OVERLAP plan tuned on the constant-length workload (bench default),
+  * the OVERLAP plan found by nf_plan_create (autosearch) for this
+    workload's batch shape on the given kernel curves (co-run calibrated),
+in interleaved rounds (power/thermal drift).  Prints one JSON line per workload.
+
+Usage: workload_sweep.py [--config c2|c3rank] [--curves profiles/curves_b200_corun.csv] [--steps N]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2", choices=["c2", "c3rank"])
+    ap.add_argument("--curves", default="profiles/curves_b200_corun.csv")
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--rounds", type=int, default=2)
+    ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--workloads", default="splitwise,lmsys,sharegpt")
+    args = ap.parse_args()
+    import torch
+
+    import synth
+    from synth import workloads as W
+    from paper_2408_12757_b200 import nf, runtime as rt
+
+    if args.config == "c3rank":
+        shape = synth.shape_with(synth.SHAPES["llama2-70b"], n_q_heads=8, n_kv_heads=1, d_ffn=3584)
+        dense, dec = 132, 16
+    else:
+        shape = synth.SHAPES["llama3-8b"]
+        dense, dec = 116, 32
+    if args.layers:
+        shape = synth.shape_with(shape, n_layers=args.layers)
+    D, F, hd, Hq, Hk, L = shape.d_model, shape.d_ffn, shape.head_dim, shape.n_q_heads, shape.n_kv_heads, shape.n_layers
+    # KV capacity of one B200 for this shape: HBM left after weights and workspace (~20 GB reserve)
+    kv_token_bytes = L * 2 * Hk * hd * 2
+    kv_cap = int((180e9 - 2 * (L * (D * (Hq + 2 * Hk) * hd + Hq * hd * D + 3 * D * F) + 2 * shape.vocab * D) - 20e9)
+                 / kv_token_bytes)
+    snaps = {}
+    for name in args.workloads.split(","):
+        ql, kp, st = W.snapshot(name, b_dense=2048, kv_cap_tokens=kv_cap)
+        snaps[name] = (ql, kp, st)
+    need = {n: int(((kp.astype("int64") + ql + 15) // 16).sum()) for n, (ql, kp, _) in snaps.items()}
+    pool_pages = max(need.values())
+    cfg = rt.cfg_from_shape(shape)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+
+    def randn(s, std=1.0, mean=0.0):
+        t = torch.empty(s, dtype=torch.bfloat16, device="cuda")
+        t.normal_(mean, std, generator=g)
+        return t
+
+    layers = []
+    for _ in range(L):
+        w = {"attn_norm": randn((D,), 0.1, 1.0), "w_q": randn((Hq * hd, D), D ** -0.5),
+             "w_k": randn((Hk * hd, D), D ** -0.5), "w_v": randn((Hk * hd, D), D ** -0.5),
+             "w_o": randn((D, Hq * hd), (Hq * hd) ** -0.5), "ffn_norm": randn((D,), 0.1, 1.0),
+             "w_gate": randn((F, D), D ** -0.5), "w_up": randn((F, D), D ** -0.5), "w_down": randn((D, F), F ** -0.5)}
+        layers.append(rt.pack_layer(cfg, w))
+    model = rt.Model(cfg, randn((shape.vocab, D)), layers,
+                     rt.pack_lm_head(cfg, randn((shape.vocab, D), D ** -0.5), randn((D,), 0.1, 1.0)))
+    pools = [randn((pool_pages, 2, Hk, 16, hd)) for _ in range(L)]
+    rows = [l.split(",") for l in open(os.path.join(ROOT, args.curves)).read().splitlines()[1:] if l.strip()]
+    pts = [(int(k), int(u), float(w), float(t)) for k, _, u, w, t in rows]
+
+    for name, (ql, kp, st) in snaps.items():
+        b = synth.make_batch(ql, kp, seed=3, pool_slack=pool_pages - need[name])
+        nb = nf.Batch.from_any(b)
+        ws = rt.workspace(cfg, nb)
+        tok = torch.randint(0, shape.vocab, (b.n_tokens,), dtype=torch.int32, device="cuda", generator=g)
+        ids = torch.empty(b.n_req, dtype=torch.int32, device="cuda")
+        auto = nf.Plan.search(cfg, nb, pts, mode=nf.OVERLAP, n_nano=2)
+        plans = [("sequential", nf.Plan.explicit(cfg, nf.SEQUENTIAL)),
+                 ("overlap_fixed", nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1),
+                                                    sm=[dense, dec, dense, dense, dense, dense, 8], balance=2)),
+                 ("overlap_autosearch", auto)]
+        for _, pl in plans:
+            for _ in range(2):
+                model.step(pl, pools, nb, tok, ws, ids)
+        times = {n: [] for n, _ in plans}
+        for _r in range(args.rounds):
+            for pn, pl in plans:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record()
+                for _ in range(args.steps):
+                    model.step(pl, pools, nb, tok, ws, ids)
+                e1.record()
+                torch.cuda.synchronize()
+                times[pn].append(e0.elapsed_time(e1) / args.steps)
+        sp = auto.spec()
+        res = {"workload": name, "config": args.config, "batch": st,
+               "autosearch_plan": {"sm": list(sp.sm), "shares": list(sp.share)[:sp.n_nano], "note": auto.runtime_note()}}
+        for pn, _ in plans:
+            ms = statistics.median(times[pn])
+            res[pn] = {"ms_per_step": ms, "tokens_per_s": b.n_tokens / (ms / 1e3)}
+        print(json.dumps(res), flush=True)
+        del ws
+
+
+if __name__ == "__main__":
+    main()
