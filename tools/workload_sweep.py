@@ -8,10 +8,11 @@ continuous-batching snapshot, and one model step is timed under
   * SEQUENTIAL (the non-overlapped baseline, same kernels),
   * the fixed OVERLAP plan tuned on the constant-length workload (bench default),
   * the OVERLAP plan found by nf_plan_create (autosearch) for this
-    workload's batch shape on the given kernel curves (co-run calibrated),
+    workload's batch shape on the given kernel curves,
+  * the best of a small measured grid (shares x partition splits) re-searched per workload,
 in interleaved rounds (power/thermal drift).  Prints one JSON line per workload.
 
-Usage: workload_sweep.py [--config c2|c3rank] [--curves profiles/curves_b200_corun.csv] [--steps N]
+Usage: workload_sweep.py [--config c2|c3rank] [--curves profiles/curves_b200_r1b.csv] [--steps N]
 """
 import argparse
 import json
@@ -26,7 +27,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2", choices=["c2", "c3rank"])
-    ap.add_argument("--curves", default="profiles/curves_b200_corun.csv")
+    ap.add_argument("--curves", default="profiles/curves_b200_r1b.csv")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--layers", type=int, default=0)
@@ -90,6 +91,14 @@ def main():
                  ("overlap_fixed", nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1),
                                                     sm=[dense, dec, dense, dense, dense, dense, 8], balance=2)),
                  ("overlap_autosearch", auto)]
+        # measured re-search per workload: a small grid of shares x partition splits
+        grid = []
+        for sh in ((1, 1), (3, 5), (5, 3)):
+            for dd, de in ((dense - 8, dec + 8), (dense, dec), (dense + 8, dec - 8)):
+                if de >= 8:
+                    grid.append((f"grid shares={sh[0]}:{sh[1]} dense={dd} dec={de}",
+                                 nf.Plan.explicit(cfg, nf.OVERLAP, shares=sh, sm=[dd, de, dd, dd, dd, dd, 8], balance=2)))
+        plans += grid
         for _, pl in plans:
             for _ in range(2):
                 model.step(pl, pools, nb, tok, ws, ids)
@@ -107,9 +116,12 @@ def main():
         sp = auto.spec()
         res = {"workload": name, "config": args.config, "batch": st,
                "autosearch_plan": {"sm": list(sp.sm), "shares": list(sp.share)[:sp.n_nano], "note": auto.runtime_note()}}
-        for pn, _ in plans:
+        for pn, _ in plans[:3]:
             ms = statistics.median(times[pn])
             res[pn] = {"ms_per_step": ms, "tokens_per_s": b.n_tokens / (ms / 1e3)}
+        gbest = min((statistics.median(times[pn]), pn) for pn, _ in grid)
+        res["overlap_measured_search"] = {"ms_per_step": gbest[0], "tokens_per_s": b.n_tokens / (gbest[0] / 1e3),
+                                          "plan": gbest[1]}
         print(json.dumps(res), flush=True)
         del ws
 
