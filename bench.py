@@ -104,13 +104,36 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- oracle sample
-def oracle_sample(shape, n_dec=64, chunk=64):
+def config_shape(config, tp=1):
+    """(shape, p_in, d_out) of a bench config (SURVEY.md §8 shape key)."""
+    import synth
+    if config == "c3rank":
+        return (synth.shape_with(synth.SHAPES["llama2-70b"], name="llama2-70b-tp8-rank", n_q_heads=8, n_kv_heads=1,
+                                 d_ffn=28672 // 8), 512, 1024)
+    if config == "c3":
+        return synth.SHAPES["llama2-70b"], 512, 1024
+    return synth.SHAPES["llama3-8b"], 1024, 512
+
+
+def workload_desc(config, L, tp=1, b_dense=2048):
+    if config == "c2":
+        return (f"configs[1]: LLaMA-3-8B-shape {L}-layer serving step, B_dense 2048 "
+                f"(683 decode ctx 1024-1535 + 341-token chunk + 1024-token prompt), page 16")
+    if config == "c3rank":
+        return (f"configs[2] rank-local proxy: one LLaMA-2-70B TP8 rank's shards (D 8192, 8/1 heads, "
+                f"F 3584), {L} layers, B_dense 2048 (1365 decode ctx 512-1535 + 171 chunk + 512 prompt), "
+                f"no collectives")
+    return (f"configs[2]: LLaMA-2-70B-shape {L}-layer serving step, TP={tp} over NCCL, B_dense {b_dense} "
+            f"(constant 512 in / 1024 out steady state), page 16")
+
+
+def oracle_sample(shape, n_dec=64, chunk=64, p_in=1024, d_out=512):
     """Bounded sample of the same workload for the CPU oracle: n_dec decode
-    requests drawn from the steady state (contexts 1024..1535) plus one prefill
-    chunk of `chunk` tokens (prefix 0), one decoder layer."""
+    requests drawn from the steady state (contexts p_in..p_in+d_out-1) plus one
+    prefill chunk of `chunk` tokens (prefix 0), one decoder layer."""
     import numpy as np
     import synth
-    full = synth.workload_batch(2048, 1024, 512)
+    full = synth.workload_batch(2048, p_in, d_out)
     q_len = [1] * n_dec + [chunk]
     prefix = list(full.kv_prefix[:n_dec]) + [0]
     b = synth.make_batch(q_len, prefix, seed=3)
@@ -151,9 +174,8 @@ def blas_threads():
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    import synth
-    shape = synth.SHAPES["llama3-8b"]
-    b, w, x, pool = oracle_sample(shape)
+    shape, p_in, d_out = config_shape(args.config)
+    b, w, x, pool = oracle_sample(shape, p_in=p_in, d_out=d_out)
     T = b.n_tokens
     for _ in range(args.warmup):
         time_oracle_layer(shape, b, w, x, pool)
@@ -162,14 +184,15 @@ def run_reference(args, rank, world):
         ts += time_oracle_layer(shape, b, w, x, pool)
     t_step = statistics.median(ts) * shape.n_layers  # x L-extrapolated step time for the sample
     value = T / t_step
-    sample = (f"one float64 oracle decoder layer (numpy/BLAS) of the LLaMA-3-8B shape over {T} tokens "
+    sample = (f"one float64 oracle decoder layer (numpy/BLAS) of the {shape.name} shape over {T} tokens "
               f"(64 decode requests with the steady-state contexts + one 64-token prefill chunk), "
               f"x{shape.n_layers} layers extrapolated")
     cores = blas_threads() or cpu_cores()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[1] LLaMA-3-8B-shape serving step (oracle sample)", "sample_tokens": T},
+            "config": {"workload": workload_desc(args.config, shape.n_layers, tp=max(1, args.gpus)),
+                       "b_dense": 2048, "n_layers": shape.n_layers, "oracle_sample_tokens": T},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -459,12 +482,7 @@ def run_nf(args, rank, world, local_rank):
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if tp > 1 else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, seeded torch RNG on device)",
-            "config": {"workload": (f"configs[1]: LLaMA-3-8B-shape {L}-layer serving step, B_dense 2048 "
-                                    f"(683 decode ctx 1024-1535 + 341-token chunk + 1024-token prompt), page 16")
-                       if args.config == "c2" else
-                       (f"configs[2] rank-local proxy: one LLaMA-2-70B TP8 rank's shards (D 8192, 8/1 heads, "
-                        f"F 3584), {L} layers, B_dense 2048 (1365 decode ctx 512-1535 + 171 chunk + 512 prompt), "
-                        f"no collectives"),
+            "config": {"workload": workload_desc(args.config, L, tp=tp, b_dense=T),
                        "b_dense": T, "n_layers": L, "mode": args.mode, "colocate": bool(plan.spec().colocate),
                        "parallelism": (f"tp{tp}" if tp > 1 else ("replicas" if world > 1 else "single-gpu")),
                        "plan_sm": list(plan.spec().sm), "plan_shares": list(plan.spec().share)[:plan.spec().n_nano],
@@ -480,12 +498,12 @@ def run_nf(args, rank, world, local_rank):
             "ablation": ablation,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}}
     if world == 1 and not args.no_cpu_baseline:
-        b_s, w_s, x_s, pool_s = oracle_sample(shape)
+        b_s, w_s, x_s, pool_s = oracle_sample(shape, p_in=p_in, d_out=d_out)
         ts = time_oracle_layer(shape, b_s, w_s, x_s, pool_s, reps=3)
         t_step = statistics.median(ts) * shape.n_layers
         line["cpu_baseline"] = {"value": b_s.n_tokens / t_step, "unit": "tokens/s",
                                 "cores": blas_threads() or cpu_cores(), "kind": "oracle",
-                                "sample": f"float64 oracle, one 8B-shape layer over {b_s.n_tokens} tokens (64 decode "
+                                "sample": f"float64 oracle, one {shape.name} layer over {b_s.n_tokens} tokens (64 decode "
                                           f"+ 64-token chunk), median of 3, x{shape.n_layers} layers extrapolated"}
     print(json.dumps(line), flush=True)
 
