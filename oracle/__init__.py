@@ -16,6 +16,9 @@ mixed prefill/decode batch with a paged KV cache, written in float64 numpy:
 * ``layer``     — RMSNorm, RoPE, KV append, paged causal GQA attention,
                   the decoder layer, per-nano-batch execution, the TP-sharded
                   algebra and the model step (embedding .. argmax).
+* ``moe``       — the Mixtral-shape MoE FFN (readings A-20..A-23):
+                  router top-k, expert SwiGLU, weighted combine, TP-sharded
+                  form, and the integer token grouping of the grouped GEMMs.
 * ``planner``   — the §5.6 autosearch step by step (critical path + greedy).
 
 Every function cites the PAPER.md line (``P:n``) or SURVEY.md reading

@@ -124,6 +124,24 @@ def qkv(h, w):
     return h @ f64(w["w_q"]).T, h @ f64(w["w_k"]).T, h @ f64(w["w_v"]).T
 
 
+def attention_block(x, w: Dict[str, np.ndarray], pool: np.ndarray, batch, shape,
+                    page_size: int = 16) -> np.ndarray:
+    """Steps 1-6 of ``decoder_layer``: h1 = x + Attn(RMSNorm(x) * g_attn) W_o^T
+    (readings A-1, A-4..A-6); appends the step's K/V to ``pool``."""
+    x = f64(x)
+    T = x.shape[0]
+    hd, qh, kh = shape.head_dim, shape.n_q_heads, shape.n_kv_heads
+    pos = md.positions(batch.q_len, batch.kv_prefix)
+    h = rmsnorm(x, w["attn_norm"], shape.rms_eps)
+    q, k, v = qkv(h, w)
+    q = rope(q.reshape(T, qh, hd), pos, shape.rope_theta)
+    k = rope(k.reshape(T, kh, hd), pos, shape.rope_theta)
+    v = v.reshape(T, kh, hd)
+    kv_append(pool, k, v, batch, page_size)
+    o = paged_attention(q, pool, batch, page_size).reshape(T, qh * hd)
+    return x + o @ f64(w["w_o"]).T
+
+
 def decoder_layer(x, w: Dict[str, np.ndarray], pool: np.ndarray, batch, shape,
                   page_size: int = 16) -> np.ndarray:
     """One LLaMA-style decoder layer (readings A-1..A-6).
@@ -138,18 +156,7 @@ def decoder_layer(x, w: Dict[str, np.ndarray], pool: np.ndarray, batch, shape,
     8. out = h1 + m W_d^T
     ``pool`` is updated in place (the appended K/V).
     """
-    x = f64(x)
-    T = x.shape[0]
-    hd, qh, kh = shape.head_dim, shape.n_q_heads, shape.n_kv_heads
-    pos = md.positions(batch.q_len, batch.kv_prefix)
-    h = rmsnorm(x, w["attn_norm"], shape.rms_eps)
-    q, k, v = qkv(h, w)
-    q = rope(q.reshape(T, qh, hd), pos, shape.rope_theta)
-    k = rope(k.reshape(T, kh, hd), pos, shape.rope_theta)
-    v = v.reshape(T, kh, hd)
-    kv_append(pool, k, v, batch, page_size)
-    o = paged_attention(q, pool, batch, page_size).reshape(T, qh * hd)
-    h1 = x + o @ f64(w["w_o"]).T
+    h1 = attention_block(x, w, pool, batch, shape, page_size)
     h2 = rmsnorm(h1, w["ffn_norm"], shape.rms_eps)
     m = silu(h2 @ f64(w["w_gate"]).T) * (h2 @ f64(w["w_up"]).T)
     return h1 + m @ f64(w["w_down"]).T

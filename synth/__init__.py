@@ -40,6 +40,8 @@ class ModelShape:
     rope_theta: float
     rms_eps: float = 1e-5          # reading A-2
     page_size: int = PAGE_SIZE
+    n_experts: int = 0             # 0 = dense FFN; > 0: MoE FFN (readings A-20..A-23)
+    top_k: int = 2
 
     @property
     def qkv_out(self) -> int:
@@ -53,6 +55,10 @@ SHAPES: Dict[str, ModelShape] = {
     "llama3-8b": ModelShape("llama3-8b", 4096, 32, 32, 8, 128, 14336, 128256, 5e5),
     # configs[2]: LLaMA-2-70B shape (F = 28672 implied by Table 2)
     "llama2-70b": ModelShape("llama2-70b", 8192, 80, 64, 8, 128, 28672, 32000, 1e4),
+    # configs[3]: Mixtral-8x7B shape (public config: 8 experts, top-2, F 14336 per expert, theta 1e6)
+    "mixtral-8x7b": ModelShape("mixtral-8x7b", 4096, 32, 32, 8, 128, 14336, 32000, 1e6, n_experts=8, top_k=2),
+    # tiny MoE layer for parity tests (configs[0] attention shape, 8 experts, ragged F)
+    "c1-moe": ModelShape("c1-moe", 512, 1, 8, 2, 64, 704, 32000, 1e4, n_experts=8, top_k=2),
 }
 
 
@@ -188,6 +194,20 @@ def layer_weights(shape: ModelShape, layer: int, seed: int = 0) -> Dict[str, np.
     D, F, hd = shape.d_model, shape.d_ffn, shape.head_dim
     Hq, Hk = shape.n_q_heads, shape.n_kv_heads
     p = f"L{layer}."
+    if shape.n_experts:
+        E = shape.n_experts
+        return {
+            "attn_norm": randn_bf16((D,), seed, p + "attn_norm", 0.1, 1.0),
+            "w_q": randn_bf16((Hq * hd, D), seed, p + "w_q", D ** -0.5),
+            "w_k": randn_bf16((Hk * hd, D), seed, p + "w_k", D ** -0.5),
+            "w_v": randn_bf16((Hk * hd, D), seed, p + "w_v", D ** -0.5),
+            "w_o": randn_bf16((D, Hq * hd), seed, p + "w_o", (Hq * hd) ** -0.5),
+            "ffn_norm": randn_bf16((D,), seed, p + "ffn_norm", 0.1, 1.0),
+            "w_router": randn_bf16((E, D), seed, p + "w_router", D ** -0.5),
+            "w_gate": randn_bf16((E, F, D), seed, p + "w_gate", D ** -0.5),
+            "w_up": randn_bf16((E, F, D), seed, p + "w_up", D ** -0.5),
+            "w_down": randn_bf16((E, D, F), seed, p + "w_down", F ** -0.5),
+        }
     return {
         "attn_norm": randn_bf16((D,), seed, p + "attn_norm", 0.1, 1.0),
         "w_q": randn_bf16((Hq * hd, D), seed, p + "w_q", D ** -0.5),
