@@ -44,10 +44,12 @@ def load_peaks():
 
 
 def p_active(shape):
-    """Matmul weights touched per token: L*(D*(Hq+2Hkv)*hd + Hq*hd*D + 3*D*F) + V*D."""
+    """Matmul weights touched per token (SURVEY §8d): L*(D*(Hq+2Hkv)*hd + Hq*hd*D + 3*D*F) + V*D;
+    MoE: the FFN term is top_k*3*D*F + E*D (router), SURVEY §8d (Mixtral 12.75e9)."""
     s = shape
+    ffn = (s.top_k * 3 * s.d_model * s.d_ffn + s.n_experts * s.d_model) if s.n_experts else 3 * s.d_model * s.d_ffn
     return s.n_layers * (s.d_model * (s.n_q_heads + 2 * s.n_kv_heads) * s.head_dim +
-                         s.n_q_heads * s.head_dim * s.d_model + 3 * s.d_model * s.d_ffn) + s.vocab * s.d_model
+                         s.n_q_heads * s.head_dim * s.d_model + ffn) + s.vocab * s.d_model
 
 
 # ---------------------------------------------------------------------------- clocks
@@ -112,7 +114,18 @@ def config_shape(config, tp=1):
                                  d_ffn=28672 // 8), 512, 1024)
     if config == "c3":
         return synth.SHAPES["llama2-70b"], 512, 1024
+    if config == "c4rank":
+        return mixtral_rank_shape(), 512, 1024
+    if config == "c4":
+        return synth.SHAPES["mixtral-8x7b"], 512, 1024
     return synth.SHAPES["llama3-8b"], 1024, 512
+
+
+def mixtral_rank_shape():
+    """One Mixtral-8x7B TP8 rank's shards: 4/1 heads, 8 experts x F 1792 (configs[3] proxy)."""
+    import synth
+    return synth.shape_with(synth.SHAPES["mixtral-8x7b"], name="mixtral-8x7b-tp8-rank", n_q_heads=4, n_kv_heads=1,
+                            d_ffn=14336 // 8)
 
 
 def workload_desc(config, L, tp=1, b_dense=2048):
@@ -123,6 +136,13 @@ def workload_desc(config, L, tp=1, b_dense=2048):
         return (f"configs[2] rank-local proxy: one LLaMA-2-70B TP8 rank's shards (D 8192, 8/1 heads, "
                 f"F 3584), {L} layers, B_dense 2048 (1365 decode ctx 512-1535 + 171 chunk + 512 prompt), "
                 f"no collectives")
+    if config == "c4rank":
+        return (f"configs[3] rank-local proxy: one Mixtral-8x7B TP8 rank's shards (D 4096, 4/1 heads, 8 experts "
+                f"x F 1792, top-2), {L} layers, B_dense 2048 (1365 decode ctx 512-1535 + 171 chunk + 512 prompt), "
+                f"no collectives")
+    if config == "c4":
+        return (f"configs[3]: Mixtral-8x7B-shape {L}-layer serving step (8 experts, top-2), TP={tp} over NCCL, "
+                f"B_dense {b_dense} (constant 512 in / 1024 out steady state), page 16")
     return (f"configs[2]: LLaMA-2-70B-shape {L}-layer serving step, TP={tp} over NCCL, B_dense {b_dense} "
             f"(constant 512 in / 1024 out steady state), page 16")
 
@@ -146,11 +166,13 @@ def oracle_sample(shape, n_dec=64, chunk=64, p_in=1024, d_out=512):
 def time_oracle_layer(shape, b, w, x, pool, reps=1):
     import numpy as np
     from oracle import layer as OL
+    from oracle import moe as OM
+    layer = OM.moe_decoder_layer if shape.n_experts else OL.decoder_layer
     ts = []
     for _ in range(reps):
         p = OL.as_pool(pool)
         t0 = time.perf_counter()
-        OL.decoder_layer(x, w, p, b, shape)
+        layer(x, w, p, b, shape)
         ts.append(time.perf_counter() - t0)
     return ts
 
@@ -218,6 +240,16 @@ def run_nf(args, rank, world, local_rank):
         tp = world
         shape = synth.SHAPES["llama2-70b"]
         p_in, d_out = 512, 1024
+    elif args.config in ("c4", "c4rank"):
+        # configs[3]: Mixtral-8x7B shape (MoE); c4 = TP over all ranks, c4rank = one TP8 rank's shards
+        if args.config == "c4":
+            if world < 2:
+                raise SystemExit("--config c4 needs torchrun with >= 2 GPUs (weights + KV of the 2048 batch exceed one B200)")
+            tp = world
+            shape = synth.SHAPES["mixtral-8x7b"]
+        else:
+            shape = mixtral_rank_shape()
+        p_in, d_out = 512, 1024
     elif args.config == "c3rank":
         # rank-local proxy of configs[2] (70B TP8): one rank's head/FFN shards, no collectives
         shape = synth.shape_with(synth.SHAPES["llama2-70b"], name="llama2-70b-tp8-rank", n_q_heads=8, n_kv_heads=1,
@@ -247,9 +279,23 @@ def run_nf(args, rank, world, local_rank):
         return t
 
     D, F, hd, Hq, Hk = shape.d_model, shape.d_ffn, shape.head_dim, shape.n_q_heads, shape.n_kv_heads
+    E = shape.n_experts
+    ex = (E,) if E else ()                     # MoE: expert-major [E, F/N, D] / [E, D, F/N]
     layers = []
     for l in range(L):
-        if tp == 1:
+        if E:
+            qs, ks, Dl, Fl = Hq // tp * hd, Hk // tp * hd, D // tp, F // tp
+            w = {"attn_norm": randn((D,), 0.1, 1.0), "w_q": randn((qs, D), D ** -0.5),
+                 "w_k": randn((ks, D), D ** -0.5), "w_v": randn((ks, D), D ** -0.5),
+                 "ffn_norm": randn((D,), 0.1, 1.0), "w_router": randn((E, D), D ** -0.5),
+                 "w_gate": randn(ex + (Fl, D), D ** -0.5), "w_up": randn(ex + (Fl, D), D ** -0.5),
+                 "w_down": randn(ex + (D, Fl), F ** -0.5)}
+            if tp == 1:
+                w["w_o"] = randn((D, Hq * hd), (Hq * hd) ** -0.5)
+            else:
+                w["w_o_col"] = randn((Dl, Hq * hd), (Hq * hd) ** -0.5)
+                w["w_o_row"] = randn((D, qs), (Hq * hd) ** -0.5)
+        elif tp == 1:
             w = {"attn_norm": randn((D,), 0.1, 1.0), "w_q": randn((Hq * hd, D), D ** -0.5),
                  "w_k": randn((Hk * hd, D), D ** -0.5), "w_v": randn((Hk * hd, D), D ** -0.5),
                  "w_o": randn((D, Hq * hd), (Hq * hd) ** -0.5), "ffn_norm": randn((D,), 0.1, 1.0),
@@ -434,8 +480,10 @@ def run_nf(args, rank, world, local_rank):
     # ---------------- roofline of the dominant kernel (per-op CUDA-event time in the timed region)
     peaks, peak_src = load_peaks()
     qkv_n = (Hq_l + 2 * Hk_l) * hd
-    flops = {"kqv": 2 * T * qkv_n * D * L, "o_proj": 2 * T * D * Hq_l * hd * L, "up_gate": 2 * T * 2 * F_l * D * L,
-             "down": 2 * T * D * F_l * L, "lm_head": 2 * b.n_req * shape.vocab * D}
+    rows_ffn = T * (shape.top_k if E else 1)          # MoE: top_k expert rows per token (padding excluded)
+    flops = {"kqv": 2 * T * qkv_n * D * L, "o_proj": 2 * T * D * Hq_l * hd * L,
+             "up_gate": 2 * rows_ffn * 2 * F_l * D * L, "down": 2 * rows_ffn * D * F_l * L,
+             "lm_head": 2 * b.n_req * shape.vocab * D}
     per_op = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
               for k, v in prof.items() if v[1]}
     dom = max(per_op, key=lambda k: per_op[k]["ms_per_step"])
@@ -522,8 +570,9 @@ def main():
     ap.add_argument("--balance", type=int, default=2, help="0 request order, 1 balanced, 2 exact shares + KV")
     ap.add_argument("--colocate", action="store_true", help="attention CTAs co-resident with GEMM CTAs")
     ap.add_argument("--sm", default="", help="comma-separated SM budget per op kind (7 values)")
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c3rank"],
-                    help="c2: configs[1] 8B 1 GPU (replicas for N>1); c3: configs[2] 70B TP=N; c3rank: 1-GPU proxy")
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c3rank", "c4", "c4rank"],
+                    help="c2: configs[1] 8B 1 GPU (replicas for N>1); c3: configs[2] 70B TP=N; c3rank: 1-GPU proxy; "
+                         "c4: configs[3] Mixtral-8x7B TP=N; c4rank: its 1-GPU TP8-rank proxy")
     ap.add_argument("--layers", type=int, default=0, help="(dev only) override layer count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ablation", action="store_true", help="skip the sequential / nano-only comparison runs")

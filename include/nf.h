@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define NF_ABI_VERSION 1
+#define NF_ABI_VERSION 2
 
 typedef enum {
   NF_OK = 0,
@@ -58,6 +58,10 @@ typedef struct {
   float rope_theta; /* RoPE base (reading A-4) */
   int32_t page_size;
   int32_t tp_size, tp_rank;
+  /* MoE FFN (Mixtral-8x7B shape; "the gating operation is required for
+   * expert selection"; readings A-20..A-23): n_experts = 0 is the dense FFN.
+   * 1 <= top_k <= min(n_experts, 4), n_experts <= 16 (NF_EUNSUPPORTED above). */
+  int32_t n_experts, top_k;
 } nf_model_cfg;
 
 /* One step's global batch (PAPER.md:155 chunked prefill co-batched with
@@ -166,19 +170,25 @@ void nf_comm_destroy(nf_comm* comm);
 /* This rank's shards in canonical [out, in] row-major bf16 (device):
  * w_q [qh/N*hd, D], w_k/w_v [kh/N*hd, D], w_o [D, qh*hd] FULL (TP1) or NULL,
  * w_o_col [D/N, qh*hd] and w_o_row [D, qh/N*hd] (TP>1), w_gate/w_up [F/N, D],
- * w_down [D, F/N], norms [D]. */
+ * w_down [D, F/N], norms [D].
+ * MoE (n_experts = E > 0): w_router [E, D] (replicated), w_gate/w_up [E][F/N, D] and
+ * w_down [E][D, F/N] expert-major (each expert's F columns split across ranks). */
 typedef struct {
   const void *attn_norm, *w_q, *w_k, *w_v, *w_o, *w_o_col, *w_o_row, *ffn_norm, *w_gate, *w_up, *w_down;
+  const void* w_router; /* MoE only, else NULL */
 } nf_layer_weights;
 /* Packed, kernel-ready layer (caller-allocated device buffers, sizes from nf_packed_layer_bytes):
  * w_qkv [(qh+2kh)/N*hd, D] with gamma_attn folded into columns;
  * w_o: TP1 [D, qh*hd]; TP>1 w_o = w_o_col [D/N, D] and w_o_row [D, D/N];
  * w_gate_up [ceil(F/N/128)*256, D] gate/up interleaved in 128-row blocks, gamma_ffn folded;
- * w_down [D, F/N]. */
+ * w_down [D, F/N].
+ * MoE: w_gate_up [E][ceil(F/N/128)*256, D], w_down [E][D, F/N], w_router fp32 [E, D] = W_r * gamma_ffn
+ * (exact: a product of two bf16 values). */
 typedef struct {
   void *w_qkv, *w_o, *w_o_row, *w_gate_up, *w_down;
+  void* w_router; /* MoE only (bytes_out[5] > 0) */
 } nf_packed_layer;
-nf_status nf_packed_layer_bytes(const nf_model_cfg* cfg, size_t bytes_out[5]);
+nf_status nf_packed_layer_bytes(const nf_model_cfg* cfg, size_t bytes_out[6]);
 nf_status nf_pack_layer(const nf_model_cfg* cfg, const nf_layer_weights* src, const nf_packed_layer* dst, void* stream);
 /* lm_head_packed [V, D] = lm_head * gamma_final (vocab is not sharded in this version). */
 nf_status nf_pack_lm_head(const nf_model_cfg* cfg, const void* lm_head, const void* final_norm, void* dst, void* stream);
@@ -222,6 +232,21 @@ size_t nf_gemm_workspace_bytes(int32_t M, int32_t N);
  * sm_decode SMs, prefill chunks on the prefill kernel with sm_prefill SMs. */
 nf_status nf_attention(const nf_model_cfg* cfg, const nf_batch* b, const void* q, const void* kv_pool, void* o,
                        void* ws, size_t ws_bytes, int32_t sm_decode, int32_t sm_prefill, void* stream);
+
+/* MoE gating and token grouping of one batch of rows (readings A-21, A-23),
+ * the first two steps of the MoE FFN that nf_layer_forward runs, exposed for the
+ * bit-exact index tests.  h1 [T, D] bf16 (device); router_packed fp32 [E, D] (from
+ * nf_pack_layer).  Outputs (device): ids/wts [T, top_k] (experts by descending logit,
+ * lowest index on ties; weights = softmax over the selected logits), grp_off [E+1]
+ * (expert segments padded to 128 rows), dst [T, top_k] (grouped row of each
+ * assignment, token-major within an expert), row_tok [nf_moe_rows_cap(T)] (token of
+ * each grouped row, -1 = padding; rows >= grp_off[E] untouched).  ws: device scratch
+ * of nf_moe_route_ws_bytes bytes. */
+int64_t nf_moe_rows_cap(const nf_model_cfg* cfg, int32_t T);
+size_t nf_moe_route_ws_bytes(const nf_model_cfg* cfg, int32_t T);
+nf_status nf_moe_route(const nf_model_cfg* cfg, const void* h1, const void* router_packed, int32_t T, int32_t* ids,
+                       float* wts, int32_t* grp_off, int32_t* dst, int32_t* row_tok, void* ws, size_t ws_bytes,
+                       void* stream);
 
 /* ------------------------------------------------------------------ instrumentation */
 /* Cumulative number of CUDA kernels this process launched through libnf. */

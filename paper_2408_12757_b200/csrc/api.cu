@@ -12,6 +12,7 @@
 #include "attention.cuh"
 #include "gemm.cuh"
 #include "host.h"
+#include "moe.cuh"
 #include "misc.cuh"
 #include "profile.h"
 
@@ -67,7 +68,18 @@ nf_status validate_cfg(const nf_model_cfg* c) {
   if (c->vocab % 32) return set_error(NF_EUNSUPPORTED, "vocab must be a multiple of 32");
   if (c->n_q_heads / c->n_kv_heads > 8) return set_error(NF_EUNSUPPORTED, "GQA group > 8 (decode kernel N = 8)");
   if (!(c->rms_eps > 0) || !(c->rope_theta > 1)) return set_error(NF_EINVAL, "bad rms_eps / rope_theta");
+  if (c->n_experts < 0) return set_error(NF_EINVAL, "n_experts %d < 0", c->n_experts);
+  if (c->n_experts > 0) {
+    if (c->top_k < 1 || c->top_k > c->n_experts) return set_error(NF_EINVAL, "top_k %d not in [1, n_experts]", c->top_k);
+    if (c->n_experts > MOE_MAX_EXPERTS || c->top_k > MOE_MAX_TOPK)
+      return set_error(NF_EUNSUPPORTED, "MoE with %d experts / top-%d (max %d / %d)", c->n_experts, c->top_k,
+                       MOE_MAX_EXPERTS, MOE_MAX_TOPK);
+  }
   return NF_OK;
+}
+
+int64_t moe_rows_cap(const nf_model_cfg* c, int64_t T) {
+  return c->n_experts > 0 ? ((T * c->top_k + GEMM_BM - 1) / GEMM_BM + c->n_experts) * GEMM_BM : 0;
 }
 
 nf_status validate_batch(const nf_model_cfg* c, const nf_batch* b) {
@@ -296,6 +308,21 @@ Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base) 
   w.sk_flag_n = (int)(((T + GEMM_BM - 1) / GEMM_BM) * ((maxN + 127) / 128) +
                       ((R + GEMM_BM - 1) / GEMM_BM) * VT + 64);
   w.sk_flag = (int*)take((size_t)w.sk_flag_n * 4);
+  if (c->n_experts > 0) {
+    const int64_t cap = moe_rows_cap(c, T), nk = T * c->top_k;
+    w.mo_cap = cap;
+    w.mo_ids = (int*)take(nk * 4);
+    w.mo_wts = (float*)take(nk * 4);
+    w.mo_inv = (float*)take(T * 4);
+    w.mo_grp = (int*)take((2 * c->n_experts + 1) * 4);
+    w.mo_dst = (int*)take(nk * 4);
+    w.mo_rowtok = (int*)take(cap * 4);
+    w.mo_roww = (float*)take(cap * 4);
+    w.mo_rowinv = (float*)take(cap * 4);
+    w.mo_x = (__nv_bfloat16*)take(cap * D * 2);
+    w.mo_m = (__nv_bfloat16*)take(cap * F * 2);
+    w.mo_y = (float*)take(cap * D * 4);
+  }
   w.total = off;
   return w;
 }
@@ -347,17 +374,18 @@ nf_status nf_workspace_size(const nf_model_cfg* cfg, const nf_batch* b, size_t* 
 }
 
 // ------------------------------------------------------------------ packing
-nf_status nf_packed_layer_bytes(const nf_model_cfg* c, size_t out[5]) {
+nf_status nf_packed_layer_bytes(const nf_model_cfg* c, size_t out[6]) {
   NF_TRY(validate_cfg(c));
   if (!out) return set_error(NF_EINVAL, "out is NULL");
   const int N = c->tp_size;
   const size_t D = c->d_model, hd = c->head_dim, qh = c->n_q_heads / N, kh = c->n_kv_heads / N;
-  const size_t F = c->d_ffn / N;
+  const size_t F = c->d_ffn / N, E = c->n_experts > 0 ? c->n_experts : 1;
   out[0] = (qh + 2 * kh) * hd * D * 2;
   out[1] = N == 1 ? D * c->n_q_heads * hd * 2 : (D / N) * c->n_q_heads * hd * 2;
   out[2] = N == 1 ? 0 : D * qh * hd * 2;
-  out[3] = ((F + 127) / 128) * 256 * D * 2;
-  out[4] = D * F * 2;
+  out[3] = E * ((F + 127) / 128) * 256 * D * 2;
+  out[4] = E * D * F * 2;
+  out[5] = c->n_experts > 0 ? (size_t)c->n_experts * D * 4 : 0;
   return NF_OK;
 }
 
@@ -384,9 +412,15 @@ nf_status nf_pack_layer(const nf_model_cfg* c, const nf_layer_weights* s, const 
     NF_CUDA(cudaMemcpyAsync(d->w_o, s->w_o_col, (size_t)(D / N) * c->n_q_heads * hd * 2, cudaMemcpyDeviceToDevice, st));
     NF_CUDA(cudaMemcpyAsync(d->w_o_row, s->w_o_row, (size_t)D * qh * hd * 2, cudaMemcpyDeviceToDevice, st));
   }
-  NF_CUDA(launch_pack_gate_up((const B*)s->w_gate, (const B*)s->w_up, (const B*)s->ffn_norm, (int)F, (int)D,
-                              (B*)d->w_gate_up, st));
-  NF_CUDA(cudaMemcpyAsync(d->w_down, s->w_down, (size_t)D * F * 2, cudaMemcpyDeviceToDevice, st));
+  const int64_t E = c->n_experts > 0 ? c->n_experts : 1, Ngu = ((F + 127) / 128) * 256;
+  if (c->n_experts > 0) {
+    if (!s->w_router || !d->w_router) return set_error(NF_EINVAL, "MoE layer needs w_router (source and packed)");
+    NF_CUDA(launch_pack_router((const B*)s->w_router, (const B*)s->ffn_norm, (int)E, (int)D, (float*)d->w_router, st));
+  }
+  for (int64_t e = 0; e < E; ++e)
+    NF_CUDA(launch_pack_gate_up((const B*)s->w_gate + e * F * D, (const B*)s->w_up + e * F * D, (const B*)s->ffn_norm,
+                                (int)F, (int)D, (B*)d->w_gate_up + e * Ngu * D, st));
+  NF_CUDA(cudaMemcpyAsync(d->w_down, s->w_down, (size_t)E * D * F * 2, cudaMemcpyDeviceToDevice, st));
   return NF_OK;
 }
 
@@ -750,6 +784,9 @@ nf_status run_attn(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
   return run_decode(L, nr, st);
 }
 
+nf_status run_moe_ffn(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* h1, const nf_packed_layer* wt,
+                      const __nv_bfloat16* resid, __nv_bfloat16* out, float* part_out);
+
 // O + residual, RMS(FFN) fold, Up/Gate + SiLU, Down + residual for one nano-batch (TP1).
 nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x, const nf_packed_layer* wt,
                          __nv_bfloat16* x_out, float* part_out) {
@@ -780,6 +817,7 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
     ProfScope ps(NF_OP_O, L.cs);
     NF_CUDA(launch_gemm(L.w->o + nr.t0 * qd, qd, (const __nv_bfloat16*)wt->w_o, qd, a, clamp_dense(L, L.p->spec.sm[NF_OP_O]), L.cs));
   }
+  if (c->n_experts > 0) return run_moe_ffn(L, nr, L.w->h1, wt, L.w->h1, x_out, part_out);
   // Up/Gate + SiLU(gate) * up, RMSNorm(h1) folded as a row scale
   GemmArgs u{};
   u.epi = EPI_SILU;
@@ -824,6 +862,75 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
     ProfScope ps(NF_OP_DOWN, L.cs);
     NF_CUDA(launch_gemm(L.w->m + nr.t0 * F, F, (const __nv_bfloat16*)wt->w_down, F, d, clamp_dense(L, L.p->spec.sm[NF_OP_DOWN]),
                         L.cs));
+  }
+  return NF_OK;
+}
+
+// MoE FFN of one nano-batch (readings A-20..A-23): gating, grouping,
+// grouped Up/Gate + SiLU (1/rms row scale), grouped Down (routing-weight row scale,
+// fp32), weighted combine.  resid != null: out = bf16(resid + sum) with RMS partials
+// (TP1); resid == null: out = bf16(sum), this rank's partial for the AllReduce (TP>1).
+// Routing buffers are reused by every nano-batch: all of it runs on the compute stream.
+nf_status run_moe_ffn(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* h1, const nf_packed_layer* wt,
+                      const __nv_bfloat16* resid, __nv_bfloat16* out, float* part_out) {
+  const nf_model_cfg* c = L.c;
+  const Workspace* w = L.w;
+  const int M = nr.t1 - nr.t0;
+  if (M <= 0) return NF_OK;
+  const int64_t D = c->d_model, Fl = c->d_ffn / c->tp_size;
+  const int E = c->n_experts, k = c->top_k, T = L.m->T;
+  const int cap = (int)moe_rows_cap(c, M);
+  int* grp_off = w->mo_grp;
+  int* grp_end = w->mo_grp + E + 1;
+  {
+    ProfScope ps(NF_PROF_MISC, L.cs);
+    NF_CUDA(launch_moe_route(h1 + nr.t0 * D, M, (int)D, (const float*)wt->w_router, E, k, c->rms_eps, w->mo_ids,
+                             w->mo_wts, w->mo_inv, L.cs));
+    NF_CUDA(launch_moe_group(w->mo_ids, w->mo_wts, w->mo_inv, M, k, E, GEMM_BM, grp_off, grp_end, w->mo_dst,
+                             w->mo_rowtok, w->mo_roww, w->mo_rowinv, L.cs));
+    NF_CUDA(launch_moe_gather(h1 + nr.t0 * D, (int)D, w->mo_rowtok, grp_off + E, cap, w->mo_x, L.cs));
+  }
+  const int stages = L.p->spec.colocate ? 3 : 4;
+  GemmArgs u{};
+  u.epi = EPI_SILU;
+  u.stages = stages;
+  u.M = cap;
+  u.N = (int)(((Fl + 127) / 128) * 256);
+  u.K = (int)D;
+  u.n_valid = (int)Fl;
+  u.out = w->mo_m;
+  u.ldo = Fl;
+  u.row_scale = w->mo_rowinv;
+  u.grp_off = grp_off;
+  u.grp_end = grp_end;
+  u.n_groups = E;
+  {
+    ProfScope ps(NF_OP_UG, L.cs);
+    NF_CUDA(launch_gemm(w->mo_x, D, (const __nv_bfloat16*)wt->w_gate_up, D, u, clamp_dense(L, L.p->spec.sm[NF_OP_UG]),
+                        L.cs));
+  }
+  GemmArgs d{};
+  d.epi = EPI_F32;
+  d.stages = stages;
+  d.M = cap;
+  d.N = (int)D;
+  d.K = (int)Fl;
+  d.n_valid = (int)D;
+  d.outf = w->mo_y;
+  d.ldo = D;
+  d.row_scale = w->mo_roww;
+  d.grp_off = grp_off;
+  d.grp_end = grp_end;
+  d.n_groups = E;
+  {
+    ProfScope ps(NF_OP_DOWN, L.cs);
+    NF_CUDA(launch_gemm(w->mo_m, Fl, (const __nv_bfloat16*)wt->w_down, Fl, d, clamp_dense(L, L.p->spec.sm[NF_OP_DOWN]),
+                        L.cs));
+  }
+  {
+    ProfScope ps(NF_PROF_MISC, L.cs);
+    NF_CUDA(launch_moe_combine(w->mo_y, w->mo_dst, M, k, (int)D, resid ? resid + nr.t0 * D : nullptr, out + nr.t0 * D,
+                               part_out ? part_out + nr.t0 : nullptr, T, nullptr, L.cs));
   }
   return NF_OK;
 }
@@ -916,6 +1023,11 @@ nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, co
     NF_TRY(from_net(L));
     NF_CUDA(launch_resid_add_rows(h1, x + nr.t0 * D, M, (int)D, L.w->part_h1 + nr.t0, L.cs));
   }
+  if (c->n_experts > 0) {
+    // MoE: every expert's F columns are split across ranks; this rank's weighted partial
+    // sum -> AR -> x_out = h1 + sum (A-12b rounding)
+    NF_TRY(run_moe_ffn(L, nr, L.w->h1, wt, nullptr, x_out, nullptr));
+  } else {
   // column-parallel Up/Gate + SiLU with the RMSNorm(h1) row scale (one partial per row)
   GemmArgs u{};
   u.epi = EPI_SILU;
@@ -949,6 +1061,7 @@ nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, co
     ProfScope ps(NF_OP_DOWN, L.cs);
     NF_CUDA(launch_gemm(L.w->m + nr.t0 * Fl, Fl, (const __nv_bfloat16*)wt->w_down, Fl, d,
                         clamp_dense(L, L.p->spec.sm[NF_OP_DOWN]), L.cs));
+  }
   }
   NF_TRY(to_net(L));
   {
@@ -1202,6 +1315,40 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
   NF_CUDA(cudaStreamWaitEvent(cs, p->ev_join, 0));
   NF_CUDA(cudaEventRecord(p->ev_join, p->net_stream));
   NF_CUDA(cudaStreamWaitEvent(cs, p->ev_join, 0));
+  return NF_OK;
+}
+
+// ------------------------------------------------------------------ MoE op-level entries
+int64_t nf_moe_rows_cap(const nf_model_cfg* c, int32_t T) {
+  if (!c || c->n_experts <= 0 || T < 0) return 0;
+  return moe_rows_cap(c, T);
+}
+
+size_t nf_moe_route_ws_bytes(const nf_model_cfg* c, int32_t T) {
+  if (!c || c->n_experts <= 0 || T < 0) return 0;
+  return ((size_t)T + c->n_experts + 2 * (size_t)moe_rows_cap(c, T)) * 4 + 1024;
+}
+
+nf_status nf_moe_route(const nf_model_cfg* c, const void* h1, const void* router_packed, int32_t T, int32_t* ids,
+                       float* wts, int32_t* grp_off, int32_t* dst, int32_t* row_tok, void* ws, size_t ws_bytes,
+                       void* stream) {
+  NF_TRY(validate_cfg(c));
+  if (c->n_experts <= 0) return set_error(NF_EINVAL, "nf_moe_route needs n_experts > 0");
+  if (T < 1) return set_error(NF_EINVAL, "T = %d < 1", T);
+  if (!h1 || !router_packed || !ids || !wts || !grp_off || !dst || !row_tok || !ws)
+    return set_error(NF_EINVAL, "NULL pointer argument");
+  if (ws_bytes < nf_moe_route_ws_bytes(c, T))
+    return set_error(NF_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, nf_moe_route_ws_bytes(c, T));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t cap = moe_rows_cap(c, T);
+  float* inv = (float*)ws;
+  int* grp_end = (int*)(inv + T);
+  float* row_w = (float*)(grp_end + c->n_experts);
+  float* row_inv = row_w + cap;
+  NF_CUDA(launch_moe_route((const __nv_bfloat16*)h1, T, c->d_model, (const float*)router_packed, c->n_experts,
+                           c->top_k, c->rms_eps, ids, wts, inv, st));
+  NF_CUDA(launch_moe_group(ids, wts, inv, T, c->top_k, c->n_experts, GEMM_BM, grp_off, grp_end, dst, row_tok, row_w,
+                           row_inv, st));
   return NF_OK;
 }
 

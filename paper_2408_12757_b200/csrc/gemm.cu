@@ -84,8 +84,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint32_t rank = 0;  // CTA rank in the pair
   if constexpr (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int wid = blockIdx.x / CG;  // tile worker: a CTA (CG 1) or a CTA pair (CG 2)
-  const int tiles_m = (M + TM - 1) / TM;
+  const bool grouped = args.grp_off != nullptr;
+  // grouped: the row count in use is device data (written by the routing kernels)
+  const int tiles_m = grouped ? min(args.grp_off[args.n_groups], M) / TM : (M + TM - 1) / TM;
   const int tiles_n = (N + BN - 1) / BN;
+  // group of an m-tile (grouped mode): the last g with grp_off[g] <= row
+  auto group_of = [&](int mb) {
+    int g = 0;
+    if (grouped)
+      while (g + 1 < args.n_groups && args.grp_off[g + 1] <= mb * TM) ++g;
+    return g;
+  };
   const int tiles = tiles_m * tiles_n;
   const int num_kb = (K + GEMM_BK - 1) / GEMM_BK;
   // Split-K tail schedule (args.tail_split = s > 1): the full waves of tiles run
@@ -156,6 +165,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint64_t b_policy = policy_evict_normal();
       for_each_seg([&](int tile, int kb0, int kb1) {
         const int mb = tile % tiles_m, nb = tile / tiles_m;
+        const int b_row0 = grouped ? group_of(mb) * N : 0;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (CG == 2) {
@@ -169,7 +179,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           } else {
             mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
             tma_load_2d_hint(sA + stage * A_STAGE_ELEMS, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM, a_policy);
-            tma_load_2d(sB + stage * B_STAGE_ELEMS, &tmB, &full[stage], kb * GEMM_BK, nb * BN);
+            tma_load_2d(sB + stage * B_STAGE_ELEMS, &tmB, &full[stage], kb * GEMM_BK, nb * BN + b_row0);
           }
           if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
         }
@@ -216,7 +226,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for_each_seg([&](int tile, int kb0, int kb1) {
       const int mb = tile % tiles_m, nb = tile / tiles_m;
       const int r = mb * TM + (int)rank * GEMM_BM + trow;
-      const bool valid = r < M;
+      const bool valid = grouped ? r < args.grp_end[group_of(mb)] : r < M;
       if (args.epi == EPI_RESID && valid && kb0 == 0) {
         // residual row segment -> L2 while the tile's mainloop still runs (short-K
         // GEMMs are otherwise epilogue-bound on these dependent global loads)
@@ -300,6 +310,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int p = 0; p < args.norm_nparts; ++p) acc += args.norm_part[(int64_t)p * args.norm_stride + r];
         s = rsqrtf(acc * args.inv_d + args.eps);
       }
+      if (args.row_scale != nullptr && valid) s *= args.row_scale[r];
       const int n0 = nb * BN;
       float v[32];
       switch (args.epi) {
@@ -574,7 +585,8 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   const int SB = std::max(1, sm_budget);
   double best = (double)((tiles + SB - 1) / SB);
   int choice = 0, best_s = 1;
-  if (tail_env && args.sk_part != nullptr && args.sk_slots >= SB) {
+  const bool grouped = args.grp_off != nullptr;  // device-sized tile list: data-parallel only
+  if (!grouped && tail_env && args.sk_part != nullptr && args.sk_slots >= SB) {
     const int rem = tiles % SB;
     if (rem > 0) {
       int s = std::min(4, SB / rem);
@@ -585,7 +597,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   }
   const int g2 = std::min(SB, 2 * tiles);
   const double rounds2 = ((2 * tiles + g2 - 1) / g2) / 2.0;
-  if (split_env && args.sk_part != nullptr && args.sk_slots >= tiles && num_kb >= 128 && rounds2 < best - 1e-9 &&
+  if (!grouped && split_env && args.sk_part != nullptr && args.sk_slots >= tiles && num_kb >= 128 && rounds2 < best - 1e-9 &&
       args.epi != EPI_SILU && args.epi != EPI_ARGMAX) {
     best = rounds2;
     choice = 2;
@@ -593,7 +605,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   const int pairs = SB / 2;
   const int pair_tiles = ((args.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((args.N + bn - 1) / bn);
   int pair_s = 1;
-  if (cg2_env && bn == 256 && !coloc && pairs >= 1) {
+  if (!grouped && cg2_env && bn == 256 && !coloc && pairs >= 1) {
     // on a tie the pair kernel measured faster only with a long mainloop and many n-tiles
     // (>= 32 k-blocks, N >= 2048; tools/gemm_micro.py): short-K pairs couple the two CTAs'
     // epilogues through the shared accumulator barrier
@@ -624,7 +636,8 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   CUtensorMap ta, tb;
   cudaError_t e = make_tmap_bf16(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
   if (e != cudaSuccess) return e;
-  e = make_tmap_bf16(&tb, B, args.K, args.N, ldb, GEMM_BK, choice == 3 ? bn / 2 : bn);
+  e = make_tmap_bf16(&tb, B, args.K, (uint64_t)args.N * (grouped ? args.n_groups : 1), ldb, GEMM_BK,
+                     choice == 3 ? bn / 2 : bn);
   if (e != cudaSuccess) return e;
   // smem ring: 4 x 48 KB (BN 256), 6 x 32 KB (BN 128 or CTA pairs); co-located plans use 3 / 4 stages
   int stages, cg = 1;

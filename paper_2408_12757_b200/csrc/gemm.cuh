@@ -62,6 +62,15 @@ struct GemmArgs {
   float* am_val;
   int* am_idx;
   int64_t am_stride;
+  // per-row output scale (multiplies the RMS row scale): MoE routing weights / 1/rms of gathered rows
+  const float* row_scale;
+  // Grouped GEMM (MoE experts, reading A-23): A rows are expert segments starting at
+  // grp_off[g] (device, multiples of GEMM_BM, grp_off[n_groups] = rows in use); rows
+  // [grp_end[g], grp_off[g+1]) are padding (not stored).  B holds n_groups blocks of N
+  // rows; the m-tile's group selects its block.  Data-parallel single-CTA tiles only.
+  const int* grp_off;
+  const int* grp_end;
+  int n_groups;
 };
 
 // Bytes of stream-K scratch for a GEMM with this many tiles at this grid.

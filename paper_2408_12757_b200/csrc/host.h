@@ -66,6 +66,17 @@ struct Workspace {
   int* sk_flag;    // stream-K tile counters
   int sk_flag_n;
   int sk_slots;
+  // MoE FFN (n_experts > 0): routing, grouping and the grouped GEMM operands (moe.cu)
+  int* mo_ids;
+  float* mo_wts;
+  float* mo_inv;
+  int* mo_grp;       // [E+1] segment offsets, then [E] segment ends
+  int* mo_dst;
+  int* mo_rowtok;
+  float *mo_roww, *mo_rowinv;
+  __nv_bfloat16 *mo_x, *mo_m;
+  float* mo_y;
+  int64_t mo_cap;    // grouped rows capacity
   size_t total;
 };
 Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base);

@@ -1,0 +1,288 @@
+// MoE FFN (Mixtral-8x7B shape) around the grouped tcgen05 GEMMs:
+//
+//   route   : RMS statistics + router logits + top-k + renormalised softmax (A-20, A-21)
+//   group   : counting sort of the T*k assignments into 128-row expert segments (A-23)
+//   gather  : h1 rows -> grouped A operand (one row per assignment)
+//   [grouped Up/Gate GEMM, SiLU*up, 1/rms row scale]    gemm.cu, EPI_SILU
+//   [grouped Down GEMM, routing-weight row scale, fp32] gemm.cu, EPI_F32
+//   combine : out = h1 + sum_j y[dst(t, j)] (fp32, one rounding) + RMS partials
+//
+// All of these are HBM/L2-bound and small next to the expert GEMMs; their bytes
+// per token are in DESIGN.md §7.
+#include "common.cuh"
+#include "profile.h"
+#include "moe.cuh"
+
+namespace nf {
+
+namespace {
+
+// TPW tokens per warp share each router read (the router stays L2-resident).
+template <int EMAX, int TPW>
+__global__ void __launch_bounds__(128) moe_route_kernel(const __nv_bfloat16* __restrict__ h1, int T, int D,
+                                                        const float* __restrict__ router, int E, int k, float eps,
+                                                        int* __restrict__ ids, float* __restrict__ wts,
+                                                        float* __restrict__ inv_rms) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int t0 = warp * TPW;
+  if (t0 >= T) return;
+  float acc[TPW][EMAX], sq[TPW];
+#pragma unroll
+  for (int j = 0; j < TPW; ++j) {
+    sq[j] = 0.f;
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) acc[j][e] = 0.f;
+  }
+  for (int i = lane * 8; i < D; i += 256) {
+    float x[TPW][8];
+#pragma unroll
+    for (int j = 0; j < TPW; ++j) {
+      uint4 u = make_uint4(0, 0, 0, 0);
+      if (t0 + j < T) u = *reinterpret_cast<const uint4*>(h1 + (int64_t)(t0 + j) * D + i);
+      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = unpack_bf16x2(w4[q]);
+        x[j][2 * q] = f.x;
+        x[j][2 * q + 1] = f.y;
+        sq[j] = fmaf(f.x, f.x, sq[j]);
+        sq[j] = fmaf(f.y, f.y, sq[j]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) {
+      if (e < E) {
+        const float4 a = *reinterpret_cast<const float4*>(router + (int64_t)e * D + i);
+        const float4 b = *reinterpret_cast<const float4*>(router + (int64_t)e * D + i + 4);
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) {
+          float s = acc[j][e];
+          s = fmaf(x[j][0], a.x, s); s = fmaf(x[j][1], a.y, s); s = fmaf(x[j][2], a.z, s); s = fmaf(x[j][3], a.w, s);
+          s = fmaf(x[j][4], b.x, s); s = fmaf(x[j][5], b.y, s); s = fmaf(x[j][6], b.z, s); s = fmaf(x[j][7], b.w, s);
+          acc[j][e] = s;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < TPW; ++j) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sq[j] += __shfl_xor_sync(0xffffffffu, sq[j], o);
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc[j][e] += __shfl_xor_sync(0xffffffffu, acc[j][e], o);
+  }
+#pragma unroll
+  for (int j = 0; j < TPW; ++j) {
+    const int t = t0 + j;
+    if (lane != j || t >= T) continue;
+    const float inv = rsqrtf(sq[j] / (float)D + eps);
+    float l[EMAX];
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) l[e] = acc[j][e] * inv;
+    // top-k: largest logit, lowest index on ties (strict > over ascending e)
+    int sel[MOE_MAX_TOPK];
+    float sl[MOE_MAX_TOPK];
+    uint32_t used = 0;
+    for (int q = 0; q < k; ++q) {
+      int bi = -1;
+      float bv = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < EMAX; ++e)
+        if (e < E && !((used >> e) & 1u) && (bi < 0 || l[e] > bv)) { bv = l[e]; bi = e; }
+      used |= 1u << bi;
+      sel[q] = bi;
+      sl[q] = bv;
+    }
+    float p[MOE_MAX_TOPK], z = 0.f;
+    for (int q = 0; q < k; ++q) { p[q] = expf(sl[q] - sl[0]); z += p[q]; }
+    for (int q = 0; q < k; ++q) {
+      ids[(int64_t)t * k + q] = sel[q];
+      wts[(int64_t)t * k + q] = p[q] / z;
+    }
+    inv_rms[t] = inv;
+  }
+}
+
+// One CTA of 1024 threads.  Pass 1 counts assignments per expert; thread 0 lays out
+// the padded segments; pass 2 ranks assignments chunk by chunk in increasing
+// assignment order (warp ballots + a per-expert scan over the 32 warps), so each
+// expert's rows are in token-major order (A-23).
+__global__ void __launch_bounds__(1024) moe_group_kernel(const int* __restrict__ ids, const float* __restrict__ wts,
+                                                         const float* __restrict__ inv_rms, int T, int k, int E,
+                                                         int tile, int* __restrict__ grp_off,
+                                                         int* __restrict__ grp_end, int* __restrict__ dst,
+                                                         int* __restrict__ row_tok, float* __restrict__ row_w,
+                                                         float* __restrict__ row_inv) {
+  __shared__ int cnt[MOE_MAX_EXPERTS], off[MOE_MAX_EXPERTS + 1], run[MOE_MAX_EXPERTS];
+  __shared__ int wcnt[32][MOE_MAX_EXPERTS];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = T * k;
+  if (tid < MOE_MAX_EXPERTS) { cnt[tid] = 0; run[tid] = 0; }
+  __syncthreads();
+  for (int a = tid; a < n; a += 1024) atomicAdd(&cnt[ids[a]], 1);
+  __syncthreads();
+  if (tid == 0) {
+    off[0] = 0;
+    for (int e = 0; e < E; ++e) off[e + 1] = off[e] + (cnt[e] + tile - 1) / tile * tile;
+    for (int e = 0; e <= E; ++e) grp_off[e] = off[e];
+    for (int e = 0; e < E; ++e) grp_end[e] = off[e] + cnt[e];
+  }
+  __syncthreads();
+  // padding rows of every segment
+  for (int e = 0; e < E; ++e)
+    for (int p = off[e] + cnt[e] + tid; p < off[e + 1]; p += 1024) {
+      row_tok[p] = -1;
+      row_w[p] = 0.f;
+      row_inv[p] = 0.f;
+    }
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int base = 0; base < n; base += 1024) {
+    const int a = base + tid;
+    const int e = a < n ? ids[a] : -1;
+    int rank = 0;
+    for (int q = 0; q < E; ++q) {
+      const uint32_t m = __ballot_sync(0xffffffffu, e == q);
+      if (e == q) rank = __popc(m & lt);
+      if (lane == 0) wcnt[warp][q] = __popc(m);
+    }
+    __syncthreads();
+    if (tid < E) {  // exclusive scan over warps for expert tid, continuing from earlier chunks
+      int s = run[tid];
+      for (int w = 0; w < 32; ++w) {
+        const int c = wcnt[w][tid];
+        wcnt[w][tid] = s;
+        s += c;
+      }
+      run[tid] = s;
+    }
+    __syncthreads();
+    if (e >= 0) {
+      const int p = off[e] + wcnt[warp][e] + rank;
+      const int t = a / k;
+      dst[a] = p;
+      row_tok[p] = t;
+      row_w[p] = wts[a];
+      row_inv[p] = inv_rms[t];
+    }
+    __syncthreads();
+  }
+}
+
+// one warp per grouped row
+__global__ void moe_gather_kernel(const __nv_bfloat16* __restrict__ h1, int D, const int* __restrict__ row_tok,
+                                  const int* __restrict__ grp_off_end, int cap, __nv_bfloat16* __restrict__ xg) {
+  const int rows = min(*grp_off_end, cap);
+  const int lane = threadIdx.x & 31;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < rows; p += (gridDim.x * blockDim.x) >> 5) {
+    const int t = row_tok[p];
+    uint4* out = reinterpret_cast<uint4*>(xg + (int64_t)p * D);
+    if (t >= 0) {
+      const uint4* in = reinterpret_cast<const uint4*>(h1 + (int64_t)t * D);
+      for (int i = lane; i < D / 8; i += 32) out[i] = in[i];
+    } else {
+      for (int i = lane; i < D / 8; i += 32) out[i] = make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
+// one warp per token; lane owns 4 consecutive columns of each 128-column unit
+__global__ void moe_combine_kernel(const float* __restrict__ y, const int* __restrict__ dst, int T, int k, int D,
+                                   const __nv_bfloat16* __restrict__ resid, __nv_bfloat16* __restrict__ out,
+                                   float* __restrict__ part, int64_t part_stride, float* __restrict__ outf) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (t >= T) return;
+  int src[MOE_MAX_TOPK];
+  for (int j = 0; j < k; ++j) src[j] = dst[(int64_t)t * k + j];
+  for (int c0 = 0; c0 < D; c0 += 128) {
+    const int c = c0 + lane * 4;
+    float4 s = *reinterpret_cast<const float4*>(y + (int64_t)src[0] * D + c);
+    for (int j = 1; j < k; ++j) {
+      const float4 v = *reinterpret_cast<const float4*>(y + (int64_t)src[j] * D + c);
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    if (outf != nullptr) {
+      *reinterpret_cast<float4*>(outf + (int64_t)t * D + c) = s;
+      continue;
+    }
+    float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
+    if (resid != nullptr) {
+      const uint2 r = *reinterpret_cast<const uint2*>(resid + (int64_t)t * D + c);
+      a = unpack_bf16x2(r.x);
+      b = unpack_bf16x2(r.y);
+    }
+    const float o0 = round_bf16(a.x + s.x), o1 = round_bf16(a.y + s.y);
+    const float o2 = round_bf16(b.x + s.z), o3 = round_bf16(b.y + s.w);
+    *reinterpret_cast<uint2*>(out + (int64_t)t * D + c) = make_uint2(pack_bf16x2(o0, o1), pack_bf16x2(o2, o3));
+    if (part != nullptr) {
+      float q = o0 * o0 + o1 * o1 + o2 * o2 + o3 * o3;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+      if (lane == 0) part[(int64_t)(c0 >> 7) * part_stride + t] = q;
+    }
+  }
+}
+
+__global__ void pack_router_kernel(const __nv_bfloat16* __restrict__ w, const __nv_bfloat16* __restrict__ g, int E,
+                                   int D, float* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)E * D) return;
+  dst[i] = __bfloat162float(w[i]) * __bfloat162float(g[i % D]);
+}
+
+}  // namespace
+
+cudaError_t launch_moe_route(const __nv_bfloat16* h1, int T, int D, const float* router, int E, int k, float eps,
+                             int* ids, float* wts, float* inv_rms, cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  if (E > MOE_MAX_EXPERTS || k > MOE_MAX_TOPK || D % 8 != 0) return cudaErrorInvalidValue;
+  constexpr int TPW = 4;
+  const int warps = (T + TPW - 1) / TPW;
+  const int blocks = (warps + 3) / 4;
+  if (E <= 8)
+    moe_route_kernel<8, TPW><<<blocks, 128, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms);
+  else
+    moe_route_kernel<16, TPW><<<blocks, 128, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_moe_group(const int* ids, const float* wts, const float* inv_rms, int T, int k, int E, int tile,
+                             int* grp_off, int* grp_end, int* dst, int* row_tok, float* row_w, float* row_inv,
+                             cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  if (E > MOE_MAX_EXPERTS) return cudaErrorInvalidValue;
+  moe_group_kernel<<<1, 1024, 0, st>>>(ids, wts, inv_rms, T, k, E, tile, grp_off, grp_end, dst, row_tok, row_w,
+                                       row_inv);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_moe_gather(const __nv_bfloat16* h1, int D, const int* row_tok, const int* grp_off_end, int cap,
+                              __nv_bfloat16* xg, cudaStream_t st) {
+  if (cap <= 0) return cudaSuccess;
+  const int blocks = std::min((cap + 7) / 8, 148 * 8);
+  moe_gather_kernel<<<blocks, 256, 0, st>>>(h1, D, row_tok, grp_off_end, cap, xg);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_moe_combine(const float* y, const int* dst, int T, int k, int D, const __nv_bfloat16* resid,
+                               __nv_bfloat16* out, float* part, int64_t part_stride, float* outf, cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  if (D % 128 != 0 || k > MOE_MAX_TOPK) return cudaErrorInvalidValue;
+  moe_combine_kernel<<<(T + 7) / 8, 256, 0, st>>>(y, dst, T, k, D, resid, out, part, part_stride, outf);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_router(const __nv_bfloat16* w_router, const __nv_bfloat16* gamma, int E, int D, float* dst,
+                               cudaStream_t st) {
+  const int64_t n = (int64_t)E * D;
+  pack_router_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w_router, gamma, E, D, dst);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace nf

@@ -37,7 +37,8 @@ class ModelCfg(C.Structure):
     _fields_ = [("d_model", C.c_int32), ("n_layers", C.c_int32), ("n_q_heads", C.c_int32),
                 ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("d_ffn", C.c_int32),
                 ("vocab", C.c_int32), ("rms_eps", C.c_float), ("rope_theta", C.c_float),
-                ("page_size", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32)]
+                ("page_size", C.c_int32), ("tp_size", C.c_int32), ("tp_rank", C.c_int32),
+                ("n_experts", C.c_int32), ("top_k", C.c_int32)]
 
 
 class _Batch(C.Structure):
@@ -61,11 +62,11 @@ class PlanOpts(C.Structure):
 
 class LayerWeights(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("attn_norm", "w_q", "w_k", "w_v", "w_o", "w_o_col", "w_o_row",
-                                          "ffn_norm", "w_gate", "w_up", "w_down")]
+                                          "ffn_norm", "w_gate", "w_up", "w_down", "w_router")]
 
 
 class PackedLayer(C.Structure):
-    _fields_ = [(n, C.c_void_p) for n in ("w_qkv", "w_o", "w_o_row", "w_gate_up", "w_down")]
+    _fields_ = [(n, C.c_void_p) for n in ("w_qkv", "w_o", "w_o_row", "w_gate_up", "w_down", "w_router")]
 
 
 class ModelWeights(C.Structure):
@@ -108,6 +109,11 @@ _sig("nf_gemm_workspace_bytes", C.c_size_t, C.c_int32, C.c_int32)
 _sig("nf_attention", C.c_int, C.POINTER(ModelCfg), C.POINTER(_Batch), C.c_void_p, C.c_void_p, C.c_void_p,
      C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.c_void_p)
 
+_sig("nf_moe_rows_cap", C.c_int64, C.POINTER(ModelCfg), C.c_int32)
+_sig("nf_moe_route_ws_bytes", C.c_size_t, C.POINTER(ModelCfg), C.c_int32)
+_sig("nf_moe_route", C.c_int, C.POINTER(ModelCfg), C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
 _sig("nf_kernel_launches", C.c_int64)
 _sig("nf_profile_enable", C.c_int, C.c_int32)
 _sig("nf_profile_read", C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64))
@@ -124,7 +130,8 @@ PROF_NAMES = ["kqv", "decode_attn", "prefill_attn", "o_proj", "up_gate", "down",
 EXPORTED = ["nf_plan_runtime_note", "nf_comm_create_local", "nf_gemm_workspace_bytes", "nf_profile_timeline", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
             "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_comm_unique_id",
             "nf_comm_create", "nf_comm_destroy", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
-            "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_gemm_bf16", "nf_attention"]
+            "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_gemm_bf16", "nf_attention",
+            "nf_moe_rows_cap", "nf_moe_route_ws_bytes", "nf_moe_route"]
 
 
 def _check(status: int):
@@ -137,9 +144,9 @@ def last_error() -> str:
 
 
 def model_cfg(d_model, n_layers, n_q_heads, n_kv_heads, head_dim, d_ffn, vocab, rms_eps=1e-5, rope_theta=1e4,
-              page_size=16, tp_size=1, tp_rank=0) -> ModelCfg:
+              page_size=16, tp_size=1, tp_rank=0, n_experts=0, top_k=2) -> ModelCfg:
     return ModelCfg(d_model, n_layers, n_q_heads, n_kv_heads, head_dim, d_ffn, vocab, rms_eps, rope_theta,
-                    page_size, tp_size, tp_rank)
+                    page_size, tp_size, tp_rank, n_experts, top_k)
 
 
 class Batch:
@@ -231,7 +238,7 @@ class Plan:
 
 
 def packed_layer_bytes(cfg: ModelCfg):
-    out = (C.c_size_t * 5)()
+    out = (C.c_size_t * 6)()
     _check(lib.nf_packed_layer_bytes(C.byref(cfg), out))
     return list(out)
 
@@ -290,6 +297,21 @@ def attention(cfg: ModelCfg, b: Batch, q: int, kv_pool: int, o: int, ws: int, ws
               sm_prefill: int, stream: int):
     _check(lib.nf_attention(C.byref(cfg), C.byref(b.c), C.c_void_p(q), C.c_void_p(kv_pool), C.c_void_p(o),
                             C.c_void_p(ws), ws_bytes, sm_decode, sm_prefill, C.c_void_p(stream)))
+
+
+def moe_rows_cap(cfg: ModelCfg, T: int) -> int:
+    return int(lib.nf_moe_rows_cap(C.byref(cfg), T))
+
+
+def moe_route_ws_bytes(cfg: ModelCfg, T: int) -> int:
+    return int(lib.nf_moe_route_ws_bytes(C.byref(cfg), T))
+
+
+def moe_route(cfg: ModelCfg, h1: int, router_packed: int, T: int, ids: int, wts: int, grp_off: int, dst: int,
+              row_tok: int, ws: int, ws_bytes: int, stream: int):
+    _check(lib.nf_moe_route(C.byref(cfg), C.c_void_p(h1), C.c_void_p(router_packed), T, C.c_void_p(ids),
+                            C.c_void_p(wts), C.c_void_p(grp_off), C.c_void_p(dst), C.c_void_p(row_tok),
+                            C.c_void_p(ws), ws_bytes, C.c_void_p(stream)))
 
 
 def kernel_launches() -> int:

@@ -16,7 +16,8 @@ def cfg_from_shape(shape, tp_size: int = 1, tp_rank: int = 0, n_layers: Optional
     """nf_model_cfg from any object with the synth.ModelShape attributes."""
     return nf.model_cfg(shape.d_model, shape.n_layers if n_layers is None else n_layers, shape.n_q_heads,
                         shape.n_kv_heads, shape.head_dim, shape.d_ffn, shape.vocab, shape.rms_eps,
-                        shape.rope_theta, shape.page_size, tp_size, tp_rank)
+                        shape.rope_theta, shape.page_size, tp_size, tp_rank, getattr(shape, "n_experts", 0),
+                        getattr(shape, "top_k", 2))
 
 
 def stream_handle(stream: Optional[torch.cuda.Stream] = None) -> int:
@@ -26,7 +27,7 @@ def stream_handle(stream: Optional[torch.cuda.Stream] = None) -> int:
 
 def alloc_packed_layer(cfg: nf.ModelCfg, device="cuda") -> Dict[str, torch.Tensor]:
     sizes = nf.packed_layer_bytes(cfg)
-    names = ["w_qkv", "w_o", "w_o_row", "w_gate_up", "w_down"]
+    names = ["w_qkv", "w_o", "w_o_row", "w_gate_up", "w_down", "w_router"]
     return {n: torch.empty(max(s, 2) // 2, dtype=BF16, device=device) for n, s in zip(names, sizes) if s > 0}
 
 
@@ -95,7 +96,7 @@ def shard_layer(w: Dict[str, torch.Tensor], n_q_heads: int, n_kv_heads: int, hea
     column W_q/W_k/W_v by heads, column O (rows of W_o) and row O (columns of
     W_o), column gate/up, row down.  Slicing only (views made contiguous)."""
     D = w["w_o"].shape[0]
-    F = w["w_gate"].shape[0]
+    F = w["w_gate"].shape[-2]
     qs, ks = n_q_heads // tp * head_dim, n_kv_heads // tp * head_dim
     ds, fs = D // tp, F // tp
     c = lambda t: t.contiguous()
@@ -106,9 +107,11 @@ def shard_layer(w: Dict[str, torch.Tensor], n_q_heads: int, n_kv_heads: int, hea
         "w_v": c(w["w_v"][rank * ks:(rank + 1) * ks]),
         "w_o_col": c(w["w_o"][rank * ds:(rank + 1) * ds, :]),
         "w_o_row": c(w["w_o"][:, rank * qs:(rank + 1) * qs]),
-        "w_gate": c(w["w_gate"][rank * fs:(rank + 1) * fs]),
-        "w_up": c(w["w_up"][rank * fs:(rank + 1) * fs]),
-        "w_down": c(w["w_down"][:, rank * fs:(rank + 1) * fs]),
+        # dense [F, D] / [D, F]; MoE [E, F, D] / [E, D, F]: every expert's F columns are split
+        "w_gate": c(w["w_gate"][..., rank * fs:(rank + 1) * fs, :]),
+        "w_up": c(w["w_up"][..., rank * fs:(rank + 1) * fs, :]),
+        "w_down": c(w["w_down"][..., rank * fs:(rank + 1) * fs]),
+        **({"w_router": w["w_router"]} if "w_router" in w else {}),
     }
 
 

@@ -34,7 +34,7 @@ def test_header_symbols_exported(nf):
     for n in names:
         assert hasattr(nf.lib, n), f"{n} declared in nf.h but not exported"
     assert set(names) == set(nf.EXPORTED)
-    assert nf.lib.nf_abi_version() == 1
+    assert nf.lib.nf_abi_version() == 2
 
 
 def _cfg(nf, shape, **kw):
@@ -110,3 +110,31 @@ def test_workspace_size_monotone(nf):
     small = nf.workspace_size(cfg, nf.Batch.from_any(synth.c1_batch()))
     big = nf.workspace_size(cfg, nf.Batch.from_any(synth.workload_batch(2048, 1024, 512)))
     assert 0 < small < big
+
+
+def test_moe_cfg_validation_and_sizes(nf):
+    """MoE fields of nf_model_cfg (A-20..A-23): validation, packed
+    sizes, grouped-row capacity (segments padded to 128 rows)."""
+    import ctypes
+    assert ctypes.sizeof(nf.ModelCfg) == 14 * 4
+    sh = synth.SHAPES["mixtral-8x7b"]
+    cfg = _cfg(nf, sh, tp_size=8)
+    D, F, E = sh.d_model, sh.d_ffn // 8, sh.n_experts
+    sizes = nf.packed_layer_bytes(cfg)
+    assert sizes[3] == E * ((F + 127) // 128) * 256 * D * 2
+    assert sizes[4] == E * D * F * 2 and sizes[5] == E * D * 4
+    assert nf.packed_layer_bytes(_cfg(nf, synth.SHAPES["llama3-8b"]))[5] == 0
+    for T in (1, 127, 2048):
+        cap = nf.moe_rows_cap(cfg, T)
+        assert cap % 128 == 0 and cap >= T * 2 + E * 127
+    b = nf.Batch.from_any(synth.c1_batch())
+    assert nf.workspace_size(cfg, b) > nf.workspace_size(_cfg(nf, synth.shape_with(sh, n_experts=0), tp_size=8), b)
+    with pytest.raises(nf.NFError) as e:
+        nf.workspace_size(_cfg(nf, synth.shape_with(sh, top_k=9)), b)
+    assert e.value.status == nf.NF_EINVAL
+    with pytest.raises(nf.NFError) as e:
+        nf.workspace_size(_cfg(nf, synth.shape_with(sh, n_experts=32)), b)
+    assert e.value.status == nf.NF_EUNSUPPORTED
+    with pytest.raises(nf.NFError) as e:
+        nf.moe_route(_cfg(nf, synth.SHAPES["llama3-8b"]), 1, 1, 4, 1, 1, 1, 1, 1, 1, 1 << 20, 0)
+    assert e.value.status == nf.NF_EINVAL

@@ -1,0 +1,218 @@
+"""GPU parity of the MoE FFN path (Mixtral-8x7B shape; readings
+A-20..A-23) through the C ABI against the float64 oracle (oracle/moe.py).
+
+* Gating + grouping (nf_moe_route): expert ids bit-exact wherever the oracle's
+  consecutive top-(k+1) logit gaps exceed GAP_ROUTE (both sides take the
+  decision from the same bf16 input; the GPU in fp32, the oracle in fp64);
+  the grouping of the GPU's own ids bit-exact against oracle.moe.group_rows.
+* Whole layers: rel L2 <= 1e-2 and max abs <= 5e-2 (north_star) on every row
+  whose routing is unambiguous.  The GPU router sees the GPU's bf16 h1, which
+  differs from the oracle's fp64 h1 by the layer's rounding (~3e-3 relative),
+  so rows whose oracle top-(k+1) gaps are below GAP_LAYER may legitimately
+  route differently; they are excluded (and counted) rather than compared."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import layer as OL
+from oracle import moe as OM
+
+from gpu_common import assert_close, compact_case, dev, dev_bits, device_weights, host, require_gpu, token_rows
+
+pytestmark = pytest.mark.gpu
+
+GAP_ROUTE = 1e-3
+GAP_LAYER = 0.05
+MIX = synth.SHAPES["mixtral-8x7b"]
+# one TP8 rank's shards of Mixtral-8x7B (the bench's --config moe proxy)
+MIX_RANK = synth.shape_with(MIX, name="mixtral-8x7b-tp8-rank", n_q_heads=4, n_kv_heads=1, d_ffn=14336 // 8)
+
+
+@pytest.fixture(scope="module")
+def env():
+    return require_gpu()
+
+
+def _unambiguous(logits, k, gap):
+    srt = -np.sort(-logits, axis=1)
+    return np.all(srt[:, :k] - srt[:, 1:k + 1] > gap, axis=1)
+
+
+def _pack_router_only(nf, rt, shape, w_router, ffn_norm):
+    """Packed layer whose only meaningful parts are the router and gamma_ffn."""
+    cfg = rt.cfg_from_shape(shape)
+    D, E, F, hd = shape.d_model, shape.n_experts, shape.d_ffn, shape.head_dim
+    z = lambda *s: torch.zeros(s, dtype=torch.bfloat16, device="cuda")
+    wd = {"attn_norm": z(D), "w_q": z(shape.n_q_heads * hd, D), "w_k": z(shape.n_kv_heads * hd, D),
+          "w_v": z(shape.n_kv_heads * hd, D), "w_o": z(D, shape.n_q_heads * hd), "ffn_norm": dev(ffn_norm),
+          "w_gate": z(E, F, D), "w_up": z(E, F, D), "w_down": z(E, D, F), "w_router": dev(w_router)}
+    return cfg, rt.pack_layer(cfg, wd)
+
+
+@pytest.mark.parametrize("shape_name,T", [("c1-moe", 300), ("c1-moe", 1), ("mixtral", 2048), ("mixtral-e16-k4", 777)])
+def test_moe_route_bit_exact(env, shape_name, T):
+    nf, rt = env
+    shape = {"c1-moe": synth.SHAPES["c1-moe"], "mixtral": MIX_RANK,
+             "mixtral-e16-k4": synth.shape_with(MIX_RANK, n_experts=16, top_k=4, d_ffn=256)}[shape_name]
+    D, E, k = shape.d_model, shape.n_experts, shape.top_k
+    w_router = synth.randn_bf16((E, D), 0, "L0.w_router", D ** -0.5)
+    ffn_norm = synth.randn_bf16((D,), 0, "L0.ffn_norm", 0.1, 1.0)
+    h1 = synth.activations(shape, T, seed=11, name="h1")
+    cfg, packed = _pack_router_only(nf, rt, shape, w_router, ffn_norm)
+    cap = nf.moe_rows_cap(cfg, T)
+    i32 = lambda n: torch.full((n,), -7, dtype=torch.int32, device="cuda")
+    ids, dst, grp, row_tok = i32(T * k), i32(T * k), i32(E + 1), i32(cap)
+    wts = torch.zeros(T * k, dtype=torch.float32, device="cuda")
+    ws = torch.empty(nf.moe_route_ws_bytes(cfg, T), dtype=torch.uint8, device="cuda")
+    nf.moe_route(cfg, dev(h1).data_ptr(), packed["w_router"].data_ptr(), T, ids.data_ptr(), wts.data_ptr(),
+                 grp.data_ptr(), dst.data_ptr(), row_tok.data_ptr(), ws.data_ptr(), ws.numel(), rt.stream_handle())
+    torch.cuda.synchronize()
+    ids_g = ids.cpu().numpy().reshape(T, k).astype(np.int64)
+    h2 = OL.rmsnorm(h1, ffn_norm, shape.rms_eps)
+    ids_r, wts_r, logits = OM.router_topk(h2, w_router, k)
+    sure = _unambiguous(logits, k, GAP_ROUTE)
+    assert sure.mean() > 0.95, sure.mean()
+    assert np.array_equal(ids_g[sure], ids_r[sure])
+    np.testing.assert_allclose(wts.cpu().numpy().reshape(T, k)[sure], wts_r[sure], rtol=0, atol=2e-5)
+    # every row: a valid selection (distinct experts in range)
+    assert ((ids_g >= 0) & (ids_g < E)).all() and all(len(set(r)) == k for r in ids_g.tolist())
+    # grouping of the GPU's own ids: bit-exact (A-23)
+    off, cnt, dst_r, row_tok_r = OM.group_rows(ids_g, E, 128)
+    assert np.array_equal(grp.cpu().numpy(), off)
+    assert np.array_equal(dst.cpu().numpy().reshape(T, k), dst_r)
+    rt_g = row_tok.cpu().numpy()
+    assert np.array_equal(rt_g[:off[-1]], row_tok_r)
+    assert (rt_g[off[-1]:] == -7).all()          # rows past the last segment untouched
+
+
+def _moe_layer_case(shape, b, seed=0):
+    w = synth.layer_weights(shape, 0, seed=seed)
+    x = synth.activations(shape, b.n_tokens, seed=1 + seed)
+    pool = synth.kv_pool(shape, b, seed=2 + seed)
+    return w, x, pool
+
+
+def _oracle_moe_layer(x, w, pool64, b, shape):
+    out, ids, wts, logits = OM.moe_decoder_layer(x, w, pool64, b, shape, return_route=True)
+    return out, _unambiguous(logits, shape.top_k, GAP_LAYER)
+
+
+def _gpu_moe_layer(env, shape, b, w, x, pool, mode, shares, pool_d=None):
+    nf, rt = env
+    cfg = rt.cfg_from_shape(shape)
+    nb = nf.Batch.from_any(b)
+    packed = rt.pack_layer(cfg, device_weights(w))
+    if pool_d is None:
+        pool_d = dev(pool)
+    plan = nf.Plan.explicit(cfg, mode=mode, shares=shares)
+    out = rt.layer_forward(plan, cfg, packed, pool_d, nb, dev(x))
+    torch.cuda.synchronize()
+    return host(out)
+
+
+@pytest.mark.parametrize("mode,shares", [(0, (1,)), (1, (1, 1)), (2, (1, 1)), (2, (1, 2, 1))])
+def test_moe_layer_c1_vs_oracle(env, mode, shares):
+    shape = synth.SHAPES["c1-moe"]
+    b = synth.c1_batch()
+    w, x, pool = _moe_layer_case(shape, b)
+    ref, sure = _oracle_moe_layer(x, w, OL.as_pool(pool), b, shape)
+    assert sure.mean() > 0.7, sure.mean()
+    out = _gpu_moe_layer(env, shape, b, w, x, pool, mode, shares)
+    assert np.isfinite(out).all()
+    assert_close(out[sure], ref[sure], what=f"MoE C1 layer mode={mode} shares={shares} ({(~sure).sum()} rows excluded)")
+
+
+def test_moe_layer_ragged_batch_split_invariance(env):
+    """Ragged batch (prefill chunks, page-boundary decodes, an expert likely
+    left empty in a small nano-batch): every plan gives the same rows within
+    tolerance, and the same row partition gives bit-identical outputs."""
+    shape = synth.shape_with(synth.SHAPES["c1-moe"], n_experts=16, top_k=4, d_ffn=320)
+    b = synth.make_batch([1] * 9 + [33, 1, 1, 130], [15, 16, 31, 32, 0, 7, 300, 50, 1, 0, 47, 63, 100], seed=4,
+                         pool_slack=3)
+    w, x, pool = _moe_layer_case(shape, b, seed=3)
+    ref, sure = _oracle_moe_layer(x, w, OL.as_pool(pool), b, shape)
+    outs = {}
+    for mode, shares in [(0, (1,)), (1, (1, 1)), (2, (1, 1)), (2, (3, 1, 1, 2))]:
+        out = _gpu_moe_layer(env, shape, b, w, x, pool, mode, shares)
+        assert_close(out[sure], ref[sure], what=f"mode={mode} shares={shares}")
+        outs[(mode, shares)] = out
+    assert np.array_equal(outs[(1, (1, 1))], outs[(2, (1, 1))])
+
+
+def test_moe_layer_mixtral_rank_full_batch_sampled(env):
+    """configs[3] at full size on one GPU: one Mixtral-8x7B TP8 rank's shards
+    (4/1 heads, 8 experts x F 1792) over the B_dense=2048 steady-state batch
+    (p=512, d=1024), in the bench's OVERLAP launch configuration; sampled
+    requests (decode and both prefill requests) checked against the oracle."""
+    nf, rt = env
+    shape = MIX_RANK
+    b = synth.workload_batch(2048, 512, 1024)
+    w = synth.layer_weights(shape, 0, seed=0)
+    x = synth.activations(shape, b.n_tokens, seed=1)
+    pool_d = dev_bits(synth.kv_pool_bits(shape, b, seed=2))
+    out = _gpu_moe_layer(env, shape, b, w, x, None, nf.OVERLAP, (1, 1), pool_d=pool_d)
+    assert np.isfinite(out).all()
+    reqs = [0, 1, 2, 100, 700, 1364, 1365, 1366, 1367]
+    sub, pool = compact_case(shape, b, reqs)
+    rows = token_rows(b, reqs)
+    ref, sure = _oracle_moe_layer(x[rows], w, pool, sub, shape)
+    assert sure.mean() > 0.7
+    assert_close(out[rows][sure], ref[sure], what="Mixtral rank full batch sampled")
+
+
+def _run_tp_moe_layer(nf, rt, shape, b, w, x, pool, tp, mode, shares):
+    comms = nf.comm_create_local(tp)
+    outs = [None] * tp
+    errs = []
+    wd = device_weights(w)
+    pool_d = dev(pool)
+    x_d = dev(x)
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                cfg = rt.cfg_from_shape(shape, tp_size=tp, tp_rank=r)
+                shard = rt.shard_layer(wd, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, tp, r)
+                packed = rt.pack_layer(cfg, shard, stream=int(st.cuda_stream))
+                p_r = rt.shard_pool(pool_d, tp, r)
+                nb = nf.Batch.from_any(b)
+                plan = nf.Plan.explicit(cfg, mode=mode, shares=shares, sm=[148] * 7)
+                ws = rt.workspace(cfg, nb)
+                y = torch.empty_like(x_d)
+                nf.layer_forward(plan, rt.ptrs(packed), p_r.data_ptr(), nb, x_d.data_ptr(), y.data_ptr(),
+                                 ws.data_ptr(), ws.numel(), int(st.cuda_stream), comm=comms[r])
+                st.synchronize()
+                outs[r] = y
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(tp)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for c in comms:
+        nf.comm_destroy(c)
+    assert not errs, errs
+    return outs
+
+
+@pytest.mark.parametrize("tp,mode,shares", [(2, 0, (1,)), (4, 2, (1, 1)), (8, 2, (2, 1, 1))])
+def test_tp_moe_layer_matches_unsharded_oracle(env, tp, mode, shares):
+    """TP-sharded MoE FFN (every expert's F columns split, per-rank weighted
+    partials AllReduced; emulated communicator on one GPU): every rank holds
+    bit-identical outputs, equal to the unsharded oracle within tolerance."""
+    nf, rt = env
+    shape = synth.shape_with(synth.SHAPES["c1-moe"], n_q_heads=8, n_kv_heads=8, d_ffn=2048)
+    b = synth.make_batch([1] * 40 + [57, 1, 23], list(range(5, 205, 5)) + [0, 64, 16], seed=6, pool_slack=2)
+    w, x, pool = _moe_layer_case(shape, b, seed=2)
+    ref, sure = _oracle_moe_layer(x, w, OL.as_pool(pool), b, shape)
+    outs = _run_tp_moe_layer(nf, rt, shape, b, w, x, pool, tp, mode, shares)
+    for r in range(1, tp):
+        assert torch.equal(outs[0], outs[r])
+    assert_close(host(outs[0])[sure], ref[sure], what=f"MoE TP{tp}")
