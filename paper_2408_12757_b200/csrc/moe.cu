@@ -170,56 +170,78 @@ __global__ void __launch_bounds__(1024) moe_group_kernel(const int* __restrict__
   }
 }
 
-// one warp per grouped row
+// one warp per grouped row; each lane keeps 4 x 16 B loads in flight
 __global__ void moe_gather_kernel(const __nv_bfloat16* __restrict__ h1, int D, const int* __restrict__ row_tok,
                                   const int* __restrict__ grp_off_end, int cap, __nv_bfloat16* __restrict__ xg) {
   const int rows = min(*grp_off_end, cap);
   const int lane = threadIdx.x & 31;
+  const int n16 = D / 8;  // 16-byte chunks per row
   for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < rows; p += (gridDim.x * blockDim.x) >> 5) {
     const int t = row_tok[p];
     uint4* out = reinterpret_cast<uint4*>(xg + (int64_t)p * D);
-    if (t >= 0) {
-      const uint4* in = reinterpret_cast<const uint4*>(h1 + (int64_t)t * D);
-      for (int i = lane; i < D / 8; i += 32) out[i] = in[i];
-    } else {
-      for (int i = lane; i < D / 8; i += 32) out[i] = make_uint4(0, 0, 0, 0);
+    const uint4* in = reinterpret_cast<const uint4*>(h1 + (int64_t)max(t, 0) * D);
+    for (int i0 = lane; i0 < n16; i0 += 128) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * 32;
+        v[u] = (t >= 0 && i < n16) ? in[i] : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u * 32 < n16) out[i0 + u * 32] = v[u];
     }
   }
 }
 
-// one warp per token; lane owns 4 consecutive columns of each 128-column unit
+// One warp per token; lane owns 4 consecutive columns of each 128-column unit.
+// CH units per batch so that 2*CH + CH loads per lane are in flight at once.
+template <int KMAX>
 __global__ void moe_combine_kernel(const float* __restrict__ y, const int* __restrict__ dst, int T, int k, int D,
                                    const __nv_bfloat16* __restrict__ resid, __nv_bfloat16* __restrict__ out,
                                    float* __restrict__ part, int64_t part_stride, float* __restrict__ outf) {
+  constexpr int CH = 8;
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t >= T) return;
-  int src[MOE_MAX_TOPK];
-  for (int j = 0; j < k; ++j) src[j] = dst[(int64_t)t * k + j];
-  for (int c0 = 0; c0 < D; c0 += 128) {
-    const int c = c0 + lane * 4;
-    float4 s = *reinterpret_cast<const float4*>(y + (int64_t)src[0] * D + c);
-    for (int j = 1; j < k; ++j) {
-      const float4 v = *reinterpret_cast<const float4*>(y + (int64_t)src[j] * D + c);
-      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-    }
-    if (outf != nullptr) {
-      *reinterpret_cast<float4*>(outf + (int64_t)t * D + c) = s;
-      continue;
-    }
-    float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
-    if (resid != nullptr) {
-      const uint2 r = *reinterpret_cast<const uint2*>(resid + (int64_t)t * D + c);
-      a = unpack_bf16x2(r.x);
-      b = unpack_bf16x2(r.y);
-    }
-    const float o0 = round_bf16(a.x + s.x), o1 = round_bf16(a.y + s.y);
-    const float o2 = round_bf16(b.x + s.z), o3 = round_bf16(b.y + s.w);
-    *reinterpret_cast<uint2*>(out + (int64_t)t * D + c) = make_uint2(pack_bf16x2(o0, o1), pack_bf16x2(o2, o3));
-    if (part != nullptr) {
-      float q = o0 * o0 + o1 * o1 + o2 * o2 + o3 * o3;
+  const float* src[KMAX];
 #pragma unroll
-      for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-      if (lane == 0) part[(int64_t)(c0 >> 7) * part_stride + t] = q;
+  for (int j = 0; j < KMAX; ++j) src[j] = j < k ? y + (int64_t)dst[(int64_t)t * k + j] * D : nullptr;
+  for (int cb = 0; cb < D; cb += 128 * CH) {
+    float4 s[CH];
+    uint2 r[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int c = cb + u * 128 + lane * 4;
+      s[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      r[u] = make_uint2(0, 0);
+      if (c < D) {
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+          if (j < k) {
+            const float4 v = *reinterpret_cast<const float4*>(src[j] + c);
+            s[u].x += v.x; s[u].y += v.y; s[u].z += v.z; s[u].w += v.w;
+          }
+        if (outf == nullptr && resid != nullptr) r[u] = *reinterpret_cast<const uint2*>(resid + (int64_t)t * D + c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int c0 = cb + u * 128, c = c0 + lane * 4;
+      if (c0 >= D) break;
+      if (outf != nullptr) {
+        *reinterpret_cast<float4*>(outf + (int64_t)t * D + c) = s[u];
+        continue;
+      }
+      const float2 a = unpack_bf16x2(r[u].x), b = unpack_bf16x2(r[u].y);
+      const float o0 = round_bf16(a.x + s[u].x), o1 = round_bf16(a.y + s[u].y);
+      const float o2 = round_bf16(b.x + s[u].z), o3 = round_bf16(b.y + s[u].w);
+      *reinterpret_cast<uint2*>(out + (int64_t)t * D + c) = make_uint2(pack_bf16x2(o0, o1), pack_bf16x2(o2, o3));
+      if (part != nullptr) {
+        float q = o0 * o0 + o1 * o1 + o2 * o2 + o3 * o3;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        if (lane == 0) part[(int64_t)(c0 >> 7) * part_stride + t] = q;
+      }
     }
   }
 }
@@ -272,7 +294,10 @@ cudaError_t launch_moe_combine(const float* y, const int* dst, int T, int k, int
                                __nv_bfloat16* out, float* part, int64_t part_stride, float* outf, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
   if (D % 128 != 0 || k > MOE_MAX_TOPK) return cudaErrorInvalidValue;
-  moe_combine_kernel<<<(T + 7) / 8, 256, 0, st>>>(y, dst, T, k, D, resid, out, part, part_stride, outf);
+  if (k <= 2)
+    moe_combine_kernel<2><<<(T + 7) / 8, 256, 0, st>>>(y, dst, T, k, D, resid, out, part, part_stride, outf);
+  else
+    moe_combine_kernel<MOE_MAX_TOPK><<<(T + 7) / 8, 256, 0, st>>>(y, dst, T, k, D, resid, out, part, part_stride, outf);
   count_launch();
   return cudaGetLastError();
 }

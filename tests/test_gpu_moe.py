@@ -155,7 +155,7 @@ def test_moe_layer_mixtral_rank_full_batch_sampled(env):
     pool_d = dev_bits(synth.kv_pool_bits(shape, b, seed=2))
     out = _gpu_moe_layer(env, shape, b, w, x, None, nf.OVERLAP, (1, 1), pool_d=pool_d)
     assert np.isfinite(out).all()
-    reqs = [0, 1, 2, 100, 700, 1364, 1365, 1366, 1367]
+    reqs = [0, 1, 2, 100, 700, 1364, 1365, 1366]
     sub, pool = compact_case(shape, b, reqs)
     rows = token_rows(b, reqs)
     ref, sure = _oracle_moe_layer(x[rows], w, pool, sub, shape)

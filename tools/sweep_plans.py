@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Time nf_model_step for many explicit plans in one process (weights and KV
-allocated once).  Usage: sweep_plans.py [--config c2|c3rank] [--steps N]
+allocated once).  Usage: sweep_plans.py [--config c2|c3rank|c4rank] [--steps N]
 Prints ms/step per plan, best first."""
 import argparse
 import itertools
@@ -28,6 +28,9 @@ def main():
     if args.config == "c3rank":
         shape = synth.shape_with(synth.SHAPES["llama2-70b"], n_q_heads=8, n_kv_heads=1, d_ffn=3584)
         p_in, d_out = 512, 1024
+    elif args.config == "c4rank":
+        shape = synth.shape_with(synth.SHAPES["mixtral-8x7b"], n_q_heads=4, n_kv_heads=1, d_ffn=1792)
+        p_in, d_out = 512, 1024
     else:
         shape = synth.SHAPES["llama3-8b"]
         p_in, d_out = 1024, 512
@@ -51,6 +54,10 @@ def main():
              "w_k": randn((Hk * hd, D), D ** -0.5), "w_v": randn((Hk * hd, D), D ** -0.5),
              "w_o": randn((D, Hq * hd), (Hq * hd) ** -0.5), "ffn_norm": randn((D,), 0.1, 1.0),
              "w_gate": randn((F, D), D ** -0.5), "w_up": randn((F, D), D ** -0.5), "w_down": randn((D, F), F ** -0.5)}
+        if shape.n_experts:
+            E = shape.n_experts
+            w.update(w_router=randn((E, D), D ** -0.5), w_gate=randn((E, F, D), D ** -0.5),
+                     w_up=randn((E, F, D), D ** -0.5), w_down=randn((E, D, F), F ** -0.5))
         layers.append(rt.pack_layer(cfg, w))
     model = rt.Model(cfg, randn((shape.vocab, D)), layers,
                      rt.pack_lm_head(cfg, randn((shape.vocab, D), D ** -0.5), randn((D,), 0.1, 1.0)))
