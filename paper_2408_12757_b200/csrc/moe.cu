@@ -17,26 +17,30 @@ namespace nf {
 
 namespace {
 
-// TPW tokens per warp share each router read (the router stays L2-resident).
-template <int EMAX, int TPW>
-__global__ void __launch_bounds__(128) moe_route_kernel(const __nv_bfloat16* __restrict__ h1, int T, int D,
+// One CTA of 8 warps per TOK tokens: warp w accumulates the RMS sum of squares and
+// the E router dot products of all TOK tokens over its D/8 slice (each router
+// element read once per CTA, reused TOK times), the CTA reduces over warps in
+// smem, and thread t < TOK runs the top-k of token t.
+template <int EMAX, int TOK>
+__global__ void __launch_bounds__(256) moe_route_kernel(const __nv_bfloat16* __restrict__ h1, int T, int D,
                                                         const float* __restrict__ router, int E, int k, float eps,
                                                         int* __restrict__ ids, float* __restrict__ wts,
                                                         float* __restrict__ inv_rms) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int t0 = warp * TPW;
-  if (t0 >= T) return;
-  float acc[TPW][EMAX], sq[TPW];
+  __shared__ float red[8][TOK][EMAX + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = blockIdx.x * TOK;
+  const int d0 = warp * (D / 8), d1 = d0 + D / 8;
+  float acc[TOK][EMAX], sq[TOK];
 #pragma unroll
-  for (int j = 0; j < TPW; ++j) {
+  for (int j = 0; j < TOK; ++j) {
     sq[j] = 0.f;
 #pragma unroll
     for (int e = 0; e < EMAX; ++e) acc[j][e] = 0.f;
   }
-  for (int i = lane * 8; i < D; i += 256) {
-    float x[TPW][8];
+  for (int i = d0 + lane * 8; i < d1; i += 256) {
+    float x[TOK][8];
 #pragma unroll
-    for (int j = 0; j < TPW; ++j) {
+    for (int j = 0; j < TOK; ++j) {
       uint4 u = make_uint4(0, 0, 0, 0);
       if (t0 + j < T) u = *reinterpret_cast<const uint4*>(h1 + (int64_t)(t0 + j) * D + i);
       const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
@@ -55,7 +59,7 @@ __global__ void __launch_bounds__(128) moe_route_kernel(const __nv_bfloat16* __r
         const float4 a = *reinterpret_cast<const float4*>(router + (int64_t)e * D + i);
         const float4 b = *reinterpret_cast<const float4*>(router + (int64_t)e * D + i + 4);
 #pragma unroll
-        for (int j = 0; j < TPW; ++j) {
+        for (int j = 0; j < TOK; ++j) {
           float s = acc[j][e];
           s = fmaf(x[j][0], a.x, s); s = fmaf(x[j][1], a.y, s); s = fmaf(x[j][2], a.z, s); s = fmaf(x[j][3], a.w, s);
           s = fmaf(x[j][4], b.x, s); s = fmaf(x[j][5], b.y, s); s = fmaf(x[j][6], b.z, s); s = fmaf(x[j][7], b.w, s);
@@ -65,7 +69,7 @@ __global__ void __launch_bounds__(128) moe_route_kernel(const __nv_bfloat16* __r
     }
   }
 #pragma unroll
-  for (int j = 0; j < TPW; ++j) {
+  for (int j = 0; j < TOK; ++j) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) sq[j] += __shfl_xor_sync(0xffffffffu, sq[j], o);
 #pragma unroll
@@ -73,36 +77,50 @@ __global__ void __launch_bounds__(128) moe_route_kernel(const __nv_bfloat16* __r
 #pragma unroll
       for (int o = 16; o; o >>= 1) acc[j][e] += __shfl_xor_sync(0xffffffffu, acc[j][e], o);
   }
+  if (lane == 0) {
 #pragma unroll
-  for (int j = 0; j < TPW; ++j) {
-    const int t = t0 + j;
-    if (lane != j || t >= T) continue;
-    const float inv = rsqrtf(sq[j] / (float)D + eps);
-    float l[EMAX];
+    for (int j = 0; j < TOK; ++j) {
+      red[warp][j][EMAX] = sq[j];
 #pragma unroll
-    for (int e = 0; e < EMAX; ++e) l[e] = acc[j][e] * inv;
-    // top-k: largest logit, lowest index on ties (strict > over ascending e)
-    int sel[MOE_MAX_TOPK];
-    float sl[MOE_MAX_TOPK];
-    uint32_t used = 0;
-    for (int q = 0; q < k; ++q) {
-      int bi = -1;
-      float bv = -INFINITY;
-#pragma unroll
-      for (int e = 0; e < EMAX; ++e)
-        if (e < E && !((used >> e) & 1u) && (bi < 0 || l[e] > bv)) { bv = l[e]; bi = e; }
-      used |= 1u << bi;
-      sel[q] = bi;
-      sl[q] = bv;
+      for (int e = 0; e < EMAX; ++e) red[warp][j][e] = acc[j][e];
     }
-    float p[MOE_MAX_TOPK], z = 0.f;
-    for (int q = 0; q < k; ++q) { p[q] = expf(sl[q] - sl[0]); z += p[q]; }
-    for (int q = 0; q < k; ++q) {
-      ids[(int64_t)t * k + q] = sel[q];
-      wts[(int64_t)t * k + q] = p[q] / z;
-    }
-    inv_rms[t] = inv;
   }
+  __syncthreads();
+  const int j = threadIdx.x, t = t0 + j;
+  if (j >= TOK || t >= T) return;
+  // fixed summation order over the 8 D-slices (deterministic)
+  float ssq = 0.f, l[EMAX];
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) l[e] = 0.f;
+  for (int w = 0; w < 8; ++w) {
+    ssq += red[w][j][EMAX];
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e) l[e] += red[w][j][e];
+  }
+  const float inv = rsqrtf(ssq / (float)D + eps);
+#pragma unroll
+  for (int e = 0; e < EMAX; ++e) l[e] *= inv;
+  // top-k: largest logit, lowest index on ties (strict > over ascending e)
+  int sel[MOE_MAX_TOPK];
+  float sl[MOE_MAX_TOPK];
+  uint32_t used = 0;
+  for (int q = 0; q < k; ++q) {
+    int bi = -1;
+    float bv = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < EMAX; ++e)
+      if (e < E && !((used >> e) & 1u) && (bi < 0 || l[e] > bv)) { bv = l[e]; bi = e; }
+    used |= 1u << bi;
+    sel[q] = bi;
+    sl[q] = bv;
+  }
+  float p[MOE_MAX_TOPK], z = 0.f;
+  for (int q = 0; q < k; ++q) { p[q] = expf(sl[q] - sl[0]); z += p[q]; }
+  for (int q = 0; q < k; ++q) {
+    ids[(int64_t)t * k + q] = sel[q];
+    wts[(int64_t)t * k + q] = p[q] / z;
+  }
+  inv_rms[t] = inv;
 }
 
 // One CTA of 1024 threads.  Pass 1 counts assignments per expert; thread 0 lays out
@@ -194,27 +212,31 @@ __global__ void moe_gather_kernel(const __nv_bfloat16* __restrict__ h1, int D, c
   }
 }
 
-// One warp per token; lane owns 4 consecutive columns of each 128-column unit.
-// CH units per batch so that 2*CH + CH loads per lane are in flight at once.
+// 4 warps per token: warp w owns the 128-column units u = w, w+4, ... (lane: 4
+// consecutive columns of a unit), up to CH units in flight per batch.
 template <int KMAX>
-__global__ void moe_combine_kernel(const float* __restrict__ y, const int* __restrict__ dst, int T, int k, int D,
-                                   const __nv_bfloat16* __restrict__ resid, __nv_bfloat16* __restrict__ out,
-                                   float* __restrict__ part, int64_t part_stride, float* __restrict__ outf) {
-  constexpr int CH = 8;
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(256) moe_combine_kernel(const float* __restrict__ y, const int* __restrict__ dst,
+                                                          int T, int k, int D,
+                                                          const __nv_bfloat16* __restrict__ resid,
+                                                          __nv_bfloat16* __restrict__ out, float* __restrict__ part,
+                                                          int64_t part_stride, float* __restrict__ outf) {
+  constexpr int CH = 8, WPT = 4;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int t = gw / WPT, w = gw % WPT;
   if (t >= T) return;
+  const int n_units = D / 128;
   const float* src[KMAX];
 #pragma unroll
   for (int j = 0; j < KMAX; ++j) src[j] = j < k ? y + (int64_t)dst[(int64_t)t * k + j] * D : nullptr;
-  for (int cb = 0; cb < D; cb += 128 * CH) {
+  for (int ub = w; ub < n_units; ub += WPT * CH) {
     float4 s[CH];
     uint2 r[CH];
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
-      const int c = cb + u * 128 + lane * 4;
+      const int unit = ub + u * WPT, c = unit * 128 + lane * 4;
       s[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       r[u] = make_uint2(0, 0);
-      if (c < D) {
+      if (unit < n_units) {
 #pragma unroll
         for (int j = 0; j < KMAX; ++j)
           if (j < k) {
@@ -226,8 +248,8 @@ __global__ void moe_combine_kernel(const float* __restrict__ y, const int* __res
     }
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
-      const int c0 = cb + u * 128, c = c0 + lane * 4;
-      if (c0 >= D) break;
+      const int unit = ub + u * WPT, c = unit * 128 + lane * 4;
+      if (unit >= n_units) break;
       if (outf != nullptr) {
         *reinterpret_cast<float4*>(outf + (int64_t)t * D + c) = s[u];
         continue;
@@ -240,7 +262,7 @@ __global__ void moe_combine_kernel(const float* __restrict__ y, const int* __res
         float q = o0 * o0 + o1 * o1 + o2 * o2 + o3 * o3;
 #pragma unroll
         for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-        if (lane == 0) part[(int64_t)(c0 >> 7) * part_stride + t] = q;
+        if (lane == 0) part[(int64_t)unit * part_stride + t] = q;
       }
     }
   }
@@ -259,13 +281,13 @@ cudaError_t launch_moe_route(const __nv_bfloat16* h1, int T, int D, const float*
                              int* ids, float* wts, float* inv_rms, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
   if (E > MOE_MAX_EXPERTS || k > MOE_MAX_TOPK || D % 8 != 0) return cudaErrorInvalidValue;
-  constexpr int TPW = 4;
-  const int warps = (T + TPW - 1) / TPW;
-  const int blocks = (warps + 3) / 4;
+  if (D % 64 != 0) return cudaErrorInvalidValue;  // 8 warps x 8-element lanes
+  constexpr int TOK = 8;
+  const int blocks = (T + TOK - 1) / TOK;
   if (E <= 8)
-    moe_route_kernel<8, TPW><<<blocks, 128, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms);
+    moe_route_kernel<8, TOK><<<blocks, 256, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms);
   else
-    moe_route_kernel<16, TPW><<<blocks, 128, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms);
+    moe_route_kernel<16, TOK><<<blocks, 256, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms);
   count_launch();
   return cudaGetLastError();
 }
@@ -294,10 +316,11 @@ cudaError_t launch_moe_combine(const float* y, const int* dst, int T, int k, int
                                __nv_bfloat16* out, float* part, int64_t part_stride, float* outf, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
   if (D % 128 != 0 || k > MOE_MAX_TOPK) return cudaErrorInvalidValue;
+  const int blocks = (T + 1) / 2;  // 2 tokens x 4 warps per CTA
   if (k <= 2)
-    moe_combine_kernel<2><<<(T + 7) / 8, 256, 0, st>>>(y, dst, T, k, D, resid, out, part, part_stride, outf);
+    moe_combine_kernel<2><<<blocks, 256, 0, st>>>(y, dst, T, k, D, resid, out, part, part_stride, outf);
   else
-    moe_combine_kernel<MOE_MAX_TOPK><<<(T + 7) / 8, 256, 0, st>>>(y, dst, T, k, D, resid, out, part, part_stride, outf);
+    moe_combine_kernel<MOE_MAX_TOPK><<<blocks, 256, 0, st>>>(y, dst, T, k, D, resid, out, part, part_stride, outf);
   count_launch();
   return cudaGetLastError();
 }
