@@ -330,7 +330,8 @@ def run_nf(args, rank, world, local_rank):
                                     colocate=True)
         else:
             # defaults = best of tools/sweep_plans.py on B200 (profiles/r1_sweep_*.log)
-            dense, dec, dshares = (132, 16, "1,1") if args.config != "c2" else (116, 32, "1,1")
+            dense, dec, dshares = {"c2": (116, 32, "1,1"), "c4rank": (132, 16, "3,5"), "c4": (132, 16, "3,5")}.get(
+                args.config, (132, 16, "1,1"))
             shares = tuple(int(x) for x in (args.shares or dshares).split(","))
             plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm or [dense, dec, dense, dense, dense, dense, 8],
                                     balance=args.balance)

@@ -248,6 +248,55 @@ nf_status nf_moe_route(const nf_model_cfg* cfg, const void* h1, const void* rout
                        float* wts, int32_t* grp_off, int32_t* dst, int32_t* row_tok, void* ws, size_t ws_bytes,
                        void* stream);
 
+/* ------------------------------------------------------------------ serving loop (NEXT-4) */
+/* Global batch scheduler + KV-cache manager (host, C++): continuous batching with
+ * chunked prefill, discrete dense batch sizes,
+ * peak-memory admission and eviction, asynchronous EOS
+ * detection one step late; readings A-25..A-29 in DESIGN.md,
+ * bit-exact contract with oracle/serving.py.  Protocol per step i:
+ *   nf_sched_next -> (upload tok_src, nf_assemble_tokens, nf_model_step of step i)
+ *   -> nf_sched_complete(i - 1, next_ids of step i - 1) -> nf_sched_next ...
+ * i.e. step i+1 is formed before step i's tokens are read; a decode whose input
+ * token was produced by the previous step gets tok_src = -(1 + row) (row of that
+ * step's next_ids), every other token id is known on the host. */
+typedef struct {
+  int32_t n_pages;       /* pages of the KV pool (per layer) */
+  int32_t page_size;     /* 16 */
+  int32_t n_bdense;      /* allowed dense batch sizes (tokens), any order, 1..16 of them */
+  const int32_t* bdense;
+  int32_t avg_decode;    /* average decode length for the peak-memory estimate */
+  int32_t eos_id;        /* token id ending a request, or -1 */
+} nf_sched_cfg;
+typedef struct nf_sched nf_sched;
+/* One formed step; arrays are owned by the scheduler and valid until the next
+ * nf_sched_next.  n_req == 0: nothing runnable (idle or blocked). */
+typedef struct {
+  int64_t step;
+  int32_t n_req, n_tokens;
+  const int64_t* req_ids;                 /* [n_req] */
+  const int32_t *q_len, *kv_prefix, *emit; /* [n_req] (nf_batch fields) */
+  const int32_t *page_indptr, *page_ids;  /* [n_req+1], [page_indptr[n_req]] */
+  const int32_t* tok_src;                 /* [n_tokens]: >= 0 token id; < 0: next_ids[-(1+v)] of step - 1 */
+} nf_sched_step;
+typedef struct {
+  int64_t steps, tokens, prefill_tokens, decode_tokens, finished, generated, useless, evictions;
+  int32_t peak_pages_used, running, queued;
+} nf_sched_stats;
+nf_status nf_sched_create(const nf_sched_cfg* cfg, nf_sched** out);
+/* Queue a request (first come, first served).  prompt: host [prompt_len] token ids
+ * (copied); out_len: the position of its EOS (synthetic traces).  NF_EINVAL on a
+ * duplicate id or empty prompt / out_len < 1. */
+nf_status nf_sched_submit(nf_sched* s, int64_t req_id, const int32_t* prompt, int32_t prompt_len, int32_t out_len);
+nf_status nf_sched_next(nf_sched* s, nf_sched_step* out);
+/* next_ids: host [n_req of that step] (the step's nf_model_step output).  NF_EINVAL
+ * if the step is not pending. */
+nf_status nf_sched_complete(nf_sched* s, int64_t step, const int32_t* next_ids);
+nf_status nf_sched_get_stats(const nf_sched* s, nf_sched_stats* out);
+void nf_sched_destroy(nf_sched* s);
+/* token_ids[t] = tok_src[t] >= 0 ? tok_src[t] : prev_next_ids[-(1 + tok_src[t])]  (device arrays, one launch). */
+nf_status nf_assemble_tokens(const int32_t* tok_src, const int32_t* prev_next_ids, int32_t* token_ids, int32_t T,
+                             void* stream);
+
 /* ------------------------------------------------------------------ instrumentation */
 /* Cumulative number of CUDA kernels this process launched through libnf. */
 int64_t nf_kernel_launches(void);

@@ -1352,6 +1352,13 @@ nf_status nf_moe_route(const nf_model_cfg* c, const void* h1, const void* router
   return NF_OK;
 }
 
+nf_status nf_assemble_tokens(const int32_t* tok_src, const int32_t* prev_next_ids, int32_t* token_ids, int32_t T,
+                             void* stream) {
+  if (T < 0 || (T > 0 && (!tok_src || !token_ids))) return set_error(NF_EINVAL, "bad arguments");
+  NF_CUDA(launch_assemble_tokens(tok_src, prev_next_ids, token_ids, T, (cudaStream_t)stream));
+  return NF_OK;
+}
+
 // ------------------------------------------------------------------ op-level entry points
 nf_status nf_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t M,
                        int32_t N, int32_t K, int32_t sm_budget, void* ws, size_t ws_bytes, void* stream) {

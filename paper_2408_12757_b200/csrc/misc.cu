@@ -215,6 +215,26 @@ cudaError_t launch_sum_bf16(const void* const* in, int n, __nv_bfloat16* out, si
 cudaError_t launch_fill_i32(int* p, int n, int v, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   fill_i32_kernel<<<(n + 255) / 256, 256, 0, st>>>(p, n, v);
+  count_launch();
+  return cudaGetLastError();
+}
+
+namespace {
+// serving loop: a decode's input token may still live only in the
+// previous step's next_ids on the device
+__global__ void assemble_tokens_kernel(const int* __restrict__ src, const int* __restrict__ prev, int* __restrict__ out,
+                                       int T) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int v = src[t];
+  out[t] = v >= 0 ? v : prev[-(1 + v)];
+}
+}  // namespace
+
+cudaError_t launch_assemble_tokens(const int* src, const int* prev, int* out, int T, cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  assemble_tokens_kernel<<<(T + 255) / 256, 256, 0, st>>>(src, prev, out, T);
+  count_launch();
   return cudaGetLastError();
 }
 

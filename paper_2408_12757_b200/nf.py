@@ -114,6 +114,31 @@ _sig("nf_moe_route_ws_bytes", C.c_size_t, C.POINTER(ModelCfg), C.c_int32)
 _sig("nf_moe_route", C.c_int, C.POINTER(ModelCfg), C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
+class SchedCfg(C.Structure):
+    _fields_ = [("n_pages", C.c_int32), ("page_size", C.c_int32), ("n_bdense", C.c_int32), ("bdense", P_i32),
+                ("avg_decode", C.c_int32), ("eos_id", C.c_int32)]
+
+
+class SchedStep(C.Structure):
+    _fields_ = [("step", C.c_int64), ("n_req", C.c_int32), ("n_tokens", C.c_int32),
+                ("req_ids", C.POINTER(C.c_int64)), ("q_len", P_i32), ("kv_prefix", P_i32), ("emit", P_i32),
+                ("page_indptr", P_i32), ("page_ids", P_i32), ("tok_src", P_i32)]
+
+
+class SchedStats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("steps", "tokens", "prefill_tokens", "decode_tokens", "finished",
+                                         "generated", "useless", "evictions")] + \
+               [("peak_pages_used", C.c_int32), ("running", C.c_int32), ("queued", C.c_int32)]
+
+
+_sig("nf_sched_create", C.c_int, C.POINTER(SchedCfg), C.POINTER(C.c_void_p))
+_sig("nf_sched_submit", C.c_int, C.c_void_p, C.c_int64, P_i32, C.c_int32, C.c_int32)
+_sig("nf_sched_next", C.c_int, C.c_void_p, C.POINTER(SchedStep))
+_sig("nf_sched_complete", C.c_int, C.c_void_p, C.c_int64, P_i32)
+_sig("nf_sched_get_stats", C.c_int, C.c_void_p, C.POINTER(SchedStats))
+_sig("nf_sched_destroy", None, C.c_void_p)
+_sig("nf_assemble_tokens", C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p)
+
 _sig("nf_kernel_launches", C.c_int64)
 _sig("nf_profile_enable", C.c_int, C.c_int32)
 _sig("nf_profile_read", C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64))
@@ -131,7 +156,8 @@ EXPORTED = ["nf_plan_runtime_note", "nf_comm_create_local", "nf_gemm_workspace_b
             "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_comm_unique_id",
             "nf_comm_create", "nf_comm_destroy", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
             "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_gemm_bf16", "nf_attention",
-            "nf_moe_rows_cap", "nf_moe_route_ws_bytes", "nf_moe_route"]
+            "nf_moe_rows_cap", "nf_moe_route_ws_bytes", "nf_moe_route", "nf_sched_create", "nf_sched_submit",
+            "nf_sched_next", "nf_sched_complete", "nf_sched_get_stats", "nf_sched_destroy", "nf_assemble_tokens"]
 
 
 def _check(status: int):
@@ -361,3 +387,48 @@ def comm_create(tp_size: int, tp_rank: int, uid: bytes) -> int:
     buf = C.create_string_buffer(uid, 128)
     _check(lib.nf_comm_create(tp_size, tp_rank, buf, C.byref(h)))
     return h.value
+
+
+class Scheduler:
+    """nf_sched_* (serving loop: batch scheduler + KV-cache manager, host C++)."""
+
+    def __init__(self, n_pages: int, page_size: int, bdense: Sequence[int], avg_decode: int, eos_id: int = -1):
+        self._bd = np.ascontiguousarray(bdense, dtype=np.int32)
+        cfg = SchedCfg(n_pages, page_size, len(self._bd), self._bd.ctypes.data_as(P_i32), avg_decode, eos_id)
+        self.h = C.c_void_p()
+        _check(lib.nf_sched_create(C.byref(cfg), C.byref(self.h)))
+
+    def submit(self, rid: int, prompt, out_len: int):
+        p = np.ascontiguousarray(prompt, dtype=np.int32)
+        _check(lib.nf_sched_submit(self.h, int(rid), p.ctypes.data_as(P_i32), len(p), int(out_len)))
+
+    def next(self) -> dict:
+        """The formed step as numpy copies (nf_batch arrays + token sources)."""
+        st = SchedStep()
+        _check(lib.nf_sched_next(self.h, C.byref(st)))
+        n, T = st.n_req, st.n_tokens
+        a = lambda ptr, k: np.ctypeslib.as_array(ptr, shape=(k,)).copy() if k > 0 else np.zeros(0, np.int32)
+        ind = a(st.page_indptr, n + 1)
+        return {"step": st.step, "req_ids": a(st.req_ids, n).astype(np.int64) if n else np.zeros(0, np.int64),
+                "q_len": a(st.q_len, n), "kv_prefix": a(st.kv_prefix, n), "emit": a(st.emit, n),
+                "page_indptr": ind, "page_ids": a(st.page_ids, int(ind[-1])) if n else np.zeros(0, np.int32),
+                "tok_src": a(st.tok_src, T)}
+
+    def complete(self, step: int, next_ids):
+        ids = np.ascontiguousarray(next_ids, dtype=np.int32)
+        _check(lib.nf_sched_complete(self.h, int(step), ids.ctypes.data_as(P_i32)))
+
+    def stats(self) -> dict:
+        s = SchedStats()
+        _check(lib.nf_sched_get_stats(self.h, C.byref(s)))
+        return {n: getattr(s, n) for n, _ in SchedStats._fields_}
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value:
+            lib.nf_sched_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+def assemble_tokens(tok_src: int, prev_next_ids: int, token_ids: int, T: int, stream: int):
+    _check(lib.nf_assemble_tokens(C.c_void_p(tok_src), C.c_void_p(prev_next_ids), C.c_void_p(token_ids), T,
+                                  C.c_void_p(stream)))
