@@ -12,7 +12,9 @@ Passages followed (readings A-25..A-29 in DESIGN.md):
 * P:504-505 discrete batching: B_dense is chosen among a few
   high-performance sizes -- the largest allowed size not above the tokens
   available, or everything when fewer tokens than the smallest size are
-  available (A-26).
+  available; decode requests are never deferred to reach a smaller size
+  (if that size is below the decode count, every decode runs, up to the
+  largest allowed size, and no prefill) (A-26).
 * P:573-575 peak-memory admission: the manager predicts each running
   request's completion assuming its total decode length equals the average
   decode length, computes the highest future memory use and admits new
@@ -168,6 +170,8 @@ class Scheduler:
         avail = len(dec) + sum(len(r.prompt) - r.prefilled for r in self.running)
         fits = [b for b in self.bdense if b <= avail]
         B = fits[0] if fits else avail
+        if B < len(dec):                            # decodes never wait for a smaller size (A-26)
+            B = min(len(dec), self.bdense[0])
         comp = []                                   # (req, q_len, kv_prefix, emit)
         for r in dec[:B]:
             comp.append((r, 1, len(r.prompt) + r.generated - 1, 1))

@@ -111,10 +111,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // partial in the tile's slot, half 0 adds it in its epilogue.
   const bool split2 = CG == 1 && args.split == 2 && args.sk_part != nullptr;
   const int ts = (!split2 && args.sk_part != nullptr) ? max(1, args.tail_split) : 1;
+  // Stream-K (args.stream_k, sub-wave GEMMs): CTA c runs k-blocks [c U / G, (c+1) U / G)
+  // of the tile-major (tile, k-block) space, U = tiles * num_kb, so every SM of the
+  // budget works even when there are fewer tiles than SMs.  A CTA's first segment
+  // may start inside a tile (a contributor: fp32 partial to its slot); the CTA
+  // holding a tile's k-block 0 owns it and adds the later CTAs' partials in CTA order.
+  const bool sk = CG == 1 && !split2 && args.stream_k && args.sk_part != nullptr;
+  const int64_t U_sk = (int64_t)tiles * num_kb;
+  auto sk_cta_of = [&](int64_t u) { return (int)(((u + 1) * G - 1) / U_sk); };  // CTA covering unit u
   const int tiles_dp = split2 ? 0 : (ts > 1 ? (tiles / G) * G : tiles);
   const int tail_units = ts > 1 ? (tiles - tiles_dp) * ts : 0;
   const int kb_half = num_kb / 2;
   auto for_each_seg = [&](auto&& fn) {
+    if (sk) {
+      const int64_t a = (int64_t)wid * U_sk / G, b = (int64_t)(wid + 1) * U_sk / G;
+      for (int64_t u = a; u < b;) {
+        const int t = (int)(u / num_kb);
+        const int k0 = (int)(u - (int64_t)t * num_kb);
+        const int k1 = (int)min((int64_t)num_kb, b - (int64_t)t * num_kb);
+        fn(t, k0, k1);
+        u = (int64_t)t * num_kb + k1;
+      }
+      return;
+    }
     if (split2) {
       for (int u = wid; u < 2 * tiles; u += G) {
         if (u & 1) fn(u >> 1, kb_half, num_kb);
@@ -275,7 +294,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           c_first = tile;  // the tile's own partial slot
           n_contrib = 1;
         } else {
-          n_contrib = ts - 1;
+          n_contrib = sk ? sk_cta_of((int64_t)tile * num_kb + num_kb - 1) - wid : ts - 1;
         }
         if (trow == 0) {
           while (ld_acquire_gpu(args.sk_flag + tile * CG + (int)rank) < n_contrib) __nanosleep(32);
@@ -627,9 +646,24 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
       choice = 3;
     }
   }
+  // stream-K for sub-wave GEMMs (fewer tiles than SMs): the work spreads over G CTAs
+  // with >= 16 k-blocks each; cost = work per CTA in tile rounds + a fix-up allowance
+  int sk_grid = 0;
+  if (!grouped && tail_env && args.sk_part != nullptr && args.sk_slots >= SB && tiles < SB && !coloc) {
+    const int64_t U = (int64_t)tiles * num_kb;
+    const int G = (int)std::min<int64_t>(SB, std::max<int64_t>(tiles, U / 16));
+    const double c = (double)U / ((double)G * num_kb) + 0.1;
+    if (G > tiles && c < best - 1e-9) {
+      best = c;
+      choice = 4;
+      sk_grid = G;
+    }
+  }
+  a2.stream_k = choice == 4 ? 1 : 0;
   a2.split = choice == 2 ? 2 : 1;
   a2.tail_split = choice == 1 ? best_s : (choice == 3 ? pair_s : 1);
   if (choice == 1) grid = SB;
+  if (choice == 4) grid = sk_grid;
   if (choice == 2) grid = g2;
   if (choice == 0 || (choice == 3 && pair_s == 1)) a2.sk_part = nullptr;
   if (grid < 1) grid = 1;

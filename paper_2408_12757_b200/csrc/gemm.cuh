@@ -58,6 +58,7 @@ struct GemmArgs {
   int sk_slots;         // partial slots available in sk_part (split-K=2 needs one per tile)
   int split;            // set by the launcher: 1 or 2 (split-K=2 schedule)
   int tail_split;       // set by the launcher: K splits of the partial last wave's tiles (1 = none)
+  int stream_k;         // set by the launcher: 1 = stream-K over the (tile, k-block) space (sub-wave GEMMs)
   // EPI_ARGMAX
   float* am_val;
   int* am_idx;

@@ -110,6 +110,7 @@ std::vector<Item> compose(nf_sched* s) {
       B = b;
       break;
     }
+  if (B < (int64_t)dec.size()) B = std::min<int64_t>((int64_t)dec.size(), s->bdense.front());  // decodes never wait
   std::vector<Item> comp;
   const int64_t nd = std::min<int64_t>((int64_t)dec.size(), B);
   for (int64_t i = 0; i < nd; ++i) {

@@ -56,6 +56,7 @@ class OfflineServer:
         and its next_ids read back from the device."""
         stream = torch.cuda.current_stream()
         prev = None
+        self.timeline = []          # per launched step: (wall s since start, tokens, requests still queued)
         host_sched_s = 0.0
         steps = tokens = 0
         t0 = time.perf_counter()
@@ -85,6 +86,7 @@ class OfflineServer:
                 launched = (st, slot, n, T)
                 steps += 1
                 tokens += T
+                self.timeline.append((time.perf_counter() - t0, T, self.sched.stats()["queued"]))
             if prev is not None:
                 pst, pslot, pn, pT = prev
                 self.done[pslot].synchronize()
@@ -106,4 +108,13 @@ class OfflineServer:
         out = self.sched.stats()
         out.update({"gpu_steps": steps, "step_tokens": tokens, "wall_s": wall,
                     "device_s": e0.elapsed_time(e1) / 1e3, "host_sched_s": host_sched_s})
+        # steady state: the steps launched while requests were still waiting for admission
+        # (the system is at capacity; the drain of the last long requests is excluded)
+        busy = [i for i, (_, _, q) in enumerate(self.timeline) if q > 0]
+        if len(busy) >= 2:
+            i0, i1 = busy[0], busy[-1]
+            t_end = self.timeline[i1 + 1][0] if i1 + 1 < len(self.timeline) else wall
+            out["steady_steps"] = i1 - i0 + 1
+            out["steady_tokens"] = sum(T for _, T, _ in self.timeline[i0:i1 + 1])
+            out["steady_s"] = t_end - self.timeline[i0][0]
         return out

@@ -83,6 +83,32 @@ def _stream_k_case(M, N, K, sm):
     assert rel < 4e-3 and mx < 2e-2 * max(1.0, np.abs(ref).max()), (rel, mx)
 
 
+@pytest.mark.parametrize("M,N,K,sm", [(2048, 1280, 8192, 148), (1024, 1280, 8192, 132), (512, 6144, 4096, 148),
+                                      (128, 4096, 14336, 148), (300, 768, 2048, 100), (1000, 1280, 8192, 116)])
+def test_gemm_stream_k_subwave_vs_oracle(env, M, N, K, sm):
+    """Stream-K schedule of sub-wave GEMMs (fewer 128x256 tiles than SMs, e.g.
+    the 70B TP8 rank's KQV: 80 tiles on 148 SMs): CTA c runs k-blocks
+    [c U/G, (c+1) U/G) of the (tile, k-block) space, owners add the later CTAs'
+    fp32 partials in CTA order.  Oracle values, bit-identical on repeat."""
+    nf, rt = env
+    rng = np.random.default_rng(M + N + K)
+    A = synth.round_bf16(rng.standard_normal((M, K), dtype=np.float32))
+    B = synth.round_bf16(rng.standard_normal((N, K), dtype=np.float32) / np.float32(np.sqrt(K)))
+    Ad, Bd = dev(A), dev(B)
+    ws = torch.empty(nf.gemm_workspace_bytes(M, N), dtype=torch.uint8, device="cuda")
+    outs = []
+    for _ in range(2):
+        C = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+        nf.gemm_bf16(Ad.data_ptr(), K, Bd.data_ptr(), K, C.data_ptr(), N, M, N, K, sm, rt.stream_handle(),
+                     ws.data_ptr(), ws.numel())
+        outs.append(C)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    rel, mx = errors(host(outs[0]), ref)
+    assert rel < 4e-3 and mx < 2e-2 * max(1.0, np.abs(ref).max()), (rel, mx)
+
+
 @pytest.mark.parametrize("M,N,K,sm", [(1024, 4096, 14336, 116), (1024, 4096, 4096, 116), (768, 28672, 4096, 116),
                                       (2048, 6144, 4096, 148), (1280, 4096, 14336, 148), (333, 4096, 4096, 20)])
 def test_gemm_cta_pair_vs_oracle(env, M, N, K, sm):

@@ -68,7 +68,8 @@ def _check_invariants(s, reqs, steps, n_pages, bdense, eos=False):
     first_admit = []
     for i, st in enumerate(steps):
         T = sum(st["q_len"])
-        assert T == 0 or T in bdense or T < min(bdense)
+        n_dec = sum(1 for r, kv in zip(st["req_ids"], st["kv_prefix"]) if kv >= len(prompts[r]))
+        assert T == 0 or T in bdense or T < min(bdense) or T == n_dec    # A-26 (decodes never wait)
         owners = {}
         src = st["tok_src"]
         row_tok0 = np.concatenate([[0], np.cumsum(st["q_len"])]).astype(int)

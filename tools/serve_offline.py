@@ -5,8 +5,10 @@ on one B200 (paper_2408_12757_b200.serving.OfflineServer).
 
 Usage: serve_offline.py [--workload splitwise|lmsys|sharegpt|const:P:D] [--n-req N]
          [--config c2|c4rank] [--pages P] [--mode overlap|sequential]
-Prints one JSON line: total (input + output) tokens/s, output tokens/s,
-steps, mean dense batch, scheduler host time share, useless tokens."""
+Prints one JSON line: total (input + output) tokens/s over the whole trace and in
+the steady state (steps launched while requests still wait for admission, i.e.
+the system at capacity, excluding the drain of the last long requests), output
+tokens/s, steps, mean dense batch, scheduler host time share, useless tokens."""
 import argparse
 import json
 import os
@@ -95,6 +97,9 @@ def main():
             "mean_input": float(inp.mean()), "mean_output": float(out.mean()),
             "throughput_tokens_per_s": total_tokens / st["wall_s"],
             "output_tokens_per_s": float(out.sum()) / st["wall_s"],
+            "steady_tokens_per_s": (st["steady_tokens"] / st["steady_s"]) if st.get("steady_s") else None,
+            "steady_steps": st.get("steady_steps"),
+            "steady_mean_step_tokens": (st["steady_tokens"] / st["steady_steps"]) if st.get("steady_steps") else None,
             "wall_s": st["wall_s"], "device_s": st["device_s"], "steps": st["gpu_steps"],
             "mean_step_tokens": st["step_tokens"] / max(1, st["gpu_steps"]),
             "ms_per_step": 1e3 * st["wall_s"] / max(1, st["gpu_steps"]),
