@@ -307,6 +307,8 @@ Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base) 
   const int64_t maxN = std::max<int64_t>({qkv_n, D, ((F + 127) / 128) * 256});
   w.sk_flag_n = (int)(((T + GEMM_BM - 1) / GEMM_BM) * ((maxN + 127) / 128) +
                       ((R + GEMM_BM - 1) / GEMM_BM) * VT + 64);
+  if (c->n_experts > 0)  // grouped expert GEMMs: up to cap/128 m-tiles
+    w.sk_flag_n = std::max<int>(w.sk_flag_n, (int)(moe_rows_cap(c, T) / GEMM_BM * ((maxN + 127) / 128) + 64));
   w.sk_flag = (int*)take((size_t)w.sk_flag_n * 4);
   if (c->n_experts > 0) {
     const int64_t cap = moe_rows_cap(c, T), nk = T * c->top_k;
@@ -901,6 +903,9 @@ nf_status run_moe_ffn(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat1
   u.out = w->mo_m;
   u.ldo = Fl;
   u.row_scale = w->mo_rowinv;
+  u.sk_part = w->sk_part;
+  u.sk_slots = w->sk_slots;
+  u.sk_flag = w->sk_flag;
   u.grp_off = grp_off;
   u.grp_end = grp_end;
   u.n_groups = E;
@@ -919,6 +924,9 @@ nf_status run_moe_ffn(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat1
   d.outf = w->mo_y;
   d.ldo = D;
   d.row_scale = w->mo_roww;
+  d.sk_part = w->sk_part;
+  d.sk_slots = w->sk_slots;
+  d.sk_flag = w->sk_flag;
   d.grp_off = grp_off;
   d.grp_end = grp_end;
   d.n_groups = E;

@@ -116,20 +116,33 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // budget works even when there are fewer tiles than SMs.  A CTA's first segment
   // may start inside a tile (a contributor: fp32 partial to its slot); the CTA
   // holding a tile's k-block 0 owns it and adds the later CTAs' partials in CTA order.
-  const bool sk = CG == 1 && !split2 && args.stream_k && args.sk_part != nullptr;
-  const int64_t U_sk = (int64_t)tiles * num_kb;
+  // Mode 2 (grouped GEMMs, whose tile count is device data): full waves run
+  // data-parallel and the remaining tiles [sk_t0, tiles) run stream-K, decided here
+  // from the device tile count when each CTA gets >= 16 of their k-blocks.
+  const int sk_mode = (CG == 1 && !split2 && args.sk_part != nullptr) ? args.stream_k : 0;
+  bool sk = sk_mode == 1;
+  int sk_t0 = 0;
+  if (sk_mode == 2) {
+    const int rem = tiles % G;
+    if (rem > 0 && (int64_t)rem * num_kb >= 16LL * G) {
+      sk = true;
+      sk_t0 = tiles - rem;
+    }
+  }
+  const int64_t U_sk = (int64_t)(tiles - sk_t0) * num_kb;
   auto sk_cta_of = [&](int64_t u) { return (int)(((u + 1) * G - 1) / U_sk); };  // CTA covering unit u
   const int tiles_dp = split2 ? 0 : (ts > 1 ? (tiles / G) * G : tiles);
   const int tail_units = ts > 1 ? (tiles - tiles_dp) * ts : 0;
   const int kb_half = num_kb / 2;
   auto for_each_seg = [&](auto&& fn) {
     if (sk) {
+      for (int t = wid; t < sk_t0; t += G) fn(t, 0, num_kb);
       const int64_t a = (int64_t)wid * U_sk / G, b = (int64_t)(wid + 1) * U_sk / G;
       for (int64_t u = a; u < b;) {
         const int t = (int)(u / num_kb);
         const int k0 = (int)(u - (int64_t)t * num_kb);
         const int k1 = (int)min((int64_t)num_kb, b - (int64_t)t * num_kb);
-        fn(t, k0, k1);
+        fn(sk_t0 + t, k0, k1);
         u = (int64_t)t * num_kb + k1;
       }
       return;
@@ -294,7 +307,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           c_first = tile;  // the tile's own partial slot
           n_contrib = 1;
         } else {
-          n_contrib = sk ? sk_cta_of((int64_t)tile * num_kb + num_kb - 1) - wid : ts - 1;
+          n_contrib = sk ? sk_cta_of((int64_t)(tile - sk_t0) * num_kb + num_kb - 1) - wid : ts - 1;
         }
         if (trow == 0) {
           while (ld_acquire_gpu(args.sk_flag + tile * CG + (int)rank) < n_contrib) __nanosleep(32);
@@ -660,12 +673,13 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     }
   }
   a2.stream_k = choice == 4 ? 1 : 0;
+  if (grouped && tail_env && args.sk_part != nullptr && args.sk_slots >= SB && !coloc) a2.stream_k = 2;
   a2.split = choice == 2 ? 2 : 1;
   a2.tail_split = choice == 1 ? best_s : (choice == 3 ? pair_s : 1);
   if (choice == 1) grid = SB;
   if (choice == 4) grid = sk_grid;
   if (choice == 2) grid = g2;
-  if (choice == 0 || (choice == 3 && pair_s == 1)) a2.sk_part = nullptr;
+  if ((choice == 0 && a2.stream_k != 2) || (choice == 3 && pair_s == 1)) a2.sk_part = nullptr;
   if (grid < 1) grid = 1;
   CUtensorMap ta, tb;
   cudaError_t e = make_tmap_bf16(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
