@@ -323,7 +323,7 @@ Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base) 
     w.mo_rowinv = (float*)take(cap * 4);
     w.mo_x = (__nv_bfloat16*)take(cap * D * 2);
     w.mo_m = (__nv_bfloat16*)take(cap * F * 2);
-    w.mo_y = (float*)take(cap * D * 4);
+    w.mo_y = (__nv_bfloat16*)take(cap * D * 2);
   }
   w.total = off;
   return w;
@@ -870,7 +870,7 @@ nf_status run_dense_tail(const LayerCtx& L, const NanoRange& nr, const __nv_bflo
 
 // MoE FFN of one nano-batch (readings A-20..A-23): gating, grouping,
 // grouped Up/Gate + SiLU (1/rms row scale), grouped Down (routing-weight row scale,
-// fp32), weighted combine.  resid != null: out = bf16(resid + sum) with RMS partials
+// bf16), weighted combine (fp32 sum).  resid != null: out = bf16(resid + sum) with RMS partials
 // (TP1); resid == null: out = bf16(sum), this rank's partial for the AllReduce (TP>1).
 // Routing buffers are reused by every nano-batch: all of it runs on the compute stream.
 nf_status run_moe_ffn(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* h1, const nf_packed_layer* wt,
@@ -915,13 +915,13 @@ nf_status run_moe_ffn(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat1
                         L.cs));
   }
   GemmArgs d{};
-  d.epi = EPI_F32;
+  d.epi = EPI_STORE;  // y = bf16(weight * expert output); summed in fp32 by the combine
   d.stages = stages;
   d.M = cap;
   d.N = (int)D;
   d.K = (int)Fl;
   d.n_valid = (int)D;
-  d.outf = w->mo_y;
+  d.out = w->mo_y;
   d.ldo = D;
   d.row_scale = w->mo_roww;
   d.sk_part = w->sk_part;

@@ -661,11 +661,17 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   }
   // stream-K for sub-wave GEMMs (fewer tiles than SMs): the work spreads over G CTAs
   // with >= 16 k-blocks each; cost = work per CTA in tile rounds + a fix-up allowance
+  // Only when A and B fit in L2 together (<= 64 MB): stream-K staggers the CTAs in K,
+  // so the weight k-blocks are no longer read in lockstep by the m-tiles (Down of the
+  // 8B nano-batch, 117 MB of weights, measured 1.6x slower); and only with a clear
+  // margin, since every split tile pays an fp32 partial round trip and a second epilogue
+  // (the 8B nano-batch O projection, 0.86 of a wave, measured 1.3x slower).
   int sk_grid = 0;
-  if (!grouped && tail_env && args.sk_part != nullptr && args.sk_slots >= SB && tiles < SB && !coloc) {
+  const double l2_mb = ((double)args.N * args.K + (double)args.M * args.K) * 2.0 / 1048576.0;
+  if (!grouped && tail_env && args.sk_part != nullptr && args.sk_slots >= SB && tiles < SB && !coloc && l2_mb <= 64.0) {
     const int64_t U = (int64_t)tiles * num_kb;
     const int G = (int)std::min<int64_t>(SB, std::max<int64_t>(tiles, U / 16));
-    const double c = (double)U / ((double)G * num_kb) + 0.1;
+    const double c = (double)U / ((double)G * num_kb) + 0.3;
     if (G > tiles && c < best - 1e-9) {
       best = c;
       choice = 4;

@@ -74,8 +74,7 @@ struct Workspace {
   int* mo_dst;
   int* mo_rowtok;
   float *mo_roww, *mo_rowinv;
-  __nv_bfloat16 *mo_x, *mo_m;
-  float* mo_y;
+  __nv_bfloat16 *mo_x, *mo_m, *mo_y;
   int64_t mo_cap;    // grouped rows capacity
   size_t total;
 };

@@ -4,8 +4,8 @@
 //   group   : counting sort of the T*k assignments into 128-row expert segments (A-23)
 //   gather  : h1 rows -> grouped A operand (one row per assignment)
 //   [grouped Up/Gate GEMM, SiLU*up, 1/rms row scale]    gemm.cu, EPI_SILU
-//   [grouped Down GEMM, routing-weight row scale, fp32] gemm.cu, EPI_F32
-//   combine : out = h1 + sum_j y[dst(t, j)] (fp32, one rounding) + RMS partials
+//   [grouped Down GEMM, routing-weight row scale, bf16] gemm.cu, EPI_STORE
+//   combine : out = h1 + sum_j y[dst(t, j)] (fp32 sum, one rounding) + RMS partials
 //
 // All of these are HBM/L2-bound and small next to the expert GEMMs; their bytes
 // per token are in DESIGN.md §7.
@@ -215,7 +215,7 @@ __global__ void moe_gather_kernel(const __nv_bfloat16* __restrict__ h1, int D, c
 // 4 warps per token: warp w owns the 128-column units u = w, w+4, ... (lane: 4
 // consecutive columns of a unit), up to CH units in flight per batch.
 template <int KMAX>
-__global__ void __launch_bounds__(256) moe_combine_kernel(const float* __restrict__ y, const int* __restrict__ dst,
+__global__ void __launch_bounds__(256) moe_combine_kernel(const __nv_bfloat16* __restrict__ y, const int* __restrict__ dst,
                                                           int T, int k, int D,
                                                           const __nv_bfloat16* __restrict__ resid,
                                                           __nv_bfloat16* __restrict__ out, float* __restrict__ part,
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const float* __restric
   const int t = gw / WPT, w = gw % WPT;
   if (t >= T) return;
   const int n_units = D / 128;
-  const float* src[KMAX];
+  const __nv_bfloat16* src[KMAX];
 #pragma unroll
   for (int j = 0; j < KMAX; ++j) src[j] = j < k ? y + (int64_t)dst[(int64_t)t * k + j] * D : nullptr;
   for (int ub = w; ub < n_units; ub += WPT * CH) {
@@ -240,8 +240,9 @@ __global__ void __launch_bounds__(256) moe_combine_kernel(const float* __restric
 #pragma unroll
         for (int j = 0; j < KMAX; ++j)
           if (j < k) {
-            const float4 v = *reinterpret_cast<const float4*>(src[j] + c);
-            s[u].x += v.x; s[u].y += v.y; s[u].z += v.z; s[u].w += v.w;
+            const uint2 vv = *reinterpret_cast<const uint2*>(src[j] + c);
+            const float2 v0 = unpack_bf16x2(vv.x), v1 = unpack_bf16x2(vv.y);
+            s[u].x += v0.x; s[u].y += v0.y; s[u].z += v1.x; s[u].w += v1.y;
           }
         if (outf == nullptr && resid != nullptr) r[u] = *reinterpret_cast<const uint2*>(resid + (int64_t)t * D + c);
       }
@@ -312,7 +313,7 @@ cudaError_t launch_moe_gather(const __nv_bfloat16* h1, int D, const int* row_tok
   return cudaGetLastError();
 }
 
-cudaError_t launch_moe_combine(const float* y, const int* dst, int T, int k, int D, const __nv_bfloat16* resid,
+cudaError_t launch_moe_combine(const __nv_bfloat16* y, const int* dst, int T, int k, int D, const __nv_bfloat16* resid,
                                __nv_bfloat16* out, float* part, int64_t part_stride, float* outf, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
   if (D % 128 != 0 || k > MOE_MAX_TOPK) return cudaErrorInvalidValue;

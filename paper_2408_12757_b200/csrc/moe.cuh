@@ -25,10 +25,11 @@ cudaError_t launch_moe_group(const int* ids, const float* wts, const float* inv_
 // xg[p] = h1[row_tok[p]] (zeros for padding rows), p < grp_off[E] <= cap.
 cudaError_t launch_moe_gather(const __nv_bfloat16* h1, int D, const int* row_tok, const int* grp_off_end, int cap,
                               __nv_bfloat16* xg, cudaStream_t st);
-// Weighted combine: out[t] = bf16(resid[t] + sum_j y[dst[t*k+j]]) in fp32 (resid may be null: the
+// Weighted combine (y: bf16 weighted expert outputs of the grouped rows):
+// out[t] = bf16(resid[t] + sum_j y[dst[t*k+j]]) in fp32 (resid may be null: the
 // bf16 partial of a TP rank) with RMS sum-of-squares partials of out per 128 columns
 // part[(c/128)*part_stride + t] (part may be null); outf != null: outf[t] = sum_j y[...] in fp32 instead.
-cudaError_t launch_moe_combine(const float* y, const int* dst, int T, int k, int D, const __nv_bfloat16* resid,
+cudaError_t launch_moe_combine(const __nv_bfloat16* y, const int* dst, int T, int k, int D, const __nv_bfloat16* resid,
                                __nv_bfloat16* out, float* part, int64_t part_stride, float* outf, cudaStream_t st);
 // router_packed[e, i] = W_r[e, i] * gamma[i] in fp32 (exact: a product of two bf16 values).
 cudaError_t launch_pack_router(const __nv_bfloat16* w_router, const __nv_bfloat16* gamma, int E, int D, float* dst,
