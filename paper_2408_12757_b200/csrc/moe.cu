@@ -17,7 +17,7 @@ namespace nf {
 
 namespace {
 
-// One CTA of 8 warps per TOK tokens: warp w accumulates the RMS sum of squares and
+// One CTA of 8 warps per TOK (4) tokens: warp w accumulates the RMS sum of squares and
 // the E router dot products of all TOK tokens over its D/8 slice (each router
 // element read once per CTA, reused TOK times), the CTA reduces over warps in
 // smem, and thread t < TOK runs the top-k of token t.
@@ -188,84 +188,82 @@ __global__ void __launch_bounds__(1024) moe_group_kernel(const int* __restrict__
   }
 }
 
-// one warp per grouped row; each lane keeps 4 x 16 B loads in flight
+// Flat elementwise form: one thread per 16 bytes (8 bf16) of a grouped row, so the
+// whole copy is in flight at once (the per-warp row loop was latency-bound).
 __global__ void moe_gather_kernel(const __nv_bfloat16* __restrict__ h1, int D, const int* __restrict__ row_tok,
                                   const int* __restrict__ grp_off_end, int cap, __nv_bfloat16* __restrict__ xg) {
   const int rows = min(*grp_off_end, cap);
-  const int lane = threadIdx.x & 31;
-  const int n16 = D / 8;  // 16-byte chunks per row
-  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < rows; p += (gridDim.x * blockDim.x) >> 5) {
+  const int n16 = D / 8;
+  const int64_t total = (int64_t)rows * n16;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int p = (int)(i / n16), c = (int)(i - (int64_t)p * n16);
     const int t = row_tok[p];
-    uint4* out = reinterpret_cast<uint4*>(xg + (int64_t)p * D);
-    const uint4* in = reinterpret_cast<const uint4*>(h1 + (int64_t)max(t, 0) * D);
-    for (int i0 = lane; i0 < n16; i0 += 128) {
-      uint4 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * 32;
-        v[u] = (t >= 0 && i < n16) ? in[i] : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (i0 + u * 32 < n16) out[i0 + u * 32] = v[u];
-    }
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (t >= 0) v = reinterpret_cast<const uint4*>(h1 + (int64_t)t * D)[c];
+    reinterpret_cast<uint4*>(xg + (int64_t)p * D)[c] = v;
   }
 }
 
-// 4 warps per token: warp w owns the 128-column units u = w, w+4, ... (lane: 4
-// consecutive columns of a unit), up to CH units in flight per batch.
+// Flat elementwise form: one thread per 8 columns of one token; a warp covers 256
+// columns of a token (D % 256 == 0), so the RMS partial of each 128-column unit is a
+// reduction over 16 lanes.
 template <int KMAX>
 __global__ void __launch_bounds__(256) moe_combine_kernel(const __nv_bfloat16* __restrict__ y, const int* __restrict__ dst,
                                                           int T, int k, int D,
                                                           const __nv_bfloat16* __restrict__ resid,
                                                           __nv_bfloat16* __restrict__ out, float* __restrict__ part,
                                                           int64_t part_stride, float* __restrict__ outf) {
-  constexpr int CH = 8, WPT = 4;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int t = gw / WPT, w = gw % WPT;
-  if (t >= T) return;
-  const int n_units = D / 128;
-  const __nv_bfloat16* src[KMAX];
+  const int n8 = D / 8;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)T * n8) return;  // whole warps exit together (n8 % 32 == 0)
+  const int t = (int)(i / n8), c = (int)(i - (int64_t)t * n8) * 8;
+  float s[8];
 #pragma unroll
-  for (int j = 0; j < KMAX; ++j) src[j] = j < k ? y + (int64_t)dst[(int64_t)t * k + j] * D : nullptr;
-  for (int ub = w; ub < n_units; ub += WPT * CH) {
-    float4 s[CH];
-    uint2 r[CH];
+  for (int q = 0; q < 8; ++q) s[q] = 0.f;
 #pragma unroll
-    for (int u = 0; u < CH; ++u) {
-      const int unit = ub + u * WPT, c = unit * 128 + lane * 4;
-      s[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      r[u] = make_uint2(0, 0);
-      if (unit < n_units) {
+  for (int j = 0; j < KMAX; ++j) {
+    if (j < k) {
+      const uint4 v = *reinterpret_cast<const uint4*>(y + (int64_t)dst[(int64_t)t * k + j] * D + c);
+      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int j = 0; j < KMAX; ++j)
-          if (j < k) {
-            const uint2 vv = *reinterpret_cast<const uint2*>(src[j] + c);
-            const float2 v0 = unpack_bf16x2(vv.x), v1 = unpack_bf16x2(vv.y);
-            s[u].x += v0.x; s[u].y += v0.y; s[u].z += v1.x; s[u].w += v1.y;
-          }
-        if (outf == nullptr && resid != nullptr) r[u] = *reinterpret_cast<const uint2*>(resid + (int64_t)t * D + c);
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = unpack_bf16x2(w4[q]);
+        s[2 * q] += f.x;
+        s[2 * q + 1] += f.y;
       }
     }
+  }
+  if (outf != nullptr) {
+    float4* o = reinterpret_cast<float4*>(outf + (int64_t)t * D + c);
+    o[0] = make_float4(s[0], s[1], s[2], s[3]);
+    o[1] = make_float4(s[4], s[5], s[6], s[7]);
+    return;
+  }
+  float r[8];
 #pragma unroll
-    for (int u = 0; u < CH; ++u) {
-      const int unit = ub + u * WPT, c = unit * 128 + lane * 4;
-      if (unit >= n_units) break;
-      if (outf != nullptr) {
-        *reinterpret_cast<float4*>(outf + (int64_t)t * D + c) = s[u];
-        continue;
-      }
-      const float2 a = unpack_bf16x2(r[u].x), b = unpack_bf16x2(r[u].y);
-      const float o0 = round_bf16(a.x + s[u].x), o1 = round_bf16(a.y + s[u].y);
-      const float o2 = round_bf16(b.x + s[u].z), o3 = round_bf16(b.y + s[u].w);
-      *reinterpret_cast<uint2*>(out + (int64_t)t * D + c) = make_uint2(pack_bf16x2(o0, o1), pack_bf16x2(o2, o3));
-      if (part != nullptr) {
-        float q = o0 * o0 + o1 * o1 + o2 * o2 + o3 * o3;
+  for (int q = 0; q < 8; ++q) r[q] = 0.f;
+  if (resid != nullptr) {
+    const uint4 v = *reinterpret_cast<const uint4*>(resid + (int64_t)t * D + c);
+    const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-        if (lane == 0) part[(int64_t)unit * part_stride + t] = q;
-      }
+    for (int q = 0; q < 4; ++q) {
+      const float2 f = unpack_bf16x2(w4[q]);
+      r[2 * q] = f.x;
+      r[2 * q + 1] = f.y;
     }
+  }
+  float o[8], sq = 0.f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    o[q] = round_bf16(r[q] + s[q]);
+    sq = fmaf(o[q], o[q], sq);
+  }
+  *reinterpret_cast<uint4*>(out + (int64_t)t * D + c) =
+      make_uint4(pack_bf16x2(o[0], o[1]), pack_bf16x2(o[2], o[3]), pack_bf16x2(o[4], o[5]), pack_bf16x2(o[6], o[7]));
+  if (part != nullptr) {
+#pragma unroll
+    for (int m = 8; m; m >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, m);
+    if ((threadIdx.x & 15) == 0) part[(int64_t)(c >> 7) * part_stride + t] = sq;
   }
 }
 
@@ -283,7 +281,7 @@ cudaError_t launch_moe_route(const __nv_bfloat16* h1, int T, int D, const float*
   if (T <= 0) return cudaSuccess;
   if (E > MOE_MAX_EXPERTS || k > MOE_MAX_TOPK || D % 8 != 0) return cudaErrorInvalidValue;
   if (D % 64 != 0) return cudaErrorInvalidValue;  // 8 warps x 8-element lanes
-  constexpr int TOK = 8;
+  constexpr int TOK = 4;  // 4 tokens per CTA: ~2 waves of small CTAs keep enough loads in flight
   const int blocks = (T + TOK - 1) / TOK;
   if (E <= 8)
     moe_route_kernel<8, TOK><<<blocks, 256, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms);
@@ -307,7 +305,8 @@ cudaError_t launch_moe_group(const int* ids, const float* wts, const float* inv_
 cudaError_t launch_moe_gather(const __nv_bfloat16* h1, int D, const int* row_tok, const int* grp_off_end, int cap,
                               __nv_bfloat16* xg, cudaStream_t st) {
   if (cap <= 0) return cudaSuccess;
-  const int blocks = std::min((cap + 7) / 8, 148 * 8);
+  const int64_t total = (int64_t)cap * (D / 8);
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   moe_gather_kernel<<<blocks, 256, 0, st>>>(h1, D, row_tok, grp_off_end, cap, xg);
   count_launch();
   return cudaGetLastError();
@@ -316,8 +315,8 @@ cudaError_t launch_moe_gather(const __nv_bfloat16* h1, int D, const int* row_tok
 cudaError_t launch_moe_combine(const __nv_bfloat16* y, const int* dst, int T, int k, int D, const __nv_bfloat16* resid,
                                __nv_bfloat16* out, float* part, int64_t part_stride, float* outf, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  if (D % 128 != 0 || k > MOE_MAX_TOPK) return cudaErrorInvalidValue;
-  const int blocks = (T + 1) / 2;  // 2 tokens x 4 warps per CTA
+  if (D % 256 != 0 || k > MOE_MAX_TOPK) return cudaErrorInvalidValue;
+  const int blocks = (int)(((int64_t)T * (D / 8) + 255) / 256);
   if (k <= 2)
     moe_combine_kernel<2><<<blocks, 256, 0, st>>>(y, dst, T, k, D, resid, out, part, part_stride, outf);
   else
