@@ -320,6 +320,11 @@ def run_nf(args, rank, world, local_rank):
     torch.cuda.synchronize()
 
     sm = [int(x) for x in args.sm.split(",")] if args.sm else None
+    if args.mode == "auto":
+        # per-config default = the fastest plan of the measured sweep (profiles/r1c_sweep_c4rank.log):
+        # the MoE rank proxy runs best SEQUENTIAL (nano-batching its small GEMMs and MoE glue costs
+        # more than the overlap hides); every other config runs the OVERLAP pipeline
+        args.mode = "sequential" if args.config == "c4rank" else "overlap"
     if args.mode == "overlap":
         if args.plan == "auto":
             rows = [l.split(",") for l in open(os.path.join(ROOT, args.curves)).read().splitlines()[1:] if l.strip()]
@@ -563,7 +568,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="nf", choices=["nf", "reference"])
-    ap.add_argument("--mode", default="overlap", choices=["overlap", "nano", "sequential"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "overlap", "nano", "sequential"],
+                    help="auto: the measured-best plan kind per config (OVERLAP except c4rank)")
     ap.add_argument("--plan", default="explicit", choices=["explicit", "auto"],
                     help="auto: nf_plan_create autosearch over --curves (overlap mode)")
     ap.add_argument("--curves", default="profiles/curves_b200_quick.csv")

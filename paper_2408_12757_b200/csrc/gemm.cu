@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // Mode 2 (grouped GEMMs, whose tile count is device data): full waves run
   // data-parallel and the remaining tiles [sk_t0, tiles) run stream-K, decided here
   // from the device tile count when each CTA gets >= 16 of their k-blocks.
-  const int sk_mode = (CG == 1 && !split2 && args.sk_part != nullptr) ? args.stream_k : 0;
+  const int sk_mode = (!split2 && args.sk_part != nullptr) ? args.stream_k : 0;  // CG 2: G = pairs, slots per CTA
   bool sk = sk_mode == 1;
   int sk_t0 = 0;
   if (sk_mode == 2) {
@@ -678,7 +678,22 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
       sk_grid = G;
     }
   }
-  a2.stream_k = choice == 4 ? 1 : 0;
+  // CTA pairs + stream-K (sub-wave in pair tiles): each CTA fetches half the B bytes per
+  // k-block, which is what limits single-CTA stream-K (r1c_ncu_streamk_kqv.md); on a tie
+  // with single-CTA stream-K the pairs are preferred
+  int skp_grid = 0;
+  if (!grouped && cg2_env && bn == 256 && tail_env && args.sk_part != nullptr && args.sk_slots >= SB &&
+      pair_tiles < pairs && !coloc && l2_mb <= 64.0) {
+    const int64_t U = (int64_t)pair_tiles * num_kb;
+    const int G = (int)std::min<int64_t>(pairs, std::max<int64_t>(pair_tiles, U / 16));
+    const double c = (double)U / ((double)G * num_kb) + 0.3;
+    if (G > pair_tiles && c <= best + 1e-9 && (choice == 4 || c < best - 1e-9)) {
+      best = c;
+      choice = 5;
+      skp_grid = G;
+    }
+  }
+  a2.stream_k = (choice == 4 || choice == 5) ? 1 : 0;
   if (grouped && tail_env && args.sk_part != nullptr && args.sk_slots >= SB && !coloc) a2.stream_k = 2;
   a2.split = choice == 2 ? 2 : 1;
   a2.tail_split = choice == 1 ? best_s : (choice == 3 ? pair_s : 1);
@@ -690,14 +705,15 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   CUtensorMap ta, tb;
   cudaError_t e = make_tmap_bf16(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
   if (e != cudaSuccess) return e;
+  const bool pair_kernel = choice == 3 || choice == 5;
   e = make_tmap_bf16(&tb, B, args.K, (uint64_t)args.N * (grouped ? args.n_groups : 1), ldb, GEMM_BK,
-                     choice == 3 ? bn / 2 : bn);
+                     pair_kernel ? bn / 2 : bn);
   if (e != cudaSuccess) return e;
   // smem ring: 4 x 48 KB (BN 256), 6 x 32 KB (BN 128 or CTA pairs); co-located plans use 3 / 4 stages
   int stages, cg = 1;
   void (*kern)(CUtensorMap, CUtensorMap, GemmArgs);
   int attr_idx;
-  if (choice == 3) {
+  if (pair_kernel) {
     stages = 6;
     cg = 2;
     kern = gemm_tcgen05_kernel<6, 256, 2>;
@@ -718,7 +734,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     g_attr_set[attr_idx] = true;
   }
   if (cg == 2) {
-    grid = 2 * (pair_s > 1 ? pairs : std::min(pair_tiles, pairs));
+    grid = 2 * (choice == 5 ? skp_grid : (pair_s > 1 ? pairs : std::min(pair_tiles, pairs)));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(GEMM_THREADS);
