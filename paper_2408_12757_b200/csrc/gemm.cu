@@ -679,15 +679,16 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     }
   }
   // CTA pairs + stream-K (sub-wave in pair tiles): each CTA fetches half the B bytes per
-  // k-block, which is what limits single-CTA stream-K (r1c_ncu_streamk_kqv.md); on a tie
-  // with single-CTA stream-K the pairs are preferred
+  // k-block
   int skp_grid = 0;
   if (!grouped && cg2_env && bn == 256 && tail_env && args.sk_part != nullptr && args.sk_slots >= SB &&
       pair_tiles < pairs && !coloc && l2_mb <= 64.0) {
     const int64_t U = (int64_t)pair_tiles * num_kb;
     const int G = (int)std::min<int64_t>(pairs, std::max<int64_t>(pair_tiles, U / 16));
     const double c = (double)U / ((double)G * num_kb) + 0.3;
-    if (G > pair_tiles && c <= best + 1e-9 && (choice == 4 || c < best - 1e-9)) {
+    // measured no faster than single-CTA stream-K on the 70B-rank KQV (r1c_gemm_micro_streamk_pairs.log:
+    // 900 vs 912 TF/s at M 2048, 626 vs 672 at M 1024): taken only when clearly better
+    if (G > pair_tiles && c < best - 0.05) {
       best = c;
       choice = 5;
       skp_grid = G;
