@@ -31,3 +31,15 @@ def test_tp_dataflow_gloo(tmp_path, world):
                        start_method="spawn")
     errs = np.load(out)
     assert len(errs) == world and (errs < 1e-12).all(), errs
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_tp_moe_dataflow_gloo(tmp_path, world):
+    """MoE FFN under TP (every expert's F columns split across ranks,
+    weighted partials AllReduced over gloo) == unsharded oracle moe_ffn."""
+    import tp_gloo_worker
+    out = str(tmp_path / "err_moe.npy")
+    mp.start_processes(tp_gloo_worker.worker_moe, args=(world, _free_port(), out), nprocs=world, join=True,
+                       start_method="spawn")
+    errs = np.load(out)
+    assert len(errs) == world and (errs < 1e-12).all(), errs

@@ -86,3 +86,40 @@ def worker(rank, world, port, out_path):
         np.save(out_path, np.array([g.item() for g in gathered]))
     dist.barrier()
     dist.destroy_process_group()
+
+
+def worker_moe(rank, world, port, out_path):
+    """MoE FFN dataflow of run_dense_tail_tp (PAPER.md:689 + :183 per expert): the
+    router on the replicated h1 (identical on every rank), this rank's column
+    shard of every expert's gate/up and row shard of its down (runtime.shard_layer),
+    weighted partial sums -> AllReduce -> + h1."""
+    from oracle import moe as OM
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    shape = synth.shape_with(synth.SHAPES["c1-moe"], d_model=256, n_q_heads=8, n_kv_heads=4, head_dim=32,
+                             d_ffn=512, n_experts=6, top_k=2)
+    w = synth.layer_weights(shape, 0)
+    h1 = synth.activations(shape, 37, seed=3, name="h1").astype(np.float64)
+    ref = OM.moe_ffn(h1, w, shape)
+    N, r = world, rank
+    s = shard(w, shape, N, r)
+    assert np.array_equal(s["w_router"], w["w_router"].astype(np.float64))
+    h2 = OL.rmsnorm(h1, w["ffn_norm"], shape.rms_eps)
+    ids, wts, _ = OM.router_topk(h2, w["w_router"], shape.top_k)
+    part = np.zeros_like(h1)
+    for e in range(shape.n_experts):
+        rows, slot = np.nonzero(ids == e)
+        if rows.size:
+            y = OM.expert_ffn(h2[rows], s["w_gate"][e], s["w_up"][e], s["w_down"][e])
+            part[rows] += wts[rows, slot][:, None] * y
+    t = torch.from_numpy(part)
+    dist.all_reduce(t)
+    out = h1 + t.numpy()
+    err = float(np.abs(out - ref).max() / np.abs(ref).max())
+    gathered = [torch.zeros(1, dtype=torch.float64) for _ in range(N)]
+    dist.all_gather(gathered, torch.tensor([err], dtype=torch.float64))
+    if r == 0:
+        np.save(out_path, np.array([g.item() for g in gathered]))
+    dist.barrier()
+    dist.destroy_process_group()
