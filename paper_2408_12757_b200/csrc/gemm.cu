@@ -42,6 +42,11 @@ NF_DEV int ld_acquire_gpu(const int* p) {
   return v;
 }
 NF_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// Programmatic dependent launch: wait for the preceding kernel of the stream (its
+// memory is visible afterwards); let the next kernel of the stream start launching.
+// Both are no-ops when the launch carries no programmatic-serialization attribute.
+NF_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+NF_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 
 // sin/cos of a large fp32 angle: Cody-Waite reduction to [-pi, pi] then SFU.
@@ -85,6 +90,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if constexpr (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int wid = blockIdx.x / CG;  // tile worker: a CTA (CG 1) or a CTA pair (CG 2)
   const bool grouped = args.grp_off != nullptr;
+  if (grouped) griddep_wait();  // the tile list is the previous kernel's output
   // grouped: the row count in use is device data (written by the routing kernels)
   const int tiles_m = grouped ? min(args.grp_off[args.n_groups], M) / TM : (M + TM - 1) / TM;
   const int tiles_n = (N + BN - 1) / BN;
@@ -187,6 +193,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // everything above (barriers, TMEM, descriptor prefetch) overlaps the previous kernel's
+  // tail under PDL; every global read of its outputs and every global write is below
+  griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -248,6 +257,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         as ^= 1;
         if (as == 0) aphase ^= 1;
       });
+      griddep_launch_dependents();  // all MMAs issued: the next kernel may start its prologue
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
@@ -617,7 +627,8 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   const int SB = std::max(1, sm_budget);
   double best = (double)((tiles + SB - 1) / SB);
   int choice = 0, best_s = 1;
-  const bool grouped = args.grp_off != nullptr;  // device-sized tile list: data-parallel only
+  const bool grouped = args.grp_off != nullptr;
+  // (grouped: device-sized tile list, data-parallel or device-decided stream-K tail only)
   if (!grouped && tail_env && args.sk_part != nullptr && args.sk_slots >= SB) {
     const int rem = tiles % SB;
     if (rem > 0) {
@@ -734,27 +745,39 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     if (e != cudaSuccess) return e;
     g_attr_set[attr_idx] = true;
   }
-  if (cg == 2) {
-    grid = 2 * (choice == 5 ? skp_grid : (pair_s > 1 ? pairs : std::min(pair_tiles, pairs)));
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(GEMM_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, ta, tb, a2);
-    count_launch();
-    return e != cudaSuccess ? e : cudaGetLastError();
+  // Programmatic dependent launch (NF_PDL=0 disables): the kernel's prologue overlaps the
+  // tail of the previous kernel on the stream; it waits (griddepcontrol.wait) before
+  // touching any global data.
+  static int pdl_env = -1;
+  if (pdl_env < 0) {
+    const char* pe = getenv("NF_PDL");
+    pdl_env = pe ? atoi(pe) : 1;
   }
-  kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, a2);
+  if (cg == 2) grid = 2 * (choice == 5 ? skp_grid : (pair_s > 1 ? pairs : std::min(pair_tiles, pairs)));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (cg == 2) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_env) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  e = cudaLaunchKernelEx(&cfg, kern, ta, tb, a2);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace nf
