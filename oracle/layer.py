@@ -256,14 +256,21 @@ def emit_rows(batch, emit: Optional[np.ndarray] = None) -> np.ndarray:
 
 
 def model_step(token_ids, weights, pools: List[np.ndarray], batch, shape, emit=None,
-               page_size: int = 16, return_logits: bool = False):
+               page_size: int = 16, return_logits: bool = False, route_logits: Optional[list] = None):
     """x0 = E[token_ids] -> L decoder layers -> RMSNorm * g_final -> logits of
     each emitting request's last row -> greedy argmax, lowest index on ties
     (reading A-15; LM head is our addition C8).  Returns next ids [n_req]
-    (-1 where not emitted)."""
+    (-1 where not emitted).  MoE shapes use oracle.moe's layer; their router
+    logits per layer are appended to ``route_logits`` when given."""
     x = f64(weights["embed"])[np.asarray(token_ids)]
     for l, w in enumerate(weights["layers"]):
-        x = decoder_layer(x, w, pools[l], batch, shape, page_size)
+        if getattr(shape, "n_experts", 0):       # Mixtral-shape MoE layer (PAPER.md:689, oracle.moe)
+            from . import moe
+            x, _, _, lg = moe.moe_decoder_layer(x, w, pools[l], batch, shape, page_size, return_route=True)
+            if route_logits is not None:
+                route_logits.append(lg)
+        else:
+            x = decoder_layer(x, w, pools[l], batch, shape, page_size)
     rows = emit_rows(batch, emit)
     sel = rows[rows >= 0]
     hN = rmsnorm(x[sel], weights["final_norm"], shape.rms_eps)

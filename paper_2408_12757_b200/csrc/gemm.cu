@@ -745,13 +745,14 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     if (e != cudaSuccess) return e;
     g_attr_set[attr_idx] = true;
   }
-  // Programmatic dependent launch (NF_PDL=0 disables): the kernel's prologue overlaps the
+  // Programmatic dependent launch (opt-in, NF_PDL=1): the kernel's prologue overlaps the
   // tail of the previous kernel on the stream; it waits (griddepcontrol.wait) before
-  // touching any global data.
+  // touching any global data.  Measured neutral on the bench steps (profiles/r1c_pdl_ab.log:
+  // 8B and 70B-rank steps within run-to-run noise), so it is off by default.
   static int pdl_env = -1;
   if (pdl_env < 0) {
     const char* pe = getenv("NF_PDL");
-    pdl_env = pe ? atoi(pe) : 1;
+    pdl_env = pe ? atoi(pe) : 0;
   }
   if (cg == 2) grid = 2 * (choice == 5 ? skp_grid : (pair_s > 1 ? pairs : std::min(pair_tiles, pairs)));
   cudaLaunchConfig_t cfg{};

@@ -216,3 +216,33 @@ def test_tp_moe_layer_matches_unsharded_oracle(env, tp, mode, shares):
     for r in range(1, tp):
         assert torch.equal(outs[0], outs[r])
     assert_close(host(outs[0])[sure], ref[sure], what=f"MoE TP{tp}")
+
+
+def test_moe_model_step_vs_oracle(env):
+    """configs[3] family through nf_model_step (embedding -> 2 MoE layers -> LM head
+    -> argmax): ids equal the oracle's wherever its top-2 logit gap > 0.1 (A-15), on
+    requests none of whose tokens had an ambiguous route in any layer."""
+    nf, rt = env
+    shape = synth.shape_with(synth.SHAPES["c1-moe"], n_layers=2, vocab=4096)
+    b = synth.make_batch([1] * 20 + [30, 1, 12], list(range(10, 210, 10)) + [0, 33, 7], seed=6, pool_slack=4)
+    W = synth.model_weights(shape, seed=0)
+    toks = synth.token_ids(b.n_tokens, shape.vocab)
+    pools = [synth.kv_pool(shape, b, seed=2, layer=l) for l in range(2)]
+    routes = []
+    ids_ref, logits, _ = OL.model_step(toks, W, [OL.as_pool(p) for p in pools], b, shape, return_logits=True,
+                                       route_logits=routes)
+    tok_ok = np.all([_unambiguous(lg, shape.top_k, GAP_LAYER) for lg in routes], axis=0)
+    ind = np.concatenate([[0], np.cumsum(b.q_len)])
+    req_ok = np.array([tok_ok[ind[r]:ind[r + 1]].all() for r in range(b.n_req)])
+    cfg = rt.cfg_from_shape(shape)
+    layers = [rt.pack_layer(cfg, device_weights(W["layers"][l])) for l in range(2)]
+    model = rt.Model(cfg, dev(W["embed"]), layers, rt.pack_lm_head(cfg, dev(W["lm_head"]), dev(W["final_norm"])))
+    nb = nf.Batch.from_any(b)
+    ws = rt.workspace(cfg, nb)
+    srt = np.sort(logits, axis=1)
+    sure = (srt[:, -1] - srt[:, -2] > 0.1) & req_ok
+    assert sure.sum() >= len(sure) // 3
+    for mode, shares in [(0, (1,)), (2, (1, 1)), (1, (1, 2))]:
+        ids = model.step(nf.Plan.explicit(cfg, mode=mode, shares=shares), [dev(p) for p in pools], nb,
+                         torch.from_numpy(toks).cuda(), ws).cpu().numpy()
+        assert np.array_equal(ids[sure], ids_ref[sure]), (mode, shares)

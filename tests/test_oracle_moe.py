@@ -158,3 +158,21 @@ def test_group_rows_invariants(T, E, k, tile):
         seg = row_tok[off[e]:off[e] + cnt[e]]
         assert (np.diff(seg) > 0).all()                     # token-major order, one row per token
         assert (row_tok[off[e] + cnt[e]:off[e + 1]] == -1).all()
+
+
+def test_moe_model_step_single_expert_is_dense_model_step():
+    """oracle.layer.model_step on an MoE shape with E = 1, k = 1 equals the dense
+    model step on the same weights (the MoE branch of the model step)."""
+    sh = synth.shape_with(SH, n_experts=1, top_k=1, n_layers=2, vocab=97)
+    dsh = synth.shape_with(sh, n_experts=0)
+    W = synth.model_weights(sh)
+    Wd = dict(W, layers=[{k: (v[0] if k in ("w_gate", "w_up", "w_down") else v) for k, v in w.items()
+                          if k != "w_router"} for w in W["layers"]])
+    b = synth.make_batch([1, 1, 6], [9, 30, 0], seed=3, pool_slack=2)
+    toks = synth.token_ids(b.n_tokens, sh.vocab)
+    pools = [L.as_pool(synth.kv_pool(sh, b, layer=l)) for l in range(2)]
+    routes = []
+    ids, lg, x = L.model_step(toks, W, [p.copy() for p in pools], b, sh, return_logits=True, route_logits=routes)
+    ids_d, lg_d, x_d = L.model_step(toks, Wd, [p.copy() for p in pools], b, dsh, return_logits=True)
+    assert len(routes) == 2 and np.array_equal(ids, ids_d)
+    np.testing.assert_allclose(lg, lg_d, rtol=0, atol=1e-10)
