@@ -399,3 +399,56 @@ def test_model_step_emit_mask(env):
     ids = model.step(nf.Plan.explicit(cfg), [dev(synth.kv_pool(shape, b))], nb,
                      torch.from_numpy(synth.token_ids(b.n_tokens, shape.vocab)).cuda(), ws).cpu().numpy()
     assert ids[1] == -1 and ids[0] >= 0 and ids[2] >= 0
+
+
+def test_layer_70b_rank_full_batch_sampled(env):
+    """configs[2] at full size on one GPU: one LLaMA-2-70B TP8 rank's shards
+    (8/1 heads, F 3584, D 8192) over the B_dense=2048 steady-state batch
+    (1365 decode + 171-token chunk + 512 prompt) in the bench's c3rank OVERLAP
+    launch configuration (132/16 SMs, shares 1:1); sampled requests (decode and
+    both prefill requests) against the oracle."""
+    nf, rt = env
+    shape = synth.shape_with(synth.SHAPES["llama2-70b"], n_q_heads=8, n_kv_heads=1, d_ffn=28672 // 8)
+    b = synth.workload_batch(2048, 512, 1024)
+    w = synth.layer_weights(shape, 0, seed=0)
+    x = synth.activations(shape, b.n_tokens, seed=1)
+    cfg = rt.cfg_from_shape(shape)
+    nb = nf.Batch.from_any(b)
+    packed = rt.pack_layer(cfg, device_weights(w))
+    pool_d = dev_bits(synth.kv_pool_bits(shape, b, seed=2))
+    plan = nf.Plan.explicit(cfg, mode=nf.OVERLAP, shares=(1, 1), sm=[132, 16, 132, 132, 132, 132, 8])
+    out = host(rt.layer_forward(plan, cfg, packed, pool_d, nb, dev(x)))
+    torch.cuda.synchronize()
+    assert np.isfinite(out).all()
+    reqs = [0, 3, 500, 1000, 1364, 1365, 1366]
+    sub, pool = compact_case(shape, b, reqs)
+    rows = token_rows(b, reqs)
+    ref = OL.decoder_layer(x[rows], w, pool, sub, shape)
+    assert_close(out[rows], ref, what="70B TP8 rank full batch sampled")
+
+
+@pytest.mark.parametrize("q_len,prefix", [([1], [0]), ([1], [511]), ([77], [0]), ([1, 1, 1], [15, 16, 17]),
+                                          ([40, 24], [0, 100])])
+def test_model_step_degenerate_batches(env, q_len, prefix):
+    """Degenerate compositions through nf_model_step in every mode: a single
+    decode request (empty second nano-batch), a first token (single-key
+    context), prefill only, decode only."""
+    nf, rt = env
+    shape = synth.shape_with(synth.SHAPES["c1"], n_layers=2, vocab=4096)
+    b = synth.make_batch(q_len, prefix, seed=6, pool_slack=2)
+    W = synth.model_weights(shape, seed=0)
+    toks = synth.token_ids(b.n_tokens, shape.vocab)
+    pools = [synth.kv_pool(shape, b, seed=2, layer=l) for l in range(2)]
+    ids_ref, logits, _ = OL.model_step(toks, W, [OL.as_pool(p) for p in pools], b, shape, return_logits=True)
+    cfg = rt.cfg_from_shape(shape)
+    layers = [rt.pack_layer(cfg, device_weights(W["layers"][l])) for l in range(2)]
+    model = rt.Model(cfg, dev(W["embed"]), layers, rt.pack_lm_head(cfg, dev(W["lm_head"]), dev(W["final_norm"])))
+    nb = nf.Batch.from_any(b)
+    ws = rt.workspace(cfg, nb)
+    srt = np.sort(logits, axis=1)
+    sure = srt[:, -1] - srt[:, -2] > 0.1
+    for mode, shares, bal in [(0, (1,), 0), (1, (1, 1), 2), (2, (1, 1), 2), (2, (1, 3), 0)]:
+        ids = model.step(nf.Plan.explicit(cfg, mode=mode, shares=shares, balance=bal), [dev(p) for p in pools], nb,
+                         torch.from_numpy(toks).cuda(), ws).cpu().numpy()
+        assert ids.shape == (b.n_req,) and ((ids >= 0) & (ids < shape.vocab)).all()
+        assert np.array_equal(ids[sure], ids_ref[sure]), (mode, shares, bal)
