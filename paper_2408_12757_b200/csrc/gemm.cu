@@ -277,6 +277,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int q = 0; q < BN * 2 / 128; ++q)
           if (nb * BN + q * 64 < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + q * 128));
       }
+      // Row scale (folded RMSNorm 1/rms from the previous kernel's sum-of-squares partials,
+      // times an optional per-row scale), computed while the tile's mainloop still runs: the
+      // D/128 partial loads are independent (4 accumulators, fixed order, so every n-tile of
+      // a row gets the bit-identical scale) instead of a serial load chain after the wait.
+      float s = 1.f;
+      if (kb0 == 0 && valid) {
+        if (args.norm_part != nullptr) {
+          float a4[4] = {0.f, 0.f, 0.f, 0.f};
+          const float* np_ = args.norm_part + r;
+          const int np = args.norm_nparts;
+          int p = 0;
+          for (; p + 4 <= np; p += 4) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) a4[q] += np_[(int64_t)(p + q) * args.norm_stride];
+          }
+          for (; p < np; ++p) a4[0] += np_[(int64_t)p * args.norm_stride];
+          s = rsqrtf(((a4[0] + a4[1]) + (a4[2] + a4[3])) * args.inv_d + args.eps);
+        }
+        if (args.row_scale != nullptr) s *= args.row_scale[r];
+      }
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + as * BN + ((uint32_t)(ew * 32) << 16);
@@ -346,13 +366,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] *= sc;
       };
-      float s = 1.f;
-      if (args.norm_part != nullptr && valid) {
-        float acc = 0.f;
-        for (int p = 0; p < args.norm_nparts; ++p) acc += args.norm_part[(int64_t)p * args.norm_stride + r];
-        s = rsqrtf(acc * args.inv_d + args.eps);
-      }
-      if (args.row_scale != nullptr && valid) s *= args.row_scale[r];
       const int n0 = nb * BN;
       float v[32];
       switch (args.epi) {
