@@ -49,6 +49,22 @@ NF_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); 
 NF_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 
+// 1/rms of one row from its sum-of-squares partials part[p * stride], p < np, with 4
+// independent accumulators in a fixed order (kept out of line: inlined into the GEMM
+// epilogue it pushed the kernel into a local-memory stack frame).
+__device__ __noinline__ float rms_row_scale(const float* part, int64_t stride, int np, float inv_d, float eps) {
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  int p = 0;
+  for (; p + 4 <= np; p += 4) {
+    a0 += part[(p + 0) * stride];
+    a1 += part[(p + 1) * stride];
+    a2 += part[(p + 2) * stride];
+    a3 += part[(p + 3) * stride];
+  }
+  for (; p < np; ++p) a0 += part[p * stride];
+  return rsqrtf(((a0 + a1) + (a2 + a3)) * inv_d + eps);
+}
+
 // sin/cos of a large fp32 angle: Cody-Waite reduction to [-pi, pi] then SFU.
 NF_DEV void sincos_reduced(float a, float* s, float* c) {
   const float k = rintf(a * 0.15915494309189535f);
@@ -277,26 +293,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int q = 0; q < BN * 2 / 128; ++q)
           if (nb * BN + q * 64 < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + q * 128));
       }
-      // Row scale (folded RMSNorm 1/rms from the previous kernel's sum-of-squares partials,
-      // times an optional per-row scale), computed while the tile's mainloop still runs: the
-      // D/128 partial loads are independent (4 accumulators, fixed order, so every n-tile of
-      // a row gets the bit-identical scale) instead of a serial load chain after the wait.
-      float s = 1.f;
-      if (kb0 == 0 && valid) {
-        if (args.norm_part != nullptr) {
-          float a4[4] = {0.f, 0.f, 0.f, 0.f};
-          const float* np_ = args.norm_part + r;
-          const int np = args.norm_nparts;
-          int p = 0;
-          for (; p + 4 <= np; p += 4) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) a4[q] += np_[(int64_t)(p + q) * args.norm_stride];
-          }
-          for (; p < np; ++p) a4[0] += np_[(int64_t)p * args.norm_stride];
-          s = rsqrtf(((a4[0] + a4[1]) + (a4[2] + a4[3])) * args.inv_d + args.eps);
-        }
-        if (args.row_scale != nullptr) s *= args.row_scale[r];
-      }
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + as * BN + ((uint32_t)(ew * 32) << 16);
@@ -366,6 +362,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] *= sc;
       };
+      float s = 1.f;
+      if (args.norm_part != nullptr && valid) {
+        // folded RMSNorm 1/rms from the previous kernel's D/128 sum-of-squares partials:
+        // 4 independent accumulators (a serial chain of dependent loads was exposed on
+        // sub-wave GEMMs), fixed order so every n-tile of a row gets the identical scale
+        s = rms_row_scale(args.norm_part + r, args.norm_stride, args.norm_nparts, args.inv_d, args.eps);
+      }
+      if (args.row_scale != nullptr && valid) s *= args.row_scale[r];
       const int n0 = nb * BN;
       float v[32];
       switch (args.epi) {
