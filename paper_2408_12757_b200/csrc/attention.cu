@@ -117,12 +117,18 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
     if (l_item >= n_items) return;
     const int s = issued % NS;
     const int64_t page = __shfl_sync(0xffffffffu, pid_win, l_page & 31);
+    // L2 prefetch of the page pf_dist ahead in this item (no shared memory: under
+    // co-running GEMMs the HBM latency exceeds what the 2-slot ring per warp covers)
+    const int pfi = l_page + a.pf_dist;
+    const bool do_pf = a.pf_dist > 0 && pfi < cur.np;
+    const int64_t pf_page = __shfl_sync(0xffffffffu, ((pfi >> 5) == (l_page >> 5)) ? pid_win : pid_nwin, pfi & 31);
     if (lane == 0) {
       uint8_t* dst = ring + s * STAGE_BYTES;
       const int rowK = (int)(((page * 2 + 0) * kh + cur.kvh) * 16);
       fence_proxy_async();  // WAR: this warp's ldmatrix reads of the slot before the async-proxy refill
       mbar_arrive_expect_tx(&bars[s], STAGE_BYTES);
       tma_load_4d_hint(dst, &pages, &bars[s], 0, rowK, 0, 0, kv_policy);  // K and V of the page: one 4-D box
+      if (do_pf) tma_prefetch_4d(&pages, 0, (int)(((pf_page * 2 + 0) * kh + cur.kvh) * 16), 0, 0);
     }
     ++issued;
     if (++l_page == cur.np) {
@@ -517,9 +523,17 @@ cudaError_t launch_prefill_hd(const CUtensorMap& m, const AttnArgs& a, const Pre
 
 }  // namespace
 
-cudaError_t launch_decode_attention(const CUtensorMap& m, const CUtensorMap& pm, const AttnArgs& a, const DecodeItem* items, int n_items,
+cudaError_t launch_decode_attention(const CUtensorMap& m, const CUtensorMap& pm, const AttnArgs& a0, const DecodeItem* items, int n_items,
                                     int sm_budget, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
+  // L2 prefetch distance (pages ahead of the TMA ring within an item; NF_DEC_PF, 0 = off)
+  static int pf_env = -1;
+  if (pf_env < 0) {
+    const char* e = getenv("NF_DEC_PF");
+    pf_env = e ? atoi(e) : 0;
+  }
+  AttnArgs a = a0;
+  a.pf_dist = std::min(std::max(pf_env, 0), 31);
   if (a.hd == 128) return launch_decode_hd<128>(m, pm, a, items, n_items, sm_budget, st);
   if (a.hd == 64) return launch_decode_hd<64>(m, pm, a, items, n_items, sm_budget, st);
   return cudaErrorInvalidValue;

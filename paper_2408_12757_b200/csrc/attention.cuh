@@ -27,6 +27,7 @@ struct AttnArgs {
   float scale_log2;         // log2(e)/sqrt(hd)
   int dec_warps;            // decode CTA size: 8 (own SMs) or 4 (co-resident with a GEMM CTA)
   int n_rows;               // T: rows of q / o (bound of the prefill kernel's q tensor map)
+  int pf_dist;              // decode: L2 prefetch distance in pages within an item (0 = off); set by the launcher
 };
 
 cudaError_t make_page_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, int kh, int hd, int page_size);
