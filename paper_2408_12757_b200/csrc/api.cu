@@ -324,6 +324,7 @@ Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base) 
     w.mo_x = (__nv_bfloat16*)take(cap * D * 2);
     w.mo_m = (__nv_bfloat16*)take(cap * F * 2);
     w.mo_y = (__nv_bfloat16*)take(cap * D * 2);
+    w.mo_cta = (int*)take(moe_group_ints(T, c->n_experts) * 4);
   }
   w.total = off;
   return w;
@@ -886,11 +887,20 @@ nf_status run_moe_ffn(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat1
   int* grp_end = w->mo_grp + E + 1;
   {
     ProfScope ps(NF_PROF_MISC, L.cs);
+    MoeGroupArgs g{};
+    g.cta_cnt = w->mo_cta;
+    g.cta_base = w->mo_cta + moe_group_ints(M, E) / 2;
+    g.counter = w->sk_flag + (w->sk_flag_n - 1);  // zeroed with the step's flags, self-resetting
+    g.grp_off = grp_off;
+    g.grp_end = grp_end;
+    g.row_tok = w->mo_rowtok;
+    g.row_w = w->mo_roww;
+    g.row_inv = w->mo_rowinv;
+    g.tile = GEMM_BM;
     NF_CUDA(launch_moe_route(h1 + nr.t0 * D, M, (int)D, (const float*)wt->w_router, E, k, c->rms_eps, w->mo_ids,
-                             w->mo_wts, w->mo_inv, L.cs));
-    NF_CUDA(launch_moe_group(w->mo_ids, w->mo_wts, w->mo_inv, M, k, E, GEMM_BM, grp_off, grp_end, w->mo_dst,
-                             w->mo_rowtok, w->mo_roww, w->mo_rowinv, L.cs));
-    NF_CUDA(launch_moe_gather(h1 + nr.t0 * D, (int)D, w->mo_rowtok, grp_off + E, cap, w->mo_x, L.cs));
+                             w->mo_wts, w->mo_inv, g, L.cs));
+    NF_CUDA(launch_moe_scatter(h1 + nr.t0 * D, M, (int)D, k, E, w->mo_ids, w->mo_wts, w->mo_inv, g, w->mo_dst,
+                               w->mo_x, L.cs));
   }
   const int stages = L.p->spec.colocate ? 3 : 4;
   GemmArgs u{};
@@ -1334,7 +1344,7 @@ int64_t nf_moe_rows_cap(const nf_model_cfg* c, int32_t T) {
 
 size_t nf_moe_route_ws_bytes(const nf_model_cfg* c, int32_t T) {
   if (!c || c->n_experts <= 0 || T < 0) return 0;
-  return ((size_t)T + c->n_experts + 2 * (size_t)moe_rows_cap(c, T)) * 4 + 1024;
+  return ((size_t)T + c->n_experts + 2 * (size_t)moe_rows_cap(c, T) + moe_group_ints(T, c->n_experts) + 1) * 4 + 1024;
 }
 
 nf_status nf_moe_route(const nf_model_cfg* c, const void* h1, const void* router_packed, int32_t T, int32_t* ids,
@@ -1353,10 +1363,22 @@ nf_status nf_moe_route(const nf_model_cfg* c, const void* h1, const void* router
   int* grp_end = (int*)(inv + T);
   float* row_w = (float*)(grp_end + c->n_experts);
   float* row_inv = row_w + cap;
+  int* cta = (int*)(row_inv + cap);
+  MoeGroupArgs g{};
+  g.cta_cnt = cta;
+  g.cta_base = cta + moe_group_ints(T, c->n_experts) / 2;
+  g.counter = cta + moe_group_ints(T, c->n_experts);
+  g.grp_off = grp_off;
+  g.grp_end = grp_end;
+  g.row_tok = row_tok;
+  g.row_w = row_w;
+  g.row_inv = row_inv;
+  g.tile = GEMM_BM;
+  NF_CUDA(cudaMemsetAsync(g.counter, 0, 4, st));
   NF_CUDA(launch_moe_route((const __nv_bfloat16*)h1, T, c->d_model, (const float*)router_packed, c->n_experts,
-                           c->top_k, c->rms_eps, ids, wts, inv, st));
-  NF_CUDA(launch_moe_group(ids, wts, inv, T, c->top_k, c->n_experts, GEMM_BM, grp_off, grp_end, dst, row_tok, row_w,
-                           row_inv, st));
+                           c->top_k, c->rms_eps, ids, wts, inv, g, st));
+  NF_CUDA(launch_moe_scatter((const __nv_bfloat16*)h1, T, c->d_model, c->top_k, c->n_experts, ids, wts, inv, g, dst,
+                             nullptr, st));
   return NF_OK;
 }
 

@@ -75,6 +75,7 @@ struct Workspace {
   int* mo_rowtok;
   float *mo_roww, *mo_rowinv;
   __nv_bfloat16 *mo_x, *mo_m, *mo_y;
+  int* mo_cta;       // per-router-CTA expert counts, then bases (moe.cuh MoeGroupArgs)
   int64_t mo_cap;    // grouped rows capacity
   size_t total;
 };

@@ -1,8 +1,9 @@
 // MoE FFN (Mixtral-8x7B shape) around the grouped tcgen05 GEMMs:
 //
 //   route   : RMS statistics + router logits + top-k + renormalised softmax (A-20, A-21)
-//   group   : counting sort of the T*k assignments into 128-row expert segments (A-23)
-//   gather  : h1 rows -> grouped A operand (one row per assignment)
+//   route also groups: per-CTA expert counts, scanned over CTAs by the last CTA into
+//            128-row padded expert segments (A-23)
+//   scatter : each assignment's grouped row + its h1 row copied into the grouped A operand
 //   [grouped Up/Gate GEMM, SiLU*up, 1/rms row scale]    gemm.cu, EPI_SILU
 //   [grouped Down GEMM, routing-weight row scale, bf16] gemm.cu, EPI_STORE
 //   combine : out = h1 + sum_j y[dst(t, j)] (fp32 sum, one rounding) + RMS partials
@@ -17,6 +18,13 @@ namespace nf {
 
 namespace {
 
+template <int EMAX, int TOK>
+NF_DEV void route_token(float (&red)[8][TOK][EMAX + 1], int j, int t, int D, int E, int k, float eps,
+                        int* __restrict__ ids, float* __restrict__ wts, float* __restrict__ inv_rms,
+                        int (&sel_out)[MOE_MAX_TOPK]);
+template <int TOK>
+NF_DEV void group_epilogue(const int (&sel_s)[TOK][MOE_MAX_TOPK], int t0, int T, int k, int E, const MoeGroupArgs& g);
+
 // One CTA of 8 warps per TOK (4) tokens: warp w accumulates the RMS sum of squares and
 // the E router dot products of all TOK tokens over its D/8 slice (each router
 // element read once per CTA, reused TOK times), the CTA reduces over warps in
@@ -25,8 +33,9 @@ template <int EMAX, int TOK>
 __global__ void __launch_bounds__(256) moe_route_kernel(const __nv_bfloat16* __restrict__ h1, int T, int D,
                                                         const float* __restrict__ router, int E, int k, float eps,
                                                         int* __restrict__ ids, float* __restrict__ wts,
-                                                        float* __restrict__ inv_rms) {
+                                                        float* __restrict__ inv_rms, MoeGroupArgs g) {
   __shared__ float red[8][TOK][EMAX + 1];
+  __shared__ int sel_s[TOK][MOE_MAX_TOPK];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * TOK;
   const int d0 = warp * (D / 8), d1 = d0 + D / 8;
@@ -87,7 +96,15 @@ __global__ void __launch_bounds__(256) moe_route_kernel(const __nv_bfloat16* __r
   }
   __syncthreads();
   const int j = threadIdx.x, t = t0 + j;
-  if (j >= TOK || t >= T) return;
+  if (j < TOK && t < T) route_token<EMAX, TOK>(red, j, t, D, E, k, eps, ids, wts, inv_rms, sel_s[j]);
+  if (g.cta_cnt != nullptr) group_epilogue<TOK>(sel_s, t0, T, k, E, g);
+}
+
+// top-k of token t (thread j of its CTA) from the CTA's per-warp partial sums
+template <int EMAX, int TOK>
+NF_DEV void route_token(float (&red)[8][TOK][EMAX + 1], int j, int t, int D, int E, int k, float eps,
+                        int* __restrict__ ids, float* __restrict__ wts, float* __restrict__ inv_rms,
+                        int (&sel_out)[MOE_MAX_TOPK]) {
   // fixed summation order over the 8 D-slices (deterministic)
   float ssq = 0.f, l[EMAX];
 #pragma unroll
@@ -119,88 +136,120 @@ __global__ void __launch_bounds__(256) moe_route_kernel(const __nv_bfloat16* __r
   for (int q = 0; q < k; ++q) {
     ids[(int64_t)t * k + q] = sel[q];
     wts[(int64_t)t * k + q] = p[q] / z;
+    sel_out[q] = sel[q];
   }
   inv_rms[t] = inv;
 }
 
-// One CTA of 1024 threads.  Pass 1 counts assignments per expert; thread 0 lays out
-// the padded segments; pass 2 ranks assignments chunk by chunk in increasing
-// assignment order (warp ballots + a per-expert scan over the 32 warps), so each
-// expert's rows are in token-major order (A-23).
-__global__ void __launch_bounds__(1024) moe_group_kernel(const int* __restrict__ ids, const float* __restrict__ wts,
-                                                         const float* __restrict__ inv_rms, int T, int k, int E,
-                                                         int tile, int* __restrict__ grp_off,
-                                                         int* __restrict__ grp_end, int* __restrict__ dst,
-                                                         int* __restrict__ row_tok, float* __restrict__ row_w,
-                                                         float* __restrict__ row_inv) {
-  __shared__ int cnt[MOE_MAX_EXPERTS], off[MOE_MAX_EXPERTS + 1], run[MOE_MAX_EXPERTS];
-  __shared__ int wcnt[32][MOE_MAX_EXPERTS];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n = T * k;
-  if (tid < MOE_MAX_EXPERTS) { cnt[tid] = 0; run[tid] = 0; }
+// Grouping fused into the router (reading A-23): every CTA publishes its per-expert
+// assignment counts; the last CTA to finish (atomic ticket) scans them over CTAs in
+// CTA order (= token order), lays out the 128-row padded expert segments, writes each
+// CTA's base rank per expert and marks the padding rows.  moe_scatter_kernel then
+// places every assignment without a separate single-CTA grouping pass.
+template <int TOK>
+NF_DEV void group_epilogue(const int (&sel_s)[TOK][MOE_MAX_TOPK], int t0, int T, int k, int E, const MoeGroupArgs& g) {
+  __shared__ bool is_last;
+  __shared__ int tot[MOE_MAX_EXPERTS], off[MOE_MAX_EXPERTS + 1];
   __syncthreads();
-  for (int a = tid; a < n; a += 1024) atomicAdd(&cnt[ids[a]], 1);
+  const int cta = blockIdx.x, nb = gridDim.x;
+  if (threadIdx.x < E) {
+    int c = 0;
+    for (int j = 0; j < TOK; ++j)
+      if (t0 + j < T)
+        for (int q = 0; q < k; ++q) c += sel_s[j][q] == (int)threadIdx.x;
+    g.cta_cnt[(int64_t)cta * E + threadIdx.x] = c;
+  }
+  __threadfence();
   __syncthreads();
-  if (tid == 0) {
-    off[0] = 0;
-    for (int e = 0; e < E; ++e) off[e + 1] = off[e] + (cnt[e] + tile - 1) / tile * tile;
-    for (int e = 0; e <= E; ++e) grp_off[e] = off[e];
-    for (int e = 0; e < E; ++e) grp_end[e] = off[e] + cnt[e];
+  if (threadIdx.x == 0) is_last = atomicAdd(g.counter, 1) == nb - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  // exclusive scan over CTAs, all experts at once: thread i owns CTAs [i*per, (i+1)*per)
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int c0 = threadIdx.x * per, c1 = min(nb, c0 + per);
+  int local[MOE_MAX_EXPERTS];
+  for (int e = 0; e < E; ++e) local[e] = 0;
+  for (int c = c0; c < c1; ++c)
+    for (int e = 0; e < E; ++e) local[e] += __ldcg(g.cta_cnt + (int64_t)c * E + e);
+  __shared__ int wsum[8][MOE_MAX_EXPERTS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl[MOE_MAX_EXPERTS];
+  for (int e = 0; e < E; ++e) {
+    int v = local[e];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += n;
+    }
+    incl[e] = v;
+    if (lane == 31) wsum[warp][e] = v;
   }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int e = 0; e < E; ++e) {
+      int run = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        const int v = wsum[w][e];
+        wsum[w][e] = run;
+        run += v;
+      }
+      tot[e] = run;
+    }
+    off[0] = 0;
+    for (int e = 0; e < E; ++e) off[e + 1] = off[e] + (tot[e] + g.tile - 1) / g.tile * g.tile;
+    for (int e = 0; e <= E; ++e) g.grp_off[e] = off[e];
+    for (int e = 0; e < E; ++e) g.grp_end[e] = off[e] + tot[e];
+    *g.counter = 0;  // self-reset for the next launch
+  }
+  __syncthreads();
+  for (int e = 0; e < E; ++e) {
+    int base = wsum[warp][e] + incl[e] - local[e];  // exclusive prefix of this thread's first CTA
+    for (int c = c0; c < c1; ++c) {
+      g.cta_base[(int64_t)c * E + e] = base;
+      base += __ldcg(g.cta_cnt + (int64_t)c * E + e);
+    }
+  }
   // padding rows of every segment
   for (int e = 0; e < E; ++e)
-    for (int p = off[e] + cnt[e] + tid; p < off[e + 1]; p += 1024) {
-      row_tok[p] = -1;
-      row_w[p] = 0.f;
-      row_inv[p] = 0.f;
+    for (int p = off[e] + tot[e] + threadIdx.x; p < off[e + 1]; p += blockDim.x) {
+      g.row_tok[p] = -1;
+      g.row_w[p] = 0.f;
+      g.row_inv[p] = 0.f;
     }
-  const uint32_t lt = (1u << lane) - 1u;
-  for (int base = 0; base < n; base += 1024) {
-    const int a = base + tid;
-    const int e = a < n ? ids[a] : -1;
-    int rank = 0;
-    for (int q = 0; q < E; ++q) {
-      const uint32_t m = __ballot_sync(0xffffffffu, e == q);
-      if (e == q) rank = __popc(m & lt);
-      if (lane == 0) wcnt[warp][q] = __popc(m);
-    }
-    __syncthreads();
-    if (tid < E) {  // exclusive scan over warps for expert tid, continuing from earlier chunks
-      int s = run[tid];
-      for (int w = 0; w < 32; ++w) {
-        const int c = wcnt[w][tid];
-        wcnt[w][tid] = s;
-        s += c;
-      }
-      run[tid] = s;
-    }
-    __syncthreads();
-    if (e >= 0) {
-      const int p = off[e] + wcnt[warp][e] + rank;
-      const int t = a / k;
-      dst[a] = p;
-      row_tok[p] = t;
-      row_w[p] = wts[a];
-      row_inv[p] = inv_rms[t];
-    }
-    __syncthreads();
-  }
 }
 
-// Flat elementwise form: one thread per 16 bytes (8 bf16) of a grouped row, so the
-// whole copy is in flight at once (the per-warp row loop was latency-bound).
-__global__ void moe_gather_kernel(const __nv_bfloat16* __restrict__ h1, int D, const int* __restrict__ row_tok,
-                                  const int* __restrict__ grp_off_end, int cap, __nv_bfloat16* __restrict__ xg) {
-  const int rows = min(*grp_off_end, cap);
+// Places the assignments of one route CTA's TOK tokens (A-23 ranks: segment offset +
+// the CTA's base + rank inside the CTA in assignment order) and copies their h1 rows
+// into the grouped A operand (xg may be null: placement only).
+template <int TOK>
+__global__ void __launch_bounds__(256) moe_scatter_kernel(const __nv_bfloat16* __restrict__ h1, int T, int D, int k,
+                                                          int E, const int* __restrict__ ids,
+                                                          const float* __restrict__ wts,
+                                                          const float* __restrict__ inv_rms, MoeGroupArgs g,
+                                                          int* __restrict__ dst, __nv_bfloat16* __restrict__ xg) {
+  __shared__ int pos[TOK * MOE_MAX_TOPK];
+  const int t0 = blockIdx.x * TOK;
+  const int n = min(TOK, T - t0) * k;
+  if ((int)threadIdx.x < n) {
+    const int a = t0 * k + threadIdx.x;
+    const int e = ids[a];
+    int r = 0;
+    for (int b = t0 * k; b < a; ++b) r += ids[b] == e;
+    const int p = g.grp_off[e] + g.cta_base[(int64_t)blockIdx.x * E + e] + r;
+    const int t = a / k;
+    pos[threadIdx.x] = p;
+    dst[a] = p;
+    g.row_tok[p] = t;
+    g.row_w[p] = wts[a];
+    g.row_inv[p] = inv_rms[t];
+  }
+  if (xg == nullptr) return;
+  __syncthreads();
   const int n16 = D / 8;
-  const int64_t total = (int64_t)rows * n16;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int p = (int)(i / n16), c = (int)(i - (int64_t)p * n16);
-    const int t = row_tok[p];
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (t >= 0) v = reinterpret_cast<const uint4*>(h1 + (int64_t)t * D)[c];
-    reinterpret_cast<uint4*>(xg + (int64_t)p * D)[c] = v;
+  for (int i = threadIdx.x; i < n * n16; i += blockDim.x) {
+    const int q = i / n16, c = i - q * n16;
+    const int t = t0 + q / k;
+    reinterpret_cast<uint4*>(xg + (int64_t)pos[q] * D)[c] = reinterpret_cast<const uint4*>(h1 + (int64_t)t * D)[c];
   }
 }
 
@@ -277,37 +326,25 @@ __global__ void pack_router_kernel(const __nv_bfloat16* __restrict__ w, const __
 }  // namespace
 
 cudaError_t launch_moe_route(const __nv_bfloat16* h1, int T, int D, const float* router, int E, int k, float eps,
-                             int* ids, float* wts, float* inv_rms, cudaStream_t st) {
+                             int* ids, float* wts, float* inv_rms, const MoeGroupArgs& g, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
   if (E > MOE_MAX_EXPERTS || k > MOE_MAX_TOPK || D % 8 != 0) return cudaErrorInvalidValue;
   if (D % 64 != 0) return cudaErrorInvalidValue;  // 8 warps x 8-element lanes
-  constexpr int TOK = 4;  // 4 tokens per CTA: ~2 waves of small CTAs keep enough loads in flight
-  const int blocks = (T + TOK - 1) / TOK;
+  const int blocks = (T + MOE_ROUTE_TOK - 1) / MOE_ROUTE_TOK;
   if (E <= 8)
-    moe_route_kernel<8, TOK><<<blocks, 256, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms);
+    moe_route_kernel<8, MOE_ROUTE_TOK><<<blocks, 256, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms, g);
   else
-    moe_route_kernel<16, TOK><<<blocks, 256, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms);
+    moe_route_kernel<16, MOE_ROUTE_TOK><<<blocks, 256, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms, g);
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_moe_group(const int* ids, const float* wts, const float* inv_rms, int T, int k, int E, int tile,
-                             int* grp_off, int* grp_end, int* dst, int* row_tok, float* row_w, float* row_inv,
-                             cudaStream_t st) {
+cudaError_t launch_moe_scatter(const __nv_bfloat16* h1, int T, int D, int k, int E, const int* ids, const float* wts,
+                               const float* inv_rms, const MoeGroupArgs& g, int* dst, __nv_bfloat16* xg,
+                               cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  if (E > MOE_MAX_EXPERTS) return cudaErrorInvalidValue;
-  moe_group_kernel<<<1, 1024, 0, st>>>(ids, wts, inv_rms, T, k, E, tile, grp_off, grp_end, dst, row_tok, row_w,
-                                       row_inv);
-  count_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_moe_gather(const __nv_bfloat16* h1, int D, const int* row_tok, const int* grp_off_end, int cap,
-                              __nv_bfloat16* xg, cudaStream_t st) {
-  if (cap <= 0) return cudaSuccess;
-  const int64_t total = (int64_t)cap * (D / 8);
-  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  moe_gather_kernel<<<blocks, 256, 0, st>>>(h1, D, row_tok, grp_off_end, cap, xg);
+  const int blocks = (T + MOE_ROUTE_TOK - 1) / MOE_ROUTE_TOK;
+  moe_scatter_kernel<MOE_ROUTE_TOK><<<blocks, 256, 0, st>>>(h1, T, D, k, E, ids, wts, inv_rms, g, dst, xg);
   count_launch();
   return cudaGetLastError();
 }
