@@ -19,6 +19,9 @@ mixed prefill/decode batch with a paged KV cache, written in float64 numpy:
 * ``moe``       — the Mixtral-shape MoE FFN (readings A-20..A-23):
                   router top-k, expert SwiGLU, weighted combine, TP-sharded
                   form, and the integer token grouping of the grouped GEMMs.
+* ``costmodel`` — the paper's analytic model (Eq. 2-10, Table 2), pinned by the
+                  golden values the paper prints (tests/golden/).
+* ``serving``   — the global batch scheduler / KV-cache manager policy (NEXT-4).
 * ``planner``   — the §5.6 autosearch step by step (critical path + greedy).
 
 Every function cites the PAPER.md line (``P:n``) or SURVEY.md reading
