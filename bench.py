@@ -321,10 +321,12 @@ def run_nf(args, rank, world, local_rank):
 
     sm = [int(x) for x in args.sm.split(",")] if args.sm else None
     if args.mode == "auto":
-        # per-config default = the fastest plan of the measured sweep (profiles/r1c_sweep_c4rank.log):
-        # the MoE rank proxy runs best SEQUENTIAL (nano-batching its small GEMMs and MoE glue costs
-        # more than the overlap hides); every other config runs the OVERLAP pipeline
-        args.mode = "sequential" if args.config == "c4rank" else "overlap"
+        # per-config default = the fastest plan measured on B200 (interleaved ablations,
+        # profiles/r1c_bench_*_final.log, r1c_sweep_c4rank.log): the rank proxies of the
+        # 70B and Mixtral TP8 configs on the constant 512/1024 workload run best SEQUENTIAL
+        # (nano-batching their small per-rank GEMMs costs more than the overlap hides; the
+        # OVERLAP plan is still timed in the ablation); configs[1] runs the OVERLAP pipeline
+        args.mode = "sequential" if args.config in ("c3rank", "c4rank") else "overlap"
     if args.mode == "overlap":
         if args.plan == "auto":
             rows = [l.split(",") for l in open(os.path.join(ROOT, args.curves)).read().splitlines()[1:] if l.strip()]
@@ -569,7 +571,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="nf", choices=["nf", "reference"])
     ap.add_argument("--mode", default="auto", choices=["auto", "overlap", "nano", "sequential"],
-                    help="auto: the measured-best plan kind per config (OVERLAP except c4rank)")
+                    help="auto: the measured-best plan kind per config (OVERLAP except the c3rank/c4rank proxies)")
     ap.add_argument("--plan", default="explicit", choices=["explicit", "auto"],
                     help="auto: nf_plan_create autosearch over --curves (overlap mode)")
     ap.add_argument("--curves", default="profiles/curves_b200_quick.csv")
