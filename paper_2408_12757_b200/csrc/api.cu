@@ -241,6 +241,26 @@ void build_meta(const nf_model_cfg* c, const nf_batch* b, const std::vector<int>
     // longest first: static round-robin over warps/CTAs is then LPT-like
     std::stable_sort(dec.begin() + nr.dec_off, dec.end(),
                      [](const DecodeItem& x, const DecodeItem& y) { return x.kv_len > y.kv_len; });
+    {
+      // (opt-in, NF_DEC_CS_FRAC = f) the shortest items holding a fraction f of the nano-batch's
+      // decode KV run on the compute partition in OVERLAP plans, to balance the two partitions
+      static double cs_frac = -1.0;
+      if (cs_frac < 0.0) {
+        const char* e = getenv("NF_DEC_CS_FRAC");
+        cs_frac = e ? std::max(0.0, std::min(0.9, atof(e))) : 0.0;
+      }
+      if (cs_frac > 0.0 && nr.dec_n > 0) {
+        int64_t tot = 0, acc = 0;
+        for (int q = nr.dec_off; q < nr.dec_off + nr.dec_n; ++q) tot += dec[q].kv_len;
+        int n = 0;
+        for (int q = nr.dec_off + nr.dec_n - 1; q >= nr.dec_off; --q) {
+          if ((double)(acc + dec[q].kv_len) > cs_frac * (double)tot) break;
+          acc += dec[q].kv_len;
+          ++n;
+        }
+        nr.dec_cs_n = std::min(n, nr.dec_n - 1);
+      }
+    }
     std::stable_sort(pf.begin() + nr.pf_off, pf.end(),
                      [](const PrefillItem& x, const PrefillItem& y) { return x.pos0 + x.n > y.pos0 + y.n; });
     m->nanos.push_back(nr);
@@ -768,17 +788,21 @@ nf_status run_prefill(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
 }
 
 // Decode attention of one nano-batch: HBM-bound, on the memory stream in OVERLAP mode.
-nf_status run_decode(const LayerCtx& L, const NanoRange& nr, cudaStream_t st) {
-  if (nr.dec_n <= 0) return NF_OK;
+// part 0: all decode items of the nano-batch; 1: all but the dec_cs_n shortest (memory
+// partition); 2: the dec_cs_n shortest, on the compute partition (OVERLAP balance option)
+nf_status run_decode(const LayerCtx& L, const NanoRange& nr, cudaStream_t st, int part = 0) {
+  const int off = part == 2 ? nr.dec_n - nr.dec_cs_n : 0;
+  const int n = part == 0 ? nr.dec_n : (part == 1 ? nr.dec_n - nr.dec_cs_n : nr.dec_cs_n);
+  if (n <= 0) return NF_OK;
   const nf_model_cfg* c = L.c;
   const AttnArgs a = attn_args(L);
-  const DecodeItem* dec = reinterpret_cast<const DecodeItem*>(L.meta_dev + L.m->off_dec) + nr.dec_off;
+  const DecodeItem* dec = reinterpret_cast<const DecodeItem*>(L.meta_dev + L.m->off_dec) + nr.dec_off + off;
+  const int sms = part == 2 ? clamp_dense(L, L.p->spec.sm[NF_OP_KQV]) : clamp_dec(L, L.p->spec.sm[NF_OP_DECODE_ATTN]);
   ProfScope ps(NF_OP_DECODE_ATTN, st);
   if (use_tc_decode(c, L.p))
-    NF_CUDA(launch_decode_attention_tc(L.pool_map, a, dec, nr.dec_n, clamp_dec(L, L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
+    NF_CUDA(launch_decode_attention_tc(L.pool_map, a, dec, n, sms, st));
   else
-    NF_CUDA(launch_decode_attention(L.pool_map, L.page_map, a, dec, nr.dec_n,
-                                    clamp_dec(L, L.p->spec.sm[NF_OP_DECODE_ATTN]), st));
+    NF_CUDA(launch_decode_attention(L.pool_map, L.page_map, a, dec, n, sms, st));
   return NF_OK;
 }
 
@@ -1143,9 +1167,10 @@ nf_status run_layer(nf_plan* p, const LayerCtx& L, const nf_packed_layer* wt, vo
     if (!kqv_done) NF_TRY(run_kqv(L, nanos[k], x, part, nparts, wt, pool));
     NF_CUDA(cudaEventRecord(p->ev_kqv[k], L.cs));
     NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
-    NF_TRY(run_decode(L, nanos[k], L.ms));
+    NF_TRY(run_decode(L, nanos[k], L.ms, 1));
     NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
     NF_TRY(run_prefill(L, nanos[k], L.cs));
+    NF_TRY(run_decode(L, nanos[k], L.cs, 2));
   }
   for (size_t k = 0; k < nanos.size(); ++k) {
     NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_att[k], 0));
@@ -1282,9 +1307,10 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
       NF_TRY(run_kqv(L, nanos[k], x, px, 1, &w->layers[0], kv_pools[0]));
       NF_CUDA(cudaEventRecord(p->ev_kqv[k], L.cs));
       NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
-      NF_TRY(run_decode(L, nanos[k], L.ms));
+      NF_TRY(run_decode(L, nanos[k], L.ms, 1));
       NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
       NF_TRY(run_prefill(L, nanos[k], L.cs));
+      NF_TRY(run_decode(L, nanos[k], L.cs, 2));
     }
     for (int l = 0; l < c->n_layers; ++l) {
       for (size_t k = 0; k < nanos.size(); ++k) {
@@ -1296,9 +1322,10 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
           NF_TRY(run_kqv(L, nanos[k], y, py, NPn, &w->layers[l + 1], kv_pools[l + 1]));
           NF_CUDA(cudaEventRecord(p->ev_kqv[k], L.cs));
           NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
-          NF_TRY(run_decode(L, nanos[k], L.ms));
+          NF_TRY(run_decode(L, nanos[k], L.ms, 1));
           NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
           NF_TRY(run_prefill(L, nanos[k], L.cs));
+          NF_TRY(run_decode(L, nanos[k], L.cs, 2));
         }
       }
       std::swap(x, y);

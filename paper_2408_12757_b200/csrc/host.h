@@ -34,6 +34,7 @@ struct NanoRange {
   int r0, r1;        // requests [r0, r1) in the internal (permuted) order
   int t0, t1;        // token rows
   int dec_off, dec_n;  // decode items
+  int dec_cs_n = 0;    // OVERLAP: this many of the shortest decode items run on the compute partition
   int pf_off, pf_n;    // prefill items
 };
 
