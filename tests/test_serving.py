@@ -160,14 +160,15 @@ def test_oracle_eviction_and_eos():
     assert drive(s2, max_steps=5000) == steps          # deterministic
 
 
-@pytest.mark.parametrize("case", range(5))
+@pytest.mark.parametrize("case", range(6))
 def test_native_scheduler_bit_exact(case):
     from paper_2408_12757_b200 import nf
     cfgs = [("lmsys", 60, 400, [256, 128, 64], 40, -1, 0.2), ("splitwise", 40, 300, [512, 256], 40, -1, 0.2),
+            ("lmsys", 120, 4000, [48, 24], 60, -1, 0.3, 7),  # decode count above the discrete size (A-26)
             ("sharegpt", 50, 2000, [256, 192, 128, 64, 32], 64, -1, 0.2), ("sharegpt", 30, 40, [64, 32], 1, 3, 0.3),
             ("splitwise", 25, 120, [2048, 1024, 512, 256], 30, 11, 0.5)]
-    name, n, pages, bd, avg, eos, scale = cfgs[case]
-    reqs = trace(n, name, seed=case + 3, scale=scale)
+    name, n, pages, bd, avg, eos, scale = cfgs[case][:7]
+    reqs = trace(n, name, seed=cfgs[case][7] if len(cfgs[case]) > 7 else case + 3, scale=scale)
     a = OS.Scheduler(pages, 16, bd, avg, eos_id=eos)
     b = nf.Scheduler(pages, 16, bd, avg, eos_id=eos)
     for r, p, o in reqs:
@@ -195,3 +196,45 @@ def test_native_scheduler_errors():
         s.submit(2, [], 1)
     with pytest.raises(nf.NFError):
         s.complete(5, [0])                                # not pending
+
+
+def test_discrete_batch_never_defers_decodes():
+    """A-26: 6 decoding requests + 1 prompt token pending, allowed sizes {8, 4}:
+    the largest size not above the 7 available tokens is 4 < 6 decodes, so the
+    step runs all 6 decodes (up to the largest size) and no prefill."""
+    s = OS.Scheduler(256, 16, [8, 4], 50)
+    for r in range(7):
+        q = OS._Req(r, [r + 1], 20, r)
+        q.admit_seq = r
+        if r < 6:
+            q.prefilled, q.generated = 1, 1
+        s.running.append(q)
+    comp = s._compose()
+    assert [(c[0].rid, c[1], c[2]) for c in comp] == [(r, 1, 1) for r in range(6)]
+    s2 = OS.Scheduler(256, 16, [8, 4], 50)
+    s2.running = s.running[:4] + s.running[6:]          # 4 decodes + 1 prompt token: B = 4, decodes only
+    assert [(c[0].rid, c[1]) for c in s2._compose()] == [(r, 1) for r in range(4)]
+
+
+def test_native_traces_exercise_the_decode_rule():
+    """The bit-exact native-vs-oracle traces include steps where the decode count
+    exceeds the largest allowed size not above the available tokens (A-26)."""
+    hits = 0
+    for (name, n, pages, bd, avg, eos, scale, seed) in [("lmsys", 120, 4000, [48, 24], 60, -1, 0.3, 7)]:
+        reqs = trace(n, name, seed=seed, scale=scale)
+        s = OS.Scheduler(pages, 16, bd, avg, eos_id=eos)
+        for r, p, o in reqs:
+            s.submit(r, p, o)
+        orig = s._compose
+
+        def spy():
+            nonlocal hits
+            dec = [r for r in s.running if r.prefilled == len(r.prompt)]
+            avail = len(dec) + sum(len(r.prompt) - r.prefilled for r in s.running)
+            fits = [b for b in s.bdense if b <= avail]
+            if (fits[0] if fits else avail) < len(dec):
+                hits += 1
+            return orig()
+        s._compose = spy
+        drive(s, max_steps=5000)
+    assert hits > 0
