@@ -78,6 +78,15 @@ nf_status validate_cfg(const nf_model_cfg* c) {
   return NF_OK;
 }
 
+// Packed-layer pointers the forward pass dereferences (NF_EINVAL instead of a device fault).
+nf_status validate_packed(const nf_model_cfg* c, const nf_packed_layer* w, int layer) {
+  if (!w->w_qkv || !w->w_o || !w->w_gate_up || !w->w_down)
+    return set_error(NF_EINVAL, "layer %d: NULL packed weight", layer);
+  if (c->tp_size > 1 && !w->w_o_row) return set_error(NF_EINVAL, "layer %d: w_o_row required at tp_size > 1", layer);
+  if (c->n_experts > 0 && !w->w_router) return set_error(NF_EINVAL, "layer %d: MoE layer without w_router", layer);
+  return NF_OK;
+}
+
 int64_t moe_rows_cap(const nf_model_cfg* c, int64_t T) {
   return c->n_experts > 0 ? ((T * c->top_k + GEMM_BM - 1) / GEMM_BM + c->n_experts) * GEMM_BM : 0;
 }
@@ -1196,6 +1205,7 @@ nf_status nf_layer_forward(const nf_plan* plan, nf_comm* comm, const nf_packed_l
                        c->tp_size, c->tp_rank);
   }
   if (!w || !kv_pool || !x_in || !x_out || !ws) return set_error(NF_EINVAL, "NULL pointer argument");
+  NF_TRY(validate_packed(c, w, 0));
   Workspace wsp = carve_workspace(c, b, ws);
   if (ws_bytes < wsp.total) return set_error(NF_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, wsp.total);
   NF_TRY(ensure_runtime(p));
@@ -1243,6 +1253,7 @@ nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weigh
     return set_error(NF_EINVAL, "NULL pointer argument");
   for (int l = 0; l < c->n_layers; ++l)
     if (!kv_pools[l]) return set_error(NF_EINVAL, "kv_pools[%d] is NULL", l);
+  for (int l = 0; l < c->n_layers; ++l) NF_TRY(validate_packed(c, &w->layers[l], l));
   Workspace wsp = carve_workspace(c, b, ws);
   if (ws_bytes < wsp.total) return set_error(NF_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, wsp.total);
   NF_TRY(ensure_runtime(p));

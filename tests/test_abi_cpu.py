@@ -138,3 +138,19 @@ def test_moe_cfg_validation_and_sizes(nf):
     with pytest.raises(nf.NFError) as e:
         nf.moe_route(_cfg(nf, synth.SHAPES["llama3-8b"]), 1, 1, 4, 1, 1, 1, 1, 1, 1, 1 << 20, 0)
     assert e.value.status == nf.NF_EINVAL
+
+
+def test_forward_rejects_incomplete_packed_layers(nf):
+    """nf_layer_forward / nf_model_step validate the packed-layer pointers before
+    any launch: a MoE layer without its router, a NULL projection (NF_EINVAL)."""
+    sh = synth.SHAPES["c1-moe"]
+    cfg = _cfg(nf, sh)
+    b = nf.Batch.from_any(synth.c1_batch())
+    plan = nf.Plan.explicit(cfg, mode=nf.SEQUENTIAL)
+    fake = {"w_qkv": 256, "w_o": 512, "w_gate_up": 768, "w_down": 1024}     # never dereferenced
+    with pytest.raises(nf.NFError) as e:
+        nf.layer_forward(plan, fake, 4096, b, 8192, 12288, 16384, 1 << 30, 0)
+    assert e.value.status == nf.NF_EINVAL and "w_router" in str(e.value)
+    with pytest.raises(nf.NFError) as e:
+        nf.layer_forward(plan, dict(fake, w_router=2048, w_down=None), 4096, b, 8192, 12288, 16384, 1 << 30, 0)
+    assert e.value.status == nf.NF_EINVAL and "NULL packed weight" in str(e.value)
