@@ -23,35 +23,22 @@ NF_DEV void route_token(float (&red)[8][TOK][EMAX + 1], int j, int t, int D, int
                         int* __restrict__ ids, float* __restrict__ wts, float* __restrict__ inv_rms,
                         int (&sel_out)[MOE_MAX_TOPK]);
 template <int TOK>
-NF_DEV void group_count(const int (&sel_s)[TOK][MOE_MAX_TOPK], int t0, int T, int k, int E, const MoeGroupArgs& g,
-                        int grp);
-NF_DEV void group_finish(int E, int ngroups, const MoeGroupArgs& g);
+NF_DEV void group_epilogue(const int (&sel_s)[TOK][MOE_MAX_TOPK], int t0, int T, int k, int E, const MoeGroupArgs& g);
 
 // One CTA of 8 warps per TOK (4) tokens: warp w accumulates the RMS sum of squares and
 // the E router dot products of all TOK tokens over its D/8 slice (each router
 // element read once per CTA, reused TOK times), the CTA reduces over warps in
 // smem, and thread t < TOK runs the top-k of token t.
-// SMEM: the router is staged once per CTA in shared memory and the CTAs are persistent
-// over the token groups (router L2 traffic once per SM instead of once per group).
-template <int EMAX, int TOK, bool SMEM>
+template <int EMAX, int TOK>
 __global__ void __launch_bounds__(256) moe_route_kernel(const __nv_bfloat16* __restrict__ h1, int T, int D,
                                                         const float* __restrict__ router, int E, int k, float eps,
                                                         int* __restrict__ ids, float* __restrict__ wts,
-                                                        float* __restrict__ inv_rms, MoeGroupArgs g, int ngroups) {
+                                                        float* __restrict__ inv_rms, MoeGroupArgs g) {
   __shared__ float red[8][TOK][EMAX + 1];
   __shared__ int sel_s[TOK][MOE_MAX_TOPK];
-  extern __shared__ float4 rsm4[];
-  const float* rt = router;
-  if constexpr (SMEM) {
-    const float4* src = reinterpret_cast<const float4*>(router);
-    for (int q = threadIdx.x; q < E * D / 4; q += blockDim.x) rsm4[q] = src[q];
-    __syncthreads();
-    rt = reinterpret_cast<const float*>(rsm4);
-  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = blockIdx.x * TOK;
   const int d0 = warp * (D / 8), d1 = d0 + D / 8;
-  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-  const int t0 = grp * TOK;
   float acc[TOK][EMAX], sq[TOK];
 #pragma unroll
   for (int j = 0; j < TOK; ++j) {
@@ -78,8 +65,8 @@ __global__ void __launch_bounds__(256) moe_route_kernel(const __nv_bfloat16* __r
 #pragma unroll
     for (int e = 0; e < EMAX; ++e) {
       if (e < E) {
-        const float4 a = *reinterpret_cast<const float4*>(rt + (int64_t)e * D + i);
-        const float4 b = *reinterpret_cast<const float4*>(rt + (int64_t)e * D + i + 4);
+        const float4 a = *reinterpret_cast<const float4*>(router + (int64_t)e * D + i);
+        const float4 b = *reinterpret_cast<const float4*>(router + (int64_t)e * D + i + 4);
 #pragma unroll
         for (int j = 0; j < TOK; ++j) {
           float s = acc[j][e];
@@ -110,10 +97,7 @@ __global__ void __launch_bounds__(256) moe_route_kernel(const __nv_bfloat16* __r
   __syncthreads();
   const int j = threadIdx.x, t = t0 + j;
   if (j < TOK && t < T) route_token<EMAX, TOK>(red, j, t, D, E, k, eps, ids, wts, inv_rms, sel_s[j]);
-  if (g.cta_cnt != nullptr) group_count<TOK>(sel_s, t0, T, k, E, g, grp);
-  __syncthreads();  // red / sel_s are rewritten by the next group
-  }
-  if (g.cta_cnt != nullptr) group_finish(E, ngroups, g);
+  if (g.cta_cnt != nullptr) group_epilogue<TOK>(sel_s, t0, T, k, E, g);
 }
 
 // top-k of token t (thread j of its CTA) from the CTA's per-warp partial sums
@@ -163,27 +147,21 @@ NF_DEV void route_token(float (&red)[8][TOK][EMAX + 1], int j, int t, int D, int
 // CTA's base rank per expert and marks the padding rows.  moe_scatter_kernel then
 // places every assignment without a separate single-CTA grouping pass.
 template <int TOK>
-NF_DEV void group_count(const int (&sel_s)[TOK][MOE_MAX_TOPK], int t0, int T, int k, int E, const MoeGroupArgs& g,
-                        int grp) {
+NF_DEV void group_epilogue(const int (&sel_s)[TOK][MOE_MAX_TOPK], int t0, int T, int k, int E, const MoeGroupArgs& g) {
+  __shared__ bool is_last;
+  __shared__ int tot[MOE_MAX_EXPERTS], off[MOE_MAX_EXPERTS + 1];
   __syncthreads();
+  const int cta = blockIdx.x, nb = gridDim.x;
   if (threadIdx.x < E) {
     int c = 0;
     for (int j = 0; j < TOK; ++j)
       if (t0 + j < T)
         for (int q = 0; q < k; ++q) c += sel_s[j][q] == (int)threadIdx.x;
-    g.cta_cnt[(int64_t)grp * E + threadIdx.x] = c;
+    g.cta_cnt[(int64_t)cta * E + threadIdx.x] = c;
   }
-}
-
-// After every CTA published its groups' counts: the last CTA (atomic ticket) scans the
-// per-group counts in group (= token) order.
-NF_DEV void group_finish(int E, int ngroups, const MoeGroupArgs& g) {
-  __shared__ bool is_last;
-  __shared__ int tot[MOE_MAX_EXPERTS], off[MOE_MAX_EXPERTS + 1];
-  const int nb = ngroups;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(g.counter, 1) == (int)gridDim.x - 1;
+  if (threadIdx.x == 0) is_last = atomicAdd(g.counter, 1) == nb - 1;
   __syncthreads();
   if (!is_last) return;
   __threadfence();
@@ -352,33 +330,11 @@ cudaError_t launch_moe_route(const __nv_bfloat16* h1, int T, int D, const float*
   if (T <= 0) return cudaSuccess;
   if (E > MOE_MAX_EXPERTS || k > MOE_MAX_TOPK || D % 8 != 0) return cudaErrorInvalidValue;
   if (D % 64 != 0) return cudaErrorInvalidValue;  // 8 warps x 8-element lanes
-  const int ngroups = (T + MOE_ROUTE_TOK - 1) / MOE_ROUTE_TOK;
-  const size_t rbytes = (size_t)E * D * 4;
-  static int n_sm = 0;
-  if (n_sm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    if (n_sm <= 0) n_sm = 148;
-  }
-  // router staged in shared memory (persistent CTAs) when it fits: E <= 8, E*D*4 <= 160 KB
-  if (E <= 8 && rbytes <= 160 * 1024 && ngroups > n_sm) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(moe_route_kernel<8, MOE_ROUTE_TOK, true>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    moe_route_kernel<8, MOE_ROUTE_TOK, true><<<n_sm, 256, rbytes, st>>>(h1, T, D, router, E, k, eps, ids, wts,
-                                                                        inv_rms, g, ngroups);
-  } else if (E <= 8) {
-    moe_route_kernel<8, MOE_ROUTE_TOK, false><<<ngroups, 256, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms,
-                                                                       g, ngroups);
-  } else {
-    moe_route_kernel<16, MOE_ROUTE_TOK, false><<<ngroups, 256, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts,
-                                                                        inv_rms, g, ngroups);
-  }
+  const int blocks = (T + MOE_ROUTE_TOK - 1) / MOE_ROUTE_TOK;
+  if (E <= 8)
+    moe_route_kernel<8, MOE_ROUTE_TOK><<<blocks, 256, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms, g);
+  else
+    moe_route_kernel<16, MOE_ROUTE_TOK><<<blocks, 256, 0, st>>>(h1, T, D, router, E, k, eps, ids, wts, inv_rms, g);
   count_launch();
   return cudaGetLastError();
 }
