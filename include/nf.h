@@ -287,6 +287,9 @@ nf_status nf_sched_create(const nf_sched_cfg* cfg, nf_sched** out);
  * (copied); out_len: the position of its EOS (synthetic traces).  NF_EINVAL on a
  * duplicate id or empty prompt / out_len < 1. */
 nf_status nf_sched_submit(nf_sched* s, int64_t req_id, const int32_t* prompt, int32_t prompt_len, int32_t out_len);
+/* NF_EINVAL if the protocol above was not followed (a step older than the previous
+ * one still not completed when a decode needs its token); the scheduler is then
+ * unusable (destroy it). */
 nf_status nf_sched_next(nf_sched* s, nf_sched_step* out);
 /* next_ids: host [n_req of that step] (the step's nf_model_step output).  NF_EINVAL
  * if the step is not pending. */
