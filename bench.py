@@ -194,8 +194,13 @@ def blas_threads():
 
 # ---------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
+    """The oracle as it stands (float64 numpy) on the host cores: each timed step is
+    one oracle decoder layer over a bounded sample of the workload (64 decode
+    requests with the steady-state contexts + one 64-token prefill chunk); value =
+    the sample's tokens per second of a whole L-layer step (t_layer x L)."""
     if rank != 0:
         return
+    args.config = args.config or ("c2" if max(1, args.gpus) == 1 else "c3")
     shape, p_in, d_out = config_shape(args.config)
     b, w, x, pool = oracle_sample(shape, p_in=p_in, d_out=d_out)
     T = b.n_tokens
@@ -204,20 +209,62 @@ def run_reference(args, rank, world):
     ts = []
     for _ in range(args.steps):
         ts += time_oracle_layer(shape, b, w, x, pool)
-    t_step = statistics.median(ts) * shape.n_layers  # x L-extrapolated step time for the sample
-    value = T / t_step
+    t_layer = statistics.median(ts)
+    value = T / (t_layer * shape.n_layers)
     sample = (f"one float64 oracle decoder layer (numpy/BLAS) of the {shape.name} shape over {T} tokens "
-              f"(64 decode requests with the steady-state contexts + one 64-token prefill chunk), "
-              f"x{shape.n_layers} layers extrapolated")
+              f"(64 decode requests with the steady-state contexts + one 64-token prefill chunk) per timed step "
+              f"(median {t_layer:.2f} s); value = {T} tokens / ({shape.n_layers} x t_layer)")
     cores = blas_threads() or cpu_cores()
+    tp = max(1, args.gpus) if args.config in ("c3", "c4") else 1
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(args.config, shape.n_layers, tp=max(1, args.gpus)),
-                       "b_dense": 2048, "n_layers": shape.n_layers, "oracle_sample_tokens": T},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_layer * 1e3, "higher_is_better": True,
+            "scaling": "strong" if tp > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": bench_config(args.config, shape, tp, 768 if (args.config == "c3" and tp == 2) else 2048),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def bench_config(config, shape, tp, b_dense):
+    """The `config` object of both arms (identical for the same workload)."""
+    return {"workload": workload_desc(config, shape.n_layers, tp=tp, b_dense=b_dense), "b_dense": b_dense,
+            "n_layers": shape.n_layers, "tp": tp,
+            "l2": "no flush: per-step inputs (KV + weights, tens of GB) >> 126 MB L2"}
+
+
+# ---------------------------------------------------------------------------- in-run parity
+PARITY_REQS = {"c2": [0, 1, 2, 341, 682, 683], "c3": [0, 1, 700, 1364, 1365], "c3_768": [0, 1, 300, 511, 512]}
+
+
+def compact_from_pool(b, reqs, pool_dev):
+    """Sub-batch of requests `reqs` with a compact float64 host pool holding their cached
+    K/V pages copied from the device pool (before the step appends to it)."""
+    import numpy as np
+    import synth
+    sub = synth.make_batch(b.q_len[reqs], b.kv_prefix[reqs], permute=False)
+    pool = np.zeros((sub.n_pages_pool,) + tuple(pool_dev.shape[1:]), dtype=np.float64)
+    for i, r in enumerate(reqs):
+        src = b.page_ids[b.page_indptr[r]:b.page_indptr[r + 1]]
+        dst = sub.page_ids[sub.page_indptr[i]:sub.page_indptr[i + 1]]
+        n = min(len(src), len(dst))
+        idx = __import__("torch").as_tensor(src[:n].astype(np.int64), device=pool_dev.device)
+        pool[dst[:n]] = pool_dev[idx].float().cpu().numpy()
+    return sub, pool
+
+
+def oracle_parity(shape, b, reqs, w_full, x_in, y_out, pool_sub, sub):
+    """Oracle layer on the GPU's own bf16 layer input for sampled requests
+    (teacher-forced) vs the GPU's layer output on those rows."""
+    import numpy as np
+    from oracle import layer as OL
+    ind = np.concatenate([[0], np.cumsum(b.q_len)])
+    rows = np.concatenate([np.arange(ind[r], ind[r + 1]) for r in reqs])
+    ref = OL.decoder_layer(x_in[rows], w_full, pool_sub, sub, shape)
+    out = y_out[rows]
+    err = out - ref
+    return {"layer": 0, "requests": list(map(int, reqs)), "rows": int(len(rows)),
+            "rel_l2": float(np.linalg.norm(err) / np.linalg.norm(ref)), "max_abs": float(np.abs(err).max()),
+            "tolerance": {"rel_l2": 1e-2, "max_abs": 5e-2}}
 
 
 # ---------------------------------------------------------------------------- nf arm
@@ -233,31 +280,12 @@ def run_nf(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     tp = 1
     comm = None
-    if args.config == "c3":
-        # configs[2]: LLaMA-2-70B shape, tensor parallel over all ranks (NCCL over NVLink)
+    if args.config in ("c3", "c4"):
+        # configs[2] / [3]: tensor parallel over all ranks (NCCL over NVLink)
         if world < 2:
-            raise SystemExit("--config c3 needs torchrun with >= 2 GPUs (70B weights + KV do not fit one B200)")
+            raise SystemExit(f"--config {args.config} needs torchrun with >= 2 GPUs (weights + KV do not fit one B200)")
         tp = world
-        shape = synth.SHAPES["llama2-70b"]
-        p_in, d_out = 512, 1024
-    elif args.config in ("c4", "c4rank"):
-        # configs[3]: Mixtral-8x7B shape (MoE); c4 = TP over all ranks, c4rank = one TP8 rank's shards
-        if args.config == "c4":
-            if world < 2:
-                raise SystemExit("--config c4 needs torchrun with >= 2 GPUs (weights + KV of the 2048 batch exceed one B200)")
-            tp = world
-            shape = synth.SHAPES["mixtral-8x7b"]
-        else:
-            shape = mixtral_rank_shape()
-        p_in, d_out = 512, 1024
-    elif args.config == "c3rank":
-        # rank-local proxy of configs[2] (70B TP8): one rank's head/FFN shards, no collectives
-        shape = synth.shape_with(synth.SHAPES["llama2-70b"], name="llama2-70b-tp8-rank", n_q_heads=8, n_kv_heads=1,
-                                 d_ffn=28672 // 8)
-        p_in, d_out = 512, 1024
-    else:
-        shape = synth.SHAPES["llama3-8b"]
-        p_in, d_out = 1024, 512
+    shape, p_in, d_out = config_shape(args.config)
     if args.layers:
         shape = synth.shape_with(shape, n_layers=args.layers)
     L = shape.n_layers
@@ -266,99 +294,145 @@ def run_nf(args, rank, world, local_rank):
     T = b.n_tokens
     nb = nf.Batch.from_any(b)
     cfg = rt.cfg_from_shape(shape, tp_size=tp, tp_rank=rank if tp > 1 else 0)
+
+    # ---------------- plan (chosen before the communicator: its network SM budget caps NCCL's CTAs)
+    sm = [int(x) for x in args.sm.split(",")] if args.sm else None
+    if args.mode == "auto":
+        # per-config default = the fastest plan measured on B200 (interleaved ablations,
+        # profiles/r1c_bench_*_final.log, r1c_sweep_c4rank.log): the rank proxies of the
+        # 70B and Mixtral TP8 configs on the constant 512/1024 workload run best SEQUENTIAL;
+        # configs[1] and the TP configs run the OVERLAP pipeline
+        args.mode = "sequential" if args.config in ("c3rank", "c4rank") else "overlap"
+    n_dense = 0
+    if args.mode == "overlap":
+        if args.plan == "auto":
+            rows = [l.split(",") for l in open(os.path.join(ROOT, args.curves)).read().splitlines()[1:] if l.strip()]
+            pts = [(int(k), int(u), float(w), float(t)) for k, _, u, w, t in rows]
+            plan = nf.Plan.search(cfg, nb, pts, mode=nf.OVERLAP, n_nano=4 if tp > 1 else 2)
+        elif args.colocate:
+            plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=sm or [148] * 7, balance=True,
+                                    colocate=True)
+        else:
+            # defaults = best of tools/sweep_plans.py on B200 (profiles/r1_sweep_*.log); TP: the
+            # paper's 4-way KQV/attention, 2-way O/UGD/network split with a network
+            # partition for the collectives
+            dense, dec, net, dshares = {"c2": (116, 32, 8, "1,1"), "c4rank": (132, 16, 8, "3,5"),
+                                        "c3": (116, 16, 16, "1,1,1,1"), "c4": (116, 16, 16, "1,1,1,1")}.get(
+                args.config, (132, 16, 8, "1,1"))
+            shares = tuple(int(x) for x in (args.shares or dshares).split(","))
+            n_dense = 2 if (tp > 1 and len(shares) == 4) else 0
+            plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm or [dense, dec, dense, dense, dense, dense, net],
+                                    balance=args.balance, n_dense=n_dense, graph=not args.no_graph)
+    elif args.mode == "nano":
+        plan = nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=tuple(int(x) for x in (args.shares or "1,1").split(",")), sm=sm,
+                                balance=args.balance, graph=not args.no_graph)
+    else:
+        plan = nf.Plan.explicit(cfg, nf.SEQUENTIAL, sm=sm, graph=not args.no_graph)
     if tp > 1:
         uid = [nf.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        comm = nf.comm_create(tp, rank, uid[0])
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
+        comm = nf.comm_create(tp, rank, uid[0], max_ctas=plan.spec().sm[nf.OP_NET])
 
-    def randn(shape_, std=1.0, mean=0.0):
+    # ---------------- weights: replicated tensors (embedding, norms) and layer 0 (in-run parity)
+    # from a generator seeded identically on every rank; every other layer's shards from a
+    # per-rank stream (random init either way)
+    g_rep = torch.Generator(device=dev)
+    g_rep.manual_seed(1234)
+    g_loc = torch.Generator(device=dev)
+    g_loc.manual_seed(4321 + rank)
+
+    def randn(shape_, std=1.0, mean=0.0, gen=None):
         t = torch.empty(shape_, dtype=torch.bfloat16, device=dev)
-        t.normal_(mean, std, generator=g)
+        t.normal_(mean, std, generator=gen or g_loc)
         return t
 
     D, F, hd, Hq, Hk = shape.d_model, shape.d_ffn, shape.head_dim, shape.n_q_heads, shape.n_kv_heads
     E = shape.n_experts
     ex = (E,) if E else ()                     # MoE: expert-major [E, F/N, D] / [E, D, F/N]
-    layers = []
-    for l in range(L):
+    qs, ks, Dl, Fl = Hq // tp * hd, Hk // tp * hd, D // tp, F // tp
+
+    def full_layer(gen):
+        w = {"attn_norm": randn((D,), 0.1, 1.0, g_rep), "w_q": randn((Hq * hd, D), D ** -0.5, gen),
+             "w_k": randn((Hk * hd, D), D ** -0.5, gen), "w_v": randn((Hk * hd, D), D ** -0.5, gen),
+             "w_o": randn((D, Hq * hd), (Hq * hd) ** -0.5, gen), "ffn_norm": randn((D,), 0.1, 1.0, g_rep),
+             "w_gate": randn(ex + (F, D), D ** -0.5, gen), "w_up": randn(ex + (F, D), D ** -0.5, gen),
+             "w_down": randn(ex + (D, F), F ** -0.5, gen)}
         if E:
-            qs, ks, Dl, Fl = Hq // tp * hd, Hk // tp * hd, D // tp, F // tp
-            w = {"attn_norm": randn((D,), 0.1, 1.0), "w_q": randn((qs, D), D ** -0.5),
-                 "w_k": randn((ks, D), D ** -0.5), "w_v": randn((ks, D), D ** -0.5),
-                 "ffn_norm": randn((D,), 0.1, 1.0), "w_router": randn((E, D), D ** -0.5),
-                 "w_gate": randn(ex + (Fl, D), D ** -0.5), "w_up": randn(ex + (Fl, D), D ** -0.5),
-                 "w_down": randn(ex + (D, Fl), F ** -0.5)}
-            if tp == 1:
-                w["w_o"] = randn((D, Hq * hd), (Hq * hd) ** -0.5)
-            else:
-                w["w_o_col"] = randn((Dl, Hq * hd), (Hq * hd) ** -0.5)
-                w["w_o_row"] = randn((D, qs), (Hq * hd) ** -0.5)
-        elif tp == 1:
-            w = {"attn_norm": randn((D,), 0.1, 1.0), "w_q": randn((Hq * hd, D), D ** -0.5),
-                 "w_k": randn((Hk * hd, D), D ** -0.5), "w_v": randn((Hk * hd, D), D ** -0.5),
-                 "w_o": randn((D, Hq * hd), (Hq * hd) ** -0.5), "ffn_norm": randn((D,), 0.1, 1.0),
-                 "w_gate": randn((F, D), D ** -0.5), "w_up": randn((F, D), D ** -0.5),
-                 "w_down": randn((D, F), F ** -0.5)}
+            w["w_router"] = randn((E, D), D ** -0.5, g_rep)
+        return w
+
+    def shard_of(w):
+        return w if tp == 1 else rt.shard_layer(w, Hq, Hk, hd, tp, rank)
+
+    layers = []
+    w0_full = None
+    for l in range(L):
+        if l == 0 or tp == 1:
+            w = full_layer(g_rep if l == 0 else g_loc)
+            if l == 0:
+                w0_full = w
+            layers.append(rt.pack_layer(cfg, shard_of(w)))
         else:  # this rank's shards only
-            qs, ks, Dl, Fl = Hq // tp * hd, Hk // tp * hd, D // tp, F // tp
-            w = {"attn_norm": randn((D,), 0.1, 1.0), "w_q": randn((qs, D), D ** -0.5),
+            w = {"attn_norm": randn((D,), 0.1, 1.0, g_rep), "w_q": randn((qs, D), D ** -0.5),
                  "w_k": randn((ks, D), D ** -0.5), "w_v": randn((ks, D), D ** -0.5),
                  "w_o_col": randn((Dl, Hq * hd), (Hq * hd) ** -0.5), "w_o_row": randn((D, qs), (Hq * hd) ** -0.5),
-                 "ffn_norm": randn((D,), 0.1, 1.0), "w_gate": randn((Fl, D), D ** -0.5),
-                 "w_up": randn((Fl, D), D ** -0.5), "w_down": randn((D, Fl), F ** -0.5)}
-        layers.append(rt.pack_layer(cfg, w))
+                 "ffn_norm": randn((D,), 0.1, 1.0, g_rep), "w_gate": randn(ex + (Fl, D), D ** -0.5),
+                 "w_up": randn(ex + (Fl, D), D ** -0.5), "w_down": randn(ex + (D, Fl), F ** -0.5)}
+            if E:
+                w["w_router"] = randn((E, D), D ** -0.5, g_rep)
+            layers.append(rt.pack_layer(cfg, w))
         del w
-    embed = randn((shape.vocab, D))
-    lm = rt.pack_lm_head(cfg, randn((shape.vocab, D), D ** -0.5), randn((D,), 0.1, 1.0))
+    embed = randn((shape.vocab, D), gen=g_rep)
+    lm_full = randn((shape.vocab, D), D ** -0.5, g_rep)
+    lm = rt.pack_lm_head(cfg, rt.shard_vocab(lm_full, tp, rank) if tp > 1 else lm_full, randn((D,), 0.1, 1.0, g_rep))
+    del lm_full
     model = rt.Model(cfg, embed, layers, lm)
-    pools = [randn((b.n_pages_pool, 2, Hk // tp, 16, hd)) for _ in range(L)]
-    tok = torch.randint(0, shape.vocab, (T,), dtype=torch.int32, device=dev, generator=g)
+    # KV pools: layer 0 full (replicated seed) then this rank's heads; the rest per rank
+    pool0_full = randn((b.n_pages_pool, 2, Hk, 16, hd), gen=g_rep)
+    pools = [rt.shard_pool(pool0_full, tp, rank) if tp > 1 else pool0_full.clone()]
+    pools += [randn((b.n_pages_pool, 2, Hk // tp, 16, hd)) for _ in range(1, L)]
+    tok = torch.randint(0, shape.vocab, (T,), dtype=torch.int32, device=dev, generator=g_rep)
     ws = rt.workspace(cfg, nb, dev)
     next_ids = torch.empty(b.n_req, dtype=torch.int32, device=dev)
     torch.cuda.synchronize()
 
-    sm = [int(x) for x in args.sm.split(",")] if args.sm else None
-    if args.mode == "auto":
-        # per-config default = the fastest plan measured on B200 (interleaved ablations,
-        # profiles/r1c_bench_*_final.log, r1c_sweep_c4rank.log): the rank proxies of the
-        # 70B and Mixtral TP8 configs on the constant 512/1024 workload run best SEQUENTIAL
-        # (nano-batching their small per-rank GEMMs costs more than the overlap hides; the
-        # OVERLAP plan is still timed in the ablation); configs[1] runs the OVERLAP pipeline
-        args.mode = "sequential" if args.config in ("c3rank", "c4rank") else "overlap"
-    if args.mode == "overlap":
-        if args.plan == "auto":
-            rows = [l.split(",") for l in open(os.path.join(ROOT, args.curves)).read().splitlines()[1:] if l.strip()]
-            pts = [(int(k), int(u), float(w), float(t)) for k, _, u, w, t in rows]
-            plan = nf.Plan.search(cfg, nb, pts, mode=nf.OVERLAP, n_nano=2)
-        elif args.colocate:
-            plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=sm or [148] * 7, balance=True,
-                                    colocate=True)
-        else:
-            # defaults = best of tools/sweep_plans.py on B200 (profiles/r1_sweep_*.log)
-            dense, dec, dshares = {"c2": (116, 32, "1,1"), "c4rank": (132, 16, "3,5"), "c4": (132, 16, "3,5")}.get(
-                args.config, (132, 16, "1,1"))
-            shares = tuple(int(x) for x in (args.shares or dshares).split(","))
-            plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm or [dense, dec, dense, dense, dense, dense, 8],
-                                    balance=args.balance)
-    elif args.mode == "nano":
-        plan = nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=tuple(int(x) for x in (args.shares or "1,1").split(",")), sm=sm,
-                                balance=args.balance)
-    else:
-        plan = nf.Plan.explicit(cfg, nf.SEQUENTIAL, sm=sm)
+    # ---------------- in-run parity (before timing; its step rewrites the same KV slots the timed steps do)
+    parity = None
+    if not args.no_parity and not E:
+        key = "c3_768" if (args.config == "c3" and tp == 2) else ("c3" if args.config in ("c3", "c3rank") else "c2")
+        reqs = [r for r in PARITY_REQS[key] if r < b.n_req]
+        if rank == 0:
+            sub, pool_sub = compact_from_pool(b, reqs, pool0_full)
+            w_host = {k: v.float().cpu().numpy() for k, v in w0_full.items()}
+        ids, _, hid = model.step_inspect(plan, pools, nb, tok, ws, comm=comm, logits=False, hidden=True)
+        torch.cuda.synchronize()
+        h0 = hid[0].float().cpu().numpy()
+        h1 = hid[1].float().cpu().numpy()
+        same = True
+        if tp > 1:
+            ck = torch.tensor([float(hid[1].float().sum()), float(hid[L].float().abs().sum())], dtype=torch.float64,
+                              device=dev)
+            allck = [torch.empty_like(ck) for _ in range(world)]
+            dist.all_gather(allck, ck)
+            same = all(torch.equal(allck[0], c) for c in allck)
+        if rank == 0:
+            parity = oracle_parity(shape, b, reqs, w_host, h0, h1, pool_sub, sub)
+            parity["ranks_identical"] = bool(same)
+            parity["ok"] = bool(parity["rel_l2"] <= 1e-2 and parity["max_abs"] <= 5e-2 and same)
+        del hid
+    del w0_full, pool0_full
+    torch.cuda.empty_cache()
     stream = torch.cuda.current_stream()
 
-    def step():
-        model.step(plan, pools, nb, tok, ws, next_ids, comm=comm)
+    def step(pl=plan):
+        model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
 
+    # ---------------- timed region: the plan alone, no per-launch instrumentation
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    nf.profile_enable(True)
-    nf.profile_read()
     launches0 = nf.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
@@ -372,9 +446,7 @@ def run_nf(args, rank, world, local_rank):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    nf.profile_enable(False)
-    launches = (nf.kernel_launches() - launches0) / args.steps
-    prof = nf.profile_read()
+    graph_launches = (nf.kernel_launches() - launches0) / args.steps
     ms = e0.elapsed_time(e1)
     t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -384,8 +456,18 @@ def run_nf(args, rank, world, local_rank):
     replicas = world // tp                                    # independent model copies (1 under TP)
     value = replicas * T * args.steps / (ms_max / 1e3)
 
+    # ---------------- per-op times: a separate instrumented pass (eager launches, CUDA events per kernel)
+    prof_steps = max(2, min(args.steps, 5))
+    nf.profile_enable(True)
+    nf.profile_read()
+    l0 = nf.kernel_launches()
+    for _ in range(prof_steps):
+        step()
+    torch.cuda.synchronize()
+    nf.profile_enable(False)
+    kernels_per_step = (nf.kernel_launches() - l0) / prof_steps
+    prof = nf.profile_read()
     if args.timeline:
-        torch.cuda.synchronize()
         nf.profile_enable(True)
         nf.profile_read()
         step()
@@ -393,7 +475,7 @@ def run_nf(args, rank, world, local_rank):
         spans = nf.profile_timeline()
         nf.profile_enable(False)
         nf.profile_read()
-        with open(args.timeline, "w") as f:
+        with open(args.timeline if world == 1 else f"{args.timeline}.rank{rank}", "w") as f:
             f.write("op,stream,start_ms,end_ms\n")
             for sp in spans:
                 f.write(f"{sp[0]},{sp[1]},{sp[2]:.4f},{sp[3]:.4f}\n")
@@ -403,53 +485,55 @@ def run_nf(args, rank, world, local_rank):
     kv_keys = sum(int(b.kv_prefix[r]) + 1 for r in range(b.n_req) if b.q_len[r] == 1)
     Hq_l, Hk_l, F_l = Hq // tp, Hk // tp, F // tp      # this rank's share under TP
     dec_bytes_step = L * (kv_keys * Hk_l * hd * 2 * 2 + n_dec * Hq_l * hd * 2 * 2)  # K+V read + q read + o write
-    # ---------------- F7 ablation with the same kernels: sequential and nano-batch-only.
-    # The three plans are timed in interleaved rounds (seq, nano, timed mode, seq, ...) so that the
-    # GPU's power / thermal state (1 kW cap) drifts equally over all of them; the
-    # comparison uses per-plan medians of the rounds.
+    # ---------------- F7 ablation with the same kernels: sequential and nano-batch-only,
+    # timed in interleaved rounds (seq, nano, timed mode, seq, ...) so that the GPU's power / thermal
+    # state (1 kW cap) drifts equally over all of them; medians of the rounds.
     ablation = {}
     if not args.no_ablation:
-        plans = [("sequential", nf.Plan.explicit(cfg, nf.SEQUENTIAL)),
-                 ("nano_only", nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=plan.spec().share[:2]
-                                                if plan.spec().n_nano == 2 else (1, 1), balance=args.balance)),
+        sp = plan.spec()
+        nano_shares = tuple(sp.share[:sp.n_nano]) if sp.n_nano > 1 else (1, 1)
+        plans = [("sequential", nf.Plan.explicit(cfg, nf.SEQUENTIAL, graph=not args.no_graph)),
+                 ("nano_only", nf.Plan.explicit(cfg, nf.NANO_ONLY, shares=nano_shares, balance=args.balance,
+                                                n_dense=sp.n_dense if tp > 1 else 0, graph=not args.no_graph)),
                  ("timed_mode", plan)]
         rounds = 3
         per_round = max(2, args.steps // 2)
         times = {n: [] for n, _ in plans}
-        prof_acc = {n: {} for n, _ in plans}
         for _, pl in plans:
             for _ in range(2):
-                model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
+                step(pl)
         for _r in range(rounds):
             for name, pl in plans:
                 a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 torch.cuda.synchronize()
                 if world > 1:
                     dist.barrier()
-                nf.profile_enable(True)
-                nf.profile_read()
                 a0.record(stream)
                 for _ in range(per_round):
-                    model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
+                    step(pl)
                 a1.record(stream)
                 torch.cuda.synchronize()
-                nf.profile_enable(False)
-                for k, v in nf.profile_read().items():
-                    if v[1]:
-                        prof_acc[name].setdefault(k, []).append(v[0] / per_round)
                 t_ab = torch.tensor([a0.elapsed_time(a1) / per_round], dtype=torch.float64, device=dev)
                 if world > 1:
                     dist.all_reduce(t_ab, op=dist.ReduceOp.MAX)
                 times[name].append(float(t_ab.item()))
+        # per-op times of the sequential plan (instrumented, separate)
+        nf.profile_enable(True)
+        nf.profile_read()
+        for _ in range(2):
+            step(plans[0][1])
+        torch.cuda.synchronize()
+        nf.profile_enable(False)
+        seq_prof = {k: v[0] / 2 for k, v in nf.profile_read().items() if v[1]}
         for name, _ in plans:
             ablation[name + "_ms_per_step"] = statistics.median(times[name])
             ablation[name + "_rounds_ms"] = times[name]
-            if name != "timed_mode":
-                ablation[name + "_per_op_ms"] = {k: statistics.median(v) for k, v in prof_acc[name].items()}
+        ablation["sequential_per_op_ms"] = seq_prof
         ablation["timed_mode"] = args.mode
-        ablation["interleaving"] = f"{rounds} rounds x {per_round} steps per plan, medians"
+        ablation["interleaving"] = f"{rounds} rounds x {per_round} steps per plan, medians, max over ranks"
         ablation["speedup_vs_sequential"] = ablation["sequential_ms_per_step"] / ablation["timed_mode_ms_per_step"]
-        seq_dec = ablation["sequential_per_op_ms"].get("decode_attn")
+        ablation["overlap_beats_sequential_p90_p10"] = bool(max(times["timed_mode"]) < min(times["sequential"]))
+        seq_dec = seq_prof.get("decode_attn")
         if seq_dec:
             ablation["sequential_decode_attn_hbm_gbs"] = dec_bytes_step / (seq_dec / 1e3) / 1e9
     # ---------------- end to end through the public API with host buffers
@@ -476,29 +560,29 @@ def run_nf(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = replicas * T * args.steps / (float(e2e_ms.item()) / 1e3)
-    n_dec = int((b.q_len == 1).sum())
-    pf_items = sum(((int(q) + 63) // 64) * Hq for q in b.q_len if q > 1)
-    meta_words = 3 * T + int(b.page_indptr[-1]) + 4 * n_dec * Hk + 8 * pf_items + 2 * b.n_req
+    pf_items = sum(((int(q) + 63) // 64) * Hq_l for q in b.q_len if q > 1)
+    meta_words = 3 * T + int(b.page_indptr[-1]) + 4 * n_dec * Hk_l + 8 * pf_items + 3 * b.n_req
     h2d = T * 4 + meta_words * 4
     d2h = b.n_req * 4
 
     if rank != 0:
         return
 
-    # ---------------- roofline of the dominant kernel (per-op CUDA-event time in the timed region)
+    # ---------------- roofline of the dominant kernel (per-op CUDA-event times of the instrumented pass)
     peaks, peak_src = load_peaks()
     qkv_n = (Hq_l + 2 * Hk_l) * hd
     rows_ffn = T * (shape.top_k if E else 1)          # MoE: top_k expert rows per token (padding excluded)
     flops = {"kqv": 2 * T * qkv_n * D * L, "o_proj": 2 * T * D * Hq_l * hd * L,
              "up_gate": 2 * rows_ffn * 2 * F_l * D * L, "down": 2 * rows_ffn * D * F_l * L,
-             "lm_head": 2 * b.n_req * shape.vocab * D}
-    per_op = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+             "lm_head": 2 * b.n_req * (shape.vocab // tp) * D}
+    per_op = {k: {"ms_per_step": v[0] / prof_steps, "launches_per_step": v[1] / prof_steps}
               for k, v in prof.items() if v[1]}
-    dom = max(per_op, key=lambda k: per_op[k]["ms_per_step"])
+    comp = {k: v for k, v in per_op.items() if k != "net"}
+    dom = max(comp, key=lambda k: comp[k]["ms_per_step"])
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dom)
+        traffic = json.load(open(tpath)).get(f"{args.config}:{dom}") or json.load(open(tpath)).get(dom)
     if dom == "decode_attn":
         achieved = dec_bytes_step / (per_op[dom]["ms_per_step"] / 1e3) / 1e9
         roof = {"kernel": "decode_attn", "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
@@ -518,8 +602,14 @@ def run_nf(args, rank, world, local_rank):
             per_op[k]["tflops"] = flops[k] / (per_op[k]["ms_per_step"] / 1e3) / 1e12
     if "decode_attn" in per_op:
         per_op["decode_attn"]["hbm_gbs"] = dec_bytes_step / (per_op["decode_attn"]["ms_per_step"] / 1e3) / 1e9
-    # every kernel against its own bound (timed mode), and decode attention in the
-    # sequential ablation (all 148 SMs: the kernel's own roofline, not its partition's)
+    if "net" in per_op and tp > 1:
+        # bytes this rank sends per step (ring): AG (N-1)/N of the gathered bytes, AR 2 (N-1)/N of the buffer
+        half = T // 2
+        qd_full = Hq * hd
+        ag = (half * qd_full * 2 + half * D * 2) * (tp - 1) / tp
+        ar = (half * D * 2 + T * D * 2) * 2 * (tp - 1) / tp
+        per_op["net"]["bytes_per_step"] = L * (ag + ar)
+        per_op["net"]["bus_gbs"] = L * (ag + ar) / (per_op["net"]["ms_per_step"] / 1e3) / 1e9
     pk_s = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     roof_all = {}
     for k, v in per_op.items():
@@ -528,40 +618,70 @@ def run_nf(args, rank, world, local_rank):
                            "sms": plan.spec().sm[1] if args.mode == "overlap" else 148}
         elif "tflops" in v:
             roof_all[k] = {"bound": "tensor", "achieved_tflops": v["tflops"], "frac": v["tflops"] / pk_s}
+        elif k == "net" and "bus_gbs" in v:
+            roof_all[k] = {"bound": "nvlink", "achieved_gbs": v["bus_gbs"], "frac": v["bus_gbs"] / 770.0,
+                           "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"}
     seq_dec = ablation.get("sequential_per_op_ms", {}).get("decode_attn")
     if seq_dec:
         gbs = dec_bytes_step / (seq_dec / 1e3) / 1e9
         roof_all["decode_attn_sequential_148sm"] = {"bound": "hbm", "achieved_gbs": gbs, "frac": gbs / peaks["hbm_gbs"]}
 
     optimal = peaks["bf16_tflops"] * 1e12 / (2 * p_active(shape))
+    cfg_line = bench_config(args.config, shape, tp, T)
+    plan_line = {"mode": args.mode, "colocate": bool(plan.spec().colocate),
+                 "parallelism": (f"tp{tp}" if tp > 1 else ("replicas" if world > 1 else "single-gpu")),
+                 "sm": list(plan.spec().sm), "shares": list(plan.spec().share)[:plan.spec().n_nano],
+                 "n_dense": int(plan.spec().n_dense), "cuda_graph": bool(plan.spec().graph),
+                 "source": args.plan, "partitions": plan.runtime_note()}
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if tp > 1 else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, seeded torch RNG on device)",
-            "config": {"workload": workload_desc(args.config, L, tp=tp, b_dense=T),
-                       "b_dense": T, "n_layers": L, "mode": args.mode, "colocate": bool(plan.spec().colocate),
-                       "parallelism": (f"tp{tp}" if tp > 1 else ("replicas" if world > 1 else "single-gpu")),
-                       "plan_sm": list(plan.spec().sm), "plan_shares": list(plan.spec().share)[:plan.spec().n_nano],
-                       "plan": args.plan, "partitions": plan.runtime_note(), "l2": "no flush: per-step inputs (KV 115 GB) >> 126 MB L2"},
+            "config": cfg_line,
+            "plan": plan_line,
             "tokens_per_s_per_gpu": value / world,
             "pct_of_optimal": 100.0 * (value / world) / optimal,
             "optimal_tokens_per_s_per_gpu": optimal,
-            "gpu_launches": launches,
+            "gpu_launches": kernels_per_step,
+            "gpu_launch_note": (f"{kernels_per_step:.0f} libnf kernels per step (instrumented pass); the timed "
+                                f"region issued {graph_launches:.0f} libnf launch call(s) per step "
+                                f"({'CUDA graph replay' if plan.spec().graph else 'eager'})"),
             "clocks": clk.summary(),
+            "parity": parity,
             "roofline": roof,
             "roofline_by_kernel": roof_all,
             "per_op": per_op,
             "ablation": ablation,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}}
     if world == 1 and not args.no_cpu_baseline:
-        b_s, w_s, x_s, pool_s = oracle_sample(shape, p_in=p_in, d_out=d_out)
-        ts = time_oracle_layer(shape, b_s, w_s, x_s, pool_s, reps=3)
-        t_step = statistics.median(ts) * shape.n_layers
-        line["cpu_baseline"] = {"value": b_s.n_tokens / t_step, "unit": "tokens/s",
-                                "cores": blas_threads() or cpu_cores(), "kind": "oracle",
-                                "sample": f"float64 oracle, one {shape.name} layer over {b_s.n_tokens} tokens (64 decode "
-                                          f"+ 64-token chunk), median of 3, x{shape.n_layers} layers extrapolated"}
+        line["cpu_baseline"] = cpu_baseline_full_layer(shape, b, p_in, d_out, args.cpu_tokens)
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_full_layer(shape, b, p_in, d_out, max_tokens):
+    """The oracle as it stands, on the host cores: one float64 decoder layer of the
+    benched workload -- the full B_dense batch when max_tokens >= B_dense,
+    else the first requests of it up to max_tokens tokens -- x L layers."""
+    import numpy as np
+    import synth
+    reqs, tok = [], 0
+    for r in range(b.n_req):
+        if tok + int(b.q_len[r]) > max_tokens:
+            break
+        reqs.append(r)
+        tok += int(b.q_len[r])
+    sub = synth.make_batch(b.q_len[reqs], b.kv_prefix[reqs], seed=3)
+    w = synth.layer_weights(shape, 0, seed=0)
+    x = synth.activations(shape, sub.n_tokens, seed=1)
+    pool = synth.kv_pool(shape, sub, seed=2)
+    ts = time_oracle_layer(shape, sub, w, x, pool, reps=1)
+    t_step = ts[0] * shape.n_layers
+    full = sub.n_tokens == b.n_tokens
+    return {"value": sub.n_tokens / t_step, "unit": "tokens/s", "cores": blas_threads() or cpu_cores(), "kind": "oracle",
+            "sample": (f"float64 oracle, one {shape.name} decoder layer over "
+                       f"{'the full' if full else 'a'} {sub.n_tokens}-token batch "
+                       f"({int((sub.q_len == 1).sum())} decode + {int((sub.q_len > 1).sum())} prefill requests of the "
+                       f"benched steady state) in {ts[0]:.1f} s, x{shape.n_layers} layers")}
 
 
 def main():
@@ -579,16 +699,25 @@ def main():
     ap.add_argument("--balance", type=int, default=2, help="0 request order, 1 balanced, 2 exact shares + KV")
     ap.add_argument("--colocate", action="store_true", help="attention CTAs co-resident with GEMM CTAs")
     ap.add_argument("--sm", default="", help="comma-separated SM budget per op kind (7 values)")
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c3rank", "c4", "c4rank"],
-                    help="c2: configs[1] 8B 1 GPU (replicas for N>1); c3: configs[2] 70B TP=N; c3rank: 1-GPU proxy; "
+    ap.add_argument("--config", default="", choices=["", "c2", "c3", "c3rank", "c4", "c4rank"],
+                    help="default: c2 at N=1, c3 at N>1.  c2: configs[1] 8B 1 GPU (replicas for N>1); c3: configs[2] "
+                         "70B TP=N over NCCL (the metric's config); c3rank: 1-GPU proxy of one TP8 rank; "
                          "c4: configs[3] Mixtral-8x7B TP=N; c4rank: its 1-GPU TP8-rank proxy")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
+    ap.add_argument("--no-parity", action="store_true", help="skip the in-run oracle parity check")
+    ap.add_argument("--cpu-tokens", type=int, default=2048, help="tokens of the cpu_baseline oracle layer")
     ap.add_argument("--layers", type=int, default=0, help="(dev only) override layer count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ablation", action="store_true", help="skip the sequential / nano-only comparison runs")
-    ap.add_argument("--timeline", default="", help="write one step's kernel spans (CSV) to this path")
+    ap.add_argument("--timeline", default="", help="write one step's kernel spans (CSV) to this path (per rank at N>1)")
     ap.add_argument("--ncu", action="store_true", help="profiling run: timed steps only, no e2e / JSON")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if not args.config:
+        args.config = "c2" if world == 1 else "c3"   # N > 1: the metric's configs[2] (70B TP=N), never replicas
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":

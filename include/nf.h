@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define NF_ABI_VERSION 2
+#define NF_ABI_VERSION 3
 
 typedef enum {
   NF_OK = 0,
@@ -119,6 +119,15 @@ typedef struct {
                                   requests split across nano-batches where needed (A-10c) */
   int32_t colocate;            /* 1: attention CTAs co-reside with GEMM CTAs on the same SMs (3-stage GEMM ring,
                                   4-warp decode CTAs) instead of disjoint SM partitions */
+  int32_t n_dense;             /* dense (O / UGD / network) nano-batches; 0 = n_nano.  At tp_size > 1 the
+                                  n_nano attention nano-batches are grouped into n_dense contiguous dense
+                                  nano-batches (n_nano % n_dense == 0): the paper's 4-way KQV/attention and
+                                  2-way O/UGD/network split is n_nano 4, n_dense 2.  Dense
+                                  nano-batch 0 runs column-parallel O + AllGather, the others row-parallel O +
+                                  AllReduce.  At tp_size 1 it must be 0 or n_nano. */
+  int32_t graph;               /* nf_model_step only: 1 = capture the step's launches in a CUDA graph per
+                                  (batch structure, buffers) and replay it; the step metadata is uploaded
+                                  outside the graph.  Ignored with an emulated communicator. */
 } nf_plan_spec;
 
 /* One measured kernel-curve sample, CSV `op_kind,resource_class,units,work,latency_s`. */
@@ -157,13 +166,21 @@ const char* nf_plan_runtime_note(const nf_plan* plan);
 typedef struct nf_comm nf_comm;
 /* 128-byte NCCL unique id, created on rank 0 and broadcast by the caller. */
 nf_status nf_comm_unique_id(void* id_out_128);
-nf_status nf_comm_create(int32_t tp_size, int32_t tp_rank, const void* id_128, nf_comm** out);
+/* NCCL communicator (bf16 AllGather / AllReduce over NVLink / NVSwitch).  max_ctas > 0 caps the
+ * CTAs of every collective (ncclConfig_t.maxCTAs): an OVERLAP plan's network partition
+ * (plan sm[NF_OP_NET]) is only used when max_ctas fits in it, so that
+ * the collective kernels can never occupy the compute or memory partitions.  0 = NCCL default. */
+nf_status nf_comm_create(int32_t tp_size, int32_t tp_rank, const void* id_128, int32_t max_ctas, nf_comm** out);
 /* tp_size communicators of one emulated group living in this process on one
  * GPU (tests, rank-local studies): rank r's calls run on host thread r;
  * collectives meet at a host barrier and exchange device buffers with
- * stream-ordered copies; AllReduce sums in rank order (bit-identical on all
- * ranks).  comms_out: [tp_size]. */
-nf_status nf_comm_create_local(int32_t tp_size, nf_comm** comms_out);
+ * stream-ordered copies.  ar_mode selects the AllReduce arithmetic:
+ *   NF_AR_F32  : sum of the bf16 inputs in fp32 in rank order, one rounding;
+ *   NF_AR_RING : NCCL's ring order with a bf16 rounding after every hop (chunk c of N
+ *                starts at rank (c+1) mod N, adds ranks c+2, ..., c in turn).
+ * Both are bit-identical on all ranks.  comms_out: [tp_size]. */
+enum { NF_AR_F32 = 0, NF_AR_RING = 1 };
+nf_status nf_comm_create_local(int32_t tp_size, int32_t ar_mode, nf_comm** comms_out);
 void nf_comm_destroy(nf_comm* comm);
 
 /* ------------------------------------------------------------------ weights */
@@ -190,13 +207,15 @@ typedef struct {
 } nf_packed_layer;
 nf_status nf_packed_layer_bytes(const nf_model_cfg* cfg, size_t bytes_out[6]);
 nf_status nf_pack_layer(const nf_model_cfg* cfg, const nf_layer_weights* src, const nf_packed_layer* dst, void* stream);
-/* lm_head_packed [V, D] = lm_head * gamma_final (vocab is not sharded in this version). */
+/* Vocab-parallel LM head: lm_head is this rank's vocab shard [V/N, D]
+ * (rows tp_rank*V/N .. +V/N of the full [V, D] head; the full head at tp_size 1);
+ * dst [V/N, D] = lm_head * gamma_final.  NF_EUNSUPPORTED unless (V/N) % 32 == 0. */
 nf_status nf_pack_lm_head(const nf_model_cfg* cfg, const void* lm_head, const void* final_norm, void* dst, void* stream);
 
 typedef struct {
-  const void* embed;               /* [V, D] */
+  const void* embed;               /* [V, D] full, replicated */
   const nf_packed_layer* layers;   /* host array [n_layers] of device pointers */
-  const void* lm_head_packed;      /* [V, D] */
+  const void* lm_head_packed;      /* [V/N, D] this rank's vocab shard (nf_pack_lm_head) */
 } nf_model_weights;
 
 /* ------------------------------------------------------------------ forward */
@@ -216,6 +235,22 @@ nf_status nf_layer_forward(const nf_plan* plan, nf_comm* comm, const nf_packed_l
 nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weights* w, void* const* kv_pools,
                         const nf_batch* b, const int32_t* token_ids, int32_t* next_ids, void* ws, size_t ws_bytes,
                         void* stream);
+/* nf_model_step with optional inspection outputs (parity tests; not on the hot path):
+ *  logits: device bf16 [n_emit, V/N]: this rank's vocab shard of the logits of every emitting
+ *          request's last row (the final-RMSNorm-ed hidden state times the packed LM head), rows in
+ *          caller request order of the emitting requests; NULL = not written.
+ *  hidden: host array [n_layers + 1] of device bf16 [T, D] buffers (or NULL entries):
+ *          hidden[0] = the embedding rows, hidden[l + 1] = decoder layer l's output, rows in caller
+ *          token order; NULL = none written.  Copies are taken as each layer's rows complete.
+ * Writing them does not change next_ids or any other result. */
+typedef struct {
+  int32_t* next_ids;      /* device [n_req] (required) */
+  void* logits;           /* device bf16 [n_emit, V/N] or NULL */
+  void* const* hidden;    /* host [n_layers + 1] of device [T, D] bf16, or NULL */
+} nf_step_outputs;
+nf_status nf_model_step_ex(const nf_plan* plan, nf_comm* comm, const nf_model_weights* w, void* const* kv_pools,
+                           const nf_batch* b, const int32_t* token_ids, const nf_step_outputs* out, void* ws,
+                           size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------ op-level entry points (tests, profiling) */
 /* C[M, N] = A[M, K] . B[N, K]^T, bf16 in/out, f32 accumulation (tcgen05).
@@ -317,7 +352,10 @@ nf_status nf_profile_read(double* ms_out, int64_t* count_out);
 typedef struct {
   int32_t op, stream;
   float start_ms, end_ms;
+  int32_t tag;  /* the launching thread's nf_profile_tag (-1 if none) */
 } nf_span;
+/* Tag the spans recorded from the calling thread (e.g. its rank in an emulated TP group). */
+nf_status nf_profile_tag(int32_t tag);
 /* Copies up to cap spans recorded since the last nf_profile_read (call before it);
  * *n_out = number recorded.  Synchronises the events. */
 nf_status nf_profile_timeline(nf_span* out, int32_t cap, int32_t* n_out);

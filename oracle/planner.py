@@ -30,6 +30,18 @@ moves, deterministic ties) with the readings listed in DESIGN.md
       the shorter result wins, so the search never returns worse than
       sequential (SPEC S:423 upper bound);
   P-7 candidate splits: nano-batch-0 token share s/8, s = 1..7 (2 nano-batches).
+  P-8 tensor parallelism: four KQV/attention nano-batches
+      (quarters Q1..Q4) and two dense nano-batches H1 = Q1+Q2 (column O +
+      AllGathers) and H2 = Q3+Q4 (row O + AllReduce); candidate splits give H1
+      the token share s/8 (s = 1..7), split evenly into its two quarters
+      (shares s, s, 8-s, 8-s).  Collectives are NET nodes whose work is the
+      AllGather-equivalent token count: an AllGather of the group's rows counts
+      its tokens, an AllReduce twice its tokens (a ring AllReduce moves twice
+      the bytes of an AllGather of the same buffer, D = Hq*hd rows here).  The
+      three streams of the executor add order edges: compute (KQV, prefill,
+      O, Up/Gate, Down), memory (decode attention) and network (collectives in
+      the fixed issue order AG_attn(H1), AG_o(H1), AR_o(H2), AR_d(H1),
+      AR_d(H2) per layer, identical on every rank).
 """
 from __future__ import annotations
 
@@ -294,6 +306,77 @@ def search(q_len, kv_prefix, curves: Curves, budget=148, q=8, max_iters=200, n_l
         shares = [s, 8 - s]
         groups = balanced_groups(q_len, kv_prefix, shares)
         nodes = build_pipeline(nano_work(q_len, kv_prefix, groups), n_layers)
+        units, mk, st, en = greedy(nodes, curves, budget, q, max_iters)
+        table.append((shares, units, mk))
+        if best is None or mk < best[2] - 1e-15:
+            best = (shares, units, mk, nodes, st, en)
+    return best, table
+
+
+# ------------------------------------------------------------------ the tensor-parallel pipeline (reading P-8)
+def build_pipeline_tp(work: List[Tuple[int, int, int]], n_layers: int = 3) -> List[Node]:
+    """PAPER.md:547-548 DAG over four quarters (work[q] = (tokens, decode keys,
+    prefill keys)); H1 = quarters 0, 1 (column O + AG), H2 = quarters 2, 3 (row O + AR)."""
+    assert len(work) == 4
+    nodes: List[Node] = []
+
+    def add(kind, nano, w, deps):
+        nodes.append(Node(len(nodes), kind, nano, float(w), [d for d in deps if d is not None]))
+        return nodes[-1].id
+
+    last_c = last_m = last_n = None
+    dec = [None] * 4
+    pf = [None] * 4
+    ready = [None, None]  # per group: the node its next-layer KQV waits for (its AR_d)
+    tok = [work[0][0] + work[1][0], work[2][0] + work[3][0]]
+
+    def front(g):
+        nonlocal last_c, last_m
+        for q in (2 * g, 2 * g + 1):
+            kq = add(KQV, q, work[q][0], [last_c, ready[g]])
+            dec[q] = add(DECODE, q, work[q][1], [kq, last_m])
+            last_m = dec[q]
+            pf[q] = add(PREFILL, q, work[q][2], [kq])
+            last_c = pf[q]
+
+    front(0)
+    front(1)
+    for l in range(n_layers):
+        ag_a = add(NET, 0, tok[0], [dec[0], dec[1], pf[1], last_n])
+        last_n = ag_a
+        o1 = add(O, 0, tok[0], [ag_a, last_c])
+        last_c = o1
+        ag_o = add(NET, 0, tok[0], [o1, last_n])
+        last_n = ag_o
+        o2 = add(O, 1, tok[1], [dec[2], dec[3], last_c])
+        last_c = o2
+        ar_o = add(NET, 1, 2 * tok[1], [o2, last_n])
+        last_n = ar_o
+        ug1 = add(UG, 0, tok[0], [ag_o, last_c])
+        d1 = add(DOWN, 0, tok[0], [ug1])
+        last_c = d1
+        ar_d1 = add(NET, 0, 2 * tok[0], [d1, last_n])
+        last_n = ar_d1
+        ug2 = add(UG, 1, tok[1], [ar_o, last_c])
+        d2 = add(DOWN, 1, tok[1], [ug2])
+        last_c = d2
+        ar_d2 = add(NET, 1, 2 * tok[1], [d2, last_n])
+        last_n = ar_d2
+        ready = [ar_d1, ar_d2]
+        if l + 1 < n_layers:
+            front(0)
+            front(1)
+    return nodes
+
+
+def search_tp(q_len, kv_prefix, curves: Curves, budget=148, q=8, max_iters=200, n_layers=3):
+    """Reading P-8 candidates (H1 share s/8, quarters even); shortest makespan wins."""
+    best = None
+    table = []
+    for s in range(1, 8):
+        shares = [s, s, 8 - s, 8 - s]
+        groups = balanced_groups(q_len, kv_prefix, shares)
+        nodes = build_pipeline_tp(nano_work(q_len, kv_prefix, groups), n_layers)
         units, mk, st, en = greedy(nodes, curves, budget, q, max_iters)
         table.append((shares, units, mk))
         if best is None or mk < best[2] - 1e-15:

@@ -65,7 +65,8 @@ nf_status validate_cfg(const nf_model_cfg* c) {
   if (c->page_size != 16) return set_error(NF_EUNSUPPORTED, "page_size must be 16");
   if (c->d_model % 256) return set_error(NF_EUNSUPPORTED, "d_model must be a multiple of 256");
   if ((c->d_ffn / c->tp_size) % 32) return set_error(NF_EUNSUPPORTED, "d_ffn/tp_size must be a multiple of 32");
-  if (c->vocab % 32) return set_error(NF_EUNSUPPORTED, "vocab must be a multiple of 32");
+  if (c->vocab % c->tp_size) return set_error(NF_EINVAL, "tp_size must divide vocab (vocab-parallel LM head)");
+  if ((c->vocab / c->tp_size) % 32) return set_error(NF_EUNSUPPORTED, "vocab/tp_size must be a multiple of 32");
   if (c->n_q_heads / c->n_kv_heads > 8) return set_error(NF_EUNSUPPORTED, "GQA group > 8 (decode kernel N = 8)");
   if (!(c->rms_eps > 0) || !(c->rope_theta > 1)) return set_error(NF_EINVAL, "bad rms_eps / rope_theta");
   if (c->n_experts < 0) return set_error(NF_EINVAL, "n_experts %d < 0", c->n_experts);
@@ -180,7 +181,7 @@ size_t meta_words_bound(const nf_model_cfg* c, const nf_batch* b) {
     if (b->q_len[r] > 1) pf_tiles += (b->q_len[r] + 63) / 64;
   // (x2 pages and + NF_MAX_NANO requests/tiles: split prefill requests duplicate their page list)
   const int64_t words = 3 * T + 2 * (int64_t)b->page_indptr[b->n_req] + 4 * ((int64_t)b->n_req + NF_MAX_NANO) * kh +
-                        8 * (pf_tiles + NF_MAX_NANO) * qh + 2 * ((int64_t)b->n_req + NF_MAX_NANO) + 64;
+                        8 * (pf_tiles + NF_MAX_NANO) * qh + 3 * ((int64_t)b->n_req + NF_MAX_NANO) + 64;
   return (size_t)words;
 }
 
@@ -286,7 +287,16 @@ void build_meta(const nf_model_cfg* c, const nf_batch* b, const std::vector<int>
   }
   m->n_emit = (int)erow.size();
   m->off_emit_req = m->off_emit_row + erow.size();
-  m->buf.resize(m->off_emit_req + ereq.size());
+  m->off_emit_sorted = m->off_emit_req + ereq.size();
+  std::vector<int32_t> esort(erow.size());
+  {
+    std::vector<int> ix(erow.size());
+    std::iota(ix.begin(), ix.end(), 0);
+    std::stable_sort(ix.begin(), ix.end(), [&](int a, int b2) { return ereq[a] < ereq[b2]; });
+    for (size_t i = 0; i < ix.size(); ++i) esort[i] = erow[ix[i]];
+  }
+  m->buf.resize(m->off_emit_sorted + esort.size());
+  std::memcpy(m->buf.data() + m->off_emit_sorted, esort.data(), esort.size() * 4);
   std::memcpy(m->buf.data(), head.data(), head.size() * 4);
   std::memcpy(m->buf.data() + m->off_dec, dec.data(), dec.size() * sizeof(DecodeItem));
   std::memcpy(m->buf.data() + m->off_pf, pf.data(), pf.size() * sizeof(PrefillItem));
@@ -299,7 +309,7 @@ Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base) 
   const int N = c->tp_size;
   const int64_t qd = (int64_t)c->n_q_heads / N * c->head_dim, D = c->d_model, F = c->d_ffn / N;
   const int64_t NP = D / GEMM_NORM_COLS;
-  const int64_t VT = (c->vocab + GEMM_BN - 1) / GEMM_BN;
+  const int64_t VT = (c->vocab / N + GEMM_BN - 1) / GEMM_BN;
   const int64_t R = b->n_req;
   Workspace w{};
   size_t off = 0;
@@ -326,7 +336,10 @@ Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base) 
   w.am_idx = (int*)take(VT * R * 4);
   w.red = N > 1 ? (float*)take(T * D * 4) : nullptr;
   const int64_t qd_full = (int64_t)c->n_q_heads * c->head_dim;
-  w.ag = N > 1 ? (__nv_bfloat16*)take(T * std::max(qd_full, D) * 2) : nullptr;
+  w.ag = N > 1 ? (__nv_bfloat16*)take(T * qd_full * 2) : nullptr;
+  w.ag2 = N > 1 ? (__nv_bfloat16*)take(T * D * 2) : nullptr;
+  w.am_pair = N > 1 ? (float*)take(R * 8) : nullptr;
+  w.am_pair_all = N > 1 ? (float*)take(R * 8 * N) : nullptr;
   w.ocat = N > 1 ? (__nv_bfloat16*)take(T * qd_full * 2) : nullptr;
   w.hcol = N > 1 ? (__nv_bfloat16*)take(T * (D / N) * 2) : nullptr;
   // stream-K / split-K partial slots: max(148 CTAs, tiles of the largest non-SiLU GEMM)
@@ -459,8 +472,8 @@ nf_status nf_pack_layer(const nf_model_cfg* c, const nf_layer_weights* s, const 
 nf_status nf_pack_lm_head(const nf_model_cfg* c, const void* lm_head, const void* final_norm, void* dst, void* stream) {
   NF_TRY(validate_cfg(c));
   if (!lm_head || !final_norm || !dst) return set_error(NF_EINVAL, "NULL pointer");
-  NF_CUDA(launch_scale_cols((const __nv_bfloat16*)lm_head, (const __nv_bfloat16*)final_norm, c->vocab, c->d_model,
-                            (__nv_bfloat16*)dst, (cudaStream_t)stream));
+  NF_CUDA(launch_scale_cols((const __nv_bfloat16*)lm_head, (const __nv_bfloat16*)final_norm, c->vocab / c->tp_size,
+                            c->d_model, (__nv_bfloat16*)dst, (cudaStream_t)stream));
   return NF_OK;
 }
 
@@ -478,12 +491,20 @@ nf_status nf_plan_create_explicit(const nf_model_cfg* cfg, const nf_plan_spec* s
   for (int o = 0; o < NF_OP_COUNT; ++o)
     if (spec->sm[o] < 1 || spec->sm[o] > 1024) return set_error(NF_EINVAL, "sm[%d] = %d out of range", o, spec->sm[o]);
   if (spec->balance < 0 || spec->balance > 2) return set_error(NF_EINVAL, "balance must be 0, 1 or 2");
+  if (spec->graph < 0 || spec->graph > 1) return set_error(NF_EINVAL, "graph must be 0 or 1");
+  const int nd = spec->n_dense > 0 ? spec->n_dense : spec->n_nano;
+  if (spec->n_dense < 0 || nd > spec->n_nano || spec->n_nano % nd)
+    return set_error(NF_EINVAL, "n_dense %d must divide n_nano %d", spec->n_dense, spec->n_nano);
+  if (cfg->tp_size == 1 && nd != spec->n_nano && spec->mode != NF_SEQUENTIAL)
+    return set_error(NF_EINVAL, "n_dense != n_nano needs tp_size > 1");
   nf_plan* p = new (std::nothrow) nf_plan();
   if (!p) return set_error(NF_ENOMEM, "plan allocation failed");
   p->cfg = *cfg;
   p->spec = *spec;
+  p->spec.n_dense = nd;
   if (spec->mode == NF_SEQUENTIAL) {
     p->spec.n_nano = 1;
+    p->spec.n_dense = 1;
     p->spec.share[0] = 1;
   }
   *out = p;
@@ -509,7 +530,9 @@ nf_status nf_plan_export_csv(const nf_plan* plan, char* buf, size_t cap, size_t*
 
 const char* nf_plan_runtime_note(const nf_plan* p) {
   if (!p) return "";
-  return p->green_note.c_str();
+  nf_plan* q = const_cast<nf_plan*>(p);
+  q->note = q->green_note + (q->spec.graph ? "; CUDA graph: " + q->graph_note : std::string());
+  return q->note.c_str();
 }
 
 void nf_plan_destroy(nf_plan* p) {
@@ -523,6 +546,13 @@ void nf_plan_destroy(nf_plan* p) {
   if (p->net_stream) cudaStreamDestroy(p->net_stream);
   if (p->ev_c2n) cudaEventDestroy(p->ev_c2n);
   if (p->ev_n2c) cudaEventDestroy(p->ev_n2c);
+  for (int k = 0; k < NF_MAX_NANO; ++k)
+    for (cudaEvent_t e : {p->ev_pre[k], p->ev_o[k], p->ev_aro[k], p->ev_d[k], p->ev_ard[k]})
+      if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {p->ev_agattn, p->ev_ago, p->ev_join_n, p->ev_fork, p->ev_join_c, p->ev_join_m})
+    if (e) cudaEventDestroy(e);
+  for (auto& g : p->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   for (int i = 0; i < 2; ++i) {
     if (p->ev_upload[i]) cudaEventDestroy(p->ev_upload[i]);
     if (p->pinned[i]) cudaFreeHost(p->pinned[i]);
@@ -555,6 +585,11 @@ nf_status ensure_runtime(nf_plan* p) {
   NF_CUDA(cudaEventCreateWithFlags(&p->ev_join_m, cudaEventDisableTiming));
   NF_CUDA(cudaEventCreateWithFlags(&p->ev_c2n, cudaEventDisableTiming));
   NF_CUDA(cudaEventCreateWithFlags(&p->ev_n2c, cudaEventDisableTiming));
+  for (int k = 0; k < NF_MAX_NANO; ++k)
+    for (cudaEvent_t* e : {&p->ev_pre[k], &p->ev_o[k], &p->ev_aro[k], &p->ev_d[k], &p->ev_ard[k]})
+      NF_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (cudaEvent_t* e : {&p->ev_agattn, &p->ev_ago, &p->ev_join_n})
+    NF_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) NF_CUDA(cudaEventCreateWithFlags(&p->ev_upload[i], cudaEventDisableTiming));
   return NF_OK;
 }
@@ -986,47 +1021,108 @@ nf_status run_moe_ffn(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat1
   return NF_OK;
 }
 
-// Hand a buffer produced on the compute stream to the network stream and back.
-nf_status to_net(const LayerCtx& L) {
-  if (L.ns == L.cs) return NF_OK;
-  NF_CUDA(cudaEventRecord(L.p->ev_c2n, L.cs));
-  NF_CUDA(cudaStreamWaitEvent(L.ns, L.p->ev_c2n, 0));
-  return NF_OK;
-}
-nf_status from_net(const LayerCtx& L) {
-  if (L.ns == L.cs) return NF_OK;
-  NF_CUDA(cudaEventRecord(L.p->ev_n2c, L.ns));
-  NF_CUDA(cudaStreamWaitEvent(L.cs, L.p->ev_n2c, 0));
+// Record `ev` on `from` and make `to` wait on it (no-op when both are the same stream).
+nf_status edge(cudaEvent_t ev, cudaStream_t from, cudaStream_t to) {
+  if (from == to) return NF_OK;
+  NF_CUDA(cudaEventRecord(ev, from));
+  NF_CUDA(cudaStreamWaitEvent(to, ev, 0));
   return NF_OK;
 }
 
-// Tensor-parallel dense tail of one nano-batch (reading A-12):
-//   col (nano 0): AG(attention out) -> O_col (+ x columns) -> AG -> h1
-//   row (others): O_row partial (+ x on rank 0) -> AR -> h1
-//   then column Up/Gate + SiLU, row Down partial (+ h1 on rank 0) -> AR -> x_out.
-// The row-parallel partials are AllReduced without the residual; one pass then
-// adds the residual in fp32 (one rounding at the residual's magnitude, reading
-// A-12b) and emits the RMS sum-of-squares of h1 / x_out (1 part per row).
-nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, const __nv_bfloat16* x,
-                            const nf_packed_layer* wt, __nv_bfloat16* x_out, float* part_out) {
-  const nf_model_cfg* c = L.c;
-  const int M = nr.t1 - nr.t0;
-  if (M <= 0) return NF_OK;
-  nf_comm* cm = L.comm;
-  const int N = c->tp_size, rank = c->tp_rank;
-  const int64_t D = c->d_model, Fl = c->d_ffn / N, qd = (int64_t)c->n_q_heads / N * c->head_dim;
-  const int64_t qd_full = qd * N, Dl = D / N;
-  const int T = L.m->T;
-  const int stages = L.p->spec.colocate ? 3 : 4;
-  __nv_bfloat16* h1 = L.w->h1 + nr.t0 * D;
-  if (col) {
-    // AG of the attention output rows of this nano-batch, then rank-major -> row-major
-    NF_TRY(to_net(L));
-    {
-      ProfScope ps(NF_OP_NET, L.ns);
-      NF_TRY(comm_all_gather(cm, L.w->o + nr.t0 * qd, L.w->ag, (size_t)M * qd, L.ns));
+// ------------------------------------------------------------------ tensor-parallel pipeline
+// PAPER.md:183, :547-548 and SURVEY.md §8 (a6-a10 DAG).  The n_nano attention
+// nano-batches (KQV, decode/prefill attention) are grouped into n_dense contiguous
+// dense nano-batches ("groups").  Group 0 (H1) runs column-parallel O:
+//   AG(attention out) -> O_col (+ x columns) -> AG -> h1,
+// the other groups (H2) row-parallel O:
+//   O_row partial -> AR -> h1 = x + sum.
+// Every group then runs column Up/Gate + SiLU and a row-parallel Down partial,
+// AR, and x_out = h1 + sum (A-12b: the residual is added after the AllReduce in
+// fp32 with one rounding; one RMS part per row).  Collectives run on the network
+// stream ns; the compute stream cs waits only right before the op that reads a
+// collective's output, so a group's AllGather / AllReduce is in flight while the
+// compute stream runs the other group's GEMMs (O2 under AG_o1, UG1 under AR_o2,
+// D2 under AR_d1, the next layer's KQV under AR_d2).  The host issue order of the
+// collectives is the same on every rank (NCCL's ordering requirement).
+struct Group {
+  NanoRange nr;  // token rows / requests of the group (t0..t1, r0..r1)
+  int k0, k1;    // its attention nano-batches
+  bool col;
+};
+
+std::vector<Group> dense_groups(const nf_plan* p, const StepMeta& m) {
+  const int nn = (int)m.nanos.size();
+  int nd = p->spec.n_dense > 0 ? std::min(p->spec.n_dense, nn) : nn;
+  if (nd < 1 || nn % nd) nd = nn;
+  const int per = nn / nd;
+  std::vector<Group> g(nd);
+  for (int i = 0; i < nd; ++i) {
+    g[i].k0 = i * per;
+    g[i].k1 = (i + 1) * per;
+    g[i].nr = m.nanos[g[i].k0];
+    g[i].nr.r1 = m.nanos[g[i].k1 - 1].r1;
+    g[i].nr.t1 = m.nanos[g[i].k1 - 1].t1;
+    g[i].col = i == 0;
+  }
+  return g;
+}
+
+// Front of a group: KQV of each of its attention nano-batches, decode attention on
+// the memory stream as soon as that KQV lands, prefill attention on the compute stream.
+nf_status tp_front(nf_plan* p, const LayerCtx& L, int gi, const Group& G, const __nv_bfloat16* x, const float* part,
+                   int nparts, const nf_packed_layer* wt, void* pool) {
+  for (int k = G.k0; k < G.k1; ++k) {
+    const NanoRange& nr = L.m->nanos[k];
+    NF_TRY(run_kqv(L, nr, x, part, nparts, wt, pool));
+    if (L.ms != L.cs) {
+      NF_TRY(edge(p->ev_kqv[k], L.cs, L.ms));
+      NF_TRY(run_decode(L, nr, L.ms, 1));
+      NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
+      NF_TRY(run_prefill(L, nr, L.cs));
+      NF_TRY(run_decode(L, nr, L.cs, 2));
+    } else {
+      NF_TRY(run_attn(L, nr, L.cs));
     }
-    NF_TRY(from_net(L));
+  }
+  if (L.ns != L.cs) NF_CUDA(cudaEventRecord(p->ev_pre[gi], L.cs));
+  return NF_OK;
+}
+
+// Make `st` wait for the decode attention of the group's nano-batches (memory stream).
+nf_status wait_attention(nf_plan* p, const LayerCtx& L, const Group& G, cudaStream_t st) {
+  if (L.ms == st) return NF_OK;
+  for (int k = G.k0; k < G.k1; ++k) NF_CUDA(cudaStreamWaitEvent(st, p->ev_att[k], 0));
+  return NF_OK;
+}
+
+// Stage A (column group): AllGather of the group's attention output rows (rank-major).
+nf_status tp_stage_a(nf_plan* p, const LayerCtx& L, int gi, const Group& G) {
+  if (!G.col) return NF_OK;
+  const int M = G.nr.t1 - G.nr.t0;
+  if (M <= 0) return NF_OK;
+  const int64_t qd = (int64_t)L.c->n_q_heads / L.c->tp_size * L.c->head_dim;
+  NF_TRY(wait_attention(p, L, G, L.ns));
+  if (L.ns != L.cs) NF_CUDA(cudaStreamWaitEvent(L.ns, p->ev_pre[gi], 0));
+  {
+    ProfScope ps(NF_OP_NET, L.ns);
+    NF_TRY(comm_all_gather(L.comm, L.w->o + G.nr.t0 * qd, L.w->ag, (size_t)M * qd, L.ns));
+  }
+  if (L.ns != L.cs) NF_CUDA(cudaEventRecord(p->ev_agattn, L.ns));
+  return NF_OK;
+}
+
+// Stage B: O projection and its collective.
+nf_status tp_stage_b(nf_plan* p, const LayerCtx& L, int gi, const Group& G, const __nv_bfloat16* x,
+                     const nf_packed_layer* wt) {
+  const nf_model_cfg* c = L.c;
+  const int M = G.nr.t1 - G.nr.t0;
+  if (M <= 0) return NF_OK;
+  const int N = c->tp_size, rank = c->tp_rank;
+  const int64_t D = c->d_model, qd = (int64_t)c->n_q_heads / N * c->head_dim, qd_full = qd * N, Dl = D / N;
+  const int stages = L.p->spec.colocate ? 3 : 4;
+  __nv_bfloat16* h1 = L.w->h1 + G.nr.t0 * D;
+  if (G.col) {
+    if (L.ns != L.cs) NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_agattn, 0));
     NF_CUDA(launch_interleave(L.w->ag, N, M, (int)qd, L.w->ocat, nullptr, L.cs));
     GemmArgs a{};
     a.epi = EPI_RESID;
@@ -1037,21 +1133,21 @@ nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, co
     a.n_valid = (int)Dl;
     a.out = L.w->hcol;
     a.ldo = Dl;
-    a.resid = x + nr.t0 * D + rank * Dl;
+    a.resid = x + G.nr.t0 * D + rank * Dl;
     a.ldr = D;
     {
       ProfScope ps(NF_OP_O, L.cs);
       NF_CUDA(launch_gemm(L.w->ocat, qd_full, (const __nv_bfloat16*)wt->w_o, qd_full, a,
                           clamp_dense(L, L.p->spec.sm[NF_OP_O]), L.cs));
     }
-    NF_TRY(to_net(L));
+    NF_TRY(edge(p->ev_o[gi], L.cs, L.ns));
     {
       ProfScope ps(NF_OP_NET, L.ns);
-      NF_TRY(comm_all_gather(cm, L.w->hcol, L.w->ag, (size_t)M * Dl, L.ns));
+      NF_TRY(comm_all_gather(L.comm, L.w->hcol, L.w->ag2, (size_t)M * Dl, L.ns));
     }
-    NF_TRY(from_net(L));
-    NF_CUDA(launch_interleave(L.w->ag, N, M, (int)Dl, h1, L.w->part_h1 + nr.t0, L.cs));
+    if (L.ns != L.cs) NF_CUDA(cudaEventRecord(p->ev_ago, L.ns));
   } else {
+    NF_TRY(wait_attention(p, L, G, L.cs));
     GemmArgs a{};
     a.epi = EPI_STORE;
     a.stages = stages;
@@ -1063,78 +1159,118 @@ nf_status run_dense_tail_tp(const LayerCtx& L, const NanoRange& nr, bool col, co
     a.ldo = D;
     {
       ProfScope ps(NF_OP_O, L.cs);
-      NF_CUDA(launch_gemm(L.w->o + nr.t0 * qd, qd, (const __nv_bfloat16*)wt->w_o_row, qd, a,
+      NF_CUDA(launch_gemm(L.w->o + G.nr.t0 * qd, qd, (const __nv_bfloat16*)wt->w_o_row, qd, a,
                           clamp_dense(L, L.p->spec.sm[NF_OP_O]), L.cs));
     }
-    NF_TRY(to_net(L));
+    NF_TRY(edge(p->ev_o[gi], L.cs, L.ns));
     {
       ProfScope ps(NF_OP_NET, L.ns);
-      NF_TRY(comm_all_reduce_bf16(cm, h1, (size_t)M * D, L.ns, L.w->red));
+      NF_TRY(comm_all_reduce_bf16(L.comm, h1, (size_t)M * D, L.ns, L.w->red));
     }
-    NF_TRY(from_net(L));
-    NF_CUDA(launch_resid_add_rows(h1, x + nr.t0 * D, M, (int)D, L.w->part_h1 + nr.t0, L.cs));
+    if (L.ns != L.cs) NF_CUDA(cudaEventRecord(p->ev_aro[gi], L.ns));
   }
-  if (c->n_experts > 0) {
-    // MoE: every expert's F columns are split across ranks; this rank's weighted partial
-    // sum -> AR -> x_out = h1 + sum (A-12b rounding)
-    NF_TRY(run_moe_ffn(L, nr, L.w->h1, wt, nullptr, x_out, nullptr));
-  } else {
-  // column-parallel Up/Gate + SiLU with the RMSNorm(h1) row scale (one partial per row)
-  GemmArgs u{};
-  u.epi = EPI_SILU;
-  u.stages = stages;
-  u.M = M;
-  u.N = (int)(((Fl + 127) / 128) * 256);
-  u.K = (int)D;
-  u.n_valid = (int)Fl;
-  u.out = L.w->m + nr.t0 * Fl;
-  u.ldo = Fl;
-  u.norm_part = L.w->part_h1 + nr.t0;
-  u.norm_nparts = 1;
-  u.norm_stride = T;
-  u.inv_d = 1.f / D;
-  u.eps = c->rms_eps;
-  {
-    ProfScope ps(NF_OP_UG, L.cs);
-    NF_CUDA(launch_gemm(h1, D, (const __nv_bfloat16*)wt->w_gate_up, D, u, clamp_dense(L, L.p->spec.sm[NF_OP_UG]), L.cs));
-  }
-  // row-parallel Down partial -> AR -> x_out = h1 + sum
-  GemmArgs d{};
-  d.epi = EPI_STORE;
-  d.stages = stages;
-  d.M = M;
-  d.N = (int)D;
-  d.K = (int)Fl;
-  d.n_valid = (int)D;
-  d.out = x_out + nr.t0 * D;
-  d.ldo = D;
-  {
-    ProfScope ps(NF_OP_DOWN, L.cs);
-    NF_CUDA(launch_gemm(L.w->m + nr.t0 * Fl, Fl, (const __nv_bfloat16*)wt->w_down, Fl, d,
-                        clamp_dense(L, L.p->spec.sm[NF_OP_DOWN]), L.cs));
-  }
-  }
-  NF_TRY(to_net(L));
-  {
-    ProfScope ps(NF_OP_NET, L.ns);
-    NF_TRY(comm_all_reduce_bf16(cm, x_out + nr.t0 * D, (size_t)M * D, L.ns, L.w->red));
-  }
-  NF_TRY(from_net(L));
-  NF_CUDA(launch_resid_add_rows(x_out + nr.t0 * D, h1, M, (int)D, part_out ? part_out + nr.t0 : nullptr, L.cs));
   return NF_OK;
 }
 
-nf_status run_tail(const LayerCtx& L, size_t k, const NanoRange& nr, const __nv_bfloat16* x, const nf_packed_layer* wt,
-                   __nv_bfloat16* x_out, float* part_out) {
-  if (L.c->tp_size > 1) return run_dense_tail_tp(L, nr, k == 0, x, wt, x_out, part_out);
-  return run_dense_tail(L, nr, x, wt, x_out, part_out);
+// Stage C: h1 (+ its RMS statistics), Up/Gate + SiLU, row-parallel Down partial, AR.
+nf_status tp_stage_c(nf_plan* p, const LayerCtx& L, int gi, const Group& G, const __nv_bfloat16* x,
+                     const nf_packed_layer* wt, __nv_bfloat16* x_out) {
+  const nf_model_cfg* c = L.c;
+  const int M = G.nr.t1 - G.nr.t0;
+  if (M <= 0) return NF_OK;
+  const int N = c->tp_size;
+  const int64_t D = c->d_model, Fl = c->d_ffn / N, Dl = D / N;
+  const int T = L.m->T;
+  const int stages = L.p->spec.colocate ? 3 : 4;
+  __nv_bfloat16* h1 = L.w->h1 + G.nr.t0 * D;
+  if (G.col) {
+    if (L.ns != L.cs) NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_ago, 0));
+    NF_CUDA(launch_interleave(L.w->ag2, N, M, (int)Dl, h1, L.w->part_h1 + G.nr.t0, L.cs));
+  } else {
+    if (L.ns != L.cs) NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_aro[gi], 0));
+    NF_CUDA(launch_resid_add_rows(h1, x + G.nr.t0 * D, M, (int)D, L.w->part_h1 + G.nr.t0, L.cs));
+  }
+  if (c->n_experts > 0) {
+    // MoE: every expert's F columns are split across ranks; this rank's weighted partial sum
+    NF_TRY(run_moe_ffn(L, G.nr, L.w->h1, wt, nullptr, x_out, nullptr));
+  } else {
+    GemmArgs u{};
+    u.epi = EPI_SILU;
+    u.stages = stages;
+    u.M = M;
+    u.N = (int)(((Fl + 127) / 128) * 256);
+    u.K = (int)D;
+    u.n_valid = (int)Fl;
+    u.out = L.w->m + G.nr.t0 * Fl;
+    u.ldo = Fl;
+    u.norm_part = L.w->part_h1 + G.nr.t0;
+    u.norm_nparts = 1;
+    u.norm_stride = T;
+    u.inv_d = 1.f / D;
+    u.eps = c->rms_eps;
+    {
+      ProfScope ps(NF_OP_UG, L.cs);
+      NF_CUDA(launch_gemm(h1, D, (const __nv_bfloat16*)wt->w_gate_up, D, u, clamp_dense(L, L.p->spec.sm[NF_OP_UG]), L.cs));
+    }
+    GemmArgs d{};
+    d.epi = EPI_STORE;
+    d.stages = stages;
+    d.M = M;
+    d.N = (int)D;
+    d.K = (int)Fl;
+    d.n_valid = (int)D;
+    d.out = x_out + G.nr.t0 * D;
+    d.ldo = D;
+    {
+      ProfScope ps(NF_OP_DOWN, L.cs);
+      NF_CUDA(launch_gemm(L.w->m + G.nr.t0 * Fl, Fl, (const __nv_bfloat16*)wt->w_down, Fl, d,
+                          clamp_dense(L, L.p->spec.sm[NF_OP_DOWN]), L.cs));
+    }
+  }
+  NF_TRY(edge(p->ev_d[gi], L.cs, L.ns));
+  {
+    ProfScope ps(NF_OP_NET, L.ns);
+    NF_TRY(comm_all_reduce_bf16(L.comm, x_out + G.nr.t0 * D, (size_t)M * D, L.ns, L.w->red));
+  }
+  if (L.ns != L.cs) NF_CUDA(cudaEventRecord(p->ev_ard[gi], L.ns));
+  return NF_OK;
+}
+
+// Stage D: x_out = h1 + AR(Down partials), RMS statistics of x_out for the next layer.
+nf_status tp_stage_d(nf_plan* p, const LayerCtx& L, int gi, const Group& G, __nv_bfloat16* x_out, float* part_out) {
+  const int M = G.nr.t1 - G.nr.t0;
+  if (M <= 0) return NF_OK;
+  const int64_t D = L.c->d_model;
+  if (L.ns != L.cs) NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_ard[gi], 0));
+  NF_CUDA(launch_resid_add_rows(x_out + G.nr.t0 * D, L.w->h1 + G.nr.t0 * D, M, (int)D,
+                                part_out ? part_out + G.nr.t0 : nullptr, L.cs));
+  return NF_OK;
+}
+
+// Optional inspection copy (nf_model_step_ex hidden taps): rows [t0, t1) of an internal-order
+// buffer to their caller rows.
+nf_status tap_rows(const LayerCtx& L, void* dst, const __nv_bfloat16* src, int t0, int t1) {
+  if (!dst || t1 <= t0) return NF_OK;
+  const int D = L.c->d_model;
+  NF_CUDA(launch_scatter_rows(src + (int64_t)t0 * D, L.meta_dev + L.m->off_tok_src + t0, t1 - t0, D,
+                              (__nv_bfloat16*)dst, L.cs));
+  return NF_OK;
 }
 
 // OVERLAP plans run on green-context partitions when available: fork the
-// caller stream into the compute / memory partition streams, join at the end.
+// caller stream into the compute / memory (/ network) partition streams, join at the end.
 nf_status enter_partitions(nf_plan* p, LayerCtx* L, cudaStream_t caller) {
   if (p->spec.mode != NF_OVERLAP || p->spec.colocate) return NF_OK;
-  if (!green_setup(p, p->spec.sm[NF_OP_DECODE_ATTN])) return NF_OK;
+  // TP: a network partition only for collectives whose CTA count is known to fit it
+  // (an emulated group, or NCCL capped to <= the partition); otherwise NCCL stays on
+  // an ordinary stream (it could otherwise wait for SMs held by a co-partitioned kernel).
+  int net = 0;
+  if (p->cfg.tp_size > 1 && L->comm) {
+    const int want = p->spec.sm[NF_OP_NET];
+    const int cap = comm_max_ctas(L->comm);
+    if (comm_emulated(L->comm) || (cap > 0 && cap <= (want + 7) / 8 * 8)) net = want;
+  }
+  if (!green_setup(p, p->spec.sm[NF_OP_DECODE_ATTN], net)) return NF_OK;
   NF_CUDA(cudaEventRecord(p->ev_fork, caller));
   NF_CUDA(cudaStreamWaitEvent(p->green_cs, p->ev_fork, 0));
   NF_CUDA(cudaStreamWaitEvent(p->green_ms, p->ev_fork, 0));
@@ -1142,40 +1278,73 @@ nf_status enter_partitions(nf_plan* p, LayerCtx* L, cudaStream_t caller) {
   L->ms = p->green_ms;
   L->cap_dense = p->green_dense_sms;
   L->cap_dec = p->green_dec_sms;
+  if (p->green_ns && L->ns != caller) {
+    NF_CUDA(cudaStreamWaitEvent(p->green_ns, p->ev_fork, 0));
+    L->ns = p->green_ns;
+  }
   return NF_OK;
 }
 nf_status leave_partitions(nf_plan* p, const LayerCtx& L, cudaStream_t caller) {
-  if (L.cs == caller) return NF_OK;
-  NF_CUDA(cudaEventRecord(p->ev_join_c, L.cs));
-  NF_CUDA(cudaEventRecord(p->ev_join_m, L.ms));
-  NF_CUDA(cudaStreamWaitEvent(caller, p->ev_join_c, 0));
-  NF_CUDA(cudaStreamWaitEvent(caller, p->ev_join_m, 0));
+  if (L.cs != caller) {
+    NF_CUDA(cudaEventRecord(p->ev_join_c, L.cs));
+    NF_CUDA(cudaStreamWaitEvent(caller, p->ev_join_c, 0));
+  }
+  if (L.ms != caller && L.ms != L.cs) {
+    NF_CUDA(cudaEventRecord(p->ev_join_m, L.ms));
+    NF_CUDA(cudaStreamWaitEvent(caller, p->ev_join_m, 0));
+  }
+  if (L.ns != caller && L.ns != L.cs) {
+    NF_CUDA(cudaEventRecord(p->ev_join_n, L.ns));
+    NF_CUDA(cudaStreamWaitEvent(caller, p->ev_join_n, 0));
+  }
   return NF_OK;
 }
 
 }  // namespace
 
 // One layer with the plan's pipeline.  x/part: input + its RMS partials (nparts),
-// x_out/part_out: output + partials for the next layer.  first/last control the
-// cross-layer overlap bookkeeping in model steps (KQV of layer l+1 issued early).
+// x_out/part_out: output + partials for the next layer.
 nf_status run_layer(nf_plan* p, const LayerCtx& L, const nf_packed_layer* wt, void* pool, const __nv_bfloat16* x,
-                    const float* part, int nparts, __nv_bfloat16* x_out, float* part_out, bool kqv_done) {
+                    const float* part, int nparts, __nv_bfloat16* x_out, float* part_out, void* tap) {
   const auto& nanos = L.m->nanos;
   const int mode = p->spec.mode;
+  if (L.c->tp_size > 1) {
+    const auto groups = dense_groups(p, *L.m);
+    if (mode != NF_OVERLAP) {
+      for (size_t g = 0; g < groups.size(); ++g) {
+        NF_TRY(tp_front(p, L, (int)g, groups[g], x, part, nparts, wt, pool));
+        NF_TRY(tp_stage_a(p, L, (int)g, groups[g]));
+        NF_TRY(tp_stage_b(p, L, (int)g, groups[g], x, wt));
+        NF_TRY(tp_stage_c(p, L, (int)g, groups[g], x, wt, x_out));
+        NF_TRY(tp_stage_d(p, L, (int)g, groups[g], x_out, part_out));
+        NF_TRY(tap_rows(L, tap, x_out, groups[g].nr.t0, groups[g].nr.t1));
+      }
+      return NF_OK;
+    }
+    for (size_t g = 0; g < groups.size(); ++g) NF_TRY(tp_front(p, L, (int)g, groups[g], x, part, nparts, wt, pool));
+    NF_TRY(tp_stage_a(p, L, 0, groups[0]));
+    for (size_t g = 0; g < groups.size(); ++g) NF_TRY(tp_stage_b(p, L, (int)g, groups[g], x, wt));
+    for (size_t g = 0; g < groups.size(); ++g) NF_TRY(tp_stage_c(p, L, (int)g, groups[g], x, wt, x_out));
+    for (size_t g = 0; g < groups.size(); ++g) {
+      NF_TRY(tp_stage_d(p, L, (int)g, groups[g], x_out, part_out));
+      NF_TRY(tap_rows(L, tap, x_out, groups[g].nr.t0, groups[g].nr.t1));
+    }
+    return NF_OK;
+  }
   if (mode != NF_OVERLAP) {
     for (size_t k = 0; k < nanos.size(); ++k) {
-      if (!kqv_done) NF_TRY(run_kqv(L, nanos[k], x, part, nparts, wt, pool));
+      NF_TRY(run_kqv(L, nanos[k], x, part, nparts, wt, pool));
       NF_TRY(run_attn(L, nanos[k], L.cs));
-      NF_TRY(run_tail(L, k, nanos[k], x, wt, x_out, part_out));
+      NF_TRY(run_dense_tail(L, nanos[k], x, wt, x_out, part_out));
+      NF_TRY(tap_rows(L, tap, x_out, nanos[k].t0, nanos[k].t1));
     }
     return NF_OK;
   }
   // OVERLAP: KQV of every nano first, attention on the memory stream as soon as
   // its KQV lands, then the dense tail of each nano after its attention.
   for (size_t k = 0; k < nanos.size(); ++k) {
-    if (!kqv_done) NF_TRY(run_kqv(L, nanos[k], x, part, nparts, wt, pool));
-    NF_CUDA(cudaEventRecord(p->ev_kqv[k], L.cs));
-    NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
+    NF_TRY(run_kqv(L, nanos[k], x, part, nparts, wt, pool));
+    NF_TRY(edge(p->ev_kqv[k], L.cs, L.ms));
     NF_TRY(run_decode(L, nanos[k], L.ms, 1));
     NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
     NF_TRY(run_prefill(L, nanos[k], L.cs));
@@ -1183,10 +1352,280 @@ nf_status run_layer(nf_plan* p, const LayerCtx& L, const nf_packed_layer* wt, vo
   }
   for (size_t k = 0; k < nanos.size(); ++k) {
     NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_att[k], 0));
-    NF_TRY(run_tail(L, k, nanos[k], x, wt, x_out, part_out));
+    NF_TRY(run_dense_tail(L, nanos[k], x, wt, x_out, part_out));
+    NF_TRY(tap_rows(L, tap, x_out, nanos[k].t0, nanos[k].t1));
   }
   return NF_OK;
 }
+
+namespace {
+
+nf_status check_comm(const nf_model_cfg* c, nf_comm* comm) {
+  if (c->tp_size == 1) return NF_OK;
+  if (!comm) return set_error(NF_EINVAL, "tp_size > 1 needs a communicator");
+  if (comm_size(comm) != c->tp_size || comm_rank(comm) != c->tp_rank)
+    return set_error(NF_EINVAL, "communicator size/rank %d/%d != cfg %d/%d", comm_size(comm), comm_rank(comm),
+                     c->tp_size, c->tp_rank);
+  return NF_OK;
+}
+
+// The launches of one model step after the metadata upload (captured into a CUDA
+// graph when the plan asks for it).
+nf_status model_step_launches(nf_plan* p, nf_comm* comm, const nf_model_weights* w, void* const* kv_pools,
+                              const nf_batch* b, const int32_t* token_ids, const nf_step_outputs* out,
+                              const StepMeta& m, const Workspace& wsp, cudaStream_t cs) {
+  const nf_model_cfg* c = &p->cfg;
+  NF_CUDA(cudaMemsetAsync(wsp.sk_flag, 0, (size_t)wsp.sk_flag_n * 4, cs));
+  const int D = c->d_model;
+  const int NP = D / GEMM_NORM_COLS;
+  void* const* taps = out->hidden;
+  // token ids in internal row order: the embedding gather reads token_ids[tok_src[row]]
+  // (+ RMS partials, one part); ids outside [0, V) are clamped (documented in nf.h)
+  NF_CUDA(launch_gather_ids_embed((const __nv_bfloat16*)w->embed, token_ids, wsp.meta + m.off_tok_src, m.T, D,
+                                  c->vocab, wsp.xa, wsp.part_a, cs));
+  LayerCtx L{};
+  L.p = p;
+  L.c = c;
+  L.m = &m;
+  L.w = &wsp;
+  L.meta_dev = wsp.meta;
+  L.cs = cs;
+  L.ms = p->spec.mode == NF_OVERLAP ? p->mem_stream : cs;
+  L.ns = (p->spec.mode == NF_OVERLAP && c->tp_size > 1) ? p->net_stream : cs;
+  L.comm = comm;
+  if (taps && taps[0]) NF_TRY(tap_rows(L, taps[0], wsp.xa, 0, m.T));
+  const int NPn = c->tp_size > 1 ? 1 : NP;  // RMS partials per row of layer outputs
+  __nv_bfloat16 *x = wsp.xa, *y = wsp.xb;
+  float *px = wsp.part_a, *py = wsp.part_b;
+  std::vector<CUtensorMap> maps(c->n_layers), pmaps(c->n_layers);
+  for (int l = 0; l < c->n_layers; ++l) {
+    NF_CUDA(make_pool_tmap(&maps[l], kv_pools[l], b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim,
+                           c->page_size));
+    NF_CUDA(make_page_tmap(&pmaps[l], kv_pools[l], b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim,
+                           c->page_size));
+  }
+  NF_TRY(enter_partitions(p, &L, cs));
+  auto tap_of = [&](int l) -> void* { return taps ? taps[l + 1] : nullptr; };
+  if (p->spec.mode != NF_OVERLAP) {
+    int nparts = 1;
+    for (int l = 0; l < c->n_layers; ++l) {
+      L.pool_map = maps[l];
+      L.page_map = pmaps[l];
+      NF_TRY(run_layer(p, L, &w->layers[l], kv_pools[l], x, px, nparts, y, py, tap_of(l)));
+      std::swap(x, y);
+      std::swap(px, py);
+      nparts = NPn;
+    }
+  } else if (c->tp_size > 1) {
+    // TP operation-level pipeline across layers: layer l+1's
+    // KQV of a group is issued right after that group's layer-l output is complete.
+    const auto groups = dense_groups(p, m);
+    const int G = (int)groups.size();
+    L.pool_map = maps[0];
+    L.page_map = pmaps[0];
+    for (int g = 0; g < G; ++g) NF_TRY(tp_front(p, L, g, groups[g], x, px, 1, &w->layers[0], kv_pools[0]));
+    for (int l = 0; l < c->n_layers; ++l) {
+      const nf_packed_layer* wt = &w->layers[l];
+      NF_TRY(tp_stage_a(p, L, 0, groups[0]));
+      for (int g = 0; g < G; ++g) NF_TRY(tp_stage_b(p, L, g, groups[g], x, wt));
+      for (int g = 0; g < G; ++g) NF_TRY(tp_stage_c(p, L, g, groups[g], x, wt, y));
+      for (int g = 0; g < G; ++g) {
+        NF_TRY(tp_stage_d(p, L, g, groups[g], y, py));
+        NF_TRY(tap_rows(L, tap_of(l), y, groups[g].nr.t0, groups[g].nr.t1));
+        if (l + 1 < c->n_layers) {
+          L.pool_map = maps[l + 1];
+          L.page_map = pmaps[l + 1];
+          NF_TRY(tp_front(p, L, g, groups[g], y, py, 1, &w->layers[l + 1], kv_pools[l + 1]));
+        }
+      }
+      std::swap(x, y);
+      std::swap(px, py);
+    }
+  } else {
+    // Operation-level pipeline across layers (PAPER.md:547, single-GPU variant
+    // PAPER.md:691): the compute stream runs, per nano-batch k, O_k UG_k D_k of
+    // layer l then KQV_k of layer l+1; the memory stream runs ATT_k(l+1) as
+    // soon as KQV_k(l+1) lands, overlapping the other nano-batches' dense ops.
+    const auto& nanos = m.nanos;
+    L.pool_map = maps[0];
+    L.page_map = pmaps[0];
+    for (size_t k = 0; k < nanos.size(); ++k) {
+      NF_TRY(run_kqv(L, nanos[k], x, px, 1, &w->layers[0], kv_pools[0]));
+      NF_TRY(edge(p->ev_kqv[k], L.cs, L.ms));
+      NF_TRY(run_decode(L, nanos[k], L.ms, 1));
+      NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
+      NF_TRY(run_prefill(L, nanos[k], L.cs));
+      NF_TRY(run_decode(L, nanos[k], L.cs, 2));
+    }
+    for (int l = 0; l < c->n_layers; ++l) {
+      for (size_t k = 0; k < nanos.size(); ++k) {
+        NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_att[k], 0));
+        NF_TRY(run_dense_tail(L, nanos[k], x, &w->layers[l], y, py));
+        NF_TRY(tap_rows(L, tap_of(l), y, nanos[k].t0, nanos[k].t1));
+        if (l + 1 < c->n_layers) {
+          L.pool_map = maps[l + 1];
+          L.page_map = pmaps[l + 1];
+          NF_TRY(run_kqv(L, nanos[k], y, py, NPn, &w->layers[l + 1], kv_pools[l + 1]));
+          NF_TRY(edge(p->ev_kqv[k], L.cs, L.ms));
+          NF_TRY(run_decode(L, nanos[k], L.ms, 1));
+          NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
+          NF_TRY(run_prefill(L, nanos[k], L.cs));
+          NF_TRY(run_decode(L, nanos[k], L.cs, 2));
+        }
+      }
+      std::swap(x, y);
+      std::swap(px, py);
+    }
+  }
+  NF_TRY(leave_partitions(p, L, cs));
+  // final RMSNorm (gamma folded into lm_head_packed) + LM head over this rank's vocab
+  // shard + argmax; at TP > 1 the per-rank (max, global index) pairs are AllGathered and
+  // merged
+  int32_t* next_ids = out->next_ids;
+  NF_CUDA(launch_fill_i32(next_ids, b->n_req, -1, cs));
+  const int Vl = c->vocab / c->tp_size;
+  if (m.n_emit > 0) {
+    const int* erow = wsp.meta + m.off_emit_row;
+    NF_CUDA(launch_gather_rows(x, erow, m.n_emit, D, wsp.lm_rows, wsp.lm_part, cs));
+    GemmArgs a{};
+    a.epi = EPI_ARGMAX;
+    a.sk_part = wsp.sk_part;
+    a.sk_slots = wsp.sk_slots;
+    a.sk_flag = wsp.sk_flag;
+    a.M = m.n_emit;
+    a.N = Vl;
+    a.K = D;
+    a.n_valid = Vl;
+    a.am_val = wsp.am_val;
+    a.am_idx = wsp.am_idx;
+    a.am_stride = m.n_emit;
+    {
+      ProfScope ps(NF_PROF_LMHEAD, cs);
+      NF_CUDA(launch_gemm(wsp.lm_rows, D, (const __nv_bfloat16*)w->lm_head_packed, D, a, num_sms(), cs));
+    }
+    const int vt = (Vl + GEMM_BN - 1) / GEMM_BN;
+    if (c->tp_size == 1) {
+      NF_CUDA(launch_argmax_reduce(wsp.am_val, wsp.am_idx, vt, m.n_emit, m.n_emit, wsp.meta + m.off_emit_req, next_ids,
+                                   cs));
+    } else {
+      NF_CUDA(launch_argmax_pairs(wsp.am_val, wsp.am_idx, vt, m.n_emit, m.n_emit, c->tp_rank * Vl, wsp.am_pair, cs));
+      {
+        ProfScope ps(NF_OP_NET, cs);
+        NF_TRY(comm_all_gather(comm, wsp.am_pair, wsp.am_pair_all, (size_t)m.n_emit * 4, cs));
+      }
+      NF_CUDA(launch_argmax_merge(wsp.am_pair_all, c->tp_size, m.n_emit, wsp.meta + m.off_emit_req, next_ids, cs));
+    }
+    if (out->logits) {
+      // inspection: logits of the emitting rows in caller request order (plain store epilogue)
+      NF_CUDA(launch_gather_rows(x, wsp.meta + m.off_emit_sorted, m.n_emit, D, wsp.lm_rows, nullptr, cs));
+      GemmArgs s{};
+      s.epi = EPI_STORE;
+      s.M = m.n_emit;
+      s.N = Vl;
+      s.K = D;
+      s.n_valid = Vl;
+      s.out = (__nv_bfloat16*)out->logits;
+      s.ldo = Vl;
+      NF_CUDA(launch_gemm(wsp.lm_rows, D, (const __nv_bfloat16*)w->lm_head_packed, D, s, num_sms(), cs));
+    }
+  }
+  // join the memory and network streams when the plan forked onto them
+  if (L.ms != cs && L.ms == p->mem_stream) {
+    NF_CUDA(cudaEventRecord(p->ev_join, p->mem_stream));
+    NF_CUDA(cudaStreamWaitEvent(cs, p->ev_join, 0));
+  }
+  if (L.ns != cs && L.ns == p->net_stream) {
+    NF_CUDA(cudaEventRecord(p->ev_join_n, p->net_stream));
+    NF_CUDA(cudaStreamWaitEvent(cs, p->ev_join_n, 0));
+  }
+  return NF_OK;
+}
+
+// Launch-structure key of a model step: everything the captured kernels' parameters
+// depend on besides the uploaded metadata contents.
+std::vector<int64_t> graph_key(const nf_plan* p, nf_comm* comm, const nf_model_weights* w, void* const* kv_pools,
+                               const nf_batch* b, const int32_t* token_ids, const nf_step_outputs* out,
+                               const StepMeta& m, void* ws, cudaStream_t cs) {
+  std::vector<int64_t> k{(int64_t)(uintptr_t)comm, (int64_t)(uintptr_t)w->embed, (int64_t)(uintptr_t)w->lm_head_packed,
+                         (int64_t)(uintptr_t)token_ids, (int64_t)(uintptr_t)out->next_ids, (int64_t)(uintptr_t)ws,
+                         (int64_t)(uintptr_t)cs, b->n_req, b->n_pages_pool, m.T, m.n_emit,
+                         (int64_t)m.off_pos, (int64_t)m.off_slot, (int64_t)m.off_pages, (int64_t)m.off_dec,
+                         (int64_t)m.off_pf, (int64_t)m.off_emit_row, (int64_t)m.off_emit_req,
+                         (int64_t)m.off_tok_src, (int64_t)m.off_emit_sorted};
+  for (const auto& nr : m.nanos)
+    for (int v : {nr.r0, nr.r1, nr.t0, nr.t1, nr.dec_off, nr.dec_n, nr.dec_cs_n, nr.pf_off, nr.pf_n}) k.push_back(v);
+  for (int l = 0; l < p->cfg.n_layers; ++l) {
+    k.push_back((int64_t)(uintptr_t)kv_pools[l]);
+    const nf_packed_layer& q = w->layers[l];
+    for (const void* ptr : {q.w_qkv, q.w_o, q.w_o_row, q.w_gate_up, q.w_down, q.w_router})
+      k.push_back((int64_t)(uintptr_t)ptr);
+  }
+  return k;
+}
+
+nf_status model_step_impl(const nf_plan* plan, nf_comm* comm, const nf_model_weights* w, void* const* kv_pools,
+                          const nf_batch* b, const int32_t* token_ids, const nf_step_outputs* out, void* ws,
+                          size_t ws_bytes, void* stream) {
+  if (!plan) return set_error(NF_EINVAL, "plan is NULL");
+  nf_plan* p = const_cast<nf_plan*>(plan);
+  const nf_model_cfg* c = &p->cfg;
+  NF_TRY(validate_batch(c, b));
+  NF_TRY(check_comm(c, comm));
+  if (!w || !w->embed || !w->layers || !w->lm_head_packed || !kv_pools || !token_ids || !out || !out->next_ids || !ws)
+    return set_error(NF_EINVAL, "NULL pointer argument");
+  for (int l = 0; l < c->n_layers; ++l)
+    if (!kv_pools[l]) return set_error(NF_EINVAL, "kv_pools[%d] is NULL", l);
+  for (int l = 0; l < c->n_layers; ++l) NF_TRY(validate_packed(c, &w->layers[l], l));
+  Workspace wsp = carve_workspace(c, b, ws);
+  if (ws_bytes < wsp.total) return set_error(NF_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, wsp.total);
+  NF_TRY(ensure_runtime(p));
+  std::vector<int> order, cuts;
+  BatchView view;
+  bool use_view = false;
+  plan_order(p, b, true, &order, &cuts, &view, &use_view);
+  StepMeta m;
+  if (use_view)
+    build_meta(c, &view.b, order, cuts, &m, &view.caller_row0, &view.caller_req);
+  else
+    build_meta(c, b, order, cuts, &m);
+  cudaStream_t cs = (cudaStream_t)stream;
+  NF_TRY(upload_meta(p, m, wsp.meta, cs));
+  // CUDA graph (plan spec.graph): not with an emulated group (host barriers inside the
+  // collectives), inspection outputs or per-launch profiling
+  const bool want_graph = p->spec.graph && !comm_emulated(comm) && !out->logits && !out->hidden && !profile_active();
+  if (!want_graph) return model_step_launches(p, comm, w, kv_pools, b, token_ids, out, m, wsp, cs);
+  std::vector<int64_t> key = graph_key(p, comm, w, kv_pools, b, token_ids, out, m, ws, cs);
+  for (auto& g : p->graphs)
+    if (g.key == key) {
+      NF_CUDA(cudaGraphLaunch(g.exec, cs));
+      count_launch(1);
+      return NF_OK;
+    }
+  NF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  const nf_status st = model_step_launches(p, comm, w, kv_pools, b, token_ids, out, m, wsp, cs);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+  if (st != NF_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (ce != cudaSuccess) return set_error(NF_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(ce));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) return set_error(NF_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ie));
+  if (p->graphs.size() >= 4) {
+    cudaGraphExecDestroy(p->graphs.front().exec);
+    p->graphs.erase(p->graphs.begin());
+  }
+  p->graphs.push_back(NfGraph{std::move(key), exec});
+  p->graph_note = "captured " + std::to_string(p->graphs.size()) + " graph(s)";
+  NF_CUDA(cudaGraphLaunch(exec, cs));
+  count_launch(1);
+  return NF_OK;
+}
+
+}  // namespace
 
 }  // namespace nf
 
@@ -1198,12 +1637,7 @@ nf_status nf_layer_forward(const nf_plan* plan, nf_comm* comm, const nf_packed_l
   nf_plan* p = const_cast<nf_plan*>(plan);
   const nf_model_cfg* c = &p->cfg;
   NF_TRY(validate_batch(c, b));
-  if (c->tp_size > 1) {
-    if (!comm) return set_error(NF_EINVAL, "tp_size > 1 needs a communicator");
-    if (comm_size(comm) != c->tp_size || comm_rank(comm) != c->tp_rank)
-      return set_error(NF_EINVAL, "communicator size/rank %d/%d != cfg %d/%d", comm_size(comm), comm_rank(comm),
-                       c->tp_size, c->tp_rank);
-  }
+  NF_TRY(check_comm(c, comm));
   if (!w || !kv_pool || !x_in || !x_out || !ws) return set_error(NF_EINVAL, "NULL pointer argument");
   NF_TRY(validate_packed(c, w, 0));
   Workspace wsp = carve_workspace(c, b, ws);
@@ -1223,155 +1657,38 @@ nf_status nf_layer_forward(const nf_plan* plan, nf_comm* comm, const nf_packed_l
   L.w = &wsp;
   L.meta_dev = wsp.meta;
   L.cs = cs;
-  L.ms = p->mem_stream;
-  L.ns = p->spec.mode == NF_OVERLAP ? p->net_stream : cs;
+  L.ms = p->spec.mode == NF_OVERLAP ? p->mem_stream : cs;
+  L.ns = (p->spec.mode == NF_OVERLAP && c->tp_size > 1) ? p->net_stream : cs;
   L.comm = comm;
   NF_CUDA(make_pool_tmap(&L.pool_map, kv_pool, b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim, c->page_size));
   NF_CUDA(make_page_tmap(&L.page_map, kv_pool, b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim, c->page_size));
   // RMS partials of x_in (one part per row)
   NF_CUDA(launch_gather_rows((const __nv_bfloat16*)x_in, nullptr, m.T, c->d_model, nullptr, wsp.part_a, cs));
   NF_TRY(enter_partitions(p, &L, cs));
-  NF_TRY(run_layer(p, L, w, kv_pool, (const __nv_bfloat16*)x_in, wsp.part_a, 1, (__nv_bfloat16*)x_out, nullptr, false));
+  NF_TRY(run_layer(p, L, w, kv_pool, (const __nv_bfloat16*)x_in, wsp.part_a, 1, (__nv_bfloat16*)x_out, nullptr, nullptr));
   NF_TRY(leave_partitions(p, L, cs));
+  if (L.ms != cs && L.ms == p->mem_stream) {
+    NF_CUDA(cudaEventRecord(p->ev_join, p->mem_stream));
+    NF_CUDA(cudaStreamWaitEvent(cs, p->ev_join, 0));
+  }
+  if (L.ns != cs && L.ns == p->net_stream) {
+    NF_CUDA(cudaEventRecord(p->ev_join_n, p->net_stream));
+    NF_CUDA(cudaStreamWaitEvent(cs, p->ev_join_n, 0));
+  }
   return NF_OK;
 }
 
 nf_status nf_model_step(const nf_plan* plan, nf_comm* comm, const nf_model_weights* w, void* const* kv_pools,
                         const nf_batch* b, const int32_t* token_ids, int32_t* next_ids, void* ws, size_t ws_bytes,
                         void* stream) {
-  if (!plan) return set_error(NF_EINVAL, "plan is NULL");
-  nf_plan* p = const_cast<nf_plan*>(plan);
-  const nf_model_cfg* c = &p->cfg;
-  NF_TRY(validate_batch(c, b));
-  if (c->tp_size > 1) {
-    if (!comm) return set_error(NF_EINVAL, "tp_size > 1 needs a communicator");
-    if (comm_size(comm) != c->tp_size || comm_rank(comm) != c->tp_rank)
-      return set_error(NF_EINVAL, "communicator size/rank %d/%d != cfg %d/%d", comm_size(comm), comm_rank(comm),
-                       c->tp_size, c->tp_rank);
-  }
-  if (!w || !w->embed || !w->layers || !w->lm_head_packed || !kv_pools || !token_ids || !next_ids || !ws)
-    return set_error(NF_EINVAL, "NULL pointer argument");
-  for (int l = 0; l < c->n_layers; ++l)
-    if (!kv_pools[l]) return set_error(NF_EINVAL, "kv_pools[%d] is NULL", l);
-  for (int l = 0; l < c->n_layers; ++l) NF_TRY(validate_packed(c, &w->layers[l], l));
-  Workspace wsp = carve_workspace(c, b, ws);
-  if (ws_bytes < wsp.total) return set_error(NF_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, wsp.total);
-  NF_TRY(ensure_runtime(p));
-  std::vector<int> order, cuts;
-  BatchView view;
-  bool use_view = false;
-  plan_order(p, b, true, &order, &cuts, &view, &use_view);
-  StepMeta m;
-  if (use_view)
-    build_meta(c, &view.b, order, cuts, &m, &view.caller_row0, &view.caller_req);
-  else
-    build_meta(c, b, order, cuts, &m);
-  cudaStream_t cs = (cudaStream_t)stream;
-  NF_TRY(upload_meta(p, m, wsp.meta, cs));
-  NF_CUDA(cudaMemsetAsync(wsp.sk_flag, 0, (size_t)wsp.sk_flag_n * 4, cs));
-  const int D = c->d_model;
-  const int NP = D / GEMM_NORM_COLS;
-  // token ids in internal row order: gather ids then embedding rows (+ RMS partials, one part)
-  // tok_src maps internal row -> caller row; ids are gathered on the fly by the embedding gather.
-  NF_CUDA(launch_gather_ids_embed((const __nv_bfloat16*)w->embed, token_ids, wsp.meta + m.off_tok_src, m.T, D, wsp.xa,
-                                  wsp.part_a, cs));
-  LayerCtx L{};
-  L.p = p;
-  L.c = c;
-  L.m = &m;
-  L.w = &wsp;
-  L.meta_dev = wsp.meta;
-  L.cs = cs;
-  L.ms = p->mem_stream;
-  L.ns = p->spec.mode == NF_OVERLAP ? p->net_stream : cs;
-  L.comm = comm;
-  const int NPn = c->tp_size > 1 ? 1 : NP;  // RMS partials per row of layer outputs
-  __nv_bfloat16 *x = wsp.xa, *y = wsp.xb;
-  float *px = wsp.part_a, *py = wsp.part_b;
-  std::vector<CUtensorMap> maps(c->n_layers), pmaps(c->n_layers);
-  for (int l = 0; l < c->n_layers; ++l) {
-    NF_CUDA(make_pool_tmap(&maps[l], kv_pools[l], b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim,
-                           c->page_size));
-    NF_CUDA(make_page_tmap(&pmaps[l], kv_pools[l], b->n_pages_pool, c->n_kv_heads / c->tp_size, c->head_dim,
-                           c->page_size));
-  }
-  NF_TRY(enter_partitions(p, &L, cs));
-  if (p->spec.mode != NF_OVERLAP) {
-    int nparts = 1;
-    for (int l = 0; l < c->n_layers; ++l) {
-      L.pool_map = maps[l];
-      L.page_map = pmaps[l];
-      NF_TRY(run_layer(p, L, &w->layers[l], kv_pools[l], x, px, nparts, y, py, false));
-      std::swap(x, y);
-      std::swap(px, py);
-      nparts = NPn;
-    }
-  } else {
-    // Operation-level pipeline across layers (PAPER.md:547, single-GPU variant
-    // PAPER.md:691): the compute stream runs, per nano-batch k, O_k UG_k D_k of
-    // layer l then KQV_k of layer l+1; the memory stream runs ATT_k(l+1) as
-    // soon as KQV_k(l+1) lands, overlapping the other nano-batches' dense ops.
-    const auto& nanos = m.nanos;
-    L.pool_map = maps[0];
-    L.page_map = pmaps[0];
-    for (size_t k = 0; k < nanos.size(); ++k) {
-      NF_TRY(run_kqv(L, nanos[k], x, px, 1, &w->layers[0], kv_pools[0]));
-      NF_CUDA(cudaEventRecord(p->ev_kqv[k], L.cs));
-      NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
-      NF_TRY(run_decode(L, nanos[k], L.ms, 1));
-      NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
-      NF_TRY(run_prefill(L, nanos[k], L.cs));
-      NF_TRY(run_decode(L, nanos[k], L.cs, 2));
-    }
-    for (int l = 0; l < c->n_layers; ++l) {
-      for (size_t k = 0; k < nanos.size(); ++k) {
-        NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_att[k], 0));
-        NF_TRY(run_tail(L, k, nanos[k], x, &w->layers[l], y, py));
-        if (l + 1 < c->n_layers) {
-          L.pool_map = maps[l + 1];
-          L.page_map = pmaps[l + 1];
-          NF_TRY(run_kqv(L, nanos[k], y, py, NPn, &w->layers[l + 1], kv_pools[l + 1]));
-          NF_CUDA(cudaEventRecord(p->ev_kqv[k], L.cs));
-          NF_CUDA(cudaStreamWaitEvent(L.ms, p->ev_kqv[k], 0));
-          NF_TRY(run_decode(L, nanos[k], L.ms, 1));
-          NF_CUDA(cudaEventRecord(p->ev_att[k], L.ms));
-          NF_TRY(run_prefill(L, nanos[k], L.cs));
-          NF_TRY(run_decode(L, nanos[k], L.cs, 2));
-        }
-      }
-      std::swap(x, y);
-      std::swap(px, py);
-    }
-  }
-  NF_TRY(leave_partitions(p, L, cs));
-  // final RMSNorm (gamma folded into lm_head_packed) + LM head + argmax
-  NF_CUDA(launch_fill_i32(next_ids, b->n_req, -1, cs));
-  if (m.n_emit > 0) {
-    const int* erow = wsp.meta + m.off_emit_row;
-    NF_CUDA(launch_gather_rows(x, erow, m.n_emit, D, wsp.lm_rows, wsp.lm_part, cs));
-    GemmArgs a{};
-    a.epi = EPI_ARGMAX;
-    a.sk_part = (&wsp)->sk_part;
-    a.sk_slots = (&wsp)->sk_slots;
-    a.sk_flag = (&wsp)->sk_flag;
-    a.M = m.n_emit;
-    a.N = c->vocab;
-    a.K = D;
-    a.n_valid = c->vocab;
-    a.am_val = wsp.am_val;
-    a.am_idx = wsp.am_idx;
-    a.am_stride = m.n_emit;
-    ProfScope ps(NF_PROF_LMHEAD, cs);
-    NF_CUDA(launch_gemm(wsp.lm_rows, D, (const __nv_bfloat16*)w->lm_head_packed, D, a, num_sms(), cs));
-    NF_CUDA(launch_argmax_reduce(wsp.am_val, wsp.am_idx, (c->vocab + GEMM_BN - 1) / GEMM_BN, m.n_emit, m.n_emit,
-                                 wsp.meta + m.off_emit_req, next_ids, cs));
-  }
-  // join the memory and network streams (nothing outstanding in sequential modes)
-  NF_CUDA(cudaEventRecord(p->ev_join, p->mem_stream));
-  NF_CUDA(cudaStreamWaitEvent(cs, p->ev_join, 0));
-  NF_CUDA(cudaEventRecord(p->ev_join, p->net_stream));
-  NF_CUDA(cudaStreamWaitEvent(cs, p->ev_join, 0));
-  return NF_OK;
+  nf_step_outputs out{next_ids, nullptr, nullptr};
+  return model_step_impl(plan, comm, w, kv_pools, b, token_ids, &out, ws, ws_bytes, stream);
+}
+
+nf_status nf_model_step_ex(const nf_plan* plan, nf_comm* comm, const nf_model_weights* w, void* const* kv_pools,
+                           const nf_batch* b, const int32_t* token_ids, const nf_step_outputs* out, void* ws,
+                           size_t ws_bytes, void* stream) {
+  return model_step_impl(plan, comm, w, kv_pools, b, token_ids, out, ws, ws_bytes, stream);
 }
 
 // ------------------------------------------------------------------ MoE op-level entries

@@ -1,8 +1,11 @@
 // Tensor-parallel communicator: NCCL (the process's own libnccl.so.2, loaded
 // with dlopen so the library links without it) over NVLink5 / NVSwitch.
-// PAPER.md:628 used MSCCL++ SM-constrained kernels; here the collectives run
-// on the plan's network stream with NCCL's CTA cap (ncclConfig_t.maxCTAs) set
-// to the plan's network SM budget.
+// PAPER.md:628 used MSCCL++ SM-constrained kernels (the network
+// operation gets its own SM budget).  Here the collectives run on the plan's network
+// stream; with nf_comm_create(max_ctas > 0) NCCL's CTA cap (ncclConfig_t.maxCTAs) is
+// set, and an OVERLAP plan places that stream in its own green-context SM partition
+// of plan sm[NF_OP_NET] SMs when the cap fits in it (api.cu enter_partitions), so the
+// collective kernels never run on the compute or memory partitions.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -51,6 +54,8 @@ struct LocalGroup {
 struct nf_comm {
   ncclComm_t comm = nullptr;
   int tp_size = 1, tp_rank = 0;
+  int max_ctas = 0;                        // NCCL CTA cap (0 = NCCL default)
+  int ar_mode = NF_AR_F32;                 // emulated AllReduce arithmetic
   std::shared_ptr<nf::LocalGroup> group;  // emulated group (nf_comm_create_local)
 };
 
@@ -88,6 +93,8 @@ nf_status load_nccl() {
 
 int comm_size(const nf_comm* c) { return c ? c->tp_size : 1; }
 int comm_rank(const nf_comm* c) { return c ? c->tp_rank : 0; }
+bool comm_emulated(const nf_comm* c) { return c && c->group; }
+int comm_max_ctas(const nf_comm* c) { return c ? c->max_ctas : 0; }
 
 // recv = [rank 0's send | rank 1's send | ...] (count bf16 elements each)
 nf_status comm_all_gather(nf_comm* c, const void* send, void* recv, size_t count_bf16, cudaStream_t st) {
@@ -126,7 +133,7 @@ nf_status comm_all_reduce_bf16(nf_comm* c, void* buf, size_t count, cudaStream_t
     g.barrier();
     for (int q = 0; q < g.n; ++q) cudaStreamWaitEvent(st, g.ev_ready[q], 0);
     std::vector<const void*> srcs(g.src.begin(), g.src.end());
-    if (launch_sum_bf16(srcs.data(), g.n, (__nv_bfloat16*)scratch, count, st) != cudaSuccess)
+    if (launch_sum_bf16(srcs.data(), g.n, (__nv_bfloat16*)scratch, count, c->ar_mode == NF_AR_RING, st) != cudaSuccess)
       return set_error(NF_ECUDA, "emulated AR sum");
     cudaEventRecord(g.ev_done[r], st);
     g.barrier();
@@ -137,11 +144,6 @@ nf_status comm_all_reduce_bf16(nf_comm* c, void* buf, size_t count, cudaStream_t
     return NF_OK;
   }
   ncclResult_t r = g_nccl.allReduce(buf, buf, count, ncclBfloat16, ncclSum, c->comm, st);
-  if (r != ncclSuccess) return set_error(NF_ENCCL, "ncclAllReduce: %s", g_nccl.getErrorString(r));
-  return NF_OK;
-}
-nf_status comm_all_reduce_f32(nf_comm* c, void* buf, size_t count, cudaStream_t st) {
-  ncclResult_t r = g_nccl.allReduce(buf, buf, count, ncclFloat32, ncclSum, c->comm, st);
   if (r != ncclSuccess) return set_error(NF_ENCCL, "ncclAllReduce: %s", g_nccl.getErrorString(r));
   return NF_OK;
 }
@@ -163,17 +165,23 @@ nf_status nf_comm_unique_id(void* id_out_128) {
   return NF_OK;
 }
 
-nf_status nf_comm_create(int32_t tp_size, int32_t tp_rank, const void* id_128, nf_comm** out) {
+nf_status nf_comm_create(int32_t tp_size, int32_t tp_rank, const void* id_128, int32_t max_ctas, nf_comm** out) {
   if (!out || !id_128) return set_error(NF_EINVAL, "NULL argument");
   if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size) return set_error(NF_EINVAL, "bad tp_size/tp_rank");
+  if (max_ctas < 0 || max_ctas > 64) return set_error(NF_EINVAL, "max_ctas %d not in [0, 64]", max_ctas);
   NF_TRY(load_nccl());
   ncclUniqueId id;
   std::memcpy(&id, id_128, 128);
   ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
   cfg.blocking = 1;
+  if (max_ctas > 0) {
+    cfg.minCTAs = 1;
+    cfg.maxCTAs = max_ctas;
+  }
   nf_comm* c = new nf_comm();
   c->tp_size = tp_size;
   c->tp_rank = tp_rank;
+  c->max_ctas = max_ctas;
   ncclResult_t r = g_nccl.commInitRankConfig(&c->comm, tp_size, id, tp_rank, &cfg);
   if (r != ncclSuccess) {
     delete c;
@@ -183,13 +191,15 @@ nf_status nf_comm_create(int32_t tp_size, int32_t tp_rank, const void* id_128, n
   return NF_OK;
 }
 
-nf_status nf_comm_create_local(int32_t tp_size, nf_comm** comms_out) {
-  if (!comms_out || tp_size < 1 || tp_size > 64) return set_error(NF_EINVAL, "bad tp_size / output");
+nf_status nf_comm_create_local(int32_t tp_size, int32_t ar_mode, nf_comm** comms_out) {
+  if (!comms_out || tp_size < 1 || tp_size > 8) return set_error(NF_EINVAL, "bad tp_size (1..8) / output");
+  if (ar_mode != NF_AR_F32 && ar_mode != NF_AR_RING) return set_error(NF_EINVAL, "bad ar_mode %d", ar_mode);
   auto g = std::make_shared<LocalGroup>(tp_size);
   for (int r = 0; r < tp_size; ++r) {
     nf_comm* c = new nf_comm();
     c->tp_size = tp_size;
     c->tp_rank = r;
+    c->ar_mode = ar_mode;
     c->group = g;
     comms_out[r] = c;
   }

@@ -46,10 +46,11 @@ bool load_api() {
 }
 }  // namespace
 
-// Creates (once per plan) the memory / compute partitions for an OVERLAP plan.
-// Returns false (and leaves the plan on ordinary streams) when disabled with
-// NF_GREEN=0 or unsupported; p->green_note says why.
-bool green_setup(nf_plan* p, int dec_sms) {
+// Creates (once per plan) the memory / compute partitions for an OVERLAP plan,
+// plus a network partition of net_sms SMs (TP plans) when
+// net_sms > 0.  Returns false (and leaves the plan on ordinary streams) when
+// disabled with NF_GREEN=0 or unsupported; p->green_note says why.
+bool green_setup(nf_plan* p, int dec_sms, int net_sms) {
   if (p->green_tried) return p->green_ok;
   p->green_tried = true;
   const char* env = getenv("NF_GREEN");
@@ -57,12 +58,20 @@ bool green_setup(nf_plan* p, int dec_sms) {
     p->green_note = "disabled (NF_GREEN=0)";
     return false;
   }
+  // Nsight Compute injects itself through CUDA_INJECTION64_PATH and cannot replay
+  // kernels of green contexts: under a profiler the plan runs on ordinary streams
+  // (same kernels, SM-bounded persistent grids) unless NF_GREEN=1 forces partitions.
+  const char* inj = getenv("CUDA_INJECTION64_PATH");
+  if (inj && inj[0] && !(env && env[0] == '1')) {
+    p->green_note = "not used under a profiler (CUDA_INJECTION64_PATH set)";
+    return false;
+  }
   if (!load_api()) {
     p->green_note = "driver lacks green-context entry points";
     return false;
   }
   CUdevice dev = p->device;
-  CUdevResource all{}, part[1]{}, rest{};
+  CUdevResource all{}, part[1]{}, rest{}, npart[1]{}, rest2{};
   if (g_api.getDevResource(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) {
     p->green_note = "cuDeviceGetDevResource failed";
     return false;
@@ -73,29 +82,48 @@ bool green_setup(nf_plan* p, int dec_sms) {
     p->green_note = "cuDevSmResourceSplitByCount failed";
     return false;
   }
-  CUdevResourceDesc d_mem, d_cmp;
-  CUgreenCtx g_mem, g_cmp;
-  if (g_api.genDesc(&d_mem, part, 1) != CUDA_SUCCESS || g_api.genDesc(&d_cmp, &rest, 1) != CUDA_SUCCESS ||
+  CUdevResource* cmp = &rest;
+  if (net_sms > 0) {
+    unsigned int n2 = 1;
+    const unsigned int want_n = (unsigned int)((net_sms + 7) / 8 * 8);
+    if (g_api.split(npart, &n2, &rest, &rest2, 0, want_n) != CUDA_SUCCESS || n2 != 1) {
+      p->green_note = "cuDevSmResourceSplitByCount (network partition) failed";
+      return false;
+    }
+    cmp = &rest2;
+  }
+  CUdevResourceDesc d_mem, d_cmp, d_net;
+  CUgreenCtx g_mem, g_cmp, g_net = nullptr;
+  if (g_api.genDesc(&d_mem, part, 1) != CUDA_SUCCESS || g_api.genDesc(&d_cmp, cmp, 1) != CUDA_SUCCESS ||
       g_api.create(&g_mem, d_mem, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
       g_api.create(&g_cmp, d_cmp, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) {
     p->green_note = "green context creation failed";
     return false;
   }
+  if (net_sms > 0 && (g_api.genDesc(&d_net, npart, 1) != CUDA_SUCCESS ||
+                      g_api.create(&g_net, d_net, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)) {
+    p->green_note = "green context creation failed (network partition)";
+    return false;
+  }
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  CUstream s_mem, s_cmp;
+  CUstream s_mem, s_cmp, s_net = nullptr;
   if (g_api.streamCreate(&s_mem, g_mem, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS ||
-      g_api.streamCreate(&s_cmp, g_cmp, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS) {
+      g_api.streamCreate(&s_cmp, g_cmp, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS ||
+      (g_net && g_api.streamCreate(&s_net, g_net, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS)) {
     p->green_note = "green stream creation failed";
     return false;
   }
   p->green_ms = (cudaStream_t)s_mem;
   p->green_cs = (cudaStream_t)s_cmp;
+  p->green_ns = (cudaStream_t)s_net;
   p->green_dec_sms = (int)part[0].sm.smCount;
-  p->green_dense_sms = (int)rest.sm.smCount;
+  p->green_dense_sms = (int)cmp->sm.smCount;
+  p->green_net_sms = g_net ? (int)npart[0].sm.smCount : 0;
   p->green_ok = true;
   p->green_note = "memory partition " + std::to_string(p->green_dec_sms) + " SMs, compute partition " +
                   std::to_string(p->green_dense_sms) + " SMs";
+  if (g_net) p->green_note += ", network partition " + std::to_string(p->green_net_sms) + " SMs";
   return true;
 }
 

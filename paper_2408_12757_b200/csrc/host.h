@@ -42,7 +42,7 @@ struct NanoRange {
 struct StepMeta {
   std::vector<int32_t> buf;   // int32 words uploaded to the workspace
   size_t off_pos = 0, off_slot = 0, off_pages = 0, off_dec = 0, off_pf = 0, off_emit_row = 0, off_emit_req = 0,
-         off_tok_src = 0;
+         off_tok_src = 0, off_emit_sorted = 0;  // emit rows in ascending caller-request order (logits output)
   int T = 0, n_req = 0, n_emit = 0;
   std::vector<NanoRange> nanos;
 };
@@ -62,7 +62,10 @@ struct Workspace {
   float *part_a, *part_b, *part_h1, *lm_part, *am_val;
   int* am_idx;
   float* red;  // TP partial sums (f32)
-  __nv_bfloat16 *ag, *ocat, *hcol;  // TP: gathered (rank-major) staging, interleaved O input, O-col output
+  __nv_bfloat16 *ag, *ag2, *ocat, *hcol;  // TP: gathered (rank-major) attention output / O-col output staging,
+                                          // interleaved O input, O-col output
+  float* am_pair;      // TP: per-row (max, global argmax) of this rank's vocab shard [n_req] (float, int)
+  float* am_pair_all;  // TP: AllGather of am_pair [tp][n_req]
   float* sk_part;  // stream-K partial tiles [148][128][256] f32
   int* sk_flag;    // stream-K tile counters
   int sk_flag_n;
@@ -85,12 +88,21 @@ Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base);
 }  // namespace nf
 
 namespace nf {
-bool green_setup(nf_plan* p, int dec_sms);
+bool green_setup(nf_plan* p, int dec_sms, int net_sms);
 int comm_size(const nf_comm* c);
 int comm_rank(const nf_comm* c);
+bool comm_emulated(const nf_comm* c);
+int comm_max_ctas(const nf_comm* c);
 nf_status comm_all_gather(nf_comm* c, const void* send, void* recv, size_t count_bf16, cudaStream_t st);
 nf_status comm_all_reduce_bf16(nf_comm* c, void* buf, size_t count, cudaStream_t st, void* scratch);
 }  // namespace nf
+
+// A captured nf_model_step (plan spec.graph): replayed while the launch structure
+// (key: shapes, item counts, metadata offsets, buffers) is unchanged.
+struct NfGraph {
+  std::vector<int64_t> key;
+  cudaGraphExec_t exec = nullptr;
+};
 
 struct nf_plan {
   nf_model_cfg cfg;
@@ -104,6 +116,15 @@ struct nf_plan {
   cudaEvent_t ev_join = nullptr;
   cudaStream_t net_stream = nullptr;
   cudaEvent_t ev_c2n = nullptr, ev_n2c = nullptr;
+  // TP pipeline edges, one per dense nano-batch (api.cu tp_* stages)
+  cudaEvent_t ev_pre[NF_MAX_NANO] = {}, ev_agattn = nullptr, ev_o[NF_MAX_NANO] = {}, ev_ago = nullptr,
+              ev_aro[NF_MAX_NANO] = {}, ev_d[NF_MAX_NANO] = {}, ev_ard[NF_MAX_NANO] = {};
+  cudaEvent_t ev_join_n = nullptr;
+  cudaStream_t green_ns = nullptr;  // network partition (TP OVERLAP plans)
+  int green_net_sms = 0;
+  std::vector<NfGraph> graphs;      // CUDA-graph cache (spec.graph)
+  std::string graph_note = "not used";
+  std::string note;                 // nf_plan_runtime_note buffer
   // green-context SM partitions (OVERLAP plans; green.cpp)
   bool green_tried = false, green_ok = false;
   std::string green_note = "not used";

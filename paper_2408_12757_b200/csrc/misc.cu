@@ -11,12 +11,15 @@ namespace {
 
 // one warp per row: dst[row] = src[idx[row]] (bf16, D % 8 == 0), sumsq -> part[row]
 // (idx2 != null: source row = idx[idx2[row]], an embedding lookup in a permuted row order)
+// (src_rows > 0: the source row is clamped to [0, src_rows): an out-of-vocabulary token id
+// reads a valid embedding row instead of faulting)
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, const int* __restrict__ idx,
-                                   const int* __restrict__ idx2, int rows, int D, __nv_bfloat16* __restrict__ dst,
-                                   float* __restrict__ part) {
+                                   const int* __restrict__ idx2, int rows, int D, int src_rows,
+                                   __nv_bfloat16* __restrict__ dst, float* __restrict__ part) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
-  const int64_t s = idx ? (int64_t)idx[idx2 ? idx2[warp] : warp] : (int64_t)warp;
+  int64_t s = idx ? (int64_t)idx[idx2 ? idx2[warp] : warp] : (int64_t)warp;
+  if (src_rows > 0) s = s < 0 ? 0 : (s >= src_rows ? src_rows - 1 : s);
   const uint4* in = reinterpret_cast<const uint4*>(src + s * D);
   uint4* out = dst ? reinterpret_cast<uint4*>(dst + (int64_t)warp * D) : nullptr;
   float sq = 0.f;
@@ -72,13 +75,55 @@ __global__ void argmax_reduce_kernel(const float* __restrict__ val, const int* _
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   float best = -INFINITY;
-  int bi = 0x7fffffff;
+  int bi = idx[r];  // tile 0's candidate: a valid id even if every logit of the row is NaN
   for (int t = 0; t < ntiles; ++t) {
     const float v = val[t * stride + r];
     const int i = idx[t * stride + r];
     if (v > best || (v == best && i < bi)) { best = v; bi = i; }
   }
   next_ids[row_req ? row_req[r] : r] = bi;
+}
+
+// Vocab-parallel LM head (TP): this rank's per-row (max, lowest global argmax) over its
+// tiles, as an 8-byte (float, int) pair for the AllGather.
+__global__ void argmax_pairs_kernel(const float* __restrict__ val, const int* __restrict__ idx, int ntiles,
+                                    int64_t stride, int rows, int idx_off, float* __restrict__ pairs) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  float best = -INFINITY;
+  int bi = idx[r];
+  for (int t = 0; t < ntiles; ++t) {
+    const float v = val[t * stride + r];
+    const int i = idx[t * stride + r];
+    if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+  }
+  pairs[2 * r] = best;
+  reinterpret_cast<int*>(pairs)[2 * r + 1] = bi + idx_off;
+}
+
+// Merge the gathered pairs [n ranks][rows]: max value, lowest global index on ties (A-15).
+__global__ void argmax_merge_kernel(const float* __restrict__ pairs, int n, int rows, const int* __restrict__ row_req,
+                                    int* __restrict__ next_ids) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  float best = pairs[2 * r];
+  int bi = reinterpret_cast<const int*>(pairs)[2 * r + 1];
+  for (int q = 1; q < n; ++q) {
+    const float v = pairs[2 * ((int64_t)q * rows + r)];
+    const int i = reinterpret_cast<const int*>(pairs)[2 * ((int64_t)q * rows + r) + 1];
+    if (v > best || (v == best && i < bi) || (best != best && v == v)) { best = v; bi = i; }
+  }
+  next_ids[row_req ? row_req[r] : r] = bi;
+}
+
+// one warp per row: dst[idx[row]] = src[row]
+__global__ void scatter_rows_kernel(const __nv_bfloat16* __restrict__ src, const int* __restrict__ idx, int rows, int D,
+                                    __nv_bfloat16* __restrict__ dst) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const uint4* in = reinterpret_cast<const uint4*>(src + (int64_t)warp * D);
+  uint4* out = reinterpret_cast<uint4*>(dst + (int64_t)idx[warp] * D);
+  for (int i = lane; i < D / 8; i += 32) out[i] = in[i];
 }
 
 __global__ void fill_i32_kernel(int* p, int n, int v) {
@@ -147,12 +192,26 @@ __global__ void interleave_kernel(const __nv_bfloat16* __restrict__ src, int n, 
 struct SumPtrs {
   const __nv_bfloat16* p[8];
 };
-// out[i] = bf16(sum_q in_q[i]) accumulated in fp32 in rank order (n <= 8)
+// out[i] = bf16(sum_q in_q[i]) accumulated in fp32 in rank order (n <= 8), one rounding
 __global__ void sum_bf16_kernel(SumPtrs in, int n, __nv_bfloat16* __restrict__ out, size_t count) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
     float acc = 0.f;
     for (int q = 0; q < n; ++q) acc += __bfloat162float(in.p[q][i]);
     out[i] = __float2bfloat16_rn(acc);
+  }
+}
+
+// NCCL ring AllReduce arithmetic (emulated group, NF_AR_RING): the buffer is cut into n
+// chunks; chunk c's reduce-scatter starts at rank (c+1) mod n and each hop adds the next
+// rank's input to the bf16 partial it received and rounds to bf16 before sending it on,
+// ending at rank c; the all-gather phase copies the reduced chunk unchanged.
+__global__ void sum_bf16_ring_kernel(SumPtrs in, int n, __nv_bfloat16* __restrict__ out, size_t count) {
+  const size_t chunk = (count + n - 1) / n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / chunk);
+    __nv_bfloat16 acc = in.p[(c + 1) % n][i];
+    for (int j = 2; j <= n; ++j) acc = __float2bfloat16_rn(__bfloat162float(acc) + __bfloat162float(in.p[(c + j) % n][i]));
+    out[i] = acc;
   }
 }
 
@@ -166,7 +225,7 @@ int grid_for(int64_t n, int block) {
 cudaError_t launch_gather_rows(const __nv_bfloat16* src, const int* idx, int rows, int D, __nv_bfloat16* dst,
                                float* part, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
-  gather_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(src, idx, nullptr, rows, D, dst, part);
+  gather_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(src, idx, nullptr, rows, D, 0, dst, part);
   count_launch();
   return cudaGetLastError();
 }
@@ -180,9 +239,9 @@ cudaError_t launch_resid_add_rows(__nv_bfloat16* acc, const __nv_bfloat16* resid
 }
 
 cudaError_t launch_gather_ids_embed(const __nv_bfloat16* embed, const int* token_ids, const int* tok_src, int rows, int D,
-                                    __nv_bfloat16* dst, float* part, cudaStream_t st) {
+                                    int vocab, __nv_bfloat16* dst, float* part, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
-  gather_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(embed, token_ids, tok_src, rows, D, dst, part);
+  gather_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(embed, token_ids, tok_src, rows, D, vocab, dst, part);
   count_launch();
   return cudaGetLastError();
 }
@@ -203,11 +262,37 @@ cudaError_t launch_interleave(const __nv_bfloat16* src, int n, int rows, int C, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_sum_bf16(const void* const* in, int n, __nv_bfloat16* out, size_t count, cudaStream_t st) {
+cudaError_t launch_sum_bf16(const void* const* in, int n, __nv_bfloat16* out, size_t count, bool ring, cudaStream_t st) {
   if (n > 8) return cudaErrorInvalidValue;
   SumPtrs ps{};
   for (int q = 0; q < n; ++q) ps.p[q] = (const __nv_bfloat16*)in[q];
-  sum_bf16_kernel<<<grid_for((int64_t)count, 256), 256, 0, st>>>(ps, n, out, count);
+  if (ring)
+    sum_bf16_ring_kernel<<<grid_for((int64_t)count, 256), 256, 0, st>>>(ps, n, out, count);
+  else
+    sum_bf16_kernel<<<grid_for((int64_t)count, 256), 256, 0, st>>>(ps, n, out, count);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_argmax_pairs(const float* val, const int* idx, int ntiles, int64_t stride, int rows, int idx_off,
+                                float* pairs, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  argmax_pairs_kernel<<<(rows + 127) / 128, 128, 0, st>>>(val, idx, ntiles, stride, rows, idx_off, pairs);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_argmax_merge(const float* pairs, int n, int rows, const int* row_req, int* next_ids, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  argmax_merge_kernel<<<(rows + 127) / 128, 128, 0, st>>>(pairs, n, rows, row_req, next_ids);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_rows(const __nv_bfloat16* src, const int* idx, int rows, int D, __nv_bfloat16* dst,
+                                cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  scatter_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(src, idx, rows, D, dst);
   count_launch();
   return cudaGetLastError();
 }

@@ -228,6 +228,66 @@ std::vector<PNode> build_pipeline(const std::vector<std::array<double, 3>>& work
   return g;
 }
 
+// The tensor-parallel pipeline (reading P-8): quarters Q1..Q4 for
+// KQV / attention, H1 = Q1+Q2 (column O + AllGathers), H2 = Q3+Q4 (row O + AllReduce);
+// NET work = AllGather-equivalent tokens (an AllReduce counts twice its tokens).
+std::vector<PNode> build_pipeline_tp(const std::vector<std::array<double, 3>>& work, int n_layers) {
+  std::vector<PNode> g;
+  auto add = [&](int kind, int nano, double w, std::vector<int> deps) {
+    PNode nd;
+    nd.kind = kind;
+    nd.nano = nano;
+    nd.work = w;
+    for (int d : deps)
+      if (d >= 0) nd.deps.push_back(d);
+    g.push_back(nd);
+    return (int)g.size() - 1;
+  };
+  int last_c = -1, last_m = -1, last_n = -1;
+  int dec[4] = {-1, -1, -1, -1}, pf[4] = {-1, -1, -1, -1}, ready[2] = {-1, -1};
+  const double tok[2] = {work[0][0] + work[1][0], work[2][0] + work[3][0]};
+  auto front = [&](int gi) {
+    for (int q = 2 * gi; q < 2 * gi + 2; ++q) {
+      const int kq = add(NF_OP_KQV, q, work[q][0], {last_c, ready[gi]});
+      dec[q] = add(NF_OP_DECODE_ATTN, q, work[q][1], {kq, last_m});
+      last_m = dec[q];
+      pf[q] = add(NF_OP_PREFILL_ATTN, q, work[q][2], {kq});
+      last_c = pf[q];
+    }
+  };
+  front(0);
+  front(1);
+  for (int l = 0; l < n_layers; ++l) {
+    const int ag_a = add(NF_OP_NET, 0, tok[0], {dec[0], dec[1], pf[1], last_n});
+    last_n = ag_a;
+    const int o1 = add(NF_OP_O, 0, tok[0], {ag_a, last_c});
+    last_c = o1;
+    const int ag_o = add(NF_OP_NET, 0, tok[0], {o1, last_n});
+    last_n = ag_o;
+    const int o2 = add(NF_OP_O, 1, tok[1], {dec[2], dec[3], last_c});
+    last_c = o2;
+    const int ar_o = add(NF_OP_NET, 1, 2 * tok[1], {o2, last_n});
+    last_n = ar_o;
+    const int ug1 = add(NF_OP_UG, 0, tok[0], {ag_o, last_c});
+    const int d1 = add(NF_OP_DOWN, 0, tok[0], {ug1});
+    last_c = d1;
+    const int ar_d1 = add(NF_OP_NET, 0, 2 * tok[0], {d1, last_n});
+    last_n = ar_d1;
+    const int ug2 = add(NF_OP_UG, 1, tok[1], {ar_o, last_c});
+    const int d2 = add(NF_OP_DOWN, 1, tok[1], {ug2});
+    last_c = d2;
+    const int ar_d2 = add(NF_OP_NET, 1, 2 * tok[1], {d2, last_n});
+    last_n = ar_d2;
+    ready[0] = ar_d1;
+    ready[1] = ar_d2;
+    if (l + 1 < n_layers) {
+      front(0);
+      front(1);
+    }
+  }
+  return g;
+}
+
 std::vector<int> rank_order(const std::vector<PNode>& g) {
   const int n = (int)g.size();
   std::vector<int> rank(n, 0), order(n);
@@ -269,7 +329,7 @@ extern "C" nf_status nf_plan_create(const nf_model_cfg* cfg, const nf_batch* sha
   if (opts->sm_budget < 1 || opts->sm_quantum < 1 || opts->sm_quantum > opts->sm_budget)
     return set_error(NF_EINVAL, "bad sm_budget/sm_quantum");
   if (opts->mode < NF_SEQUENTIAL || opts->mode > NF_OVERLAP) return set_error(NF_EINVAL, "bad mode");
-  if (cfg->tp_size > 1) return set_error(NF_EUNSUPPORTED, "autosearch for tp_size > 1 not built yet");
+  const bool tp = cfg->tp_size > 1;
   const int budget = opts->sm_budget, q = opts->sm_quantum, iters = std::max(0, opts->max_iters);
   nf_plan_spec spec{};
   spec.mode = opts->mode;
@@ -288,7 +348,9 @@ extern "C" nf_status nf_plan_create(const nf_model_cfg* cfg, const nf_batch* sha
       cv.add(pts[i].op_kind, pts[i].units, pts[i].work, pts[i].latency_s);
     }
     cv.finish();
-    const int nn = 2;  // single-GPU pipeline: two nano-batches
+    // single-GPU pipeline: two nano-batches; TP: four attention quarters
+    // grouped into two dense halves (reading P-8)
+    const int nn = tp ? 4 : 2;
     bool have = false;
     double best_m = 0.0;
     int best_s = 0;
@@ -296,7 +358,7 @@ extern "C" nf_status nf_plan_create(const nf_model_cfg* cfg, const nf_batch* sha
     std::vector<PNode> best_g;
     Sched best_sched;
     for (int s8 = 1; s8 <= 7; ++s8) {
-      const int32_t sh[2] = {s8, 8 - s8};
+      const int32_t sh[4] = {s8, tp ? s8 : 8 - s8, 8 - s8, 8 - s8};
       std::vector<std::vector<int>> grp;
       balance_requests(shape, nn, sh, &grp);
       std::vector<std::array<double, 3>> work;
@@ -312,7 +374,7 @@ extern "C" nf_status nf_plan_create(const nf_model_cfg* cfg, const nf_batch* sha
         }
         work.push_back({tok, dk, pk});
       }
-      std::vector<PNode> g = build_pipeline(work, 3);
+      std::vector<PNode> g = tp ? build_pipeline_tp(work, 3) : build_pipeline(work, 3);
       for (const auto& nd : g)
         if (nd.work > 0 && !cv.has(nd.kind))
           return set_error(NF_EINVAL, "no curve for op kind %d (%s)", nd.kind, kind_name(nd.kind));
@@ -332,8 +394,15 @@ extern "C" nf_status nf_plan_create(const nf_model_cfg* cfg, const nf_batch* sha
     }
     if (!have) return set_error(NF_EINFEASIBLE, "no candidate split fits the SM budget");
     spec.n_nano = nn;
-    spec.share[0] = best_s;
-    spec.share[1] = 8 - best_s;
+    if (tp) {
+      spec.n_dense = 2;
+      spec.share[0] = spec.share[1] = best_s;
+      spec.share[2] = spec.share[3] = 8 - best_s;
+      spec.balance = 2;
+    } else {
+      spec.share[0] = best_s;
+      spec.share[1] = 8 - best_s;
+    }
     for (int k = 0; k < NF_OP_COUNT; ++k) spec.sm[k] = std::max(1, best_u[k]);
     char line[160];
     for (size_t i = 0; i < best_g.size(); ++i) {

@@ -15,7 +15,9 @@ struct Rec {
   int op;
   cudaStream_t st;
   cudaEvent_t a, b;
+  int tag;
 };
+thread_local int t_tag = -1;
 cudaEvent_t g_base = nullptr;
 std::mutex g_mu;
 std::vector<Rec> g_recs;
@@ -34,6 +36,7 @@ cudaEvent_t get_event() {
 }  // namespace
 
 void count_launch(int n) { g_launches += n; }
+bool profile_active() { return g_prof_on.load() != 0; }
 
 ProfScope::ProfScope(int op, cudaStream_t st) : op_(op), st_(st) {
   if (!g_prof_on.load()) return;
@@ -46,7 +49,7 @@ ProfScope::~ProfScope() {
   if (!a_) return;
   std::lock_guard<std::mutex> lk(g_mu);
   cudaEventRecord(b_, st_);
-  g_recs.push_back(Rec{op_, st_, a_, b_});
+  g_recs.push_back(Rec{op_, st_, a_, b_, t_tag});
 }
 
 }  // namespace nf
@@ -54,6 +57,11 @@ ProfScope::~ProfScope() {
 extern "C" {
 
 int64_t nf_kernel_launches(void) { return nf::g_launches.load(); }
+
+nf_status nf_profile_tag(int32_t tag) {
+  nf::t_tag = tag;
+  return NF_OK;
+}
 
 nf_status nf_profile_enable(int32_t on) {
   if (on && !nf::g_prof_on.load()) {
@@ -84,7 +92,7 @@ nf_status nf_profile_timeline(nf_span* out, int32_t cap, int32_t* n_out) {
         si = (int)streams.size();
         streams.push_back(r.st);
       }
-      out[n] = nf_span{r.op, si, a, b};
+      out[n] = nf_span{r.op, si, a, b, r.tag};
     }
     ++n;
   }

@@ -3,6 +3,7 @@
 
 namespace nf {
 void count_launch(int n = 1);
+bool profile_active();
 // RAII: when profiling is enabled, records CUDA events around the enclosed launches on `st`.
 class ProfScope {
  public:

@@ -48,7 +48,8 @@ class _Batch(C.Structure):
 
 class PlanSpec(C.Structure):
     _fields_ = [("mode", C.c_int32), ("n_nano", C.c_int32), ("share", C.c_int32 * MAX_NANO),
-                ("sm", C.c_int32 * OP_COUNT), ("balance", C.c_int32), ("colocate", C.c_int32)]
+                ("sm", C.c_int32 * OP_COUNT), ("balance", C.c_int32), ("colocate", C.c_int32),
+                ("n_dense", C.c_int32), ("graph", C.c_int32)]
 
 
 class CurvePoint(C.Structure):
@@ -92,9 +93,10 @@ _sig("nf_plan_export_csv", C.c_int, C.c_void_p, C.c_char_p, C.c_size_t, C.POINTE
 _sig("nf_plan_destroy", None, C.c_void_p)
 _sig("nf_plan_runtime_note", C.c_char_p, C.c_void_p)
 _sig("nf_comm_unique_id", C.c_int, C.c_void_p)
-_sig("nf_comm_create", C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p))
+_sig("nf_comm_create", C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p))
 _sig("nf_comm_destroy", None, C.c_void_p)
-_sig("nf_comm_create_local", C.c_int, C.c_int32, C.POINTER(C.c_void_p))
+_sig("nf_comm_create_local", C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_void_p))
+AR_F32, AR_RING = 0, 1
 _sig("nf_packed_layer_bytes", C.c_int, C.POINTER(ModelCfg), C.POINTER(C.c_size_t))
 _sig("nf_pack_layer", C.c_int, C.POINTER(ModelCfg), C.POINTER(LayerWeights), C.POINTER(PackedLayer), C.c_void_p)
 _sig("nf_pack_lm_head", C.c_int, C.POINTER(ModelCfg), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
@@ -103,6 +105,14 @@ _sig("nf_layer_forward", C.c_int, C.c_void_p, C.c_void_p, C.POINTER(PackedLayer)
      C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 _sig("nf_model_step", C.c_int, C.c_void_p, C.c_void_p, C.POINTER(ModelWeights), C.POINTER(C.c_void_p),
      C.POINTER(_Batch), C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+class StepOutputs(C.Structure):
+    _fields_ = [("next_ids", C.c_void_p), ("logits", C.c_void_p), ("hidden", C.POINTER(C.c_void_p))]
+
+
+_sig("nf_model_step_ex", C.c_int, C.c_void_p, C.c_void_p, C.POINTER(ModelWeights), C.POINTER(C.c_void_p),
+     C.POINTER(_Batch), C.c_void_p, C.POINTER(StepOutputs), C.c_void_p, C.c_size_t, C.c_void_p)
 _sig("nf_gemm_bf16", C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
      C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p)
 _sig("nf_gemm_workspace_bytes", C.c_size_t, C.c_int32, C.c_int32)
@@ -146,16 +156,18 @@ PROF_LMHEAD, PROF_MISC, PROF_COUNT = OP_COUNT, OP_COUNT + 1, OP_COUNT + 2
 
 
 class Span(C.Structure):
-    _fields_ = [("op", C.c_int32), ("stream", C.c_int32), ("start_ms", C.c_float), ("end_ms", C.c_float)]
+    _fields_ = [("op", C.c_int32), ("stream", C.c_int32), ("start_ms", C.c_float), ("end_ms", C.c_float),
+                ("tag", C.c_int32)]
 
 
 _sig("nf_profile_timeline", C.c_int, C.POINTER(Span), C.c_int32, P_i32)
+_sig("nf_profile_tag", C.c_int, C.c_int32)
 PROF_NAMES = ["kqv", "decode_attn", "prefill_attn", "o_proj", "up_gate", "down", "net", "lm_head", "misc"]
 
-EXPORTED = ["nf_plan_runtime_note", "nf_comm_create_local", "nf_gemm_workspace_bytes", "nf_profile_timeline", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
+EXPORTED = ["nf_plan_runtime_note", "nf_comm_create_local", "nf_gemm_workspace_bytes", "nf_profile_timeline", "nf_profile_tag", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
             "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_comm_unique_id",
             "nf_comm_create", "nf_comm_destroy", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
-            "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_gemm_bf16", "nf_attention",
+            "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_model_step_ex", "nf_gemm_bf16", "nf_attention",
             "nf_moe_rows_cap", "nf_moe_route_ws_bytes", "nf_moe_route", "nf_sched_create", "nf_sched_submit",
             "nf_sched_next", "nf_sched_complete", "nf_sched_get_stats", "nf_sched_destroy", "nf_assemble_tokens"]
 
@@ -218,7 +230,8 @@ class Plan:
 
     @classmethod
     def explicit(cls, cfg: ModelCfg, mode: int = SEQUENTIAL, shares: Sequence[int] = (1,),
-                 sm: Optional[Sequence[int]] = None, balance: bool = False, colocate: bool = False) -> "Plan":
+                 sm: Optional[Sequence[int]] = None, balance: bool = False, colocate: bool = False,
+                 n_dense: int = 0, graph: bool = False) -> "Plan":
         spec = PlanSpec()
         spec.mode = mode
         spec.n_nano = len(shares)
@@ -229,6 +242,8 @@ class Plan:
             spec.sm[i] = int(sm[i])
         spec.balance = int(balance)  # bool True -> 1
         spec.colocate = int(colocate)
+        spec.n_dense = int(n_dense)
+        spec.graph = int(graph)
         h = C.c_void_p()
         _check(lib.nf_plan_create_explicit(C.byref(cfg), C.byref(spec), C.byref(h)))
         return cls(h.value)
@@ -240,6 +255,12 @@ class Plan:
         opts = PlanOpts(sm_budget, sm_quantum, mode, n_nano, max_iters)
         h = C.c_void_p()
         _check(lib.nf_plan_create(C.byref(cfg), C.byref(shape.c), arr, len(points), C.byref(opts), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_spec(cls, cfg: ModelCfg, spec: PlanSpec) -> "Plan":
+        h = C.c_void_p()
+        _check(lib.nf_plan_create_explicit(C.byref(cfg), C.byref(spec), C.byref(h)))
         return cls(h.value)
 
     def runtime_note(self) -> str:
@@ -309,6 +330,16 @@ def model_step(plan: Plan, model: ModelHandle, kv_pools: Sequence[int], b: Batch
                              C.c_void_p(next_ids), C.c_void_p(ws), ws_bytes, C.c_void_p(stream)))
 
 
+def model_step_ex(plan: Plan, model: ModelHandle, kv_pools: Sequence[int], b: Batch, token_ids: int, next_ids: int,
+                  ws: int, ws_bytes: int, stream: int, comm: Optional[int] = None, logits: int = 0,
+                  hidden: Optional[Sequence[int]] = None):
+    pools = (C.c_void_p * len(kv_pools))(*kv_pools)
+    hid = (C.c_void_p * len(hidden))(*[h or None for h in hidden]) if hidden is not None else None
+    out = StepOutputs(next_ids, logits or None, C.cast(hid, C.POINTER(C.c_void_p)) if hid is not None else None)
+    _check(lib.nf_model_step_ex(plan.h, C.c_void_p(comm), C.byref(model.c), pools, C.byref(b.c), C.c_void_p(token_ids),
+                                C.byref(out), C.c_void_p(ws), ws_bytes, C.c_void_p(stream)))
+
+
 def gemm_workspace_bytes(M: int, N: int) -> int:
     return int(lib.nf_gemm_workspace_bytes(M, N))
 
@@ -348,13 +379,20 @@ def profile_enable(on: bool = True):
     _check(lib.nf_profile_enable(1 if on else 0))
 
 
-def profile_timeline():
-    """[(op name, stream index, start ms, end ms)] recorded since the last profile_read()."""
+def profile_timeline(with_tag: bool = False):
+    """[(op name, stream index, start ms, end ms[, tag])] recorded since the last profile_read()."""
     n = C.c_int32()
     _check(lib.nf_profile_timeline(None, 0, C.byref(n)))
     arr = (Span * max(n.value, 1))()
     _check(lib.nf_profile_timeline(arr, n.value, C.byref(n)))
+    if with_tag:
+        return [(PROF_NAMES[s.op], s.stream, s.start_ms, s.end_ms, s.tag) for s in arr[:n.value]]
     return [(PROF_NAMES[s.op], s.stream, s.start_ms, s.end_ms) for s in arr[:n.value]]
+
+
+def profile_tag(tag: int):
+    """Tag the profile spans recorded from this thread (e.g. its emulated rank)."""
+    _check(lib.nf_profile_tag(tag))
 
 
 def profile_read():
@@ -371,10 +409,11 @@ def comm_unique_id() -> bytes:
     return buf.raw
 
 
-def comm_create_local(tp_size: int):
-    """Handles of an emulated single-GPU TP group (one per rank; drive rank r from thread r)."""
+def comm_create_local(tp_size: int, ar_mode: int = AR_RING):
+    """Handles of an emulated single-GPU TP group (one per rank; drive rank r from thread r).
+    ar_mode: AR_RING (NCCL ring order, bf16 rounding per hop; default) or AR_F32 (fp32 sum, one rounding)."""
     arr = (C.c_void_p * tp_size)()
-    _check(lib.nf_comm_create_local(tp_size, arr))
+    _check(lib.nf_comm_create_local(tp_size, ar_mode, arr))
     return [arr[i] for i in range(tp_size)]
 
 
@@ -382,10 +421,11 @@ def comm_destroy(h: int):
     lib.nf_comm_destroy(C.c_void_p(h))
 
 
-def comm_create(tp_size: int, tp_rank: int, uid: bytes) -> int:
+def comm_create(tp_size: int, tp_rank: int, uid: bytes, max_ctas: int = 0) -> int:
+    """NCCL communicator; max_ctas > 0 caps NCCL's CTAs per collective (the plan's network SM budget)."""
     h = C.c_void_p()
     buf = C.create_string_buffer(uid, 128)
-    _check(lib.nf_comm_create(tp_size, tp_rank, buf, C.byref(h)))
+    _check(lib.nf_comm_create(tp_size, tp_rank, buf, max_ctas, C.byref(h)))
     return h.value
 
 

@@ -89,6 +89,21 @@ class Model:
                       ws.data_ptr(), ws.numel(), stream_handle(), comm)
         return next_ids
 
+    def step_inspect(self, plan: nf.Plan, pools: Sequence[torch.Tensor], b: nf.Batch, token_ids: torch.Tensor,
+                     ws: torch.Tensor, comm: Optional[int] = None, logits: bool = True, hidden: bool = True):
+        """nf_model_step_ex: (next_ids, logits [n_emit, V/N] or None, [L+1] hidden [T, D] or None)."""
+        dev = token_ids.device
+        T, D = b.n_tokens, self.cfg.d_model
+        next_ids = torch.empty(len(b.q_len), dtype=torch.int32, device=dev)
+        n_emit = len(b.q_len) if b.emit is None else int((b.emit != 0).sum())
+        lg = torch.empty((n_emit, self.cfg.vocab // self.cfg.tp_size), dtype=BF16, device=dev) if logits else None
+        hs = [torch.empty((T, D), dtype=BF16, device=dev) for _ in range(self.cfg.n_layers + 1)] if hidden else None
+        nf.model_step_ex(plan, self.handle, [p.data_ptr() for p in pools], b, token_ids.data_ptr(),
+                         next_ids.data_ptr(), ws.data_ptr(), ws.numel(), stream_handle(), comm,
+                         logits=lg.data_ptr() if lg is not None else 0,
+                         hidden=[h.data_ptr() for h in hs] if hs is not None else None)
+        return next_ids, lg, hs
+
 
 def shard_layer(w: Dict[str, torch.Tensor], n_q_heads: int, n_kv_heads: int, head_dim: int, tp: int,
                 rank: int) -> Dict[str, torch.Tensor]:
@@ -113,6 +128,12 @@ def shard_layer(w: Dict[str, torch.Tensor], n_q_heads: int, n_kv_heads: int, hea
         "w_down": c(w["w_down"][..., rank * fs:(rank + 1) * fs]),
         **({"w_router": w["w_router"]} if "w_router" in w else {}),
     }
+
+
+def shard_vocab(lm_head: torch.Tensor, tp: int, rank: int) -> torch.Tensor:
+    """Rank's rows of a [V, D] LM head (vocab-parallel head)."""
+    v = lm_head.shape[0] // tp
+    return lm_head[rank * v:(rank + 1) * v].contiguous()
 
 
 def shard_pool(pool: torch.Tensor, tp: int, rank: int) -> torch.Tensor:

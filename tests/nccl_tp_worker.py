@@ -1,0 +1,103 @@
+"""Worker of tests/test_gpu_nccl.py: one rank of a real NCCL TP group whose ranks all
+share GPU 0 (NCCL_HOSTID differs per process, so NCCL treats the ranks as separate
+hosts and moves data over its socket transport on loopback).  Exercises the shipped
+NCCL data plane -- nf_comm_create (CTA cap), ncclAllGather / ncclAllReduce in bf16
+on the plan's network stream / green-context partition, the 4-way / 2-way TP
+pipeline, the vocab-parallel LM head's AllGather, and CUDA-graph capture of a model
+step with NCCL inside -- and checks the result against the float64 oracle.
+Launched as: python tests/nccl_tp_worker.py <rank> <world> <port> <out.json>"""
+import json
+import os
+import sys
+
+rank, world, port, out_path = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+os.environ["NCCL_HOSTID"] = f"nf-test-host-{rank}"
+os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+os.environ.setdefault("NCCL_IB_DISABLE", "1")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+from oracle import layer as OL  # noqa: E402
+from paper_2408_12757_b200 import nf, runtime as rt  # noqa: E402
+
+torch.cuda.set_device(0)
+dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+res = {"rank": rank}
+uid = [nf.comm_unique_id() if rank == 0 else None]
+dist.broadcast_object_list(uid, src=0)
+comm = nf.comm_create(world, rank, uid[0], max_ctas=8)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda().to(torch.bfloat16)
+
+
+def gather_eq(t):
+    h = torch.tensor([float(t.float().sum()), float(t.float().abs().sum()), float((t.float() ** 2).sum())],
+                     dtype=torch.float64)
+    allh = [torch.empty_like(h) for _ in range(world)]
+    dist.all_gather(allh, h)
+    return all(torch.equal(allh[0], x) for x in allh)
+
+
+# ---- one layer, every mode (incl. the paper's 4/2 pipeline on green partitions)
+shape = synth.shape_with(synth.SHAPES["c1"], name="tp-small", n_q_heads=16, n_kv_heads=8, head_dim=64, d_ffn=2048,
+                         vocab=4096, n_layers=2)
+b = synth.make_batch([1] * 20 + [37, 1, 16, 1, 70], list(range(5, 205, 10)) + [0, 130, 33, 3, 20], seed=4,
+                     pool_slack=3)
+w = synth.layer_weights(shape, 0)
+x = synth.activations(shape, b.n_tokens)
+pool = synth.kv_pool(shape, b)
+ref = OL.decoder_layer(x, w, OL.as_pool(pool), b, shape)
+cfg = rt.cfg_from_shape(shape, tp_size=world, tp_rank=rank)
+wd = {k: dev(v) for k, v in w.items()}
+packed = rt.pack_layer(cfg, rt.shard_layer(wd, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, world, rank))
+nb = nf.Batch.from_any(b)
+ws = rt.workspace(cfg, nb)
+layer_res = {}
+for name, mode, shares, nd in [("sequential", nf.SEQUENTIAL, (1,), 0), ("nano", nf.NANO_ONLY, (1, 1, 1, 1), 2),
+                               ("overlap42", nf.OVERLAP, (1, 1, 1, 1), 2)]:
+    plan = nf.Plan.explicit(cfg, mode, shares=shares, sm=[116, 16, 116, 116, 116, 116, 16], n_dense=nd)
+    y = rt.layer_forward(plan, cfg, packed, rt.shard_pool(dev(pool), world, rank), nb, dev(x), ws=ws, comm=comm)
+    torch.cuda.synchronize()
+    out = y.float().cpu().numpy().astype(np.float64)
+    err = out - ref
+    layer_res[name] = {"rel_l2": float(np.linalg.norm(err) / np.linalg.norm(ref)), "max_abs": float(np.abs(err).max()),
+                       "ranks_identical": gather_eq(y), "partitions": plan.runtime_note()}
+res["layer"] = layer_res
+
+# ---- model step: vocab-parallel LM head (AG of (max, idx)) eager and CUDA-graph replay
+W = synth.model_weights(shape, seed=0)
+toks = synth.token_ids(b.n_tokens, shape.vocab)
+pools = [synth.kv_pool(shape, b, seed=2, layer=l) for l in range(2)]
+ids_ref, logits, _ = OL.model_step(toks, W, [OL.as_pool(p) for p in pools], b, shape, return_logits=True)
+layers = [rt.pack_layer(cfg, rt.shard_layer({k: dev(v) for k, v in W["layers"][l].items()}, shape.n_q_heads,
+                                            shape.n_kv_heads, shape.head_dim, world, rank)) for l in range(2)]
+model = rt.Model(cfg, dev(W["embed"]), layers, rt.pack_lm_head(cfg, rt.shard_vocab(dev(W["lm_head"]), world, rank),
+                                                                dev(W["final_norm"])))
+tok_d = torch.from_numpy(toks).cuda()
+srt = np.sort(logits, axis=1)
+sure = srt[:, -1] - srt[:, -2] > 0.1
+step_res = {}
+for name, graph in [("eager", False), ("graph", True)]:
+    plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1, 1, 1), sm=[116, 16, 116, 116, 116, 116, 16], n_dense=2,
+                            balance=2, graph=graph)
+    runs = []
+    for it in range(3):  # graph: capture, then two replays
+        ids = model.step(plan, [rt.shard_pool(dev(p), world, rank) for p in pools], nb, tok_d, ws, comm=comm)
+        torch.cuda.synchronize()
+        runs.append(ids.cpu().numpy())
+    step_res[name] = {"argmax_ok": bool(np.array_equal(runs[0][sure], ids_ref[sure])),
+                      "replays_identical": bool(all(np.array_equal(runs[0], r) for r in runs)),
+                      "ranks_identical": gather_eq(torch.from_numpy(runs[0])), "n_sure": int(sure.sum()),
+                      "graph_note": plan.runtime_note()}
+res["step"] = step_res
+json.dump(res, open(out_path, "w"))
+nf.comm_destroy(comm)
+dist.destroy_process_group()

@@ -34,7 +34,7 @@ def test_header_symbols_exported(nf):
     for n in names:
         assert hasattr(nf.lib, n), f"{n} declared in nf.h but not exported"
     assert set(names) == set(nf.EXPORTED)
-    assert nf.lib.nf_abi_version() == 2
+    assert nf.lib.nf_abi_version() == 3
 
 
 def _cfg(nf, shape, **kw):

@@ -73,3 +73,63 @@ def test_autosearch_errors_and_sequential(nf):
         nf.Plan.search(cfg, b, [], sm_budget=0)
     p = nf.Plan.search(cfg, b, [], mode=nf.SEQUENTIAL)
     assert p.spec().n_nano == 1 and list(p.spec().sm) == [148] * 7
+
+
+def synthetic_curves_tp():
+    pts = synthetic_curves()
+    for u in (8, 16, 24, 32, 48):
+        for w in (256.0, 1024.0, 4096.0):   # NET: AllGather-equivalent tokens (reading P-8)
+            pts.append((P.NET, u, w, 2.5e-8 * w * min(1.0, 16 / u) ** 0.8 + 8e-6))
+    return pts
+
+
+def test_tp_pipeline_dag_structure():
+    """Reading P-8: per layer five collectives in the fixed order
+    AG_attn(H1), AG_o(H1), AR_o(H2), AR_d(H1), AR_d(H2); column O waits for the
+    attention AllGather, row O for the decode attention of Q3 and Q4, Up/Gate of H1
+    for AG_o, of H2 for AR_o; the next layer's KQV of a half waits for its AR_d."""
+    work = [(300, 1000, 0), (300, 900, 0), (200, 800, 5000), (200, 700, 0)]
+    nodes = P.build_pipeline_tp(work, n_layers=2)
+    kinds = [n.kind for n in nodes]
+    assert kinds.count(P.NET) == 10 and kinds.count(P.KQV) == 8 and kinds.count(P.O) == 4
+    net = [n for n in nodes if n.kind == P.NET]
+    assert [(n.nano, n.work) for n in net[:5]] == [(0, 600), (0, 600), (1, 800), (0, 1200), (1, 800)]
+    by_id = {n.id: n for n in nodes}
+    o1, o2 = [n for n in nodes if n.kind == P.O][:2]
+    assert net[0].id in o1.deps
+    dec = [n for n in nodes if n.kind == P.DECODE]
+    assert dec[2].id in o2.deps and dec[3].id in o2.deps
+    ug = [n for n in nodes if n.kind == P.UG][:2]
+    assert net[1].id in ug[0].deps and net[2].id in ug[1].deps
+    kqv2 = [n for n in nodes if n.kind == P.KQV][4:]
+    assert net[3].id in kqv2[0].deps and net[3].id in kqv2[1].deps
+    assert net[4].id in kqv2[2].deps and net[4].id in kqv2[3].deps
+    for n in nodes:
+        assert all(d < n.id for d in n.deps)
+        for d in n.deps:
+            assert d in by_id
+
+
+def test_tp_autosearch_matches_oracle(nf):
+    """nf_plan_create at tp_size 8 (the 70B TP8 rank) == the oracle's reading-P-8 search."""
+    from paper_2408_12757_b200.runtime import cfg_from_shape
+    pts = synthetic_curves_tp()
+    b = synth.workload_batch(512, 512, 1024)
+    q_len, prefix = list(map(int, b.q_len)), list(map(int, b.kv_prefix))
+    cfg = cfg_from_shape(synth.SHAPES["llama2-70b"], tp_size=8, tp_rank=3)
+    iters = 30
+    best, table = P.search_tp(q_len, prefix, P.Curves(pts), budget=148, q=8, max_iters=iters, n_layers=3)
+    plan = nf.Plan.search(cfg, nf.Batch.from_any(b), pts, sm_budget=148, sm_quantum=8, mode=nf.OVERLAP, n_nano=4,
+                          max_iters=iters)
+    spec = plan.spec()
+    assert spec.n_nano == 4 and spec.n_dense == 2
+    assert [spec.share[i] for i in range(4)] == best[0]
+    kinds = sorted({n.kind for n in best[3]})
+    assert P.NET in kinds
+    assert [spec.sm[k] for k in kinds] == [best[1][k] for k in kinds]
+    csv = [l.split(",") for l in plan.csv().splitlines()[1:]]
+    assert len(csv) == len(best[3])
+    assert max(float(r[5]) for r in csv) == pytest.approx(best[2], rel=1e-7)
+    # lower bound: never worse than the whole budget per kind (SPEC S:423)
+    seq = P.simulate(best[3], [148] * P.N_KINDS, P.Curves(pts), 148)[0]
+    assert best[2] <= seq + 1e-12
