@@ -112,7 +112,7 @@ def config_shape(config, tp=1):
     if config == "c3rank":
         return (synth.shape_with(synth.SHAPES["llama2-70b"], name="llama2-70b-tp8-rank", n_q_heads=8, n_kv_heads=1,
                                  d_ffn=28672 // 8), 512, 1024)
-    if config == "c3":
+    if config in ("c3", "c3loop"):
         return synth.SHAPES["llama2-70b"], 512, 1024
     if config == "c4rank":
         return mixtral_rank_shape(), 512, 1024
@@ -136,6 +136,11 @@ def workload_desc(config, L, tp=1, b_dense=2048):
         return (f"configs[2] rank-local proxy: one LLaMA-2-70B TP8 rank's shards (D 8192, 8/1 heads, "
                 f"F 3584), {L} layers, B_dense 2048 (1365 decode ctx 512-1535 + 171 chunk + 512 prompt), "
                 f"no collectives")
+    if config == "c3loop":
+        return (f"configs[2] rank proxy: rank 0 of a LLaMA-2-70B TP8 group on one GPU ({L} layers, its head / FFN / "
+                f"vocab shards, B_dense 2048 = 1365 decode ctx 512-1535 + 171 chunk + 512 prompt) running the TP "
+                f"pipeline with loopback collectives (local copies of the AllGather / AllReduce bytes, no peers); "
+                f"value = 2048 / (T_step x 8) tokens/s/GPU")
     if config == "c4rank":
         return (f"configs[3] rank-local proxy: one Mixtral-8x7B TP8 rank's shards (D 4096, 4/1 heads, 8 experts "
                 f"x F 1792, top-2), {L} layers, B_dense 2048 (1365 decode ctx 512-1535 + 171 chunk + 512 prompt), "
@@ -280,6 +285,9 @@ def run_nf(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     tp = 1
     comm = None
+    loop = args.config == "c3loop"
+    if loop:
+        tp = 8   # rank 0 of a TP8 group, loopback collectives
     if args.config in ("c3", "c4"):
         # configs[2] / [3]: tensor parallel over all ranks (NCCL over NVLink)
         if world < 2:
@@ -293,7 +301,7 @@ def run_nf(args, rank, world, local_rank):
     b = synth.workload_batch(b_dense, p_in, d_out)
     T = b.n_tokens
     nb = nf.Batch.from_any(b)
-    cfg = rt.cfg_from_shape(shape, tp_size=tp, tp_rank=rank if tp > 1 else 0)
+    cfg = rt.cfg_from_shape(shape, tp_size=tp, tp_rank=rank if (tp > 1 and not loop) else 0)
 
     # ---------------- plan (chosen before the communicator: its network SM budget caps NCCL's CTAs)
     sm = [int(x) for x in args.sm.split(",")] if args.sm else None
@@ -305,10 +313,13 @@ def run_nf(args, rank, world, local_rank):
         args.mode = "sequential" if args.config in ("c3rank", "c4rank") else "overlap"
     n_dense = 0
     if args.mode == "overlap":
-        if args.plan == "auto":
-            rows = [l.split(",") for l in open(os.path.join(ROOT, args.curves)).read().splitlines()[1:] if l.strip()]
+        if args.plan in ("auto", "refine") and not (tp > 1 and not os.path.exists(os.path.join(ROOT, args.curves_tp))):
+            cpath = os.path.join(ROOT, args.curves_tp if tp > 1 else args.curves)
+            rows = [l.split(",") for l in open(cpath).read().splitlines()[1:] if l.strip()]
             pts = [(int(k), int(u), float(w), float(t)) for k, _, u, w, t in rows]
-            plan = nf.Plan.search(cfg, nb, pts, mode=nf.OVERLAP, n_nano=4 if tp > 1 else 2)
+            sp = nf.Plan.search(cfg, nb, pts, mode=nf.OVERLAP, n_nano=4 if tp > 1 else 2).spec()
+            sp.graph = int(not args.no_graph)
+            plan = nf.Plan.from_spec(cfg, sp)
         elif args.colocate:
             plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=sm or [148] * 7, balance=True,
                                     colocate=True)
@@ -317,7 +328,8 @@ def run_nf(args, rank, world, local_rank):
             # paper's 4-way KQV/attention, 2-way O/UGD/network split with a network
             # partition for the collectives
             dense, dec, net, dshares = {"c2": (116, 32, 8, "1,1"), "c4rank": (132, 16, 8, "3,5"),
-                                        "c3": (116, 16, 16, "1,1,1,1"), "c4": (116, 16, 16, "1,1,1,1")}.get(
+                                        "c3": (116, 16, 16, "1,1,1,1"), "c4": (116, 16, 16, "1,1,1,1"),
+                                        "c3loop": (116, 16, 16, "1,1,1,1")}.get(
                 args.config, (132, 16, 8, "1,1"))
             shares = tuple(int(x) for x in (args.shares or dshares).split(","))
             n_dense = 2 if (tp > 1 and len(shares) == 4) else 0
@@ -328,7 +340,9 @@ def run_nf(args, rank, world, local_rank):
                                 balance=args.balance, graph=not args.no_graph)
     else:
         plan = nf.Plan.explicit(cfg, nf.SEQUENTIAL, sm=sm, graph=not args.no_graph)
-    if tp > 1:
+    if loop:
+        comm = nf.comm_create_loopback(tp, 0)
+    elif tp > 1:
         uid = [nf.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = nf.comm_create(tp, rank, uid[0], max_ctas=plan.spec().sm[nf.OP_NET])
@@ -352,17 +366,19 @@ def run_nf(args, rank, world, local_rank):
     qs, ks, Dl, Fl = Hq // tp * hd, Hk // tp * hd, D // tp, F // tp
 
     def full_layer(gen):
-        w = {"attn_norm": randn((D,), 0.1, 1.0, g_rep), "w_q": randn((Hq * hd, D), D ** -0.5, gen),
-             "w_k": randn((Hk * hd, D), D ** -0.5, gen), "w_v": randn((Hk * hd, D), D ** -0.5, gen),
-             "w_o": randn((D, Hq * hd), (Hq * hd) ** -0.5, gen), "ffn_norm": randn((D,), 0.1, 1.0, g_rep),
-             "w_gate": randn(ex + (F, D), D ** -0.5, gen), "w_up": randn(ex + (F, D), D ** -0.5, gen),
-             "w_down": randn(ex + (D, F), F ** -0.5, gen)}
+        w = {"attn_norm": randn((D,), 0.1, 1.0, gen=g_rep), "w_q": randn((Hq * hd, D), D ** -0.5, gen=gen),
+             "w_k": randn((Hk * hd, D), D ** -0.5, gen=gen), "w_v": randn((Hk * hd, D), D ** -0.5, gen=gen),
+             "w_o": randn((D, Hq * hd), (Hq * hd) ** -0.5, gen=gen), "ffn_norm": randn((D,), 0.1, 1.0, gen=g_rep),
+             "w_gate": randn(ex + (F, D), D ** -0.5, gen=gen), "w_up": randn(ex + (F, D), D ** -0.5, gen=gen),
+             "w_down": randn(ex + (D, F), F ** -0.5, gen=gen)}
         if E:
-            w["w_router"] = randn((E, D), D ** -0.5, g_rep)
+            w["w_router"] = randn((E, D), D ** -0.5, gen=g_rep)
         return w
 
+    srank = 0 if loop else rank
+
     def shard_of(w):
-        return w if tp == 1 else rt.shard_layer(w, Hq, Hk, hd, tp, rank)
+        return w if tp == 1 else rt.shard_layer(w, Hq, Hk, hd, tp, srank)
 
     layers = []
     w0_full = None
@@ -373,23 +389,23 @@ def run_nf(args, rank, world, local_rank):
                 w0_full = w
             layers.append(rt.pack_layer(cfg, shard_of(w)))
         else:  # this rank's shards only
-            w = {"attn_norm": randn((D,), 0.1, 1.0, g_rep), "w_q": randn((qs, D), D ** -0.5),
+            w = {"attn_norm": randn((D,), 0.1, 1.0, gen=g_rep), "w_q": randn((qs, D), D ** -0.5),
                  "w_k": randn((ks, D), D ** -0.5), "w_v": randn((ks, D), D ** -0.5),
                  "w_o_col": randn((Dl, Hq * hd), (Hq * hd) ** -0.5), "w_o_row": randn((D, qs), (Hq * hd) ** -0.5),
-                 "ffn_norm": randn((D,), 0.1, 1.0, g_rep), "w_gate": randn(ex + (Fl, D), D ** -0.5),
+                 "ffn_norm": randn((D,), 0.1, 1.0, gen=g_rep), "w_gate": randn(ex + (Fl, D), D ** -0.5),
                  "w_up": randn(ex + (Fl, D), D ** -0.5), "w_down": randn(ex + (D, Fl), F ** -0.5)}
             if E:
-                w["w_router"] = randn((E, D), D ** -0.5, g_rep)
+                w["w_router"] = randn((E, D), D ** -0.5, gen=g_rep)
             layers.append(rt.pack_layer(cfg, w))
         del w
     embed = randn((shape.vocab, D), gen=g_rep)
-    lm_full = randn((shape.vocab, D), D ** -0.5, g_rep)
-    lm = rt.pack_lm_head(cfg, rt.shard_vocab(lm_full, tp, rank) if tp > 1 else lm_full, randn((D,), 0.1, 1.0, g_rep))
+    lm_full = randn((shape.vocab, D), D ** -0.5, gen=g_rep)
+    lm = rt.pack_lm_head(cfg, rt.shard_vocab(lm_full, tp, srank) if tp > 1 else lm_full, randn((D,), 0.1, 1.0, gen=g_rep))
     del lm_full
     model = rt.Model(cfg, embed, layers, lm)
     # KV pools: layer 0 full (replicated seed) then this rank's heads; the rest per rank
     pool0_full = randn((b.n_pages_pool, 2, Hk, 16, hd), gen=g_rep)
-    pools = [rt.shard_pool(pool0_full, tp, rank) if tp > 1 else pool0_full.clone()]
+    pools = [rt.shard_pool(pool0_full, tp, srank) if tp > 1 else pool0_full.clone()]
     pools += [randn((b.n_pages_pool, 2, Hk // tp, 16, hd)) for _ in range(1, L)]
     tok = torch.randint(0, shape.vocab, (T,), dtype=torch.int32, device=dev, generator=g_rep)
     ws = rt.workspace(cfg, nb, dev)
@@ -398,7 +414,9 @@ def run_nf(args, rank, world, local_rank):
 
     # ---------------- in-run parity (before timing; its step rewrites the same KV slots the timed steps do)
     parity = None
-    if not args.no_parity and not E:
+    if loop:
+        parity = {"skipped": "loopback collectives do not reduce: the proxy's values are not the model's"}
+    elif not args.no_parity and not E:
         key = "c3_768" if (args.config == "c3" and tp == 2) else ("c3" if args.config in ("c3", "c3rank") else "c2")
         reqs = [r for r in PARITY_REQS[key] if r < b.n_req]
         if rank == 0:
@@ -423,6 +441,73 @@ def run_nf(args, rank, world, local_rank):
     del w0_full, pool0_full
     torch.cuda.empty_cache()
     stream = torch.cuda.current_stream()
+
+    # ---------------- measured refinement of the (searched) plan: coordinate moves of the memory
+    # partition (+-8 SMs) and the nano-batch token shares (+-1/8), kept while the measured
+    # step time (max over ranks) improves by > 0.5 %; the network partition is held fixed
+    refine_log = []
+    if args.plan == "refine" and plan.spec().mode == nf.OVERLAP and not plan.spec().colocate:
+        def timed(pl, n=4):
+            for _ in range(2):
+                model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(n):
+                model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([a0.elapsed_time(a1) / n], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+
+        def variant(base, dec, s8):
+            sp = nf.PlanSpec()
+            for f, _ in nf.PlanSpec._fields_:
+                setattr(sp, f, getattr(base, f))
+            for k in range(nf.OP_COUNT):
+                sp.sm[k] = base.sm[k]
+            sp.sm[nf.OP_DECODE_ATTN] = dec
+            for k in (nf.OP_KQV, nf.OP_PREFILL_ATTN, nf.OP_O, nf.OP_UG, nf.OP_DOWN):
+                sp.sm[k] = 148
+            sh = (s8, s8, 8 - s8, 8 - s8) if base.n_nano == 4 else (s8, 8 - s8)
+            for i, v in enumerate(sh):
+                sp.share[i] = v
+            return nf.Plan.from_spec(cfg, sp)
+
+        base = plan.spec()
+        tot = sum(base.share[:base.n_nano])
+        s8 = max(1, min(7, round(8 * base.share[0] * (2 if base.n_nano == 4 else 1) / tot)))
+        dec = max(8, (base.sm[nf.OP_DECODE_ATTN] + 7) // 8 * 8)
+        cur = variant(base, dec, s8)
+        best_t = timed(cur)
+        refine_log.append({"dec_sms": dec, "share8": s8, "ms": best_t})
+        seen = {(dec, s8)}
+        for _move in range(8):
+            cands = [(dec + dd, s8 + ds) for dd, ds in ((-8, 0), (8, 0), (0, -1), (0, 1))
+                     if 8 <= dec + dd <= 64 and 1 <= s8 + ds <= 7 and (dec + dd, s8 + ds) not in seen]
+            if not cands:
+                break
+            res = []
+            for d2, s2 in cands:
+                seen.add((d2, s2))
+                pl = variant(base, d2, s2)
+                t = timed(pl)
+                refine_log.append({"dec_sms": d2, "share8": s2, "ms": t})
+                res.append((t, d2, s2, pl))
+            t, d2, s2, pl = min(res, key=lambda x: x[0])
+            if t >= best_t * 0.995:
+                break
+            best_t, dec, s8, cur = t, d2, s2, pl
+        plan = cur
+    if world > 1:   # every rank must hold the same plan: same collectives in the same order
+        hs = [None] * world
+        dist.all_gather_object(hs, plan.hash())
+        if len(set(hs)) != 1:
+            raise SystemExit(f"plan hashes differ across ranks: {hs}")
 
     def step(pl=plan):
         model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
@@ -453,7 +538,7 @@ def run_nf(args, rank, world, local_rank):
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms_max = float(t_max.item())
     ms_step = ms_max / args.steps
-    replicas = world // tp                                    # independent model copies (1 under TP)
+    replicas = world // tp if not loop else 1.0 / tp           # independent model copies (1 under TP)
     value = replicas * T * args.steps / (ms_max / 1e3)
 
     # ---------------- per-op times: a separate instrumented pass (eager launches, CUDA events per kernel)
@@ -632,7 +717,9 @@ def run_nf(args, rank, world, local_rank):
                  "parallelism": (f"tp{tp}" if tp > 1 else ("replicas" if world > 1 else "single-gpu")),
                  "sm": list(plan.spec().sm), "shares": list(plan.spec().share)[:plan.spec().n_nano],
                  "n_dense": int(plan.spec().n_dense), "cuda_graph": bool(plan.spec().graph),
-                 "source": args.plan, "partitions": plan.runtime_note()}
+                 "source": {"explicit": "measured default", "auto": "nf_plan_create",
+                            "refine": "nf_plan_create + measured refinement"}[args.plan],
+                 "refinement": refine_log, "hash": f"{plan.hash():016x}", "partitions": plan.runtime_note()}
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if tp > 1 else "weak",
@@ -692,14 +779,17 @@ def main():
     ap.add_argument("--impl", default="nf", choices=["nf", "reference"])
     ap.add_argument("--mode", default="auto", choices=["auto", "overlap", "nano", "sequential"],
                     help="auto: the measured-best plan kind per config (OVERLAP except the c3rank/c4rank proxies)")
-    ap.add_argument("--plan", default="explicit", choices=["explicit", "auto"],
-                    help="auto: nf_plan_create autosearch over --curves (overlap mode)")
+    ap.add_argument("--plan", default="explicit", choices=["explicit", "auto", "refine"],
+                    help="auto: nf_plan_create autosearch over --curves (overlap mode); refine: the searched plan "
+                         "(or the explicit default when no curves exist) refined by measured coordinate moves")
     ap.add_argument("--curves", default="profiles/curves_b200_quick.csv")
+    ap.add_argument("--curves-tp", default="profiles/curves_b200_tp8.csv",
+                    help="curves with NET points for the TP autosearch")
     ap.add_argument("--shares", default="", help="nano-batch token shares (overlap / nano modes; default per config)")
     ap.add_argument("--balance", type=int, default=2, help="0 request order, 1 balanced, 2 exact shares + KV")
     ap.add_argument("--colocate", action="store_true", help="attention CTAs co-resident with GEMM CTAs")
     ap.add_argument("--sm", default="", help="comma-separated SM budget per op kind (7 values)")
-    ap.add_argument("--config", default="", choices=["", "c2", "c3", "c3rank", "c4", "c4rank"],
+    ap.add_argument("--config", default="", choices=["", "c2", "c3", "c3rank", "c3loop", "c4", "c4rank"],
                     help="default: c2 at N=1, c3 at N>1.  c2: configs[1] 8B 1 GPU (replicas for N>1); c3: configs[2] "
                          "70B TP=N over NCCL (the metric's config); c3rank: 1-GPU proxy of one TP8 rank; "
                          "c4: configs[3] Mixtral-8x7B TP=N; c4rank: its 1-GPU TP8-rank proxy")

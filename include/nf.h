@@ -158,6 +158,10 @@ nf_status nf_plan_get_spec(const nf_plan* plan, nf_plan_spec* out);
 /* Gantt CSV `node_id,kind,nano_index,units,start_s,end_s` of the searched schedule. */
 nf_status nf_plan_export_csv(const nf_plan* plan, char* buf, size_t cap, size_t* len);
 void nf_plan_destroy(nf_plan* plan);
+/* 64-bit hash of the plan's launch decisions and model config (tp_rank excluded).  The
+ * ranks of one TP group must hold plans with equal hashes: they then issue the same
+ * collectives in the same order (callers check it with one AllGather at setup). */
+uint64_t nf_plan_hash(const nf_plan* plan);
 /* How an OVERLAP plan partitions the GPU at run time (green-context SM
  * partitions, or why they are not used).  Valid until the plan is destroyed. */
 const char* nf_plan_runtime_note(const nf_plan* plan);
@@ -181,6 +185,11 @@ nf_status nf_comm_create(int32_t tp_size, int32_t tp_rank, const void* id_128, i
  * Both are bit-identical on all ranks.  comms_out: [tp_size]. */
 enum { NF_AR_F32 = 0, NF_AR_RING = 1 };
 nf_status nf_comm_create_local(int32_t tp_size, int32_t ar_mode, nf_comm** comms_out);
+/* Performance proxy of one rank of a tp_size group on one GPU (bench --config c3loop):
+ * collectives move this rank's bytes locally (AllGather: its buffer copied into every
+ * slot; AllReduce: a local copy, values unchanged) -- the rank's compute, pipeline and
+ * local copy traffic without peers.  Results are NOT the model's (no reduction). */
+nf_status nf_comm_create_loopback(int32_t tp_size, int32_t tp_rank, nf_comm** out);
 void nf_comm_destroy(nf_comm* comm);
 
 /* ------------------------------------------------------------------ weights */
@@ -282,6 +291,12 @@ size_t nf_moe_route_ws_bytes(const nf_model_cfg* cfg, int32_t T);
 nf_status nf_moe_route(const nf_model_cfg* cfg, const void* h1, const void* router_packed, int32_t T, int32_t* ids,
                        float* wts, int32_t* grp_off, int32_t* dst, int32_t* row_tok, void* ws, size_t ws_bytes,
                        void* stream);
+
+/* Inspection (parity tests): device pointer to the routing ids [T, top_k] that the most
+ * recent nf_layer_forward with this workspace and batch chose (rows in the caller's token
+ * order; the experts of each row by descending logit).  Valid until the workspace is reused. */
+nf_status nf_moe_last_ids(const nf_model_cfg* cfg, const nf_batch* b, const void* ws, size_t ws_bytes,
+                          const int32_t** ids_out);
 
 /* ------------------------------------------------------------------ serving loop (NEXT-4) */
 /* Global batch scheduler + KV-cache manager (host, C++): continuous batching with

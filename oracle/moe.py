@@ -58,13 +58,26 @@ def expert_ffn(h2, w_gate_e, w_up_e, w_down_e):
     return (silu(h2 @ f64(w_gate_e).T) * (h2 @ f64(w_up_e).T)) @ f64(w_down_e).T
 
 
-def moe_ffn(h1, w: Dict[str, np.ndarray], shape, return_route: bool = False):
+def forced_weights(logits, ids):
+    """Reading A-21 weights for a given selection: softmax over the selected logits."""
+    sel = np.take_along_axis(f64(logits), np.asarray(ids, dtype=np.int64), axis=1)
+    p = np.exp(sel - sel.max(axis=1, keepdims=True))
+    return p / p.sum(axis=1, keepdims=True)
+
+
+def moe_ffn(h1, w: Dict[str, np.ndarray], shape, return_route: bool = False, forced_ids=None):
     """out = h1 + sum_j w_j * expert_{e_j}(h2), h2 = RMSNorm(h1) * g_ffn (A-20..A-22).
 
-    w: ffn_norm [D], w_router [E, D], w_gate / w_up [E, F, D], w_down [E, D, F]."""
+    w: ffn_norm [D], w_router [E, D], w_gate / w_up [E, F, D], w_down [E, D, F].
+    forced_ids [T, k] (optional): use this expert selection instead of the top-k (the
+    weights are still A-21's softmax over the selected logits) -- for comparing rows
+    whose top-k is a near-tie with the selection another implementation made."""
     h1 = f64(h1)
     h2 = rmsnorm(h1, w["ffn_norm"], shape.rms_eps)
     ids, wts, logits = router_topk(h2, w["w_router"], shape.top_k)
+    if forced_ids is not None:
+        ids = np.asarray(forced_ids, dtype=np.int64).reshape(ids.shape)
+        wts = forced_weights(logits, ids)
     out = h1.copy()
     for e in range(shape.n_experts):
         rows, slot = np.nonzero(ids == e)
@@ -129,12 +142,12 @@ def group_rows(ids, n_experts: int, tile: int = 128):
 
 
 def moe_decoder_layer(x, w: Dict[str, np.ndarray], pool: np.ndarray, batch, shape, page_size: int = 16,
-                      return_route: bool = False):
+                      return_route: bool = False, forced_ids=None):
     """Decoder layer with the MoE FFN: steps 1-6 of
     ``oracle.layer.decoder_layer`` (attention block unchanged), then moe_ffn."""
     from . import layer as OL
     h1 = OL.attention_block(x, w, pool, batch, shape, page_size)
-    return moe_ffn(h1, w, shape, return_route=return_route)
+    return moe_ffn(h1, w, shape, return_route=return_route, forced_ids=forced_ids)
 
 
 def moe_model_layers(x, layers: List[Dict[str, np.ndarray]], pools, batch, shape, page_size: int = 16):

@@ -528,6 +528,22 @@ nf_status nf_plan_export_csv(const nf_plan* plan, char* buf, size_t cap, size_t*
   return NF_OK;
 }
 
+uint64_t nf_plan_hash(const nf_plan* p) {
+  if (!p) return 0;
+  // FNV-1a over the model config and the plan spec (the executor's launch decisions);
+  // ranks of one TP group must agree on it (collective issue order)
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void* d, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(d);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  nf_model_cfg c = p->cfg;
+  c.tp_rank = 0;  // the rank differs by design
+  mix(&c, sizeof(c));
+  mix(&p->spec, sizeof(p->spec));
+  return h;
+}
+
 const char* nf_plan_runtime_note(const nf_plan* p) {
   if (!p) return "";
   nf_plan* q = const_cast<nf_plan*>(p);
@@ -544,6 +560,7 @@ void nf_plan_destroy(nf_plan* p) {
   }
   if (p->ev_join) cudaEventDestroy(p->ev_join);
   if (p->net_stream) cudaStreamDestroy(p->net_stream);
+  if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->ev_c2n) cudaEventDestroy(p->ev_c2n);
   if (p->ev_n2c) cudaEventDestroy(p->ev_n2c);
   for (int k = 0; k < NF_MAX_NANO; ++k)
@@ -965,9 +982,13 @@ nf_status run_moe_ffn(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat1
     g.row_w = w->mo_roww;
     g.row_inv = w->mo_rowinv;
     g.tile = GEMM_BM;
-    NF_CUDA(launch_moe_route(h1 + nr.t0 * D, M, (int)D, (const float*)wt->w_router, E, k, c->rms_eps, w->mo_ids,
-                             w->mo_wts, w->mo_inv, g, L.cs));
-    NF_CUDA(launch_moe_scatter(h1 + nr.t0 * D, M, (int)D, k, E, w->mo_ids, w->mo_wts, w->mo_inv, g, w->mo_dst,
+    // routing of the nano-batch's rows at their row offset (the whole batch's routing stays
+    // in the workspace after a layer: nf_moe_last_ids)
+    NF_CUDA(launch_moe_route(h1 + nr.t0 * D, M, (int)D, (const float*)wt->w_router, E, k, c->rms_eps,
+                             w->mo_ids + (int64_t)nr.t0 * k, w->mo_wts + (int64_t)nr.t0 * k, w->mo_inv + nr.t0, g,
+                             L.cs));
+    NF_CUDA(launch_moe_scatter(h1 + nr.t0 * D, M, (int)D, k, E, w->mo_ids + (int64_t)nr.t0 * k,
+                               w->mo_wts + (int64_t)nr.t0 * k, w->mo_inv + nr.t0, g, w->mo_dst + (int64_t)nr.t0 * k,
                                w->mo_x, L.cs));
   }
   const int stages = L.p->spec.colocate ? 3 : 4;
@@ -1015,7 +1036,7 @@ nf_status run_moe_ffn(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat1
   }
   {
     ProfScope ps(NF_PROF_MISC, L.cs);
-    NF_CUDA(launch_moe_combine(w->mo_y, w->mo_dst, M, k, (int)D, resid ? resid + nr.t0 * D : nullptr, out + nr.t0 * D,
+    NF_CUDA(launch_moe_combine(w->mo_y, w->mo_dst + (int64_t)nr.t0 * k, M, k, (int)D, resid ? resid + nr.t0 * D : nullptr, out + nr.t0 * D,
                                part_out ? part_out + nr.t0 : nullptr, T, nullptr, L.cs));
   }
   return NF_OK;
@@ -1517,13 +1538,20 @@ nf_status model_step_launches(nf_plan* p, nf_comm* comm, const nf_model_weights*
     }
     if (out->logits) {
       // inspection: logits of the emitting rows in caller request order (plain store epilogue)
-      NF_CUDA(launch_gather_rows(x, wsp.meta + m.off_emit_sorted, m.n_emit, D, wsp.lm_rows, nullptr, cs));
+      // (the argmax above skips the final RMSNorm's positive row scale 1/rms, which cannot
+      // change a row's argmax; the logits apply it)
+      NF_CUDA(launch_gather_rows(x, wsp.meta + m.off_emit_sorted, m.n_emit, D, wsp.lm_rows, wsp.lm_part, cs));
       GemmArgs s{};
       s.epi = EPI_STORE;
       s.M = m.n_emit;
       s.N = Vl;
       s.K = D;
       s.n_valid = Vl;
+      s.norm_part = wsp.lm_part;
+      s.norm_nparts = 1;
+      s.norm_stride = m.n_emit;
+      s.inv_d = 1.f / D;
+      s.eps = c->rms_eps;
       s.out = (__nv_bfloat16*)out->logits;
       s.ldo = Vl;
       NF_CUDA(launch_gemm(wsp.lm_rows, D, (const __nv_bfloat16*)w->lm_head_packed, D, s, num_sms(), cs));
@@ -1546,9 +1574,10 @@ nf_status model_step_launches(nf_plan* p, nf_comm* comm, const nf_model_weights*
 std::vector<int64_t> graph_key(const nf_plan* p, nf_comm* comm, const nf_model_weights* w, void* const* kv_pools,
                                const nf_batch* b, const int32_t* token_ids, const nf_step_outputs* out,
                                const StepMeta& m, void* ws, cudaStream_t cs) {
+  (void)cs;
   std::vector<int64_t> k{(int64_t)(uintptr_t)comm, (int64_t)(uintptr_t)w->embed, (int64_t)(uintptr_t)w->lm_head_packed,
                          (int64_t)(uintptr_t)token_ids, (int64_t)(uintptr_t)out->next_ids, (int64_t)(uintptr_t)ws,
-                         (int64_t)(uintptr_t)cs, b->n_req, b->n_pages_pool, m.T, m.n_emit,
+                         b->n_req, b->n_pages_pool, m.T, m.n_emit,
                          (int64_t)m.off_pos, (int64_t)m.off_slot, (int64_t)m.off_pages, (int64_t)m.off_dec,
                          (int64_t)m.off_pf, (int64_t)m.off_emit_row, (int64_t)m.off_emit_req,
                          (int64_t)m.off_tok_src, (int64_t)m.off_emit_sorted};
@@ -1592,7 +1621,7 @@ nf_status model_step_impl(const nf_plan* plan, nf_comm* comm, const nf_model_wei
   NF_TRY(upload_meta(p, m, wsp.meta, cs));
   // CUDA graph (plan spec.graph): not with an emulated group (host barriers inside the
   // collectives), inspection outputs or per-launch profiling
-  const bool want_graph = p->spec.graph && !comm_emulated(comm) && !out->logits && !out->hidden && !profile_active();
+  const bool want_graph = p->spec.graph && !comm_host_sync(comm) && !out->logits && !out->hidden && !profile_active();
   if (!want_graph) return model_step_launches(p, comm, w, kv_pools, b, token_ids, out, m, wsp, cs);
   std::vector<int64_t> key = graph_key(p, comm, w, kv_pools, b, token_ids, out, m, ws, cs);
   for (auto& g : p->graphs)
@@ -1601,10 +1630,14 @@ nf_status model_step_impl(const nf_plan* plan, nf_comm* comm, const nf_model_wei
       count_launch(1);
       return NF_OK;
     }
-  NF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-  const nf_status st = model_step_launches(p, comm, w, kv_pools, b, token_ids, out, m, wsp, cs);
+  // capture on the plan's own stream (the caller's may be the legacy default stream,
+  // which cannot be captured); the graph is then launched on the caller's stream,
+  // after the metadata upload
+  if (!p->cap_stream) NF_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+  NF_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+  const nf_status st = model_step_launches(p, comm, w, kv_pools, b, token_ids, out, m, wsp, p->cap_stream);
   cudaGraph_t graph = nullptr;
-  const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+  const cudaError_t ce = cudaStreamEndCapture(p->cap_stream, &graph);
   if (st != NF_OK) {
     if (graph) cudaGraphDestroy(graph);
     return st;
@@ -1734,6 +1767,18 @@ nf_status nf_moe_route(const nf_model_cfg* c, const void* h1, const void* router
                            c->top_k, c->rms_eps, ids, wts, inv, g, st));
   NF_CUDA(launch_moe_scatter((const __nv_bfloat16*)h1, T, c->d_model, c->top_k, c->n_experts, ids, wts, inv, g, dst,
                              nullptr, st));
+  return NF_OK;
+}
+
+nf_status nf_moe_last_ids(const nf_model_cfg* c, const nf_batch* b, const void* ws, size_t ws_bytes,
+                          const int32_t** ids_out) {
+  NF_TRY(validate_cfg(c));
+  NF_TRY(validate_batch(c, b));
+  if (c->n_experts <= 0) return set_error(NF_EINVAL, "not a MoE model");
+  if (!ws || !ids_out) return set_error(NF_EINVAL, "NULL pointer");
+  Workspace w = carve_workspace(c, b, const_cast<void*>(ws));
+  if (ws_bytes < w.total) return set_error(NF_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, w.total);
+  *ids_out = w.mo_ids;
   return NF_OK;
 }
 

@@ -56,6 +56,7 @@ struct nf_comm {
   int tp_size = 1, tp_rank = 0;
   int max_ctas = 0;                        // NCCL CTA cap (0 = NCCL default)
   int ar_mode = NF_AR_F32;                 // emulated AllReduce arithmetic
+  bool loopback = false;                   // nf_comm_create_loopback: one rank, local copies
   std::shared_ptr<nf::LocalGroup> group;  // emulated group (nf_comm_create_local)
 };
 
@@ -93,11 +94,19 @@ nf_status load_nccl() {
 
 int comm_size(const nf_comm* c) { return c ? c->tp_size : 1; }
 int comm_rank(const nf_comm* c) { return c ? c->tp_rank : 0; }
-bool comm_emulated(const nf_comm* c) { return c && c->group; }
+bool comm_emulated(const nf_comm* c) { return c && (c->group || c->loopback); }
+bool comm_host_sync(const nf_comm* c) { return c && c->group; }
 int comm_max_ctas(const nf_comm* c) { return c ? c->max_ctas : 0; }
 
 // recv = [rank 0's send | rank 1's send | ...] (count bf16 elements each)
 nf_status comm_all_gather(nf_comm* c, const void* send, void* recv, size_t count_bf16, cudaStream_t st) {
+  if (c->loopback) {  // this rank's buffer into every slot: the AllGather's bytes, no peers
+    for (int q = 0; q < c->tp_size; ++q)
+      if (cudaMemcpyAsync((char*)recv + q * count_bf16 * 2, send, count_bf16 * 2, cudaMemcpyDeviceToDevice, st) !=
+          cudaSuccess)
+        return set_error(NF_ECUDA, "loopback AG copy");
+    return NF_OK;
+  }
   if (c->group) {
     LocalGroup& g = *c->group;
     const int r = c->tp_rank;
@@ -124,6 +133,11 @@ nf_status comm_all_gather(nf_comm* c, const void* send, void* recv, size_t count
 
 // in-place sum over ranks; scratch: count bf16 elements of device memory (emulation only)
 nf_status comm_all_reduce_bf16(nf_comm* c, void* buf, size_t count, cudaStream_t st, void* scratch) {
+  if (c->loopback) {  // a read + write of the buffer (the reduction's local traffic), values unchanged
+    if (cudaMemcpyAsync(scratch, buf, count * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return set_error(NF_ECUDA, "loopback AR copy");
+    return NF_OK;
+  }
   if (c->group) {
     LocalGroup& g = *c->group;
     const int r = c->tp_rank;
@@ -206,9 +220,20 @@ nf_status nf_comm_create_local(int32_t tp_size, int32_t ar_mode, nf_comm** comms
   return NF_OK;
 }
 
+nf_status nf_comm_create_loopback(int32_t tp_size, int32_t tp_rank, nf_comm** out) {
+  if (!out || tp_size < 1 || tp_size > 64 || tp_rank < 0 || tp_rank >= tp_size)
+    return set_error(NF_EINVAL, "bad tp_size/tp_rank/output");
+  nf_comm* c = new nf_comm();
+  c->tp_size = tp_size;
+  c->tp_rank = tp_rank;
+  c->loopback = true;
+  *out = c;
+  return NF_OK;
+}
+
 void nf_comm_destroy(nf_comm* c) {
   if (!c) return;
-  if (!c->group && c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+  if (!c->group && !c->loopback && c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
   delete c;
 }
 

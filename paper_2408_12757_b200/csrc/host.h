@@ -91,7 +91,8 @@ namespace nf {
 bool green_setup(nf_plan* p, int dec_sms, int net_sms);
 int comm_size(const nf_comm* c);
 int comm_rank(const nf_comm* c);
-bool comm_emulated(const nf_comm* c);
+bool comm_emulated(const nf_comm* c);   // emulated group or loopback (no NCCL kernels)
+bool comm_host_sync(const nf_comm* c);  // collectives meet at host barriers (not capturable)
 int comm_max_ctas(const nf_comm* c);
 nf_status comm_all_gather(nf_comm* c, const void* send, void* recv, size_t count_bf16, cudaStream_t st);
 nf_status comm_all_reduce_bf16(nf_comm* c, void* buf, size_t count, cudaStream_t st, void* scratch);
@@ -123,6 +124,7 @@ struct nf_plan {
   cudaStream_t green_ns = nullptr;  // network partition (TP OVERLAP plans)
   int green_net_sms = 0;
   std::vector<NfGraph> graphs;      // CUDA-graph cache (spec.graph)
+  cudaStream_t cap_stream = nullptr;  // capture stream
   std::string graph_note = "not used";
   std::string note;                 // nf_plan_runtime_note buffer
   // green-context SM partitions (OVERLAP plans; green.cpp)

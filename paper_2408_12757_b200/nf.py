@@ -91,12 +91,14 @@ _sig("nf_plan_create", C.c_int, C.POINTER(ModelCfg), C.POINTER(_Batch), C.POINTE
 _sig("nf_plan_get_spec", C.c_int, C.c_void_p, C.POINTER(PlanSpec))
 _sig("nf_plan_export_csv", C.c_int, C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t))
 _sig("nf_plan_destroy", None, C.c_void_p)
+_sig("nf_plan_hash", C.c_uint64, C.c_void_p)
 _sig("nf_plan_runtime_note", C.c_char_p, C.c_void_p)
 _sig("nf_comm_unique_id", C.c_int, C.c_void_p)
 _sig("nf_comm_create", C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p))
 _sig("nf_comm_destroy", None, C.c_void_p)
 _sig("nf_comm_create_local", C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_void_p))
 AR_F32, AR_RING = 0, 1
+_sig("nf_comm_create_loopback", C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_void_p))
 _sig("nf_packed_layer_bytes", C.c_int, C.POINTER(ModelCfg), C.POINTER(C.c_size_t))
 _sig("nf_pack_layer", C.c_int, C.POINTER(ModelCfg), C.POINTER(LayerWeights), C.POINTER(PackedLayer), C.c_void_p)
 _sig("nf_pack_lm_head", C.c_int, C.POINTER(ModelCfg), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
@@ -121,6 +123,8 @@ _sig("nf_attention", C.c_int, C.POINTER(ModelCfg), C.POINTER(_Batch), C.c_void_p
 
 _sig("nf_moe_rows_cap", C.c_int64, C.POINTER(ModelCfg), C.c_int32)
 _sig("nf_moe_route_ws_bytes", C.c_size_t, C.POINTER(ModelCfg), C.c_int32)
+_sig("nf_moe_last_ids", C.c_int, C.POINTER(ModelCfg), C.POINTER(_Batch), C.c_void_p, C.c_size_t,
+     C.POINTER(C.c_void_p))
 _sig("nf_moe_route", C.c_int, C.POINTER(ModelCfg), C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
@@ -165,10 +169,10 @@ _sig("nf_profile_tag", C.c_int, C.c_int32)
 PROF_NAMES = ["kqv", "decode_attn", "prefill_attn", "o_proj", "up_gate", "down", "net", "lm_head", "misc"]
 
 EXPORTED = ["nf_plan_runtime_note", "nf_comm_create_local", "nf_gemm_workspace_bytes", "nf_profile_timeline", "nf_profile_tag", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
-            "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_comm_unique_id",
-            "nf_comm_create", "nf_comm_destroy", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
+            "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_plan_hash", "nf_comm_unique_id",
+            "nf_comm_create", "nf_comm_destroy", "nf_comm_create_loopback", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
             "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_model_step_ex", "nf_gemm_bf16", "nf_attention",
-            "nf_moe_rows_cap", "nf_moe_route_ws_bytes", "nf_moe_route", "nf_sched_create", "nf_sched_submit",
+            "nf_moe_rows_cap", "nf_moe_route_ws_bytes", "nf_moe_route", "nf_moe_last_ids", "nf_sched_create", "nf_sched_submit",
             "nf_sched_next", "nf_sched_complete", "nf_sched_get_stats", "nf_sched_destroy", "nf_assemble_tokens"]
 
 
@@ -262,6 +266,10 @@ class Plan:
         h = C.c_void_p()
         _check(lib.nf_plan_create_explicit(C.byref(cfg), C.byref(spec), C.byref(h)))
         return cls(h.value)
+
+    def hash(self) -> int:
+        """nf_plan_hash: equal on every rank of a TP group."""
+        return int(lib.nf_plan_hash(self.h))
 
     def runtime_note(self) -> str:
         return lib.nf_plan_runtime_note(self.h).decode()
@@ -371,6 +379,13 @@ def moe_route(cfg: ModelCfg, h1: int, router_packed: int, T: int, ids: int, wts:
                             C.c_void_p(ws), ws_bytes, C.c_void_p(stream)))
 
 
+def moe_last_ids(cfg: ModelCfg, b: Batch, ws: int, ws_bytes: int) -> int:
+    """Device pointer of the [T, top_k] routing ids of the last nf_layer_forward on this workspace."""
+    p = C.c_void_p()
+    _check(lib.nf_moe_last_ids(C.byref(cfg), C.byref(b.c), C.c_void_p(ws), ws_bytes, C.byref(p)))
+    return p.value
+
+
 def kernel_launches() -> int:
     return int(lib.nf_kernel_launches())
 
@@ -415,6 +430,13 @@ def comm_create_local(tp_size: int, ar_mode: int = AR_RING):
     arr = (C.c_void_p * tp_size)()
     _check(lib.nf_comm_create_local(tp_size, ar_mode, arr))
     return [arr[i] for i in range(tp_size)]
+
+
+def comm_create_loopback(tp_size: int, tp_rank: int = 0) -> int:
+    """One-rank performance proxy of a tp_size group (local copies instead of peers)."""
+    h = C.c_void_p()
+    _check(lib.nf_comm_create_loopback(tp_size, tp_rank, C.byref(h)))
+    return h.value
 
 
 def comm_destroy(h: int):

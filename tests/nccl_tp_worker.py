@@ -12,6 +12,18 @@ import sys
 
 rank, world, port, out_path = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
 os.environ["NCCL_HOSTID"] = f"nf-test-host-{rank}"
+os.environ.setdefault("NCCL_DEBUG", "INFO")
+os.environ.setdefault("NCCL_DEBUG_FILE", out_path + f".nccl.%h.%p.log")
+_log = open(out_path + ".progress.log", "w")
+
+
+def log(msg):
+    import time as _t
+    _log.write(f"{_t.time():.3f} rank{rank}: {msg}\n")
+    _log.flush()
+
+
+log("start")
 os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
 os.environ.setdefault("NCCL_IB_DISABLE", "1")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -31,7 +43,9 @@ dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank
 res = {"rank": rank}
 uid = [nf.comm_unique_id() if rank == 0 else None]
 dist.broadcast_object_list(uid, src=0)
+log("uid exchanged")
 comm = nf.comm_create(world, rank, uid[0], max_ctas=8)
+log("comm created")
 
 
 def dev(a):
@@ -60,12 +74,14 @@ wd = {k: dev(v) for k, v in w.items()}
 packed = rt.pack_layer(cfg, rt.shard_layer(wd, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, world, rank))
 nb = nf.Batch.from_any(b)
 ws = rt.workspace(cfg, nb)
+log("weights packed")
 layer_res = {}
 for name, mode, shares, nd in [("sequential", nf.SEQUENTIAL, (1,), 0), ("nano", nf.NANO_ONLY, (1, 1, 1, 1), 2),
                                ("overlap42", nf.OVERLAP, (1, 1, 1, 1), 2)]:
     plan = nf.Plan.explicit(cfg, mode, shares=shares, sm=[116, 16, 116, 116, 116, 116, 16], n_dense=nd)
     y = rt.layer_forward(plan, cfg, packed, rt.shard_pool(dev(pool), world, rank), nb, dev(x), ws=ws, comm=comm)
     torch.cuda.synchronize()
+    log(f"layer {name} done")
     out = y.float().cpu().numpy().astype(np.float64)
     err = out - ref
     layer_res[name] = {"rel_l2": float(np.linalg.norm(err) / np.linalg.norm(ref)), "max_abs": float(np.abs(err).max()),
@@ -92,6 +108,7 @@ for name, graph in [("eager", False), ("graph", True)]:
     for it in range(3):  # graph: capture, then two replays
         ids = model.step(plan, [rt.shard_pool(dev(p), world, rank) for p in pools], nb, tok_d, ws, comm=comm)
         torch.cuda.synchronize()
+        log(f"step {name} run {it} done")
         runs.append(ids.cpu().numpy())
     step_res[name] = {"argmax_ok": bool(np.array_equal(runs[0][sure], ids_ref[sure])),
                       "replays_identical": bool(all(np.array_equal(runs[0], r) for r in runs)),

@@ -154,3 +154,45 @@ def test_forward_rejects_incomplete_packed_layers(nf):
     with pytest.raises(nf.NFError) as e:
         nf.layer_forward(plan, dict(fake, w_router=2048, w_down=None), 4096, b, 8192, 12288, 16384, 1 << 30, 0)
     assert e.value.status == nf.NF_EINVAL and "NULL packed weight" in str(e.value)
+
+
+def test_tp_plan_and_comm_validation(nf):
+    """n_dense must divide n_nano (and equal it at tp_size 1); SEQUENTIAL collapses to one
+    nano-batch; the emulated group's AllReduce mode, the loopback communicator and the
+    vocab-parallel head's divisibility are validated; plan hashes ignore tp_rank only."""
+    from paper_2408_12757_b200.runtime import cfg_from_shape
+    c8 = cfg_from_shape(synth.SHAPES["llama2-70b"], tp_size=8, tp_rank=1)
+    p = nf.Plan.explicit(c8, nf.OVERLAP, shares=(1, 1, 1, 1), n_dense=2)
+    assert p.spec().n_dense == 2 and p.spec().n_nano == 4
+    assert nf.Plan.explicit(c8, nf.OVERLAP, shares=(1, 1, 1, 1)).spec().n_dense == 4   # 0 = n_nano
+    for bad in (3, 5, -1):
+        with pytest.raises(nf.NFError) as e:
+            nf.Plan.explicit(c8, nf.OVERLAP, shares=(1, 1, 1, 1), n_dense=bad)
+        assert e.value.status == nf.NF_EINVAL
+    c1 = cfg_from_shape(synth.SHAPES["llama3-8b"])
+    with pytest.raises(nf.NFError):
+        nf.Plan.explicit(c1, nf.OVERLAP, shares=(1, 1, 1, 1), n_dense=2)
+    s = nf.Plan.explicit(c8, nf.SEQUENTIAL, n_dense=0).spec()
+    assert s.n_nano == 1 and s.n_dense == 1
+    # hashes: equal across ranks, different across plans
+    c8b = cfg_from_shape(synth.SHAPES["llama2-70b"], tp_size=8, tp_rank=5)
+    assert nf.Plan.explicit(c8b, nf.OVERLAP, shares=(1, 1, 1, 1), n_dense=2).hash() == p.hash()
+    assert nf.Plan.explicit(c8, nf.OVERLAP, shares=(1, 1, 1, 1), n_dense=1).hash() != p.hash()
+    with pytest.raises(nf.NFError):
+        nf.lib.nf_comm_create_local  # noqa: B018  (exists)
+        nf.comm_create_local(2, 7)
+    with pytest.raises(nf.NFError):
+        nf.comm_create_local(9)
+    h = nf.comm_create_loopback(8, 3)
+    assert h
+    nf.comm_destroy(h)
+    with pytest.raises(nf.NFError):
+        nf.comm_create_loopback(8, 8)
+    # vocab-parallel head: V % N and (V/N) % 32
+    for V, ok in ((32000, True), (32008, False), (8448, True), (8320, False)):
+        cfg = cfg_from_shape(synth.shape_with(synth.SHAPES["llama2-70b"], vocab=V), tp_size=8)
+        if ok:
+            nf.packed_layer_bytes(cfg)
+        else:
+            with pytest.raises(nf.NFError):
+                nf.packed_layer_bytes(cfg)

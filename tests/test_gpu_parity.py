@@ -452,3 +452,84 @@ def test_model_step_degenerate_batches(env, q_len, prefix):
                          torch.from_numpy(toks).cuda(), ws).cpu().numpy()
         assert ids.shape == (b.n_req,) and ((ids >= 0) & (ids < shape.vocab)).all()
         assert np.array_equal(ids[sure], ids_ref[sure]), (mode, shares, bal)
+
+
+def _device_pages_to_compact(b, reqs, pool_d):
+    """Sub-batch of `reqs` with a float64 host pool holding their cached pages copied
+    from the device pool (taken before the step appends this step's K/V)."""
+    sub = synth.make_batch(b.q_len[reqs], b.kv_prefix[reqs], permute=False)
+    pool = np.zeros((sub.n_pages_pool,) + tuple(pool_d.shape[1:]))
+    for i, r in enumerate(reqs):
+        src = torch.as_tensor(b.page_ids[b.page_indptr[r]:b.page_indptr[r + 1]].astype(np.int64), device="cuda")
+        dst = sub.page_ids[sub.page_indptr[i]:sub.page_indptr[i + 1]]
+        pool[dst] = pool_d[src[:len(dst)]].float().cpu().numpy()
+    return sub, pool
+
+
+def test_model_step_8b_full_teacher_forced(env):
+    """The benched step itself (configs[1]: LLaMA-3-8B shape, 32 layers, B_dense 2048,
+    OVERLAP plan of the bench, CUDA graph off because of the inspection outputs):
+    teacher-forced per-layer parity on layers {0, 1, 15, 31} -- the oracle
+    layer l on the GPU's own bf16 input of layer l, sampled requests -- and the
+    LM-head logits of sampled requests against the oracle head on the GPU's final
+    hidden state, plus argmax agreement with the GPU's own logits.  Weights and KV
+    are drawn on the device (seeded) and copied to the host for the oracle."""
+    nf, rt = env
+    shape = synth.SHAPES["llama3-8b"]
+    L, D, F, hd, Hq, Hk, V = (shape.n_layers, shape.d_model, shape.d_ffn, shape.head_dim, shape.n_q_heads,
+                              shape.n_kv_heads, shape.vocab)
+    b = synth.workload_batch(2048, 1024, 512)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+
+    def randn(s, std=1.0, mean=0.0):
+        return torch.empty(s, dtype=torch.bfloat16, device="cuda").normal_(mean, std, generator=g)
+
+    check = [0, 1, 15, 31]
+    cfg = rt.cfg_from_shape(shape)
+    layers, kept = [], {}
+    for l in range(L):
+        w = {"attn_norm": randn((D,), 0.1, 1.0), "w_q": randn((Hq * hd, D), D ** -0.5),
+             "w_k": randn((Hk * hd, D), D ** -0.5), "w_v": randn((Hk * hd, D), D ** -0.5),
+             "w_o": randn((D, Hq * hd), (Hq * hd) ** -0.5), "ffn_norm": randn((D,), 0.1, 1.0),
+             "w_gate": randn((F, D), D ** -0.5), "w_up": randn((F, D), D ** -0.5), "w_down": randn((D, F), F ** -0.5)}
+        layers.append(rt.pack_layer(cfg, w))
+        if l in check:
+            kept[l] = {k: host(v) for k, v in w.items()}
+        del w
+    embed, lm, fnorm = randn((V, D)), randn((V, D), D ** -0.5), randn((D,), 0.1, 1.0)
+    model = rt.Model(cfg, embed, layers, rt.pack_lm_head(cfg, lm, fnorm))
+    pools = [randn((b.n_pages_pool, 2, Hk, 16, hd)) for _ in range(L)]
+    n_dec = int((b.q_len == 1).sum())
+    reqs = [0, 1, n_dec // 2, n_dec - 1, n_dec, n_dec + 1]
+    compact = {l: _device_pages_to_compact(b, reqs, pools[l]) for l in check}
+    tok = torch.randint(0, V, (b.n_tokens,), dtype=torch.int32, device="cuda", generator=g)
+    nb = nf.Batch.from_any(b)
+    ws = rt.workspace(cfg, nb)
+    plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=[116, 32, 116, 116, 116, 116, 8], balance=2)
+    ids, lg, hs = model.step_inspect(plan, pools, nb, tok, ws)
+    torch.cuda.synchronize()
+    rows = token_rows(b, reqs)
+    for l in check:
+        sub, pool = compact[l]
+        x_in = host(hs[l][torch.as_tensor(rows, device="cuda")])
+        ref = OL.decoder_layer(x_in, kept[l], pool, sub, shape)
+        out = host(hs[l + 1][torch.as_tensor(rows, device="cuda")])
+        rms = float(np.sqrt(np.mean(ref ** 2)))
+        rel, mx = assert_close(out, ref, what=f"8B step layer {l} (teacher-forced, output RMS {rms:.2f})", scale_rms=True)
+        print(f"layer {l}: output RMS {rms:.2f}, rel L2 {rel:.3e} max abs {mx:.3e}")
+    # logits of the sampled requests (all requests emit: logits row i = request i)
+    last = np.concatenate([[0], np.cumsum(b.q_len)])[1:] - 1
+    xf = host(hs[L][torch.as_tensor(last[reqs], device="cuda")])
+    ref_lg = OL.rmsnorm(xf, host(fnorm), shape.rms_eps) @ host(lm).T
+    out_lg = host(lg[torch.as_tensor(reqs, device="cuda")])
+    rel, mx = errors(out_lg, ref_lg)
+    assert rel <= 1e-2 and mx <= 0.25, f"logits rel L2 {rel:.3e} max abs {mx:.3e}"
+    ids_h = ids.cpu().numpy()
+    full = host(lg)
+    top = np.sort(full, axis=1)
+    clear = top[:, -1] - top[:, -2] > 0.05
+    assert np.array_equal(ids_h[clear], np.argmax(full, axis=1)[clear])
+    # the inspection pass did not change the result of the plain step
+    ids2 = model.step(plan, pools, nb, tok, ws).cpu().numpy()
+    assert np.array_equal(ids_h, ids2)

@@ -176,3 +176,23 @@ def test_moe_model_step_single_expert_is_dense_model_step():
     ids_d, lg_d, x_d = L.model_step(toks, Wd, [p.copy() for p in pools], b, dsh, return_logits=True)
     assert len(routes) == 2 and np.array_equal(ids, ids_d)
     np.testing.assert_allclose(lg, lg_d, rtol=0, atol=1e-10)
+
+
+def test_forced_ids_reduce_to_topk_and_tie_rule():
+    """moe_ffn(forced_ids=the router's own top-k) == moe_ffn (same weights, A-21); a
+    forced swap of the two selected experts gives the same output (the weights follow
+    the experts); forcing another pair uses the softmax over those two logits."""
+    shape = synth.SHAPES["c1-moe"]
+    w = synth.layer_weights(shape, 0)
+    h1 = synth.activations(shape, 40, seed=9)
+    out, ids, wts, logits = M.moe_ffn(h1, w, shape, return_route=True)
+    out2, ids2, wts2, _ = M.moe_ffn(h1, w, shape, return_route=True, forced_ids=ids)
+    assert np.array_equal(ids, ids2) and np.allclose(wts, wts2, rtol=0, atol=1e-15)
+    assert np.allclose(out, out2, rtol=0, atol=1e-12)
+    out3 = M.moe_ffn(h1, w, shape, forced_ids=ids[:, ::-1])
+    assert np.allclose(out, out3, rtol=1e-12, atol=1e-12)
+    alt = np.stack([ids[:, 0], (ids[:, 1] + 1) % shape.n_experts], axis=1)
+    alt[alt[:, 1] == alt[:, 0], 1] = (alt[alt[:, 1] == alt[:, 0], 1] + 1) % shape.n_experts
+    _, _, wa, _ = M.moe_ffn(h1, w, shape, return_route=True, forced_ids=alt)
+    sel = np.take_along_axis(logits, alt, axis=1)
+    assert np.allclose(wa[:, 0], 1.0 / (1.0 + np.exp(sel[:, 1] - sel[:, 0])), rtol=1e-12)

@@ -43,3 +43,17 @@ def test_tp_moe_dataflow_gloo(tmp_path, world):
                        start_method="spawn")
     errs = np.load(out)
     assert len(errs) == world and (errs < 1e-12).all(), errs
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_tp_plans_identical_across_ranks(tmp_path, world):
+    """libnf on every rank (gloo, CPU): explicit and autosearched TP plans, their hashes,
+    schedules, step metadata and workspace sizes are identical on all ranks."""
+    from paper_2408_12757_b200 import build
+    build.build()
+    import tp_plan_worker
+    out = str(tmp_path / "ok.npy")
+    mp.start_processes(tp_plan_worker.worker, args=(world, _free_port(), out), nprocs=world, join=True,
+                       start_method="spawn")
+    ok, distinct = np.load(out)
+    assert ok and distinct
