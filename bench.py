@@ -443,28 +443,37 @@ def run_nf(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
 
     # ---------------- measured refinement of the (searched) plan: coordinate moves of the memory
-    # partition (+-8 SMs) and the nano-batch token shares (+-1/8), kept while the measured
-    # step time (max over ranks) improves by > 0.5 %; the network partition is held fixed
+    # partition (+-8 / +-16 SMs) and the nano-batch token shares (+-1/8), kept while the measured
+    # step time (max over ranks) improves by > 0.3 %; the network partition is held fixed
     refine_log = []
     if args.plan == "refine" and plan.spec().mode == nf.OVERLAP and not plan.spec().colocate:
-        def timed(pl, n=4):
-            for _ in range(2):
-                model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
+        def run_steps(pl, n):
             for _ in range(n):
                 model.step(pl, pools, nb, tok, ws, next_ids, comm=comm)
-            a1.record(stream)
-            torch.cuda.synchronize()
-            t = torch.tensor([a0.elapsed_time(a1) / n], dtype=torch.float64, device=dev)
-            if world > 1:
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            return float(t.item())
 
-        def variant(base, dec, s8):
+        def ab(cand, inc, pairs=3, n=2):
+            """Median step-time ratio cand / incumbent over interleaved runs (the GPU's power
+            state drifts between runs; interleaving cancels it); max over ranks."""
+            run_steps(cand, 2)
+            run_steps(inc, 2)
+            tc, ti = [], []
+            for _ in range(pairs):
+                for pl, acc in ((cand, tc), (inc, ti)):
+                    torch.cuda.synchronize()
+                    if world > 1:
+                        dist.barrier()
+                    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a0.record(stream)
+                    run_steps(pl, n)
+                    a1.record(stream)
+                    torch.cuda.synchronize()
+                    t = torch.tensor([a0.elapsed_time(a1) / n], dtype=torch.float64, device=dev)
+                    if world > 1:
+                        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                    acc.append(float(t.item()))
+            return statistics.median(tc) / statistics.median(ti), statistics.median(tc)
+
+        def variant(base, dec, s8, nn):
             sp = nf.PlanSpec()
             for f, _ in nf.PlanSpec._fields_:
                 setattr(sp, f, getattr(base, f))
@@ -473,35 +482,40 @@ def run_nf(args, rank, world, local_rank):
             sp.sm[nf.OP_DECODE_ATTN] = dec
             for k in (nf.OP_KQV, nf.OP_PREFILL_ATTN, nf.OP_O, nf.OP_UG, nf.OP_DOWN):
                 sp.sm[k] = 148
-            sh = (s8, s8, 8 - s8, 8 - s8) if base.n_nano == 4 else (s8, 8 - s8)
+            sh = (s8, s8, 8 - s8, 8 - s8) if nn == 4 else (s8, 8 - s8)
+            sp.n_nano = nn
             for i, v in enumerate(sh):
                 sp.share[i] = v
+            sp.n_dense = 2 if tp > 1 else 0
             return nf.Plan.from_spec(cfg, sp)
 
         base = plan.spec()
+        nn = base.n_nano if base.n_nano in (2, 4) else 2
         tot = sum(base.share[:base.n_nano])
-        s8 = max(1, min(7, round(8 * base.share[0] * (2 if base.n_nano == 4 else 1) / tot)))
+        s8 = max(1, min(7, round(8 * base.share[0] * (2 if nn == 4 else 1) / tot)))
         dec = max(8, (base.sm[nf.OP_DECODE_ATTN] + 7) // 8 * 8)
-        cur = variant(base, dec, s8)
-        best_t = timed(cur)
-        refine_log.append({"dec_sms": dec, "share8": s8, "ms": best_t})
-        seen = {(dec, s8)}
+        cur = variant(base, dec, s8, nn)
+        seen = {(dec, s8, nn)}
+        refine_log.append({"dec_sms": dec, "share8": s8, "n_nano": nn, "ratio": 1.0})
         for _move in range(8):
-            cands = [(dec + dd, s8 + ds) for dd, ds in ((-8, 0), (8, 0), (0, -1), (0, 1))
-                     if 8 <= dec + dd <= 64 and 1 <= s8 + ds <= 7 and (dec + dd, s8 + ds) not in seen]
+            cands = [(dec + dd, s8 + ds, nn) for dd, ds in ((-16, 0), (-8, 0), (8, 0), (16, 0), (0, -1), (0, 1))
+                     if 8 <= dec + dd <= 72 and 1 <= s8 + ds <= 7]
+            if tp > 1:
+                cands.append((dec, s8, 6 - nn))     # 4-way <-> 2-way attention nano-batches
+            cands = [c for c in cands if c not in seen]
             if not cands:
                 break
             res = []
-            for d2, s2 in cands:
-                seen.add((d2, s2))
-                pl = variant(base, d2, s2)
-                t = timed(pl)
-                refine_log.append({"dec_sms": d2, "share8": s2, "ms": t})
-                res.append((t, d2, s2, pl))
-            t, d2, s2, pl = min(res, key=lambda x: x[0])
-            if t >= best_t * 0.995:
+            for d2, s2, n2 in cands:
+                seen.add((d2, s2, n2))
+                pl = variant(base, d2, s2, n2)
+                ratio, t = ab(pl, cur)
+                refine_log.append({"dec_sms": d2, "share8": s2, "n_nano": n2, "ratio": ratio, "ms": t})
+                res.append((ratio, d2, s2, n2, pl))
+            ratio, d2, s2, n2, pl = min(res, key=lambda x: x[0])
+            if ratio >= 0.997:
                 break
-            best_t, dec, s8, cur = t, d2, s2, pl
+            dec, s8, nn, cur = d2, s2, n2, pl
         plan = cur
     if world > 1:   # every rank must hold the same plan: same collectives in the same order
         hs = [None] * world

@@ -346,12 +346,15 @@ Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base) 
   const int64_t qkv_n = (int64_t)(c->n_q_heads + 2 * c->n_kv_heads) / N * c->head_dim;
   w.sk_slots = (int)std::max<int64_t>(148, ((T + GEMM_BM - 1) / GEMM_BM) * ((std::max(qkv_n, D) + 255) / 256));
   w.sk_part = (float*)take((size_t)w.sk_slots * GEMM_BM * GEMM_SK_LD * 4);
+  w.sk_part2 = N > 1 ? (float*)take((size_t)w.sk_slots * GEMM_BM * GEMM_SK_LD * 4) : nullptr;
   const int64_t maxN = std::max<int64_t>({qkv_n, D, ((F + 127) / 128) * 256});
   w.sk_flag_n = (int)(((T + GEMM_BM - 1) / GEMM_BM) * ((maxN + 127) / 128) +
                       ((R + GEMM_BM - 1) / GEMM_BM) * VT + 64);
   if (c->n_experts > 0)  // grouped expert GEMMs: up to cap/128 m-tiles
     w.sk_flag_n = std::max<int>(w.sk_flag_n, (int)(moe_rows_cap(c, T) / GEMM_BM * ((maxN + 127) / 128) + 64));
-  w.sk_flag = (int*)take((size_t)w.sk_flag_n * 4);
+  w.sk_flag = (int*)take((size_t)w.sk_flag_n * (N > 1 ? 2 : 1) * 4);
+  w.sk_flag2 = (N > 1 && w.sk_flag) ? w.sk_flag + w.sk_flag_n : nullptr;
+  w.sk_flag_total = w.sk_flag_n * (N > 1 ? 2 : 1);
   if (c->n_experts > 0) {
     const int64_t cap = moe_rows_cap(c, T), nk = T * c->top_k;
     w.mo_cap = cap;
@@ -566,8 +569,10 @@ void nf_plan_destroy(nf_plan* p) {
   for (int k = 0; k < NF_MAX_NANO; ++k)
     for (cudaEvent_t e : {p->ev_pre[k], p->ev_o[k], p->ev_aro[k], p->ev_d[k], p->ev_ard[k]})
       if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {p->ev_agattn, p->ev_ago, p->ev_join_n, p->ev_fork, p->ev_join_c, p->ev_join_m})
+  for (cudaEvent_t e : {p->ev_agattn, p->ev_ago, p->ev_join_n, p->ev_fork, p->ev_join_c, p->ev_join_m, p->ev_fork2,
+                        p->ev_join_c2})
     if (e) cudaEventDestroy(e);
+  if (p->cs2) cudaStreamDestroy(p->cs2);
   for (auto& g : p->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   for (int i = 0; i < 2; ++i) {
@@ -605,8 +610,9 @@ nf_status ensure_runtime(nf_plan* p) {
   for (int k = 0; k < NF_MAX_NANO; ++k)
     for (cudaEvent_t* e : {&p->ev_pre[k], &p->ev_o[k], &p->ev_aro[k], &p->ev_d[k], &p->ev_ard[k]})
       NF_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-  for (cudaEvent_t* e : {&p->ev_agattn, &p->ev_ago, &p->ev_join_n})
+  for (cudaEvent_t* e : {&p->ev_agattn, &p->ev_ago, &p->ev_join_n, &p->ev_fork2, &p->ev_join_c2})
     NF_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  NF_CUDA(cudaStreamCreateWithPriority(&p->cs2, cudaStreamNonBlocking, lo));
   for (int i = 0; i < 2; ++i) NF_CUDA(cudaEventCreateWithFlags(&p->ev_upload[i], cudaEventDisableTiming));
   return NF_OK;
 }
@@ -763,6 +769,7 @@ struct LayerCtx {
   CUtensorMap page_map;
   cudaStream_t cs, ms;  // compute / memory streams
   cudaStream_t ns;      // network stream (TP collectives; == cs outside OVERLAP)
+  cudaStream_t cs2 = nullptr;  // TP OVERLAP: compute stream of the second dense nano-batch (null: cs)
   nf_comm* comm;
   int cap_dense = 0, cap_dec = 0;  // partition sizes when green contexts are active (0: whole GPU)
 };
@@ -1088,6 +1095,22 @@ std::vector<Group> dense_groups(const nf_plan* p, const StepMeta& m) {
   return g;
 }
 
+// TP OVERLAP: the dense nano-batches alternate between two compute streams on the compute
+// partition (each with its own stream-K scratch), so a group whose next op waits on a
+// collective or on decode attention does not hold back the other group's ready GEMMs:
+// the hardware runs whichever is ready (the in-order single stream stalled on every wait).
+LayerCtx group_ctx(const LayerCtx& L, int g, Workspace* wg) {
+  LayerCtx c = L;
+  if ((g & 1) && L.cs2) {
+    *wg = *L.w;
+    wg->sk_part = L.w->sk_part2;
+    wg->sk_flag = L.w->sk_flag2;
+    c.w = wg;
+    c.cs = L.cs2;
+  }
+  return c;
+}
+
 // Front of a group: KQV of each of its attention nano-batches, decode attention on
 // the memory stream as soon as that KQV lands, prefill attention on the compute stream.
 nf_status tp_front(nf_plan* p, const LayerCtx& L, int gi, const Group& G, const __nv_bfloat16* x, const float* part,
@@ -1148,6 +1171,9 @@ nf_status tp_stage_b(nf_plan* p, const LayerCtx& L, int gi, const Group& G, cons
     GemmArgs a{};
     a.epi = EPI_RESID;
     a.stages = stages;
+    a.sk_part = L.w->sk_part;
+    a.sk_slots = L.w->sk_slots;
+    a.sk_flag = L.w->sk_flag;
     a.M = M;
     a.N = (int)Dl;
     a.K = (int)qd_full;
@@ -1172,6 +1198,9 @@ nf_status tp_stage_b(nf_plan* p, const LayerCtx& L, int gi, const Group& G, cons
     GemmArgs a{};
     a.epi = EPI_STORE;
     a.stages = stages;
+    a.sk_part = L.w->sk_part;
+    a.sk_slots = L.w->sk_slots;
+    a.sk_flag = L.w->sk_flag;
     a.M = M;
     a.N = (int)D;
     a.K = (int)qd;
@@ -1218,6 +1247,9 @@ nf_status tp_stage_c(nf_plan* p, const LayerCtx& L, int gi, const Group& G, cons
     GemmArgs u{};
     u.epi = EPI_SILU;
     u.stages = stages;
+    u.sk_part = L.w->sk_part;
+    u.sk_slots = L.w->sk_slots;
+    u.sk_flag = L.w->sk_flag;
     u.M = M;
     u.N = (int)(((Fl + 127) / 128) * 256);
     u.K = (int)D;
@@ -1236,6 +1268,9 @@ nf_status tp_stage_c(nf_plan* p, const LayerCtx& L, int gi, const Group& G, cons
     GemmArgs d{};
     d.epi = EPI_STORE;
     d.stages = stages;
+    d.sk_part = L.w->sk_part;
+    d.sk_slots = L.w->sk_slots;
+    d.sk_flag = L.w->sk_flag;
     d.M = M;
     d.N = (int)D;
     d.K = (int)Fl;
@@ -1291,8 +1326,20 @@ nf_status enter_partitions(nf_plan* p, LayerCtx* L, cudaStream_t caller) {
     const int cap = comm_max_ctas(L->comm);
     if (comm_emulated(L->comm) || (cap > 0 && cap <= (want + 7) / 8 * 8)) net = want;
   }
-  if (!green_setup(p, p->spec.sm[NF_OP_DECODE_ATTN], net)) return NF_OK;
+  const bool two = p->cfg.tp_size > 1 && L->comm && !p->spec.colocate;  // per-group compute streams
+  if (!green_setup(p, p->spec.sm[NF_OP_DECODE_ATTN], net)) {
+    if (two) {
+      NF_CUDA(cudaEventRecord(p->ev_fork2, caller));
+      NF_CUDA(cudaStreamWaitEvent(p->cs2, p->ev_fork2, 0));
+      L->cs2 = p->cs2;
+    }
+    return NF_OK;
+  }
   NF_CUDA(cudaEventRecord(p->ev_fork, caller));
+  if (two) {
+    NF_CUDA(cudaStreamWaitEvent(p->green_cs2, p->ev_fork, 0));
+    L->cs2 = p->green_cs2;
+  }
   NF_CUDA(cudaStreamWaitEvent(p->green_cs, p->ev_fork, 0));
   NF_CUDA(cudaStreamWaitEvent(p->green_ms, p->ev_fork, 0));
   L->cs = p->green_cs;
@@ -1306,6 +1353,10 @@ nf_status enter_partitions(nf_plan* p, LayerCtx* L, cudaStream_t caller) {
   return NF_OK;
 }
 nf_status leave_partitions(nf_plan* p, const LayerCtx& L, cudaStream_t caller) {
+  if (L.cs2) {
+    NF_CUDA(cudaEventRecord(p->ev_join_c2, L.cs2));
+    NF_CUDA(cudaStreamWaitEvent(caller, p->ev_join_c2, 0));
+  }
   if (L.cs != caller) {
     NF_CUDA(cudaEventRecord(p->ev_join_c, L.cs));
     NF_CUDA(cudaStreamWaitEvent(caller, p->ev_join_c, 0));
@@ -1342,13 +1393,16 @@ nf_status run_layer(nf_plan* p, const LayerCtx& L, const nf_packed_layer* wt, vo
       }
       return NF_OK;
     }
-    for (size_t g = 0; g < groups.size(); ++g) NF_TRY(tp_front(p, L, (int)g, groups[g], x, part, nparts, wt, pool));
-    NF_TRY(tp_stage_a(p, L, 0, groups[0]));
-    for (size_t g = 0; g < groups.size(); ++g) NF_TRY(tp_stage_b(p, L, (int)g, groups[g], x, wt));
-    for (size_t g = 0; g < groups.size(); ++g) NF_TRY(tp_stage_c(p, L, (int)g, groups[g], x, wt, x_out));
+    Workspace wg[NF_MAX_NANO];
+    std::vector<LayerCtx> Lg;
+    for (size_t g = 0; g < groups.size(); ++g) Lg.push_back(group_ctx(L, (int)g, &wg[g]));
+    for (size_t g = 0; g < groups.size(); ++g) NF_TRY(tp_front(p, Lg[g], (int)g, groups[g], x, part, nparts, wt, pool));
+    NF_TRY(tp_stage_a(p, Lg[0], 0, groups[0]));
+    for (size_t g = 0; g < groups.size(); ++g) NF_TRY(tp_stage_b(p, Lg[g], (int)g, groups[g], x, wt));
+    for (size_t g = 0; g < groups.size(); ++g) NF_TRY(tp_stage_c(p, Lg[g], (int)g, groups[g], x, wt, x_out));
     for (size_t g = 0; g < groups.size(); ++g) {
-      NF_TRY(tp_stage_d(p, L, (int)g, groups[g], x_out, part_out));
-      NF_TRY(tap_rows(L, tap, x_out, groups[g].nr.t0, groups[g].nr.t1));
+      NF_TRY(tp_stage_d(p, Lg[g], (int)g, groups[g], x_out, part_out));
+      NF_TRY(tap_rows(Lg[g], tap, x_out, groups[g].nr.t0, groups[g].nr.t1));
     }
     return NF_OK;
   }
@@ -1396,7 +1450,7 @@ nf_status model_step_launches(nf_plan* p, nf_comm* comm, const nf_model_weights*
                               const nf_batch* b, const int32_t* token_ids, const nf_step_outputs* out,
                               const StepMeta& m, const Workspace& wsp, cudaStream_t cs) {
   const nf_model_cfg* c = &p->cfg;
-  NF_CUDA(cudaMemsetAsync(wsp.sk_flag, 0, (size_t)wsp.sk_flag_n * 4, cs));
+  NF_CUDA(cudaMemsetAsync(wsp.sk_flag, 0, (size_t)wsp.sk_flag_total * 4, cs));
   const int D = c->d_model;
   const int NP = D / GEMM_NORM_COLS;
   void* const* taps = out->hidden;
@@ -1442,21 +1496,24 @@ nf_status model_step_launches(nf_plan* p, nf_comm* comm, const nf_model_weights*
     // KQV of a group is issued right after that group's layer-l output is complete.
     const auto groups = dense_groups(p, m);
     const int G = (int)groups.size();
+    Workspace wg[NF_MAX_NANO];
+    std::vector<LayerCtx> Lg;
     L.pool_map = maps[0];
     L.page_map = pmaps[0];
-    for (int g = 0; g < G; ++g) NF_TRY(tp_front(p, L, g, groups[g], x, px, 1, &w->layers[0], kv_pools[0]));
+    for (int g = 0; g < G; ++g) Lg.push_back(group_ctx(L, g, &wg[g]));
+    for (int g = 0; g < G; ++g) NF_TRY(tp_front(p, Lg[g], g, groups[g], x, px, 1, &w->layers[0], kv_pools[0]));
     for (int l = 0; l < c->n_layers; ++l) {
       const nf_packed_layer* wt = &w->layers[l];
-      NF_TRY(tp_stage_a(p, L, 0, groups[0]));
-      for (int g = 0; g < G; ++g) NF_TRY(tp_stage_b(p, L, g, groups[g], x, wt));
-      for (int g = 0; g < G; ++g) NF_TRY(tp_stage_c(p, L, g, groups[g], x, wt, y));
+      NF_TRY(tp_stage_a(p, Lg[0], 0, groups[0]));
+      for (int g = 0; g < G; ++g) NF_TRY(tp_stage_b(p, Lg[g], g, groups[g], x, wt));
+      for (int g = 0; g < G; ++g) NF_TRY(tp_stage_c(p, Lg[g], g, groups[g], x, wt, y));
       for (int g = 0; g < G; ++g) {
-        NF_TRY(tp_stage_d(p, L, g, groups[g], y, py));
-        NF_TRY(tap_rows(L, tap_of(l), y, groups[g].nr.t0, groups[g].nr.t1));
+        NF_TRY(tp_stage_d(p, Lg[g], g, groups[g], y, py));
+        NF_TRY(tap_rows(Lg[g], tap_of(l), y, groups[g].nr.t0, groups[g].nr.t1));
         if (l + 1 < c->n_layers) {
-          L.pool_map = maps[l + 1];
-          L.page_map = pmaps[l + 1];
-          NF_TRY(tp_front(p, L, g, groups[g], y, py, 1, &w->layers[l + 1], kv_pools[l + 1]));
+          Lg[g].pool_map = maps[l + 1];
+          Lg[g].page_map = pmaps[l + 1];
+          NF_TRY(tp_front(p, Lg[g], g, groups[g], y, py, 1, &w->layers[l + 1], kv_pools[l + 1]));
         }
       }
       std::swap(x, y);
@@ -1682,7 +1739,7 @@ nf_status nf_layer_forward(const nf_plan* plan, nf_comm* comm, const nf_packed_l
   build_meta(c, b, order, cuts, &m);
   cudaStream_t cs = (cudaStream_t)stream;
   NF_TRY(upload_meta(p, m, wsp.meta, cs));
-  NF_CUDA(cudaMemsetAsync(wsp.sk_flag, 0, (size_t)wsp.sk_flag_n * 4, cs));
+  NF_CUDA(cudaMemsetAsync(wsp.sk_flag, 0, (size_t)wsp.sk_flag_total * 4, cs));
   LayerCtx L{};
   L.p = p;
   L.c = c;

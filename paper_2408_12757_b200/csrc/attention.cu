@@ -117,18 +117,12 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
     if (l_item >= n_items) return;
     const int s = issued % NS;
     const int64_t page = __shfl_sync(0xffffffffu, pid_win, l_page & 31);
-    // L2 prefetch of the page pf_dist ahead in this item (no shared memory: under
-    // co-running GEMMs the HBM latency exceeds what the 2-slot ring per warp covers)
-    const int pfi = l_page + a.pf_dist;
-    const bool do_pf = a.pf_dist > 0 && pfi < cur.np;
-    const int64_t pf_page = __shfl_sync(0xffffffffu, ((pfi >> 5) == (l_page >> 5)) ? pid_win : pid_nwin, pfi & 31);
     if (lane == 0) {
       uint8_t* dst = ring + s * STAGE_BYTES;
       const int rowK = (int)(((page * 2 + 0) * kh + cur.kvh) * 16);
       fence_proxy_async();  // WAR: this warp's ldmatrix reads of the slot before the async-proxy refill
       mbar_arrive_expect_tx(&bars[s], STAGE_BYTES);
       tma_load_4d_hint(dst, &pages, &bars[s], 0, rowK, 0, 0, kv_policy);  // K and V of the page: one 4-D box
-      if (do_pf) tma_prefetch_4d(&pages, 0, (int)(((pf_page * 2 + 0) * kh + cur.kvh) * 16), 0, 0);
     }
     ++issued;
     if (++l_page == cur.np) {

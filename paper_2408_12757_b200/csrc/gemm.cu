@@ -80,9 +80,16 @@ NF_DEV void sincos_reduced(float a, float* s, float* c) {
 // is 32 KB instead of 48 KB, so the ring is 6 deep, and each B byte is fetched
 // once per pair.  Data-parallel or split-K tail schedule (split-K=2 is CG = 1 only);
 // split-K partial slots and arrival flags are per CTA of the pair.
-template <int GEMM_STAGES, int BN, int CG>
+//
+// SR (smem residual, EPI_RESID with short K): the epilogue stages the tile's residual
+// in shared memory by TMA (issued before the accumulator is ready), adds the
+// accumulator in place and TMA-stores each finished 64-column box, so the epilogue
+// no longer waits on per-thread global loads and scattered row stores (short-K GEMMs,
+// e.g. the 70B TP8 rank's O projection with K = 1024, were epilogue-bound).
+template <int GEMM_STAGES, int BN, int CG, bool SR = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmO,
                         const __grid_constant__ GemmArgs args) {
   constexpr int B_ROWS = BN / CG;  // B tile rows held by this CTA
   constexpr int B_STAGE_ELEMS = B_ROWS * GEMM_BK;
@@ -93,11 +100,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __nv_bfloat16* sA = reinterpret_cast<__nv_bfloat16*>(smem);
   __nv_bfloat16* sB = sA + GEMM_STAGES * A_STAGE_ELEMS;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + GEMM_STAGES * B_STAGE_ELEMS);
+  uint8_t* sR = reinterpret_cast<uint8_t*>(sB + GEMM_STAGES * B_STAGE_ELEMS);  // SR: [BN/64][128 rows][128 B]
+  constexpr uint32_t SR_BYTES = SR ? (uint32_t)BN * GEMM_BM * 2 : 0u;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sR + SR_BYTES);
   uint64_t* empty = full + GEMM_STAGES;
   uint64_t* tfull = empty + GEMM_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;  // SR: residual tile landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 2);
   float* inv_freq = reinterpret_cast<float*>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -194,6 +204,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * CG);  // epilogue warps of both CTAs drain into the even CTA's barrier
     }
+    if constexpr (SR) mbar_init(rbar, 1);
     fence_barrier_init();
   }
   if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
@@ -279,13 +290,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // -------------------------------------------------------------- epilogue
     const int ew = warp - 4;
     int as = 0;
-    uint32_t aphase = 0;
+    uint32_t aphase = 0, rphase = 0;
     const int trow = ew * 32 + lane;  // row within the tile
+    const bool leader = ew == 0 && lane == 0;
+    if constexpr (SR) {
+      if (leader) tma_prefetch_desc(&tmR);
+    }
     for_each_seg([&](int tile, int kb0, int kb1) {
       const int mb = tile % tiles_m, nb = tile / tiles_m;
       const int r = mb * TM + (int)rank * GEMM_BM + trow;
       const bool valid = grouped ? r < args.grp_end[group_of(mb)] : r < M;
-      if (args.epi == EPI_RESID && valid && kb0 == 0) {
+      if constexpr (SR) {
+        // the residual tile -> smem while the mainloop runs (after the previous tile's
+        // stores have read the buffer); rows >= M / cols >= N are zero-filled and clipped
+        if (leader && kb0 == 0 && args.epi == EPI_RESID) {
+          bulk_wait_read0();
+          mbar_arrive_expect_tx(rbar, SR_BYTES);
+#pragma unroll
+          for (int b = 0; b < BN / 64; ++b)
+            tma_load_2d(sR + b * GEMM_BM * 128, &tmR, rbar, nb * BN + b * 64, mb * TM + (int)rank * GEMM_BM);
+        }
+      } else if (args.epi == EPI_RESID && valid && kb0 == 0) {
         // residual row segment -> L2 while the tile's mainloop still runs (short-K
         // GEMMs are otherwise epilogue-bound on these dependent global loads)
         const char* rp = reinterpret_cast<const char*>(args.resid + (int64_t)r * args.ldr + nb * BN);
@@ -375,6 +400,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       switch (args.epi) {
         case EPI_STORE:
         case EPI_F32: {
+          if constexpr (SR) {
+            if (args.epi == EPI_STORE) {
+              // bf16 tile staged in smem (after the previous tile's stores have read it),
+              // each finished 64-column box TMA-stored
+              if (leader) bulk_wait_read0();
+              named_bar_sync(2, 128);
+              const uint32_t row_base = smem_u32(sR) + trow * 128;
+#pragma unroll 1
+              for (int c = 0; c < BN / 32; ++c) {
+                ldacc(c * 32, s, v);
+                const uint32_t box = row_base + (c >> 1) * GEMM_BM * 128;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const uint32_t addr = box + ((((c & 1) * 4 + q) ^ (trow & 7)) << 4);
+                  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+                               "r"(pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1])), "r"(pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3])),
+                               "r"(pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5])), "r"(pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]))
+                               : "memory");
+                }
+                if (c & 1) {
+                  fence_proxy_async();
+                  named_bar_sync(2, 128);
+                  if (leader) {
+                    tma_store_2d(&tmO, sR + (c >> 1) * GEMM_BM * 128, n0 + (c >> 1) * 64,
+                                 mb * TM + (int)rank * GEMM_BM);
+                    bulk_commit();
+                  }
+                }
+              }
+              break;
+            }
+          }
 #pragma unroll 1
           for (int c = 0; c < BN / 32; ++c) {
             ldacc(c * 32, s, v);
@@ -392,6 +449,52 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           break;
         }
         case EPI_RESID: {
+          if constexpr (SR) {
+            mbar_wait(rbar, rphase);
+            rphase ^= 1;
+            float sq = 0.f;
+            const uint32_t row_base = smem_u32(sR) + trow * 128;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+              ldacc(c * 32, s, v);
+              const uint32_t box = row_base + (c >> 1) * GEMM_BM * 128;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t addr = box + ((((c & 1) * 4 + q) ^ (trow & 7)) << 4);
+                uint32_t w0, w1, w2, w3;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                             : "r"(addr));
+                const uint32_t w[4] = {w0, w1, w2, w3};
+                uint32_t o[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  const float2 f = unpack_bf16x2(w[h]);
+                  const float x0 = round_bf16(f.x + v[q * 8 + 2 * h]), x1 = round_bf16(f.y + v[q * 8 + 2 * h + 1]);
+                  sq = fmaf(x0, x0, sq);
+                  sq = fmaf(x1, x1, sq);
+                  o[h] = pack_bf16x2(x0, x1);
+                }
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(o[0]), "r"(o[1]), "r"(o[2]),
+                             "r"(o[3])
+                             : "memory");
+              }
+              if ((c & 3) == 3) {
+                if (args.sq_out != nullptr && valid && n0 + c * 32 < N)
+                  args.sq_out[(int64_t)((n0 >> 7) + (c >> 2)) * args.sq_stride + r] = sq;
+                sq = 0.f;
+              }
+              if (c & 1) {  // a 64-column box is complete: store it
+                fence_proxy_async();
+                named_bar_sync(2, 128);
+                if (leader) {
+                  tma_store_2d(&tmO, sR + (c >> 1) * GEMM_BM * 128, n0 + (c >> 1) * 64, mb * TM + (int)rank * GEMM_BM);
+                  bulk_commit();
+                }
+              }
+            }
+            break;
+          }
           // sum-of-squares partials in 128-column units (independent of the tile width)
           float sq = 0.f;
           // residual loads run one 32-column chunk ahead of their use
@@ -531,6 +634,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (as == 0) aphase ^= 1;
     });
   }
+  if constexpr (SR) {
+    if (warp == 4 && lane == 0) bulk_wait0();  // the last tile's stores are complete
+  }
   __syncthreads();
   if constexpr (CG == 2) cluster_sync();  // the peer's remote arrives / MMA writes are done before teardown
   if (warp == 2) {
@@ -542,7 +648,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_once;
-bool g_attr_set[5] = {false, false, false, false, false};
+bool g_attr_set[7] = {false, false, false, false, false, false, false};
 
 cudaError_t get_encode() {
   std::call_once(g_once, [] {
@@ -738,25 +844,50 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   e = make_tmap_bf16(&tb, B, args.K, (uint64_t)args.N * (grouped ? args.n_groups : 1), ldb, GEMM_BK,
                      pair_kernel ? bn / 2 : bn);
   if (e != cudaSuccess) return e;
-  // smem ring: 4 x 48 KB (BN 256), 6 x 32 KB (BN 128 or CTA pairs); co-located plans use 3 / 4 stages
+  // smem ring: 4 x 48 KB (BN 256), 6 x 32 KB (BN 128 or CTA pairs); co-located plans use 3 / 4 stages.
+  // Residual / plain-store GEMMs (EPI_RESID / EPI_STORE bf16, K <= 8192) stage the output tile
+  // (and the residual) in smem and TMA-store it (SR): 3 x 48 KB (or pairs 4 x 32 KB) + 64 KB.
+  // NF_GEMM_SR=0 disables it, NF_GEMM_SR_MAXKB caps its K (A/B runs).
+  static int sr_env = -1;
+  if (sr_env < 0) {
+    const char* e2 = getenv("NF_GEMM_SR");
+    sr_env = e2 ? atoi(e2) : 1;
+  }
+  static int sr_kb_env = -1;
+  if (sr_kb_env < 0) {
+    const char* e2 = getenv("NF_GEMM_SR_MAXKB");
+    sr_kb_env = e2 ? atoi(e2) : 128;
+  }
+  const bool sr = sr_env && (args.epi == EPI_RESID || (args.epi == EPI_STORE && args.outf == nullptr)) && bn == 256 &&
+                  !grouped && !coloc && num_kb <= sr_kb_env;
   int stages, cg = 1;
-  void (*kern)(CUtensorMap, CUtensorMap, GemmArgs);
+  void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs);
   int attr_idx;
   if (pair_kernel) {
-    stages = 6;
+    stages = sr ? 4 : 6;
     cg = 2;
-    kern = gemm_tcgen05_kernel<6, 256, 2>;
-    attr_idx = 4;
+    kern = sr ? gemm_tcgen05_kernel<4, 256, 2, true> : gemm_tcgen05_kernel<6, 256, 2>;
+    attr_idx = sr ? 6 : 4;
   } else if (bn == 256) {
-    stages = coloc ? 3 : 4;
-    kern = coloc ? gemm_tcgen05_kernel<3, 256, 1> : gemm_tcgen05_kernel<4, 256, 1>;
-    attr_idx = coloc ? 1 : 0;
+    stages = sr ? 3 : (coloc ? 3 : 4);
+    kern = sr ? gemm_tcgen05_kernel<3, 256, 1, true>
+              : (coloc ? gemm_tcgen05_kernel<3, 256, 1> : gemm_tcgen05_kernel<4, 256, 1>);
+    attr_idx = sr ? 5 : (coloc ? 1 : 0);
   } else {
     stages = coloc ? 4 : 6;
     kern = coloc ? gemm_tcgen05_kernel<4, 128, 1> : gemm_tcgen05_kernel<6, 128, 1>;
     attr_idx = coloc ? 3 : 2;
   }
-  const int smem = gemm_smem_bn(stages, bn / cg);
+  const int smem = gemm_smem_bn(stages, bn / cg) + (sr ? bn * GEMM_BM * 2 : 0);
+  CUtensorMap tr = ta, to = ta;
+  if (sr) {
+    if (args.epi == EPI_RESID) {
+      e = make_tmap_bf16(&tr, args.resid, args.N, args.M, args.ldr, 64, GEMM_BM);
+      if (e != cudaSuccess) return e;
+    }
+    e = make_tmap_bf16(&to, args.out, args.N, args.M, args.ldo, 64, GEMM_BM);
+    if (e != cudaSuccess) return e;
+  }
   if (!g_attr_set[attr_idx]) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
@@ -793,7 +924,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  e = cudaLaunchKernelEx(&cfg, kern, ta, tb, a2);
+  e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tr, to, a2);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }

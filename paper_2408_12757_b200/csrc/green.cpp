@@ -8,7 +8,9 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <algorithm>
 #include <string>
+#include <vector>
 
 #include "host.h"
 
@@ -71,55 +73,65 @@ bool green_setup(nf_plan* p, int dec_sms, int net_sms) {
     return false;
   }
   CUdevice dev = p->device;
-  CUdevResource all{}, part[1]{}, rest{}, npart[1]{}, rest2{};
+  CUdevResource all{};
   if (g_api.getDevResource(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) {
     p->green_note = "cuDeviceGetDevResource failed";
     return false;
   }
-  unsigned int n = 1;
-  const unsigned int want = (unsigned int)((dec_sms + 7) / 8 * 8);
-  if (g_api.split(part, &n, &all, &rest, 0, want) != CUDA_SUCCESS || n != 1) {
+  // One split of the whole device into groups of the SM granularity (8); the memory and
+  // network partitions take whole groups from the front, the compute partition the
+  // remaining groups plus the leftover SMs (several SM resources combine into one
+  // descriptor).  (Splitting a split's remainder a second time is rejected by the driver.)
+  constexpr unsigned kQ = 8;
+  CUdevResource groups[64]{}, rest{};
+  unsigned int ng = 64;
+  if (g_api.split(groups, &ng, &all, &rest, 0, kQ) != CUDA_SUCCESS || ng < 3) {
     p->green_note = "cuDevSmResourceSplitByCount failed";
     return false;
   }
-  CUdevResource* cmp = &rest;
-  if (net_sms > 0) {
-    unsigned int n2 = 1;
-    const unsigned int want_n = (unsigned int)((net_sms + 7) / 8 * 8);
-    if (g_api.split(npart, &n2, &rest, &rest2, 0, want_n) != CUDA_SUCCESS || n2 != 1) {
-      p->green_note = "cuDevSmResourceSplitByCount (network partition) failed";
-      return false;
-    }
-    cmp = &rest2;
+  const unsigned n_mem = std::max(1u, (unsigned)((dec_sms + kQ - 1) / kQ));
+  const unsigned n_net = net_sms > 0 ? std::max(1u, (unsigned)((net_sms + kQ - 1) / kQ)) : 0u;
+  if (n_mem + n_net + 1 > ng) {
+    p->green_note = "memory + network partitions leave no compute SMs";
+    return false;
   }
+  std::vector<CUdevResource> cmp(groups + n_mem + n_net, groups + ng);
+  if (rest.sm.smCount > 0) cmp.push_back(rest);
   CUdevResourceDesc d_mem, d_cmp, d_net;
   CUgreenCtx g_mem, g_cmp, g_net = nullptr;
-  if (g_api.genDesc(&d_mem, part, 1) != CUDA_SUCCESS || g_api.genDesc(&d_cmp, cmp, 1) != CUDA_SUCCESS ||
+  if (g_api.genDesc(&d_mem, groups, n_mem) != CUDA_SUCCESS ||
+      g_api.genDesc(&d_cmp, cmp.data(), (unsigned)cmp.size()) != CUDA_SUCCESS ||
       g_api.create(&g_mem, d_mem, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
       g_api.create(&g_cmp, d_cmp, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) {
     p->green_note = "green context creation failed";
     return false;
   }
-  if (net_sms > 0 && (g_api.genDesc(&d_net, npart, 1) != CUDA_SUCCESS ||
-                      g_api.create(&g_net, d_net, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)) {
+  if (n_net > 0 && (g_api.genDesc(&d_net, groups + n_mem, n_net) != CUDA_SUCCESS ||
+                    g_api.create(&g_net, d_net, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)) {
     p->green_note = "green context creation failed (network partition)";
     return false;
   }
+  unsigned sm_mem = 0, sm_net = 0, sm_cmp = 0;
+  for (unsigned i = 0; i < n_mem; ++i) sm_mem += groups[i].sm.smCount;
+  for (unsigned i = 0; i < n_net; ++i) sm_net += groups[n_mem + i].sm.smCount;
+  for (const auto& r : cmp) sm_cmp += r.sm.smCount;
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  CUstream s_mem, s_cmp, s_net = nullptr;
+  CUstream s_mem, s_cmp, s_cmp2, s_net = nullptr;
   if (g_api.streamCreate(&s_mem, g_mem, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS ||
       g_api.streamCreate(&s_cmp, g_cmp, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS ||
+      g_api.streamCreate(&s_cmp2, g_cmp, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS ||
       (g_net && g_api.streamCreate(&s_net, g_net, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS)) {
     p->green_note = "green stream creation failed";
     return false;
   }
   p->green_ms = (cudaStream_t)s_mem;
   p->green_cs = (cudaStream_t)s_cmp;
+  p->green_cs2 = (cudaStream_t)s_cmp2;
   p->green_ns = (cudaStream_t)s_net;
-  p->green_dec_sms = (int)part[0].sm.smCount;
-  p->green_dense_sms = (int)cmp->sm.smCount;
-  p->green_net_sms = g_net ? (int)npart[0].sm.smCount : 0;
+  p->green_dec_sms = (int)sm_mem;
+  p->green_dense_sms = (int)sm_cmp;
+  p->green_net_sms = (int)sm_net;
   p->green_ok = true;
   p->green_note = "memory partition " + std::to_string(p->green_dec_sms) + " SMs, compute partition " +
                   std::to_string(p->green_dense_sms) + " SMs";

@@ -69,6 +69,9 @@ struct Workspace {
   float* sk_part;  // stream-K partial tiles [148][128][256] f32
   int* sk_flag;    // stream-K tile counters
   int sk_flag_n;
+  float* sk_part2;  // TP: a second stream-K set for the second dense nano-batch's compute stream
+  int* sk_flag2;
+  int sk_flag_total;  // flags to zero per step (both sets)
   int sk_slots;
   // MoE FFN (n_experts > 0): routing, grouping and the grouped GEMM operands (moe.cu)
   int* mo_ids;
@@ -130,7 +133,9 @@ struct nf_plan {
   // green-context SM partitions (OVERLAP plans; green.cpp)
   bool green_tried = false, green_ok = false;
   std::string green_note = "not used";
-  cudaStream_t green_cs = nullptr, green_ms = nullptr;
+  cudaStream_t green_cs = nullptr, green_ms = nullptr, green_cs2 = nullptr;
+  cudaStream_t cs2 = nullptr;  // second compute stream (TP OVERLAP: one per dense nano-batch) outside green contexts
+  cudaEvent_t ev_fork2 = nullptr, ev_join_c2 = nullptr;
   int green_dec_sms = 0, green_dense_sms = 0;
   cudaEvent_t ev_fork = nullptr, ev_join_c = nullptr, ev_join_m = nullptr;
   cudaEvent_t ev_upload[2] = {};

@@ -116,5 +116,8 @@ for name, graph in [("eager", False), ("graph", True)]:
                       "graph_note": plan.runtime_note()}
 res["step"] = step_res
 json.dump(res, open(out_path, "w"))
-nf.comm_destroy(comm)
-dist.destroy_process_group()
+log("results written")
+dist.barrier()
+# exit without tearing down NCCL: with the socket transport between "hosts" sharing one
+# GPU the communicator's teardown can block on the peer's proxy thread
+os._exit(0)
