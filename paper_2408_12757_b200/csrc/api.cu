@@ -782,14 +782,15 @@ int clamp_dec(const LayerCtx& L, int v) { return clampsm(L.cap_dec ? std::min(v,
 // 4-D TMA box per page) is the default: it reaches the HBM roofline at ~80 SMs.
 // The tcgen05 kernel (decode_tc.cu, one item in flight per CTA) is selectable
 // with NF_DECODE_IMPL=tc for head_dim 128 / GQA <= 8 (not in co-located plans).
-bool use_tc_decode(const nf_model_cfg* c, const nf_plan* p) {
-  static int env = -1;
-  if (env < 0) {
-    const char* e = getenv("NF_DECODE_IMPL");
-    env = (e && std::string(e) == "tc") ? 1 : 0;
-  }
-  return env == 1 && !p->spec.colocate && c->head_dim == 128 && c->n_q_heads / c->n_kv_heads <= 8;
+int decode_impl_env() {  // read per launch (tests switch it at run time)
+  const char* e = getenv("NF_DECODE_IMPL");
+  return (e && std::string(e) == "tc") ? 1 : ((e && std::string(e) == "ws") ? 2 : 0);
 }
+bool use_tc_decode(const nf_model_cfg* c, const nf_plan* p) {
+  return decode_impl_env() == 1 && !p->spec.colocate && c->head_dim == 128 && c->n_q_heads / c->n_kv_heads <= 8;
+}
+// warp-specialised decode (decode_ws.cu): NF_DECODE_IMPL=ws, not in co-located plans
+bool use_ws_decode(const nf_plan* p) { return decode_impl_env() == 2 && !p->spec.colocate; }
 
 nf_status run_kqv(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x, const float* part, int nparts,
                   const nf_packed_layer* wt, void* pool) {
@@ -869,6 +870,8 @@ nf_status run_decode(const LayerCtx& L, const NanoRange& nr, cudaStream_t st, in
   ProfScope ps(NF_OP_DECODE_ATTN, st);
   if (use_tc_decode(c, L.p))
     NF_CUDA(launch_decode_attention_tc(L.pool_map, a, dec, n, sms, st));
+  else if (use_ws_decode(L.p))
+    NF_CUDA(launch_decode_attention_ws(L.page_map, a, dec, n, sms, st));
   else
     NF_CUDA(launch_decode_attention(L.pool_map, L.page_map, a, dec, n, sms, st));
   return NF_OK;

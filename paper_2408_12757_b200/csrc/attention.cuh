@@ -37,6 +37,9 @@ cudaError_t make_pool_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, in
 
 cudaError_t launch_decode_attention(const CUtensorMap& pool_map, const CUtensorMap& page_map, const AttnArgs& a, const DecodeItem* items,
                                     int n_items, int sm_budget, cudaStream_t stream);
+// warp-specialised decode attention (one producer warp drives every consumer warp's TMA ring); decode_ws.cu
+cudaError_t launch_decode_attention_ws(const CUtensorMap& page_map, const AttnArgs& a, const DecodeItem* items,
+                                       int n_items, int sm_budget, cudaStream_t stream);
 // tcgen05 decode attention (head_dim 128, GQA group <= 8); decode_tc.cu
 cudaError_t launch_decode_attention_tc(const CUtensorMap& pool_map, const AttnArgs& a, const DecodeItem* items,
                                        int n_items, int sm_budget, cudaStream_t stream);

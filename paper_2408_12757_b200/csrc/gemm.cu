@@ -845,7 +845,8 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
                      pair_kernel ? bn / 2 : bn);
   if (e != cudaSuccess) return e;
   // smem ring: 4 x 48 KB (BN 256), 6 x 32 KB (BN 128 or CTA pairs); co-located plans use 3 / 4 stages.
-  // Residual / plain-store GEMMs (EPI_RESID / EPI_STORE bf16, K <= 8192) stage the output tile
+  // Short-K residual / plain-store GEMMs (EPI_RESID / EPI_STORE bf16, K <= 2048: the 3-stage ring
+  // costs 8-34 % on long mainloops, tools/gemm_micro.py r2f) stage the output tile
   // (and the residual) in smem and TMA-store it (SR): 3 x 48 KB (or pairs 4 x 32 KB) + 64 KB.
   // NF_GEMM_SR=0 disables it, NF_GEMM_SR_MAXKB caps its K (A/B runs).
   static int sr_env = -1;
@@ -856,7 +857,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   static int sr_kb_env = -1;
   if (sr_kb_env < 0) {
     const char* e2 = getenv("NF_GEMM_SR_MAXKB");
-    sr_kb_env = e2 ? atoi(e2) : 128;
+    sr_kb_env = e2 ? atoi(e2) : 32;
   }
   const bool sr = sr_env && (args.epi == EPI_RESID || (args.epi == EPI_STORE && args.outf == nullptr)) && bn == 256 &&
                   !grouped && !coloc && num_kb <= sr_kb_env;

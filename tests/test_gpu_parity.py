@@ -533,3 +533,23 @@ def test_model_step_8b_full_teacher_forced(env):
     # the inspection pass did not change the result of the plain step
     ids2 = model.step(plan, pools, nb, tok, ws).cpu().numpy()
     assert np.array_equal(ids_h, ids2)
+
+
+@pytest.mark.parametrize("impl", ["ws"])
+def test_decode_impl_variants_vs_oracle(env, impl, monkeypatch):
+    """The warp-specialised decode kernel (NF_DECODE_IMPL=ws) against the oracle on the 8B
+    shape (GQA 4) and a 70B TP8 rank (GQA 8, one KV head): mixed lengths incl. partial last
+    pages, SM budgets 1 / 7 / 148; bit-identical across SM budgets (same per-item order)."""
+    monkeypatch.setenv("NF_DECODE_IMPL", impl)
+    for shape in (synth.SHAPES["llama3-8b"], synth.shape_with(synth.SHAPES["llama2-70b"], n_q_heads=8, n_kv_heads=1,
+                                                             d_ffn=3584)):
+        q_len = [1] * 37
+        prefix = [0, 1, 15, 16, 17, 31, 32, 33, 100, 255, 256, 257, 1000, 1535] + list(range(40, 40 + 23 * 37, 37))
+        b, pool, q = _attn_case(shape, q_len, prefix, seed=5)
+        ref = OL.paged_attention(q, pool, b)
+        outs = []
+        for sm in (1, 7, 148):
+            out = _run_attn(env, shape, b, pool, q, sm_dec=sm)
+            assert_close(out.reshape(ref.shape), ref, what=f"decode {impl} sm={sm} {shape.name}")
+            outs.append(out)
+        assert all(np.array_equal(outs[0], o) for o in outs[1:])
