@@ -770,6 +770,7 @@ struct LayerCtx {
   cudaStream_t cs, ms;  // compute / memory streams
   cudaStream_t ns;      // network stream (TP collectives; == cs outside OVERLAP)
   cudaStream_t cs2 = nullptr;  // TP OVERLAP: compute stream of the second dense nano-batch (null: cs)
+  bool dec_on_cs = false;      // no memory partition: decode attention on the (group's) compute stream
   nf_comm* comm;
   int cap_dense = 0, cap_dec = 0;  // partition sizes when green contexts are active (0: whole GPU)
 };
@@ -866,7 +867,9 @@ nf_status run_decode(const LayerCtx& L, const NanoRange& nr, cudaStream_t st, in
   const nf_model_cfg* c = L.c;
   const AttnArgs a = attn_args(L);
   const DecodeItem* dec = reinterpret_cast<const DecodeItem*>(L.meta_dev + L.m->off_dec) + nr.dec_off + off;
-  const int sms = part == 2 ? clamp_dense(L, L.p->spec.sm[NF_OP_KQV]) : clamp_dec(L, L.p->spec.sm[NF_OP_DECODE_ATTN]);
+  const int sms = part == 2     ? clamp_dense(L, L.p->spec.sm[NF_OP_KQV])
+                  : L.dec_on_cs ? clamp_dense(L, L.p->spec.sm[NF_OP_DECODE_ATTN])
+                                : clamp_dec(L, L.p->spec.sm[NF_OP_DECODE_ATTN]);
   ProfScope ps(NF_OP_DECODE_ATTN, st);
   if (use_tc_decode(c, L.p))
     NF_CUDA(launch_decode_attention_tc(L.pool_map, a, dec, n, sms, st));
@@ -1111,6 +1114,7 @@ LayerCtx group_ctx(const LayerCtx& L, int g, Workspace* wg) {
     c.w = wg;
     c.cs = L.cs2;
   }
+  if (L.dec_on_cs) c.ms = c.cs;
   return c;
 }
 
@@ -1330,7 +1334,12 @@ nf_status enter_partitions(nf_plan* p, LayerCtx* L, cudaStream_t caller) {
     if (comm_emulated(L->comm) || (cap > 0 && cap <= (want + 7) / 8 * 8)) net = want;
   }
   const bool two = p->cfg.tp_size > 1 && L->comm && !p->spec.colocate;  // per-group compute streams
+  const bool no_mem = p->spec.sm[NF_OP_DECODE_ATTN] >= num_sms();  // plan without a memory partition
   if (!green_setup(p, p->spec.sm[NF_OP_DECODE_ATTN], net)) {
+    if (no_mem) {
+      L->ms = L->cs;
+      L->dec_on_cs = true;
+    }
     if (two) {
       NF_CUDA(cudaEventRecord(p->ev_fork2, caller));
       NF_CUDA(cudaStreamWaitEvent(p->cs2, p->ev_fork2, 0));
@@ -1344,9 +1353,14 @@ nf_status enter_partitions(nf_plan* p, LayerCtx* L, cudaStream_t caller) {
     L->cs2 = p->green_cs2;
   }
   NF_CUDA(cudaStreamWaitEvent(p->green_cs, p->ev_fork, 0));
-  NF_CUDA(cudaStreamWaitEvent(p->green_ms, p->ev_fork, 0));
   L->cs = p->green_cs;
-  L->ms = p->green_ms;
+  if (p->green_ms) {
+    NF_CUDA(cudaStreamWaitEvent(p->green_ms, p->ev_fork, 0));
+    L->ms = p->green_ms;
+  } else {
+    L->ms = L->cs;
+    L->dec_on_cs = true;
+  }
   L->cap_dense = p->green_dense_sms;
   L->cap_dec = p->green_dec_sms;
   if (p->green_ns && L->ns != caller) {

@@ -89,8 +89,14 @@ bool green_setup(nf_plan* p, int dec_sms, int net_sms) {
     p->green_note = "cuDevSmResourceSplitByCount failed";
     return false;
   }
-  const unsigned n_mem = std::max(1u, (unsigned)((dec_sms + kQ - 1) / kQ));
+  // dec_sms >= all SMs: no memory partition (decode attention runs on the compute streams;
+  // a TP plan that overlaps only the collectives)
+  const unsigned n_mem = dec_sms >= (int)all.sm.smCount ? 0u : std::max(1u, (unsigned)((dec_sms + kQ - 1) / kQ));
   const unsigned n_net = net_sms > 0 ? std::max(1u, (unsigned)((net_sms + kQ - 1) / kQ)) : 0u;
+  if (n_mem == 0 && n_net == 0) {
+    p->green_note = "no partition requested";
+    return false;
+  }
   if (n_mem + n_net + 1 > ng) {
     p->green_note = "memory + network partitions leave no compute SMs";
     return false;
@@ -98,10 +104,10 @@ bool green_setup(nf_plan* p, int dec_sms, int net_sms) {
   std::vector<CUdevResource> cmp(groups + n_mem + n_net, groups + ng);
   if (rest.sm.smCount > 0) cmp.push_back(rest);
   CUdevResourceDesc d_mem, d_cmp, d_net;
-  CUgreenCtx g_mem, g_cmp, g_net = nullptr;
-  if (g_api.genDesc(&d_mem, groups, n_mem) != CUDA_SUCCESS ||
+  CUgreenCtx g_mem = nullptr, g_cmp, g_net = nullptr;
+  if ((n_mem > 0 && (g_api.genDesc(&d_mem, groups, n_mem) != CUDA_SUCCESS ||
+                     g_api.create(&g_mem, d_mem, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)) ||
       g_api.genDesc(&d_cmp, cmp.data(), (unsigned)cmp.size()) != CUDA_SUCCESS ||
-      g_api.create(&g_mem, d_mem, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
       g_api.create(&g_cmp, d_cmp, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) {
     p->green_note = "green context creation failed";
     return false;
@@ -117,8 +123,8 @@ bool green_setup(nf_plan* p, int dec_sms, int net_sms) {
   for (const auto& r : cmp) sm_cmp += r.sm.smCount;
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  CUstream s_mem, s_cmp, s_cmp2, s_net = nullptr;
-  if (g_api.streamCreate(&s_mem, g_mem, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS ||
+  CUstream s_mem = nullptr, s_cmp, s_cmp2, s_net = nullptr;
+  if ((g_mem && g_api.streamCreate(&s_mem, g_mem, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS) ||
       g_api.streamCreate(&s_cmp, g_cmp, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS ||
       g_api.streamCreate(&s_cmp2, g_cmp, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS ||
       (g_net && g_api.streamCreate(&s_net, g_net, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS)) {
@@ -133,8 +139,9 @@ bool green_setup(nf_plan* p, int dec_sms, int net_sms) {
   p->green_dense_sms = (int)sm_cmp;
   p->green_net_sms = (int)sm_net;
   p->green_ok = true;
-  p->green_note = "memory partition " + std::to_string(p->green_dec_sms) + " SMs, compute partition " +
-                  std::to_string(p->green_dense_sms) + " SMs";
+  p->green_note = (g_mem ? "memory partition " + std::to_string(p->green_dec_sms) + " SMs, "
+                          : std::string("no memory partition (decode on the compute streams), ")) +
+                  "compute partition " + std::to_string(p->green_dense_sms) + " SMs";
   if (g_net) p->green_note += ", network partition " + std::to_string(p->green_net_sms) + " SMs";
   return true;
 }
