@@ -1,21 +1,28 @@
 #!/usr/bin/env python
 """Benchmark of the NanoFlow hot path on B200 (one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1], the largest config that fits one GPU; the
-metric's configs[2] 70B-TP8 does not): a LLaMA-3-8B-shape model (32 layers,
-D 4096, 32/8 heads, hd 128, F 14336, V 128256), random-init bf16 weights,
-serving step over the B_dense = 2048 steady state of the constant 1024-in /
-512-out workload: 683 decode requests (contexts 1024..1535) +
-a 341-token chunk (prefix 683) + one 1024-token prompt, paged KV (page 16).
-A "step" = one nf_model_step: embedding -> 32 decoder layers (KQV+RoPE+KV
-append, paged decode/prefill attention, O, RMSNorm, SwiGLU, Down) -> final
-norm -> LM head -> argmax, through the C ABI.  Inputs are resident in HBM
-(KV 115 GB + weights 15 GB per step, far above the 126 MB L2: no flush needed).
+N = 1 (default, --config c2): BASELINE.json configs[1], the largest config that
+fits one GPU (the metric's configs[2] 70B-TP8 does not): a LLaMA-3-8B-shape model
+(32 layers, D 4096, 32/8 heads, hd 128, F 14336, V 128256), random-init bf16
+weights, serving step over the B_dense = 2048 steady state of the constant
+1024-in / 512-out workload: 683 decode requests (contexts
+1024..1535) + a 341-token chunk (prefix 683) + one 1024-token prompt, paged KV
+(page 16).  A "step" = one nf_model_step: embedding -> 32 decoder layers
+(KQV+RoPE+KV append, paged decode/prefill attention, O, RMSNorm, SwiGLU, Down)
+-> final norm -> LM head -> argmax, through the C ABI, replayed as a CUDA graph.
+Inputs are resident in HBM (KV 115 GB + weights 15 GB per step, far above the
+126 MB L2: no flush needed).
 
---gpus N > 1 (torchrun): N independent replicas (data parallel, no exchange:
-the 8B shape fits one GPU), weak scaling; value = all ranks' tokens / max time.
---impl reference: the CPU oracle (oracle/, float64 numpy) as the reference
-arm, timed on the host cores on a bounded sample.
+N > 1 (torchrun; default --config c3): the metric's configs[2], LLaMA-2-70B
+shape (80 layers) tensor-parallel over all N ranks with NCCL (B_dense 768 at
+TP2, 2048 at TP4/8), the paper's TP pipeline (4 attention / 2 dense
+nano-batches, collectives on a network partition); value = the job's
+tokens/s, tokens_per_s_per_gpu = value / N.  Rank 0 checks layer 0 against the
+oracle in the run (sampled requests) and every rank's hidden states agree.
+--config c3loop: rank 0 of a TP8 group on one GPU with loopback collectives
+(per-rank performance proxy).  --impl reference: the CPU oracle (oracle/,
+float64 numpy) as the reference arm, on a bounded sample.
+--plan refine: the autosearched plan refined by interleaved measured A/B moves.
 """
 from __future__ import annotations
 
@@ -327,12 +334,15 @@ def run_nf(args, rank, world, local_rank):
             # defaults = best of tools/sweep_plans.py on B200 (profiles/r1_sweep_*.log); TP: the
             # paper's 4-way KQV/attention, 2-way O/UGD/network split with a network
             # partition for the collectives
+            # TP (c3 / c4 / c3loop): two dense nano-batches on per-group compute streams with decode
+            # attention on them (no memory partition) and the collectives on a 16-SM network
+            # partition -- the best TP8-rank plan measured on one GPU (profiles/r2_tp8_rank_plans.md)
             dense, dec, net, dshares = {"c2": (116, 32, 8, "1,1"), "c4rank": (132, 16, 8, "3,5"),
-                                        "c3": (116, 16, 16, "1,1,1,1"), "c4": (116, 16, 16, "1,1,1,1"),
-                                        "c3loop": (116, 16, 16, "1,1,1,1")}.get(
+                                        "c3": (148, 148, 16, "1,1"), "c4": (148, 148, 16, "1,1"),
+                                        "c3loop": (148, 148, 16, "1,1")}.get(
                 args.config, (132, 16, 8, "1,1"))
             shares = tuple(int(x) for x in (args.shares or dshares).split(","))
-            n_dense = 2 if (tp > 1 and len(shares) == 4) else 0
+            n_dense = 2 if (tp > 1 and len(shares) in (2, 4)) else 0
             plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=shares, sm=sm or [dense, dec, dense, dense, dense, dense, net],
                                     balance=args.balance, n_dense=n_dense, graph=not args.no_graph)
     elif args.mode == "nano":
@@ -499,9 +509,12 @@ def run_nf(args, rank, world, local_rank):
         refine_log.append({"dec_sms": dec, "share8": s8, "n_nano": nn, "ratio": 1.0})
         for _move in range(8):
             cands = [(dec + dd, s8 + ds, nn) for dd, ds in ((-16, 0), (-8, 0), (8, 0), (16, 0), (0, -1), (0, 1))
-                     if 8 <= dec + dd <= 72 and 1 <= s8 + ds <= 7]
+                     if (dd == 0 or dec < 148) and 8 <= dec + dd <= 72 and 1 <= s8 + ds <= 7]
+            if dec >= 148:
+                cands += [(dec, s8 - 1, nn), (dec, s8 + 1, nn)] if 1 < s8 < 7 else []
             if tp > 1:
                 cands.append((dec, s8, 6 - nn))     # 4-way <-> 2-way attention nano-batches
+                cands.append((148 if dec < 148 else 24, s8, nn))  # with / without a memory partition
             cands = [c for c in cands if c not in seen]
             if not cands:
                 break
@@ -793,7 +806,7 @@ def main():
     ap.add_argument("--impl", default="nf", choices=["nf", "reference"])
     ap.add_argument("--mode", default="auto", choices=["auto", "overlap", "nano", "sequential"],
                     help="auto: the measured-best plan kind per config (OVERLAP except the c3rank/c4rank proxies)")
-    ap.add_argument("--plan", default="explicit", choices=["explicit", "auto", "refine"],
+    ap.add_argument("--plan", default="", choices=["", "explicit", "auto", "refine"],
                     help="auto: nf_plan_create autosearch over --curves (overlap mode); refine: the searched plan "
                          "(or the explicit default when no curves exist) refined by measured coordinate moves")
     ap.add_argument("--curves", default="profiles/curves_b200_quick.csv")
@@ -819,6 +832,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if not args.config:
         args.config = "c2" if world == 1 else "c3"   # N > 1: the metric's configs[2] (70B TP=N), never replicas
+    if not args.plan:   # TP on a multi-GPU box: the default plan refined by measurement on that box
+        args.plan = "refine" if (world > 1 and args.config in ("c3", "c4")) else "explicit"
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
