@@ -503,7 +503,7 @@ def run_nf(args, rank, world, local_rank):
         nn = base.n_nano if base.n_nano in (2, 4) else 2
         tot = sum(base.share[:base.n_nano])
         s8 = max(1, min(7, round(8 * base.share[0] * (2 if nn == 4 else 1) / tot)))
-        dec = max(8, (base.sm[nf.OP_DECODE_ATTN] + 7) // 8 * 8)
+        dec = min(148, max(8, (base.sm[nf.OP_DECODE_ATTN] + 7) // 8 * 8))
         cur = variant(base, dec, s8, nn)
         seen = {(dec, s8, nn)}
         refine_log.append({"dec_sms": dec, "share8": s8, "n_nano": nn, "ratio": 1.0})
@@ -834,9 +834,9 @@ def main():
         args.config = "c2" if world == 1 else "c3"   # N > 1: the metric's configs[2] (70B TP=N), never replicas
     if not args.plan:   # TP on a multi-GPU box: the default plan refined by measurement on that box
         args.plan = "refine" if (world > 1 and args.config in ("c3", "c4")) else "explicit"
-    if world > 1:
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    if world > 1:   # NCCL's init log (ranks, nranks, channels, NVLS) for the run's record
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":

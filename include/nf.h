@@ -192,6 +192,14 @@ nf_status nf_comm_create_local(int32_t tp_size, int32_t ar_mode, nf_comm** comms
 nf_status nf_comm_create_loopback(int32_t tp_size, int32_t tp_rank, nf_comm** out);
 void nf_comm_destroy(nf_comm* comm);
 
+/* Evidence of execution-unit partitioning: launches a probe kernel
+ * (4 CTAs per SM of the device) on each of the plan's partition streams -- memory,
+ * compute, network -- as an OVERLAP step would use them, and writes, per partition,
+ * smids_out[part * n_sm + sm] = number of probe CTAs that ran on SM `sm` (%smid).
+ * n_sm = device SM count (148); partitions the plan does not use are all-zero.
+ * Synchronises `stream`.  NF_EINVAL if the plan is not an OVERLAP plan. */
+nf_status nf_plan_probe_partitions(nf_plan* plan, nf_comm* comm, int32_t* smids_out, int32_t n_sm, void* stream);
+
 /* ------------------------------------------------------------------ weights */
 /* This rank's shards in canonical [out, in] row-major bf16 (device):
  * w_q [qh/N*hd, D], w_k/w_v [kh/N*hd, D], w_o [D, qh*hd] FULL (TP1) or NULL,

@@ -1844,6 +1844,36 @@ nf_status nf_moe_route(const nf_model_cfg* c, const void* h1, const void* router
   return NF_OK;
 }
 
+nf_status nf_plan_probe_partitions(nf_plan* p, nf_comm* comm, int32_t* smids_out, int32_t n_sm, void* stream) {
+  if (!p || !smids_out) return set_error(NF_EINVAL, "NULL plan/output");
+  if (p->spec.mode != NF_OVERLAP) return set_error(NF_EINVAL, "not an OVERLAP plan");
+  if (n_sm != num_sms()) return set_error(NF_EINVAL, "n_sm %d != device SMs %d", n_sm, num_sms());
+  NF_TRY(ensure_runtime(p));
+  cudaStream_t cs = (cudaStream_t)stream;
+  LayerCtx L{};
+  L.p = p;
+  L.c = &p->cfg;
+  L.cs = cs;
+  L.ms = p->mem_stream;
+  L.ns = p->cfg.tp_size > 1 ? p->net_stream : cs;
+  L.comm = comm;
+  NF_TRY(enter_partitions(p, &L, cs));
+  int* d = nullptr;
+  NF_CUDA(cudaMalloc(&d, (size_t)3 * n_sm * sizeof(int)));  // (probe only; not on the forward path)
+  NF_CUDA(cudaMemsetAsync(d, 0, (size_t)3 * n_sm * sizeof(int), cs));
+  NF_CUDA(cudaStreamSynchronize(cs));
+  const cudaStream_t parts[3] = {L.dec_on_cs ? nullptr : L.ms, L.cs, (L.ns != L.cs) ? L.ns : nullptr};
+  for (int i = 0; i < 3; ++i)
+    if (parts[i]) NF_CUDA(launch_smid_probe(d + i * n_sm, 4 * n_sm, parts[i]));
+  NF_TRY(leave_partitions(p, L, cs));
+  for (int i = 0; i < 3; ++i)
+    if (parts[i]) NF_CUDA(cudaStreamSynchronize(parts[i]));
+  NF_CUDA(cudaStreamSynchronize(cs));
+  NF_CUDA(cudaMemcpy(smids_out, d, (size_t)3 * n_sm * sizeof(int), cudaMemcpyDeviceToHost));
+  NF_CUDA(cudaFree(d));
+  return NF_OK;
+}
+
 nf_status nf_moe_last_ids(const nf_model_cfg* c, const nf_batch* b, const void* ws, size_t ws_bytes,
                           const int32_t** ids_out) {
   NF_TRY(validate_cfg(c));

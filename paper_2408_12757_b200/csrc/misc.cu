@@ -126,6 +126,17 @@ __global__ void scatter_rows_kernel(const __nv_bfloat16* __restrict__ src, const
   for (int i = lane; i < D / 8; i += 32) out[i] = in[i];
 }
 
+// %smid of every CTA of the probe grid -> per-SM counters (partition evidence)
+__global__ void smid_probe_kernel(int* counts) {
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  if (threadIdx.x == 0) atomicAdd(counts + smid, 1);
+  // keep the CTA resident a little so the grid spreads over the partition's SMs
+  const long long t0 = clock64();
+  while (clock64() - t0 < 20000) {
+  }
+}
+
 __global__ void fill_i32_kernel(int* p, int n, int v) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -293,6 +304,12 @@ cudaError_t launch_scatter_rows(const __nv_bfloat16* src, const int* idx, int ro
                                 cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
   scatter_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(src, idx, rows, D, dst);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_smid_probe(int* counts, int ctas, cudaStream_t st) {
+  smid_probe_kernel<<<ctas, 32, 0, st>>>(counts);
   count_launch();
   return cudaGetLastError();
 }

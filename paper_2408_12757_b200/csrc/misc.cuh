@@ -21,6 +21,7 @@ cudaError_t launch_interleave(const __nv_bfloat16* src, int n, int rows, int C, 
                               cudaStream_t st);
 cudaError_t launch_sum_bf16(const void* const* in, int n, __nv_bfloat16* out, size_t count, bool ring, cudaStream_t st);
 cudaError_t launch_fill_i32(int* p, int n, int v, cudaStream_t st);
+cudaError_t launch_smid_probe(int* counts, int ctas, cudaStream_t st);
 cudaError_t launch_assemble_tokens(const int* src, const int* prev, int* out, int T, cudaStream_t st);
 cudaError_t launch_scale_cols(const __nv_bfloat16* src, const __nv_bfloat16* gamma, int64_t rows, int cols,
                               __nv_bfloat16* dst, cudaStream_t st);

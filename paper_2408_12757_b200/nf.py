@@ -93,6 +93,7 @@ _sig("nf_plan_export_csv", C.c_int, C.c_void_p, C.c_char_p, C.c_size_t, C.POINTE
 _sig("nf_plan_destroy", None, C.c_void_p)
 _sig("nf_plan_hash", C.c_uint64, C.c_void_p)
 _sig("nf_plan_runtime_note", C.c_char_p, C.c_void_p)
+_sig("nf_plan_probe_partitions", C.c_int, C.c_void_p, C.c_void_p, P_i32, C.c_int32, C.c_void_p)
 _sig("nf_comm_unique_id", C.c_int, C.c_void_p)
 _sig("nf_comm_create", C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p))
 _sig("nf_comm_destroy", None, C.c_void_p)
@@ -168,7 +169,7 @@ _sig("nf_profile_timeline", C.c_int, C.POINTER(Span), C.c_int32, P_i32)
 _sig("nf_profile_tag", C.c_int, C.c_int32)
 PROF_NAMES = ["kqv", "decode_attn", "prefill_attn", "o_proj", "up_gate", "down", "net", "lm_head", "misc"]
 
-EXPORTED = ["nf_plan_runtime_note", "nf_comm_create_local", "nf_gemm_workspace_bytes", "nf_profile_timeline", "nf_profile_tag", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
+EXPORTED = ["nf_plan_runtime_note", "nf_plan_probe_partitions", "nf_comm_create_local", "nf_gemm_workspace_bytes", "nf_profile_timeline", "nf_profile_tag", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
             "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_plan_hash", "nf_comm_unique_id",
             "nf_comm_create", "nf_comm_destroy", "nf_comm_create_loopback", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
             "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_model_step_ex", "nf_gemm_bf16", "nf_attention",
@@ -266,6 +267,13 @@ class Plan:
         h = C.c_void_p()
         _check(lib.nf_plan_create_explicit(C.byref(cfg), C.byref(spec), C.byref(h)))
         return cls(h.value)
+
+    def probe_partitions(self, stream: int, comm: Optional[int] = None, n_sm: int = 148):
+        """[3][n_sm] probe-CTA counts per SM for the memory / compute / network partitions."""
+        out = np.zeros(3 * n_sm, np.int32)
+        _check(lib.nf_plan_probe_partitions(self.h, C.c_void_p(comm), out.ctypes.data_as(P_i32), n_sm,
+                                            C.c_void_p(stream)))
+        return out.reshape(3, n_sm)
 
     def hash(self) -> int:
         """nf_plan_hash: equal on every rank of a TP group."""

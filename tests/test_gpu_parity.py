@@ -553,3 +553,32 @@ def test_decode_impl_variants_vs_oracle(env, impl, monkeypatch):
             assert_close(out.reshape(ref.shape), ref, what=f"decode {impl} sm={sm} {shape.name}")
             outs.append(out)
         assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+@pytest.mark.parametrize("dec,net,tp", [(32, 8, 1), (16, 16, 8), (148, 16, 8)])
+def test_overlap_partitions_are_sm_disjoint(env, dec, net, tp):
+    """Execution-unit scheduling evidence (SURVEY §5 %smid check): probe CTAs
+    launched on an OVERLAP plan's memory / compute / network partition streams run on
+    pairwise disjoint SM sets of the planned sizes (green contexts), covering the GPU."""
+    nf, rt = env
+    shape = synth.SHAPES["llama2-70b"] if tp > 1 else synth.SHAPES["llama3-8b"]
+    cfg = rt.cfg_from_shape(shape, tp_size=tp)
+    comm = nf.comm_create_loopback(tp, 0) if tp > 1 else None
+    plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1), sm=[148, dec, 148, 148, 148, 148, net],
+                            n_dense=2 if tp > 1 else 0)
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    cnt = plan.probe_partitions(rt.stream_handle(), comm, n_sm)
+    sets = [set(np.nonzero(c)[0].tolist()) for c in cnt]
+    if comm:
+        nf.comm_destroy(comm)
+    note = plan.runtime_note()
+    mem, cmp_, netp = sets
+    assert not (mem & cmp_) and not (mem & netp) and not (cmp_ & netp), note
+    if dec < n_sm:
+        assert len(mem) == (dec + 7) // 8 * 8, (len(mem), note)
+    else:
+        assert not mem and "no memory partition" in note
+    if tp > 1:
+        assert len(netp) == (net + 7) // 8 * 8, (len(netp), note)
+    assert len(mem | cmp_ | netp) == n_sm
+    print(note, {k: len(v) for k, v in zip(("memory", "compute", "network"), sets)})
