@@ -305,6 +305,8 @@ def run_nf(args, rank, world, local_rank):
         shape = synth.shape_with(shape, n_layers=args.layers)
     L = shape.n_layers
     b_dense = 768 if (args.config == "c3" and tp == 2) else 2048   # TP2: memory cap
+    if args.b_dense:
+        b_dense = args.b_dense   # (dev) e.g. 2049 for the batch-size cliff
     b = synth.workload_batch(b_dense, p_in, d_out)
     T = b.n_tokens
     nb = nf.Batch.from_any(b)
@@ -483,53 +485,8 @@ def run_nf(args, rank, world, local_rank):
                     acc.append(float(t.item()))
             return statistics.median(tc) / statistics.median(ti), statistics.median(tc)
 
-        def variant(base, dec, s8, nn):
-            sp = nf.PlanSpec()
-            for f, _ in nf.PlanSpec._fields_:
-                setattr(sp, f, getattr(base, f))
-            for k in range(nf.OP_COUNT):
-                sp.sm[k] = base.sm[k]
-            sp.sm[nf.OP_DECODE_ATTN] = dec
-            for k in (nf.OP_KQV, nf.OP_PREFILL_ATTN, nf.OP_O, nf.OP_UG, nf.OP_DOWN):
-                sp.sm[k] = 148
-            sh = (s8, s8, 8 - s8, 8 - s8) if nn == 4 else (s8, 8 - s8)
-            sp.n_nano = nn
-            for i, v in enumerate(sh):
-                sp.share[i] = v
-            sp.n_dense = 2 if tp > 1 else 0
-            return nf.Plan.from_spec(cfg, sp)
-
-        base = plan.spec()
-        nn = base.n_nano if base.n_nano in (2, 4) else 2
-        tot = sum(base.share[:base.n_nano])
-        s8 = max(1, min(7, round(8 * base.share[0] * (2 if nn == 4 else 1) / tot)))
-        dec = min(148, max(8, (base.sm[nf.OP_DECODE_ATTN] + 7) // 8 * 8))
-        cur = variant(base, dec, s8, nn)
-        seen = {(dec, s8, nn)}
-        refine_log.append({"dec_sms": dec, "share8": s8, "n_nano": nn, "ratio": 1.0})
-        for _move in range(8):
-            cands = [(dec + dd, s8 + ds, nn) for dd, ds in ((-16, 0), (-8, 0), (8, 0), (16, 0), (0, -1), (0, 1))
-                     if (dd == 0 or dec < 148) and 8 <= dec + dd <= 72 and 1 <= s8 + ds <= 7]
-            if dec >= 148:
-                cands += [(dec, s8 - 1, nn), (dec, s8 + 1, nn)] if 1 < s8 < 7 else []
-            if tp > 1:
-                cands.append((dec, s8, 6 - nn))     # 4-way <-> 2-way attention nano-batches
-                cands.append((148 if dec < 148 else 24, s8, nn))  # with / without a memory partition
-            cands = [c for c in cands if c not in seen]
-            if not cands:
-                break
-            res = []
-            for d2, s2, n2 in cands:
-                seen.add((d2, s2, n2))
-                pl = variant(base, d2, s2, n2)
-                ratio, t = ab(pl, cur)
-                refine_log.append({"dec_sms": d2, "share8": s2, "n_nano": n2, "ratio": ratio, "ms": t})
-                res.append((ratio, d2, s2, n2, pl))
-            ratio, d2, s2, n2, pl = min(res, key=lambda x: x[0])
-            if ratio >= 0.997:
-                break
-            dec, s8, nn, cur = d2, s2, n2, pl
-        plan = cur
+        from paper_2408_12757_b200 import refine as R
+        plan, refine_log = R.refine(cfg, plan, ab, tp)
     if world > 1:   # every rank must hold the same plan: same collectives in the same order
         hs = [None] * world
         dist.all_gather_object(hs, plan.hash())
@@ -824,6 +781,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true", help="skip the in-run oracle parity check")
     ap.add_argument("--cpu-tokens", type=int, default=2048, help="tokens of the cpu_baseline oracle layer")
     ap.add_argument("--layers", type=int, default=0, help="(dev only) override layer count")
+    ap.add_argument("--b-dense", type=int, default=0, help="(dev only) override the dense batch size (tokens)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ablation", action="store_true", help="skip the sequential / nano-only comparison runs")
     ap.add_argument("--timeline", default="", help="write one step's kernel spans (CSV) to this path (per rank at N>1)")
