@@ -28,6 +28,11 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--corun", action="store_true", help="measure each point next to a co-runner on 148-u SMs")
+    ap.add_argument("--shape", default="8b", choices=["8b", "c3rank"],
+                    help="c3rank: one LLaMA-2-70B TP8 rank's shards (8/1 heads, F 3584) on the 512/1024 workload, "
+                         "plus NET points of an NVLink model (see --net-gbs)")
+    ap.add_argument("--net-gbs", type=float, default=770.0,
+                    help="c3rank NET model: per-direction NVLink GB/s reached with >= 16 SMs (B200_PROFILING.md)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -36,7 +41,12 @@ def main():
     from paper_2408_12757_b200 import nf, runtime as rt
 
     dev = torch.device("cuda")
-    shape = synth.SHAPES["llama3-8b"]
+    if args.shape == "c3rank":
+        shape = synth.shape_with(synth.SHAPES["llama2-70b"], n_q_heads=8, n_kv_heads=1, d_ffn=3584)
+        p_in, d_out = 512, 1024
+    else:
+        shape = synth.SHAPES["llama3-8b"]
+        p_in, d_out = 1024, 512
     D, F, hd, Hq, Hk = shape.d_model, shape.d_ffn, shape.head_dim, shape.n_q_heads, shape.n_kv_heads
     units = [8, 16, 32, 48, 64, 80, 96, 112, 128, 148] if args.quick else list(range(8, 145, 8)) + [148]
     rows = []
@@ -90,7 +100,7 @@ def main():
 
     # co-runners: decode attention over the steady-state decode batch (next to GEMMs / prefill),
     # the Up/Gate GEMM at M=1024 (next to decode attention)
-    full0 = synth.workload_batch(2048, 1024, 512)
+    full0 = synth.workload_batch(2048, p_in, d_out)
     n0 = int((full0.q_len == 1).sum())
     b_cr = synth.make_batch([1] * n0, full0.kv_prefix[:n0], seed=5)
     nb_cr = nf.Batch.from_any(b_cr)
@@ -112,6 +122,7 @@ def main():
 
     # dense GEMMs at the nano-batch size (1024 tokens) and the full batch
     gemms = {nf.OP_KQV: ((Hq + 2 * Hk) * hd, D), nf.OP_O: (D, Hq * hd), nf.OP_UG: (2 * F, D), nf.OP_DOWN: (D, F)}
+    # (c3rank: O is the rank's row-parallel O2 [M, D] x [D, D/8]^T; its column-parallel O1 has the same FLOPs)
     corunner["fn"] = cr_decode
     for M in (512, 1024, 2048):
         A = torch.randn(M, max(D, F), device=dev).to(torch.bfloat16)
@@ -127,7 +138,7 @@ def main():
         del A
     # decode attention over the steady-state decode requests (683, contexts 1024..1535)
     corunner["fn"] = cr_gemm
-    full = synth.workload_batch(2048, 1024, 512)
+    full = synth.workload_batch(2048, p_in, d_out)
     n_dec = int((full.q_len == 1).sum())
     for frac in (0.5, 1.0):
         n = int(n_dec * frac)
@@ -147,7 +158,8 @@ def main():
         del pool
     # prefill attention: the chunk (341, prefix 683) + prompt (1024)
     corunner["fn"] = cr_decode
-    b = synth.make_batch([341, 1024], [683, 0], seed=3)
+    b = synth.make_batch([341, 1024], [683, 0], seed=3) if args.shape == "8b" else \
+        synth.make_batch([171, 512], [341, 0], seed=3)
     nb = nf.Batch.from_any(b)
     pool = torch.randn((b.n_pages_pool, 2, Hk, 16, hd), device=dev).to(torch.bfloat16)
     q = torch.randn((b.n_tokens, Hq, hd), device=dev).to(torch.bfloat16)
@@ -158,6 +170,16 @@ def main():
         t = timeit(lambda: nf.attention(cfg, nb, q.data_ptr(), pool.data_ptr(), o.data_ptr(), ws.data_ptr(),
                                         ws.numel(), u, u, st), u)
         rows.append((nf.OP_PREFILL_ATTN, "compute", u, keys, t))
+    if args.shape == "c3rank":
+        # NET: NO measurement is possible on one GPU.  Model (reading P-8 / §7a): an
+        # AllGather-equivalent token moves (N-1)/N * D * 2 bytes per rank at N = 8; NCCL reaches
+        # the measured per-direction NVLink bandwidth with >= 16 CTAs (PAPER.md:614 reports 92 % of
+        # peak with 35 of 108 A100 SMs), proportionally less below; 10 us launch + sync latency.
+        per_tok = 7 / 8 * D * 2
+        for u in units:
+            for w in (256.0, 1024.0, 2048.0, 4096.0):
+                bw = args.net_gbs * 1e9 * min(1.0, u / 16.0)
+                rows.append((nf.OP_NET, "network", u, w, 10e-6 + w * per_tok / bw))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
         f.write("op_kind,resource_class,units,work,latency_s\n")
