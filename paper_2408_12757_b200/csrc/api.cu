@@ -248,6 +248,10 @@ void build_meta(const nf_model_cfg* c, const nf_batch* b, const std::vector<int>
     }
     nr.dec_n = (int)dec.size() - nr.dec_off;
     nr.pf_n = (int)pf.size() - nr.pf_off;
+    nr.dec_rows_off = m->nanos.empty() ? 0 : m->nanos.back().dec_rows_off;
+    if (!m->nanos.empty())
+      for (int q = m->nanos.back().dec_off; q < m->nanos.back().dec_off + m->nanos.back().dec_n; ++q)
+        nr.dec_rows_off += (dec[q].kv_len + P - 1) / P;
     // longest first: static round-robin over warps/CTAs is then LPT-like
     std::stable_sort(dec.begin() + nr.dec_off, dec.end(),
                      [](const DecodeItem& x, const DecodeItem& y) { return x.kv_len > y.kv_len; });
@@ -355,6 +359,13 @@ Workspace carve_workspace(const nf_model_cfg* c, const nf_batch* b, void* base) 
   w.sk_flag = (int*)take((size_t)w.sk_flag_n * (N > 1 ? 2 : 1) * 4);
   w.sk_flag2 = (N > 1 && w.sk_flag) ? w.sk_flag + w.sk_flag_n : nullptr;
   w.sk_flag_total = w.sk_flag_n * (N > 1 ? 2 : 1);
+  {
+    int64_t dec_pages = 0;
+    for (int r = 0; r < b->n_req; ++r)
+      if (b->q_len[r] == 1) dec_pages += ((int64_t)b->kv_prefix[r] + 1 + c->page_size - 1) / c->page_size;
+    w.dec_rows = (int*)take((size_t)(dec_pages * (c->n_kv_heads / N) + 64) * 4);
+    w.dec_wstart = (int*)take((size_t)NF_MAX_NANO * 2049 * 4);
+  }
   if (c->n_experts > 0) {
     const int64_t cap = moe_rows_cap(c, T), nk = T * c->top_k;
     w.mo_cap = cap;
@@ -771,6 +782,7 @@ struct LayerCtx {
   cudaStream_t ns;      // network stream (TP collectives; == cs outside OVERLAP)
   cudaStream_t cs2 = nullptr;  // TP OVERLAP: compute stream of the second dense nano-batch (null: cs)
   bool dec_on_cs = false;      // no memory partition: decode attention on the (group's) compute stream
+  mutable bool rows_built[NF_MAX_NANO] = {};  // decode row streams written this step (ROWS loader)
   nf_comm* comm;
   int cap_dense = 0, cap_dec = 0;  // partition sizes when green contexts are active (0: whole GPU)
 };
@@ -792,6 +804,11 @@ bool use_tc_decode(const nf_model_cfg* c, const nf_plan* p) {
 }
 // warp-specialised decode (decode_ws.cu): NF_DECODE_IMPL=ws, not in co-located plans
 bool use_ws_decode(const nf_plan* p) { return decode_impl_env() == 2 && !p->spec.colocate; }
+// row-stream loader of the default decode kernel (NF_DEC_ROWS=0 disables it)
+bool use_rows_decode() {
+  const char* e = getenv("NF_DEC_ROWS");
+  return !(e && e[0] == '0');
+}
 
 nf_status run_kqv(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x, const float* part, int nparts,
                   const nf_packed_layer* wt, void* pool) {
@@ -865,17 +882,34 @@ nf_status run_decode(const LayerCtx& L, const NanoRange& nr, cudaStream_t st, in
   const int n = part == 0 ? nr.dec_n : (part == 1 ? nr.dec_n - nr.dec_cs_n : nr.dec_cs_n);
   if (n <= 0) return NF_OK;
   const nf_model_cfg* c = L.c;
-  const AttnArgs a = attn_args(L);
+  AttnArgs a = attn_args(L);
   const DecodeItem* dec = reinterpret_cast<const DecodeItem*>(L.meta_dev + L.m->off_dec) + nr.dec_off + off;
   const int sms = part == 2     ? clamp_dense(L, L.p->spec.sm[NF_OP_KQV])
                   : L.dec_on_cs ? clamp_dense(L, L.p->spec.sm[NF_OP_DECODE_ATTN])
                                 : clamp_dec(L, L.p->spec.sm[NF_OP_DECODE_ATTN]);
   ProfScope ps(NF_OP_DECODE_ATTN, st);
-  if (use_tc_decode(c, L.p))
+  if (use_tc_decode(c, L.p)) {
     NF_CUDA(launch_decode_attention_tc(L.pool_map, a, dec, n, sms, st));
-  else if (use_ws_decode(L.p))
+  } else if (use_ws_decode(L.p)) {
     NF_CUDA(launch_decode_attention_ws(L.page_map, a, dec, n, sms, st));
-  else
+  } else if (part != 2 && use_rows_decode() && a.dec_warps != 4 && L.w->dec_rows) {
+    // row streams of this nano-batch's launch geometry, written once per step (every layer
+    // of a step has the same items, pages and grid)
+    const int k = (int)(&nr - &L.m->nanos[0]);
+    const int W = decode_warps(c->head_dim, a.dec_warps);
+    const int grid = decode_grid(n, sms, W);
+    int* rows = L.w->dec_rows + nr.dec_rows_off;
+    int* wst = L.w->dec_wstart + k * 2049;
+    if (grid * W <= 2048) {
+      if (k < 0 || k >= NF_MAX_NANO || !L.rows_built[k]) {
+        NF_CUDA(launch_build_dec_rows(dec, n, grid, W, a.page_ids, a.kh, rows, wst, st));
+        if (k >= 0 && k < NF_MAX_NANO) L.rows_built[k] = true;
+      }
+      a.dec_rows = rows;
+      a.dec_wstart = wst;
+    }
+    NF_CUDA(launch_decode_attention(L.pool_map, L.page_map, a, dec, n, sms, st));
+  } else
     NF_CUDA(launch_decode_attention(L.pool_map, L.page_map, a, dec, n, sms, st));
   return NF_OK;
 }

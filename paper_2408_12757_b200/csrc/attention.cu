@@ -59,7 +59,11 @@ NF_DEV uint32_t movmatrix_trans(uint32_t a) {
   return d;
 }
 
-template <int HD, int DEC_WARPS>
+// ROWS: the loader streams precomputed TMA rows (a.dec_rows / a.dec_wstart: the warp's
+// pages in consumption order across its items) instead of walking item headers and
+// page-id windows -- the loader bookkeeping was ~1/4 of the issued instructions per page
+// (profiles/r2_ncu_decode.md).
+template <int HD, int DEC_WARPS, bool ROWS = false>
 __global__ void __launch_bounds__(DEC_WARPS * 32)
     decode_attn_kernel(const __grid_constant__ CUtensorMap pool, const __grid_constant__ CUtensorMap pages,
                        const AttnArgs a,
@@ -109,11 +113,42 @@ __global__ void __launch_bounds__(DEC_WARPS * 32)
     return first + lane < h.np ? a.page_ids[h.ps + first + lane] : 0;
   };
   int l_round = 0, l_item = gw, l_page = 0;
-  Hdr cur = header(l_item), nxt = header(item_of(1)), nn = header(item_of(2));
-  int pid_win = window(cur, 0), pid_nwin = window(cur, 32), n_win = window(nxt, 0);
+  Hdr cur{0, 0, 0}, nxt{0, 0, 0}, nn{0, 0, 0};
+  int pid_win = 0, pid_nwin = 0, n_win = 0;
+  // ROWS loader state: position in the warp's row stream and two 32-row windows
+  int r_pos = 0, r_len = 0, r_base = 0, r_win = 0, r_nwin = 0;
+  if constexpr (ROWS) {
+    r_base = a.dec_wstart[gw];
+    r_len = a.dec_wstart[gw + 1] - r_base;
+    r_win = lane < r_len ? a.dec_rows[r_base + lane] : 0;
+    r_nwin = 32 + lane < r_len ? a.dec_rows[r_base + 32 + lane] : 0;
+  } else {
+    cur = header(l_item);
+    nxt = header(item_of(1));
+    nn = header(item_of(2));
+    pid_win = window(cur, 0);
+    pid_nwin = window(cur, 32);
+    n_win = window(nxt, 0);
+  }
   uint32_t issued = 0, consumed = 0;
   const uint64_t kv_policy = policy_evict_first();  // K/V pages are read exactly once: keep L2 for the GEMMs
   auto issue_one = [&]() {
+    if constexpr (ROWS) {
+      if (r_pos >= r_len) return;
+      const int s = issued % NS;
+      const int rowK = __shfl_sync(0xffffffffu, r_win, r_pos & 31);
+      if (lane == 0) {
+        fence_proxy_async();  // WAR: this warp's ldmatrix reads of the slot before the async-proxy refill
+        mbar_arrive_expect_tx(&bars[s], STAGE_BYTES);
+        tma_load_4d_hint(ring + s * STAGE_BYTES, &pages, &bars[s], 0, rowK, 0, 0, kv_policy);
+      }
+      ++issued;
+      if ((++r_pos & 31) == 0) {
+        r_win = r_nwin;
+        r_nwin = r_pos + 32 + lane < r_len ? a.dec_rows[r_base + r_pos + 32 + lane] : 0;
+      }
+      return;
+    }
     if (l_item >= n_items) return;
     const int s = issued % NS;
     const int64_t page = __shfl_sync(0xffffffffu, pid_win, l_page & 31);
@@ -465,6 +500,46 @@ __global__ void __launch_bounds__(PF_THREADS)
   }
 }
 
+// Row streams for one decode launch: block-parallel.  Every block computes the page totals
+// of all consumer warps (their items in the kernel's snake order) and the exclusive scan
+// (block 0 writes wstart); then each warp of the grid writes one consumer warp's rows
+// (lanes over pages).
+__global__ void build_dec_rows_kernel(const DecodeItem* __restrict__ items, int n_items, int grid, int warps,
+                                      const int* __restrict__ page_ids, int kh, int* __restrict__ rows,
+                                      int* __restrict__ wstart) {
+  __shared__ int tot[2048 + 1];
+  const int TW = grid * warps;
+  auto item_of = [&](int gw, int round) { return round * TW + ((round & 1) ? TW - 1 - gw : gw); };
+  for (int gw = threadIdx.x; gw < TW; gw += blockDim.x) {
+    int t = 0;
+    for (int round = 0, it = item_of(gw, 0); it < n_items; it = item_of(gw, ++round)) t += (items[it].kv_len + 15) >> 4;
+    tot[gw] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // TW <= 2048: a serial scan is ~2k adds
+    int acc = 0;
+    for (int gw = 0; gw < TW; ++gw) {
+      const int v = tot[gw];
+      tot[gw] = acc;
+      acc += v;
+    }
+    tot[TW] = acc;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int gw = threadIdx.x; gw <= TW; gw += blockDim.x) wstart[gw] = tot[gw];
+  const int lane = threadIdx.x & 31;
+  for (int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gw < TW; gw += gridDim.x * (blockDim.x >> 5)) {
+    int o = tot[gw];
+    for (int round = 0, it = item_of(gw, 0); it < n_items; it = item_of(gw, ++round)) {
+      const DecodeItem d = items[it];
+      const int np = (d.kv_len + 15) >> 4;
+      for (int p = lane; p < np; p += 32) rows[o + p] = ((page_ids[d.page_start + p] * 2) * kh + d.kvh) * 16;
+      o += np;
+    }
+  }
+}
+
 template <int HD, int W>
 cudaError_t launch_decode_hdw(const CUtensorMap& m, const CUtensorMap& pm, const AttnArgs& a, const DecodeItem* items, int n_items,
                               int sm_budget, cudaStream_t st) {
@@ -476,8 +551,19 @@ cudaError_t launch_decode_hdw(const CUtensorMap& m, const CUtensorMap& pm, const
     attr = true;
   }
   // one CTA per SM of the budget (8-warp CTAs fill an SM's smem; 4-warp CTAs leave room for a GEMM CTA)
-  int grid = std::min((n_items + W - 1) / W, std::max(sm_budget, 1));
-  decode_attn_kernel<HD, W><<<grid, W * 32, dec_smem<HD, W>(), st>>>(m, pm, a, items, n_items);
+  int grid = decode_grid(n_items, sm_budget, W);
+  if (a.dec_rows) {
+    static bool attr_r = false;
+    if (!attr_r) {
+      cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<HD, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           dec_smem<HD, W>());
+      if (e != cudaSuccess) return e;
+      attr_r = true;
+    }
+    decode_attn_kernel<HD, W, true><<<grid, W * 32, dec_smem<HD, W>(), st>>>(m, pm, a, items, n_items);
+  } else {
+    decode_attn_kernel<HD, W><<<grid, W * 32, dec_smem<HD, W>(), st>>>(m, pm, a, items, n_items);
+  }
   count_launch();
   return cudaGetLastError();
 }
@@ -485,12 +571,7 @@ cudaError_t launch_decode_hdw(const CUtensorMap& m, const CUtensorMap& pm, const
 template <int HD>
 cudaError_t launch_decode_hd(const CUtensorMap& m, const CUtensorMap& pm, const AttnArgs& a, const DecodeItem* items, int n_items,
                              int sm_budget, cudaStream_t st) {
-  static int env_w = -1;
-  if (env_w < 0) {
-    const char* e = getenv("NF_DEC_WARPS");
-    env_w = e ? atoi(e) : 0;
-  }
-  const int w = a.dec_warps == 4 ? 4 : (env_w ? env_w : (HD == 128 ? 12 : 8));
+  const int w = decode_warps(HD, a.dec_warps);
   if (w == 4) return launch_decode_hdw<HD, 4>(m, pm, a, items, n_items, sm_budget, st);
   if (w == 6) return launch_decode_hdw<HD, 6>(m, pm, a, items, n_items, sm_budget, st);
   if (w == 12) return launch_decode_hdw<HD, 12>(m, pm, a, items, n_items, sm_budget, st);
@@ -516,6 +597,30 @@ cudaError_t launch_prefill_hd(const CUtensorMap& m, const AttnArgs& a, const Pre
 }
 
 }  // namespace
+
+int decode_warps(int hd, int dec_warps_arg) {
+  static int env_w = -1;
+  if (env_w < 0) {
+    const char* e = getenv("NF_DEC_WARPS");
+    env_w = e ? atoi(e) : 0;
+  }
+  const int w = dec_warps_arg == 4 ? 4 : (env_w ? env_w : (hd == 128 ? 12 : 8));
+  return (w == 4 || w == 6 || w == 8 || w == 12 || w == 14) ? w : 8;
+}
+
+int decode_grid(int n_items, int sm_budget, int warps) {
+  return std::min((n_items + warps - 1) / warps, std::max(sm_budget, 1));
+}
+
+cudaError_t launch_build_dec_rows(const DecodeItem* items, int n_items, int grid, int warps, const int* page_ids, int kh,
+                                  int* rows, int* wstart, cudaStream_t st) {
+  if (n_items <= 0) return cudaSuccess;
+  if (grid * warps > 2048) return cudaErrorInvalidValue;
+  build_dec_rows_kernel<<<std::max(1, std::min(64, grid)), 256, 0, st>>>(items, n_items, grid, warps, page_ids, kh,
+                                                                          rows, wstart);
+  count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_decode_attention(const CUtensorMap& m, const CUtensorMap& pm, const AttnArgs& a0, const DecodeItem* items, int n_items,
                                     int sm_budget, cudaStream_t st) {

@@ -28,7 +28,19 @@ struct AttnArgs {
   int dec_warps;            // decode CTA size: 8 (own SMs) or 4 (co-resident with a GEMM CTA)
   int n_rows;               // T: rows of q / o (bound of the prefill kernel's q tensor map)
   int pf_dist;              // decode: L2 prefetch distance in pages within an item (0 = off); set by the launcher
+  // decode row streams (optional): per consumer warp gw the TMA rows of all pages of its items in
+  // order, dec_rows[dec_wstart[gw] .. dec_wstart[gw+1]) (built by launch_build_dec_rows)
+  const int* dec_rows;
+  const int* dec_wstart;
 };
+
+// Decode launch geometry shared by the row-stream builder and the kernel.
+int decode_warps(int hd, int dec_warps_arg);
+int decode_grid(int n_items, int sm_budget, int warps);
+// Row streams of one decode launch (items sorted as the kernel takes them, `grid` CTAs of
+// `warps` consumer warps): rows [sum of the items' pages] and wstart [grid * warps + 1].
+cudaError_t launch_build_dec_rows(const DecodeItem* items, int n_items, int grid, int warps, const int* page_ids, int kh,
+                                  int* rows, int* wstart, cudaStream_t st);
 
 cudaError_t make_page_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, int kh, int hd, int page_size);
 // q [T, qh, hd] as a 3-D map {hd, qh, T}: box {64, 1, 128} = 128 token rows of one head, 128B-swizzled

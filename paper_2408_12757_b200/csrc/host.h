@@ -35,6 +35,7 @@ struct NanoRange {
   int t0, t1;        // token rows
   int dec_off, dec_n;  // decode items
   int dec_cs_n = 0;    // OVERLAP: this many of the shortest decode items run on the compute partition
+  int dec_rows_off = 0;  // offset of this nano-batch's decode row streams in the workspace (ROWS loader)
   int pf_off, pf_n;    // prefill items
 };
 
@@ -83,6 +84,8 @@ struct Workspace {
   float *mo_roww, *mo_rowinv;
   __nv_bfloat16 *mo_x, *mo_m, *mo_y;
   int* mo_cta;       // per-router-CTA expert counts, then bases (moe.cuh MoeGroupArgs)
+  int* dec_rows;     // decode row streams of every nano-batch (sum of decode pages x kv heads)
+  int* dec_wstart;   // [NF_MAX_NANO][2049] per-warp stream offsets
   int64_t mo_cap;    // grouped rows capacity
   size_t total;
 };

@@ -582,3 +582,29 @@ def test_overlap_partitions_are_sm_disjoint(env, dec, net, tp):
         assert len(netp) == (net + 7) // 8 * 8, (len(netp), note)
     assert len(mem | cmp_ | netp) == n_sm
     print(note, {k: len(v) for k, v in zip(("memory", "compute", "network"), sets)})
+
+
+def test_decode_row_stream_loader_bit_exact(env, monkeypatch):
+    """The row-stream loader (default) and the item-walking loader (NF_DEC_ROWS=0) feed the
+    same pages in the same order to the same math: bit-identical outputs, at several SM
+    budgets and through a full OVERLAP layer (the rows are built once per step and reused)."""
+    shape = synth.SHAPES["llama3-8b"]
+    q_len = [1] * 41
+    prefix = [0, 1, 15, 16, 17, 31, 32, 33, 100, 255, 256, 257, 1000, 1535, 511, 512] + list(range(40, 40 + 25 * 29, 29))
+    b, pool, q = _attn_case(shape, q_len, prefix, seed=9)
+    for sm in (3, 32, 148):
+        monkeypatch.setenv("NF_DEC_ROWS", "0")
+        ref = _run_attn(env, shape, b, pool, q, sm_dec=sm)
+        monkeypatch.setenv("NF_DEC_ROWS", "1")
+        out = _run_attn(env, shape, b, pool, q, sm_dec=sm)
+        assert np.array_equal(ref, out), sm
+    nf, rt = env
+    sh = synth.shape_with(synth.SHAPES["llama3-8b"], n_layers=3)
+    bb = synth.workload_batch(512, 1024, 512)
+    w, x, pl = _layer_case(sh, bb)
+    outs = []
+    for rows in ("0", "1"):
+        monkeypatch.setenv("NF_DEC_ROWS", rows)
+        o, _ = _gpu_layer(env, sh, bb, w, x, pl, 2, (1, 1))
+        outs.append(o)
+    assert np.array_equal(outs[0], outs[1])
