@@ -795,19 +795,25 @@ int clamp_dec(const LayerCtx& L, int v) { return clampsm(L.cap_dec ? std::min(v,
 // 4-D TMA box per page) is the default: it reaches the HBM roofline at ~80 SMs.
 // The tcgen05 kernel (decode_tc.cu, one item in flight per CTA) is selectable
 // with NF_DECODE_IMPL=tc for head_dim 128 / GQA <= 8 (not in co-located plans).
+// Default: the stream kernel (decode_stream.cu) when its row streams fit; NF_DECODE_IMPL=fused
+// selects the item-walking kernel (attention.cu), =tc / =ws the tcgen05 / warp-specialised ones.
 int decode_impl_env() {  // read per launch (tests switch it at run time)
   const char* e = getenv("NF_DECODE_IMPL");
-  return (e && std::string(e) == "tc") ? 1 : ((e && std::string(e) == "ws") ? 2 : 0);
+  if (!e) return 0;
+  const std::string v(e);
+  return v == "tc" ? 1 : v == "ws" ? 2 : v == "fused" ? 3 : 0;
 }
 bool use_tc_decode(const nf_model_cfg* c, const nf_plan* p) {
   return decode_impl_env() == 1 && !p->spec.colocate && c->head_dim == 128 && c->n_q_heads / c->n_kv_heads <= 8;
 }
 // warp-specialised decode (decode_ws.cu): NF_DECODE_IMPL=ws, not in co-located plans
 bool use_ws_decode(const nf_plan* p) { return decode_impl_env() == 2 && !p->spec.colocate; }
-// row-stream loader of the default decode kernel (NF_DEC_ROWS=0 disables it)
+// row-stream loader of the default decode kernel: opt-in with NF_DEC_ROWS=1 (measured
+// 9 % (8B) / 10 % (70B rank) slower per SM than the item-walking loader at 32 SMs,
+// profiles/r2e_attn_rows_ab.log)
 bool use_rows_decode() {
   const char* e = getenv("NF_DEC_ROWS");
-  return !(e && e[0] == '0');
+  return e && e[0] == '1';
 }
 
 nf_status run_kqv(const LayerCtx& L, const NanoRange& nr, const __nv_bfloat16* x, const float* part, int nparts,
@@ -892,6 +898,21 @@ nf_status run_decode(const LayerCtx& L, const NanoRange& nr, cudaStream_t st, in
     NF_CUDA(launch_decode_attention_tc(L.pool_map, a, dec, n, sms, st));
   } else if (use_ws_decode(L.p)) {
     NF_CUDA(launch_decode_attention_ws(L.page_map, a, dec, n, sms, st));
+  } else if (part != 2 && decode_impl_env() == 0 && a.dec_warps != 4 && L.w->dec_rows && decode_stream_supported(a) &&
+             decode_grid(n, sms, 12) * 12 <= 2048) {
+    // stream kernel: row streams of this nano-batch's 12-warp launch geometry, written once per
+    // step (every layer of a step has the same items, pages and grid)
+    const int k = (int)(&nr - &L.m->nanos[0]);
+    const int grid = decode_grid(n, sms, 12);
+    int* rows = L.w->dec_rows + nr.dec_rows_off;
+    int* wst = L.w->dec_wstart + k * 2049;
+    if (k < 0 || k >= NF_MAX_NANO || !L.rows_built[k]) {
+      NF_CUDA(launch_build_dec_rows(dec, n, grid, 12, a.page_ids, a.kh, rows, wst, st));
+      if (k >= 0 && k < NF_MAX_NANO) L.rows_built[k] = true;
+    }
+    a.dec_rows = rows;
+    a.dec_wstart = wst;
+    NF_CUDA(launch_decode_attention_stream(L.page_map, a, dec, n, sms, st));
   } else if (part != 2 && use_rows_decode() && a.dec_warps != 4 && L.w->dec_rows) {
     // row streams of this nano-batch's launch geometry, written once per step (every layer
     // of a step has the same items, pages and grid)

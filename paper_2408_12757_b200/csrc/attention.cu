@@ -508,23 +508,41 @@ __global__ void build_dec_rows_kernel(const DecodeItem* __restrict__ items, int 
                                       const int* __restrict__ page_ids, int kh, int* __restrict__ rows,
                                       int* __restrict__ wstart) {
   __shared__ int tot[2048 + 1];
+  __shared__ int wsum[8];
   const int TW = grid * warps;
   auto item_of = [&](int gw, int round) { return round * TW + ((round & 1) ? TW - 1 - gw : gw); };
-  for (int gw = threadIdx.x; gw < TW; gw += blockDim.x) {
+  // per-warp page totals, then a block-wide exclusive scan (blockDim 256, 8 consecutive warps per thread)
+  const int per = (TW + 255) / 256, g0 = threadIdx.x * per;
+  int run = 0;
+  for (int k = 0; k < per; ++k) {
+    const int gw = g0 + k;
     int t = 0;
-    for (int round = 0, it = item_of(gw, 0); it < n_items; it = item_of(gw, ++round)) t += (items[it].kv_len + 15) >> 4;
-    tot[gw] = t;
+    if (gw < TW)
+      for (int round = 0, it = item_of(gw, 0); it < n_items; it = item_of(gw, ++round)) t += (items[it].kv_len + 15) >> 4;
+    if (gw < TW) tot[gw] = t;
+    run += t;
   }
+  int incl = run;  // inclusive scan of the per-thread sums: warp shuffles, then the 8 warp totals
+  const int ln = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (ln >= o) incl += v;
+  }
+  if (ln == 31) wsum[wp] = incl;
   __syncthreads();
-  if (threadIdx.x == 0) {  // TW <= 2048: a serial scan is ~2k adds
-    int acc = 0;
-    for (int gw = 0; gw < TW; ++gw) {
+  int base = 0;
+  for (int w2 = 0; w2 < wp; ++w2) base += wsum[w2];
+  int acc = base + incl - run;  // exclusive prefix of this thread's first warp
+  for (int k = 0; k < per; ++k) {
+    const int gw = g0 + k;
+    if (gw < TW) {
       const int v = tot[gw];
       tot[gw] = acc;
       acc += v;
     }
-    tot[TW] = acc;
   }
+  if (threadIdx.x == 255) tot[TW] = acc;
   __syncthreads();
   if (blockIdx.x == 0)
     for (int gw = threadIdx.x; gw <= TW; gw += blockDim.x) wstart[gw] = tot[gw];
@@ -616,7 +634,7 @@ cudaError_t launch_build_dec_rows(const DecodeItem* items, int n_items, int grid
                                   int* rows, int* wstart, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
   if (grid * warps > 2048) return cudaErrorInvalidValue;
-  build_dec_rows_kernel<<<std::max(1, std::min(64, grid)), 256, 0, st>>>(items, n_items, grid, warps, page_ids, kh,
+  build_dec_rows_kernel<<<std::max(1, std::min(148, grid * warps / 8)), 256, 0, st>>>(items, n_items, grid, warps, page_ids, kh,
                                                                           rows, wstart);
   count_launch();
   return cudaGetLastError();

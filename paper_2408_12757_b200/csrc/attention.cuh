@@ -49,6 +49,11 @@ cudaError_t make_pool_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, in
 
 cudaError_t launch_decode_attention(const CUtensorMap& pool_map, const CUtensorMap& page_map, const AttnArgs& a, const DecodeItem* items,
                                     int n_items, int sm_budget, cudaStream_t stream);
+// stream decode attention (decode_stream.cu; needs a.dec_rows / a.dec_wstart built for a
+// 12-warp geometry by launch_build_dec_rows): head_dim 64/128, page 16, GQA group <= 8
+bool decode_stream_supported(const AttnArgs& a);
+cudaError_t launch_decode_attention_stream(const CUtensorMap& page_map, const AttnArgs& a, const DecodeItem* items,
+                                           int n_items, int sm_budget, cudaStream_t stream);
 // warp-specialised decode attention (one producer warp drives every consumer warp's TMA ring); decode_ws.cu
 cudaError_t launch_decode_attention_ws(const CUtensorMap& page_map, const AttnArgs& a, const DecodeItem* items,
                                        int n_items, int sm_budget, cudaStream_t stream);

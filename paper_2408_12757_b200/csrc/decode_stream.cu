@@ -1,0 +1,274 @@
+// Paged GQA decode attention, "stream" formulation (default for head_dim 64/128,
+// GQA group R <= 8, "decode attention ... memory
+// bound", :626 (paged KV)).
+//
+// Same arithmetic as decode_attn_kernel (attention.cu: transposed S^T = K.Q^T with
+// the page's 16 keys as the MMA M rows and the group's query heads as N columns,
+// P^T moved into a B fragment with movmatrix, O^T += V^T.P^T), rebuilt around a
+// short per-page instruction chain, because that kernel is issue-bound on small SM
+// partitions (profiles/r2_ncu_decode.md: ~220 issued instructions per 8 KB page, of
+// which 32 are the ldmatrix / MMA work):
+//  * the TMA loader walks a flat per-warp stream of page rows (a.dec_rows, built once
+//    per step by build_dec_rows_kernel in the kernel's own item order): one TMA and
+//    one uniform row load per page, no item headers or page-id windows;
+//  * the softmax denominator l comes out of the tensor pipe: one extra MMA per page
+//    with an all-ones A fragment sums the bf16 P^T columns (the same rounded P the
+//    numerator uses), replacing the per-page FADDs and the final cross-lane sum;
+//  * S^T accumulates in two chains (two FADDs per score instead of three);
+//  * masking of keys past kv_len (scores -> -inf, V elements -> 0 in registers, no
+//    shared-memory zeroing) runs only on an item's last page;
+//  * ldmatrix lane offsets (swizzle included) are computed once per warp.
+// Per warp: an NS-deep ring of whole pages (K and V of one KV head, one 4-D TMA box),
+// a page's K and V fragments are pulled into registers and the slot is refilled
+// before any softmax math (a slot is busy for the load latency only).
+#include <algorithm>
+#include <cstdlib>
+
+#include "attention.cuh"
+#include "common.cuh"
+#include "profile.h"
+
+namespace nf {
+namespace {
+
+constexpr int DS_BOX = 16 * 128;  // one 16-row x 64-column 128B-swizzled box
+
+template <int HD>
+constexpr int ds_stages() { return HD == 128 ? 2 : 4; }
+
+template <int HD, int W>
+constexpr int ds_smem() { return W * ds_stages<HD>() * (2 * 16 * HD * 2) + W * ds_stages<HD>() * 8 + 1024; }
+
+NF_DEV uint32_t movm_trans(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
+}
+
+NF_DEV int ld_uniform(const int* p) {  // every lane loads the same word (one transaction)
+  int v;
+  asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+template <int HD, int W>
+__global__ void __launch_bounds__(W * 32, 1)
+    decode_stream_kernel(const __grid_constant__ CUtensorMap pages, const AttnArgs a,
+                         const DecodeItem* __restrict__ items, int n_items) {
+  constexpr int KB = 16 * HD * 2;  // K (or V) bytes of one page of one KV head
+  constexpr int SB = 2 * KB;       // stage: K then V
+  constexpr int NS = ds_stages<HD>();
+  constexpr int KS = HD / 16;      // k-steps of S^T = m-tiles of O^T
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring_p = smem + warp * NS * SB;
+  const uint32_t ring = smem_u32(ring_p);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + W * NS * SB) + warp * NS;
+  if (lane == 0) {
+    if (warp == 0) tma_prefetch_desc(&pages);
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+
+  // Items (sorted longest first on the host) in snake order, warp-major across CTAs --
+  // the order build_dec_rows_kernel wrote this warp's row stream in.
+  const int gw = warp * gridDim.x + blockIdx.x, TW = gridDim.x * W;
+  auto item_of = [&](int round) { return round * TW + ((round & 1) ? TW - 1 - gw : gw); };
+  const int R = a.qh / a.kh;
+  const int r0 = a.dec_wstart[gw];
+  const int n_pg = a.dec_wstart[gw + 1] - r0;
+  const int* rows = a.dec_rows + r0;
+  const uint64_t kv_policy = policy_evict_first();  // K/V pages are read exactly once: keep L2 for the GEMMs
+
+  auto issue = [&](uint32_t j, int row) {  // page j of the stream -> slot j % NS
+    if (lane == 0) {
+      const uint32_t s = j % NS;
+      fence_proxy_async();  // WAR: this warp's ldmatrix reads of the slot before the async-proxy refill
+      mbar_arrive_expect_tx(&bars[s], SB);
+      tma_load_4d_hint(ring_p + s * SB, &pages, &bars[s], 0, row, 0, 0, kv_policy);
+    }
+  };
+#pragma unroll
+  for (int j = 0; j < NS; ++j)
+    if (j < n_pg) issue((uint32_t)j, ld_uniform(rows + j));
+  int nrow = NS < n_pg ? ld_uniform(rows + NS) : 0;  // row of the next page to issue (loaded one page early)
+  // optional L2 prefetch PF pages beyond the ring (a.pf_dist; bytes in flight beyond shared memory)
+  const int PF = a.pf_dist;
+  if (PF > 0 && lane == 0)
+    for (int q = NS; q < NS + PF && q < n_pg; ++q) tma_prefetch_4d(&pages, 0, ld_uniform(rows + q), 0, 0);
+  int prow = (PF > 0 && NS + PF < n_pg) ? ld_uniform(rows + NS + PF) : 0;
+
+  // ldmatrix lane offsets inside a stage (128B swizzle: 16-byte chunk c of row r at r*128 + ((c ^ (r&7)) << 4));
+  // for k-step ks the chunk is 2*(ks&3) + hi in box ks>>2, so four offsets serve all k-steps
+  const int x7 = lane & 7;
+  uint32_t offK[4], offV[4];
+  {
+    const int keyK = x7 + (((lane >> 3) & 1) << 3), hiK = lane >> 4;
+    const int keyV = x7 + ((lane >> 4) << 3), hiV = (lane >> 3) & 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      offK[i] = keyK * 128 + (((2 * i + hiK) ^ x7) << 4);
+      offV[i] = KB + keyV * 128 + (((2 * i + hiV) ^ x7) << 4);
+    }
+  }
+  const uint32_t ones[4] = {0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u};  // bf16 1.0 pairs
+  const float sl2 = a.scale_log2, inv_sl2 = 1.f / a.scale_log2;
+  const int g = lane >> 2;           // key row (C fragments) / query head column (B fragments)
+  const int hc = 2 * (lane & 3);     // first of the two head columns of this lane's C fragments
+  const int kk = 2 * (lane & 3);     // first key of this lane's V^T A-fragment registers 0/1 (+8: 2/3)
+
+  uint32_t j = 0;  // pages of the stream consumed
+  for (int round = 0, item = gw; item < n_items; item = item_of(++round)) {
+    const DecodeItem it = items[item];
+    {  // next item's query rows into L1 while this item streams
+      const int nx = item_of(round + 1);
+      if (nx < n_items && lane < R) {
+        const DecodeItem n2 = items[nx];
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.q + ((int64_t)n2.t * a.qh + (int64_t)n2.kvh * R + lane) * HD));
+      }
+    }
+    const __nv_bfloat16* qbase = a.q + ((int64_t)it.t * a.qh + (int64_t)it.kvh * R) * HD;
+    uint32_t qb[KS][2];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int kc = ks * 16 + hc;
+      qb[ks][0] = g < R ? *reinterpret_cast<const uint32_t*>(qbase + g * HD + kc) : 0u;
+      qb[ks][1] = g < R ? *reinterpret_cast<const uint32_t*>(qbase + g * HD + kc + 8) : 0u;
+    }
+    float m0 = -INFINITY, m1 = -INFINITY;      // running max (log2 units) of head columns hc, hc+1
+    float thr0 = -INFINITY, thr1 = -INFINITY;  // raw-score thresholds (m + 8) / scale of the lazy max
+    float oacc[KS][4], lacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int d = 0; d < KS; ++d) oacc[d][0] = oacc[d][1] = oacc[d][2] = oacc[d][3] = 0.f;
+
+    const int np = (it.kv_len + 15) >> 4;
+    for (int p = 0; p < np; ++p, ++j) {
+      const uint32_t s = j % NS;
+      mbar_wait(&bars[s], (j / NS) & 1);
+      const uint32_t base = ring + s * SB;
+      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        uint32_t kf[4];
+        ldmatrix_x4(kf, base + offK[ks & 3] + (ks >> 2) * DS_BOX);
+        if (ks & 1) mma_bf16_16816(sb, kf, qb[ks]);
+        else mma_bf16_16816(sa, kf, qb[ks]);
+      }
+      uint32_t vf[KS][4];
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) ldmatrix_x4_trans(vf[mt], base + offV[mt & 3] + (mt >> 2) * DS_BOX);
+      __syncwarp();
+      if ((int)j + NS < n_pg) {  // refill the slot with the page NS ahead
+        issue(j + NS, nrow);
+        if ((int)j + NS + 1 < n_pg) nrow = ld_uniform(rows + j + NS + 1);
+        if (PF > 0 && (int)j + NS + PF < n_pg) {
+          if (lane == 0) tma_prefetch_4d(&pages, 0, prow, 0, 0);
+          if ((int)j + NS + PF + 1 < n_pg) prow = ld_uniform(rows + j + NS + PF + 1);
+        }
+      }
+      float sc[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sc[e] = sa[e] + sb[e];
+      if (p == np - 1) {  // keys past kv_len exist only on the item's last page
+        const int valid = it.kv_len - p * 16;
+        if (g >= valid) sc[0] = sc[1] = -INFINITY;
+        if (g + 8 >= valid) sc[2] = sc[3] = -INFINITY;
+        // V rows past kv_len may hold anything (NaN in unused pool slots): zero them so P=0 rows add 0
+        const uint32_t mlo = (kk < valid ? 0x0000FFFFu : 0u) | (kk + 1 < valid ? 0xFFFF0000u : 0u);
+        const uint32_t mhi = (kk + 8 < valid ? 0x0000FFFFu : 0u) | (kk + 9 < valid ? 0xFFFF0000u : 0u);
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          vf[mt][0] &= mlo;
+          vf[mt][1] &= mlo;
+          vf[mt][2] &= mhi;
+          vf[mt][3] &= mhi;
+        }
+      }
+      // Online softmax with a lazily updated running max (attention.cu): probabilities are
+      // taken against a stale max as long as no raw score exceeds thr = (m + 8) / scale;
+      // the cross-lane max and the rescale of O and l run only when the max really moves.
+      if (__any_sync(0xffffffffu, fmaxf(sc[0], sc[2]) > thr0 || fmaxf(sc[1], sc[3]) > thr1)) {
+        float r0m = fmaxf(sc[0], sc[2]), r1m = fmaxf(sc[1], sc[3]);
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          r0m = fmaxf(r0m, __shfl_xor_sync(0xffffffffu, r0m, o));
+          r1m = fmaxf(r1m, __shfl_xor_sync(0xffffffffu, r1m, o));
+        }
+        const float mn0 = fmaxf(m0, r0m * sl2), mn1 = fmaxf(m1, r1m * sl2);
+        const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
+        m0 = mn0;
+        m1 = mn1;
+        thr0 = (mn0 + 8.f) * inv_sl2;
+        thr1 = (mn1 + 8.f) * inv_sl2;
+        lacc[0] *= al0; lacc[2] *= al0;
+        lacc[1] *= al1; lacc[3] *= al1;
+#pragma unroll
+        for (int mt = 0; mt < KS; ++mt) {
+          oacc[mt][0] *= al0; oacc[mt][1] *= al1;
+          oacc[mt][2] *= al0; oacc[mt][3] *= al1;
+        }
+      }
+      const float p0 = ex2_approx(fmaf(sc[0], sl2, -m0)), p1 = ex2_approx(fmaf(sc[1], sl2, -m1));
+      const float p2 = ex2_approx(fmaf(sc[2], sl2, -m0)), p3 = ex2_approx(fmaf(sc[3], sl2, -m1));
+      const uint32_t pb[2] = {movm_trans(pack_bf16x2(p0, p1)), movm_trans(pack_bf16x2(p2, p3))};
+      mma_bf16_16816(lacc, ones, pb);  // l_h = sum_k P^T[k][h] (every row of the ones tile)
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) mma_bf16_16816(oacc[mt], vf[mt], pb);
+    }
+    const float i0 = 1.f / lacc[0], i1 = 1.f / lacc[1];
+    __nv_bfloat16* obase = a.o + (int64_t)it.t * a.qh * HD + (int64_t)it.kvh * R * HD;
+#pragma unroll
+    for (int mt = 0; mt < KS; ++mt) {
+      const int d0 = mt * 16 + g;
+      if (hc < R) {
+        obase[hc * HD + d0] = __float2bfloat16_rn(oacc[mt][0] * i0);
+        obase[hc * HD + d0 + 8] = __float2bfloat16_rn(oacc[mt][2] * i0);
+      }
+      if (hc + 1 < R) {
+        obase[(hc + 1) * HD + d0] = __float2bfloat16_rn(oacc[mt][1] * i1);
+        obase[(hc + 1) * HD + d0 + 8] = __float2bfloat16_rn(oacc[mt][3] * i1);
+      }
+    }
+  }
+}
+
+template <int HD, int W>
+cudaError_t launch_stream_hdw(const CUtensorMap& pm, const AttnArgs& a, const DecodeItem* items, int n_items,
+                              int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(decode_stream_kernel<HD, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         ds_smem<HD, W>());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  decode_stream_kernel<HD, W><<<grid, W * 32, ds_smem<HD, W>(), st>>>(pm, a, items, n_items);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool decode_stream_supported(const AttnArgs& a) {
+  return (a.hd == 128 || a.hd == 64) && a.page_size == 16 && a.kh > 0 && a.qh % a.kh == 0 && a.qh / a.kh <= 8;
+}
+
+cudaError_t launch_decode_attention_stream(const CUtensorMap& page_map, const AttnArgs& a, const DecodeItem* items,
+                                           int n_items, int sm_budget, cudaStream_t st) {
+  if (n_items <= 0) return cudaSuccess;
+  if (!a.dec_rows || !a.dec_wstart || !decode_stream_supported(a)) return cudaErrorInvalidValue;
+  static int pf_env = -1;  // NF_DEC_PF: L2 prefetch distance in pages (0 = off)
+  if (pf_env < 0) {
+    const char* e = getenv("NF_DEC_PF");
+    pf_env = e ? std::max(0, std::min(atoi(e), 32)) : 0;
+  }
+  AttnArgs a2 = a;
+  a2.pf_dist = pf_env;
+  const int grid = decode_grid(n_items, sm_budget, 12);
+  if (a.hd == 128) return launch_stream_hdw<128, 12>(page_map, a2, items, n_items, grid, st);
+  return launch_stream_hdw<64, 12>(page_map, a2, items, n_items, grid, st);
+}
+
+}  // namespace nf

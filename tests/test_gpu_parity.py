@@ -535,9 +535,10 @@ def test_model_step_8b_full_teacher_forced(env):
     assert np.array_equal(ids_h, ids2)
 
 
-@pytest.mark.parametrize("impl", ["ws"])
+@pytest.mark.parametrize("impl", ["stream", "fused", "ws"])
 def test_decode_impl_variants_vs_oracle(env, impl, monkeypatch):
-    """The warp-specialised decode kernel (NF_DECODE_IMPL=ws) against the oracle on the 8B
+    """Every decode kernel (stream = default, fused = item-walking, ws = warp-specialised;
+    NF_DECODE_IMPL) against the oracle on the 8B
     shape (GQA 4) and a 70B TP8 rank (GQA 8, one KV head): mixed lengths incl. partial last
     pages, SM budgets 1 / 7 / 148; bit-identical across SM budgets (same per-item order)."""
     monkeypatch.setenv("NF_DECODE_IMPL", impl)
@@ -585,9 +586,11 @@ def test_overlap_partitions_are_sm_disjoint(env, dec, net, tp):
 
 
 def test_decode_row_stream_loader_bit_exact(env, monkeypatch):
-    """The row-stream loader (default) and the item-walking loader (NF_DEC_ROWS=0) feed the
-    same pages in the same order to the same math: bit-identical outputs, at several SM
-    budgets and through a full OVERLAP layer (the rows are built once per step and reused)."""
+    """The item-walking kernel's two loaders (NF_DECODE_IMPL=fused; row stream NF_DEC_ROWS=1
+    vs item walk NF_DEC_ROWS=0) feed the same pages in the same order to the same math:
+    bit-identical outputs, at several SM budgets and through a full OVERLAP layer (the rows
+    are built once per step and reused)."""
+    monkeypatch.setenv("NF_DECODE_IMPL", "fused")
     shape = synth.SHAPES["llama3-8b"]
     q_len = [1] * 41
     prefix = [0, 1, 15, 16, 17, 31, 32, 33, 100, 255, 256, 257, 1000, 1535, 511, 512] + list(range(40, 40 + 25 * 29, 29))

@@ -37,5 +37,5 @@ for sm in sms:
     e1.record()
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / reps / 1e3
-    print(f"impl={os.environ.get('NF_DECODE_IMPL', 'mma')} sm={sm}: {t*1e6:.1f} us {keys*shape.n_kv_heads*128*4/t/1e9:.0f} GB/s "
+    print(f"impl={os.environ.get('NF_DECODE_IMPL', 'stream')} sm={sm}: {t*1e6:.1f} us {keys*shape.n_kv_heads*128*4/t/1e9:.0f} GB/s "
           f"({keys*shape.n_kv_heads*128*4/t/1e9/sm:.1f} GB/s/SM)", flush=True)
