@@ -192,6 +192,44 @@ nf_status nf_comm_create_local(int32_t tp_size, int32_t ar_mode, nf_comm** comms
 nf_status nf_comm_create_loopback(int32_t tp_size, int32_t tp_rank, nf_comm** out);
 void nf_comm_destroy(nf_comm* comm);
 
+/* ---- Fused collectives over peer memory (PAPER.md:628 used
+ * MSCCL++ SM-constrained collective kernels, PAPER.md:612-614 the network SM budget).
+ * With symmetric buffers open, every row-parallel GEMM whose output the TP group sums
+ * (O2 row-parallel O projection, Down projection) runs a fused
+ * epilogue that stores each 128x256 bf16 partial block directly into the block owner's
+ * staging slot (owner = block % tp_size; a peer store over NVLink), and the owner's
+ * reduce kernel on the network stream sums the tp_size partials in rank order in fp32
+ * (one bf16 rounding: the NF_AR_F32 arithmetic) and pushes the block to every rank
+ * (all-gather), replacing the NCCL AllReduce of that site.  Dense FFN only (MoE layers
+ * keep the NCCL AllReduce).  All ranks of a group must enable it together.
+ *
+ * nf_comm_sym_bytes: size of one rank's symmetric buffer for steps of at most max_tokens
+ *   rows (d_model % 256 == 0).
+ * nf_comm_sym_alloc: allocates this rank's buffer (cudaMalloc; owned by the communicator,
+ *   freed by nf_comm_destroy) and writes its 64-byte CUDA IPC handle to ipc_handle_out_64
+ *   (may be NULL; all-zero for emulated / loopback communicators).  The caller gathers the
+ *   tp_size handles (rank order) and passes them to nf_comm_sym_open.
+ * nf_comm_sym_open: maps the other ranks' buffers (cudaIpcOpenMemHandle; emulated groups
+ *   use their shared registry and ignore ipc_handles, which may then be NULL; a loopback
+ *   rank runs its sites as a group of one) and switches the fused path on.
+ *   NF_EINVAL before nf_comm_sym_alloc or when an emulated rank has no buffer yet.
+ * nf_comm_set_fused: 0 = back to the plain AllReduce (A/B), 1 = fused (buffers must be open).
+ * nf_comm_sym_status: number of bounded waits that timed out so far (0 = healthy; a
+ *   timeout means a peer never delivered -- results of that step are invalid, nothing
+ *   hangs; NF_PEER_TIMEOUT_MS sets the bound, default 20000; nf_last_error() then names the
+ *   first one) and, if fused_sites_out is not NULL, how many fused sites this rank issued.
+ *   Synchronous.
+ * Where it runs: the owner reduce spins until the partials arrive, so it is used only where
+ * it cannot hold SMs a producer needs: SEQUENTIAL / NANO_ONLY plans (single compute stream,
+ * the reduce follows the GEMM in stream order) and OVERLAP plans whose network operation has
+ * its own green-context partition (plan sm[NF_OP_NET]); other OVERLAP plans keep the
+ * AllReduce of the communicator. */
+nf_status nf_comm_sym_bytes(const nf_model_cfg* cfg, int32_t max_tokens, size_t* bytes);
+nf_status nf_comm_sym_alloc(nf_comm* comm, const nf_model_cfg* cfg, int32_t max_tokens, void* ipc_handle_out_64);
+nf_status nf_comm_sym_open(nf_comm* comm, const void* ipc_handles);
+nf_status nf_comm_set_fused(nf_comm* comm, int32_t on);
+nf_status nf_comm_sym_status(nf_comm* comm, int32_t* timeouts_out, int64_t* fused_sites_out);
+
 /* Evidence of execution-unit partitioning: launches a probe kernel
  * (4 CTAs per SM of the device) on each of the plan's partition streams -- memory,
  * compute, network -- as an OVERLAP step would use them, and writes, per partition,

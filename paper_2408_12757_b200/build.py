@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libnf.so")
-SOURCES = ["gemm.cu", "moe.cu", "attention.cu", "misc.cu", "api.cu", "comm.cu", "planner.cpp", "profile.cu", "decode_tc.cu", "decode_ws.cu", "decode_stream.cu", "prefill_tc.cu", "green.cpp", "sched.cpp"]
+SOURCES = ["gemm.cu", "moe.cu", "attention.cu", "misc.cu", "api.cu", "comm.cu", "planner.cpp", "profile.cu", "decode_tc.cu", "decode_ws.cu", "decode_stream.cu", "peer.cu", "prefill_tc.cu", "green.cpp", "sched.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <ctime>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -14,6 +16,7 @@
 #include "host.h"
 #include "moe.cuh"
 #include "misc.cuh"
+#include "peer.cuh"
 #include "profile.h"
 
 namespace nf {
@@ -1173,6 +1176,59 @@ LayerCtx group_ctx(const LayerCtx& L, int g, Workspace* wg) {
   return c;
 }
 
+// Fused GEMM -> AllReduce sites (peer.cuh, NEXT-3): the O row-parallel projection of dense
+// group g uses site g, its Down projection site NF_MAX_NANO + g.  The decision is a pure
+// function of the communicator and the group's shape, so stages b/c/d agree on it.
+// The owner reduce spins until the group's partials arrive, so it must never hold SMs that a
+// kernel it (transitively) waits for needs: it runs either in stream order on the single
+// compute stream (SEQUENTIAL / NANO_ONLY: ns == cs) or inside the OVERLAP plan's network
+// green-context partition, whose SMs no GEMM uses.  An OVERLAP plan without a network
+// partition keeps the plain AllReduce.
+bool fused_site_ok(const LayerCtx& L, int M) {
+  if (!comm_fused(L.comm) || M <= 0) return false;
+  const bool streams_ok = L.ns == L.cs || (L.p->green_ns && L.ns == L.p->green_ns);
+  const PeerGeom& g = comm_peer_geom(L.comm);
+  const bool ok = streams_ok && M <= g.max_rows && g.cols == L.c->d_model;
+  static const bool dbg = getenv("NF_PEER_DEBUG") != nullptr;
+  if (dbg) {
+    timespec ts;
+    clock_gettime(CLOCK_REALTIME, &ts);
+    fprintf(stderr, "[nf peer] rank %d M %d streams_ok %d -> %s at host %lld ms\n", comm_rank(L.comm), M,
+            (int)streams_ok, ok ? "fused" : "plain", ((long long)ts.tv_sec * 1000 + ts.tv_nsec / 1000000) % 1000000);
+  }
+  return ok;
+}
+int site_of(bool down, int gi) { return (down ? NF_MAX_NANO : 0) + gi; }
+void set_peer_args(GemmArgs* a, const LayerCtx& L, int site, int M) {
+  const PeerGeom& g = comm_peer_geom(L.comm);
+  a->epi = EPI_PEER;
+  a->peer_bases = comm_peer_bases(L.comm);
+  a->peer_site_off = g.site(site);
+  a->peer_stage_off = g.stage_off;
+  a->peer_flags_off = g.flags_off;
+  a->peer_n = g.n;
+  a->peer_rank = g.rank;
+  a->peer_maxown = g.maxown;
+  a->peer_mb = (M + PEER_BM - 1) / PEER_BM;
+}
+const __nv_bfloat16* peer_result(const LayerCtx& L, int site) {
+  const PeerGeom& g = comm_peer_geom(L.comm);
+  return reinterpret_cast<const __nv_bfloat16*>(comm_sym_local(L.comm) + g.site(site) + g.result_off);
+}
+// Owner-side reduce + all-gather of a site on the network stream: ~2 CTAs per SM of the
+// plan's network budget (they are light: 128 threads, no shared memory)
+nf_status run_peer_reduce(const LayerCtx& L, int site, int M) {
+  comm_fused_site_barrier(L.comm);
+  // (an emulated group runs every rank's reduce on the same GPU: 2 CTAs each, so the ranks' spinning
+  // reduce CTAs never crowd out the GEMM CTAs they wait for)
+  const int ctas = comm_host_sync(L.comm) ? 2 : std::max(4, std::min(64, 2 * std::max(1, L.p->spec.sm[NF_OP_NET])));
+  ProfScope ps(NF_OP_NET, L.ns);
+  NF_CUDA(launch_peer_reduce(comm_peer_bases(L.comm), comm_peer_geom(L.comm), site, M, ctas,
+                             comm_peer_timeout_ns(L.comm), L.ns));
+  comm_count_fused(L.comm);
+  return NF_OK;
+}
+
 // Front of a group: KQV of each of its attention nano-batches, decode attention on
 // the memory stream as soon as that KQV lands, prefill attention on the compute stream.
 nf_status tp_front(nf_plan* p, const LayerCtx& L, int gi, const Group& G, const __nv_bfloat16* x, const float* part,
@@ -1257,6 +1313,7 @@ nf_status tp_stage_b(nf_plan* p, const LayerCtx& L, int gi, const Group& G, cons
     if (L.ns != L.cs) NF_CUDA(cudaEventRecord(p->ev_ago, L.ns));
   } else {
     NF_TRY(wait_attention(p, L, G, L.cs));
+    const bool fz = fused_site_ok(L, M);
     GemmArgs a{};
     a.epi = EPI_STORE;
     a.stages = stages;
@@ -1269,13 +1326,19 @@ nf_status tp_stage_b(nf_plan* p, const LayerCtx& L, int gi, const Group& G, cons
     a.n_valid = (int)D;
     a.out = h1;
     a.ldo = D;
+    if (fz) {  // reduce-scatter in the epilogue; the owner reduce runs on the network stream meanwhile
+      set_peer_args(&a, L, site_of(false, gi), M);
+      NF_TRY(edge(p->ev_o[gi], L.cs, L.ns));
+    }
     {
       ProfScope ps(NF_OP_O, L.cs);
       NF_CUDA(launch_gemm(L.w->o + G.nr.t0 * qd, qd, (const __nv_bfloat16*)wt->w_o_row, qd, a,
                           clamp_dense(L, L.p->spec.sm[NF_OP_O]), L.cs));
     }
-    NF_TRY(edge(p->ev_o[gi], L.cs, L.ns));
-    {
+    if (fz) {
+      NF_TRY(run_peer_reduce(L, site_of(false, gi), M));
+    } else {
+      NF_TRY(edge(p->ev_o[gi], L.cs, L.ns));
       ProfScope ps(NF_OP_NET, L.ns);
       NF_TRY(comm_all_reduce_bf16(L.comm, h1, (size_t)M * D, L.ns, L.w->red));
     }
@@ -1300,7 +1363,11 @@ nf_status tp_stage_c(nf_plan* p, const LayerCtx& L, int gi, const Group& G, cons
     NF_CUDA(launch_interleave(L.w->ag2, N, M, (int)Dl, h1, L.w->part_h1 + G.nr.t0, L.cs));
   } else {
     if (L.ns != L.cs) NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_aro[gi], 0));
-    NF_CUDA(launch_resid_add_rows(h1, x + G.nr.t0 * D, M, (int)D, L.w->part_h1 + G.nr.t0, L.cs));
+    if (fused_site_ok(L, M))
+      NF_CUDA(launch_resid_add_rows_from(h1, peer_result(L, site_of(false, gi)), x + G.nr.t0 * D, M, (int)D,
+                                         L.w->part_h1 + G.nr.t0, L.cs));
+    else
+      NF_CUDA(launch_resid_add_rows(h1, x + G.nr.t0 * D, M, (int)D, L.w->part_h1 + G.nr.t0, L.cs));
   }
   if (c->n_experts > 0) {
     // MoE: every expert's F columns are split across ranks; this rank's weighted partial sum
@@ -1339,14 +1406,20 @@ nf_status tp_stage_c(nf_plan* p, const LayerCtx& L, int gi, const Group& G, cons
     d.n_valid = (int)D;
     d.out = x_out + G.nr.t0 * D;
     d.ldo = D;
+    if (fused_site_ok(L, M)) {
+      set_peer_args(&d, L, site_of(true, gi), M);
+      NF_TRY(edge(p->ev_d[gi], L.cs, L.ns));
+    }
     {
       ProfScope ps(NF_OP_DOWN, L.cs);
       NF_CUDA(launch_gemm(L.w->m + G.nr.t0 * Fl, Fl, (const __nv_bfloat16*)wt->w_down, Fl, d,
                           clamp_dense(L, L.p->spec.sm[NF_OP_DOWN]), L.cs));
     }
   }
-  NF_TRY(edge(p->ev_d[gi], L.cs, L.ns));
-  {
+  if (c->n_experts == 0 && fused_site_ok(L, M)) {
+    NF_TRY(run_peer_reduce(L, site_of(true, gi), M));
+  } else {
+    NF_TRY(edge(p->ev_d[gi], L.cs, L.ns));
     ProfScope ps(NF_OP_NET, L.ns);
     NF_TRY(comm_all_reduce_bf16(L.comm, x_out + G.nr.t0 * D, (size_t)M * D, L.ns, L.w->red));
   }
@@ -1360,8 +1433,12 @@ nf_status tp_stage_d(nf_plan* p, const LayerCtx& L, int gi, const Group& G, __nv
   if (M <= 0) return NF_OK;
   const int64_t D = L.c->d_model;
   if (L.ns != L.cs) NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_ard[gi], 0));
-  NF_CUDA(launch_resid_add_rows(x_out + G.nr.t0 * D, L.w->h1 + G.nr.t0 * D, M, (int)D,
-                                part_out ? part_out + G.nr.t0 : nullptr, L.cs));
+  if (L.c->n_experts == 0 && fused_site_ok(L, M))
+    NF_CUDA(launch_resid_add_rows_from(x_out + G.nr.t0 * D, peer_result(L, site_of(true, gi)), L.w->h1 + G.nr.t0 * D,
+                                       M, (int)D, part_out ? part_out + G.nr.t0 : nullptr, L.cs));
+  else
+    NF_CUDA(launch_resid_add_rows(x_out + G.nr.t0 * D, L.w->h1 + G.nr.t0 * D, M, (int)D,
+                                  part_out ? part_out + G.nr.t0 : nullptr, L.cs));
   return NF_OK;
 }
 
@@ -1552,6 +1629,7 @@ nf_status model_step_launches(nf_plan* p, nf_comm* comm, const nf_model_weights*
                            c->page_size));
   }
   NF_TRY(enter_partitions(p, &L, cs));
+  comm_fused_step_barrier(comm);
   auto tap_of = [&](int l) -> void* { return taps ? taps[l + 1] : nullptr; };
   if (p->spec.mode != NF_OVERLAP) {
     int nparts = 1;
@@ -1827,6 +1905,7 @@ nf_status nf_layer_forward(const nf_plan* plan, nf_comm* comm, const nf_packed_l
   // RMS partials of x_in (one part per row)
   NF_CUDA(launch_gather_rows((const __nv_bfloat16*)x_in, nullptr, m.T, c->d_model, nullptr, wsp.part_a, cs));
   NF_TRY(enter_partitions(p, &L, cs));
+  comm_fused_step_barrier(comm);
   NF_TRY(run_layer(p, L, w, kv_pool, (const __nv_bfloat16*)x_in, wsp.part_a, 1, (__nv_bfloat16*)x_out, nullptr, nullptr));
   NF_TRY(leave_partitions(p, L, cs));
   if (L.ms != cs && L.ms == p->mem_stream) {
@@ -1913,6 +1992,7 @@ nf_status nf_plan_probe_partitions(nf_plan* p, nf_comm* comm, int32_t* smids_out
   L.ns = p->cfg.tp_size > 1 ? p->net_stream : cs;
   L.comm = comm;
   NF_TRY(enter_partitions(p, &L, cs));
+  comm_fused_step_barrier(comm);
   int* d = nullptr;
   NF_CUDA(cudaMalloc(&d, (size_t)3 * n_sm * sizeof(int)));  // (probe only; not on the forward path)
   NF_CUDA(cudaMemsetAsync(d, 0, (size_t)3 * n_sm * sizeof(int), cs));

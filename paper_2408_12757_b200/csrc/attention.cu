@@ -674,4 +674,7 @@ cudaError_t launch_prefill_attention(const CUtensorMap& m, const AttnArgs& a, co
   return cudaErrorInvalidValue;
 }
 
+// One kernel of this translation unit (preload_all_kernels: its module is loaded eagerly).
+const void* kernel_anchor_attention() { return reinterpret_cast<const void*>(build_dec_rows_kernel); }
+
 }  // namespace nf

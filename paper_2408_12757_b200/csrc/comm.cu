@@ -9,12 +9,15 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <condition_variable>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
 #include "host.h"
 #include "misc.cuh"
+#include "peer.cuh"
 
 namespace nf {
 // Single-process, single-GPU emulation of a TP group (tests / rank-local
@@ -31,7 +34,8 @@ struct LocalGroup {
   std::vector<const void*> src;
   std::vector<cudaStream_t> st;
   std::vector<cudaEvent_t> ev_ready, ev_done;
-  explicit LocalGroup(int n_) : n(n_), src(n_), st(n_), ev_ready(n_), ev_done(n_) {
+  std::vector<uint8_t*> sym;  // every rank's symmetric buffer (fused collectives)
+  explicit LocalGroup(int n_) : n(n_), src(n_), st(n_), ev_ready(n_), ev_done(n_), sym(n_, nullptr) {
     for (int i = 0; i < n; ++i) {
       cudaEventCreateWithFlags(&ev_ready[i], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming);
@@ -58,6 +62,15 @@ struct nf_comm {
   int ar_mode = NF_AR_F32;                 // emulated AllReduce arithmetic
   bool loopback = false;                   // nf_comm_create_loopback: one rank, local copies
   std::shared_ptr<nf::LocalGroup> group;  // emulated group (nf_comm_create_local)
+  // fused collectives (peer.cuh): this rank's symmetric buffer, every rank's mapping of theirs
+  uint8_t* sym = nullptr;
+  size_t sym_bytes = 0;
+  std::vector<uint8_t*> sym_peer;          // [tp_size] (own entry = sym); IPC-opened for NCCL groups
+  uint8_t** sym_peer_dev = nullptr;        // device copy of sym_peer
+  nf::PeerGeom* geom = nullptr;
+  bool fused = false;
+  long long fused_sites = 0;  // fused sites issued (host count)
+  long long timeout_ns = 20000000000LL;
 };
 
 namespace nf {
@@ -97,6 +110,27 @@ int comm_rank(const nf_comm* c) { return c ? c->tp_rank : 0; }
 bool comm_emulated(const nf_comm* c) { return c && (c->group || c->loopback); }
 bool comm_host_sync(const nf_comm* c) { return c && c->group; }
 int comm_max_ctas(const nf_comm* c) { return c ? c->max_ctas : 0; }
+bool comm_fused(const nf_comm* c) { return c && c->fused && c->sym_peer_dev && c->geom; }
+// Emulated group with the fused path: the rank threads meet before a step launches any
+// spin-waiting kernel, so that no rank is still in a host call that may wait for the device
+// to be idle (first pinned-staging allocation, allocator calls) while another rank's reduce
+// kernel spins on it.
+void comm_count_fused(nf_comm* c) { ++c->fused_sites; }
+// Emulated group: every rank has enqueued its producer GEMM of a site before any rank enqueues
+// that site's spin-waiting reduce.  (The ranks' streams share the GPU's hardware work queues;
+// a reduce queued ahead of another rank's producer in the same queue would wait for it
+// forever.  With one rank per GPU each rank enqueues its own GEMM before its reduce, which is
+// all that is needed.)
+void comm_fused_site_barrier(nf_comm* c) {
+  if (c && c->group && comm_fused(c)) c->group->barrier();
+}
+void comm_fused_step_barrier(nf_comm* c) {
+  if (c && c->group && comm_fused(c)) c->group->barrier();
+}
+const PeerGeom& comm_peer_geom(const nf_comm* c) { return *c->geom; }
+uint8_t* const* comm_peer_bases(const nf_comm* c) { return c->sym_peer_dev; }
+uint8_t* comm_sym_local(const nf_comm* c) { return c->sym; }
+long long comm_peer_timeout_ns(const nf_comm* c) { return c->timeout_ns; }
 
 // recv = [rank 0's send | rank 1's send | ...] (count bf16 elements each)
 nf_status comm_all_gather(nf_comm* c, const void* send, void* recv, size_t count_bf16, cudaStream_t st) {
@@ -231,8 +265,124 @@ nf_status nf_comm_create_loopback(int32_t tp_size, int32_t tp_rank, nf_comm** ou
   return NF_OK;
 }
 
+nf_status nf_comm_sym_bytes(const nf_model_cfg* cfg, int32_t max_tokens, size_t* bytes) {
+  if (!cfg || !bytes || max_tokens < 1) return set_error(NF_EINVAL, "NULL argument / max_tokens < 1");
+  if (cfg->d_model % PEER_BN) return set_error(NF_EINVAL, "d_model %d not a multiple of %d", cfg->d_model, PEER_BN);
+  const int n = std::max(1, (int)cfg->tp_size);
+  *bytes = (size_t)peer_geom(n, 0, max_tokens, cfg->d_model).total_bytes;
+  return NF_OK;
+}
+
+nf_status nf_comm_sym_alloc(nf_comm* c, const nf_model_cfg* cfg, int32_t max_tokens, void* ipc_handle_out_64) {
+  if (!c || !cfg) return set_error(NF_EINVAL, "NULL argument");
+  if (c->sym) return set_error(NF_EINVAL, "symmetric buffer already allocated");
+  if (cfg->tp_size != c->tp_size) return set_error(NF_EINVAL, "cfg tp_size %d != communicator %d", cfg->tp_size, c->tp_size);
+  size_t bytes = 0;
+  NF_TRY(nf_comm_sym_bytes(cfg, max_tokens, &bytes));
+  // a loopback rank has no peers: its fused sites run as a group of one (local staging and result)
+  const int n = c->loopback ? 1 : c->tp_size, rank = c->loopback ? 0 : c->tp_rank;
+  if (cudaMalloc(&c->sym, bytes) != cudaSuccess) {
+    c->sym = nullptr;
+    return set_error(NF_ECUDA, "cudaMalloc of %zu symmetric bytes failed", bytes);
+  }
+  // zeroed and complete before any rank's kernels run (they are on non-blocking streams, which
+  // do not order after this legacy-stream memset)
+  if (cudaMemset(c->sym, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    return set_error(NF_ECUDA, "cudaMemset symmetric buffer");
+  c->sym_bytes = bytes;
+  c->geom = new PeerGeom(peer_geom(n, rank, max_tokens, cfg->d_model));
+  if (ipc_handle_out_64) {
+    std::memset(ipc_handle_out_64, 0, 64);
+    if (!c->group && !c->loopback) {
+      cudaIpcMemHandle_t h;
+      if (cudaIpcGetMemHandle(&h, c->sym) != cudaSuccess) return set_error(NF_ECUDA, "cudaIpcGetMemHandle failed");
+      static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+      std::memcpy(ipc_handle_out_64, &h, 64);
+    }
+  }
+  if (c->group) {
+    std::lock_guard<std::mutex> lk(c->group->mu);
+    c->group->sym[c->tp_rank] = c->sym;
+  }
+  return NF_OK;
+}
+
+nf_status nf_comm_sym_open(nf_comm* c, const void* ipc_handles) {
+  if (!c || !c->sym) return set_error(NF_EINVAL, "communicator without a symmetric buffer (nf_comm_sym_alloc first)");
+  const int n = c->geom->n;
+  c->sym_peer.assign(n, nullptr);
+  if (c->loopback) {
+    c->sym_peer[0] = c->sym;
+  } else if (c->group) {
+    std::lock_guard<std::mutex> lk(c->group->mu);
+    for (int r = 0; r < n; ++r) {
+      if (!c->group->sym[r]) return set_error(NF_EINVAL, "rank %d of the emulated group has no symmetric buffer", r);
+      c->sym_peer[r] = c->group->sym[r];
+    }
+  } else {
+    if (!ipc_handles) return set_error(NF_EINVAL, "ipc_handles is NULL");
+    for (int r = 0; r < n; ++r) {
+      if (r == c->tp_rank) {
+        c->sym_peer[r] = c->sym;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, (const char*)ipc_handles + 64 * r, 64);
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+        return set_error(NF_ECUDA, "cudaIpcOpenMemHandle of rank %d: %s", r, cudaGetErrorString(cudaGetLastError()));
+      c->sym_peer[r] = (uint8_t*)p;
+    }
+  }
+  if (!c->sym_peer_dev && cudaMalloc(&c->sym_peer_dev, sizeof(uint8_t*) * n) != cudaSuccess)
+    return set_error(NF_ECUDA, "cudaMalloc peer table");
+  if (cudaMemcpy(c->sym_peer_dev, c->sym_peer.data(), sizeof(uint8_t*) * n, cudaMemcpyHostToDevice) != cudaSuccess)
+    return set_error(NF_ECUDA, "peer table upload");
+  if (preload_all_kernels() != cudaSuccess) return set_error(NF_ECUDA, "preloading the library's kernels failed");
+  const char* e = getenv("NF_PEER_TIMEOUT_MS");
+  if (e) c->timeout_ns = std::max(1LL, atoll(e)) * 1000000LL;
+  c->fused = true;
+  return NF_OK;
+}
+
+nf_status nf_comm_set_fused(nf_comm* c, int32_t on) {
+  if (!c) return set_error(NF_EINVAL, "NULL communicator");
+  if (on && !c->sym_peer_dev) return set_error(NF_EINVAL, "symmetric buffers not open (nf_comm_sym_open)");
+  c->fused = on != 0;
+  return NF_OK;
+}
+
+nf_status nf_comm_sym_status(nf_comm* c, int32_t* timeouts_out, int64_t* fused_sites_out) {
+  if (!c || !timeouts_out) return set_error(NF_EINVAL, "NULL argument");
+  *timeouts_out = 0;
+  if (fused_sites_out) *fused_sites_out = c->fused_sites;
+  if (!c->sym) return NF_OK;
+  uint32_t v[16 + 8 * 16] = {};
+  if (cudaMemcpy(v, c->sym, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return set_error(NF_ECUDA, "status read");
+  *timeouts_out = (int32_t)v[0];
+  if (getenv("NF_PEER_DEBUG")) {
+    fprintf(stderr, "[nf peer] rank %d: timeouts %u, longest flag wait %u us, longest done wait %u us\n", c->tp_rank,
+            v[0], v[8], v[9]);
+  }
+  if (v[0]) {  // the first timeout's record, for the caller's error report (nf_last_error)
+    set_error(NF_OK, "peer wait timeout: site %u %s block %u src %u observed %u target %u (%u timeouts)", v[16],
+              v[17] ? "done" : "flag", v[18] / 16, v[18] % 16, v[19], v[20], v[0]);
+  }
+  return NF_OK;
+}
+
 void nf_comm_destroy(nf_comm* c) {
   if (!c) return;
+  if (!c->group && !c->loopback)
+    for (int r = 0; r < (int)c->sym_peer.size(); ++r)
+      if (r != c->tp_rank && c->sym_peer[r]) cudaIpcCloseMemHandle(c->sym_peer[r]);
+  if (c->group && c->sym) {
+    std::lock_guard<std::mutex> lk(c->group->mu);
+    c->group->sym[c->tp_rank] = nullptr;
+  }
+  if (c->sym_peer_dev) cudaFree(c->sym_peer_dev);
+  if (c->sym) cudaFree(c->sym);
+  delete c->geom;
   if (!c->group && !c->loopback && c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
   delete c;
 }

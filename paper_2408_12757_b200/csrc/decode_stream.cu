@@ -271,4 +271,7 @@ cudaError_t launch_decode_attention_stream(const CUtensorMap& page_map, const At
   return launch_stream_hdw<64, 12>(page_map, a2, items, n_items, grid, st);
 }
 
+// One kernel of this translation unit (preload_all_kernels: its module is loaded eagerly).
+const void* kernel_anchor_decode_stream() { return reinterpret_cast<const void*>(decode_stream_kernel<128, 12>); }
+
 }  // namespace nf

@@ -340,4 +340,7 @@ cudaError_t launch_decode_attention_tc(const CUtensorMap& m, const AttnArgs& a, 
   return cudaGetLastError();
 }
 
+// One kernel of this translation unit (preload_all_kernels: its module is loaded eagerly).
+const void* kernel_anchor_decode_tc() { return reinterpret_cast<const void*>(decode_tc_kernel); }
+
 }  // namespace nf

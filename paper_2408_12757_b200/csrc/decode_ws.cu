@@ -304,4 +304,7 @@ cudaError_t launch_decode_attention_ws(const CUtensorMap& page_map, const AttnAr
   return cudaErrorInvalidValue;
 }
 
+// One kernel of this translation unit (preload_all_kernels: its module is loaded eagerly).
+const void* kernel_anchor_decode_ws() { return reinterpret_cast<const void*>(decode_ws_kernel<128, 12>); }
+
 }  // namespace nf

@@ -14,6 +14,7 @@ enum GemmEpiMode : int {
   EPI_QKV = 3,     // q/k RoPE at pos, q -> q_out, k/v -> paged KV pool slots
   EPI_ARGMAX = 4,  // per (n-tile,row) partial (max, argmax) of acc
   EPI_F32 = 5,     // outf = acc * row_scale (f32, for TP partial sums)
+  EPI_PEER = 6,    // bf16(acc * row_scale) partial 128x256 blocks into their owner ranks' staging (peer.cuh)
 };
 
 constexpr int GEMM_BM = 128;
@@ -72,6 +73,14 @@ struct GemmArgs {
   const int* grp_off;
   const int* grp_end;
   int n_groups;
+  // EPI_PEER (peer.cuh): block (bm, bn) of 128 rows x 256 columns belongs to
+  // rank (bm + bn * peer_mb) % peer_n; the partial goes to that rank's buffer at
+  // peer_site_off + peer_stage_off + [peer_rank][owned index][128][256], then the owner's flag
+  // at peer_site_off + peer_flags_off + 256 + 4 * (owned index * peer_n + peer_rank) is bumped by BN/64
+  // (release, sys scope)
+  uint8_t* const* peer_bases;  // device array [peer_n]: every rank's symmetric buffer
+  int64_t peer_site_off, peer_stage_off, peer_flags_off;
+  int peer_n, peer_rank, peer_maxown, peer_mb;
 };
 
 // Bytes of stream-K scratch for a GEMM with this many tiles at this grid.

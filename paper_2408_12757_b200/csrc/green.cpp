@@ -117,6 +117,13 @@ bool green_setup(nf_plan* p, int dec_sms, int net_sms) {
     p->green_note = "green context creation failed (network partition)";
     return false;
   }
+  // every kernel of the library loaded into the new contexts now (no lazy load later, while a
+  // spin-waiting kernel may run: see preload_kernels_green)
+  for (CUgreenCtx g : {g_mem, g_cmp, g_net})
+    if (g && preload_kernels_green((void*)g) != cudaSuccess) {
+      p->green_note = "kernel preload into a green context failed";
+      return false;
+    }
   unsigned sm_mem = 0, sm_net = 0, sm_cmp = 0;
   for (unsigned i = 0; i < n_mem; ++i) sm_mem += groups[i].sm.smCount;
   for (unsigned i = 0; i < n_net; ++i) sm_net += groups[n_mem + i].sm.smCount;

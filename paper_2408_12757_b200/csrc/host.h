@@ -102,6 +102,18 @@ bool comm_host_sync(const nf_comm* c);  // collectives meet at host barriers (no
 int comm_max_ctas(const nf_comm* c);
 nf_status comm_all_gather(nf_comm* c, const void* send, void* recv, size_t count_bf16, cudaStream_t st);
 nf_status comm_all_reduce_bf16(nf_comm* c, void* buf, size_t count, cudaStream_t st, void* scratch);
+// Fused GEMM -> AllReduce over peer memory (peer.cuh; NEXT-3): active once the communicator's
+// symmetric buffers are open (nf_comm_sym_open) and not switched off (nf_comm_set_fused).
+struct PeerGeom;
+bool comm_fused(const nf_comm* c);
+void comm_fused_step_barrier(nf_comm* c);
+void comm_count_fused(nf_comm* c);
+void comm_fused_site_barrier(nf_comm* c);
+cudaError_t preload_kernels_green(void* green_ctx);  // peer.cu: load the library's kernels into a green context  // one fused site issued (nf_comm_sym_status reports the count)
+const PeerGeom& comm_peer_geom(const nf_comm* c);
+uint8_t* const* comm_peer_bases(const nf_comm* c);  // device array [geom.n]
+uint8_t* comm_sym_local(const nf_comm* c);          // this rank's buffer
+long long comm_peer_timeout_ns(const nf_comm* c);
 }  // namespace nf
 
 // A captured nf_model_step (plan spec.graph): replayed while the launch structure

@@ -41,15 +41,19 @@ __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, const 
 
 // one warp per row, in place: acc[row] = bf16(resid[row] + acc[row]) in fp32, sumsq of the
 // rounded row -> part[row] (the residual add after a TP AllReduce of partial sums)
-__global__ void resid_add_rows_kernel(__nv_bfloat16* __restrict__ acc, const __nv_bfloat16* __restrict__ resid,
-                                      int rows, int D, float* __restrict__ part) {
+// acc = bf16(src + resid) row-wise (src == acc: in place); src rows at stride D.  CG: src was
+// written by other GPUs (fused AllReduce result region): read it through L2 (ld.global.cg).
+template <bool CG>
+__global__ void resid_add_rows_kernel(__nv_bfloat16* acc, const __nv_bfloat16* src_,
+                                      const __nv_bfloat16* __restrict__ resid, int rows, int D, float* __restrict__ part) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
   uint4* a = reinterpret_cast<uint4*>(acc + (int64_t)warp * D);
+  const uint4* sp = reinterpret_cast<const uint4*>(src_ + (int64_t)warp * D);
   const uint4* r = reinterpret_cast<const uint4*>(resid + (int64_t)warp * D);
   float sq = 0.f;
   for (int i = lane; i < D / 8; i += 32) {
-    uint4 u = a[i], v = r[i];
+    uint4 u = CG ? __ldcg(sp + i) : sp[i], v = r[i];
     uint32_t w[4] = {u.x, u.y, u.z, u.w};
     const uint32_t x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -244,7 +248,15 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* src, const int* idx, int row
 cudaError_t launch_resid_add_rows(__nv_bfloat16* acc, const __nv_bfloat16* resid, int rows, int D, float* part,
                                   cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
-  resid_add_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(acc, resid, rows, D, part);
+  resid_add_rows_kernel<false><<<(rows + 7) / 8, 256, 0, st>>>(acc, acc, resid, rows, D, part);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resid_add_rows_from(__nv_bfloat16* out, const __nv_bfloat16* src, const __nv_bfloat16* resid, int rows,
+                                       int D, float* part, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  resid_add_rows_kernel<true><<<(rows + 7) / 8, 256, 0, st>>>(out, src, resid, rows, D, part);
   count_launch();
   return cudaGetLastError();
 }
@@ -354,5 +366,8 @@ cudaError_t launch_pack_gate_up(const __nv_bfloat16* gate, const __nv_bfloat16* 
   count_launch();
   return cudaGetLastError();
 }
+
+// One kernel of this translation unit (preload_all_kernels: its module is loaded eagerly).
+const void* kernel_anchor_misc() { return reinterpret_cast<const void*>(fill_i32_kernel); }
 
 }  // namespace nf

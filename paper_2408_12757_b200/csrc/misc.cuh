@@ -8,6 +8,9 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* src, const int* idx, int row
                                float* part, cudaStream_t st);
 cudaError_t launch_resid_add_rows(__nv_bfloat16* acc, const __nv_bfloat16* resid, int rows, int D, float* part,
                                   cudaStream_t st);
+// out = bf16(src + resid) (src written by peers: read through L2), part = row sums of squares
+cudaError_t launch_resid_add_rows_from(__nv_bfloat16* out, const __nv_bfloat16* src, const __nv_bfloat16* resid, int rows,
+                                       int D, float* part, cudaStream_t st);
 cudaError_t launch_gather_ids_embed(const __nv_bfloat16* embed, const int* token_ids, const int* tok_src, int rows, int D,
                                     int vocab, __nv_bfloat16* dst, float* part, cudaStream_t st);
 cudaError_t launch_argmax_pairs(const float* val, const int* idx, int ntiles, int64_t stride, int rows, int idx_off,

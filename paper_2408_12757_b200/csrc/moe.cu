@@ -370,4 +370,7 @@ cudaError_t launch_pack_router(const __nv_bfloat16* w_router, const __nv_bfloat1
   return cudaGetLastError();
 }
 
+// One kernel of this translation unit (preload_all_kernels: its module is loaded eagerly).
+const void* kernel_anchor_moe() { return reinterpret_cast<const void*>(pack_router_kernel); }
+
 }  // namespace nf

@@ -418,4 +418,7 @@ cudaError_t launch_prefill_attention_tc(const CUtensorMap& m, const AttnArgs& a,
   return cudaGetLastError();
 }
 
+// One kernel of this translation unit (preload_all_kernels: its module is loaded eagerly).
+const void* kernel_anchor_prefill_tc() { return reinterpret_cast<const void*>(prefill_tc_kernel); }
+
 }  // namespace nf

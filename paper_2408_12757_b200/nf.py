@@ -100,6 +100,11 @@ _sig("nf_comm_destroy", None, C.c_void_p)
 _sig("nf_comm_create_local", C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_void_p))
 AR_F32, AR_RING = 0, 1
 _sig("nf_comm_create_loopback", C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_void_p))
+_sig("nf_comm_sym_bytes", C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_size_t))
+_sig("nf_comm_sym_alloc", C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p)
+_sig("nf_comm_sym_open", C.c_int, C.c_void_p, C.c_void_p)
+_sig("nf_comm_set_fused", C.c_int, C.c_void_p, C.c_int32)
+_sig("nf_comm_sym_status", C.c_int, C.c_void_p, P_i32, C.POINTER(C.c_int64))
 _sig("nf_packed_layer_bytes", C.c_int, C.POINTER(ModelCfg), C.POINTER(C.c_size_t))
 _sig("nf_pack_layer", C.c_int, C.POINTER(ModelCfg), C.POINTER(LayerWeights), C.POINTER(PackedLayer), C.c_void_p)
 _sig("nf_pack_lm_head", C.c_int, C.POINTER(ModelCfg), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
@@ -171,7 +176,8 @@ PROF_NAMES = ["kqv", "decode_attn", "prefill_attn", "o_proj", "up_gate", "down",
 
 EXPORTED = ["nf_plan_runtime_note", "nf_plan_probe_partitions", "nf_comm_create_local", "nf_gemm_workspace_bytes", "nf_profile_timeline", "nf_profile_tag", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
             "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_plan_hash", "nf_comm_unique_id",
-            "nf_comm_create", "nf_comm_destroy", "nf_comm_create_loopback", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
+            "nf_comm_create", "nf_comm_destroy", "nf_comm_create_loopback", "nf_comm_sym_bytes", "nf_comm_sym_alloc",
+            "nf_comm_sym_open", "nf_comm_set_fused", "nf_comm_sym_status", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
             "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_model_step_ex", "nf_gemm_bf16", "nf_attention",
             "nf_moe_rows_cap", "nf_moe_route_ws_bytes", "nf_moe_route", "nf_moe_last_ids", "nf_sched_create", "nf_sched_submit",
             "nf_sched_next", "nf_sched_complete", "nf_sched_get_stats", "nf_sched_destroy", "nf_assemble_tokens"]
@@ -457,6 +463,48 @@ def comm_create(tp_size: int, tp_rank: int, uid: bytes, max_ctas: int = 0) -> in
     buf = C.create_string_buffer(uid, 128)
     _check(lib.nf_comm_create(tp_size, tp_rank, buf, max_ctas, C.byref(h)))
     return h.value
+
+
+def comm_sym_bytes(cfg, max_tokens: int) -> int:
+    """Bytes of one rank's symmetric buffer for the fused GEMM->AllReduce (NEXT-3)."""
+    n = C.c_size_t()
+    _check(lib.nf_comm_sym_bytes(C.byref(cfg), max_tokens, C.byref(n)))
+    return n.value
+
+
+def comm_sym_alloc(h: int, cfg, max_tokens: int) -> bytes:
+    """Allocate this rank's symmetric buffer; returns its 64-byte CUDA IPC handle (zeros when emulated)."""
+    buf = C.create_string_buffer(64)
+    _check(lib.nf_comm_sym_alloc(C.c_void_p(h), C.byref(cfg), max_tokens, buf))
+    return buf.raw
+
+
+def comm_sym_open(h: int, handles: Optional[Sequence[bytes]] = None):
+    """Map the group's buffers (handles: every rank's 64-byte IPC handle in rank order; None when
+    emulated / loopback) and switch the fused GEMM->AllReduce on."""
+    buf = C.create_string_buffer(b"".join(handles), 64 * len(handles)) if handles else None
+    _check(lib.nf_comm_sym_open(C.c_void_p(h), buf))
+
+
+def comm_set_fused(h: int, on: bool):
+    _check(lib.nf_comm_set_fused(C.c_void_p(h), 1 if on else 0))
+
+
+def comm_sym_status(h: int, with_sites: bool = False):
+    """Number of bounded peer waits that timed out (0 = healthy); with_sites: (timeouts, fused
+    sites this rank issued)."""
+    v = C.c_int32()
+    n = C.c_int64()
+    _check(lib.nf_comm_sym_status(C.c_void_p(h), C.byref(v), C.byref(n)))
+    return (v.value, n.value) if with_sites else v.value
+
+
+def comm_enable_fused_local(comms: Sequence[int], cfgs, max_tokens: int):
+    """Emulated group: allocate every rank's buffer, then open them (one thread)."""
+    for h, c in zip(comms, cfgs):
+        comm_sym_alloc(h, c, max_tokens)
+    for h in comms:
+        comm_sym_open(h, None)
 
 
 class Scheduler:

@@ -115,6 +115,40 @@ for name, graph in [("eager", False), ("graph", True)]:
                       "ranks_identical": gather_eq(torch.from_numpy(runs[0])), "n_sure": int(sure.sum()),
                       "graph_note": plan.runtime_note()}
 res["step"] = step_res
+
+# ---- fused GEMM -> AllReduce over CUDA IPC peer memory (NEXT-3): the symmetric buffers are
+# exchanged as IPC handles through the process group and mapped into every rank
+fz = {}
+try:
+    h = nf.comm_sym_alloc(comm, cfg, b.n_tokens)
+    hs = [None] * world
+    dist.all_gather_object(hs, h)
+    nf.comm_sym_open(comm, hs)
+    log("symmetric buffers open")
+    for name, mode, shares, nd in [("sequential", nf.SEQUENTIAL, (1,), 0), ("overlap42", nf.OVERLAP, (1, 1, 1, 1), 2)]:
+        plan = nf.Plan.explicit(cfg, mode, shares=shares, sm=[116, 16, 116, 116, 116, 116, 16], n_dense=nd)
+        y = rt.layer_forward(plan, cfg, packed, rt.shard_pool(dev(pool), world, rank), nb, dev(x), ws=ws, comm=comm)
+        torch.cuda.synchronize()
+        log(f"fused layer {name} done")
+        out = y.float().cpu().numpy().astype(np.float64)
+        err = out - ref
+        fz[name] = {"rel_l2": float(np.linalg.norm(err) / np.linalg.norm(ref)), "max_abs": float(np.abs(err).max()),
+                    "ranks_identical": gather_eq(y)}
+    plan = nf.Plan.explicit(cfg, nf.OVERLAP, shares=(1, 1, 1, 1), sm=[116, 16, 116, 116, 116, 116, 16], n_dense=2,
+                            balance=2, graph=True)
+    runs = []
+    for it in range(3):
+        ids = model.step(plan, [rt.shard_pool(dev(p), world, rank) for p in pools], nb, tok_d, ws, comm=comm)
+        torch.cuda.synchronize()
+        runs.append(ids.cpu().numpy())
+    log("fused graph steps done")
+    fz["graph"] = {"argmax_ok": bool(np.array_equal(runs[0][sure], ids_ref[sure])),
+                   "replays_identical": bool(all(np.array_equal(runs[0], r) for r in runs)),
+                   "ranks_identical": gather_eq(torch.from_numpy(runs[0]))}
+    fz["timeouts"] = nf.comm_sym_status(comm)
+except Exception as e:  # noqa: BLE001  (reported to the test, which decides)
+    fz["error"] = f"{type(e).__name__}: {e}"
+res["fused"] = fz
 json.dump(res, open(out_path, "w"))
 log("results written")
 dist.barrier()

@@ -85,3 +85,12 @@ def test_nccl_tp_group_on_one_gpu(tmp_path, world, mps):
             assert v["rel_l2"] <= 1e-2 and v["max_abs"] <= 5e-2, (r["rank"], name, v)
         for name, v in r["step"].items():
             assert v["argmax_ok"] and v["replays_identical"] and v["ranks_identical"], (r["rank"], name, v)
+        # fused GEMM -> AllReduce through CUDA IPC peer mappings (NEXT-3)
+        fz = r["fused"]
+        assert "error" not in fz, (r["rank"], fz)
+        assert fz["timeouts"] == 0, (r["rank"], fz)
+        for name in ("sequential", "overlap42"):
+            v = fz[name]
+            assert v["ranks_identical"] and v["rel_l2"] <= 1e-2 and v["max_abs"] <= 5e-2, (r["rank"], name, v)
+        g = fz["graph"]
+        assert g["argmax_ok"] and g["replays_identical"] and g["ranks_identical"], (r["rank"], g)

@@ -10,6 +10,7 @@ bit-identical hidden states (T16); the 70B-shape layer at the full configs[2]
 batch on sampled requests; the TP model step (vocab-parallel LM head + AllGather
 of (max, idx)) against the oracle per layer (teacher-forced) and on logits; and
 that the network spans of the pipeline overlap the compute spans of the same rank."""
+import gc
 import threading
 
 import numpy as np
@@ -27,9 +28,15 @@ SMALL = synth.shape_with(synth.SHAPES["c1"], name="tp-small", n_q_heads=16, n_kv
                          vocab=4096)
 
 
-def run_ranks(nf, tp, fn, ar_mode=None):
-    """fn(rank, comm, stream) on tp host threads of one emulated group; returns the results."""
+def run_ranks(nf, tp, fn, ar_mode=None, fused=None):
+    """fn(rank, comm, stream) on tp host threads of one emulated group; returns the results.
+    fused = (rt, shape, max_tokens): the group's symmetric buffers are opened first, so the
+    row-parallel GEMMs run the fused peer AllReduce (NEXT-3) instead of the emulated one."""
     comms = nf.comm_create_local(tp, nf.AR_RING if ar_mode is None else ar_mode)
+    if fused is not None:
+        rt_, shape_, max_tokens = fused
+        nf.comm_enable_fused_local(comms, [rt_.cfg_from_shape(shape_, tp_size=tp, tp_rank=r) for r in range(tp)],
+                                   max_tokens)
     outs = [None] * tp
     errs = []
 
@@ -43,18 +50,37 @@ def run_ranks(nf, tp, fn, ar_mode=None):
         except Exception as e:  # noqa: BLE001
             errs.append((r, e))
 
+    # No rank thread may run an implicitly device-synchronising call (a garbage-collected plan's
+    # stream / green-context / pinned-buffer teardown) while another rank's spin-waiting reduce
+    # kernel waits for its kernels: on one GPU that blocks until the wait times out.  Collect
+    # first and keep the collector off while the ranks run.
+    gc.collect()
+    torch.cuda.synchronize()
+    gc.disable()
     th = [threading.Thread(target=main, args=(r,)) for r in range(tp)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join(timeout=600)
+    try:
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=600)
+    finally:
+        gc.enable()
+    timeouts, sites = [], []
+    if fused is not None:
+        for c in comms:
+            n, k = nf.comm_sym_status(c, with_sites=True)
+            timeouts.append((n, nf.last_error()) if n else 0)
+            sites.append(k)
     for c in comms:
         nf.comm_destroy(c)
     assert not errs, errs
+    assert not any(timeouts), f"fused AllReduce waits timed out: {timeouts}"
+    if fused is not None:
+        assert all(k > 0 for k in sites), f"fused path not taken on every rank: {sites}"
     return outs
 
 
-def _tp_layer(nf, rt, shape, b, wd, x_d, pool_d, tp, mode, shares, n_dense=0, ar_mode=None, sm=None):
+def _tp_layer(nf, rt, shape, b, wd, x_d, pool_d, tp, mode, shares, n_dense=0, ar_mode=None, sm=None, fused=False):
     def fn(r, comm, st):
         cfg = rt.cfg_from_shape(shape, tp_size=tp, tp_rank=r)
         shard = rt.shard_layer(wd, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, tp, r)
@@ -69,7 +95,7 @@ def _tp_layer(nf, rt, shape, b, wd, x_d, pool_d, tp, mode, shares, n_dense=0, ar
                          ws.data_ptr(), ws.numel(), int(st.cuda_stream), comm=comm)
         return y
 
-    return run_ranks(nf, tp, fn, ar_mode)
+    return run_ranks(nf, tp, fn, ar_mode, fused=(rt, shape, b.n_tokens) if fused else None)
 
 
 # (tp, mode, shares, n_dense, ar_mode): SEQUENTIAL / NANO_ONLY / OVERLAP 2-way, and the paper's
@@ -93,6 +119,36 @@ def test_tp_layer_matches_unsharded_oracle(tp, mode, shares, n_dense, ar_mode):
     for r in range(1, tp):
         assert torch.equal(outs[0], outs[r]), f"rank {r} differs from rank 0 (T16)"
     assert_close(host(outs[0]), ref, what=f"TP{tp} mode={mode} shares={shares} n_dense={n_dense} ar={ar_mode}")
+
+
+# fused GEMM -> AllReduce over peer memory (NEXT-3): SEQUENTIAL, NANO_ONLY and the 4/2 OVERLAP pipeline
+FUSED_CASES = [(2, 0, (1,), 0), (4, 0, (1,), 0), (2, 2, (1, 1, 1, 1), 2), (4, 2, (1, 1, 1, 1), 2),
+               (8, 2, (1, 1, 1, 1), 2), (4, 2, (1, 1), 0)]
+
+
+@pytest.mark.parametrize("tp,mode,shares,n_dense", FUSED_CASES)
+def test_tp_fused_allreduce_bit_identical(tp, mode, shares, n_dense):
+    """The fused path (EPI_PEER epilogue pushing 128x256 partial blocks to their owners, owner
+    reduce in rank order in fp32, push of the block to every rank) computes exactly the
+    NF_AR_F32 arithmetic: outputs bit-identical to the emulated fp32 AllReduce, identical on
+    every rank, within the north_star tolerance of the unsharded oracle; no bounded wait
+    timed out.  The batch has a ragged last 128-row block per dense nano-batch."""
+    nf, rt = require_gpu()
+    shape = SMALL
+    b = synth.make_batch([1] * 150 + [37, 1, 16, 1, 70], list(range(5, 1505, 10)) + [0, 130, 33, 3, 20], seed=4,
+                         pool_slack=3)
+    w = synth.layer_weights(shape, 0)
+    x = synth.activations(shape, b.n_tokens)
+    pool = synth.kv_pool(shape, b)
+    ref = OL.decoder_layer(x, w, OL.as_pool(pool), b, shape)
+    wd, xd, pd = device_weights(w), dev(x), dev(pool)
+    sm = [148, 148, 148, 148, 148, 148, 16]  # OVERLAP: the reduce runs in a 16-SM network partition
+    plain = _tp_layer(nf, rt, shape, b, wd, xd, pd.clone(), tp, mode, shares, n_dense, nf.AR_F32, sm=sm)
+    fused = _tp_layer(nf, rt, shape, b, wd, xd, pd.clone(), tp, mode, shares, n_dense, nf.AR_F32, sm=sm, fused=True)
+    for r in range(tp):
+        assert torch.equal(fused[r], fused[0]), f"rank {r} differs from rank 0 (T16)"
+        assert torch.equal(fused[r], plain[r]), f"rank {r}: fused AllReduce != emulated fp32 AllReduce"
+    assert_close(host(fused[0]), ref, what=f"fused TP{tp} mode={mode} n_dense={n_dense}")
 
 
 def test_tp2_8b_shape():
@@ -128,7 +184,8 @@ def _full_70b_case(b_dense):
     return _FULL[b_dense]
 
 
-@pytest.mark.parametrize("tp,b_dense,ar_mode", [(2, 768, 1), (4, 2048, 1), (8, 2048, 1), (8, 2048, 0)])
+@pytest.mark.parametrize("tp,b_dense,ar_mode", [(2, 768, 1), (4, 2048, 1), (8, 2048, 1), (8, 2048, 0), (8, 2048, "fused"),
+                                               (2, 768, "fused")])
 def test_tp_70b_full_batch_sampled(tp, b_dense, ar_mode):
     """T15 at the metric's configuration: one LLaMA-2-70B-shape layer at TP 2 / 4 / 8 over
     the full B_dense batch (768 at TP2) in the bench's launch configuration
@@ -150,8 +207,9 @@ def test_tp_70b_full_batch_sampled(tp, b_dense, ar_mode):
         src = torch.as_tensor(b.page_ids[b.page_indptr[r]:b.page_indptr[r + 1]].astype(np.int64), device="cuda")
         dst = sub.page_ids[sub.page_indptr[i]:sub.page_indptr[i + 1]]
         pool[dst] = pool_d[src[:len(dst)]].float().cpu().numpy()
-    outs = _tp_layer(nf, rt, shape, b, device_weights(w), dev(x), pool_d, tp, 2, (1, 1, 1, 1), 2, ar_mode,
-                     sm=[116, 16, 116, 116, 116, 116, 16])
+    fused = ar_mode == "fused"
+    outs = _tp_layer(nf, rt, shape, b, device_weights(w), dev(x), pool_d, tp, 2, (1, 1, 1, 1), 2,
+                     nf.AR_F32 if fused else ar_mode, sm=[116, 16, 116, 116, 116, 116, 16], fused=fused)
     for r in range(1, tp):
         assert torch.equal(outs[0], outs[r]), f"rank {r} differs (T16)"
     out = host(outs[0])
