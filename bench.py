@@ -360,6 +360,17 @@ def run_nf(args, rank, world, local_rank):
         uid = [nf.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = nf.comm_create(tp, rank, uid[0], max_ctas=plan.spec().sm[nf.OP_NET])
+    fused_note = None
+    if comm is not None and args.fused_ar:
+        # NEXT-3: row-parallel GEMM -> AllReduce over peer memory (CUDA IPC handles exchanged
+        # through the process group; a loopback rank runs its sites as a group of one)
+        h = nf.comm_sym_alloc(comm, cfg, T)
+        hs = [h]
+        if not loop:
+            hs = [None] * world
+            dist.all_gather_object(hs, h)
+        nf.comm_sym_open(comm, None if loop else hs)
+        fused_note = "fused GEMM->AllReduce over peer memory (EPI_PEER + owner reduce), NCCL for the AllGathers"
 
     # ---------------- weights: replicated tensors (embedding, norms) and layer 0 (in-run parity)
     # from a generator seeded identically on every rank; every other layer's shards from a
@@ -706,6 +717,10 @@ def run_nf(args, rank, world, local_rank):
                  "source": {"explicit": "measured default", "auto": "nf_plan_create",
                             "refine": "nf_plan_create + measured refinement"}[args.plan],
                  "refinement": refine_log, "hash": f"{plan.hash():016x}", "partitions": plan.runtime_note()}
+    if fused_note:
+        timeouts, n_sites = nf.comm_sym_status(comm, with_sites=True)
+        plan_line["collectives"] = {"allreduce": fused_note, "fused_sites_issued": n_sites,
+                                    "peer_wait_timeouts": timeouts}
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if tp > 1 else "weak",
@@ -780,6 +795,8 @@ def main():
                          "70B TP=N over NCCL (the metric's config); c3rank: 1-GPU proxy of one TP8 rank; "
                          "c4: configs[3] Mixtral-8x7B TP=N; c4rank: its 1-GPU TP8-rank proxy")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
+    ap.add_argument("--fused-ar", action="store_true",
+                    help="TP: fuse the row-parallel GEMMs with their AllReduce over peer memory (NEXT-3)")
     ap.add_argument("--no-parity", action="store_true", help="skip the in-run oracle parity check")
     ap.add_argument("--cpu-tokens", type=int, default=2048, help="tokens of the cpu_baseline oracle layer")
     ap.add_argument("--layers", type=int, default=0, help="(dev only) override layer count")

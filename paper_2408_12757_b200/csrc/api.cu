@@ -1221,7 +1221,10 @@ nf_status run_peer_reduce(const LayerCtx& L, int site, int M) {
   comm_fused_site_barrier(L.comm);
   // (an emulated group runs every rank's reduce on the same GPU: 2 CTAs each, so the ranks' spinning
   // reduce CTAs never crowd out the GEMM CTAs they wait for)
-  const int ctas = comm_host_sync(L.comm) ? 2 : std::max(4, std::min(64, 2 * std::max(1, L.p->spec.sm[NF_OP_NET])));
+  // (SEQUENTIAL / NANO_ONLY: the reduce follows the GEMM on the compute stream and has the GPU)
+  const int ctas = comm_host_sync(L.comm) ? 2
+                   : L.ns == L.cs       ? 2 * num_sms()
+                                        : std::max(4, std::min(64, 4 * std::max(1, L.p->green_net_sms)));
   ProfScope ps(NF_OP_NET, L.ns);
   NF_CUDA(launch_peer_reduce(comm_peer_bases(L.comm), comm_peer_geom(L.comm), site, M, ctas,
                              comm_peer_timeout_ns(L.comm), L.ns));

@@ -73,12 +73,13 @@ NF_DEV bool wait_geq(const uint32_t* p, uint32_t target, uint32_t* err, long lon
   return true;
 }
 
-// 128 threads and <= 51 registers (6 K registers, no shared memory): a reduce CTA spinning on an
-// SM must leave room for a whole GEMM CTA (256 threads x <= 224 registers = 57 K of the 64 K
-// register file), since the persistent GEMMs whose partials it waits for need all their CTAs
-// resident (split-K / stream-K lockstep).
+// 128 threads and <= 64 registers (8 K registers, no shared memory): a reduce CTA spinning on an
+// SM leaves room for a whole GEMM CTA (256 threads x <= 224 registers = 57 K of the 64 K
+// register file) -- the fused path only runs where the reduce cannot hold SMs a producer needs
+// (fused_site_ok in api.cu), this keeps even a co-resident reduce harmless.
 constexpr int PR_THREADS = 128;
-__global__ void __launch_bounds__(PR_THREADS, 10) peer_reduce_kernel(uint8_t* const* __restrict__ bases, PeerGeom g, int site,
+constexpr int PR_U = 4;  // 16-byte chunks per thread per pass (memory-level parallelism)
+__global__ void __launch_bounds__(PR_THREADS, 8) peer_reduce_kernel(uint8_t* const* __restrict__ bases, PeerGeom g, int site,
                                                           int M, long long timeout_ns) {
   const int P = g.n, me = g.rank;
   const int MB = (M + PEER_BM - 1) / PEER_BM, NB = g.cols / PEER_BN, nblk = MB * NB;
@@ -101,29 +102,47 @@ __global__ void __launch_bounds__(PR_THREADS, 10) peer_reduce_kernel(uint8_t* co
     }
     __syncthreads();
     // 128 rows x 32 chunks of 8 bf16: consecutive threads take consecutive 16 B of a row
-    for (int i = threadIdx.x; i < PEER_BM * (PEER_BN / 8); i += blockDim.x) {
-      const int row = i >> 5, ch = i & 31;
-      if (row >= rows) break;
-      float acc[8];
+    // 128 rows x 32 chunks of 8 bf16; each thread takes PR_U chunks per pass (consecutive threads
+    // -> consecutive 16 B of a row), all PR_U loads of a source issued before their adds
+    uint8_t* const* bp = bases;
+    const int64_t rbase = g.site(site) + g.result_off;
+    for (int i0 = threadIdx.x; i0 < PEER_BM * (PEER_BN / 8); i0 += PR_U * blockDim.x) {
+      float acc[PR_U][8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+      for (int u = 0; u < PR_U; ++u)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
+#pragma unroll 2
       for (int src = 0; src < P; ++src) {  // rank order: the emulated NF_AR_F32 arithmetic
-        const uint4 u = ld_cg_u4(stage + (((int64_t)src * g.maxown + lb) * PEER_BM + row) * PEER_BN + ch * 8);
-        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        const __nv_bfloat16* sp = stage + ((int64_t)src * g.maxown + lb) * PEER_BM * PEER_BN;
+        uint4 w[PR_U];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float2 f = unpack_bf16x2(w[k]);
-          acc[2 * k] += f.x;
-          acc[2 * k + 1] += f.y;
+        for (int u = 0; u < PR_U; ++u) {
+          const int i = i0 + u * blockDim.x, row = i >> 5, ch = i & 31;
+          w[u] = row < rows ? ld_cg_u4(sp + row * PEER_BN + ch * 8) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < PR_U; ++u) {
+          const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = unpack_bf16x2(ww[k]);
+            acc[u][2 * k] += f.x;
+            acc[u][2 * k + 1] += f.y;
+          }
         }
       }
-      const uint4 o = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
-                                 pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
-      const int64_t off = g.site(site) + g.result_off +
-                          (((int64_t)(bm * PEER_BM + row)) * g.cols + bn * PEER_BN + ch * 8) * 2;
-      for (int q = 0; q < P; ++q) {  // all-gather: start with the next rank so the links are spread
-        const int p = (me + 1 + q) % P;
-        *reinterpret_cast<uint4*>(bases[p] + off) = o;
+#pragma unroll
+      for (int u = 0; u < PR_U; ++u) {
+        const int i = i0 + u * blockDim.x, row = i >> 5, ch = i & 31;
+        if (row >= rows) continue;
+        const uint4 o = make_uint4(pack_bf16x2(acc[u][0], acc[u][1]), pack_bf16x2(acc[u][2], acc[u][3]),
+                                   pack_bf16x2(acc[u][4], acc[u][5]), pack_bf16x2(acc[u][6], acc[u][7]));
+        const int64_t off = rbase + (((int64_t)(bm * PEER_BM + row)) * g.cols + bn * PEER_BN + ch * 8) * 2;
+        for (int q = 0; q < P; ++q) {  // all-gather: start with the next rank so the links are spread
+          const int p = (me + 1 + q) % P;
+          *reinterpret_cast<uint4*>(bp[p] + off) = o;
+        }
       }
     }
     fence_sys();
