@@ -902,15 +902,17 @@ nf_status run_decode(const LayerCtx& L, const NanoRange& nr, cudaStream_t st, in
   } else if (use_ws_decode(L.p)) {
     NF_CUDA(launch_decode_attention_ws(L.page_map, a, dec, n, sms, st));
   } else if (part != 2 && decode_impl_env() == 0 && a.dec_warps != 4 && L.w->dec_rows && decode_stream_supported(a) &&
-             decode_grid(n, sms, 12) * 12 <= 2048) {
-    // stream kernel: row streams of this nano-batch's 12-warp launch geometry, written once per
-    // step (every layer of a step has the same items, pages and grid)
+             decode_grid(n, sms, a.hd == 128 ? decode_stream_warps() : 12) * (a.hd == 128 ? decode_stream_warps() : 12) <=
+                 2048) {
+    // stream kernel: row streams of this nano-batch's launch geometry, written once per step
+    // (every layer of a step has the same items, pages and grid)
+    const int W = a.hd == 128 ? decode_stream_warps() : 12;
     const int k = (int)(&nr - &L.m->nanos[0]);
-    const int grid = decode_grid(n, sms, 12);
+    const int grid = decode_grid(n, sms, W);
     int* rows = L.w->dec_rows + nr.dec_rows_off;
     int* wst = L.w->dec_wstart + k * 2049;
     if (k < 0 || k >= NF_MAX_NANO || !L.rows_built[k]) {
-      NF_CUDA(launch_build_dec_rows(dec, n, grid, 12, a.page_ids, a.kh, rows, wst, st));
+      NF_CUDA(launch_build_dec_rows(dec, n, grid, W, a.page_ids, a.kh, rows, wst, st));
       if (k >= 0 && k < NF_MAX_NANO) L.rows_built[k] = true;
     }
     a.dec_rows = rows;

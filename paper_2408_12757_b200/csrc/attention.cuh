@@ -52,6 +52,7 @@ cudaError_t launch_decode_attention(const CUtensorMap& pool_map, const CUtensorM
 // stream decode attention (decode_stream.cu; needs a.dec_rows / a.dec_wstart built for a
 // 12-warp geometry by launch_build_dec_rows): head_dim 64/128, page 16, GQA group <= 8
 bool decode_stream_supported(const AttnArgs& a);
+int decode_stream_warps();  // consumer warps per CTA of the stream kernel (row-stream geometry)
 cudaError_t launch_decode_attention_stream(const CUtensorMap& page_map, const AttnArgs& a, const DecodeItem* items,
                                            int n_items, int sm_budget, cudaStream_t stream);
 // warp-specialised decode attention (one producer warp drives every consumer warp's TMA ring); decode_ws.cu

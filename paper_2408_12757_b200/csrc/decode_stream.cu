@@ -94,12 +94,6 @@ __global__ void __launch_bounds__(W * 32, 1)
   for (int j = 0; j < NS; ++j)
     if (j < n_pg) issue((uint32_t)j, ld_uniform(rows + j));
   int nrow = NS < n_pg ? ld_uniform(rows + NS) : 0;  // row of the next page to issue (loaded one page early)
-  // optional L2 prefetch PF pages beyond the ring (a.pf_dist; bytes in flight beyond shared memory)
-  const int PF = a.pf_dist;
-  if (PF > 0 && lane == 0)
-    for (int q = NS; q < NS + PF && q < n_pg; ++q) tma_prefetch_4d(&pages, 0, ld_uniform(rows + q), 0, 0);
-  int prow = (PF > 0 && NS + PF < n_pg) ? ld_uniform(rows + NS + PF) : 0;
-
   // ldmatrix lane offsets inside a stage (128B swizzle: 16-byte chunk c of row r at r*128 + ((c ^ (r&7)) << 4));
   // for k-step ks the chunk is 2*(ks&3) + hi in box ks>>2, so four offsets serve all k-steps
   const int x7 = lane & 7;
@@ -163,10 +157,6 @@ __global__ void __launch_bounds__(W * 32, 1)
       if ((int)j + NS < n_pg) {  // refill the slot with the page NS ahead
         issue(j + NS, nrow);
         if ((int)j + NS + 1 < n_pg) nrow = ld_uniform(rows + j + NS + 1);
-        if (PF > 0 && (int)j + NS + PF < n_pg) {
-          if (lane == 0) tma_prefetch_4d(&pages, 0, prow, 0, 0);
-          if ((int)j + NS + PF + 1 < n_pg) prow = ld_uniform(rows + j + NS + PF + 1);
-        }
       }
       float sc[4];
 #pragma unroll
@@ -251,6 +241,18 @@ cudaError_t launch_stream_hdw(const CUtensorMap& pm, const AttnArgs& a, const De
 
 }  // namespace
 
+// Consumer warps per CTA (each with a 2 x 8 KB ring at head_dim 128): 12 by default;
+// NF_DEC_STREAM_WARPS=13 / 14 fill up to 225 KB of shared memory (A/B runs).
+int decode_stream_warps() {
+  static int w = -1;
+  if (w < 0) {
+    const char* e = getenv("NF_DEC_STREAM_WARPS");
+    w = e ? atoi(e) : 12;
+    if (w != 13 && w != 14) w = 12;
+  }
+  return w;
+}
+
 bool decode_stream_supported(const AttnArgs& a) {
   return (a.hd == 128 || a.hd == 64) && a.page_size == 16 && a.kh > 0 && a.qh % a.kh == 0 && a.qh / a.kh <= 8;
 }
@@ -259,15 +261,16 @@ cudaError_t launch_decode_attention_stream(const CUtensorMap& page_map, const At
                                            int n_items, int sm_budget, cudaStream_t st) {
   if (n_items <= 0) return cudaSuccess;
   if (!a.dec_rows || !a.dec_wstart || !decode_stream_supported(a)) return cudaErrorInvalidValue;
-  static int pf_env = -1;  // NF_DEC_PF: L2 prefetch distance in pages (0 = off)
-  if (pf_env < 0) {
-    const char* e = getenv("NF_DEC_PF");
-    pf_env = e ? std::max(0, std::min(atoi(e), 32)) : 0;
+  // (an L2 prefetch of pages ahead of the ring, TMA or LSU, measured slower in every
+  // configuration: profiles/r2f_decode_stream_l2_prefetch_ab.log, r2f_tma_probe_lsu.log)
+  const AttnArgs& a2 = a;
+  const int W = decode_stream_warps();
+  const int grid = decode_grid(n_items, sm_budget, W);
+  if (a.hd == 128) {
+    if (W == 13) return launch_stream_hdw<128, 13>(page_map, a2, items, n_items, grid, st);
+    if (W == 14) return launch_stream_hdw<128, 14>(page_map, a2, items, n_items, grid, st);
+    return launch_stream_hdw<128, 12>(page_map, a2, items, n_items, grid, st);
   }
-  AttnArgs a2 = a;
-  a2.pf_dist = pf_env;
-  const int grid = decode_grid(n_items, sm_budget, 12);
-  if (a.hd == 128) return launch_stream_hdw<128, 12>(page_map, a2, items, n_items, grid, st);
   return launch_stream_hdw<64, 12>(page_map, a2, items, n_items, grid, st);
 }
 

@@ -1,4 +1,6 @@
-for f in "" "--fused-ar" "" "--fused-ar"; do timeout 900 python bench.py --config c3loop --no-cpu-baseline --no-ablation --steps 10 $f 2>&1 | tail -1 | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print('[$f]', round(d['ms_per_step'],2), round(d['value']), d['clocks']['sm_mhz'], (d['plan'].get('collectives') or {}).get('peer_wait_timeouts'), round(d['per_op']['net']['ms_per_step'],2))"; done > gpurun_out/r2g_c3loop_fused_ab2.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_tp.py -x -q -k "fused" 2>&1 | tail -1 >> gpurun_out/r2g_c3loop_fused_ab2.log
-cat gpurun_out/r2g_c3loop_fused_ab2.log
+timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/r2h_gputest.log 2>&1; tail -3 gpurun_out/r2h_gputest.log
+timeout 600 python bench.py > gpurun_out/r2h_bench_default.log 2>&1; tail -c 400 gpurun_out/r2h_bench_default.log
+NF_GREEN=0 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2h_launches.csv python bench.py --steps 1 --warmup 3 --ncu > gpurun_out/r2h_ncu_launches.out 2>&1
+NF_GREEN=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_stream -s 8 -c 1 -o gpurun_out/r2h_dec_step python bench.py --steps 1 --warmup 3 --ncu > gpurun_out/r2h_ncu_step.out 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:decode_stream -c 1 -o gpurun_out/r2h_dec32 python tools/attn_micro.py 32 1 > gpurun_out/r2h_ncu_micro.out 2>&1
+ls -la gpurun_out/
