@@ -52,6 +52,26 @@ NF_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_de
 // 1/rms of one row from its sum-of-squares partials part[p * stride], p < np, with 4
 // independent accumulators in a fixed order (kept out of line: inlined into the GEMM
 // epilogue it pushed the kernel into a local-memory stack frame).
+// EPI_PEER (peer.cuh): base such that base + col addresses row `trow` of output block
+// (bm, n0 / 256) in its owner's staging slot [this rank][owned block][128][256].
+__device__ __forceinline__ __nv_bfloat16* peer_row(const GemmArgs& a, int bm, int n0, int trow) {
+  const int blk = bm + (n0 / 256) * a.peer_mb;
+  const int owner = blk % a.peer_n, lb = blk / a.peer_n;
+  __nv_bfloat16* row = reinterpret_cast<__nv_bfloat16*>(a.peer_bases[owner] + a.peer_site_off + a.peer_stage_off) +
+                       (((int64_t)a.peer_rank * a.peer_maxown + lb) * 128 + trow) * 256;
+  return row - (n0 & ~255);
+}
+// EPI_PEER: after every epilogue thread's stores are fenced (system scope) and the 128
+// threads met, add BN/64 to the owner's flag of (block, this rank) with release semantics.
+__device__ __forceinline__ void peer_signal(const GemmArgs& a, int bm, int n0, int bn) {
+  if (bm >= a.peer_mb || n0 >= a.N) return;
+  const int blk = bm + (n0 / 256) * a.peer_mb;
+  const int owner = blk % a.peer_n, lb = blk / a.peer_n;
+  uint32_t* flag = reinterpret_cast<uint32_t*>(a.peer_bases[owner] + a.peer_site_off + a.peer_flags_off + 256) +
+                   lb * a.peer_n + a.peer_rank;
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(flag), "r"((uint32_t)(bn / 64)) : "memory");
+}
+
 __device__ __noinline__ float rms_row_scale(const float* part, int64_t stride, int np, float inv_d, float eps) {
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
   int p = 0;
@@ -86,7 +106,8 @@ NF_DEV void sincos_reduced(float a, float* s, float* c) {
 // accumulator in place and TMA-stores each finished 64-column box, so the epilogue
 // no longer waits on per-thread global loads and scattered row stores (short-K GEMMs,
 // e.g. the 70B TP8 rank's O projection with K = 1024, were epilogue-bound).
-template <int GEMM_STAGES, int BN, int CG, bool SR = false>
+// PEER: EPI_PEER instances (peer.cuh) -- the plain instances carry no peer code.
+template <int GEMM_STAGES, int BN, int CG, bool SR = false, bool PEER = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmO,
@@ -166,7 +187,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int tiles_dp = split2 ? 0 : (ts > 1 ? (tiles / G) * G : tiles);
   const int tail_units = ts > 1 ? (tiles - tiles_dp) * ts : 0;
   const int kb_half = num_kb / 2;
-  auto for_each_seg = [&](auto&& fn) {
+  // (the tile loop and its three bodies are always inlined: a body the compiler keeps out of
+  // line gets its captures through a local-memory closure -- a 328-400 byte stack frame that
+  // cost the sub-wave / short-K GEMMs 15-28 %, profiles/r2i_gemm_r1_vs_now.log)
+  auto for_each_seg = [&](auto&& fn) __attribute__((always_inline)) {
     if (sk) {
       for (int t = wid; t < sk_t0; t += G) fn(t, 0, num_kb);
       const int64_t a = (int64_t)wid * U_sk / G, b = (int64_t)(wid + 1) * U_sk / G;
@@ -231,7 +255,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       const uint64_t a_policy = policy_evict_last();  // activations are re-read by every n-tile
       const uint64_t b_policy = policy_evict_normal();
-      for_each_seg([&](int tile, int kb0, int kb1) {
+      for_each_seg([&](int tile, int kb0, int kb1) __attribute__((always_inline)) {
         const int mb = tile % tiles_m, nb = tile / tiles_m;
         const int b_row0 = grouped ? group_of(mb) * N : 0;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -261,7 +285,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       int as = 0;
       uint32_t aphase = 0;
-      for_each_seg([&](int tile, int kb0, int kb1) {
+      for_each_seg([&](int tile, int kb0, int kb1) __attribute__((always_inline)) {
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + as * BN;
@@ -296,7 +320,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if constexpr (SR) {
       if (leader) tma_prefetch_desc(&tmR);
     }
-    for_each_seg([&](int tile, int kb0, int kb1) {
+    for_each_seg([&](int tile, int kb0, int kb1) __attribute__((always_inline)) {
       const int mb = tile % tiles_m, nb = tile / tiles_m;
       const int r = mb * TM + (int)rank * GEMM_BM + trow;
       const bool valid = grouped ? r < args.grp_end[group_of(mb)] : r < M;
@@ -368,7 +392,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         (void)ld_acquire_gpu(args.sk_flag + tile * CG + (int)rank);
       }
       // accumulator + contributors' partials (fixed CTA order), times the row scale
-      auto ldacc = [&](int col, float sc, float (&v)[32]) {
+      auto ldacc = [&](int col, float sc, float (&v)[32]) __attribute__((always_inline)) {
         uint32_t rr[32];
         tmem_ld32(taddr + col, rr);
         tmem_ld_wait();
@@ -399,6 +423,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       float v[32];
       switch (args.epi) {
         case EPI_STORE:
+        case EPI_PEER:
         case EPI_F32: {
           if constexpr (SR) {
             if (args.epi == EPI_STORE) {
@@ -432,19 +457,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               break;
             }
           }
+          // EPI_PEER: the same bf16 stores, into the block owner's staging row (peer_row: the
+          // tile's columns all lie in one 256-column block) -- out of line, like the signal
+          // below, so the epilogue keeps its registers (inlined, they pushed the kernel into
+          // a local-memory stack frame)
+          __nv_bfloat16* obase;
+          if constexpr (PEER) obase = peer_row(args, mb * CG + (int)rank, n0, trow);
+          else obase = args.out + (int64_t)r * args.ldo;
 #pragma unroll 1
           for (int c = 0; c < BN / 32; ++c) {
             ldacc(c * 32, s, v);
             const int col = n0 + c * 32;
             if (valid && col < N) {
-              if (args.epi == EPI_STORE) {
-                store32_bf16(args.out + (int64_t)r * args.ldo + col, v);
+              if (args.epi != EPI_F32) {
+                store32_bf16(obase + col, v);
               } else {
                 float4* d = reinterpret_cast<float4*>(args.outf + (int64_t)r * args.ldo + col);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
               }
             }
+          }
+          if constexpr (PEER) {
+            asm volatile("fence.acq_rel.sys;" ::: "memory");  // this thread's peer stores before the flag
+            named_bar_sync(1, 128);
+            if (trow == 0) peer_signal(args, mb * CG + (int)rank, n0, BN);
           }
           break;
         }
@@ -621,34 +658,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           break;
         }
-        case EPI_PEER: {
-          // reduce-scatter fused into the epilogue: this unit's 128 rows of the block go to
-          // the block owner's staging slot (a peer store over NVLink for other owners)
-          const int bm = mb * CG + (int)rank;  // 128-row block of this unit
-#pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            ldacc(c * 32, s, v);
-            const int col = n0 + c * 32;
-            if (valid && col < N) {
-              const int blk = bm + (col / 256) * args.peer_mb;
-              const int owner = blk % args.peer_n, lb = blk / args.peer_n;
-              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.peer_bases[owner] + args.peer_site_off +
-                                                                    args.peer_stage_off) +
-                                   (((int64_t)args.peer_rank * args.peer_maxown + lb) * 128 + trow) * 256 + (col & 255);
-              store32_bf16(dst, v);
-            }
-          }
-          asm volatile("fence.acq_rel.sys;" ::: "memory");  // this thread's peer stores before the flag
-          named_bar_sync(1, 128);
-          if (trow == 0 && bm < args.peer_mb && n0 < N) {
-            const int blk = bm + (n0 / 256) * args.peer_mb;
-            const int owner = blk % args.peer_n, lb = blk / args.peer_n;
-            uint32_t* flag = reinterpret_cast<uint32_t*>(args.peer_bases[owner] + args.peer_site_off +
-                                                         args.peer_flags_off + 256) + lb * args.peer_n + args.peer_rank;
-            asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(flag), "r"((uint32_t)(BN / 64)) : "memory");
-          }
-          break;
-        }
         default:
           break;
       }
@@ -676,7 +685,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_once;
-bool g_attr_set[7] = {false, false, false, false, false, false, false};
+bool g_attr_set[12] = {};
 
 cudaError_t get_encode() {
   std::call_once(g_once, [] {
@@ -892,20 +901,28 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   int stages, cg = 1;
   void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs);
   int attr_idx;
+  const bool peer = args.epi == EPI_PEER;  // (never SR: see `sr`)
   if (pair_kernel) {
     stages = sr ? 4 : 6;
     cg = 2;
-    kern = sr ? gemm_tcgen05_kernel<4, 256, 2, true> : gemm_tcgen05_kernel<6, 256, 2>;
-    attr_idx = sr ? 6 : 4;
+    kern = sr ? gemm_tcgen05_kernel<4, 256, 2, true>
+              : (peer ? gemm_tcgen05_kernel<6, 256, 2, false, true> : gemm_tcgen05_kernel<6, 256, 2>);
+    attr_idx = sr ? 6 : (peer ? 7 : 4);
   } else if (bn == 256) {
     stages = sr ? 3 : (coloc ? 3 : 4);
-    kern = sr ? gemm_tcgen05_kernel<3, 256, 1, true>
-              : (coloc ? gemm_tcgen05_kernel<3, 256, 1> : gemm_tcgen05_kernel<4, 256, 1>);
-    attr_idx = sr ? 5 : (coloc ? 1 : 0);
+    if (peer)
+      kern = coloc ? gemm_tcgen05_kernel<3, 256, 1, false, true> : gemm_tcgen05_kernel<4, 256, 1, false, true>;
+    else
+      kern = sr ? gemm_tcgen05_kernel<3, 256, 1, true>
+                : (coloc ? gemm_tcgen05_kernel<3, 256, 1> : gemm_tcgen05_kernel<4, 256, 1>);
+    attr_idx = sr ? 5 : (peer ? (coloc ? 8 : 9) : (coloc ? 1 : 0));
   } else {
     stages = coloc ? 4 : 6;
-    kern = coloc ? gemm_tcgen05_kernel<4, 128, 1> : gemm_tcgen05_kernel<6, 128, 1>;
-    attr_idx = coloc ? 3 : 2;
+    if (peer)
+      kern = coloc ? gemm_tcgen05_kernel<4, 128, 1, false, true> : gemm_tcgen05_kernel<6, 128, 1, false, true>;
+    else
+      kern = coloc ? gemm_tcgen05_kernel<4, 128, 1> : gemm_tcgen05_kernel<6, 128, 1>;
+    attr_idx = peer ? (coloc ? 10 : 11) : (coloc ? 3 : 2);
   }
   const int smem = gemm_smem_bn(stages, bn / cg) + (sr ? bn * GEMM_BM * 2 : 0);
   CUtensorMap tr = ta, to = ta;
