@@ -1,4 +1,2 @@
-for i in 1 2; do
-echo "== r1 tree"; (cd _r1tree && MS=1024,2048 timeout 600 python tools/gemm_micro.py 148)
-echo "== now"; MS=1024,2048 timeout 600 python tools/gemm_micro.py 148
-done
+timeout 3000 python tools/workload_sweep.py --config c3loop --curves profiles/curves_b200_tp8.csv --steps 3 --rounds 2 > gpurun_out/r2j_workloads_c3loop.jsonl 2> gpurun_out/r2j_workloads_c3loop.err
+tail -5 gpurun_out/r2j_workloads_c3loop.err; cat gpurun_out/r2j_workloads_c3loop.jsonl | cut -c1-600
