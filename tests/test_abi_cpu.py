@@ -196,3 +196,28 @@ def test_tp_plan_and_comm_validation(nf):
         else:
             with pytest.raises(nf.NFError):
                 nf.packed_layer_bytes(cfg)
+
+
+def test_comm_sym_bytes_layout():
+    """nf_comm_sym_bytes (NEXT-3 symmetric buffer, host-only size query): it must hold, for
+    each of the 8 fused sites, a result region of max_tokens x d_model bf16 and the staging of
+    every 128x256 output block once, grows with the token count and the group size only
+    through the per-owner rounding, and rejects d_model not a multiple of 256."""
+    import ctypes as C
+
+    from paper_2408_12757_b200 import nf
+    cfg = nf.ModelCfg()
+    cfg.d_model, cfg.n_layers, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim = 8192, 1, 64, 8, 128
+    cfg.d_ffn, cfg.vocab, cfg.page_size, cfg.tp_rank = 28672, 32000, 16, 0
+    sizes = {}
+    for tp in (1, 2, 8):
+        cfg.tp_size = tp
+        for T in (1, 2048):
+            sizes[(tp, T)] = nf.comm_sym_bytes(cfg, T)
+    blocks = (2048 + 127) // 128 * (8192 // 256)
+    for tp in (1, 2, 8):
+        assert sizes[(tp, 2048)] >= 8 * (2048 * 8192 * 2 + blocks * 128 * 256 * 2)
+        assert sizes[(tp, 2048)] > sizes[(tp, 1)]
+    cfg.d_model = 8192 + 128
+    with pytest.raises(nf.NFError):
+        nf.comm_sym_bytes(cfg, 16)

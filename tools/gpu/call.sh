@@ -1,2 +1,2 @@
-timeout 3000 python tools/workload_sweep.py --config c3loop --curves profiles/curves_b200_tp8.csv --steps 3 --rounds 2 > gpurun_out/r2j_workloads_c3loop.jsonl 2> gpurun_out/r2j_workloads_c3loop.err
-tail -5 gpurun_out/r2j_workloads_c3loop.err; cat gpurun_out/r2j_workloads_c3loop.jsonl | cut -c1-600
+timeout 900 python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > gpurun_out/r2j_smoke.log 2>&1; tail -2 gpurun_out/r2j_smoke.log
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r2j_reference.log 2>&1; tail -c 800 gpurun_out/r2j_reference.log
