@@ -785,7 +785,14 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     tail_env = e ? atoi(e) : 1;
   }
   const int SB = std::max(1, sm_budget);
-  double best = (double)((tiles + SB - 1) / SB);
+  // (dev) NF_GEMM_FORCE=k: schedule k wins whenever it is feasible (A/B of schedules)
+  static int force_env = -2;
+  if (force_env == -2) {
+    const char* e = getenv("NF_GEMM_FORCE");
+    force_env = e ? atoi(e) : -1;
+  }
+  auto bias = [&](int k) { return force_env == k ? -1000.0 : 0.0; };
+  double best = (double)((tiles + SB - 1) / SB) + bias(0);
   int choice = 0, best_s = 1;
   const bool grouped = args.grp_off != nullptr;
   // (grouped: device-sized tile list, data-parallel or device-decided stream-K tail only)
@@ -794,12 +801,12 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     if (rem > 0) {
       int s = std::min(4, SB / rem);
       while (s > 1 && num_kb / s < 32) --s;
-      const double c = tiles / SB + 1.0 / s;
+      const double c = tiles / SB + 1.0 / s + bias(1);
       if (s > 1 && c < best - 1e-9) { best = c; choice = 1; best_s = s; }
     }
   }
   const int g2 = std::min(SB, 2 * tiles);
-  const double rounds2 = ((2 * tiles + g2 - 1) / g2) / 2.0;
+  const double rounds2 = ((2 * tiles + g2 - 1) / g2) / 2.0 + bias(2);
   if (!grouped && split_env && args.sk_part != nullptr && args.sk_slots >= tiles && num_kb >= 128 && rounds2 < best - 1e-9 &&
       args.epi != EPI_SILU && args.epi != EPI_ARGMAX) {
     best = rounds2;
@@ -813,7 +820,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     // (>= 32 k-blocks, N >= 2048; tools/gemm_micro.py): short-K pairs couple the two CTAs'
     // epilogues through the shared accumulator barrier
     const bool tie_ok = num_kb >= 32 && args.N >= 2048;
-    double c = (double)((pair_tiles + pairs - 1) / pairs);
+    double c = (double)((pair_tiles + pairs - 1) / pairs) + bias(3);
     // pairs with a split-K tail (same rule as single CTAs, pair tiles over pairs)
     const int rem = pair_tiles % pairs;
     if (tail_env && rem > 0 && args.sk_part != nullptr && args.sk_slots >= SB && pair_tiles > pairs / 4) {
@@ -842,7 +849,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   if (!grouped && tail_env && args.sk_part != nullptr && args.sk_slots >= SB && tiles < SB && !coloc && l2_mb <= 64.0) {
     const int64_t U = (int64_t)tiles * num_kb;
     const int G = (int)std::min<int64_t>(SB, std::max<int64_t>(tiles, U / 16));
-    const double c = (double)U / ((double)G * num_kb) + 0.3;
+    const double c = (double)U / ((double)G * num_kb) + 0.3 + bias(4);
     if (G > tiles && c < best - 1e-9) {
       best = c;
       choice = 4;
@@ -856,7 +863,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
       pair_tiles < pairs && !coloc && l2_mb <= 64.0) {
     const int64_t U = (int64_t)pair_tiles * num_kb;
     const int G = (int)std::min<int64_t>(pairs, std::max<int64_t>(pair_tiles, U / 16));
-    const double c = (double)U / ((double)G * num_kb) + 0.3;
+    const double c = (double)U / ((double)G * num_kb) + 0.3 + bias(5);
     // measured no faster than single-CTA stream-K on the 70B-rank KQV (r1c_gemm_micro_streamk_pairs.log:
     // 900 vs 912 TF/s at M 2048, 626 vs 672 at M 1024): taken only when clearly better
     if (G > pair_tiles && c < best - 0.05) {

@@ -11,7 +11,7 @@ from paper_2408_12757_b200 import nf, runtime as rt  # noqa: E402
 
 SHAPES = {  # name: (N, K)
     "8b.kqv": (6144, 4096), "8b.o": (4096, 4096), "8b.ug": (28672, 4096), "8b.down": (4096, 14336),
-    "70r.kqv": (1280, 8192), "70r.o": (8192, 1024), "70r.ug": (7168, 8192), "70r.down": (8192, 3584),
+    "70r.kqv": (1280, 8192), "70r.o": (8192, 1024), "70r.ocol": (1024, 8192), "70r.ug": (7168, 8192), "70r.down": (8192, 3584),
 }
 budgets = [int(x) for x in sys.argv[1:]] or [148, 108]
 st = rt.stream_handle()

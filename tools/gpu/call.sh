@@ -1,2 +1,1 @@
-timeout 900 python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > gpurun_out/r2j_smoke.log 2>&1; tail -2 gpurun_out/r2j_smoke.log
-timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r2j_reference.log 2>&1; tail -c 800 gpurun_out/r2j_reference.log
+for f in -1 0 1 2 3 4 5; do echo "== force $f"; NF_GEMM_FORCE=$f ONLY=70r MS=512,1024,2048 timeout 600 python tools/gemm_micro.py 148 132 2>&1 | grep -E "kqv|ocol|70r.o "; done
