@@ -370,7 +370,8 @@ def run_nf(args, rank, world, local_rank):
             hs = [None] * world
             dist.all_gather_object(hs, h)
         nf.comm_sym_open(comm, None if loop else hs)
-        fused_note = "fused GEMM->AllReduce over peer memory (EPI_PEER + owner reduce), NCCL for the AllGathers"
+        fused_note = ("fused over peer memory: row-parallel GEMM->AllReduce (EPI_PEER + owner reduce) and the O "
+                      "column-parallel GEMM->AllGather (epilogue stores to every rank); NCCL for the attention AllGather")
 
     # ---------------- weights: replicated tensors (embedding, norms) and layer 0 (in-run parity)
     # from a generator seeded identically on every rank; every other layer's shards from a

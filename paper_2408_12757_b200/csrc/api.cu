@@ -1213,6 +1213,18 @@ void set_peer_args(GemmArgs* a, const LayerCtx& L, int site, int M) {
   a->peer_maxown = g.maxown;
   a->peer_mb = (M + PEER_BM - 1) / PEER_BM;
 }
+// Fused AllGather of the O column-parallel projection (group 0): its EPI_RESID epilogue
+// writes the rank's slice into every rank's site-0 result region (site 0 = the O-row site
+// of group 0, which the column group never uses) -- peer.cuh.
+bool fused_ag_ok(const LayerCtx& L, int M) {
+  return fused_site_ok(L, M) && (L.c->d_model / L.c->tp_size) % 64 == 0;
+}
+void set_peer_ag_args(GemmArgs* a, const LayerCtx& L, int M) {
+  set_peer_args(a, L, 0, M);
+  a->epi = EPI_RESID;
+  a->peer_mode = 1;
+  a->peer_result_off = comm_peer_geom(L.comm).result_off;
+}
 const __nv_bfloat16* peer_result(const LayerCtx& L, int site) {
   const PeerGeom& g = comm_peer_geom(L.comm);
   return reinterpret_cast<const __nv_bfloat16*>(comm_sym_local(L.comm) + g.site(site) + g.result_off);
@@ -1305,13 +1317,22 @@ nf_status tp_stage_b(nf_plan* p, const LayerCtx& L, int gi, const Group& G, cons
     a.ldo = Dl;
     a.resid = x + G.nr.t0 * D + rank * Dl;
     a.ldr = D;
+    const bool fz = fused_ag_ok(L, M);
+    if (fz) set_peer_ag_args(&a, L, M);  // all-gather fused into the epilogue (NEXT-3)
     {
       ProfScope ps(NF_OP_O, L.cs);
       NF_CUDA(launch_gemm(L.w->ocat, qd_full, (const __nv_bfloat16*)wt->w_o, qd_full, a,
                           clamp_dense(L, L.p->spec.sm[NF_OP_O]), L.cs));
     }
-    NF_TRY(edge(p->ev_o[gi], L.cs, L.ns));
-    {
+    if (fz) {
+      comm_fused_site_barrier(L.comm);
+      const PeerGeom& g = comm_peer_geom(L.comm);
+      ProfScope ps(NF_OP_NET, L.ns);
+      NF_CUDA(launch_peer_wait(comm_peer_bases(L.comm), g, 0, (uint32_t)(g.n * ((M + PEER_BM - 1) / PEER_BM) * (Dl / 64)),
+                               comm_peer_timeout_ns(L.comm), L.ns));
+      comm_count_fused(L.comm);
+    } else {
+      NF_TRY(edge(p->ev_o[gi], L.cs, L.ns));
       ProfScope ps(NF_OP_NET, L.ns);
       NF_TRY(comm_all_gather(L.comm, L.w->hcol, L.w->ag2, (size_t)M * Dl, L.ns));
     }
@@ -1365,7 +1386,10 @@ nf_status tp_stage_c(nf_plan* p, const LayerCtx& L, int gi, const Group& G, cons
   __nv_bfloat16* h1 = L.w->h1 + G.nr.t0 * D;
   if (G.col) {
     if (L.ns != L.cs) NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_ago, 0));
-    NF_CUDA(launch_interleave(L.w->ag2, N, M, (int)Dl, h1, L.w->part_h1 + G.nr.t0, L.cs));
+    if (fused_ag_ok(L, M))
+      NF_CUDA(launch_interleave_from_peers(peer_result(L, 0), N, M, (int)Dl, h1, L.w->part_h1 + G.nr.t0, L.cs));
+    else
+      NF_CUDA(launch_interleave(L.w->ag2, N, M, (int)Dl, h1, L.w->part_h1 + G.nr.t0, L.cs));
   } else {
     if (L.ns != L.cs) NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_aro[gi], 0));
     if (fused_site_ok(L, M))

@@ -366,7 +366,7 @@ nf_status nf_comm_sym_status(nf_comm* c, int32_t* timeouts_out, int64_t* fused_s
   }
   if (v[0]) {  // the first timeout's record, for the caller's error report (nf_last_error)
     set_error(NF_OK, "peer wait timeout: site %u %s block %u src %u observed %u target %u (%u timeouts)", v[16],
-              v[17] ? "done" : "flag", v[18] / 16, v[18] % 16, v[19], v[20], v[0]);
+              v[17] == 2 ? "all-gather done" : v[17] ? "done" : "flag", v[18] / 16, v[18] % 16, v[19], v[20], v[0]);
   }
   return NF_OK;
 }

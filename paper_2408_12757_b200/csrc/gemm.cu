@@ -61,6 +61,22 @@ __device__ __forceinline__ __nv_bfloat16* peer_row(const GemmArgs& a, int bm, in
                        (((int64_t)a.peer_rank * a.peer_maxown + lb) * 128 + trow) * 256;
   return row - (n0 & ~255);
 }
+// EPI_RESID in a PEER instance (args.peer_mode 1, the O column-parallel projection): row r
+// of this rank's slice in rank q's all-gather region [peer_n][M][N] (a site's result region).
+__device__ __forceinline__ __nv_bfloat16* peer_ag_row(const GemmArgs& a, int q, int r) {
+  return reinterpret_cast<__nv_bfloat16*>(a.peer_bases[q] + a.peer_site_off + a.peer_result_off) +
+         ((int64_t)a.peer_rank * a.M + r) * a.N;
+}
+// ... then every rank's `done` counter of the site grows by this unit's 64-column chunks.
+__device__ __forceinline__ void peer_ag_signal(const GemmArgs& a, int bm, int n0, int bn) {
+  if (bm >= a.peer_mb || n0 >= a.N) return;
+  const uint32_t chunks = (uint32_t)(min(bn, a.N - n0) / 64);
+  for (int q = 0; q < a.peer_n; ++q) {
+    uint32_t* done = reinterpret_cast<uint32_t*>(a.peer_bases[(a.peer_rank + 1 + q) % a.peer_n] + a.peer_site_off +
+                                                 a.peer_flags_off);
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(done), "r"(chunks) : "memory");
+  }
+}
 // EPI_PEER: after every epilogue thread's stores are fenced (system scope) and the 128
 // threads met, add BN/64 to the owner's flag of (block, this rank) with release semantics.
 __device__ __forceinline__ void peer_signal(const GemmArgs& a, int bm, int n0, int bn) {
@@ -566,12 +582,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 v[j] = round_bf16(rr[j] + v[j]);
                 sq = fmaf(v[j], v[j], sq);
               }
-              store32_bf16(args.out + (int64_t)r * args.ldo + col, v);
+              if constexpr (PEER) {  // all-gather fused into the epilogue: the row segment to every rank
+                for (int q = 0; q < args.peer_n; ++q) store32_bf16(peer_ag_row(args, (args.peer_rank + 1 + q) % args.peer_n, r) + col, v);
+              } else {
+                store32_bf16(args.out + (int64_t)r * args.ldo + col, v);
+              }
             }
             if ((c & 3) == 3) {
               if (args.sq_out != nullptr && valid) args.sq_out[(int64_t)((n0 >> 7) + (c >> 2)) * args.sq_stride + r] = sq;
               sq = 0.f;
             }
+          }
+          if constexpr (PEER) {
+            asm volatile("fence.acq_rel.sys;" ::: "memory");  // this thread's peer stores before the counters
+            named_bar_sync(1, 128);
+            if (trow == 0) peer_ag_signal(args, mb * CG + (int)rank, n0, BN);
           }
           break;
         }
@@ -903,12 +928,12 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     const char* e2 = getenv("NF_GEMM_SR_MAXKB");
     sr_kb_env = e2 ? atoi(e2) : 32;
   }
+  const bool peer = args.epi == EPI_PEER || args.peer_mode == 1;  // fused reduce-scatter / all-gather epilogues
   const bool sr = sr_env && (args.epi == EPI_RESID || (args.epi == EPI_STORE && args.outf == nullptr)) && bn == 256 &&
-                  !grouped && !coloc && num_kb <= sr_kb_env;
+                  !grouped && !coloc && num_kb <= sr_kb_env && !peer;
   int stages, cg = 1;
   void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, GemmArgs);
   int attr_idx;
-  const bool peer = args.epi == EPI_PEER;  // (never SR: see `sr`)
   if (pair_kernel) {
     stages = sr ? 4 : 6;
     cg = 2;

@@ -79,8 +79,12 @@ struct GemmArgs {
   // at peer_site_off + peer_flags_off + 256 + 4 * (owned index * peer_n + peer_rank) is bumped by BN/64
   // (release, sys scope)
   uint8_t* const* peer_bases;  // device array [peer_n]: every rank's symmetric buffer
-  int64_t peer_site_off, peer_stage_off, peer_flags_off;
+  int64_t peer_site_off, peer_stage_off, peer_flags_off, peer_result_off;
   int peer_n, peer_rank, peer_maxown, peer_mb;
+  // peer_mode 1 (EPI_RESID, the O column-parallel projection): the output slice goes to every
+  // rank's all-gather region [peer_n][M][N] at peer_site_off + peer_result_off instead of `out`,
+  // then every rank's site `done` counter grows by the unit's 64-column chunks (release, sys)
+  int peer_mode;
 };
 
 // Bytes of stream-K scratch for a GEMM with this many tiles at this grid.

@@ -181,6 +181,7 @@ __global__ void pack_gate_up_kernel(const __nv_bfloat16* __restrict__ gate, cons
 
 // dst[row][q*C + c] = src[q][row][c] for q < n (rank-major gather -> row-major),
 // optional per-row sum of squares of the written values into part[row]
+template <bool CG>  // CG: src written by other GPUs (fused all-gather region): loads through L2
 __global__ void interleave_kernel(const __nv_bfloat16* __restrict__ src, int n, int rows, int C,
                                   __nv_bfloat16* __restrict__ dst, float* __restrict__ part) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -189,7 +190,8 @@ __global__ void interleave_kernel(const __nv_bfloat16* __restrict__ src, int n, 
   const int cv = C / 8;
   for (int i = lane; i < n * cv; i += 32) {
     const int q = i / cv, c = i % cv;
-    const uint4 u = reinterpret_cast<const uint4*>(src + ((int64_t)q * rows + warp) * C)[c];
+    const uint4* sp = reinterpret_cast<const uint4*>(src + ((int64_t)q * rows + warp) * C) + c;
+    const uint4 u = CG ? __ldcg(sp) : *sp;
     reinterpret_cast<uint4*>(dst + (int64_t)warp * n * C + (int64_t)q * C)[c] = u;
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
@@ -280,7 +282,15 @@ cudaError_t launch_argmax_reduce(const float* val, const int* idx, int ntiles, i
 cudaError_t launch_interleave(const __nv_bfloat16* src, int n, int rows, int C, __nv_bfloat16* dst, float* part,
                               cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
-  interleave_kernel<<<(rows + 7) / 8, 256, 0, st>>>(src, n, rows, C, dst, part);
+  interleave_kernel<false><<<(rows + 7) / 8, 256, 0, st>>>(src, n, rows, C, dst, part);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_interleave_from_peers(const __nv_bfloat16* src, int n, int rows, int C, __nv_bfloat16* dst,
+                                         float* part, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  interleave_kernel<true><<<(rows + 7) / 8, 256, 0, st>>>(src, n, rows, C, dst, part);
   count_launch();
   return cudaGetLastError();
 }

@@ -22,6 +22,9 @@ cudaError_t launch_argmax_reduce(const float* val, const int* idx, int ntiles, i
                                  const int* row_req, int* next_ids, cudaStream_t st);
 cudaError_t launch_interleave(const __nv_bfloat16* src, int n, int rows, int C, __nv_bfloat16* dst, float* part,
                               cudaStream_t st);
+// launch_interleave reading a region other GPUs wrote (the fused all-gather): loads through L2
+cudaError_t launch_interleave_from_peers(const __nv_bfloat16* src, int n, int rows, int C, __nv_bfloat16* dst,
+                                         float* part, cudaStream_t st);
 cudaError_t launch_sum_bf16(const void* const* in, int n, __nv_bfloat16* out, size_t count, bool ring, cudaStream_t st);
 cudaError_t launch_fill_i32(int* p, int n, int v, cudaStream_t st);
 cudaError_t launch_smid_probe(int* counts, int ctas, cudaStream_t st);

@@ -162,7 +162,26 @@ __global__ void __launch_bounds__(PR_THREADS, 8) peer_reduce_kernel(uint8_t* con
   }
 }
 
+// Consumer side of the fused all-gather (EPI_RESID peer_mode 1): wait until every rank's
+// producer units have landed here (the site's `done` counter reaches `expected`), clear it.
+__global__ void peer_wait_kernel(uint8_t* const* __restrict__ bases, PeerGeom g, int site, uint32_t expected,
+                                 long long timeout_ns) {
+  uint8_t* mine = bases[g.rank];
+  uint32_t* done = reinterpret_cast<uint32_t*>(mine + g.site(site) + g.flags_off);
+  wait_geq(done, expected, reinterpret_cast<uint32_t*>(mine), timeout_ns, site, 2, 0);
+  *done = 0;
+  fence_sys();
+}
+
 }  // namespace
+
+cudaError_t launch_peer_wait(uint8_t* const* bases, const PeerGeom& g, int site, uint32_t expected, long long timeout_ns,
+                             cudaStream_t st) {
+  if (site < 0 || site >= PEER_SITES) return cudaErrorInvalidValue;
+  peer_wait_kernel<<<1, 32, 0, st>>>(bases, g, site, expected, timeout_ns);
+  count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_peer_reduce(uint8_t* const* bases, const PeerGeom& g, int site, int M, int ctas,
                                long long timeout_ns, cudaStream_t st) {

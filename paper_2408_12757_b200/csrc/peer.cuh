@@ -17,6 +17,11 @@
 // counters; it ends when its own `done` counter has seen every block.  The
 // consumer then adds the residual from the result region (tp_stage_c / _d).
 //
+// The O column-parallel projection's AllGather (H1) is fused the same way:
+// its EPI_RESID epilogue (peer_mode 1) stores the rank's output slice into every rank's
+// all-gather region (site 0's result region, [N][M][D/N]) and bumps every rank's site-0
+// `done` counter; peer_wait on the network stream waits for all ranks' units.
+//
 // Flags and `done` counters reset themselves (a flag is cleared by its owner
 // before the block's broadcast; `done` by its rank after the last block), which is
 // safe because the next use of a site on any rank causally follows the completion
@@ -54,6 +59,11 @@ PeerGeom peer_geom(int n, int rank, int max_rows, int cols);
 // bases: device array [n] of every rank's buffer base (this rank's mapping); M rows x geom.cols.
 cudaError_t launch_peer_reduce(uint8_t* const* bases, const PeerGeom& g, int site, int M, int ctas,
                                long long timeout_ns, cudaStream_t st);
+
+// Wait (one thread) until this rank's `done` counter of `site` reaches `expected` (the fused
+// all-gather's producer units from every rank), then clear it.
+cudaError_t launch_peer_wait(uint8_t* const* bases, const PeerGeom& g, int site, uint32_t expected, long long timeout_ns,
+                             cudaStream_t st);
 
 // Load every kernel of the library into the current context / a green context (see peer.cu).
 cudaError_t preload_all_kernels();
