@@ -200,8 +200,11 @@ void nf_comm_destroy(nf_comm* comm);
  * staging slot (owner = block % tp_size; a peer store over NVLink), and the owner's
  * reduce kernel on the network stream sums the tp_size partials in rank order in fp32
  * (one bf16 rounding: the NF_AR_F32 arithmetic) and pushes the block to every rank
- * (all-gather), replacing the NCCL AllReduce of that site.  Dense FFN only (MoE layers
- * keep the NCCL AllReduce).  All ranks of a group must enable it together.
+ * (all-gather), replacing the NCCL AllReduce of that site (Down: dense FFN only, MoE layers
+ * keep the communicator's AllReduce).  The O column-parallel projection's AllGather
+ * is fused the same way: its residual epilogue stores the rank's output
+ * slice into every rank's all-gather region.  The attention-output AllGather stays on
+ * the communicator.  All ranks of a group must enable it together.
  *
  * nf_comm_sym_bytes: size of one rank's symmetric buffer for steps of at most max_tokens
  *   rows (d_model % 256 == 0).

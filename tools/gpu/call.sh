@@ -1,3 +1,2 @@
-timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/r2k_gputest.log 2>&1; tail -3 gpurun_out/r2k_gputest.log
-timeout 900 python bench.py > gpurun_out/r2k_bench_default.log 2>&1; tail -c 300 gpurun_out/r2k_bench_default.log
-timeout 900 python bench.py --config c3loop --steps 10 > gpurun_out/r2k_bench_c3loop.log 2>&1; tail -c 300 gpurun_out/r2k_bench_c3loop.log
+NF_GREEN=0 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:gemm_tcgen05 -s 407 -c 4 -o gpurun_out/r2k_8b_seq_gemms python bench.py --mode sequential --steps 1 --warmup 3 --ncu > gpurun_out/r2k_ncu_8b_seq.out 2>&1
+tail -2 gpurun_out/r2k_ncu_8b_seq.out
