@@ -33,11 +33,9 @@ namespace {
 
 constexpr int DS_BOX = 16 * 128;  // one 16-row x 64-column 128B-swizzled box
 
-template <int HD>
-constexpr int ds_stages() { return HD == 128 ? 2 : 4; }
-
-template <int HD, int W>
-constexpr int ds_smem() { return W * ds_stages<HD>() * (2 * 16 * HD * 2) + W * ds_stages<HD>() * 8 + 1024; }
+// NS = pages in flight per warp (the warp's ring depth)
+template <int HD, int W, int NS>
+constexpr int ds_smem() { return W * NS * (2 * 16 * HD * 2) + W * NS * 8 + 1024; }
 
 NF_DEV uint32_t movm_trans(uint32_t a) {
   uint32_t d;
@@ -51,13 +49,13 @@ NF_DEV int ld_uniform(const int* p) {  // every lane loads the same word (one tr
   return v;
 }
 
-template <int HD, int W>
-__global__ void __launch_bounds__(W * 32, 1)
+template <int HD, int W, int NS, int CH = 2, bool LA = false>
+// (registers: the warps of an SM sub-partition share its 16 K registers, ceil(W / 4) warps each)
+__global__ void __maxnreg__((512 / ((W + 3) / 4) / 8 * 8) < 255 ? (512 / ((W + 3) / 4) / 8 * 8) : 255)
     decode_stream_kernel(const __grid_constant__ CUtensorMap pages, const AttnArgs a,
                          const DecodeItem* __restrict__ items, int n_items) {
   constexpr int KB = 16 * HD * 2;  // K (or V) bytes of one page of one KV head
   constexpr int SB = 2 * KB;       // stage: K then V
-  constexpr int NS = ds_stages<HD>();
   constexpr int KS = HD / 16;      // k-steps of S^T = m-tiles of O^T
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -112,6 +110,85 @@ __global__ void __launch_bounds__(W * 32, 1)
   const int g = lane >> 2;           // key row (C fragments) / query head column (B fragments)
   const int hc = 2 * (lane & 3);     // first of the two head columns of this lane's C fragments
   const int kk = 2 * (lane & 3);     // first key of this lane's V^T A-fragment registers 0/1 (+8: 2/3)
+  uint32_t qb[KS][2];                // the item's query rows as B fragments
+
+  // One page of the stream: wait for its slot, S^T = K.Q^T in CH independent MMA chains,
+  // V^T fragments into registers, then refill the slot with the page NS ahead.
+  auto load_page = [&](uint32_t jj, float (&sc)[4], uint32_t (&vf)[KS][4]) __attribute__((always_inline)) {
+    const uint32_t s = jj % NS;
+    mbar_wait(&bars[s], (jj / NS) & 1);
+    const uint32_t base = ring + s * SB;
+    float sa[CH][4];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) sa[c][0] = sa[c][1] = sa[c][2] = sa[c][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      uint32_t kf[4];
+      ldmatrix_x4(kf, base + offK[ks & 3] + (ks >> 2) * DS_BOX);
+      mma_bf16_16816(sa[ks % CH], kf, qb[ks]);
+    }
+#pragma unroll
+    for (int mt = 0; mt < KS; ++mt) ldmatrix_x4_trans(vf[mt], base + offV[mt & 3] + (mt >> 2) * DS_BOX);
+    __syncwarp();
+    if ((int)jj + NS < n_pg) {  // refill the slot with the page NS ahead
+      issue(jj + NS, nrow);
+      if ((int)jj + NS + 1 < n_pg) nrow = ld_uniform(rows + jj + NS + 1);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if constexpr (CH == 4) sc[e] = (sa[0][e] + sa[1][e]) + (sa[2][e] + sa[3][e]);
+      else sc[e] = sa[0][e] + sa[1][e];
+    }
+  };
+  // Softmax of one page's scores and its P.V contribution (page p of an item with np pages).
+  auto consume = [&](int p, int np, int kv_len, float (&sc)[4], uint32_t (&vf)[KS][4], float& m0, float& m1,
+                     float& thr0, float& thr1, float (&oacc)[KS][4], float (&lacc)[4]) __attribute__((always_inline)) {
+    if (p == np - 1) {  // keys past kv_len exist only on the item's last page
+      const int valid = kv_len - p * 16;
+      if (g >= valid) sc[0] = sc[1] = -INFINITY;
+      if (g + 8 >= valid) sc[2] = sc[3] = -INFINITY;
+      // V rows past kv_len may hold anything (NaN in unused pool slots): zero them so P=0 rows add 0
+      const uint32_t mlo = (kk < valid ? 0x0000FFFFu : 0u) | (kk + 1 < valid ? 0xFFFF0000u : 0u);
+      const uint32_t mhi = (kk + 8 < valid ? 0x0000FFFFu : 0u) | (kk + 9 < valid ? 0xFFFF0000u : 0u);
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) {
+        vf[mt][0] &= mlo;
+        vf[mt][1] &= mlo;
+        vf[mt][2] &= mhi;
+        vf[mt][3] &= mhi;
+      }
+    }
+    // Online softmax with a lazily updated running max (attention.cu): probabilities are
+    // taken against a stale max as long as no raw score exceeds thr = (m + 8) / scale;
+    // the cross-lane max and the rescale of O and l run only when the max really moves.
+    if (__any_sync(0xffffffffu, fmaxf(sc[0], sc[2]) > thr0 || fmaxf(sc[1], sc[3]) > thr1)) {
+      float r0m = fmaxf(sc[0], sc[2]), r1m = fmaxf(sc[1], sc[3]);
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        r0m = fmaxf(r0m, __shfl_xor_sync(0xffffffffu, r0m, o));
+        r1m = fmaxf(r1m, __shfl_xor_sync(0xffffffffu, r1m, o));
+      }
+      const float mn0 = fmaxf(m0, r0m * sl2), mn1 = fmaxf(m1, r1m * sl2);
+      const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
+      m0 = mn0;
+      m1 = mn1;
+      thr0 = (mn0 + 8.f) * inv_sl2;
+      thr1 = (mn1 + 8.f) * inv_sl2;
+      lacc[0] *= al0; lacc[2] *= al0;
+      lacc[1] *= al1; lacc[3] *= al1;
+#pragma unroll
+      for (int mt = 0; mt < KS; ++mt) {
+        oacc[mt][0] *= al0; oacc[mt][1] *= al1;
+        oacc[mt][2] *= al0; oacc[mt][3] *= al1;
+      }
+    }
+    const float p0 = ex2_approx(fmaf(sc[0], sl2, -m0)), p1 = ex2_approx(fmaf(sc[1], sl2, -m1));
+    const float p2 = ex2_approx(fmaf(sc[2], sl2, -m0)), p3 = ex2_approx(fmaf(sc[3], sl2, -m1));
+    const uint32_t pb[2] = {movm_trans(pack_bf16x2(p0, p1)), movm_trans(pack_bf16x2(p2, p3))};
+    mma_bf16_16816(lacc, ones, pb);  // l_h = sum_k P^T[k][h] (every row of the ones tile)
+#pragma unroll
+    for (int mt = 0; mt < KS; ++mt) mma_bf16_16816(oacc[mt], vf[mt], pb);
+  };
 
   uint32_t j = 0;  // pages of the stream consumed
   for (int round = 0, item = gw; item < n_items; item = item_of(++round)) {
@@ -124,7 +201,6 @@ __global__ void __launch_bounds__(W * 32, 1)
       }
     }
     const __nv_bfloat16* qbase = a.q + ((int64_t)it.t * a.qh + (int64_t)it.kvh * R) * HD;
-    uint32_t qb[KS][2];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
       const int kc = ks * 16 + hc;
@@ -138,74 +214,29 @@ __global__ void __launch_bounds__(W * 32, 1)
     for (int d = 0; d < KS; ++d) oacc[d][0] = oacc[d][1] = oacc[d][2] = oacc[d][3] = 0.f;
 
     const int np = (it.kv_len + 15) >> 4;
-    for (int p = 0; p < np; ++p, ++j) {
-      const uint32_t s = j % NS;
-      mbar_wait(&bars[s], (j / NS) & 1);
-      const uint32_t base = ring + s * SB;
-      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        uint32_t kf[4];
-        ldmatrix_x4(kf, base + offK[ks & 3] + (ks >> 2) * DS_BOX);
-        if (ks & 1) mma_bf16_16816(sb, kf, qb[ks]);
-        else mma_bf16_16816(sa, kf, qb[ks]);
+    if constexpr (!LA) {
+      for (int p = 0; p < np; ++p, ++j) {
+        float sc[4];
+        uint32_t vf[KS][4];
+        load_page(j, sc, vf);
+        consume(p, np, it.kv_len, sc, vf, m0, m1, thr0, thr1, oacc, lacc);
       }
-      uint32_t vf[KS][4];
-#pragma unroll
-      for (int mt = 0; mt < KS; ++mt) ldmatrix_x4_trans(vf[mt], base + offV[mt & 3] + (mt >> 2) * DS_BOX);
-      __syncwarp();
-      if ((int)j + NS < n_pg) {  // refill the slot with the page NS ahead
-        issue(j + NS, nrow);
-        if ((int)j + NS + 1 < n_pg) nrow = ld_uniform(rows + j + NS + 1);
+    } else {
+      // look-ahead: page p+1's S^T chain is issued before page p's softmax and P.V, so the
+      // two dependent chains of consecutive pages overlap (ping-pong register sets A / B)
+      float scA[4], scB[4];
+      uint32_t vA[KS][4], vB[KS][4];
+      load_page(j, scA, vA);
+      for (int p = 0;;) {
+        if (p + 1 < np) load_page(j + 1, scB, vB);
+        consume(p, np, it.kv_len, scA, vA, m0, m1, thr0, thr1, oacc, lacc);
+        ++p, ++j;
+        if (p >= np) break;
+        if (p + 1 < np) load_page(j + 1, scA, vA);
+        consume(p, np, it.kv_len, scB, vB, m0, m1, thr0, thr1, oacc, lacc);
+        ++p, ++j;
+        if (p >= np) break;
       }
-      float sc[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) sc[e] = sa[e] + sb[e];
-      if (p == np - 1) {  // keys past kv_len exist only on the item's last page
-        const int valid = it.kv_len - p * 16;
-        if (g >= valid) sc[0] = sc[1] = -INFINITY;
-        if (g + 8 >= valid) sc[2] = sc[3] = -INFINITY;
-        // V rows past kv_len may hold anything (NaN in unused pool slots): zero them so P=0 rows add 0
-        const uint32_t mlo = (kk < valid ? 0x0000FFFFu : 0u) | (kk + 1 < valid ? 0xFFFF0000u : 0u);
-        const uint32_t mhi = (kk + 8 < valid ? 0x0000FFFFu : 0u) | (kk + 9 < valid ? 0xFFFF0000u : 0u);
-#pragma unroll
-        for (int mt = 0; mt < KS; ++mt) {
-          vf[mt][0] &= mlo;
-          vf[mt][1] &= mlo;
-          vf[mt][2] &= mhi;
-          vf[mt][3] &= mhi;
-        }
-      }
-      // Online softmax with a lazily updated running max (attention.cu): probabilities are
-      // taken against a stale max as long as no raw score exceeds thr = (m + 8) / scale;
-      // the cross-lane max and the rescale of O and l run only when the max really moves.
-      if (__any_sync(0xffffffffu, fmaxf(sc[0], sc[2]) > thr0 || fmaxf(sc[1], sc[3]) > thr1)) {
-        float r0m = fmaxf(sc[0], sc[2]), r1m = fmaxf(sc[1], sc[3]);
-#pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-          r0m = fmaxf(r0m, __shfl_xor_sync(0xffffffffu, r0m, o));
-          r1m = fmaxf(r1m, __shfl_xor_sync(0xffffffffu, r1m, o));
-        }
-        const float mn0 = fmaxf(m0, r0m * sl2), mn1 = fmaxf(m1, r1m * sl2);
-        const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);
-        m0 = mn0;
-        m1 = mn1;
-        thr0 = (mn0 + 8.f) * inv_sl2;
-        thr1 = (mn1 + 8.f) * inv_sl2;
-        lacc[0] *= al0; lacc[2] *= al0;
-        lacc[1] *= al1; lacc[3] *= al1;
-#pragma unroll
-        for (int mt = 0; mt < KS; ++mt) {
-          oacc[mt][0] *= al0; oacc[mt][1] *= al1;
-          oacc[mt][2] *= al0; oacc[mt][3] *= al1;
-        }
-      }
-      const float p0 = ex2_approx(fmaf(sc[0], sl2, -m0)), p1 = ex2_approx(fmaf(sc[1], sl2, -m1));
-      const float p2 = ex2_approx(fmaf(sc[2], sl2, -m0)), p3 = ex2_approx(fmaf(sc[3], sl2, -m1));
-      const uint32_t pb[2] = {movm_trans(pack_bf16x2(p0, p1)), movm_trans(pack_bf16x2(p2, p3))};
-      mma_bf16_16816(lacc, ones, pb);  // l_h = sum_k P^T[k][h] (every row of the ones tile)
-#pragma unroll
-      for (int mt = 0; mt < KS; ++mt) mma_bf16_16816(oacc[mt], vf[mt], pb);
     }
     const float i0 = 1.f / lacc[0], i1 = 1.f / lacc[1];
     __nv_bfloat16* obase = a.o + (int64_t)it.t * a.qh * HD + (int64_t)it.kvh * R * HD;
@@ -224,31 +255,43 @@ __global__ void __launch_bounds__(W * 32, 1)
   }
 }
 
-template <int HD, int W>
+template <int HD, int W, int NS, int CH = 2, bool LA = false>
 cudaError_t launch_stream_hdw(const CUtensorMap& pm, const AttnArgs& a, const DecodeItem* items, int n_items,
                               int grid, cudaStream_t st) {
+  static_assert(ds_smem<HD, W, NS>() <= 232448, "shared memory");
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_stream_kernel<HD, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         ds_smem<HD, W>());
+    cudaError_t e = cudaFuncSetAttribute(decode_stream_kernel<HD, W, NS, CH, LA>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, ds_smem<HD, W, NS>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  decode_stream_kernel<HD, W><<<grid, W * 32, ds_smem<HD, W>(), st>>>(pm, a, items, n_items);
+  decode_stream_kernel<HD, W, NS, CH, LA><<<grid, W * 32, ds_smem<HD, W, NS>(), st>>>(pm, a, items, n_items);
   count_launch();
   return cudaGetLastError();
 }
 
+// (dev) NF_DEC_STREAM_VAR: 1 = four S^T chains, 2 = look-ahead, 3 = both (A/B runs)
+int decode_stream_var() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NF_DEC_STREAM_VAR");
+    v = e ? atoi(e) : 0;
+    if (v < 0 || v > 3) v = 0;
+  }
+  return v;
+}
+
 }  // namespace
 
-// Consumer warps per CTA (each with a 2 x 8 KB ring at head_dim 128): 12 by default;
-// NF_DEC_STREAM_WARPS=13 / 14 fill up to 225 KB of shared memory (A/B runs).
+// Consumer warps per CTA at head_dim 128 and their ring depth (8 KB pages): 12 x 2 by
+// default; NF_DEC_STREAM_WARPS (A/B runs) = 13 / 14 / 11 / 10 (x 2 pages), 9 / 8 (x 3), 7 / 6 (x 4).
 int decode_stream_warps() {
   static int w = -1;
   if (w < 0) {
     const char* e = getenv("NF_DEC_STREAM_WARPS");
     w = e ? atoi(e) : 12;
-    if (w != 13 && w != 14) w = 12;
+    if (w != 13 && w != 14 && w != 11 && w != 10 && w != 9 && w != 8 && w != 7 && w != 6) w = 12;
   }
   return w;
 }
@@ -267,14 +310,30 @@ cudaError_t launch_decode_attention_stream(const CUtensorMap& page_map, const At
   const int W = decode_stream_warps();
   const int grid = decode_grid(n_items, sm_budget, W);
   if (a.hd == 128) {
-    if (W == 13) return launch_stream_hdw<128, 13>(page_map, a2, items, n_items, grid, st);
-    if (W == 14) return launch_stream_hdw<128, 14>(page_map, a2, items, n_items, grid, st);
-    return launch_stream_hdw<128, 12>(page_map, a2, items, n_items, grid, st);
+    const int v = decode_stream_var();
+    switch (W * 4 + v) {
+      case 12 * 4 + 1: return launch_stream_hdw<128, 12, 2, 4, false>(page_map, a2, items, n_items, grid, st);
+      case 12 * 4 + 2: return launch_stream_hdw<128, 12, 2, 2, true>(page_map, a2, items, n_items, grid, st);
+      case 12 * 4 + 3: return launch_stream_hdw<128, 12, 2, 4, true>(page_map, a2, items, n_items, grid, st);
+      case 8 * 4 + 2: return launch_stream_hdw<128, 8, 3, 2, true>(page_map, a2, items, n_items, grid, st);
+      case 8 * 4 + 3: return launch_stream_hdw<128, 8, 3, 4, true>(page_map, a2, items, n_items, grid, st);
+      case 8 * 4 + 1: return launch_stream_hdw<128, 8, 3, 4, false>(page_map, a2, items, n_items, grid, st);
+      case 11 * 4: return launch_stream_hdw<128, 11, 2>(page_map, a2, items, n_items, grid, st);
+      case 10 * 4: return launch_stream_hdw<128, 10, 2>(page_map, a2, items, n_items, grid, st);
+      case 13 * 4: return launch_stream_hdw<128, 13, 2>(page_map, a2, items, n_items, grid, st);
+      case 14 * 4: return launch_stream_hdw<128, 14, 2>(page_map, a2, items, n_items, grid, st);
+      case 9 * 4: return launch_stream_hdw<128, 9, 3>(page_map, a2, items, n_items, grid, st);
+      case 8 * 4: return launch_stream_hdw<128, 8, 3>(page_map, a2, items, n_items, grid, st);
+      case 7 * 4: return launch_stream_hdw<128, 7, 4>(page_map, a2, items, n_items, grid, st);
+      case 6 * 4: return launch_stream_hdw<128, 6, 4>(page_map, a2, items, n_items, grid, st);
+      case 12 * 4: return launch_stream_hdw<128, 12, 2>(page_map, a2, items, n_items, grid, st);
+      default: return cudaErrorInvalidValue;  // (dev) warps / variant combination not instantiated
+    }
   }
-  return launch_stream_hdw<64, 12>(page_map, a2, items, n_items, grid, st);
+  return launch_stream_hdw<64, 12, 4>(page_map, a2, items, n_items, grid, st);
 }
 
 // One kernel of this translation unit (preload_all_kernels: its module is loaded eagerly).
-const void* kernel_anchor_decode_stream() { return reinterpret_cast<const void*>(decode_stream_kernel<128, 12>); }
+const void* kernel_anchor_decode_stream() { return reinterpret_cast<const void*>(decode_stream_kernel<128, 12, 2>); }
 
 }  // namespace nf
