@@ -358,6 +358,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int q = 0; q < BN * 2 / 128; ++q)
           if (nb * BN + q * 64 < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + q * 128));
       }
+      // the row's scale (folded RMSNorm 1/rms from the previous kernel's D/128 sum-of-squares
+      // partials, 4 independent accumulators in a fixed order so every n-tile of a row gets the
+      // identical scale) while the tile's mainloop still runs: its dependent loads are off the
+      // epilogue's critical path (split-K contributors store raw partials and need none)
+      float s = 1.f;
+      if (kb0 == 0 && valid) {
+        if (args.norm_part != nullptr)
+          s = rms_row_scale(args.norm_part + r, args.norm_stride, args.norm_nparts, args.inv_d, args.eps);
+        if (args.row_scale != nullptr) s *= args.row_scale[r];
+      }
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + as * BN + ((uint32_t)(ew * 32) << 16);
@@ -427,14 +437,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] *= sc;
       };
-      float s = 1.f;
-      if (args.norm_part != nullptr && valid) {
-        // folded RMSNorm 1/rms from the previous kernel's D/128 sum-of-squares partials:
-        // 4 independent accumulators (a serial chain of dependent loads was exposed on
-        // sub-wave GEMMs), fixed order so every n-tile of a row gets the identical scale
-        s = rms_row_scale(args.norm_part + r, args.norm_stride, args.norm_nparts, args.inv_d, args.eps);
-      }
-      if (args.row_scale != nullptr && valid) s *= args.row_scale[r];
       const int n0 = nb * BN;
       float v[32];
       switch (args.epi) {
