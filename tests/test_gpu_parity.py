@@ -384,6 +384,12 @@ def test_model_step_vs_oracle(env):
         sure = gap > 0.1
         assert sure.sum() >= len(gap) // 2
         assert np.array_equal(ids[sure], ids_ref[sure]), (mode, shares, bal)
+        # every emitted row's logits (not only the clear argmax rows) within tolerance of the
+        # oracle's, through nf_model_step_ex on a fresh copy of the KV pools
+        ids2, lg, _ = model.step_inspect(plan, [dev(p) for p in pools], nb, tok_d, ws, hidden=False)
+        assert np.array_equal(ids2.cpu().numpy(), ids), (mode, shares, bal)
+        assert host(lg).shape == logits.shape
+        assert_close(host(lg), logits, max_abs=0.25, what=f"C1 model-step logits {mode} {shares} {bal} {col}")
 
 
 def test_model_step_emit_mask(env):
