@@ -239,6 +239,9 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+NVLINK_BUS_GBS = 725.0   # B200_PROFILING.md: measured 8-rank all-reduce bus bandwidth at 1 GiB
+
+
 def bench_config(config, shape, tp, b_dense):
     """The `config` object of both arms (identical for the same workload)."""
     return {"workload": workload_desc(config, shape.n_layers, tp=tp, b_dense=b_dense), "b_dense": b_dense,
@@ -356,6 +359,10 @@ def run_nf(args, rank, world, local_rank):
         plan = nf.Plan.explicit(cfg, nf.SEQUENTIAL, sm=sm, graph=not args.no_graph)
     if loop:
         comm = nf.comm_create_loopback(tp, 0)
+        if args.net_model == "nvlink":
+            # link-time model (not a measurement): every collective lasts >= its ring bytes per
+            # GPU / 725 GB/s, the 8-rank all-reduce bus bandwidth B200_PROFILING.md measured at 1 GiB
+            nf.comm_loopback_set_link(comm, NVLINK_BUS_GBS)
     elif tp > 1:
         uid = [nf.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -711,6 +718,10 @@ def run_nf(args, rank, world, local_rank):
 
     optimal = peaks["bf16_tflops"] * 1e12 / (2 * p_active(shape))
     cfg_line = bench_config(args.config, shape, tp, T)
+    if loop and args.net_model == "nvlink":
+        cfg_line["net_model"] = (f"modeled: each loopback collective lasts >= ring bytes per GPU / {NVLINK_BUS_GBS:g} GB/s "
+                                 f"(measured 8-rank all-reduce bus bandwidth at 1 GiB, B200_PROFILING.md); NVLink "
+                                 f"itself not measured")
     plan_line = {"mode": args.mode, "colocate": bool(plan.spec().colocate),
                  "parallelism": (f"tp{tp}" if tp > 1 else ("replicas" if world > 1 else "single-gpu")),
                  "sm": list(plan.spec().sm), "shares": list(plan.spec().share)[:plan.spec().n_nano],
@@ -795,6 +806,8 @@ def main():
                     help="default: c2 at N=1, c3 at N>1.  c2: configs[1] 8B 1 GPU (replicas for N>1); c3: configs[2] "
                          "70B TP=N over NCCL (the metric's config); c3rank: 1-GPU proxy of one TP8 rank; "
                          "c4: configs[3] Mixtral-8x7B TP=N; c4rank: its 1-GPU TP8-rank proxy")
+    ap.add_argument("--net-model", default="", choices=["", "nvlink"],
+                    help="c3loop only: model the collectives' link time (ring bytes / 725 GB/s) on the loopback rank")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
     ap.add_argument("--fused-ar", action="store_true",
                     help="TP: fuse the row-parallel GEMMs with their AllReduce over peer memory (NEXT-3)")

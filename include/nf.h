@@ -190,6 +190,14 @@ nf_status nf_comm_create_local(int32_t tp_size, int32_t ar_mode, nf_comm** comms
  * slot; AllReduce: a local copy, values unchanged) -- the rank's compute, pipeline and
  * local copy traffic without peers.  Results are NOT the model's (no reduction). */
 nf_status nf_comm_create_loopback(int32_t tp_size, int32_t tp_rank, nf_comm** out);
+/* Link-time model for a loopback communicator (bench --config c3loop --net-model nvlink): every
+ * collective lasts at least the bytes a ring moves per GPU divided by link_gbs (GB/s).  An
+ * AllGather of N slots of S bytes moves (N-1) S; an AllReduce of B bytes moves 2 (N-1)/N B.
+ * The local copy runs first; one thread per block then holds until that time has passed since
+ * the copy kernel started, on the collective's stream.  This models the link's duration; it
+ * is not a measurement of NVLink.  link_gbs = 0 (the default) turns the model off.
+ * NF_EINVAL if comm is not a loopback communicator, or if link_gbs is negative or > 1e6. */
+nf_status nf_comm_loopback_set_link(nf_comm* comm, double link_gbs);
 void nf_comm_destroy(nf_comm* comm);
 
 /* ---- Fused collectives over peer memory (PAPER.md:628 used

@@ -18,6 +18,7 @@
 #include "host.h"
 #include "misc.cuh"
 #include "peer.cuh"
+#include "profile.h"
 
 namespace nf {
 // Single-process, single-GPU emulation of a TP group (tests / rank-local
@@ -61,6 +62,7 @@ struct nf_comm {
   int max_ctas = 0;                        // NCCL CTA cap (0 = NCCL default)
   int ar_mode = NF_AR_F32;                 // emulated AllReduce arithmetic
   bool loopback = false;                   // nf_comm_create_loopback: one rank, local copies
+  double link_gbs = 0.0;                   // loopback link-time model (nf_comm_loopback_set_link), 0 = off
   std::shared_ptr<nf::LocalGroup> group;  // emulated group (nf_comm_create_local)
   // fused collectives (peer.cuh): this rank's symmetric buffer, every rank's mapping of theirs
   uint8_t* sym = nullptr;
@@ -132,15 +134,48 @@ uint8_t* const* comm_peer_bases(const nf_comm* c) { return c->sym_peer_dev; }
 uint8_t* comm_sym_local(const nf_comm* c) { return c->sym; }
 long long comm_peer_timeout_ns(const nf_comm* c) { return c->timeout_ns; }
 
-// recv = [rank 0's send | rank 1's send | ...] (count bf16 elements each)
-nf_status comm_all_gather(nf_comm* c, const void* send, void* recv, size_t count_bf16, cudaStream_t st) {
-  if (c->loopback) {  // this rank's buffer into every slot: the AllGather's bytes, no peers
-    for (int q = 0; q < c->tp_size; ++q)
-      if (cudaMemcpyAsync((char*)recv + q * count_bf16 * 2, send, count_bf16 * 2, cudaMemcpyDeviceToDevice, st) !=
-          cudaSuccess)
-        return set_error(NF_ECUDA, "loopback AG copy");
+namespace {
+// Loopback link-time model: copy src into `reps` slots of dst (the collective's local HBM
+// traffic), then hold until t_ns after the kernel started -- a ring collective over a link of
+// the modeled bandwidth ends no earlier (nf_comm_loopback_set_link).
+__global__ void paced_copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, size_t n16, int reps,
+                                  size_t stride16, unsigned long long t_ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int q = 0; q < reps; ++q)
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+      dst[q * stride16 + i] = src[i];
+  if (threadIdx.x == 0) {
+    do {
+      __nanosleep(256);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < t_ns);
+  }
+}
+}  // namespace
+
+// loopback collective: `reps` copies of `bytes` from src to dst (slot stride `bytes`), lasting at
+// least link_bytes / link_gbs when the link model is on
+nf_status loopback_copy(nf_comm* c, const void* src, void* dst, size_t bytes, int reps, double link_bytes,
+                        cudaStream_t st) {
+  if (c->link_gbs > 0.0 && bytes % 16 == 0 && ((uintptr_t)src | (uintptr_t)dst) % 16 == 0) {
+    const unsigned long long t_ns = (unsigned long long)(link_bytes / c->link_gbs);  // bytes / (GB/s) = ns
+    paced_copy_kernel<<<32, 256, 0, st>>>((const uint4*)src, (uint4*)dst, bytes / 16, reps, bytes / 16, t_ns);
+    count_launch();
+    if (cudaGetLastError() != cudaSuccess) return set_error(NF_ECUDA, "loopback paced copy");
     return NF_OK;
   }
+  for (int q = 0; q < reps; ++q)
+    if (cudaMemcpyAsync((char*)dst + q * bytes, src, bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return set_error(NF_ECUDA, "loopback copy");
+  return NF_OK;
+}
+
+// recv = [rank 0's send | rank 1's send | ...] (count bf16 elements each)
+nf_status comm_all_gather(nf_comm* c, const void* send, void* recv, size_t count_bf16, cudaStream_t st) {
+  if (c->loopback)  // this rank's buffer into every slot: the AllGather's bytes, no peers (a ring
+                    // AllGather receives N-1 slots per GPU)
+    return loopback_copy(c, send, recv, count_bf16 * 2, c->tp_size, (double)(c->tp_size - 1) * count_bf16 * 2, st);
   if (c->group) {
     LocalGroup& g = *c->group;
     const int r = c->tp_rank;
@@ -167,11 +202,9 @@ nf_status comm_all_gather(nf_comm* c, const void* send, void* recv, size_t count
 
 // in-place sum over ranks; scratch: count bf16 elements of device memory (emulation only)
 nf_status comm_all_reduce_bf16(nf_comm* c, void* buf, size_t count, cudaStream_t st, void* scratch) {
-  if (c->loopback) {  // a read + write of the buffer (the reduction's local traffic), values unchanged
-    if (cudaMemcpyAsync(scratch, buf, count * 2, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-      return set_error(NF_ECUDA, "loopback AR copy");
-    return NF_OK;
-  }
+  if (c->loopback)  // a read + write of the buffer (the reduction's local traffic), values unchanged
+                    // (a ring AllReduce sends 2 (N-1) / N of the buffer per GPU)
+    return loopback_copy(c, buf, scratch, count * 2, 1, 2.0 * (c->tp_size - 1) / c->tp_size * count * 2, st);
   if (c->group) {
     LocalGroup& g = *c->group;
     const int r = c->tp_rank;
@@ -262,6 +295,13 @@ nf_status nf_comm_create_loopback(int32_t tp_size, int32_t tp_rank, nf_comm** ou
   c->tp_rank = tp_rank;
   c->loopback = true;
   *out = c;
+  return NF_OK;
+}
+
+nf_status nf_comm_loopback_set_link(nf_comm* comm, double link_gbs) {
+  if (!comm || !comm->loopback) return set_error(NF_EINVAL, "not a loopback communicator");
+  if (!(link_gbs >= 0.0) || link_gbs > 1e6) return set_error(NF_EINVAL, "link_gbs %g out of range", link_gbs);
+  comm->link_gbs = link_gbs;
   return NF_OK;
 }
 

@@ -100,6 +100,7 @@ _sig("nf_comm_destroy", None, C.c_void_p)
 _sig("nf_comm_create_local", C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_void_p))
 AR_F32, AR_RING = 0, 1
 _sig("nf_comm_create_loopback", C.c_int, C.c_int32, C.c_int32, C.POINTER(C.c_void_p))
+_sig("nf_comm_loopback_set_link", C.c_int, C.c_void_p, C.c_double)
 _sig("nf_comm_sym_bytes", C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_size_t))
 _sig("nf_comm_sym_alloc", C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p)
 _sig("nf_comm_sym_open", C.c_int, C.c_void_p, C.c_void_p)
@@ -176,7 +177,7 @@ PROF_NAMES = ["kqv", "decode_attn", "prefill_attn", "o_proj", "up_gate", "down",
 
 EXPORTED = ["nf_plan_runtime_note", "nf_plan_probe_partitions", "nf_comm_create_local", "nf_gemm_workspace_bytes", "nf_profile_timeline", "nf_profile_tag", "nf_kernel_launches", "nf_profile_enable", "nf_profile_read", "nf_last_error", "nf_abi_version", "nf_batch_metadata", "nf_snap_cuts", "nf_plan_create_explicit",
             "nf_plan_create", "nf_plan_get_spec", "nf_plan_export_csv", "nf_plan_destroy", "nf_plan_hash", "nf_comm_unique_id",
-            "nf_comm_create", "nf_comm_destroy", "nf_comm_create_loopback", "nf_comm_sym_bytes", "nf_comm_sym_alloc",
+            "nf_comm_create", "nf_comm_destroy", "nf_comm_create_loopback", "nf_comm_loopback_set_link", "nf_comm_sym_bytes", "nf_comm_sym_alloc",
             "nf_comm_sym_open", "nf_comm_set_fused", "nf_comm_sym_status", "nf_packed_layer_bytes", "nf_pack_layer", "nf_pack_lm_head",
             "nf_workspace_size", "nf_layer_forward", "nf_model_step", "nf_model_step_ex", "nf_gemm_bf16", "nf_attention",
             "nf_moe_rows_cap", "nf_moe_route_ws_bytes", "nf_moe_route", "nf_moe_last_ids", "nf_sched_create", "nf_sched_submit",
@@ -451,6 +452,11 @@ def comm_create_loopback(tp_size: int, tp_rank: int = 0) -> int:
     h = C.c_void_p()
     _check(lib.nf_comm_create_loopback(tp_size, tp_rank, C.byref(h)))
     return h.value
+
+
+def comm_loopback_set_link(comm: int, link_gbs: float):
+    """Link-time model of a loopback communicator (0 = off): collectives last >= ring bytes / link_gbs."""
+    _check(lib.nf_comm_loopback_set_link(C.c_void_p(comm), float(link_gbs)))
 
 
 def comm_destroy(h: int):

@@ -185,7 +185,17 @@ def test_tp_plan_and_comm_validation(nf):
         nf.comm_create_local(9)
     h = nf.comm_create_loopback(8, 3)
     assert h
+    nf.comm_loopback_set_link(h, 725.0)   # link-time model on / off
+    nf.comm_loopback_set_link(h, 0.0)
+    for bad in (-1.0, float("nan"), 1e7):
+        with pytest.raises(nf.NFError):
+            nf.comm_loopback_set_link(h, bad)
     nf.comm_destroy(h)
+    g = nf.comm_create_local(2)
+    with pytest.raises(nf.NFError):   # only a loopback communicator has a link model
+        nf.comm_loopback_set_link(g[0], 725.0)
+    for c in g:
+        nf.comm_destroy(c)
     with pytest.raises(nf.NFError):
         nf.comm_create_loopback(8, 8)
     # vocab-parallel head: V % N and (V/N) % 32
