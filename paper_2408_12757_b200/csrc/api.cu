@@ -1246,6 +1246,11 @@ nf_status run_peer_reduce(const LayerCtx& L, int site, int M) {
   return NF_OK;
 }
 
+int gemm_aslots_env() {  // read per launch (tests switch it at run time)
+  const char* e = getenv("NF_GEMM_ASLOTS");
+  return !(e && e[0] == '0');
+}
+
 // Front of a group: KQV of each of its attention nano-batches, decode attention on
 // the memory stream as soon as that KQV lands, prefill attention on the compute stream.
 nf_status tp_front(nf_plan* p, const LayerCtx& L, int gi, const Group& G, const __nv_bfloat16* x, const float* part,
@@ -1302,8 +1307,15 @@ nf_status tp_stage_b(nf_plan* p, const LayerCtx& L, int gi, const Group& G, cons
   __nv_bfloat16* h1 = L.w->h1 + G.nr.t0 * D;
   if (G.col) {
     if (L.ns != L.cs) NF_CUDA(cudaStreamWaitEvent(L.cs, p->ev_agattn, 0));
-    NF_CUDA(launch_interleave(L.w->ag, N, M, (int)qd, L.w->ocat, nullptr, L.cs));
+    // the gathered attention output [N][M][qd] is the GEMM's A in slot layout (a 3-D TMA box per
+    // k-block); NF_GEMM_ASLOTS=0 restores the interleave pass into [M][N qd] (A/B runs)
+    const bool aslots = gemm_aslots_env() && qd % 64 == 0;
+    if (!aslots) NF_CUDA(launch_interleave(L.w->ag, N, M, (int)qd, L.w->ocat, nullptr, L.cs));
     GemmArgs a{};
+    if (aslots) {
+      a.a_slots = N;
+      a.a_slot_w = (int)qd;
+    }
     a.epi = EPI_RESID;
     a.stages = stages;
     a.sk_part = L.w->sk_part;
@@ -1321,8 +1333,8 @@ nf_status tp_stage_b(nf_plan* p, const LayerCtx& L, int gi, const Group& G, cons
     if (fz) set_peer_ag_args(&a, L, M);  // all-gather fused into the epilogue (NEXT-3)
     {
       ProfScope ps(NF_OP_O, L.cs);
-      NF_CUDA(launch_gemm(L.w->ocat, qd_full, (const __nv_bfloat16*)wt->w_o, qd_full, a,
-                          clamp_dense(L, L.p->spec.sm[NF_OP_O]), L.cs));
+      NF_CUDA(launch_gemm(aslots ? L.w->ag : L.w->ocat, aslots ? qd : qd_full, (const __nv_bfloat16*)wt->w_o, qd_full,
+                          a, clamp_dense(L, L.p->spec.sm[NF_OP_O]), L.cs));
     }
     if (fz) {
       comm_fused_site_barrier(L.comm);

@@ -286,7 +286,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                             b_policy);
           } else {
             mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-            tma_load_2d_hint(sA + stage * A_STAGE_ELEMS, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM, a_policy);
+            if (args.a_slots > 1)  // slot layout: k-block kb lies in slot kb*BK / a_slot_w
+              tma_load_3d(sA + stage * A_STAGE_ELEMS, &tmA, &full[stage], (kb * GEMM_BK) % args.a_slot_w, mb * GEMM_BM,
+                          (kb * GEMM_BK) / args.a_slot_w);
+            else
+              tma_load_2d_hint(sA + stage * A_STAGE_ELEMS, &tmA, &full[stage], kb * GEMM_BK, mb * GEMM_BM, a_policy);
             tma_load_2d(sB + stage * B_STAGE_ELEMS, &tmB, &full[stage], kb * GEMM_BK, nb * BN + b_row0);
           }
           if (++stage == GEMM_STAGES) { stage = 0; phase ^= 1; }
@@ -742,6 +746,21 @@ cudaError_t make_tmap_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Slot-layout A (GemmArgs::a_slots): dims (slot width, rows, slots), box (box_inner, box_rows, 1)
+cudaError_t make_tmap_slots_bf16(CUtensorMap* m, const void* ptr, uint64_t slot_w, uint64_t rows, uint64_t slots,
+                                 uint32_t box_inner, uint32_t box_rows) {
+  cudaError_t e = get_encode();
+  if (e != cudaSuccess) return e;
+  cuuint64_t dims[3] = {slot_w, rows, slots};
+  cuuint64_t strides[2] = {slot_w * 2, rows * slot_w * 2};
+  cuuint32_t box[3] = {box_inner, box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 // Paged-KV page map: dims (64 cols, rows, half, kv) so one box {64, 16, hd/64, 2} = one page's
 // K and V block of one KV head (hd*16*2*2 bytes) lands as [kv][half][16 rows][128 B], 128B-swizzled.
 cudaError_t make_page_tmap(CUtensorMap* m, const void* pool, int64_t n_pages, int kh, int hd, int page_size) {
@@ -839,10 +858,13 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     best = rounds2;
     choice = 2;
   }
+  const bool aslots = args.a_slots > 1;  // slot-layout A: single-CTA schedules only
+  if (aslots && (args.a_slot_w % GEMM_BK != 0 || (int64_t)args.a_slots * args.a_slot_w != args.K || grouped))
+    return cudaErrorInvalidValue;
   const int pairs = SB / 2;
   const int pair_tiles = ((args.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((args.N + bn - 1) / bn);
   int pair_s = 1;
-  if (!grouped && cg2_env && bn == 256 && !coloc && pairs >= 1) {
+  if (!grouped && !aslots && cg2_env && bn == 256 && !coloc && pairs >= 1) {
     // on a tie the pair kernel measured faster only with a long mainloop and many n-tiles
     // (>= 32 k-blocks, N >= 2048; tools/gemm_micro.py): short-K pairs couple the two CTAs'
     // epilogues through the shared accumulator barrier
@@ -886,7 +908,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   // CTA pairs + stream-K (sub-wave in pair tiles): each CTA fetches half the B bytes per
   // k-block
   int skp_grid = 0;
-  if (!grouped && cg2_env && bn == 256 && tail_env && args.sk_part != nullptr && args.sk_slots >= SB &&
+  if (!grouped && !aslots && cg2_env && bn == 256 && tail_env && args.sk_part != nullptr && args.sk_slots >= SB &&
       pair_tiles < pairs && !coloc && l2_mb <= 64.0) {
     const int64_t U = (int64_t)pair_tiles * num_kb;
     const int G = (int)std::min<int64_t>(pairs, std::max<int64_t>(pair_tiles, U / 16));
@@ -909,7 +931,8 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   if ((choice == 0 && a2.stream_k != 2) || (choice == 3 && pair_s == 1)) a2.sk_part = nullptr;
   if (grid < 1) grid = 1;
   CUtensorMap ta, tb;
-  cudaError_t e = make_tmap_bf16(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
+  cudaError_t e = aslots ? make_tmap_slots_bf16(&ta, A, args.a_slot_w, args.M, args.a_slots, GEMM_BK, GEMM_BM)
+                         : make_tmap_bf16(&ta, A, args.K, args.M, lda, GEMM_BK, GEMM_BM);
   if (e != cudaSuccess) return e;
   const bool pair_kernel = choice == 3 || choice == 5;
   e = make_tmap_bf16(&tb, B, args.K, (uint64_t)args.N * (grouped ? args.n_groups : 1), ldb, GEMM_BK,

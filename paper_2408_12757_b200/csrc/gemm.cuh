@@ -85,6 +85,10 @@ struct GemmArgs {
   // rank's all-gather region [peer_n][M][N] at peer_site_off + peer_result_off instead of `out`,
   // then every rank's site `done` counter grows by the unit's 64-column chunks (release, sys)
   int peer_mode;
+  // A in slot layout (a_slots > 1): A[m][s * a_slot_w + j] is stored at A + (s * M + m) * a_slot_w + j,
+  // the layout an AllGather of a_slots row blocks [M][a_slot_w] leaves (TP: the attention output
+  // feeding the O column-parallel projection); loaded by a 3-D TMA box per k-block, no interleave pass
+  int a_slots, a_slot_w;
 };
 
 // Bytes of stream-K scratch for a GEMM with this many tiles at this grid.
