@@ -158,16 +158,18 @@ __global__ void paced_copy_kernel(const uint4* __restrict__ src, uint4* __restri
 // least link_bytes / link_gbs when the link model is on
 nf_status loopback_copy(nf_comm* c, const void* src, void* dst, size_t bytes, int reps, double link_bytes,
                         cudaStream_t st) {
-  if (c->link_gbs > 0.0 && bytes % 16 == 0 && ((uintptr_t)src | (uintptr_t)dst) % 16 == 0) {
+  const bool paced = c->link_gbs > 0.0;
+  const bool vec = bytes % 16 == 0 && ((uintptr_t)src | (uintptr_t)dst) % 16 == 0;
+  if (!paced || !vec)
+    for (int q = 0; q < reps; ++q)
+      if (cudaMemcpyAsync((char*)dst + q * bytes, src, bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return set_error(NF_ECUDA, "loopback copy");
+  if (paced) {  // (unaligned buffers: the copies above, then the hold alone)
     const unsigned long long t_ns = (unsigned long long)(link_bytes / c->link_gbs);  // bytes / (GB/s) = ns
-    paced_copy_kernel<<<32, 256, 0, st>>>((const uint4*)src, (uint4*)dst, bytes / 16, reps, bytes / 16, t_ns);
+    paced_copy_kernel<<<32, 256, 0, st>>>((const uint4*)src, (uint4*)dst, vec ? bytes / 16 : 0, reps, bytes / 16, t_ns);
     count_launch();
     if (cudaGetLastError() != cudaSuccess) return set_error(NF_ECUDA, "loopback paced copy");
-    return NF_OK;
   }
-  for (int q = 0; q < reps; ++q)
-    if (cudaMemcpyAsync((char*)dst + q * bytes, src, bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-      return set_error(NF_ECUDA, "loopback copy");
   return NF_OK;
 }
 
