@@ -23,6 +23,20 @@ namespace {
 
 constexpr int A_STAGE_ELEMS = GEMM_BM * GEMM_BK;
 
+#ifdef NF_GEMM_TS
+// (dev build, -DNF_GEMM_TS) phase timestamps of CTA 0 of the last GEMM launch (tools/gemm_phases.py)
+__device__ unsigned long long g_gemm_ts[8];
+NF_DEV void gemm_ts(int i) {
+  if (blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gemm_ts[i] = t;
+  }
+}
+#else
+NF_DEV void gemm_ts(int) {}
+#endif
+
 NF_DEV void store32_bf16(__nv_bfloat16* dst, const float (&v)[32]) {
   uint4* d = reinterpret_cast<uint4*>(dst);
 #pragma unroll
@@ -34,6 +48,14 @@ NF_DEV void store32_bf16(__nv_bfloat16* dst, const float (&v)[32]) {
     u.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
     d[q] = u;
   }
+}
+
+// 1-D bulk copy global -> shared memory, completing on an mbarrier (transaction bytes)
+NF_DEV void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
 NF_DEV int ld_acquire_gpu(const int* p) {
@@ -148,6 +170,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   float* inv_freq = reinterpret_cast<float*>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef NF_GEMM_TS
+  if (threadIdx.x == 0 && blockIdx.x == 0) g_gemm_ts[6] = g_gemm_ts[5];  // previous launch's CTA-0 exit
+#endif
+  if (threadIdx.x == 0) gemm_ts(0);  // kernel entry
   const int M = args.M, N = args.N, K = args.K;
   uint32_t rank = 0;  // CTA rank in the pair
   if constexpr (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
@@ -206,30 +232,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // (the tile loop and its three bodies are always inlined: a body the compiler keeps out of
   // line gets its captures through a local-memory closure -- a 328-400 byte stack frame that
   // cost the sub-wave / short-K GEMMs 15-28 %, profiles/r2i_gemm_r1_vs_now.log)
+  // fn(tile, kb0, kb1, last): `last` = no further segment follows on this CTA (its smem stages
+  // are idle once this segment's accumulator is complete)
   auto for_each_seg = [&](auto&& fn) __attribute__((always_inline)) {
     if (sk) {
-      for (int t = wid; t < sk_t0; t += G) fn(t, 0, num_kb);
       const int64_t a = (int64_t)wid * U_sk / G, b = (int64_t)(wid + 1) * U_sk / G;
+      for (int t = wid; t < sk_t0; t += G) fn(t, 0, num_kb, t + G >= sk_t0 && a >= b);
       for (int64_t u = a; u < b;) {
         const int t = (int)(u / num_kb);
         const int k0 = (int)(u - (int64_t)t * num_kb);
         const int k1 = (int)min((int64_t)num_kb, b - (int64_t)t * num_kb);
-        fn(sk_t0 + t, k0, k1);
+        fn(sk_t0 + t, k0, k1, (int64_t)t * num_kb + k1 >= b);
         u = (int64_t)t * num_kb + k1;
       }
       return;
     }
     if (split2) {
       for (int u = wid; u < 2 * tiles; u += G) {
-        if (u & 1) fn(u >> 1, kb_half, num_kb);
-        else fn(u >> 1, 0, kb_half);
+        if (u & 1) fn(u >> 1, kb_half, num_kb, u + G >= 2 * tiles);
+        else fn(u >> 1, 0, kb_half, u + G >= 2 * tiles);
       }
       return;
     }
-    for (int t = wid; t < tiles_dp; t += G) fn(t, 0, num_kb);
+    for (int t = wid; t < tiles_dp; t += G) fn(t, 0, num_kb, t + G >= tiles_dp && wid >= tail_units);
     if (wid < tail_units) {
       const int j = wid % ts;
-      fn(tiles_dp + wid / ts, j * num_kb / ts, (j + 1) * num_kb / ts);
+      fn(tiles_dp + wid / ts, j * num_kb / ts, (j + 1) * num_kb / ts, true);
     }
   };
 
@@ -245,6 +273,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&tempty[a], 4 * CG);  // epilogue warps of both CTAs drain into the even CTA's barrier
     }
     if constexpr (SR) mbar_init(rbar, 1);
+    mbar_init(rbar + 1, 1);  // smem-staged stream-K fix-up
     fence_barrier_init();
   }
   if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
@@ -260,6 +289,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) gemm_ts(1);  // prologue done (barriers, TMEM allocated)
   // everything above (barriers, TMEM, descriptor prefetch) overlaps the previous kernel's
   // tail under PDL; every global read of its outputs and every global write is below
   griddep_wait();
@@ -271,7 +301,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       const uint64_t a_policy = policy_evict_last();  // activations are re-read by every n-tile
       const uint64_t b_policy = policy_evict_normal();
-      for_each_seg([&](int tile, int kb0, int kb1) __attribute__((always_inline)) {
+      for_each_seg([&](int tile, int kb0, int kb1, bool) __attribute__((always_inline)) {
         const int mb = tile % tiles_m, nb = tile / tiles_m;
         const int b_row0 = grouped ? group_of(mb) * N : 0;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -305,12 +335,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       int as = 0;
       uint32_t aphase = 0;
-      for_each_seg([&](int tile, int kb0, int kb1) __attribute__((always_inline)) {
+      bool first_full = true;
+      for_each_seg([&](int tile, int kb0, int kb1, bool) __attribute__((always_inline)) {
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + as * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (first_full) {
+            gemm_ts(2);  // first A/B stage landed
+            first_full = false;
+          }
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(sA + stage * A_STAGE_ELEMS);
           const uint64_t bd = sdesc_sw128(sB + stage * B_STAGE_ELEMS);
@@ -328,19 +363,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         as ^= 1;
         if (as == 0) aphase ^= 1;
       });
+      gemm_ts(3);                   // last MMA issued
       griddep_launch_dependents();  // all MMAs issued: the next kernel may start its prologue
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
     const int ew = warp - 4;
     int as = 0;
-    uint32_t aphase = 0, rphase = 0;
+    uint32_t aphase = 0, rphase = 0, fphase = 0;
+    // smem-staged fix-up (NF_GEMM_SKSMEM=0 disables it for A/B): the stage ring holds one partial
+    const bool sk_smem_ok = args.sk_smem && (uint32_t)GEMM_STAGES * STAGE_BYTES >= (uint32_t)(GEMM_BM * BN * 4);
     const int trow = ew * 32 + lane;  // row within the tile
     const bool leader = ew == 0 && lane == 0;
     if constexpr (SR) {
       if (leader) tma_prefetch_desc(&tmR);
     }
-    for_each_seg([&](int tile, int kb0, int kb1) __attribute__((always_inline)) {
+    for_each_seg([&](int tile, int kb0, int kb1, bool last) __attribute__((always_inline)) {
       const int mb = tile % tiles_m, nb = tile / tiles_m;
       const int r = mb * TM + (int)rank * GEMM_BM + trow;
       const bool valid = grouped ? r < args.grp_end[group_of(mb)] : r < M;
@@ -374,6 +412,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
+      bool fix_smem = false;
       const uint32_t taddr = tmem_base + as * BN + ((uint32_t)(ew * 32) << 16);
       if (kb0 > 0) {
         // split-K contributor: raw fp32 partial tile to its slot, then signal the
@@ -414,12 +453,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         } else {
           n_contrib = sk ? sk_cta_of((int64_t)(tile - sk_t0) * num_kb + num_kb - 1) - wid : ts - 1;
         }
+        // the CTA's last segment: its stage buffers are idle once the accumulator is complete, so
+        // the first contributor's fp32 partial (128 x BN) comes in by one bulk copy and the fix-up
+        // reads it from shared memory (a chain of dependent L2 round trips otherwise)
+        fix_smem = last && sk_smem_ok;
         if (trow == 0) {
           while (ld_acquire_gpu(args.sk_flag + tile * CG + (int)rank) < n_contrib) __nanosleep(32);
           args.sk_flag[tile * CG + (int)rank] = 0;  // self-reset for the next launch
+          if (fix_smem) {
+            const size_t cs = split2 ? (size_t)c_first : (size_t)(c_first * CG + (int)rank);
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy partial stores -> bulk copy
+            mbar_arrive_expect_tx(rbar + 1, (uint32_t)(GEMM_BM * BN * 4));
+            bulk_load_1d(smem, args.sk_part + cs * GEMM_BM * GEMM_SK_LD, (uint32_t)(GEMM_BM * BN * 4), rbar + 1);
+          }
         }
         named_bar_sync(1, 128);
         (void)ld_acquire_gpu(args.sk_flag + tile * CG + (int)rank);
+        if (fix_smem) {
+          mbar_wait(rbar + 1, fphase);
+          fphase ^= 1;
+        }
       }
       // accumulator + contributors' partials (fixed CTA order), times the row scale
       auto ldacc = [&](int col, float sc, float (&v)[32]) __attribute__((always_inline)) {
@@ -428,7 +481,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(rr[j]);
-        for (int c = c_first; c < c_first + n_contrib; ++c) {
+        int c = c_first;
+        if (fix_smem) {  // first contributor from shared memory (same float4[BN/4][128] layout)
+          const uint32_t sp = smem_u32(smem) + (uint32_t)(((col / 4) * GEMM_BM + trow) * 16);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float f0, f1, f2, f3;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(f0), "=f"(f1), "=f"(f2), "=f"(f3)
+                         : "r"(sp + q * GEMM_BM * 16));
+            v[4 * q] += f0; v[4 * q + 1] += f1; v[4 * q + 2] += f2; v[4 * q + 3] += f3;
+          }
+          ++c;
+        }
+        for (; c < c_first + n_contrib; ++c) {
           const size_t cs = split2 ? (size_t)c : (size_t)(c * CG + (int)rank);
           const float4* src = reinterpret_cast<const float4*>(args.sk_part + cs * GEMM_BM * GEMM_SK_LD) + trow +
                               (col / 4) * GEMM_BM;
@@ -702,6 +768,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (as == 0) aphase ^= 1;
     });
   }
+  if (warp == 4 && lane == 0) gemm_ts(4);  // epilogue done
   if constexpr (SR) {
     if (warp == 4 && lane == 0) bulk_wait0();  // the last tile's stores are complete
   }
@@ -711,6 +778,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_after();
     if constexpr (CG == 2) tmem_dealloc_cg2(tmem_base, TMEM_COLS);
     else tmem_dealloc(tmem_base, TMEM_COLS);
+    if (lane == 0) gemm_ts(5);  // teardown done
   }
 }
 
@@ -921,6 +989,16 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
       skp_grid = G;
     }
   }
+  static int sks_env = -1;
+  if (sks_env < 0) {
+    // (dev) NF_GEMM_SKSMEM=1: the owner of a split tile stages its first contributor's partial in the
+    // idle stage ring (one bulk copy) instead of reading it chunk by chunk from L2.  Off by default:
+    // shape-dependent, +13 % on the 70B-rank O_col, -7 % on the 70B-rank Up/Gate at M 1024
+    // (profiles/r2l_sksmem_*.log)
+    const char* e2 = getenv("NF_GEMM_SKSMEM");
+    sks_env = e2 ? atoi(e2) : 0;
+  }
+  a2.sk_smem = sks_env;
   a2.stream_k = (choice == 4 || choice == 5) ? 1 : 0;
   if (grouped && tail_env && args.sk_part != nullptr && args.sk_slots >= SB && !coloc) a2.stream_k = 2;
   a2.split = choice == 2 ? 2 : 1;
@@ -1031,6 +1109,12 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
+
+#ifdef NF_GEMM_TS
+extern "C" int nf_debug_gemm_ts(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_gemm_ts, sizeof(g_gemm_ts));
+}
+#endif
 
 // One kernel of this translation unit (preload_all_kernels: its module is loaded eagerly).
 const void* kernel_anchor_gemm() { return reinterpret_cast<const void*>(gemm_tcgen05_kernel<4, 256, 1>); }

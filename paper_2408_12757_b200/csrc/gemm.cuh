@@ -89,6 +89,7 @@ struct GemmArgs {
   // the layout an AllGather of a_slots row blocks [M][a_slot_w] leaves (TP: the attention output
   // feeding the O column-parallel projection); loaded by a 3-D TMA box per k-block, no interleave pass
   int a_slots, a_slot_w;
+  int sk_smem;          // set by the launcher: the owner of a split tile stages a partial in smem
 };
 
 // Bytes of stream-K scratch for a GEMM with this many tiles at this grid.
