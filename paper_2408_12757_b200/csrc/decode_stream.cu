@@ -49,7 +49,7 @@ NF_DEV int ld_uniform(const int* p) {  // every lane loads the same word (one tr
   return v;
 }
 
-template <int HD, int W, int NS, int CH = 2, bool LA = false>
+template <int HD, int W, int NS, int CH = 2, int LA = 0>
 // (registers: the warps of an SM sub-partition share its 16 K registers, ceil(W / 4) warps each)
 __global__ void __maxnreg__((512 / ((W + 3) / 4) / 8 * 8) < 255 ? (512 / ((W + 3) / 4) / 8 * 8) : 255)
     decode_stream_kernel(const __grid_constant__ CUtensorMap pages, const AttnArgs a,
@@ -140,6 +140,37 @@ __global__ void __maxnreg__((512 / ((W + 3) / 4) / 8 * 8) < 255 ? (512 / ((W + 3
       else sc[e] = sa[0][e] + sa[1][e];
     }
   };
+  // LA 2 halves of load_page: S^T of page jj (slot waited, K fragments, CH chains) ...
+  auto s_only = [&](uint32_t jj, float (&sc)[4]) __attribute__((always_inline)) {
+    const uint32_t s = jj % NS;
+    mbar_wait(&bars[s], (jj / NS) & 1);
+    const uint32_t base = ring + s * SB;
+    float sa[CH][4];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) sa[c][0] = sa[c][1] = sa[c][2] = sa[c][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      uint32_t kf[4];
+      ldmatrix_x4(kf, base + offK[ks & 3] + (ks >> 2) * DS_BOX);
+      mma_bf16_16816(sa[ks % CH], kf, qb[ks]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if constexpr (CH == 4) sc[e] = (sa[0][e] + sa[1][e]) + (sa[2][e] + sa[3][e]);
+      else sc[e] = sa[0][e] + sa[1][e];
+    }
+  };
+  // ... and its V^T fragments, then the slot's refill with the page NS ahead
+  auto v_only = [&](uint32_t jj, uint32_t (&vf)[KS][4]) __attribute__((always_inline)) {
+    const uint32_t base = ring + (jj % NS) * SB;
+#pragma unroll
+    for (int mt = 0; mt < KS; ++mt) ldmatrix_x4_trans(vf[mt], base + offV[mt & 3] + (mt >> 2) * DS_BOX);
+    __syncwarp();
+    if ((int)jj + NS < n_pg) {
+      issue(jj + NS, nrow);
+      if ((int)jj + NS + 1 < n_pg) nrow = ld_uniform(rows + jj + NS + 1);
+    }
+  };
   // Softmax of one page's scores and its P.V contribution (page p of an item with np pages).
   auto consume = [&](int p, int np, int kv_len, float (&sc)[4], uint32_t (&vf)[KS][4], float& m0, float& m1,
                      float& thr0, float& thr1, float (&oacc)[KS][4], float (&lacc)[4]) __attribute__((always_inline)) {
@@ -214,7 +245,26 @@ __global__ void __maxnreg__((512 / ((W + 3) / 4) / 8 * 8) < 255 ? (512 / ((W + 3
     for (int d = 0; d < KS; ++d) oacc[d][0] = oacc[d][1] = oacc[d][2] = oacc[d][3] = 0.f;
 
     const int np = (it.kv_len + 15) >> 4;
-    if constexpr (!LA) {
+    if constexpr (LA == 2) {
+      // S^T look-ahead: page p+1's K fragments and S^T MMAs are issued before page p's softmax
+      // and P.V (independent chains in one warp's instruction stream); page p+1's V fragments
+      // come in after page p's P.V, reusing page p's registers (one V set: 3 warps per SM
+      // sub-partition still fit)
+      float sc[4];
+      uint32_t vf[KS][4];
+      load_page(j, sc, vf);
+      for (int p = 0; p < np; ++p, ++j) {
+        float sn[4];
+        const bool more = p + 1 < np;
+        if (more) s_only(j + 1, sn);
+        consume(p, np, it.kv_len, sc, vf, m0, m1, thr0, thr1, oacc, lacc);
+        if (more) {
+          v_only(j + 1, vf);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sc[e] = sn[e];
+        }
+      }
+    } else if constexpr (LA == 0) {
       for (int p = 0; p < np; ++p, ++j) {
         float sc[4];
         uint32_t vf[KS][4];
@@ -255,7 +305,7 @@ __global__ void __maxnreg__((512 / ((W + 3) / 4) / 8 * 8) < 255 ? (512 / ((W + 3
   }
 }
 
-template <int HD, int W, int NS, int CH = 2, bool LA = false>
+template <int HD, int W, int NS, int CH = 2, int LA = 0>
 cudaError_t launch_stream_hdw(const CUtensorMap& pm, const AttnArgs& a, const DecodeItem* items, int n_items,
                               int grid, cudaStream_t st) {
   static_assert(ds_smem<HD, W, NS>() <= 232448, "shared memory");
@@ -271,13 +321,14 @@ cudaError_t launch_stream_hdw(const CUtensorMap& pm, const AttnArgs& a, const De
   return cudaGetLastError();
 }
 
-// (dev) NF_DEC_STREAM_VAR: 1 = four S^T chains, 2 = look-ahead, 3 = both (A/B runs)
+// (dev) NF_DEC_STREAM_VAR: 1 = four S^T chains, 2 = page look-ahead (two V register sets), 3 = both,
+// 4 / 5 = S^T look-ahead with one V register set (two / four chains) (A/B runs)
 int decode_stream_var() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("NF_DEC_STREAM_VAR");
     v = e ? atoi(e) : 0;
-    if (v < 0 || v > 3) v = 0;
+    if (v < 0 || v > 5) v = 0;
   }
   return v;
 }
@@ -311,13 +362,20 @@ cudaError_t launch_decode_attention_stream(const CUtensorMap& page_map, const At
   const int grid = decode_grid(n_items, sm_budget, W);
   if (a.hd == 128) {
     const int v = decode_stream_var();
+    if (v >= 4) {  // S^T look-ahead (4: two chains, 5: four chains)
+      if (W == 12) return v == 4 ? launch_stream_hdw<128, 12, 2, 2, 2>(page_map, a2, items, n_items, grid, st)
+                                 : launch_stream_hdw<128, 12, 2, 4, 2>(page_map, a2, items, n_items, grid, st);
+      if (W == 8) return v == 4 ? launch_stream_hdw<128, 8, 3, 2, 2>(page_map, a2, items, n_items, grid, st)
+                                : launch_stream_hdw<128, 8, 3, 4, 2>(page_map, a2, items, n_items, grid, st);
+      return cudaErrorInvalidValue;
+    }
     switch (W * 4 + v) {
-      case 12 * 4 + 1: return launch_stream_hdw<128, 12, 2, 4, false>(page_map, a2, items, n_items, grid, st);
-      case 12 * 4 + 2: return launch_stream_hdw<128, 12, 2, 2, true>(page_map, a2, items, n_items, grid, st);
-      case 12 * 4 + 3: return launch_stream_hdw<128, 12, 2, 4, true>(page_map, a2, items, n_items, grid, st);
-      case 8 * 4 + 2: return launch_stream_hdw<128, 8, 3, 2, true>(page_map, a2, items, n_items, grid, st);
-      case 8 * 4 + 3: return launch_stream_hdw<128, 8, 3, 4, true>(page_map, a2, items, n_items, grid, st);
-      case 8 * 4 + 1: return launch_stream_hdw<128, 8, 3, 4, false>(page_map, a2, items, n_items, grid, st);
+      case 12 * 4 + 1: return launch_stream_hdw<128, 12, 2, 4, 0>(page_map, a2, items, n_items, grid, st);
+      case 12 * 4 + 2: return launch_stream_hdw<128, 12, 2, 2, 1>(page_map, a2, items, n_items, grid, st);
+      case 12 * 4 + 3: return launch_stream_hdw<128, 12, 2, 4, 1>(page_map, a2, items, n_items, grid, st);
+      case 8 * 4 + 2: return launch_stream_hdw<128, 8, 3, 2, 1>(page_map, a2, items, n_items, grid, st);
+      case 8 * 4 + 3: return launch_stream_hdw<128, 8, 3, 4, 1>(page_map, a2, items, n_items, grid, st);
+      case 8 * 4 + 1: return launch_stream_hdw<128, 8, 3, 4, 0>(page_map, a2, items, n_items, grid, st);
       case 11 * 4: return launch_stream_hdw<128, 11, 2>(page_map, a2, items, n_items, grid, st);
       case 10 * 4: return launch_stream_hdw<128, 10, 2>(page_map, a2, items, n_items, grid, st);
       case 13 * 4: return launch_stream_hdw<128, 13, 2>(page_map, a2, items, n_items, grid, st);
