@@ -583,7 +583,7 @@ void nf_plan_destroy(nf_plan* p) {
   for (int k = 0; k < NF_MAX_NANO; ++k)
     for (cudaEvent_t e : {p->ev_pre[k], p->ev_o[k], p->ev_aro[k], p->ev_d[k], p->ev_ard[k]})
       if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {p->ev_agattn, p->ev_ago, p->ev_join_n, p->ev_fork, p->ev_join_c, p->ev_join_m, p->ev_fork2,
+  for (cudaEvent_t e : {p->ev_agattn, p->ev_ago, p->ev_join_n, p->ev_fork, p->ev_join_c, p->ev_join_m, p->ev_join_m2, p->ev_fork2,
                         p->ev_join_c2})
     if (e) cudaEventDestroy(e);
   if (p->cs2) cudaStreamDestroy(p->cs2);
@@ -619,6 +619,7 @@ nf_status ensure_runtime(nf_plan* p) {
   NF_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
   NF_CUDA(cudaEventCreateWithFlags(&p->ev_join_c, cudaEventDisableTiming));
   NF_CUDA(cudaEventCreateWithFlags(&p->ev_join_m, cudaEventDisableTiming));
+  NF_CUDA(cudaEventCreateWithFlags(&p->ev_join_m2, cudaEventDisableTiming));
   NF_CUDA(cudaEventCreateWithFlags(&p->ev_c2n, cudaEventDisableTiming));
   NF_CUDA(cudaEventCreateWithFlags(&p->ev_n2c, cudaEventDisableTiming));
   for (int k = 0; k < NF_MAX_NANO; ++k)
@@ -785,6 +786,8 @@ struct LayerCtx {
   cudaStream_t ns;      // network stream (TP collectives; == cs outside OVERLAP)
   cudaStream_t cs2 = nullptr;  // TP OVERLAP: compute stream of the second dense nano-batch (null: cs)
   bool dec_on_cs = false;      // no memory partition: decode attention on the (group's) compute stream
+  bool dec_side = false;       // no memory partition: decode on side streams of the compute partition
+  cudaStream_t ms2 = nullptr;  // dec_side: the second dense group's decode stream
   mutable bool rows_built[NF_MAX_NANO] = {};  // decode row streams written this step (ROWS loader)
   nf_comm* comm;
   int cap_dense = 0, cap_dec = 0;  // partition sizes when green contexts are active (0: whole GPU)
@@ -894,7 +897,7 @@ nf_status run_decode(const LayerCtx& L, const NanoRange& nr, cudaStream_t st, in
   AttnArgs a = attn_args(L);
   const DecodeItem* dec = reinterpret_cast<const DecodeItem*>(L.meta_dev + L.m->off_dec) + nr.dec_off + off;
   const int sms = part == 2     ? clamp_dense(L, L.p->spec.sm[NF_OP_KQV])
-                  : L.dec_on_cs ? clamp_dense(L, L.p->spec.sm[NF_OP_DECODE_ATTN])
+                  : (L.dec_on_cs || L.dec_side) ? clamp_dense(L, L.p->spec.sm[NF_OP_DECODE_ATTN])
                                 : clamp_dec(L, L.p->spec.sm[NF_OP_DECODE_ATTN]);
   ProfScope ps(NF_OP_DECODE_ATTN, st);
   if (use_tc_decode(c, L.p)) {
@@ -1175,6 +1178,7 @@ LayerCtx group_ctx(const LayerCtx& L, int g, Workspace* wg) {
     c.cs = L.cs2;
   }
   if (L.dec_on_cs) c.ms = c.cs;
+  else if ((g & 1) && L.ms2) c.ms = L.ms2;
   return c;
 }
 
@@ -1493,6 +1497,11 @@ nf_status tap_rows(const LayerCtx& L, void* dst, const __nv_bfloat16* src, int t
   return NF_OK;
 }
 
+int tp_dec_side_env() {  // (dev) NF_TP_DEC_SIDE=1: decode side streams when there is no memory partition
+  const char* e = getenv("NF_TP_DEC_SIDE");
+  return e && e[0] == '1';
+}
+
 // OVERLAP plans run on green-context partitions when available: fork the
 // caller stream into the compute / memory (/ network) partition streams, join at the end.
 nf_status enter_partitions(nf_plan* p, LayerCtx* L, cudaStream_t caller) {
@@ -1530,6 +1539,14 @@ nf_status enter_partitions(nf_plan* p, LayerCtx* L, cudaStream_t caller) {
   if (p->green_ms) {
     NF_CUDA(cudaStreamWaitEvent(p->green_ms, p->ev_fork, 0));
     L->ms = p->green_ms;
+  } else if (tp_dec_side_env() && p->green_ds1 && p->green_ds2) {
+    NF_CUDA(cudaStreamWaitEvent(p->green_ds1, p->ev_fork, 0));
+    L->ms = p->green_ds1;
+    if (two) {
+      NF_CUDA(cudaStreamWaitEvent(p->green_ds2, p->ev_fork, 0));
+      L->ms2 = p->green_ds2;
+    }
+    L->dec_side = true;
   } else {
     L->ms = L->cs;
     L->dec_on_cs = true;
@@ -1550,6 +1567,10 @@ nf_status leave_partitions(nf_plan* p, const LayerCtx& L, cudaStream_t caller) {
   if (L.cs != caller) {
     NF_CUDA(cudaEventRecord(p->ev_join_c, L.cs));
     NF_CUDA(cudaStreamWaitEvent(caller, p->ev_join_c, 0));
+  }
+  if (L.ms2) {
+    NF_CUDA(cudaEventRecord(p->ev_join_m2, L.ms2));
+    NF_CUDA(cudaStreamWaitEvent(caller, p->ev_join_m2, 0));
   }
   if (L.ms != caller && L.ms != L.cs) {
     NF_CUDA(cudaEventRecord(p->ev_join_m, L.ms));

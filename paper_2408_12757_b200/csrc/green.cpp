@@ -138,6 +138,16 @@ bool green_setup(nf_plan* p, int dec_sms, int net_sms) {
     p->green_note = "green stream creation failed";
     return false;
   }
+  // without a memory partition: two high-priority side streams in the compute partition for decode
+  // attention (one per dense group), so a group's decode runs beside its prefill (NF_TP_DEC_SIDE=1)
+  CUstream s_d1 = nullptr, s_d2 = nullptr;
+  if (!g_mem && (g_api.streamCreate(&s_d1, g_cmp, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS ||
+                 g_api.streamCreate(&s_d2, g_cmp, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS)) {
+    p->green_note = "green stream creation failed";
+    return false;
+  }
+  p->green_ds1 = (cudaStream_t)s_d1;
+  p->green_ds2 = (cudaStream_t)s_d2;
   p->green_ms = (cudaStream_t)s_mem;
   p->green_cs = (cudaStream_t)s_cmp;
   p->green_cs2 = (cudaStream_t)s_cmp2;

@@ -149,10 +149,11 @@ struct nf_plan {
   bool green_tried = false, green_ok = false;
   std::string green_note = "not used";
   cudaStream_t green_cs = nullptr, green_ms = nullptr, green_cs2 = nullptr;
+  cudaStream_t green_ds1 = nullptr, green_ds2 = nullptr;  // no memory partition: decode side streams (compute partition)
   cudaStream_t cs2 = nullptr;  // second compute stream (TP OVERLAP: one per dense nano-batch) outside green contexts
   cudaEvent_t ev_fork2 = nullptr, ev_join_c2 = nullptr;
   int green_dec_sms = 0, green_dense_sms = 0;
-  cudaEvent_t ev_fork = nullptr, ev_join_c = nullptr, ev_join_m = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join_c = nullptr, ev_join_m = nullptr, ev_join_m2 = nullptr;
   cudaEvent_t ev_upload[2] = {};
   void* pinned[2] = {nullptr, nullptr};
   size_t pinned_cap[2] = {0, 0};
