@@ -35,6 +35,8 @@ def main():
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--workloads", default="splitwise,lmsys,sharegpt")
+    ap.add_argument("--net-model", default="", choices=["", "nvlink"],
+                    help="c3loop: model the collectives' link time (ring bytes / 725 GB/s, bench.py --net-model)")
     args = ap.parse_args()
     import torch
 
@@ -67,6 +69,8 @@ def main():
     pool_pages = max(need.values())
     cfg = rt.cfg_from_shape(shape, tp_size=tp, tp_rank=0)
     comm = nf.comm_create_loopback(tp, 0) if tp > 1 else None
+    if comm is not None and args.net_model == "nvlink":
+        nf.comm_loopback_set_link(comm, 725.0)   # bench.py NVLINK_BUS_GBS (a model, not a measurement)
     g = torch.Generator(device="cuda")
     g.manual_seed(0)
 
