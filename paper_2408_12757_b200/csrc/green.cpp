@@ -60,13 +60,17 @@ bool green_setup(nf_plan* p, int dec_sms, int net_sms) {
     p->green_note = "disabled (NF_GREEN=0)";
     return false;
   }
-  // Nsight Compute injects itself through CUDA_INJECTION64_PATH and cannot replay
-  // kernels of green contexts: under a profiler the plan runs on ordinary streams
-  // (same kernels, SM-bounded persistent grids) unless NF_GREEN=1 forces partitions.
-  const char* inj = getenv("CUDA_INJECTION64_PATH");
-  if (inj && inj[0] && !(env && env[0] == '1')) {
-    p->green_note = "not used under a profiler (CUDA_INJECTION64_PATH set)";
-    return false;
+  // Nsight Compute cannot replay kernels of green contexts ("Failed to prepare kernel for
+  // profiling"): under a profiler the plan runs on ordinary streams (same kernels,
+  // SM-bounded persistent grids) unless NF_GREEN=1 forces partitions.  The profiler is
+  // recognised by the variables it sets in the target's environment (ncu 2025.2 sets the
+  // NV_NSIGHT_INJECTION_* / NV_COMPUTE_PROFILER_* ones; older injection used CUDA_INJECTION64_PATH).
+  for (const char* var : {"CUDA_INJECTION64_PATH", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE", "NV_COMPUTE_PROFILER_PERFWORKS_DIR"}) {
+    const char* inj = getenv(var);
+    if (inj && inj[0] && !(env && env[0] == '1')) {
+      p->green_note = std::string("not used under a profiler (") + var + " set)";
+      return false;
+    }
   }
   if (!load_api()) {
     p->green_note = "driver lacks green-context entry points";
