@@ -936,7 +936,14 @@ cudaError_t launch_gemm(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16
     // on a tie the pair kernel measured faster only with a long mainloop and many n-tiles
     // (>= 32 k-blocks, N >= 2048; tools/gemm_micro.py): short-K pairs couple the two CTAs'
     // epilogues through the shared accumulator barrier
-    const bool tie_ok = num_kb >= 32 && args.N >= 2048;
+    // (dev) NF_GEMM_PAIR_MINN raises the N threshold of the tie rule (A/B of single-CTA tiles on
+    // the narrow-N GEMMs: O, Down, KQV)
+    static int pair_min_n = -1;
+    if (pair_min_n < 0) {
+      const char* e2 = getenv("NF_GEMM_PAIR_MINN");
+      pair_min_n = e2 ? atoi(e2) : 2048;
+    }
+    const bool tie_ok = num_kb >= 32 && args.N >= pair_min_n;
     double c = (double)((pair_tiles + pairs - 1) / pairs) + bias(3);
     // pairs with a split-K tail (same rule as single CTAs, pair tiles over pairs)
     const int rem = pair_tiles % pairs;
