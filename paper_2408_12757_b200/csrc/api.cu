@@ -2128,7 +2128,15 @@ nf_status nf_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, v
     a.sk_part = (float*)ws;
     a.sk_slots = slots;
     a.sk_flag = (int*)((char*)ws + (size_t)slots * GEMM_BM * GEMM_SK_LD * 4);
-    NF_CUDA(cudaMemsetAsync(a.sk_flag, 0, (size_t)tiles * 4, (cudaStream_t)stream));
+    // (dev) NF_GEMM_NOZERO=1: the caller zeroed the workspace once (the kernel leaves its arrival
+    // flags zeroed), so no memset node sits between back-to-back launches in a graph -- GEMM to
+    // GEMM as in the model step, whose flags are cleared once per step (tools/gemm_phases.py)
+    static int nozero_env = -1;
+    if (nozero_env < 0) {
+      const char* e = getenv("NF_GEMM_NOZERO");
+      nozero_env = e ? atoi(e) : 0;
+    }
+    if (!nozero_env) NF_CUDA(cudaMemsetAsync(a.sk_flag, 0, (size_t)tiles * 4, (cudaStream_t)stream));
   }
   NF_CUDA(launch_gemm((const __nv_bfloat16*)A, lda, (const __nv_bfloat16*)B, ldb, a, grid_max, (cudaStream_t)stream));
   return NF_OK;

@@ -22,7 +22,7 @@ for M, N, K in SHAPES:
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     B = (torch.randn(N, K, device="cuda") * K ** -0.5).to(torch.bfloat16)
     Cm = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    ws = torch.empty(nf.gemm_workspace_bytes(M, N), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(nf.gemm_workspace_bytes(M, N), dtype=torch.uint8, device="cuda")  # NF_GEMM_NOZERO=1 needs it zeroed once
 
     def f():
         nf.gemm_bf16(A.data_ptr(), K, B.data_ptr(), K, Cm.data_ptr(), N, M, N, K, budget,
